@@ -1,0 +1,350 @@
+#!/usr/bin/env python
+"""bench.py -- FastFourierSAT hot path on B200 (BASELINE.json metric: literal-gradient terms/s).
+
+Default workload = BASELINE.json configs[1] (c2): uniform random 7-SAT, n = 200, m = 17000
+(alpha = 85), a batch of 1024 restart points per GPU, the full projected-gradient CLS loop.
+
+One *step* = one CLS iteration over the batch (every row of SURVEY.md 8(a) on the hot path):
+  A4-A7  one batched f + grad evaluation at the trial points (gather, products, deterministic reductions),
+         with the fused A9 sign check of the trial points,
+  A8     the Armijo accept / eta update / next projected trial point,
+and every --round-len steps the round end: A9 exact check of sgn(x) (unsat[b], U_c), A11 the
+restart-sharding collectives (U_c SUM and any-solved MAX over ranks, NCCL), A10 ERWA + rephase,
+and the next round's start evaluation.  A1-A3 (parse, layout, coefficients) run once at load.
+
+value = literal-gradient terms per second over all ranks = sum_c k_c * B_total * K / t, with t the
+max over ranks of the summed CUDA-event step times (L2 flushed between steps, untimed).
+`--impl reference` times the oracle (oracle/dp.c, the CPU fp64 GradSAT DP) on the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+import synth  # noqa: E402
+
+CONFIGS = {
+    "c2": dict(make=lambda: synth.config2(0), B=1024, desc="c2: uniform random 7-SAT n=200 m=17000 (alpha=85)"),
+    "c1": dict(make=lambda: synth.config1(0), B=1, desc="c1: uniform random 3-SAT n=20 m=91, single point"),
+    "c3": dict(make=lambda: synth.config3(0), B=32, desc="c3: n=4096, 8192 planted 3-SAT + 32 at-most-b k=500..2000, fp64"),
+    "c4": dict(make=lambda: synth.config4_hybrid(0), B=1024, desc="c4: n=1024, 2048 planted 3-CNF + 512 XOR k=3..64"),
+    "c5": dict(make=lambda: synth.config5(0), B=32, desc="c5: uniform random 3-SAT n=1e6 m=4.2e6"),
+}
+SM_COUNT = 148
+FP32_LANES, FP64_LANES = 128, 64  # per SM per clock (B200_PROFILING.md / blackwell guide)
+FAST_FLOPS_PER_TERM = 6           # factor FMA + prefix MUL + suffix MUL + combine FMA
+ROOT_FLOPS_PER_LIT_ROOT = 20      # factor 2 FMA + 2 complex MUL (4 MUL + 4 FMA) + Re-accumulate 2 FMA
+
+
+def env_rank():
+    return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
+
+
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as fh:
+            return json.load(fh), "measured"
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "sm_max_mhz": 1965.0}, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled every 200 ms during the timed region."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, dev):
+        self.dev = dev
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                                          "-lms", "200", "-i", str(self.dev)], stdout=subprocess.PIPE,
+                                         stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for l in self.lines:
+            f = [v.strip() for v in l.split(",")]
+            if len(f) < 8:
+                continue
+            try:
+                sm.append(float(f[1])); smax.append(float(f[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[4:8]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(smax) if smax else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def ncu_traffic(kernel_key):
+    """dram bytes per launch of the dominant kernel from the committed ncu --set full summary, or None."""
+    p = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    if not os.path.exists(p):
+        return None
+    try:
+        with open(p) as fh:
+            d = json.load(fh)
+        return d.get(kernel_key, {}).get("dram_bytes_per_launch")
+    except (OSError, ValueError):
+        return None
+
+
+# ------------------------------------------------------------------------------------------------ reference arm
+
+
+def run_reference(args, cfg, inst):
+    """The oracle (oracle/dp.c, fp64 CPU GradSAT DP, OpenMP over points) as it stands, on the same workload:
+    each step evaluates f and grad on a bounded sample of the workload's points."""
+    from oracle import cdp
+    from oracle.formula import OracleFormula
+    Fo = OracleFormula.from_arrays(*inst.arrays())
+    threads = cdp.max_threads()
+    X = synth.points("U", cfg["B"], inst.n, 1000, np.float64)
+    t0 = time.perf_counter()
+    cdp.evaluate(Fo, X[:1])
+    one = time.perf_counter() - t0
+    budget = max(0.05, 150.0 / max(1, args.steps + args.warmup))  # whole run within ~3 minutes
+    S = int(max(1, min(cfg["B"], budget / max(one / max(1, threads), 1e-6))))
+    Xs = X[:S]
+    for _ in range(args.warmup):
+        cdp.evaluate(Fo, Xs)
+    ts = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        cdp.evaluate(Fo, Xs)
+        ts.append(time.perf_counter() - t0)
+    t = sum(ts)
+    L = inst.n_lits
+    value = L * S * args.steps / t
+    sample = f"{S} of the {cfg['B']} points per step (fp64 f + grad), {threads} OpenMP threads"
+    line = {"impl": "reference", "metric": "literal-gradient terms/s", "value": value, "unit": "terms/s",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": cfg["desc"], "points_per_step": S},
+            "cpu_baseline": {"value": value, "unit": "terms/s", "cores": threads, "kind": "oracle", "sample": sample},
+            "e2e": {"value": value, "unit": "terms/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def cpu_baseline(cfg, inst, X):
+    """Oracle timed on the host cores on a bounded sample (~10 s of CPU work)."""
+    from oracle import cdp
+    from oracle.formula import OracleFormula
+    Fo = OracleFormula.from_arrays(*inst.arrays())
+    threads = cdp.max_threads()
+    Xd = X.astype(np.float64)
+    t0 = time.perf_counter()
+    cdp.evaluate(Fo, Xd[:min(len(Xd), threads)])
+    probe = time.perf_counter() - t0
+    per_pt = probe / min(len(Xd), threads) * threads  # wall per point per thread-batch
+    S = int(max(1, min(len(Xd), 10.0 / max(per_pt / threads, 1e-9))))
+    t0 = time.perf_counter()
+    cdp.evaluate(Fo, Xd[:S])
+    t = time.perf_counter() - t0
+    return {"value": inst.n_lits * S / t, "unit": "terms/s", "cores": threads, "kind": "oracle",
+            "sample": f"f + grad of {S} of the workload's {len(Xd)} points in fp64 ({t:.1f} s)"}
+
+
+# ------------------------------------------------------------------------------------------------ our arm
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--impl", default="ffsat", choices=["ffsat", "reference"])
+    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    ap.add_argument("--round-len", type=int, default=10)
+    ap.add_argument("--no-flush", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    rank, world, local = env_rank()
+    cfg = CONFIGS[args.config]
+
+    if args.impl == "reference":
+        if rank == 0:
+            run_reference(args, cfg, cfg["make"]())
+        return
+
+    import torch
+    import torch.distributed as dist
+    import paper_2308_15020_b200 as P
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    inst = cfg["make"]()
+    B = cfg["B"]
+    ctx = P.Context.from_instance(inst, device=local)
+    info = ctx.info
+    L = info["n_lits"]
+    search = ctx.search(B, seed=20230815, point0=rank * B, max_inner=args.round_len, check_every=args.round_len)
+    T = search.tensors()
+    flag = torch.zeros(1, dtype=torch.int32, device=dev)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+    stream = torch.cuda.current_stream(dev)
+
+    def step(i):
+        search.iterate(1)
+        if (i + 1) % args.round_len == 0:
+            search.check()
+            if world > 1:
+                dist.all_reduce(T["U"], op=dist.ReduceOp.SUM)
+            flag.copy_((T["unsat"].min() == 0).to(torch.int32).view(1))
+            if world > 1:
+                dist.all_reduce(flag, op=dist.ReduceOp.MAX)
+            search.restart(T["U"])
+            search.begin_round()
+
+    search.begin_round()
+    for i in range(args.warmup):
+        step(i)
+    torch.cuda.synchronize()
+    clocks = ClockSampler(local)
+    clocks.start()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    launches0 = ctx.launch_count()
+    evs = []
+    for i in range(args.steps):
+        if not args.no_flush:
+            flush.zero_()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        step(args.warmup + i)
+        e1.record(stream)
+        evs.append((e0, e1))
+    torch.cuda.synchronize()
+    launches = ctx.launch_count() - launches0
+    if world > 1:
+        dist.barrier()
+    ms = sum(a.elapsed_time(b) for a, b in evs)
+    clk = clocks.stop()
+    t_local = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t_local, op=dist.ReduceOp.MAX)
+    ms_max = float(t_local.item())
+    B_total = B * world
+    value = L * B_total * args.steps / (ms_max * 1e-3)
+
+    # ---- e2e: the public API with pinned host buffers (H2D of x, D2H of f and grad every step)
+    dt = torch.float64 if info["precision"] == 64 else torch.float32
+    xh = torch.from_numpy(synth.points("U", B, inst.n, 1000 + rank, np.float64)).to(dt).pin_memory()
+    fh = torch.empty(B, dtype=torch.float64).pin_memory()
+    gh = torch.empty((B, inst.n), dtype=dt).pin_memory()
+    e2e_steps = max(5, min(args.steps, 50))
+    for _ in range(3):
+        P.ffsat_eval(ctx.ptr, xh, B, fh, gh)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e2e_ms = []
+    for _ in range(e2e_steps):
+        if not args.no_flush:
+            flush.zero_()
+            torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        P.ffsat_eval(ctx.ptr, xh, B, fh, gh)   # synchronous: H2D, kernels, D2H
+        e2e_ms.append((time.perf_counter() - t0) * 1e3)
+    te = torch.tensor([sum(e2e_ms)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    e2e_value = L * B_total * e2e_steps / (float(te.item()) * 1e-3)
+    esz = 8 if info["precision"] == 64 else 4
+    e2e = {"value": e2e_value, "unit": "terms/s", "h2d_bytes_per_step": B * inst.n * esz,
+           "d2h_bytes_per_step": B * 8 + B * inst.n * esz}
+
+    # ---- roofline of the dominant kernel: per-phase CUDA events on the launching stream
+    xd = torch.from_numpy(synth.points("U", B, inst.n, 1000 + rank, np.float64)).to(dt).to(dev)
+    fd = torch.empty(B, dtype=torch.float64, device=dev)
+    gd = torch.empty_like(xd)
+    ud = torch.empty(B, dtype=torch.int32, device=dev)
+    phases = []
+    for i in range(max(5, min(args.steps, 50))):
+        if not args.no_flush:
+            flush.zero_()
+        phases.append(ctx.eval_profiled(xd, fd, gd, ud))
+    ph = np.mean(np.array(phases[2:]), axis=0)  # ms: fast, root, grad-reduce, f-reduce
+    peaks, peak_src = measured_peaks()
+    mhz = float(peaks.get("sm_max_mhz", 1965.0))
+    fast_ms, root_ms = float(ph[0]), float(ph[1])
+    if fast_ms >= root_ms:
+        kname = "fast_tiled_kernel" if info["path"] == 1 else "fast_global_kernel"
+        flops = FAST_FLOPS_PER_TERM * info["n_fast_lits"] * B
+        kms = fast_ms
+        peak = SM_COUNT * FP32_LANES * 2 * mhz * 1e6 / 1e12 if info["precision"] == 32 else SM_COUNT * FP64_LANES * 2 * mhz * 1e6 / 1e12
+    else:
+        kname = "sym_kernel"
+        flops = ROOT_FLOPS_PER_LIT_ROOT * info["sym_root_lits"] * B
+        kms = root_ms
+        lanes = FP64_LANES if info["precision"] == 64 else FP32_LANES
+        peak = SM_COUNT * lanes * 2 * mhz * 1e6 / 1e12
+    achieved = flops / (kms * 1e-3) / 1e12
+    traffic = ncu_traffic(kname)
+    roofline = {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
+                "traffic": traffic, "kernel": kname, "kernel_ms": kms,
+                "eval_phase_ms": {"fast": float(ph[0]), "root": float(ph[1]), "grad_reduce": float(ph[2]),
+                                  "f_reduce": float(ph[3])},
+                "kernel_share_of_eval": kms / float(np.sum(ph)),
+                "peak_source": f"{SM_COUNT} SMs x {FP32_LANES if info['precision'] == 32 else FP64_LANES} lanes x 2 flops x "
+                               f"{mhz:.0f} MHz ({peak_src} sm_max_mhz); FMA = 2 flops"}
+
+    if rank == 0:
+        base = None if args.no_cpu_baseline or world > 1 else cpu_baseline(cfg, inst, xd.cpu().numpy())
+        line = {"metric": "literal-gradient terms/s", "value": value, "unit": "terms/s", "n_gpus": world,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max / args.steps,
+                "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+                "dtype": "f64" if info["precision"] == 64 else "f32", "data": "synthetic",
+                "config": {"workload": cfg["desc"], "n": inst.n, "m": inst.m, "literals": L,
+                           "batch_per_gpu": B, "global_batch": B_total, "round_len": args.round_len,
+                           "parallelism": f"restart-sharded x{world}" if world > 1 else "single GPU",
+                           "l2": "flushed between timed steps (256 MiB write, untimed)" if not args.no_flush else "not flushed",
+                           "path": "tiled" if info["path"] == 1 else "global"},
+                "evals_per_s": B_total * args.steps / (ms_max * 1e-3),
+                "e2e": e2e, "gpu_launches": launches, "roofline": roofline, "clocks": clk}
+        if base is not None:
+            line["cpu_baseline"] = base
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

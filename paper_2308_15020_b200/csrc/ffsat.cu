@@ -1,0 +1,936 @@
+// ffsat.cu -- libffsat.so: context, device layout, launch orchestration and the C-ABI of include/ffsat.h.
+// Every compute step runs in the kernels of kernels_eval.cuh / kernels_solve.cuh; the host only parses,
+// lays out data (A1-A3) and enqueues launches.  No CPU fallback exists: without a CUDA device every
+// compute entry point fails with FFSAT_ERR_CUDA / FFSAT_ERR_ARG.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <fstream>
+#include <memory>
+#include <sstream>
+#include <string>
+#include <vector>
+
+#include "../../include/ffsat.h"
+#include "host.hpp"
+#include "kernels_eval.cuh"
+#include "kernels_solve.cuh"
+
+using namespace ffsat;
+
+namespace {
+
+thread_local std::string g_err;
+const int kNumSM_default = 148;
+
+#define CK(call)                                                                                     \
+    do {                                                                                             \
+        cudaError_t e_ = (call);                                                                     \
+        if (e_ != cudaSuccess)                                                                       \
+            throw Error(e_ == cudaErrorMemoryAllocation ? FFSAT_ERR_OOM : FFSAT_ERR_CUDA,            \
+                        std::string(#call) + ": " + cudaGetErrorString(e_));                         \
+    } while (0)
+
+struct DBuf {
+    void* p = nullptr;
+    size_t bytes = 0;
+    DBuf() = default;
+    DBuf(const DBuf&) = delete;
+    DBuf& operator=(const DBuf&) = delete;
+    ~DBuf() {
+        if (p) cudaFree(p);
+    }
+    void ensure(size_t b) {
+        if (b <= bytes && p) return;
+        if (p) cudaFree(p);
+        p = nullptr;
+        bytes = 0;
+        if (b == 0) return;
+        cudaError_t e = cudaMalloc(&p, b);
+        if (e != cudaSuccess) {
+            p = nullptr;
+            cudaGetLastError();
+            throw Error(FFSAT_ERR_OOM, "cudaMalloc(" + std::to_string(b) + "): " + cudaGetErrorString(e));
+        }
+        bytes = b;
+    }
+    template <class U>
+    U* as() const { return reinterpret_cast<U*>(p); }
+};
+
+template <class V>
+void upload(DBuf& d, const std::vector<V>& h) {
+    d.ensure(std::max<size_t>(h.size() * sizeof(V), 16));
+    if (!h.empty()) CK(cudaMemcpy(d.p, h.data(), h.size() * sizeof(V), cudaMemcpyHostToDevice));
+}
+
+inline cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+inline unsigned blocks_for(int64_t n, int t) { return (unsigned)((n + t - 1) / t); }
+
+}  // namespace
+
+struct ffsat_ctx {
+    Formula F;
+    Layout Lo;
+    int device = -1;
+    int num_sm = kNumSM_default;
+    size_t esize = 4;
+    std::string err;
+    // persistent device layout
+    DBuf fast_words, tiled_words, units, segs, buckets, sym_words, sym_off, sym_sig, sigs, coef, occ_off, occ_slot,
+        w_pos, w_static_orig, order, chk_off, chk_words, chk_rule;
+    int64_t persistent_bytes = 0;
+    // per-B scratch
+    DBuf xT, Tb, P, fpart, upart, fsym, usym, chunk_units, x_stage, g_stage, f_stage, u_stage, w_stage;
+    int64_t plan_B = -1;
+    int32_t n_chunks = 0;
+    size_t tiled_smem = 0;
+    int64_t launches = 0;
+    cudaEvent_t ev[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
+    ~ffsat_ctx() {
+        for (cudaEvent_t& e : ev)
+            if (e) cudaEventDestroy(e);
+    }
+};
+
+struct ffsat_search {
+    ffsat_ctx* ctx = nullptr;
+    int64_t B = 0, point0 = 0;
+    uint64_t seed = 0;
+    ffsat_solve_params P{};
+    DBuf X, Xp, Gx, Gp, fX, fP, dot, eta, done, iters, unsatP, solved, sol, unsat, U, stats;
+    int64_t round = 0, iters_issued = 0;
+};
+
+namespace {
+
+// ------------------------------------------------------------------------------------------------ setup
+
+void upload_layout(ffsat_ctx* c) {
+    const Layout& L = c->Lo;
+    const bool f64 = L.precision == 64;
+    c->esize = f64 ? 8 : 4;
+    upload(c->fast_words, L.fast_words);
+    if (L.path == 1) upload(c->tiled_words, L.tiled_words);
+    std::vector<dev::UnitDev> units;
+    for (const SubChunk& s : L.subchunks) units.push_back({s.bucket, s.seg_begin, s.seg_end, s.rows, s.pos_begin, s.pos_end});
+    upload(c->units, units);
+    upload(c->segs, L.segs);
+    std::vector<dev::FastBucketDev> bks;
+    for (const FastBucket& b : L.fbuckets) {
+        dev::FastBucketDev d{};
+        d.k = b.k; d.kp = b.kp; d.pos_begin = b.pos_begin; d.word_off = b.word_off; d.slot_off = b.slot_off;
+        d.g0 = b.g0;
+        int ch = 0;
+        if (b.gA != 0) { d.c0[ch] = 0.5; d.c1[ch] = 0.5; d.g[ch] = b.gA; ++ch; }   // A: (1 + l)/2
+        if (b.gB != 0) { d.c0[ch] = 0.5; d.c1[ch] = -0.5; d.g[ch] = b.gB; ++ch; }  // B: (1 - l)/2
+        if (b.gX != 0) { d.c0[ch] = 0.0; d.c1[ch] = 1.0; d.g[ch] = b.gX; ++ch; }   // X: l
+        d.nch = ch;
+        d.tmin = b.rule.tmin; d.tmax = b.rule.tmax; d.parity = b.rule.parity;
+        bks.push_back(d);
+    }
+    upload(c->buckets, bks);
+    upload(c->sym_words, L.sym_words);
+    upload(c->sym_off, L.sym_off);
+    upload(c->sym_sig, L.sym_sig);
+    std::vector<dev::SymSigDev> sg;
+    for (const SymSig& s : L.sigs) sg.push_back({s.k, s.Mp, s.tmin, s.tmax, s.parity, 0, s.coef_off, s.g0});
+    upload(c->sigs, sg);
+    if (f64) upload(c->coef, L.coef);
+    else {
+        std::vector<float> cf(L.coef.begin(), L.coef.end());
+        upload(c->coef, cf);
+    }
+    upload(c->occ_off, L.occ_off);
+    if (L.tb_slots > INT32_MAX) throw Error(FFSAT_ERR_ARG, "too many literal slots");
+    std::vector<int32_t> occ(L.occ_slot.begin(), L.occ_slot.end());
+    upload(c->occ_slot, occ);
+    if (f64) upload(c->w_pos, L.w_pos);
+    else {
+        std::vector<float> w(L.w_pos.begin(), L.w_pos.end());
+        upload(c->w_pos, w);
+    }
+    upload(c->w_static_orig, c->F.weight);
+    upload(c->order, L.order);
+    // unified position-order CSR for the exact check kernel
+    std::vector<int64_t> off{0};
+    std::vector<uint32_t> words;
+    std::vector<int32_t> rule;
+    const Formula& F = c->F;
+    for (int64_t p = 0; p < L.m; ++p) {
+        int64_t oc = L.order[p];
+        int k = (int)(F.offsets[oc + 1] - F.offsets[oc]);
+        for (int64_t i = F.offsets[oc]; i < F.offsets[oc + 1]; ++i) {
+            int32_t lit = F.lits[i];
+            words.push_back((uint32_t)((lit > 0 ? lit : -lit) - 1) | (lit < 0 ? 0x80000000u : 0u));
+        }
+        off.push_back((int64_t)words.size());
+        SatRule r = sat_rule(F.kind[oc], k, F.bound[oc]);
+        rule.push_back(r.tmin); rule.push_back(r.tmax); rule.push_back(r.parity);
+    }
+    upload(c->chk_off, off);
+    upload(c->chk_words, words);
+    upload(c->chk_rule, rule);
+    for (DBuf* d : {&c->fast_words, &c->tiled_words, &c->units, &c->segs, &c->buckets, &c->sym_words, &c->sym_off,
+                    &c->sym_sig, &c->sigs, &c->coef, &c->occ_off, &c->occ_slot, &c->w_pos, &c->w_static_orig, &c->order,
+                    &c->chk_off, &c->chk_words, &c->chk_rule})
+        c->persistent_bytes += (int64_t)d->bytes;
+}
+
+ffsat_ctx* make_ctx(Formula&& F, const ffsat_options* opt) {
+    ffsat_options o{0, 0, 0, 0};
+    if (opt) o = *opt;
+    validate(F);
+    std::unique_ptr<ffsat_ctx> c(new ffsat_ctx());
+    c->F = std::move(F);
+    c->Lo = build_layout(c->F, o.path, o.precision);
+    c->device = o.device;
+    if (o.device >= 0) {
+        int ndev = 0;
+        cudaError_t e = cudaGetDeviceCount(&ndev);
+        if (e != cudaSuccess || ndev == 0) {
+            cudaGetLastError();
+            throw Error(FFSAT_ERR_CUDA, "no CUDA device available (libffsat has no CPU fallback)");
+        }
+        if (o.device >= ndev) throw Error(FFSAT_ERR_ARG, "device ordinal out of range");
+        CK(cudaSetDevice(o.device));
+        CK(cudaDeviceGetAttribute(&c->num_sm, cudaDevAttrMultiProcessorCount, o.device));
+        upload_layout(c.get());
+    }
+    return c.release();
+}
+
+void need_device(const ffsat_ctx* c) {
+    if (!c) throw Error(FFSAT_ERR_ARG, "null context");
+    if (c->device < 0) throw Error(FFSAT_ERR_ARG, "host-only context (device = -1) cannot compute");
+    CK(cudaSetDevice(c->device));
+}
+
+// ------------------------------------------------------------------------------------------------ eval
+
+// Pick the number of clause chunks so (point tiles x chunks) fills whole waves of CTAs.
+int pick_chunks(int64_t point_tiles, int ctas_per_sm, int num_sm, int64_t n_units) {
+    if (n_units <= 0) return 0;
+    const int64_t slots = (int64_t)num_sm * std::max(1, ctas_per_sm);
+    int best = 1;
+    double best_eff = -1;
+    for (int w = 1; w <= 4; ++w) {
+        int64_t nc = std::max<int64_t>(1, (w * slots) / point_tiles);
+        nc = std::min<int64_t>(nc, n_units);
+        int64_t ctas = nc * point_tiles;
+        int64_t waves = (ctas + slots - 1) / slots;
+        double eff = (double)ctas / (double)(waves * slots);
+        if (eff > best_eff + 0.05) {
+            best_eff = eff;
+            best = (int)nc;
+        }
+        if (eff >= 0.9) break;
+    }
+    return best;
+}
+
+void plan(ffsat_ctx* c, int64_t B) {
+    if (c->plan_B == B) return;
+    const Layout& L = c->Lo;
+    const size_t es = c->esize;
+    const int64_t PT = (B + 31) / 32;
+    int cps = 8;
+    if (L.path == 1) {
+        c->tiled_smem = tiled_smem_bytes(L.n, L.precision, L.stage_rows);
+        cps = std::max(1, (int)std::min<size_t>(8, (228 * 1024) / (c->tiled_smem + 1024)));
+    }
+    const int64_t n_units = (int64_t)L.subchunks.size();
+    c->n_chunks = L.n_fast > 0 ? pick_chunks(PT, cps, c->num_sm, n_units) : 0;
+    // balanced contiguous unit ranges by literal rows
+    std::vector<int32_t> cu((size_t)c->n_chunks + 1, 0);
+    if (c->n_chunks > 0) {
+        int64_t total = 0;
+        for (const SubChunk& s : L.subchunks) total += s.rows;
+        int64_t acc = 0;
+        int j = 1;
+        for (int64_t u = 0; u < n_units && j < c->n_chunks; ++u) {
+            acc += L.subchunks[u].rows;
+            while (j < c->n_chunks && acc * c->n_chunks >= total * j) cu[j++] = (int32_t)(u + 1);
+        }
+        for (; j <= c->n_chunks; ++j) cu[j] = (int32_t)n_units;
+        cu[c->n_chunks] = (int32_t)n_units;
+    }
+    upload(c->chunk_units, cu);
+    const int64_t parts = std::max<int64_t>(1, c->n_chunks);
+    if (L.path == 1) c->P.ensure(std::max<size_t>(16, (size_t)c->n_chunks * L.n * B * es));
+    if (L.path == 2) c->xT.ensure(std::max<size_t>(16, (size_t)L.n * B * es));
+    c->Tb.ensure(std::max<size_t>(16, (size_t)L.tb_slots * B * es));
+    c->fpart.ensure((size_t)parts * B * 8);
+    c->upart.ensure((size_t)parts * B * 4);
+    c->fsym.ensure(std::max<size_t>(16, (size_t)L.n_sym * B * 8));
+    c->usym.ensure(std::max<size_t>(16, (size_t)L.n_sym * B * 4));
+    if (L.path == 1) {
+        const void* kerns[8] = {(const void*)dev::fast_tiled_kernel<float, 4>, (const void*)dev::fast_tiled_kernel<float, 8>,
+                                (const void*)dev::fast_tiled_kernel<float, 16>, (const void*)dev::fast_tiled_kernel<float, 64>,
+                                (const void*)dev::fast_tiled_kernel<double, 4>, (const void*)dev::fast_tiled_kernel<double, 8>,
+                                (const void*)dev::fast_tiled_kernel<double, 16>, (const void*)dev::fast_tiled_kernel<double, 64>};
+        for (const void* k : kerns) CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->tiled_smem));
+    }
+    c->plan_B = B;
+}
+
+int fast_kmax(const Layout& L) {
+    int km = 0;
+    for (const FastBucket& b : L.fbuckets) km = std::max(km, b.k);
+    return km;
+}
+
+template <typename T>
+void launch_sym_class(ffsat_ctx* c, const SymClass& cl, const dev::SymArgs<T>& a, cudaStream_t st) {
+    const int64_t groups = (cl.end - cl.begin) * a.B;
+    switch (cl.G) {
+    case 32: dev::sym_kernel<T, 32><<<blocks_for(groups, 8), 256, 0, st>>>(a, cl.begin, cl.end); break;
+    case 64: dev::sym_kernel<T, 64><<<(unsigned)groups, 64, 0, st>>>(a, cl.begin, cl.end); break;
+    case 128: dev::sym_kernel<T, 128><<<(unsigned)groups, 128, 0, st>>>(a, cl.begin, cl.end); break;
+    case 256: dev::sym_kernel<T, 256><<<(unsigned)groups, 256, 0, st>>>(a, cl.begin, cl.end); break;
+    case 512: dev::sym_kernel<T, 512><<<(unsigned)groups, 512, 0, st>>>(a, cl.begin, cl.end); break;
+    default: throw Error(FFSAT_ERR_ARG, "unsupported group size");
+    }
+}
+
+// f (fp64), grad (T, may be null), unsat (int32, may be null) at device points x [B][n]; async on st.
+template <typename T>
+void eval_device_t(ffsat_ctx* c, const T* x, int64_t B, double* f, T* grad, int32_t* unsat, const T* w_pos, cudaStream_t st,
+                   bool profiled = false) {
+    const Layout& L = c->Lo;
+    plan(c, B);
+    const int64_t PT = (B + 31) / 32;
+    if (B == 0) return;
+    auto mark = [&](int i) {
+        if (profiled) CK(cudaEventRecord(c->ev[i], st));
+    };
+    mark(0);
+    if (L.n_fast > 0 && c->n_chunks > 0) {
+        c->launches += L.path == 1 ? 1 : 2;
+        if (L.path == 1) {
+            dev::TiledArgs<T> a{};
+            a.x = x; a.B = B; a.n = L.n; a.stage_rows = L.stage_rows;
+            a.words = c->tiled_words.as<uint32_t>(); a.units = c->units.as<dev::UnitDev>(); a.segs = c->segs.as<uint2>();
+            a.buckets = c->buckets.as<dev::FastBucketDev>(); a.chunk_units = c->chunk_units.as<int32_t>(); a.w_pos = w_pos;
+            a.P = c->P.as<T>(); a.fpart = c->fpart.as<double>(); a.upart = c->upart.as<int32_t>();
+            dim3 grid((unsigned)PT, (unsigned)c->n_chunks);
+            const int km = fast_kmax(L);
+            if (km <= 4) dev::fast_tiled_kernel<T, 4><<<grid, 256, c->tiled_smem, st>>>(a);
+            else if (km <= 8) dev::fast_tiled_kernel<T, 8><<<grid, 256, c->tiled_smem, st>>>(a);
+            else if (km <= 16) dev::fast_tiled_kernel<T, 16><<<grid, 256, c->tiled_smem, st>>>(a);
+            else dev::fast_tiled_kernel<T, 64><<<grid, 256, c->tiled_smem, st>>>(a);
+        } else {
+            dim3 tg(blocks_for(L.n, 32), blocks_for(B, 32)), tb(32, 8);
+            dev::transpose_kernel<T><<<tg, tb, 0, st>>>(x, c->xT.as<T>(), B, L.n);
+            dev::GlobalArgs<T> a{};
+            a.xT = c->xT.as<T>(); a.B = B; a.n = L.n; a.words = c->fast_words.as<uint32_t>();
+            a.units = c->units.as<dev::UnitDev>(); a.buckets = c->buckets.as<dev::FastBucketDev>();
+            a.chunk_units = c->chunk_units.as<int32_t>(); a.w_pos = w_pos; a.Tb = c->Tb.as<T>();
+            a.fpart = c->fpart.as<double>(); a.upart = c->upart.as<int32_t>();
+            dim3 grid((unsigned)PT, (unsigned)c->n_chunks);
+            const int km = fast_kmax(L);
+            if (km <= 4) dev::fast_global_kernel<T, 4><<<grid, 256, 0, st>>>(a);
+            else if (km <= 8) dev::fast_global_kernel<T, 8><<<grid, 256, 0, st>>>(a);
+            else if (km <= 16) dev::fast_global_kernel<T, 16><<<grid, 256, 0, st>>>(a);
+            else dev::fast_global_kernel<T, 64><<<grid, 256, 0, st>>>(a);
+        }
+        CK(cudaGetLastError());
+    }
+    mark(1);
+    if (L.n_sym > 0) {
+        c->launches += (int64_t)L.sym_classes.size();
+        dev::SymArgs<T> a{};
+        a.x = x; a.sb = L.n; a.sv = 1; a.B = B;
+        a.words = c->sym_words.as<uint32_t>(); a.off = c->sym_off.as<int64_t>(); a.sig_of = c->sym_sig.as<int32_t>();
+        a.sigs = c->sigs.as<dev::SymSigDev>(); a.coef = c->coef.as<T>(); a.w_sym = w_pos + L.n_fast;
+        a.tb_fast = L.tb_fast; a.Tb = c->Tb.as<T>(); a.fsym = c->fsym.as<double>(); a.usym = c->usym.as<int32_t>();
+        for (const SymClass& cl : L.sym_classes) launch_sym_class<T>(c, cl, a, st);
+        CK(cudaGetLastError());
+    }
+    mark(2);
+    if (grad) {
+        c->launches += 1;
+        dev::ReduceArgs<T> r{};
+        r.B = B; r.n = L.n; r.n_chunks = L.path == 1 ? c->n_chunks : 0; r.P = c->P.as<T>(); r.Tb = c->Tb.as<T>();
+        r.occ_off = c->occ_off.as<int64_t>(); r.occ_slot = c->occ_slot.as<int32_t>(); r.grad = grad;
+        dim3 grid(blocks_for(B, 32), blocks_for(L.n, 32)), blk(32, 8);
+        dev::reduce_grad_kernel<T><<<grid, blk, 0, st>>>(r);
+    }
+    mark(3);
+    c->launches += 1;
+    dev::ReduceFArgs rf{};
+    rf.B = B; rf.n_parts = L.n_fast > 0 ? c->n_chunks : 0; rf.n_sym = L.n_sym;
+    rf.fpart = c->fpart.as<double>(); rf.upart = c->upart.as<int32_t>(); rf.fsym = c->fsym.as<double>();
+    rf.usym = c->usym.as<int32_t>(); rf.f = f; rf.unsat = unsat;
+    dev::reduce_f_kernel<<<blocks_for(B, 256), 256, 0, st>>>(rf);
+    CK(cudaGetLastError());
+    mark(4);
+}
+
+void eval_device(ffsat_ctx* c, const void* x, int64_t B, double* f, void* grad, int32_t* unsat, cudaStream_t st,
+                 bool profiled = false) {
+    if (c->Lo.precision == 64)
+        eval_device_t<double>(c, (const double*)x, B, f, (double*)grad, unsat, c->w_pos.as<double>(), st, profiled);
+    else
+        eval_device_t<float>(c, (const float*)x, B, f, (float*)grad, unsat, c->w_pos.as<float>(), st, profiled);
+}
+
+ffsat_status fail(ffsat_ctx* c, const Error& e) {
+    g_err = e.what();
+    if (c) c->err = e.what();
+    return e.code;
+}
+
+ffsat_status fail_std(ffsat_ctx* c, const std::exception& e) {
+    g_err = std::string("internal error: ") + e.what();
+    if (c) c->err = g_err;
+    return FFSAT_ERR_ARG;
+}
+
+#define ABI_TRY(ctxp) try {
+#define ABI_CATCH(ctxp)                                       \
+    }                                                         \
+    catch (const Error& e) { return fail(ctxp, e); }          \
+    catch (const std::bad_alloc&) { return fail(ctxp, Error(FFSAT_ERR_OOM, "host out of memory")); } \
+    catch (const std::exception& e) { return fail_std(ctxp, e); }
+
+int64_t exact_unsat(const Formula& F, const int8_t* a, double* fw) {
+    int64_t cnt = 0;
+    double w = 0;
+    for (int64_t c = 0; c < F.m(); ++c) {
+        int k = (int)(F.offsets[c + 1] - F.offsets[c]);
+        int t = 0;
+        for (int64_t i = F.offsets[c]; i < F.offsets[c + 1]; ++i) {
+            int32_t lit = F.lits[i];
+            bool var_true = a[(lit > 0 ? lit : -lit) - 1] < 0;
+            t += (lit > 0) == var_true;
+        }
+        SatRule r = sat_rule(F.kind[c], k, F.bound[c]);
+        bool sat = t >= r.tmin && t <= r.tmax && (r.parity == 0 || (r.parity == 1) == ((t & 1) == 1));
+        if (!sat) {
+            ++cnt;
+            w += F.weight[c];
+        }
+    }
+    if (fw) *fw = w;
+    return cnt;
+}
+
+// ------------------------------------------------------------------------------------------------ search
+
+template <typename T>
+void search_eval(ffsat_search* s, const void* x, double* f, void* g, int32_t* u, cudaStream_t st) {
+    eval_device_t<T>(s->ctx, (const T*)x, s->B, f, (T*)g, u, s->ctx->w_pos.as<T>(), st);
+}
+
+void search_alloc(ffsat_search* s) {
+    const size_t es = s->ctx->esize, Bn = (size_t)s->B * s->ctx->Lo.n;
+    const int64_t B = s->B, m = s->ctx->Lo.m;
+    for (DBuf* d : {&s->X, &s->Xp, &s->Gx, &s->Gp}) d->ensure(std::max<size_t>(16, Bn * es));
+    for (DBuf* d : {&s->fX, &s->fP, &s->dot, &s->eta}) d->ensure((size_t)B * 8);
+    for (DBuf* d : {&s->done, &s->iters, &s->unsatP, &s->solved, &s->unsat}) d->ensure((size_t)B * 4);
+    s->sol.ensure(std::max<size_t>(16, Bn));
+    s->U.ensure(std::max<size_t>(16, (size_t)m * 4));
+    s->stats.ensure(64);
+    CK(cudaMemset(s->solved.p, 0, (size_t)B * 4));
+    CK(cudaMemset(s->unsat.p, 0, (size_t)B * 4));
+    CK(cudaMemset(s->U.p, 0, (size_t)std::max<int64_t>(m, 4) * 4));
+    CK(cudaMemset(s->done.p, 0, (size_t)B * 4));
+}
+
+dev::PgdArgs pgd_args(ffsat_search* s, int mode) {
+    dev::PgdArgs a{};
+    a.B = s->B; a.n = s->ctx->Lo.n; a.eta0 = s->P.eta0; a.eta_min = s->P.eta_min; a.c1 = s->P.armijo_c1;
+    a.max_inner = s->P.max_inner; a.X = s->X.p; a.Xp = s->Xp.p; a.Gx = s->Gx.p; a.Gp = s->Gp.p;
+    a.fX = s->fX.as<double>(); a.fP = s->fP.as<double>(); a.dot = s->dot.as<double>(); a.eta = s->eta.as<double>();
+    a.done = s->done.as<int32_t>(); a.iters = s->iters.as<int32_t>(); a.unsatP = s->unsatP.as<int32_t>();
+    a.solved = s->solved.as<int32_t>(); a.sol = s->sol.as<int8_t>(); a.mode = mode;
+    return a;
+}
+
+void search_begin_round(ffsat_search* s, cudaStream_t st) {
+    const bool f64 = s->ctx->Lo.precision == 64;
+    s->ctx->launches += 2;
+    dev::reset_round_kernel<<<blocks_for(s->B, 256), 256, 0, st>>>(s->eta.as<double>(), s->done.as<int32_t>(),
+                                                                    s->iters.as<int32_t>(), s->B, s->P.eta0);
+    if (f64) search_eval<double>(s, s->X.p, s->fX.as<double>(), s->Gx.p, s->unsatP.as<int32_t>(), st);
+    else search_eval<float>(s, s->X.p, s->fX.as<double>(), s->Gx.p, s->unsatP.as<int32_t>(), st);
+    dev::PgdArgs a = pgd_args(s, 0);
+    if (f64) dev::pgd_step_kernel<double><<<(unsigned)s->B, 256, 0, st>>>(a);
+    else dev::pgd_step_kernel<float><<<(unsigned)s->B, 256, 0, st>>>(a);
+    CK(cudaGetLastError());
+    s->iters_issued = 0;
+}
+
+void search_iterate(ffsat_search* s, int n_iters, cudaStream_t st) {
+    const bool f64 = s->ctx->Lo.precision == 64;
+    dev::PgdArgs a = pgd_args(s, 1);
+    for (int i = 0; i < n_iters; ++i) {
+        s->ctx->launches += 1;
+        if (f64) {
+            search_eval<double>(s, s->Xp.p, s->fP.as<double>(), s->Gp.p, s->unsatP.as<int32_t>(), st);
+            dev::pgd_step_kernel<double><<<(unsigned)s->B, 256, 0, st>>>(a);
+        } else {
+            search_eval<float>(s, s->Xp.p, s->fP.as<double>(), s->Gp.p, s->unsatP.as<int32_t>(), st);
+            dev::pgd_step_kernel<float><<<(unsigned)s->B, 256, 0, st>>>(a);
+        }
+    }
+    CK(cudaGetLastError());
+    s->iters_issued += n_iters;
+}
+
+void search_check(ffsat_search* s, cudaStream_t st) {
+    const Layout& L = s->ctx->Lo;
+    CK(cudaMemsetAsync(s->unsat.p, 0, (size_t)s->B * 4, st));
+    dev::CheckArgs a{};
+    a.X = s->X.p; a.B = s->B; a.n = L.n; a.m = L.m; a.off = s->ctx->chk_off.as<int64_t>();
+    a.words = s->ctx->chk_words.as<uint32_t>(); a.rule = s->ctx->chk_rule.as<int32_t>();
+    a.U = s->U.as<int32_t>(); a.unsat = s->unsat.as<int32_t>();
+    if (L.m > 0) {
+        s->ctx->launches += 1;
+        if (L.precision == 64) dev::check_kernel<double><<<blocks_for(L.m, 8), 256, 0, st>>>(a);
+        else dev::check_kernel<float><<<blocks_for(L.m, 8), 256, 0, st>>>(a);
+    }
+    CK(cudaGetLastError());
+}
+
+int policy_codes(int policy, int* p) {  // 'R' = 0, 'O' = 1, 'F' = 2
+    if (policy == 0) { p[0] = 0; p[1] = 1; p[2] = 2; return 3; }   // (ROF)^inf
+    if (policy == 1) { p[0] = 0; p[1] = 2; p[2] = 0; return 2; }   // (RF)^inf
+    p[0] = 0; p[1] = 0; p[2] = 0;
+    return 1;                                                      // R only
+}
+
+void search_restart(ffsat_search* s, const int32_t* Ug, cudaStream_t st) {
+    const Layout& L = s->ctx->Lo;
+    const bool f64 = L.precision == 64;
+    const int32_t* U = Ug ? Ug : s->U.as<int32_t>();
+    if (s->P.adaptive_weights && L.m > 0) {
+        s->ctx->launches += 1;
+        if (f64) dev::erwa_kernel<double><<<1, 1024, 0, st>>>(s->ctx->w_pos.as<double>(), U, L.m, s->P.alpha);
+        else dev::erwa_kernel<float><<<1, 1024, 0, st>>>(s->ctx->w_pos.as<float>(), U, L.m, s->P.alpha);
+    }
+    int p[3];
+    int len = policy_codes(s->P.policy, p);
+    const int64_t tot = s->B * L.n;
+    const uint32_t nr = (uint32_t)(s->round + 1);
+    if (tot > 0) {
+        s->ctx->launches += 1;
+        if (f64) dev::rephase_kernel<double><<<blocks_for(tot, 256), 256, 0, st>>>(s->X.as<double>(), s->B, L.n, s->seed, s->point0, nr, len, p[0], p[1], p[2]);
+        else dev::rephase_kernel<float><<<blocks_for(tot, 256), 256, 0, st>>>(s->X.as<float>(), s->B, L.n, s->seed, s->point0, nr, len, p[0], p[1], p[2]);
+    }
+    CK(cudaGetLastError());
+    s->round += 1;
+}
+
+void search_stats(ffsat_search* s, cudaStream_t st, ffsat_search_stats* out) {
+    s->ctx->launches += 1;
+    dev::stats_kernel<<<1, 1024, 0, st>>>(s->done.as<int32_t>(), s->solved.as<int32_t>(), s->unsat.as<int32_t>(), s->B,
+                                          s->stats.as<int64_t>());
+    int64_t h[4];
+    CK(cudaMemcpyAsync(h, s->stats.p, sizeof(h), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    out->round = s->round;
+    out->iterations = s->iters_issued;
+    out->active = h[0];
+    out->solved_point = h[1] >= 0 ? h[1] + s->point0 : -1;
+    out->best_unsat = h[2];
+    out->best_point = h[3] >= 0 ? h[3] + s->point0 : -1;
+}
+
+void search_assignment(ffsat_search* s, int64_t lp, int8_t* out) {
+    const int n = s->ctx->Lo.n;
+    int32_t solved = 0;
+    CK(cudaMemcpy(&solved, s->solved.as<int32_t>() + lp, 4, cudaMemcpyDeviceToHost));
+    if (solved) {
+        CK(cudaMemcpy(out, s->sol.as<int8_t>() + lp * n, (size_t)n, cudaMemcpyDeviceToHost));
+        return;
+    }
+    const size_t es = s->ctx->esize;
+    std::vector<unsigned char> row((size_t)n * es);
+    CK(cudaMemcpy(row.data(), (const char*)s->X.p + lp * n * es, row.size(), cudaMemcpyDeviceToHost));
+    for (int v = 0; v < n; ++v) {
+        double xv = es == 8 ? ((double*)row.data())[v] : (double)((float*)row.data())[v];
+        out[v] = xv < 0 ? -1 : 1;
+    }
+}
+
+void check_params(const ffsat_solve_params& p) {
+    if (!(p.eta0 > 0) || !(p.eta_min >= 0) || !(p.armijo_c1 >= 0 && p.armijo_c1 < 1) || !(p.alpha >= 0 && p.alpha <= 1) ||
+        p.max_inner < 1 || p.check_every < 1 || p.policy < 0 || p.policy > 2)
+        throw Error(FFSAT_ERR_ARG, "invalid solve parameters");
+}
+
+}  // namespace
+
+// ================================================================================================ C-ABI
+
+extern "C" {
+
+void ffsat_default_params(ffsat_solve_params* p) {
+    if (!p) return;
+    p->eta0 = 1.0;
+    p->eta_min = 1e-12;
+    p->armijo_c1 = 1e-4;
+    p->alpha = 0.4;
+    p->max_inner = 500;
+    p->check_every = 10;
+    p->policy = 0;
+    p->adaptive_weights = 1;
+    p->timeout_s = 0;
+}
+
+const char* ffsat_version(void) { return "ffsat-b200 1 (sm_100a)"; }
+
+const char* ffsat_last_error(const ffsat_ctx* ctx) { return ctx ? ctx->err.c_str() : g_err.c_str(); }
+
+ffsat_status ffsat_load(const ffsat_formula* f, const ffsat_options* opt, ffsat_ctx** out) {
+    ABI_TRY(nullptr)
+    if (!f || !out) throw Error(FFSAT_ERR_ARG, "null argument");
+    *out = nullptr;
+    *out = make_ctx(from_arrays(*f), opt);
+    return FFSAT_OK;
+    ABI_CATCH(nullptr)
+}
+
+ffsat_status ffsat_load_file(const char* path, const ffsat_options* opt, ffsat_ctx** out) {
+    ABI_TRY(nullptr)
+    if (!path || !out) throw Error(FFSAT_ERR_ARG, "null argument");
+    *out = nullptr;
+    std::ifstream in(path, std::ios::binary);
+    if (!in) throw Error(FFSAT_ERR_ARG, std::string("cannot open ") + path);
+    std::stringstream ss;
+    ss << in.rdbuf();
+    *out = make_ctx(parse_text(ss.str()), opt);
+    return FFSAT_OK;
+    ABI_CATCH(nullptr)
+}
+
+ffsat_status ffsat_info(const ffsat_ctx* c, ffsat_info_t* o) {
+    ABI_TRY(nullptr)
+    if (!c || !o) throw Error(FFSAT_ERR_ARG, "null argument");
+    const Layout& L = c->Lo;
+    o->n_vars = L.n; o->precision = L.precision; o->n_cons = L.m; o->n_lits = L.L;
+    o->n_fast_cons = L.n_fast; o->n_sym_cons = L.n_sym; o->n_fast_lits = L.n_fast_lits; o->n_sym_lits = L.n_sym_lits;
+    o->sym_root_lits = L.sym_root_lits; o->path = L.path; o->max_k = L.max_k; o->device_bytes = c->persistent_bytes;
+    return FFSAT_OK;
+    ABI_CATCH(nullptr)
+}
+
+ffsat_status ffsat_export(const ffsat_ctx* c, uint8_t* kind, int32_t* bound, double* weight, int64_t* offsets, int32_t* lits) {
+    ABI_TRY(nullptr)
+    if (!c) throw Error(FFSAT_ERR_ARG, "null context");
+    const Formula& F = c->F;
+    if (kind) std::copy(F.kind.begin(), F.kind.end(), kind);
+    if (bound) std::copy(F.bound.begin(), F.bound.end(), bound);
+    if (weight) std::copy(F.weight.begin(), F.weight.end(), weight);
+    if (offsets) std::copy(F.offsets.begin(), F.offsets.end(), offsets);
+    if (lits) std::copy(F.lits.begin(), F.lits.end(), lits);
+    return FFSAT_OK;
+    ABI_CATCH(nullptr)
+}
+
+ffsat_status ffsat_eval(ffsat_ctx* c, const void* x, int64_t B, int32_t on_device, double* f_out, void* grad_out,
+                        int32_t* unsat_out, void* stream) {
+    ABI_TRY(c)
+    need_device(c);
+    if (B < 0 || (B > 0 && (!x || !f_out))) throw Error(FFSAT_ERR_ARG, "bad eval arguments");
+    if (B > INT32_MAX / 2) throw Error(FFSAT_ERR_ARG, "batch too large");
+    cudaStream_t st = S(stream);
+    const size_t es = c->esize, Bn = (size_t)B * c->Lo.n;
+    if (on_device) {
+        eval_device(c, x, B, f_out, grad_out, unsat_out, st);
+        return FFSAT_OK;
+    }
+    // host buffers: validate, stage, compute, copy back
+    if (es == 8) {
+        const double* xd = (const double*)x;
+        for (size_t i = 0; i < Bn; ++i) if (!std::isfinite(xd[i])) throw Error(FFSAT_ERR_NONFINITE, "non-finite point coordinate");
+    } else {
+        const float* xf = (const float*)x;
+        for (size_t i = 0; i < Bn; ++i) if (!std::isfinite(xf[i])) throw Error(FFSAT_ERR_NONFINITE, "non-finite point coordinate");
+    }
+    c->x_stage.ensure(std::max<size_t>(16, Bn * es));
+    c->f_stage.ensure(std::max<size_t>(16, (size_t)B * 8));
+    c->u_stage.ensure(std::max<size_t>(16, (size_t)B * 4));
+    if (grad_out) c->g_stage.ensure(std::max<size_t>(16, Bn * es));
+    if (Bn) CK(cudaMemcpyAsync(c->x_stage.p, x, Bn * es, cudaMemcpyHostToDevice, st));
+    eval_device(c, c->x_stage.p, B, c->f_stage.as<double>(), grad_out ? c->g_stage.p : nullptr,
+                unsat_out ? c->u_stage.as<int32_t>() : nullptr, st);
+    if (B) CK(cudaMemcpyAsync(f_out, c->f_stage.p, (size_t)B * 8, cudaMemcpyDeviceToHost, st));
+    if (grad_out && Bn) CK(cudaMemcpyAsync(grad_out, c->g_stage.p, Bn * es, cudaMemcpyDeviceToHost, st));
+    if (unsat_out && B) CK(cudaMemcpyAsync(unsat_out, c->u_stage.p, (size_t)B * 4, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    return FFSAT_OK;
+    ABI_CATCH(c)
+}
+
+ffsat_status ffsat_set_weights(ffsat_ctx* c, const double* w, int32_t on_device, void* stream) {
+    ABI_TRY(c)
+    need_device(c);
+    if (!w) throw Error(FFSAT_ERR_ARG, "null weights");
+    const int64_t m = c->Lo.m;
+    if (m == 0) return FFSAT_OK;
+    cudaStream_t st = S(stream);
+    const double* src = w;
+    if (!on_device) {
+        for (int64_t i = 0; i < m; ++i) if (!std::isfinite(w[i])) throw Error(FFSAT_ERR_NONFINITE, "non-finite weight");
+        c->w_stage.ensure((size_t)m * 8);
+        CK(cudaMemcpyAsync(c->w_stage.p, w, (size_t)m * 8, cudaMemcpyHostToDevice, st));
+        src = c->w_stage.as<double>();
+    }
+    if (c->Lo.precision == 64) dev::permute_weights_kernel<double><<<blocks_for(m, 256), 256, 0, st>>>(c->w_pos.as<double>(), src, c->order.as<int64_t>(), m);
+    else dev::permute_weights_kernel<float><<<blocks_for(m, 256), 256, 0, st>>>(c->w_pos.as<float>(), src, c->order.as<int64_t>(), m);
+    CK(cudaGetLastError());
+    if (!on_device) CK(cudaStreamSynchronize(st));
+    return FFSAT_OK;
+    ABI_CATCH(c)
+}
+
+ffsat_status ffsat_get_weights(ffsat_ctx* c, double* w, int32_t on_device, void* stream) {
+    ABI_TRY(c)
+    need_device(c);
+    if (!w) throw Error(FFSAT_ERR_ARG, "null weights");
+    const int64_t m = c->Lo.m;
+    if (m == 0) return FFSAT_OK;
+    cudaStream_t st = S(stream);
+    double* dst = w;
+    if (!on_device) {
+        c->w_stage.ensure((size_t)m * 8);
+        dst = c->w_stage.as<double>();
+    }
+    if (c->Lo.precision == 64) dev::unpermute_weights_kernel<double><<<blocks_for(m, 256), 256, 0, st>>>(dst, c->w_pos.as<double>(), c->order.as<int64_t>(), m);
+    else dev::unpermute_weights_kernel<float><<<blocks_for(m, 256), 256, 0, st>>>(dst, c->w_pos.as<float>(), c->order.as<int64_t>(), m);
+    CK(cudaGetLastError());
+    if (!on_device) {
+        CK(cudaMemcpyAsync(w, dst, (size_t)m * 8, cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+    }
+    return FFSAT_OK;
+    ABI_CATCH(c)
+}
+
+ffsat_status ffsat_check(const ffsat_ctx* c, const int8_t* a, int64_t* n_unsat, double* fw) {
+    ABI_TRY(nullptr)
+    if (!c || !a) throw Error(FFSAT_ERR_ARG, "null argument");
+    for (int32_t v = 0; v < c->F.n; ++v)
+        if (a[v] != 1 && a[v] != -1) throw Error(FFSAT_ERR_ARG, "assignment entries must be -1 or +1");
+    int64_t cnt = exact_unsat(c->F, a, fw);
+    if (n_unsat) *n_unsat = cnt;
+    return FFSAT_OK;
+    ABI_CATCH(nullptr)
+}
+
+ffsat_status ffsat_search_create(ffsat_ctx* c, int64_t batch, int64_t point0, uint64_t seed, const ffsat_solve_params* params,
+                                 ffsat_search** out) {
+    ABI_TRY(c)
+    need_device(c);
+    if (!out || batch <= 0 || point0 < 0 || point0 + batch > (int64_t)UINT32_MAX) throw Error(FFSAT_ERR_ARG, "bad search arguments");
+    *out = nullptr;
+    std::unique_ptr<ffsat_search> s(new ffsat_search());
+    s->ctx = c;
+    s->B = batch;
+    s->point0 = point0;
+    s->seed = seed;
+    ffsat_default_params(&s->P);
+    if (params) s->P = *params;
+    check_params(s->P);
+    search_alloc(s.get());
+    // current weights start from the static weights (w0 = 1 for unweighted formulas, #15)
+    const int64_t m = c->Lo.m;
+    if (m > 0) {
+        if (c->Lo.precision == 64) dev::permute_weights_kernel<double><<<blocks_for(m, 256), 256>>>(c->w_pos.as<double>(), c->w_static_orig.as<double>(), c->order.as<int64_t>(), m);
+        else dev::permute_weights_kernel<float><<<blocks_for(m, 256), 256>>>(c->w_pos.as<float>(), c->w_static_orig.as<double>(), c->order.as<int64_t>(), m);
+    }
+    const int64_t tot = batch * c->Lo.n;
+    if (tot > 0) {
+        if (c->Lo.precision == 64) dev::init_points_kernel<double><<<blocks_for(tot, 256), 256>>>(s->X.as<double>(), batch, c->Lo.n, seed, point0, 0);
+        else dev::init_points_kernel<float><<<blocks_for(tot, 256), 256>>>(s->X.as<float>(), batch, c->Lo.n, seed, point0, 0);
+    }
+    CK(cudaGetLastError());
+    CK(cudaDeviceSynchronize());
+    *out = s.release();
+    return FFSAT_OK;
+    ABI_CATCH(c)
+}
+
+ffsat_status ffsat_search_set_x(ffsat_search* s, const void* x, int32_t on_device, void* stream) {
+    ffsat_ctx* c = s ? s->ctx : nullptr;
+    ABI_TRY(c)
+    if (!s || !x) throw Error(FFSAT_ERR_ARG, "null argument");
+    need_device(c);
+    const size_t bytes = (size_t)s->B * c->Lo.n * c->esize;
+    CK(cudaMemcpyAsync(s->X.p, x, bytes, on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, S(stream)));
+    if (!on_device) CK(cudaStreamSynchronize(S(stream)));
+    return FFSAT_OK;
+    ABI_CATCH(c)
+}
+
+ffsat_status ffsat_search_begin_round(ffsat_search* s, void* stream) {
+    ffsat_ctx* c = s ? s->ctx : nullptr;
+    ABI_TRY(c)
+    if (!s) throw Error(FFSAT_ERR_ARG, "null search");
+    need_device(c);
+    search_begin_round(s, S(stream));
+    return FFSAT_OK;
+    ABI_CATCH(c)
+}
+
+ffsat_status ffsat_search_iterate(ffsat_search* s, int32_t n_iters, void* stream) {
+    ffsat_ctx* c = s ? s->ctx : nullptr;
+    ABI_TRY(c)
+    if (!s || n_iters < 0) throw Error(FFSAT_ERR_ARG, "bad iterate arguments");
+    need_device(c);
+    search_iterate(s, n_iters, S(stream));
+    return FFSAT_OK;
+    ABI_CATCH(c)
+}
+
+ffsat_status ffsat_search_check(ffsat_search* s, void* stream) {
+    ffsat_ctx* c = s ? s->ctx : nullptr;
+    ABI_TRY(c)
+    if (!s) throw Error(FFSAT_ERR_ARG, "null search");
+    need_device(c);
+    search_check(s, S(stream));
+    return FFSAT_OK;
+    ABI_CATCH(c)
+}
+
+ffsat_status ffsat_search_restart(ffsat_search* s, const int32_t* U_global, void* stream) {
+    ffsat_ctx* c = s ? s->ctx : nullptr;
+    ABI_TRY(c)
+    if (!s) throw Error(FFSAT_ERR_ARG, "null search");
+    need_device(c);
+    search_restart(s, U_global, S(stream));
+    return FFSAT_OK;
+    ABI_CATCH(c)
+}
+
+ffsat_status ffsat_search_stats_get(ffsat_search* s, void* stream, ffsat_search_stats* out) {
+    ffsat_ctx* c = s ? s->ctx : nullptr;
+    ABI_TRY(c)
+    if (!s || !out) throw Error(FFSAT_ERR_ARG, "null argument");
+    need_device(c);
+    search_stats(s, S(stream), out);
+    return FFSAT_OK;
+    ABI_CATCH(c)
+}
+
+ffsat_status ffsat_search_get_buffers(ffsat_search* s, ffsat_search_buffers* o) {
+    ffsat_ctx* c = s ? s->ctx : nullptr;
+    ABI_TRY(c)
+    if (!s || !o) throw Error(FFSAT_ERR_ARG, "null argument");
+    o->x = s->X.p; o->grad = s->Gx.p; o->f = s->fX.as<double>(); o->eta = s->eta.as<double>();
+    o->unsat = s->unsat.as<int32_t>(); o->U = s->U.as<int32_t>(); o->weights = c->w_pos.p;
+    return FFSAT_OK;
+    ABI_CATCH(c)
+}
+
+ffsat_status ffsat_search_assignment(ffsat_search* s, int64_t lp, int8_t* out) {
+    ffsat_ctx* c = s ? s->ctx : nullptr;
+    ABI_TRY(c)
+    if (!s || !out || lp < 0 || lp >= s->B) throw Error(FFSAT_ERR_ARG, "bad assignment arguments");
+    need_device(c);
+    search_assignment(s, lp, out);
+    return FFSAT_OK;
+    ABI_CATCH(c)
+}
+
+void ffsat_search_free(ffsat_search* s) { delete s; }
+
+ffsat_status ffsat_solve(ffsat_ctx* c, int64_t batch, int64_t max_restarts, uint64_t seed, const ffsat_solve_params* params,
+                         int8_t* assignment_out, ffsat_result* res) {
+    ABI_TRY(c)
+    if (!assignment_out || !res || max_restarts < 1) throw Error(FFSAT_ERR_ARG, "bad solve arguments");
+    need_device(c);
+    auto t0 = std::chrono::steady_clock::now();
+    ffsat_search* sp = nullptr;
+    ffsat_status st0 = ffsat_search_create(c, batch, 0, seed, params, &sp);
+    if (st0 != FFSAT_OK) return st0;
+    std::unique_ptr<ffsat_search> s(sp);
+    cudaStream_t st = nullptr;
+    const int n = c->Lo.n;
+    std::vector<int8_t> cand((size_t)n), best((size_t)n, 1);
+    int64_t best_cnt = INT64_MAX;
+    double best_w = 0;
+    std::memset(res, 0, sizeof(*res));
+    auto elapsed = [&] { return std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count(); };
+    auto consider = [&](int64_t lp) {
+        search_assignment(s.get(), lp, cand.data());
+        double fw = 0;
+        int64_t cnt = exact_unsat(c->F, cand.data(), &fw);
+        if (cnt < best_cnt || (cnt == best_cnt && fw < best_w)) {
+            best_cnt = cnt;
+            best_w = fw;
+            best = cand;
+        }
+        return cnt == 0;
+    };
+    bool sat = false;
+    const ffsat_solve_params& P = s->P;
+    for (int64_t r = 0; r < max_restarts && !sat; ++r) {
+        search_begin_round(s.get(), st);
+        ffsat_search_stats ss{};
+        int it = 0;
+        while (it < P.max_inner) {
+            int step = std::min(P.check_every, P.max_inner - it);
+            search_iterate(s.get(), step, st);
+            it += step;
+            search_stats(s.get(), st, &ss);
+            res->iterations += step;
+            if (ss.solved_point >= 0 || ss.active == 0) break;
+            if (P.timeout_s > 0 && elapsed() > P.timeout_s) break;
+        }
+        search_stats(s.get(), st, &ss);
+        if (ss.solved_point >= 0 && consider(ss.solved_point)) sat = true;
+        search_check(s.get(), st);
+        search_stats(s.get(), st, &ss);
+        res->restarts = r + 1;
+        if (!sat && ss.best_point >= 0 && consider(ss.best_point)) sat = true;
+        if (sat) break;
+        if (P.timeout_s > 0 && elapsed() > P.timeout_s) break;
+        search_restart(s.get(), nullptr, st);
+    }
+    CK(cudaStreamSynchronize(st));
+    std::memcpy(assignment_out, best.data(), (size_t)n);
+    res->sat = sat ? 1 : 0;
+    res->best_unsat = best_cnt == INT64_MAX ? -1 : best_cnt;
+    res->best_falsified_weight = best_w;
+    res->seconds = elapsed();
+    return FFSAT_OK;
+    ABI_CATCH(c)
+}
+
+ffsat_status ffsat_launch_count(const ffsat_ctx* c, int64_t* out) {
+    ABI_TRY(nullptr)
+    if (!c || !out) throw Error(FFSAT_ERR_ARG, "null argument");
+    *out = c->launches;
+    return FFSAT_OK;
+    ABI_CATCH(nullptr)
+}
+
+ffsat_status ffsat_eval_profiled(ffsat_ctx* c, const void* x, int64_t B, double* f_out, void* grad_out, int32_t* unsat_out,
+                                 void* stream, double* ms4) {
+    ABI_TRY(c)
+    need_device(c);
+    if (B <= 0 || !x || !f_out || !ms4) throw Error(FFSAT_ERR_ARG, "bad profiled eval arguments");
+    for (cudaEvent_t& e : c->ev)
+        if (!e) CK(cudaEventCreate(&e));
+    cudaStream_t st = S(stream);
+    eval_device(c, x, B, f_out, grad_out, unsat_out, st, true);
+    CK(cudaEventSynchronize(c->ev[4]));
+    for (int i = 0; i < 4; ++i) {
+        float ms = 0;
+        CK(cudaEventElapsedTime(&ms, c->ev[i], c->ev[i + 1]));
+        ms4[i] = ms;
+    }
+    return FFSAT_OK;
+    ABI_CATCH(c)
+}
+
+void ffsat_free(ffsat_ctx* c) { delete c; }
+
+}  // extern "C"

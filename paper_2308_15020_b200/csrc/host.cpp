@@ -1,0 +1,429 @@
+// host.cpp -- host formula layer of libffsat: A1 parse/validate, A2 bucketing and CSR layouts,
+// A3 coefficient tables.  See host.hpp and DESIGN.md.
+#include "host.hpp"
+
+#include <algorithm>
+#include <array>
+#include <cerrno>
+#include <climits>
+#include <cmath>
+#include <cstring>
+#include <numeric>
+#include <sstream>
+
+namespace ffsat {
+
+// ------------------------------------------------------------------------------- A1: parse
+
+static bool parse_int(const std::string& s, long long* v) {
+    if (s.empty()) return false;
+    char* end = nullptr;
+    errno = 0;
+    long long r = std::strtoll(s.c_str(), &end, 10);
+    if (errno || *end) return false;
+    *v = r;
+    return true;
+}
+
+Formula parse_text(const std::string& text) {
+    Formula F;
+    bool have_header = false, weighted = false, cnf = false;
+    std::istringstream in(text);
+    std::string line;
+    long long lineno = 0;
+    std::vector<int32_t> stamp;
+    auto fail = [&](ffsat_status c, const std::string& msg) {
+        throw Error(c, "line " + std::to_string(lineno) + ": " + msg);
+    };
+    while (std::getline(in, line)) {
+        ++lineno;
+        std::istringstream ls(line);
+        std::vector<std::string> tok;
+        for (std::string t; ls >> t;) tok.push_back(t);
+        if (tok.empty() || tok[0] == "c" || tok[0][0] == '%') continue;
+        if (tok[0] == "p") {
+            long long n, m;
+            if (have_header) fail(FFSAT_ERR_PARSE, "second header");
+            if (tok.size() != 4 || (tok[1] != "cnf" && tok[1] != "hnf" && tok[1] != "whnf") ||
+                !parse_int(tok[2], &n) || !parse_int(tok[3], &m) || n < 0 || n > INT32_MAX || m < 0)
+                fail(FFSAT_ERR_PARSE, "bad header (expected 'p cnf|hnf|whnf <n> <m>')");
+            F.n = (int32_t)n;
+            cnf = tok[1] == "cnf";
+            weighted = tok[1] == "whnf";
+            have_header = true;
+            stamp.assign((size_t)n + 1, -1);
+            continue;
+        }
+        if (!have_header) fail(FFSAT_ERR_PARSE, "constraint before header");
+        size_t i = 0;
+        double w = 1.0;
+        if (weighted) {
+            char* end = nullptr;
+            w = std::strtod(tok[0].c_str(), &end);
+            if (*end) fail(FFSAT_ERR_PARSE, "bad weight '" + tok[0] + "'");
+            if (!std::isfinite(w)) fail(FFSAT_ERR_NONFINITE, "non-finite weight");
+            ++i;
+        }
+        int kind = FFSAT_OR;
+        long long bound = 0;
+        if (!cnf) {
+            if (i >= tok.size()) fail(FFSAT_ERR_PARSE, "missing constraint tag");
+            const std::string& tag = tok[i++];
+            if (tag == "o") kind = FFSAT_OR;
+            else if (tag == "x") kind = FFSAT_XOR;
+            else if (tag == "xn") kind = FFSAT_XNOR;
+            else if (tag == "n") kind = FFSAT_NAE;
+            else if (tag == "d" || tag == "a") {
+                kind = tag == "d" ? FFSAT_CARD_GE : FFSAT_CARD_LE;
+                if (i >= tok.size() || !parse_int(tok[i], &bound)) fail(FFSAT_ERR_PARSE, "bad cardinality bound");
+                ++i;
+            } else fail(FFSAT_ERR_PARSE, "unknown constraint tag '" + tag + "'");
+        }
+        if (tok.back() != "0") fail(FFSAT_ERR_PARSE, "constraint not terminated by 0");
+        int32_t cidx = (int32_t)F.kind.size();
+        int64_t k = 0;
+        for (; i + 1 < tok.size(); ++i) {
+            long long v;
+            if (!parse_int(tok[i], &v) || v == 0) fail(FFSAT_ERR_PARSE, "bad literal '" + tok[i] + "'");
+            long long a = v < 0 ? -v : v;
+            if (a > F.n) fail(FFSAT_ERR_RANGE, "literal " + tok[i] + " out of range");
+            if (stamp[(size_t)a] == cidx) fail(FFSAT_ERR_DUPVAR, "duplicate variable " + std::to_string(a));
+            stamp[(size_t)a] = cidx;
+            F.lits.push_back((int32_t)v);
+            ++k;
+        }
+        if (k == 0) fail(FFSAT_ERR_PARSE, "empty constraint");
+        if ((kind == FFSAT_CARD_GE || kind == FFSAT_CARD_LE) && (bound < 0 || bound > k))
+            fail(FFSAT_ERR_BOUND, "cardinality bound out of range");
+        F.kind.push_back((uint8_t)kind);
+        F.bound.push_back((int32_t)bound);
+        F.weight.push_back(w);
+        F.offsets.push_back((int64_t)F.lits.size());
+    }
+    if (!have_header) throw Error(FFSAT_ERR_PARSE, "line " + std::to_string(lineno) + ": missing header");
+    return F;
+}
+
+Formula from_arrays(const ffsat_formula& f) {
+    if (f.n_vars < 0 || f.n_cons < 0) throw Error(FFSAT_ERR_ARG, "negative sizes");
+    if (f.n_cons > 0 && (!f.kind || !f.offsets || !f.lits)) throw Error(FFSAT_ERR_ARG, "null formula arrays");
+    Formula F;
+    F.n = f.n_vars;
+    int64_t m = f.n_cons;
+    if (m == 0) return F;
+    if (f.offsets[0] != 0) throw Error(FFSAT_ERR_ARG, "offsets[0] must be 0");
+    for (int64_t c = 0; c < m; ++c)
+        if (f.offsets[c + 1] < f.offsets[c]) throw Error(FFSAT_ERR_ARG, "offsets must be non-decreasing");
+    int64_t L = f.offsets[m];
+    F.kind.assign(f.kind, f.kind + m);
+    F.bound.assign((size_t)m, 0);
+    if (f.bound) F.bound.assign(f.bound, f.bound + m);
+    F.weight.assign((size_t)m, 1.0);
+    if (f.weight) F.weight.assign(f.weight, f.weight + m);
+    F.offsets.assign(f.offsets, f.offsets + m + 1);
+    F.lits.assign(f.lits, f.lits + L);
+    return F;
+}
+
+void validate(const Formula& F) {
+    std::vector<int64_t> stamp((size_t)F.n + 1, -1);
+    for (int64_t c = 0; c < F.m(); ++c) {
+        std::string where = "constraint " + std::to_string(c);
+        if (F.kind[c] > FFSAT_NAE) throw Error(FFSAT_ERR_ARG, where + ": unknown kind");
+        int64_t k = F.offsets[c + 1] - F.offsets[c];
+        if (k <= 0) throw Error(FFSAT_ERR_ARG, where + ": empty constraint");
+        if (!std::isfinite(F.weight[c])) throw Error(FFSAT_ERR_NONFINITE, where + ": non-finite weight");
+        if ((F.kind[c] == FFSAT_CARD_GE || F.kind[c] == FFSAT_CARD_LE) && (F.bound[c] < 0 || F.bound[c] > k))
+            throw Error(FFSAT_ERR_BOUND, where + ": cardinality bound out of range");
+        for (int64_t i = F.offsets[c]; i < F.offsets[c + 1]; ++i) {
+            int64_t v = F.lits[i];
+            int64_t a = v < 0 ? -v : v;
+            if (v == 0 || a > F.n) throw Error(FFSAT_ERR_RANGE, where + ": literal out of range");
+            if (stamp[(size_t)a] == c) throw Error(FFSAT_ERR_DUPVAR, where + ": duplicate variable " + std::to_string(a));
+            stamp[(size_t)a] = c;
+        }
+    }
+}
+
+// ------------------------------------------------------------------------------- classification
+
+SatRule sat_rule(int kind, int k, int bound) {
+    switch (kind) {
+    case FFSAT_OR: return {1, k, 0};
+    case FFSAT_XOR: return {0, k, 1};
+    case FFSAT_XNOR: return {0, k, 2};
+    case FFSAT_CARD_GE: return {bound, k, 0};
+    case FFSAT_CARD_LE: return {0, bound, 0};
+    case FFSAT_NAE: return {1, k - 1, 0};
+    }
+    return {1, 0, 0};
+}
+
+bool fast_form(int kind, int k, int bound, FastForm* o) {
+    *o = FastForm{V_OR, 0, 0, 0, 0};
+    if (k > kFastKMax) return false;  // long constraints of any kind take the root-product path
+    if (kind == FFSAT_XOR) { *o = {V_XOR, 0, 0, 0, 1}; return true; }
+    if (kind == FFSAT_XNOR) { *o = {V_XNOR, 0, 0, 0, -1}; return true; }
+    if (kind == FFSAT_NAE) { *o = {V_NAE, -1, 2, 2, 0}; return true; }
+    if (kind == FFSAT_OR || (kind == FFSAT_CARD_GE && bound == 1)) { *o = {V_OR, -1, 2, 0, 0}; return true; }
+    if ((kind == FFSAT_CARD_GE && bound == 0) || (kind == FFSAT_CARD_LE && bound == k)) { *o = {V_TRUE, -1, 0, 0, 0}; return true; }
+    if (kind == FFSAT_CARD_GE && bound == k) { *o = {V_AND, 1, 0, -2, 0}; return true; }
+    if (kind == FFSAT_CARD_LE && bound == 0) { *o = {V_NOR, 1, -2, 0, 0}; return true; }
+    if (kind == FFSAT_CARD_LE && bound == k - 1) { *o = {V_NAND, -1, 0, 2, 0}; return true; }
+    return false;
+}
+
+// ------------------------------------------------------------------------------- A3: coefficients
+
+// g_m = 1/(k+1) sum_t f(t) w^{-tm}, w = exp(-2 pi i/(k+1)) (P:151 sign, #1); f(t) = -1 on the
+// satisfying interval, +1 elsewhere.  Root-product factors alpha_m + beta_m l with alpha = (1+w^m)/2,
+// beta = (1-w^m)/2 (probability basis); G_m = 2 g_m except the Nyquist root.
+static void sym_coefficients(int k, SatRule r, std::vector<double>& coef, double* g0_out, int* Mp_out) {
+    const int K1 = k + 1;
+    std::vector<long double> cs(K1), sn(K1);
+    const long double two_pi = 6.283185307179586476925286766559005768L;
+    for (int j = 0; j < K1; ++j) {
+        long double a = two_pi * (long double)j / (long double)K1;
+        cs[j] = cosl(a);
+        sn[j] = sinl(a);
+    }
+    std::vector<int> f(K1);
+    long double s0 = 0;
+    for (int t = 0; t <= k; ++t) {
+        bool sat = t >= r.tmin && t <= r.tmax && (r.parity == 0 || (r.parity == 1) == ((t & 1) == 1));
+        f[t] = sat ? -1 : 1;
+        s0 += f[t];
+    }
+    *g0_out = (double)(s0 / K1);
+    const int Mp = K1 / 2;
+    *Mp_out = Mp;
+    for (int m = 1; m <= Mp; ++m) {
+        long double re = 0, im = 0;  // sum_t f(t) e^{+2 pi i t m/(k+1)} = sum_t f(t) w^{-tm}
+        for (int t = 0; t <= k; ++t) {
+            int j = (int)(((long long)t * m) % K1);
+            re += f[t] * cs[j];
+            im += f[t] * sn[j];
+        }
+        long double gre = re / K1, gim = im / K1;
+        long double mult = (2 * m == K1) ? 1.0L : 2.0L;
+        long double Gre = mult * gre, Gim = mult * gim;
+        // w^m = exp(-2 pi i m / K1) = cos - i sin
+        int jm = m % K1;
+        long double wr = cs[jm], wi = -sn[jm];
+        long double ar = (1 + wr) / 2, ai = wi / 2;
+        long double br = (1 - wr) / 2, bi = -wi / 2;
+        long double Hr = Gre * br - Gim * bi, Hi = Gre * bi + Gim * br;
+        double row[8] = {(double)ar, (double)ai, (double)br, (double)bi, (double)Gre, (double)Gim, (double)Hr, (double)Hi};
+        coef.insert(coef.end(), row, row + 8);
+    }
+}
+
+// ------------------------------------------------------------------------------- tiled sizing
+
+int tiled_stage_rows(int precision) { return precision == 64 ? 256 : 512; }
+
+size_t tiled_smem_bytes(int n, int precision, int stage_rows) {
+    size_t es = precision == 64 ? 8 : 4;
+    return (size_t)32 * es * (2 * (size_t)n + (size_t)stage_rows) + 64 * 8;
+}
+
+int tiled_max_n(int precision) {
+    const size_t budget = 227 * 1024;
+    int rows = tiled_stage_rows(precision);
+    int n = 0;
+    while (tiled_smem_bytes(n + 1, precision, rows) <= budget && n < 32767) ++n;
+    return n;
+}
+
+// ------------------------------------------------------------------------------- A2: layout
+
+int sym_group(int k) {
+    int need = (k + 7) / 8;  // CK = 8 literals per thread at most (G <= 512: k <= 4096)
+    int G = 32;
+    while (G < need) G *= 2;
+    return G;
+}
+
+Layout build_layout(const Formula& F, int path, int precision) {
+    Layout Lo;
+    Lo.n = F.n;
+    Lo.m = F.m();
+    Lo.L = F.lits.size();
+    const int64_t m = F.m();
+    std::vector<FastForm> ff((size_t)m);
+    std::vector<char> is_fast((size_t)m, 0);
+    bool need64 = false;
+    for (int64_t c = 0; c < m; ++c) {
+        int k = (int)(F.offsets[c + 1] - F.offsets[c]);
+        Lo.max_k = std::max(Lo.max_k, k);
+        is_fast[c] = fast_form(F.kind[c], k, F.bound[c], &ff[c]);
+        if (!is_fast[c]) {
+            if (k > 4096) throw Error(FFSAT_ERR_ARG, "constraint " + std::to_string(c) + ": cardinality length > 4096 unsupported");
+            if (k > 64) need64 = true;
+        }
+    }
+    if (precision == 0) precision = need64 ? 64 : 32;
+    if (precision != 32 && precision != 64) throw Error(FFSAT_ERR_ARG, "precision must be 0, 32 or 64");
+    Lo.precision = precision;
+
+    // fast buckets keyed by (k, variant), sym grouped by (G class, k, rule)
+    std::vector<int64_t> fast_ids, sym_ids;
+    for (int64_t c = 0; c < m; ++c) (is_fast[c] ? fast_ids : sym_ids).push_back(c);
+    auto klen = [&](int64_t c) { return (int)(F.offsets[c + 1] - F.offsets[c]); };
+    std::stable_sort(fast_ids.begin(), fast_ids.end(), [&](int64_t a, int64_t b) {
+        int ka = klen(a), kb = klen(b);
+        if (ka != kb) return ka < kb;
+        return ff[a].variant < ff[b].variant;
+    });
+    std::stable_sort(sym_ids.begin(), sym_ids.end(), [&](int64_t a, int64_t b) {
+        int ga = sym_group(klen(a)), gb = sym_group(klen(b));
+        if (ga != gb) return ga < gb;
+        return klen(a) > klen(b);
+    });
+    Lo.order = fast_ids;
+    Lo.order.insert(Lo.order.end(), sym_ids.begin(), sym_ids.end());
+    Lo.pos_of.assign((size_t)m, 0);
+    for (int64_t p = 0; p < m; ++p) Lo.pos_of[Lo.order[p]] = p;
+    Lo.w_pos.resize((size_t)m);
+    for (int64_t p = 0; p < m; ++p) Lo.w_pos[p] = F.weight[Lo.order[p]];
+
+    // ---- fast layout
+    Lo.n_fast = (int64_t)fast_ids.size();
+    for (int64_t p = 0; p < Lo.n_fast; ++p) {
+        int64_t c = fast_ids[p];
+        int k = klen(c);
+        if (Lo.fbuckets.empty() || Lo.fbuckets.back().k != k || Lo.fbuckets.back().variant != ff[c].variant) {
+            FastBucket b{};
+            b.variant = ff[c].variant;
+            b.k = k;
+            b.kp = (k + 3) / 4 * 4;
+            b.pos_begin = p;
+            b.word_off = Lo.n_fast_words;
+            b.slot_off = Lo.n_fast_lits;
+            b.g0 = ff[c].g0; b.gA = ff[c].gA; b.gB = ff[c].gB; b.gX = ff[c].gX;
+            b.rule = sat_rule(F.kind[c], k, F.bound[c]);
+            Lo.fbuckets.push_back(b);
+        }
+        FastBucket& b = Lo.fbuckets.back();
+        b.pos_end = p + 1;
+        for (int i = 0; i < b.kp; ++i) {
+            uint32_t w = 0;
+            if (i < k) {
+                int32_t lit = F.lits[F.offsets[c] + i];
+                w = (uint32_t)((lit > 0 ? lit : -lit) - 1) | (lit < 0 ? 0x80000000u : 0u);
+            }
+            Lo.fast_words.push_back(w);
+        }
+        Lo.n_fast_words += b.kp;
+        Lo.n_fast_lits += k;
+    }
+
+    // ---- sym layout
+    Lo.n_sym = (int64_t)sym_ids.size();
+    Lo.sym_off.push_back(0);
+    std::vector<std::array<int, 4>> sig_keys;
+    for (int64_t s = 0; s < Lo.n_sym; ++s) {
+        int64_t c = sym_ids[s];
+        int k = klen(c);
+        SatRule r = sat_rule(F.kind[c], k, F.bound[c]);
+        std::array<int, 4> key{k, r.tmin, r.tmax, r.parity};
+        int sig = -1;
+        for (size_t q = 0; q < sig_keys.size(); ++q)
+            if (sig_keys[q] == key) { sig = (int)q; break; }
+        if (sig < 0) {
+            SymSig S{};
+            S.k = k; S.tmin = r.tmin; S.tmax = r.tmax; S.parity = r.parity;
+            S.coef_off = (int64_t)Lo.coef.size() / 8;
+            sym_coefficients(k, r, Lo.coef, &S.g0, &S.Mp);
+            sig = (int)Lo.sigs.size();
+            Lo.sigs.push_back(S);
+            sig_keys.push_back(key);
+        }
+        Lo.sym_sig.push_back(sig);
+        Lo.sym_rule.push_back(r.tmin); Lo.sym_rule.push_back(r.tmax); Lo.sym_rule.push_back(r.parity);
+        for (int i = 0; i < k; ++i) {
+            int32_t lit = F.lits[F.offsets[c] + i];
+            Lo.sym_words.push_back((uint32_t)((lit > 0 ? lit : -lit) - 1) | (lit < 0 ? 0x80000000u : 0u));
+        }
+        Lo.n_sym_lits += k;
+        Lo.sym_root_lits += (int64_t)k * ((k + 1) / 2);
+        Lo.sym_off.push_back(Lo.n_sym_lits);
+        int G = sym_group(k);
+        if (Lo.sym_classes.empty() || Lo.sym_classes.back().G != G) Lo.sym_classes.push_back({G, s, s + 1});
+        else Lo.sym_classes.back().end = s + 1;
+    }
+
+    // ---- path
+    if (path == 0) path = (Lo.n_fast > 0 && F.n <= tiled_max_n(precision)) ? 1 : 2;
+    if (path == 1 && F.n > tiled_max_n(precision)) throw Error(FFSAT_ERR_ARG, "tiled path needs n <= " + std::to_string(tiled_max_n(precision)));
+    if (path != 1 && path != 2) throw Error(FFSAT_ERR_ARG, "path must be 0, 1 or 2");
+    Lo.path = path;
+
+    // ---- T-buffer slots and occurrence CSR (ascending slot order per variable)
+    Lo.tb_fast = path == 2 ? Lo.n_fast_lits : 0;
+    Lo.tb_slots = Lo.tb_fast + Lo.n_sym_lits;
+    std::vector<int32_t> slot_var((size_t)Lo.tb_slots);
+    if (path == 2) {
+        for (const FastBucket& b : Lo.fbuckets)
+            for (int64_t p = b.pos_begin; p < b.pos_end; ++p)
+                for (int i = 0; i < b.k; ++i)
+                    slot_var[(size_t)(b.slot_off + (p - b.pos_begin) * b.k + i)] =
+                        (int32_t)(Lo.fast_words[(size_t)(b.word_off + (p - b.pos_begin) * b.kp + i)] & 0x7fffffffu);
+    }
+    for (int64_t j = 0; j < Lo.n_sym_lits; ++j) slot_var[(size_t)(Lo.tb_fast + j)] = (int32_t)(Lo.sym_words[(size_t)j] & 0x7fffffffu);
+    Lo.occ_off.assign((size_t)F.n + 1, 0);
+    for (int32_t v : slot_var) Lo.occ_off[(size_t)v + 1]++;
+    for (int32_t v = 0; v < F.n; ++v) Lo.occ_off[(size_t)v + 1] += Lo.occ_off[(size_t)v];
+    Lo.occ_slot.assign((size_t)Lo.tb_slots, 0);
+    {
+        std::vector<int64_t> cur(Lo.occ_off.begin(), Lo.occ_off.end() - 1);
+        for (int64_t s = 0; s < Lo.tb_slots; ++s) Lo.occ_slot[(size_t)cur[(size_t)slot_var[(size_t)s]]++] = s;
+    }
+
+    // ---- work units (both paths): runs of one bucket with <= unit_rows literals; on the tiled path each
+    //      unit is one shared-memory staging batch with var-sorted rows and per-variable segments
+    Lo.stage_rows = path == 1 ? tiled_stage_rows(precision) : 512;
+    if (path == 1) Lo.tiled_words.assign(Lo.fast_words.size(), 0);
+    std::vector<std::pair<uint32_t, int64_t>> pairs;  // (var, word index)
+    for (size_t bi = 0; bi < Lo.fbuckets.size(); ++bi) {
+        const FastBucket& b = Lo.fbuckets[bi];
+        int64_t p = b.pos_begin;
+        while (p < b.pos_end) {
+            int64_t per = std::max<int64_t>(1, Lo.stage_rows / b.k);
+            int64_t q = std::min(b.pos_end, p + per);
+            SubChunk sc{};
+            sc.bucket = (int32_t)bi;
+            sc.pos_begin = p;
+            sc.pos_end = q;
+            sc.rows = (int32_t)((q - p) * b.k);
+            sc.seg_begin = sc.seg_end = (int32_t)(Lo.segs.size() / 2);
+            if (path == 1) {
+                pairs.clear();
+                for (int64_t r = p; r < q; ++r)
+                    for (int i = 0; i < b.k; ++i) {
+                        int64_t wi = b.word_off + (r - b.pos_begin) * b.kp + i;
+                        pairs.push_back({Lo.fast_words[(size_t)wi] & 0x7fffffffu, wi});
+                    }
+                std::stable_sort(pairs.begin(), pairs.end(),
+                                 [](const std::pair<uint32_t, int64_t>& a, const std::pair<uint32_t, int64_t>& c) { return a.first < c.first; });
+                int32_t row = 0;
+                for (size_t j = 0; j < pairs.size(); ++j) {
+                    if (j == 0 || pairs[j].first != pairs[j - 1].first) {
+                        Lo.segs.push_back(pairs[j].first);
+                        Lo.segs.push_back((uint32_t)row);
+                    }
+                    uint32_t w = Lo.fast_words[(size_t)pairs[j].second];
+                    Lo.tiled_words[(size_t)pairs[j].second] = (w & 0x7fffffffu) | ((uint32_t)row << 16) | (w & 0x80000000u);
+                    ++row;
+                    Lo.segs[Lo.segs.size() - 1] = (Lo.segs[Lo.segs.size() - 1] & 0xffffu) | ((uint32_t)row << 16);
+                }
+                sc.seg_end = (int32_t)(Lo.segs.size() / 2);
+            }
+            Lo.subchunks.push_back(sc);
+            p = q;
+        }
+    }
+    return Lo;
+}
+
+}  // namespace ffsat

@@ -1,0 +1,112 @@
+// host.hpp -- host-side formula layer of libffsat (steps A1-A3 of DESIGN.md):
+// parse + validate (A1), classify / bucket / CSR layouts (A2), per-signature fp64
+// coefficient tables (A3).  Plain C++17, no CUDA.
+#pragma once
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/ffsat.h"
+
+namespace ffsat {
+
+struct Error : std::runtime_error {
+    ffsat_status code;
+    Error(ffsat_status c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+struct Formula {
+    int32_t n = 0;
+    std::vector<uint8_t> kind;
+    std::vector<int32_t> bound;
+    std::vector<double> weight;
+    std::vector<int64_t> offsets{0};
+    std::vector<int32_t> lits;
+    int64_t m() const { return (int64_t)kind.size(); }
+};
+
+Formula parse_text(const std::string& text);           // throws Error (FFSAT_ERR_PARSE/RANGE/DUPVAR/BOUND)
+Formula from_arrays(const ffsat_formula& f);           // copies
+void validate(const Formula& F);                       // throws Error
+
+// Satisfaction of a constraint as an interval of the True-count t plus a parity rule:
+// satisfied iff tmin <= t <= tmax and (parity == 0 || (parity == 1 && t odd) || (parity == 2 && t even)).
+struct SatRule { int32_t tmin, tmax, parity; };
+SatRule sat_rule(int kind, int k, int bound);
+
+// Fast-path variants (PAPER.md footnote P:964 and App. B):
+// FE = g0 + gA * A + gB * Bp + gX * X with A = prod (1+l)/2, Bp = prod (1-l)/2, X = prod l.
+enum Variant : int32_t { V_OR = 0, V_AND, V_NAE, V_XOR, V_XNOR, V_TRUE, V_NOR, V_NAND, V_COUNT };
+struct FastForm { int32_t variant; double g0, gA, gB, gX; };
+bool fast_form(int kind, int k, int bound, FastForm* out);
+
+struct FastBucket {
+    int32_t variant, k, kp;        // kp = k rounded up to a multiple of 4 (16-byte literal rows)
+    int64_t pos_begin, pos_end;    // constraint positions (layout order)
+    int64_t word_off;              // first padded literal word of the bucket
+    int64_t slot_off;              // first (unpadded) literal slot of the bucket
+    double g0, gA, gB, gX;
+    SatRule rule;
+};
+
+constexpr int kFastKMax = 64;       // fast product paths handle k <= 64; longer constraints use roots
+
+struct SymSig {                     // a (k, sat rule) signature with its root table
+    int32_t k, tmin, tmax, parity, Mp;  // Mp = floor((k+1)/2) roots m = 1..Mp
+    int64_t coef_off;               // 8 doubles per root: alpha(re,im) beta(re,im) G(re,im) H(re,im)
+    double g0;
+};
+
+struct SymClass {                   // launch class: group size G threads per (constraint, point)
+    int32_t G;
+    int64_t begin, end;             // sym constraint indices
+};
+
+struct SubChunk {                   // tiled path: one smem staging batch
+    int32_t bucket;
+    int32_t seg_begin, seg_end;
+    int64_t pos_begin, pos_end;     // fast constraint positions
+    int32_t rows;                   // staging rows used
+};
+
+int sym_group(int k);               // threads per (constraint, point) on the root path
+
+struct Layout {
+    int32_t n = 0, path = 0, precision = 32, max_k = 0;
+    int64_t m = 0, L = 0;
+    std::vector<int64_t> order;     // position -> original constraint index (fast first, then sym)
+    std::vector<int64_t> pos_of;    // original constraint index -> position
+    std::vector<double> w_pos;      // static weight by position
+    // fast
+    int64_t n_fast = 0, n_fast_lits = 0, n_fast_words = 0;
+    std::vector<FastBucket> fbuckets;
+    std::vector<uint32_t> fast_words;   // var | neg << 31 (padded rows)
+    // sym
+    int64_t n_sym = 0, n_sym_lits = 0, sym_root_lits = 0;
+    std::vector<SymSig> sigs;
+    std::vector<double> coef;
+    std::vector<int32_t> sym_sig;       // per sym constraint
+    std::vector<int64_t> sym_off;       // [n_sym + 1] literal offsets into sym_words
+    std::vector<uint32_t> sym_words;    // var | neg << 31
+    std::vector<int32_t> sym_rule;      // 3 ints per sym constraint (tmin, tmax, parity)
+    std::vector<SymClass> sym_classes;
+    // T-buffer slots (global path: fast slots then sym slots; tiled path: sym slots only)
+    int64_t tb_fast = 0, tb_slots = 0;
+    std::vector<int64_t> occ_off;       // [n + 1]
+    std::vector<int64_t> occ_slot;      // ascending slot ids per variable
+    // tiled fast path
+    int32_t stage_rows = 0;
+    std::vector<uint32_t> tiled_words;  // var | row << 16 | neg << 31 (padded rows)
+    std::vector<SubChunk> subchunks;
+    std::vector<uint32_t> segs;         // 2 words per segment: var, row_begin | row_end << 16
+};
+
+// Build everything; path: 0 auto, 1 tiled, 2 global; precision 0 auto / 32 / 64.
+Layout build_layout(const Formula& F, int path, int precision);
+// Tiled-path admission: staging rows and the max n that fits shared memory for the dtype.
+int tiled_stage_rows(int precision);
+int tiled_max_n(int precision);
+size_t tiled_smem_bytes(int n, int precision, int stage_rows);
+
+}  // namespace ffsat

@@ -1,0 +1,328 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the oracle on the same seeded inputs.
+
+Tolerances (BASELINE.json north_star): f and grad within 1e-4 * max(1, |ref|) elementwise on the
+fp32 path, 1e-9 * max(1, |ref|) on the fp64 path; satisfied/unsat counts bit-exact.  The oracle
+evaluates at exactly the values the GPU received (fp32 inputs promoted to fp64).
+"""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+import paper_2308_15020_b200 as P
+import synth
+from conftest import golden
+from oracle import cdp
+from oracle import solve as osolve
+from oracle.formula import OracleFormula, parse
+from oracle.philox import uniform_pm1
+
+TOL = {32: 1e-4, 64: 1e-9}
+
+
+@pytest.fixture(scope="module", autouse=True)
+def cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    torch.cuda.set_device(0)
+
+
+def oracle_of(inst):
+    return OracleFormula.from_arrays(*inst.arrays())
+
+
+def compare(inst, X, precision=32, path=0, check_unsat=True, device_path=True, ctx=None):
+    ctx = ctx or P.Context.from_instance(inst, precision=precision, path=path, device=0)
+    dt = np.float64 if ctx.info["precision"] == 64 else np.float32
+    X = np.ascontiguousarray(X, dtype=dt)
+    if device_path:
+        f, g, u = ctx.eval(torch.from_numpy(X).cuda(), grad=True, unsat=True)
+        torch.cuda.synchronize()
+        f, g, u = f.cpu().numpy(), g.cpu().numpy(), u.cpu().numpy()
+    else:
+        f, g, u = ctx.eval(X, grad=True, unsat=True)
+    Fo = oracle_of(inst)
+    fo, go = cdp.evaluate(Fo, X.astype(np.float64))
+    tol = TOL[ctx.info["precision"]]
+    ef = np.max(np.abs(f - fo) / np.maximum(1.0, np.abs(fo))) if len(fo) else 0.0
+    eg = np.max(np.abs(g - go) / np.maximum(1.0, np.abs(go))) if g.size else 0.0
+    assert ef <= tol, f"f rel err {ef:.3e} > {tol}"
+    assert eg <= tol, f"grad rel err {eg:.3e} > {tol}"
+    if check_unsat:
+        uo, _ = cdp.check(Fo, X.astype(np.float64))
+        assert np.array_equal(u, uo), "unsat counts differ"
+    return ctx, ef, eg
+
+
+# ------------------------------------------------------------------ eval parity, small sizes
+
+
+@pytest.mark.parametrize("path", [1, 2])
+@pytest.mark.parametrize("dist", ["U", "N", "C", "Z"])
+def test_c1_3sat(path, dist):
+    inst = synth.config1(0)
+    for B in (1, 37):
+        compare(inst, synth.points(dist, B, inst.n, 1000 + B), path=path)
+
+
+@pytest.mark.parametrize("precision", [32, 64])
+@pytest.mark.parametrize("path", [1, 2])
+def test_mixed_all_kinds(precision, path):
+    """Every kind, k = 1..64 (fast templated k <= 16, blocked 16 < k <= 64, root path for the
+    cardinalities), random weights, ragged batch."""
+    inst = synth.random_mixed(n=90, m=400, seed=11, kmax=64)
+    compare(inst, synth.points("U", 77, inst.n, 3), precision=precision, path=path)
+    compare(inst, synth.points("N", 33, inst.n, 4), precision=precision, path=path)
+
+
+def test_host_buffers_equal_device_buffers():
+    inst = synth.random_mixed(n=50, m=200, seed=12, kmax=30)
+    X = synth.points("U", 40, inst.n, 5)
+    ctx = P.Context.from_instance(inst, device=0)
+    fh, gh, uh = ctx.eval(X, grad=True, unsat=True)
+    fd, gd, ud = ctx.eval(torch.from_numpy(X).cuda(), grad=True, unsat=True)
+    assert np.array_equal(fh, fd.cpu().numpy()) and np.array_equal(gh, gd.cpu().numpy())
+    assert np.array_equal(uh, ud.cpu().numpy())
+
+
+def test_deterministic_bitwise():
+    inst = synth.config2(0)
+    X = torch.from_numpy(synth.points("U", 256, inst.n, 7)).cuda()
+    ctx = P.Context.from_instance(inst, device=0)
+    a = ctx.eval(X)
+    b = ctx.eval(X)
+    assert torch.equal(a[0], b[0]) and torch.equal(a[1], b[1])
+
+
+def test_paths_agree_bitwise_on_f_within_tol_on_grad():
+    inst = synth.random_mixed(n=60, m=300, seed=13, kmax=16)
+    X = synth.points("U", 64, inst.n, 8)
+    compare(inst, X, path=1)
+    compare(inst, X, path=2)
+
+
+@pytest.mark.parametrize("name", ["xor1", "xor2", "xor3", "card1", "card2", "card3", "xor+card"])
+def test_rq1_workloads(name):
+    """PAPER.md App. D RQ1 formulas: XOR k = 8..32 fast path, cardinality k = 8..32 root path."""
+    inst = synth.rq1(name, seed=1)
+    compare(inst, synth.points("U", 64, inst.n, 21))
+    compare(inst, synth.points("N", 32, inst.n, 22))
+
+
+@pytest.mark.parametrize("N", [20, 60])
+def test_benchmark1_cardinality(N):
+    inst = synth.random_card(N, seed=2)
+    compare(inst, synth.points("U", 40, inst.n, 23))
+
+
+def test_parity_learning_c4():
+    inst = synth.config4_parity(0)
+    compare(inst, synth.points("U", 50, inst.n, 24))
+    compare(inst, synth.points("C", 50, inst.n, 25))
+
+
+def test_c4_hybrid_small():
+    inst = synth.config4_hybrid(0, n=300, m3=600, n_xor=120)
+    compare(inst, synth.points("U", 64, inst.n, 26))
+
+
+@pytest.mark.parametrize("k", [65, 130, 300, 700])
+def test_long_cardinality_fp64(k):
+    """Root path in fp64 at long k (group sizes 32..128), at-most-b, mixed with clauses."""
+    inst = synth.config3(0, n=1500, m3=200, n_card=3, kmin=k, kmax=k)
+    compare(inst, synth.points("U", 5, inst.n, 27))
+    compare(inst, synth.points("N", 3, inst.n, 28))
+
+
+def test_long_xor_or_root_path():
+    """Fast kinds longer than 64 go to the root path (general truth table incl. parity)."""
+    cons = [(1, 0, 1.0, list(range(1, 101))), (0, 0, 2.0, [-v for v in range(20, 120)]),
+            (5, 0, 0.5, list(range(5, 90))), (2, 0, 1.0, list(range(3, 70)))]
+    Fo = OracleFormula.from_constraints(130, cons)
+    inst = synth.Instance("longfast", 130, Fo.kind, Fo.bound, Fo.weight, Fo.offsets, Fo.lits)
+    compare(inst, synth.points("U", 9, 130, 29) * 0.3 + 0.5, precision=64)
+
+
+def test_edge_cases():
+    # single literal, single constraint, B = 1
+    Fo = OracleFormula.from_constraints(1, [(0, 0, 1.0, [1])])
+    inst = synth.Instance("unit", 1, Fo.kind, Fo.bound, Fo.weight, Fo.offsets, Fo.lits)
+    compare(inst, np.array([[0.25]], np.float32))
+    compare(inst, np.array([[0.0], [-0.0], [1.0], [-1.0]], np.float32))
+    # constant constraints (GE b = 0, LE b = k) contribute -w and no gradient
+    Fo = OracleFormula.from_constraints(3, [(3, 0, 1.0, [1, 2]), (4, 3, 2.0, [1, 2, 3]), (0, 0, 1.0, [2, -3])])
+    inst = synth.Instance("const", 3, Fo.kind, Fo.bound, Fo.weight, Fo.offsets, Fo.lits)
+    compare(inst, synth.points("U", 5, 3, 30))
+    # empty batch
+    ctx = P.Context.from_instance(synth.config1(0), device=0)
+    f, g, u = ctx.eval(np.zeros((0, 20), np.float32), unsat=True)
+    assert f.shape == (0,)
+    # no constraints at all
+    inst = synth.Instance("empty", 4, np.zeros(0, np.uint8), np.zeros(0, np.int32), np.zeros(0),
+                          np.zeros(1, np.int64), np.zeros(0, np.int32))
+    ctx = P.Context.from_instance(inst, device=0)
+    f, g, u = ctx.eval(np.ones((3, 4), np.float32), unsat=True)
+    assert np.all(f == 0) and np.all(g == 0) and np.all(u == 0)
+
+
+def test_paper_examples_on_gpu():
+    """Eg. 3: -59/128 and grad (19/64, 19/64, 33/64, 33/64); Eg. 8 weighted gradient."""
+    for prec in (32, 64):
+        ctx = P.Context.from_file(golden("eg2_eg3_card4_ge2.hnf"), precision=prec, device=0)
+        f, g, _ = ctx.eval(np.array([[0.5, 0.5, -0.5, -0.5]], ctx.dtype))
+        assert abs(f[0] + 59 / 128) < TOL[prec]
+        assert np.max(np.abs(g[0] - np.array([19, 19, 33, 33]) / 64)) < TOL[prec]
+    ctx = P.Context.from_file(golden("eg8_local.hnf"), device=0)
+    ctx.set_weights(np.array([0.6, 1.0, 0.6]))
+    _, g, _ = ctx.eval(np.array([[1, -1, -1, 1]], np.float32))
+    assert np.max(np.abs(g[0] - np.array([-0.6, -0.4, -0.4, -0.6]))) < 1e-6
+    assert np.allclose(ctx.get_weights(), [0.6, 1.0, 0.6])
+
+
+# ------------------------------------------------------------------ full-size configs (sampled)
+
+
+def test_c2_full_size_sampled():
+    """c2 at full size (7-SAT n=200, m=17000, B=1024, the bench launch configuration); the oracle
+    recomputes 12 sampled points."""
+    inst = synth.config2(0)
+    X = synth.points("U", 1024, inst.n, 1000)
+    ctx = P.Context.from_instance(inst, device=0)
+    f, g, u = ctx.eval(torch.from_numpy(X).cuda(), unsat=True)
+    f, g, u = f.cpu().numpy(), g.cpu().numpy(), u.cpu().numpy()
+    idx = np.array([0, 1, 31, 32, 33, 500, 511, 512, 767, 1000, 1022, 1023])
+    Fo = oracle_of(inst)
+    fo, go = cdp.evaluate(Fo, X[idx].astype(np.float64))
+    uo, _ = cdp.check(Fo, X[idx].astype(np.float64))
+    assert np.max(np.abs(f[idx] - fo) / np.maximum(1, np.abs(fo))) <= 1e-4
+    assert np.max(np.abs(g[idx] - go) / np.maximum(1, np.abs(go))) <= 1e-4
+    assert np.array_equal(u[idx], uo)
+
+
+def test_c3_full_size_sampled():
+    """c3 at full size (n=4096, 8192 clauses, 32 at-most-b of length 500..2000, fp64, B=32)."""
+    inst = synth.config3(0)
+    X = synth.points("U", 32, inst.n, 1000, np.float64)
+    ctx = P.Context.from_instance(inst, device=0)
+    assert ctx.info["precision"] == 64
+    f, g, u = ctx.eval(torch.from_numpy(X).cuda(), unsat=True)
+    f, g, u = f.cpu().numpy(), g.cpu().numpy(), u.cpu().numpy()
+    idx = np.array([0, 17, 31])
+    Fo = oracle_of(inst)
+    fo, go = cdp.evaluate(Fo, X[idx])
+    uo, _ = cdp.check(Fo, X[idx])
+    assert np.max(np.abs(f[idx] - fo) / np.maximum(1, np.abs(fo))) <= 1e-9
+    assert np.max(np.abs(g[idx] - go) / np.maximum(1, np.abs(go))) <= 1e-9
+    assert np.array_equal(u[idx], uo)
+
+
+def test_c5_full_size_sampled():
+    """c5 at full size (3-SAT n=10^6, m=4.2*10^6, B=32, global path); oracle on 2 sampled points."""
+    inst = synth.config5(0)
+    X = synth.points("U", 32, inst.n, 1000)
+    ctx = P.Context.from_instance(inst, device=0)
+    assert ctx.info["path"] == 2
+    f, g, u = ctx.eval(torch.from_numpy(X).cuda(), unsat=True)
+    idx = np.array([0, 31])
+    f, u = f.cpu().numpy()[idx], u.cpu().numpy()[idx]
+    g = g[torch.from_numpy(idx).cuda()].cpu().numpy()
+    Fo = oracle_of(inst)
+    fo, go = cdp.evaluate(Fo, X[idx].astype(np.float64))
+    uo, _ = cdp.check(Fo, X[idx].astype(np.float64))
+    assert np.max(np.abs(f - fo) / np.maximum(1, np.abs(fo))) <= 1e-4
+    assert np.max(np.abs(g - go) / np.maximum(1, np.abs(go))) <= 1e-4
+    assert np.array_equal(u, uo)
+
+
+# ------------------------------------------------------------------ solve-loop parity (per step)
+
+
+def test_initial_points_and_rephase_match_oracle_philox():
+    inst = synth.config1(0)
+    ctx = P.Context.from_instance(inst, device=0)
+    s = ctx.search(48, seed=77, point0=5)
+    x0 = s.tensors()["x"].cpu().numpy().astype(np.float64)
+    want = osolve.initial_points(77, range(5, 53), inst.n)
+    assert np.array_equal(x0, want)
+    s.begin_round()
+    s.check()
+    s.restart()
+    torch.cuda.synchronize()
+    x1 = s.tensors()["x"].cpu().numpy().astype(np.float64)
+    want1 = osolve.rephase(x0, 77, 5, 1, osolve.Params())
+    assert np.array_equal(x1, want1)
+
+
+@pytest.mark.parametrize("precision", [32, 64])
+def test_pgd_steps_match_oracle(precision):
+    """Per-step parity: from the same x, each PGD iteration gives the same accept decision, eta and
+    x' (within tolerance); trajectories are compared only while decisions agree."""
+    inst = synth.config1(3)
+    ctx = P.Context.from_instance(inst, precision=precision, device=0)
+    B = 16
+    s = ctx.search(B, seed=9, max_inner=500)
+    Fo = oracle_of(inst)
+    Pp = osolve.Params(max_inner=500)
+    x0 = s.tensors()["x"].cpu().numpy().astype(np.float64)
+    st = osolve.State(x=x0.copy(), f=None, g=None, eta=None, done=None, iters=None, w=np.ones(Fo.m))
+    osolve.start_round(Fo, st, Pp)
+    s.begin_round()
+    tol = TOL[precision]
+    for it in range(6):
+        s.iterate(1)
+        torch.cuda.synchronize()
+        osolve.pgd_iteration(Fo, st, Pp)
+        T = s.tensors()
+        x = T["x"].cpu().numpy()
+        eta = T["eta"].cpu().numpy()
+        f = T["f"].cpu().numpy()
+        assert np.array_equal(eta, st.eta), f"eta differs at iteration {it}"
+        assert np.max(np.abs(x - st.x)) <= 10 * tol
+        assert np.max(np.abs(f - st.f) / np.maximum(1, np.abs(st.f))) <= tol
+
+
+def test_check_U_and_erwa_match_oracle():
+    inst = synth.config2(1)
+    ctx = P.Context.from_instance(inst, device=0)
+    s = ctx.search(64, seed=3)
+    s.check()
+    torch.cuda.synchronize()
+    T = s.tensors()
+    x = T["x"].cpu().numpy().astype(np.float64)
+    Fo = oracle_of(inst)
+    cnt, _, U = cdp.check(Fo, x, want_U=True)
+    assert np.array_equal(T["unsat"].cpu().numpy(), cnt)
+    # device U is in the library's internal constraint order; compare as multisets and via ERWA
+    assert np.array_equal(np.sort(T["U"].cpu().numpy()), np.sort(U))
+    s.restart()
+    torch.cuda.synchronize()
+    w_dev = ctx.get_weights()
+    w_or = osolve.erwa_update(np.ones(Fo.m), U, 0.4)
+    assert np.max(np.abs(w_dev - w_or)) < 1e-6
+
+
+def test_solve_small_formulas():
+    ctx = P.Context.from_file(golden("eg7_saddle.hnf"), device=0)
+    r, a = ctx.solve(batch=8, max_restarts=5, seed=1, max_inner=50)
+    assert r["sat"] == 1 and ctx.check(a)[0] == 0
+    Fo = OracleFormula.from_constraints(1, [(0, 0, 1.0, [1]), (0, 0, 1.0, [-1])])
+    ctx = P.Context.from_arrays(1, Fo.kind, Fo.bound, Fo.weight, Fo.offsets, Fo.lits, device=0)
+    r, a = ctx.solve(batch=8, max_restarts=3, seed=1, max_inner=30)
+    assert r["sat"] == 0 and r["best_unsat"] == 1
+    for seed in range(3):
+        inst = synth.config1(seed)
+        ctx = P.Context.from_instance(inst, device=0)
+        r, a = ctx.solve(batch=256, max_restarts=20, seed=seed, max_inner=100)
+        if r["sat"]:
+            assert ctx.check(a)[0] == 0
+            assert cdp.check(oracle_of(inst), np.where(a < 0, -1.0, 1.0)[None])[0][0] == 0
+
+
+def test_solve_planted_hybrid():
+    inst = synth.config4_hybrid(1, n=200, m3=400, n_xor=20, kmax=8)
+    ctx = P.Context.from_instance(inst, device=0)
+    r, a = ctx.solve(batch=512, max_restarts=30, seed=2, max_inner=200)
+    if r["sat"]:
+        assert ctx.check(a)[0] == 0
+    assert r["best_unsat"] >= 0
