@@ -301,9 +301,9 @@ template <typename T>
 void eval_device_t(ffsat_ctx* c, const T* x, int64_t B, double* f, T* grad, int32_t* unsat, const T* w_pos, cudaStream_t st,
                    bool profiled = false) {
     const Layout& L = c->Lo;
+    if (B == 0) return;
     plan(c, B);
     const int64_t PT = (B + 31) / 32;
-    if (B == 0) return;
     auto mark = [&](int i) {
         if (profiled) CK(cudaEventRecord(c->ev[i], st));
     };

@@ -224,7 +224,8 @@ int tiled_stage_rows(int precision) { return precision == 64 ? 256 : 512; }
 
 size_t tiled_smem_bytes(int n, int precision, int stage_rows) {
     size_t es = precision == 64 ? 8 : 4;
-    return (size_t)32 * es * (2 * (size_t)n + (size_t)stage_rows) + 64 * 8;
+    // x tile and gradient tile [n][33] (padded rows), staging rows [stage_rows][32]
+    return es * (33 * 2 * (size_t)n + 32 * (size_t)stage_rows) + 64;
 }
 
 int tiled_max_n(int precision) {
