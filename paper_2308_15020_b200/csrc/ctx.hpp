@@ -1,0 +1,96 @@
+// ctx.hpp -- internal state of libffsat shared by its translation units (not part of the ABI).
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "../../include/ffsat.h"
+#include "host.hpp"
+
+namespace ffsat {
+
+#define CK(call)                                                                                     \
+    do {                                                                                             \
+        cudaError_t e_ = (call);                                                                     \
+        if (e_ != cudaSuccess)                                                                       \
+            throw ::ffsat::Error(e_ == cudaErrorMemoryAllocation ? FFSAT_ERR_OOM : FFSAT_ERR_CUDA,   \
+                                 std::string(#call) + ": " + cudaGetErrorString(e_));                \
+    } while (0)
+
+struct DBuf {
+    void* p = nullptr;
+    size_t bytes = 0;
+    DBuf() = default;
+    DBuf(const DBuf&) = delete;
+    DBuf& operator=(const DBuf&) = delete;
+    ~DBuf() {
+        if (p) cudaFree(p);
+    }
+    void ensure(size_t b) {
+        if (b <= bytes && p) return;
+        if (p) cudaFree(p);
+        p = nullptr;
+        bytes = 0;
+        if (b == 0) return;
+        cudaError_t e = cudaMalloc(&p, b);
+        if (e != cudaSuccess) {
+            p = nullptr;
+            cudaGetLastError();
+            throw Error(FFSAT_ERR_OOM, "cudaMalloc(" + std::to_string(b) + "): " + cudaGetErrorString(e));
+        }
+        bytes = b;
+    }
+    template <class U>
+    U* as() const { return reinterpret_cast<U*>(p); }
+};
+
+template <class V>
+void upload(DBuf& d, const std::vector<V>& h) {
+    d.ensure(std::max<size_t>(h.size() * sizeof(V), 16));
+    if (!h.empty()) CK(cudaMemcpy(d.p, h.data(), h.size() * sizeof(V), cudaMemcpyHostToDevice));
+}
+
+inline unsigned blocks_for(int64_t n, int t) { return (unsigned)((n + t - 1) / t); }
+
+}  // namespace ffsat
+
+struct ffsat_ctx {
+    ffsat::Formula F;
+    ffsat::Layout Lo;
+    int device = -1;
+    int num_sm = 148;
+    size_t esize = 4;
+    std::string err;
+    // persistent device layout
+    ffsat::DBuf fast_words, tiled_words, units, buckets, sym_words, sym_off, sym_sig, sigs, coef, occ_off, occ_slot,
+        w_pos, w_static_orig, order, chk_off, chk_words, chk_rule;
+    int64_t persistent_bytes = 0;
+    // per-B scratch
+    ffsat::DBuf xT, Tb, P, fpart, upart, fsym, usym, chunk_units, x_stage, g_stage, f_stage, u_stage, w_stage;
+    int64_t plan_B = -1;
+    int32_t n_chunks = 0;
+    size_t tiled_smem = 0;
+    int64_t launches = 0;
+    cudaEvent_t ev[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
+    ~ffsat_ctx() {
+        for (cudaEvent_t& e : ev)
+            if (e) cudaEventDestroy(e);
+    }
+};
+
+namespace ffsat {
+
+// Size the per-batch scratch and the chunk split of the fast kernels for batch B (eval.cu).
+void plan(ffsat_ctx* c, int64_t B);
+// f (fp64), grad (T, may be null), unsat (int32, may be null) at device points x [B][n]; async on st
+// (eval_f32.cu / eval_f64.cu).  profiled: record c->ev[0..4] around the phases.
+template <typename T>
+void eval_device_t(ffsat_ctx* c, const T* x, int64_t B, double* f, T* grad, int32_t* unsat, const T* w_pos, cudaStream_t st,
+                   bool profiled);
+// allow the tiled kernels of dtype T the dynamic shared memory they need (eval_f32.cu / eval_f64.cu)
+template <typename T>
+void set_tiled_smem(size_t bytes);
+
+}  // namespace ffsat

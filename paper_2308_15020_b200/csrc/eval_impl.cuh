@@ -1,0 +1,112 @@
+// eval_impl.cuh -- launch orchestration of ffsat_eval (steps A4-A7), instantiated per dtype by
+// eval_f32.cu and eval_f64.cu so the two dtypes compile in parallel.
+#pragma once
+#include <algorithm>
+
+#include "ctx.hpp"
+#include "kernels_eval.cuh"
+
+namespace ffsat {
+
+inline int fast_kmax(const Layout& L) {
+    int km = 0;
+    for (const FastBucket& b : L.fbuckets) km = std::max(km, b.k);
+    return km;
+}
+
+template <typename T>
+void launch_sym_class(ffsat_ctx* c, const SymClass& cl, const dev::SymArgs<T>& a, cudaStream_t st) {
+    const int64_t groups = (cl.end - cl.begin) * a.B;
+    switch (cl.G) {
+    case 32: dev::sym_kernel<T, 32><<<blocks_for(groups, 8), 256, 0, st>>>(a, cl.begin, cl.end); break;
+    case 64: dev::sym_kernel<T, 64><<<(unsigned)groups, 64, 0, st>>>(a, cl.begin, cl.end); break;
+    case 128: dev::sym_kernel<T, 128><<<(unsigned)groups, 128, 0, st>>>(a, cl.begin, cl.end); break;
+    case 256: dev::sym_kernel<T, 256><<<(unsigned)groups, 256, 0, st>>>(a, cl.begin, cl.end); break;
+    case 512: dev::sym_kernel<T, 512><<<(unsigned)groups, 512, 0, st>>>(a, cl.begin, cl.end); break;
+    default: throw Error(FFSAT_ERR_ARG, "unsupported group size");
+    }
+}
+
+// f (fp64), grad (T, may be null), unsat (int32, may be null) at device points x [B][n]; async on st.
+template <typename T>
+void eval_device_t(ffsat_ctx* c, const T* x, int64_t B, double* f, T* grad, int32_t* unsat, const T* w_pos, cudaStream_t st,
+                   bool profiled) {
+    const Layout& L = c->Lo;
+    if (B == 0) return;
+    plan(c, B);
+    const int64_t PT = (B + 31) / 32;
+    auto mark = [&](int i) {
+        if (profiled) CK(cudaEventRecord(c->ev[i], st));
+    };
+    mark(0);
+    if (L.n_fast > 0 && c->n_chunks > 0) {
+        c->launches += L.path == 1 ? 1 : 2;
+        if (L.path == 1) {
+            dev::TiledArgs<T> a{};
+            a.x = x; a.B = B; a.n = L.n;
+            a.words = c->tiled_words.as<uint32_t>(); a.units = c->units.as<dev::UnitDev>();
+            a.buckets = c->buckets.as<dev::FastBucketDev>(); a.chunk_units = c->chunk_units.as<int32_t>(); a.w_pos = w_pos;
+            a.P = c->P.as<T>(); a.fpart = c->fpart.as<double>(); a.upart = c->upart.as<int32_t>();
+            dim3 grid((unsigned)PT, (unsigned)c->n_chunks);
+            const int km = fast_kmax(L);
+            if (km <= 4) dev::fast_tiled_kernel<T, 4><<<grid, 256, c->tiled_smem, st>>>(a);
+            else if (km <= 8) dev::fast_tiled_kernel<T, 8><<<grid, 256, c->tiled_smem, st>>>(a);
+            else if (km <= 16) dev::fast_tiled_kernel<T, 16><<<grid, 256, c->tiled_smem, st>>>(a);
+            else dev::fast_tiled_kernel<T, 64><<<grid, 256, c->tiled_smem, st>>>(a);
+        } else {
+            dim3 tg(blocks_for(L.n, 32), blocks_for(B, 32)), tb(32, 8);
+            dev::transpose_kernel<T><<<tg, tb, 0, st>>>(x, c->xT.as<T>(), B, L.n);
+            dev::GlobalArgs<T> a{};
+            a.xT = c->xT.as<T>(); a.B = B; a.n = L.n; a.words = c->fast_words.as<uint32_t>();
+            a.units = c->units.as<dev::UnitDev>(); a.buckets = c->buckets.as<dev::FastBucketDev>();
+            a.chunk_units = c->chunk_units.as<int32_t>(); a.w_pos = w_pos; a.Tb = c->Tb.as<T>();
+            a.fpart = c->fpart.as<double>(); a.upart = c->upart.as<int32_t>();
+            dim3 grid((unsigned)PT, (unsigned)c->n_chunks);
+            const int km = fast_kmax(L);
+            if (km <= 4) dev::fast_global_kernel<T, 4><<<grid, 256, 0, st>>>(a);
+            else if (km <= 8) dev::fast_global_kernel<T, 8><<<grid, 256, 0, st>>>(a);
+            else if (km <= 16) dev::fast_global_kernel<T, 16><<<grid, 256, 0, st>>>(a);
+            else dev::fast_global_kernel<T, 64><<<grid, 256, 0, st>>>(a);
+        }
+        CK(cudaGetLastError());
+    }
+    mark(1);
+    if (L.n_sym > 0) {
+        c->launches += (int64_t)L.sym_classes.size();
+        dev::SymArgs<T> a{};
+        a.x = x; a.sb = L.n; a.sv = 1; a.B = B;
+        a.words = c->sym_words.as<uint32_t>(); a.off = c->sym_off.as<int64_t>(); a.sig_of = c->sym_sig.as<int32_t>();
+        a.sigs = c->sigs.as<dev::SymSigDev>(); a.coef = c->coef.as<T>(); a.w_sym = w_pos + L.n_fast;
+        a.tb_fast = L.tb_fast; a.Tb = c->Tb.as<T>(); a.fsym = c->fsym.as<double>(); a.usym = c->usym.as<int32_t>();
+        for (const SymClass& cl : L.sym_classes) launch_sym_class<T>(c, cl, a, st);
+        CK(cudaGetLastError());
+    }
+    mark(2);
+    if (grad) {
+        c->launches += 1;
+        dev::ReduceArgs<T> r{};
+        r.B = B; r.n = L.n; r.n_chunks = L.path == 1 ? c->n_chunks : 0; r.P = c->P.as<T>(); r.Tb = c->Tb.as<T>();
+        r.occ_off = c->occ_off.as<int64_t>(); r.occ_slot = c->occ_slot.as<int32_t>(); r.grad = grad;
+        dim3 grid(blocks_for(B, 32), blocks_for(L.n, 32)), blk(32, 8);
+        dev::reduce_grad_kernel<T><<<grid, blk, 0, st>>>(r);
+    }
+    mark(3);
+    c->launches += 1;
+    dev::ReduceFArgs rf{};
+    rf.B = B; rf.n_parts = L.n_fast > 0 ? c->n_chunks : 0; rf.n_sym = L.n_sym;
+    rf.fpart = c->fpart.as<double>(); rf.upart = c->upart.as<int32_t>(); rf.fsym = c->fsym.as<double>();
+    rf.usym = c->usym.as<int32_t>(); rf.f = f; rf.unsat = unsat;
+    dev::reduce_f_kernel<<<(unsigned)B, 128, 0, st>>>(rf);
+    CK(cudaGetLastError());
+    mark(4);
+}
+
+
+template <typename T>
+void set_tiled_smem(size_t bytes) {
+    const void* kerns[4] = {(const void*)dev::fast_tiled_kernel<T, 4>, (const void*)dev::fast_tiled_kernel<T, 8>,
+                            (const void*)dev::fast_tiled_kernel<T, 16>, (const void*)dev::fast_tiled_kernel<T, 64>};
+    for (const void* k : kerns) CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+}
+
+}  // namespace ffsat

@@ -16,7 +16,7 @@
 
 #include "../../include/ffsat.h"
 #include "host.hpp"
-#include "kernels_eval.cuh"
+#include "ctx.hpp"
 #include "kernels_solve.cuh"
 
 using namespace ffsat;
@@ -24,77 +24,10 @@ using namespace ffsat;
 namespace {
 
 thread_local std::string g_err;
-const int kNumSM_default = 148;
-
-#define CK(call)                                                                                     \
-    do {                                                                                             \
-        cudaError_t e_ = (call);                                                                     \
-        if (e_ != cudaSuccess)                                                                       \
-            throw Error(e_ == cudaErrorMemoryAllocation ? FFSAT_ERR_OOM : FFSAT_ERR_CUDA,            \
-                        std::string(#call) + ": " + cudaGetErrorString(e_));                         \
-    } while (0)
-
-struct DBuf {
-    void* p = nullptr;
-    size_t bytes = 0;
-    DBuf() = default;
-    DBuf(const DBuf&) = delete;
-    DBuf& operator=(const DBuf&) = delete;
-    ~DBuf() {
-        if (p) cudaFree(p);
-    }
-    void ensure(size_t b) {
-        if (b <= bytes && p) return;
-        if (p) cudaFree(p);
-        p = nullptr;
-        bytes = 0;
-        if (b == 0) return;
-        cudaError_t e = cudaMalloc(&p, b);
-        if (e != cudaSuccess) {
-            p = nullptr;
-            cudaGetLastError();
-            throw Error(FFSAT_ERR_OOM, "cudaMalloc(" + std::to_string(b) + "): " + cudaGetErrorString(e));
-        }
-        bytes = b;
-    }
-    template <class U>
-    U* as() const { return reinterpret_cast<U*>(p); }
-};
-
-template <class V>
-void upload(DBuf& d, const std::vector<V>& h) {
-    d.ensure(std::max<size_t>(h.size() * sizeof(V), 16));
-    if (!h.empty()) CK(cudaMemcpy(d.p, h.data(), h.size() * sizeof(V), cudaMemcpyHostToDevice));
-}
 
 inline cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
-inline unsigned blocks_for(int64_t n, int t) { return (unsigned)((n + t - 1) / t); }
 
 }  // namespace
-
-struct ffsat_ctx {
-    Formula F;
-    Layout Lo;
-    int device = -1;
-    int num_sm = kNumSM_default;
-    size_t esize = 4;
-    std::string err;
-    // persistent device layout
-    DBuf fast_words, tiled_words, units, segs, buckets, sym_words, sym_off, sym_sig, sigs, coef, occ_off, occ_slot,
-        w_pos, w_static_orig, order, chk_off, chk_words, chk_rule;
-    int64_t persistent_bytes = 0;
-    // per-B scratch
-    DBuf xT, Tb, P, fpart, upart, fsym, usym, chunk_units, x_stage, g_stage, f_stage, u_stage, w_stage;
-    int64_t plan_B = -1;
-    int32_t n_chunks = 0;
-    size_t tiled_smem = 0;
-    int64_t launches = 0;
-    cudaEvent_t ev[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
-    ~ffsat_ctx() {
-        for (cudaEvent_t& e : ev)
-            if (e) cudaEventDestroy(e);
-    }
-};
 
 struct ffsat_search {
     ffsat_ctx* ctx = nullptr;
@@ -116,9 +49,11 @@ void upload_layout(ffsat_ctx* c) {
     upload(c->fast_words, L.fast_words);
     if (L.path == 1) upload(c->tiled_words, L.tiled_words);
     std::vector<dev::UnitDev> units;
-    for (const SubChunk& s : L.subchunks) units.push_back({s.bucket, s.seg_begin, s.seg_end, s.rows, s.pos_begin, s.pos_end});
+    for (const WorkUnit& u : L.units) {
+        const FastBucket& b = L.fbuckets[(size_t)u.bucket];
+        units.push_back({u.bucket, u.count, b.kp, 0, u.pos_begin, b.word_off + (u.pos_begin - b.pos_begin) * b.kp});
+    }
     upload(c->units, units);
-    upload(c->segs, L.segs);
     std::vector<dev::FastBucketDev> bks;
     for (const FastBucket& b : L.fbuckets) {
         dev::FastBucketDev d{};
@@ -174,7 +109,7 @@ void upload_layout(ffsat_ctx* c) {
     upload(c->chk_off, off);
     upload(c->chk_words, words);
     upload(c->chk_rule, rule);
-    for (DBuf* d : {&c->fast_words, &c->tiled_words, &c->units, &c->segs, &c->buckets, &c->sym_words, &c->sym_off,
+    for (DBuf* d : {&c->fast_words, &c->tiled_words, &c->units, &c->buckets, &c->sym_words, &c->sym_off,
                     &c->sym_sig, &c->sigs, &c->coef, &c->occ_off, &c->occ_slot, &c->w_pos, &c->w_static_orig, &c->order,
                     &c->chk_off, &c->chk_words, &c->chk_rule})
         c->persistent_bytes += (int64_t)d->bytes;
@@ -210,165 +145,6 @@ void need_device(const ffsat_ctx* c) {
 }
 
 // ------------------------------------------------------------------------------------------------ eval
-
-// Pick the number of clause chunks so (point tiles x chunks) fills whole waves of CTAs.
-int pick_chunks(int64_t point_tiles, int ctas_per_sm, int num_sm, int64_t n_units) {
-    if (n_units <= 0) return 0;
-    const int64_t slots = (int64_t)num_sm * std::max(1, ctas_per_sm);
-    int best = 1;
-    double best_eff = -1;
-    for (int w = 1; w <= 4; ++w) {
-        int64_t nc = std::max<int64_t>(1, (w * slots) / point_tiles);
-        nc = std::min<int64_t>(nc, n_units);
-        int64_t ctas = nc * point_tiles;
-        int64_t waves = (ctas + slots - 1) / slots;
-        double eff = (double)ctas / (double)(waves * slots);
-        if (eff > best_eff + 0.05) {
-            best_eff = eff;
-            best = (int)nc;
-        }
-        if (eff >= 0.9) break;
-    }
-    return best;
-}
-
-void plan(ffsat_ctx* c, int64_t B) {
-    if (c->plan_B == B) return;
-    const Layout& L = c->Lo;
-    const size_t es = c->esize;
-    const int64_t PT = (B + 31) / 32;
-    int cps = 8;
-    if (L.path == 1) {
-        c->tiled_smem = tiled_smem_bytes(L.n, L.precision, L.stage_rows);
-        cps = std::max(1, (int)std::min<size_t>(8, (228 * 1024) / (c->tiled_smem + 1024)));
-    }
-    const int64_t n_units = (int64_t)L.subchunks.size();
-    c->n_chunks = L.n_fast > 0 ? pick_chunks(PT, cps, c->num_sm, n_units) : 0;
-    // balanced contiguous unit ranges by literal rows
-    std::vector<int32_t> cu((size_t)c->n_chunks + 1, 0);
-    if (c->n_chunks > 0) {
-        int64_t total = 0;
-        for (const SubChunk& s : L.subchunks) total += s.rows;
-        int64_t acc = 0;
-        int j = 1;
-        for (int64_t u = 0; u < n_units && j < c->n_chunks; ++u) {
-            acc += L.subchunks[u].rows;
-            while (j < c->n_chunks && acc * c->n_chunks >= total * j) cu[j++] = (int32_t)(u + 1);
-        }
-        for (; j <= c->n_chunks; ++j) cu[j] = (int32_t)n_units;
-        cu[c->n_chunks] = (int32_t)n_units;
-    }
-    upload(c->chunk_units, cu);
-    const int64_t parts = std::max<int64_t>(1, c->n_chunks);
-    if (L.path == 1) c->P.ensure(std::max<size_t>(16, (size_t)c->n_chunks * L.n * B * es));
-    if (L.path == 2) c->xT.ensure(std::max<size_t>(16, (size_t)L.n * B * es));
-    c->Tb.ensure(std::max<size_t>(16, (size_t)L.tb_slots * B * es));
-    c->fpart.ensure((size_t)parts * B * 8);
-    c->upart.ensure((size_t)parts * B * 4);
-    c->fsym.ensure(std::max<size_t>(16, (size_t)L.n_sym * B * 8));
-    c->usym.ensure(std::max<size_t>(16, (size_t)L.n_sym * B * 4));
-    if (L.path == 1) {
-        const void* kerns[8] = {(const void*)dev::fast_tiled_kernel<float, 4>, (const void*)dev::fast_tiled_kernel<float, 8>,
-                                (const void*)dev::fast_tiled_kernel<float, 16>, (const void*)dev::fast_tiled_kernel<float, 64>,
-                                (const void*)dev::fast_tiled_kernel<double, 4>, (const void*)dev::fast_tiled_kernel<double, 8>,
-                                (const void*)dev::fast_tiled_kernel<double, 16>, (const void*)dev::fast_tiled_kernel<double, 64>};
-        for (const void* k : kerns) CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->tiled_smem));
-    }
-    c->plan_B = B;
-}
-
-int fast_kmax(const Layout& L) {
-    int km = 0;
-    for (const FastBucket& b : L.fbuckets) km = std::max(km, b.k);
-    return km;
-}
-
-template <typename T>
-void launch_sym_class(ffsat_ctx* c, const SymClass& cl, const dev::SymArgs<T>& a, cudaStream_t st) {
-    const int64_t groups = (cl.end - cl.begin) * a.B;
-    switch (cl.G) {
-    case 32: dev::sym_kernel<T, 32><<<blocks_for(groups, 8), 256, 0, st>>>(a, cl.begin, cl.end); break;
-    case 64: dev::sym_kernel<T, 64><<<(unsigned)groups, 64, 0, st>>>(a, cl.begin, cl.end); break;
-    case 128: dev::sym_kernel<T, 128><<<(unsigned)groups, 128, 0, st>>>(a, cl.begin, cl.end); break;
-    case 256: dev::sym_kernel<T, 256><<<(unsigned)groups, 256, 0, st>>>(a, cl.begin, cl.end); break;
-    case 512: dev::sym_kernel<T, 512><<<(unsigned)groups, 512, 0, st>>>(a, cl.begin, cl.end); break;
-    default: throw Error(FFSAT_ERR_ARG, "unsupported group size");
-    }
-}
-
-// f (fp64), grad (T, may be null), unsat (int32, may be null) at device points x [B][n]; async on st.
-template <typename T>
-void eval_device_t(ffsat_ctx* c, const T* x, int64_t B, double* f, T* grad, int32_t* unsat, const T* w_pos, cudaStream_t st,
-                   bool profiled = false) {
-    const Layout& L = c->Lo;
-    if (B == 0) return;
-    plan(c, B);
-    const int64_t PT = (B + 31) / 32;
-    auto mark = [&](int i) {
-        if (profiled) CK(cudaEventRecord(c->ev[i], st));
-    };
-    mark(0);
-    if (L.n_fast > 0 && c->n_chunks > 0) {
-        c->launches += L.path == 1 ? 1 : 2;
-        if (L.path == 1) {
-            dev::TiledArgs<T> a{};
-            a.x = x; a.B = B; a.n = L.n; a.stage_rows = L.stage_rows;
-            a.words = c->tiled_words.as<uint32_t>(); a.units = c->units.as<dev::UnitDev>(); a.segs = c->segs.as<uint2>();
-            a.buckets = c->buckets.as<dev::FastBucketDev>(); a.chunk_units = c->chunk_units.as<int32_t>(); a.w_pos = w_pos;
-            a.P = c->P.as<T>(); a.fpart = c->fpart.as<double>(); a.upart = c->upart.as<int32_t>();
-            dim3 grid((unsigned)PT, (unsigned)c->n_chunks);
-            const int km = fast_kmax(L);
-            if (km <= 4) dev::fast_tiled_kernel<T, 4><<<grid, 256, c->tiled_smem, st>>>(a);
-            else if (km <= 8) dev::fast_tiled_kernel<T, 8><<<grid, 256, c->tiled_smem, st>>>(a);
-            else if (km <= 16) dev::fast_tiled_kernel<T, 16><<<grid, 256, c->tiled_smem, st>>>(a);
-            else dev::fast_tiled_kernel<T, 64><<<grid, 256, c->tiled_smem, st>>>(a);
-        } else {
-            dim3 tg(blocks_for(L.n, 32), blocks_for(B, 32)), tb(32, 8);
-            dev::transpose_kernel<T><<<tg, tb, 0, st>>>(x, c->xT.as<T>(), B, L.n);
-            dev::GlobalArgs<T> a{};
-            a.xT = c->xT.as<T>(); a.B = B; a.n = L.n; a.words = c->fast_words.as<uint32_t>();
-            a.units = c->units.as<dev::UnitDev>(); a.buckets = c->buckets.as<dev::FastBucketDev>();
-            a.chunk_units = c->chunk_units.as<int32_t>(); a.w_pos = w_pos; a.Tb = c->Tb.as<T>();
-            a.fpart = c->fpart.as<double>(); a.upart = c->upart.as<int32_t>();
-            dim3 grid((unsigned)PT, (unsigned)c->n_chunks);
-            const int km = fast_kmax(L);
-            if (km <= 4) dev::fast_global_kernel<T, 4><<<grid, 256, 0, st>>>(a);
-            else if (km <= 8) dev::fast_global_kernel<T, 8><<<grid, 256, 0, st>>>(a);
-            else if (km <= 16) dev::fast_global_kernel<T, 16><<<grid, 256, 0, st>>>(a);
-            else dev::fast_global_kernel<T, 64><<<grid, 256, 0, st>>>(a);
-        }
-        CK(cudaGetLastError());
-    }
-    mark(1);
-    if (L.n_sym > 0) {
-        c->launches += (int64_t)L.sym_classes.size();
-        dev::SymArgs<T> a{};
-        a.x = x; a.sb = L.n; a.sv = 1; a.B = B;
-        a.words = c->sym_words.as<uint32_t>(); a.off = c->sym_off.as<int64_t>(); a.sig_of = c->sym_sig.as<int32_t>();
-        a.sigs = c->sigs.as<dev::SymSigDev>(); a.coef = c->coef.as<T>(); a.w_sym = w_pos + L.n_fast;
-        a.tb_fast = L.tb_fast; a.Tb = c->Tb.as<T>(); a.fsym = c->fsym.as<double>(); a.usym = c->usym.as<int32_t>();
-        for (const SymClass& cl : L.sym_classes) launch_sym_class<T>(c, cl, a, st);
-        CK(cudaGetLastError());
-    }
-    mark(2);
-    if (grad) {
-        c->launches += 1;
-        dev::ReduceArgs<T> r{};
-        r.B = B; r.n = L.n; r.n_chunks = L.path == 1 ? c->n_chunks : 0; r.P = c->P.as<T>(); r.Tb = c->Tb.as<T>();
-        r.occ_off = c->occ_off.as<int64_t>(); r.occ_slot = c->occ_slot.as<int32_t>(); r.grad = grad;
-        dim3 grid(blocks_for(B, 32), blocks_for(L.n, 32)), blk(32, 8);
-        dev::reduce_grad_kernel<T><<<grid, blk, 0, st>>>(r);
-    }
-    mark(3);
-    c->launches += 1;
-    dev::ReduceFArgs rf{};
-    rf.B = B; rf.n_parts = L.n_fast > 0 ? c->n_chunks : 0; rf.n_sym = L.n_sym;
-    rf.fpart = c->fpart.as<double>(); rf.upart = c->upart.as<int32_t>(); rf.fsym = c->fsym.as<double>();
-    rf.usym = c->usym.as<int32_t>(); rf.f = f; rf.unsat = unsat;
-    dev::reduce_f_kernel<<<blocks_for(B, 256), 256, 0, st>>>(rf);
-    CK(cudaGetLastError());
-    mark(4);
-}
 
 void eval_device(ffsat_ctx* c, const void* x, int64_t B, double* f, void* grad, int32_t* unsat, cudaStream_t st,
                  bool profiled = false) {
@@ -423,7 +199,7 @@ int64_t exact_unsat(const Formula& F, const int8_t* a, double* fw) {
 
 template <typename T>
 void search_eval(ffsat_search* s, const void* x, double* f, void* g, int32_t* u, cudaStream_t st) {
-    eval_device_t<T>(s->ctx, (const T*)x, s->B, f, (T*)g, u, s->ctx->w_pos.as<T>(), st);
+    eval_device_t<T>(s->ctx, (const T*)x, s->B, f, (T*)g, u, s->ctx->w_pos.as<T>(), st, false);
 }
 
 void search_alloc(ffsat_search* s) {

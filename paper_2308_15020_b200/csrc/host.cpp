@@ -220,20 +220,49 @@ static void sym_coefficients(int k, SatRule r, std::vector<double>& coef, double
 
 // ------------------------------------------------------------------------------- tiled sizing
 
-int tiled_stage_rows(int precision) { return precision == 64 ? 256 : 512; }
-
-size_t tiled_smem_bytes(int n, int precision, int stage_rows) {
+size_t tiled_smem_bytes(int n, int precision) {
     size_t es = precision == 64 ? 8 : 4;
-    // x tile and gradient tile [n][33] (padded rows), staging rows [stage_rows][32]
-    return es * (33 * 2 * (size_t)n + 32 * (size_t)stage_rows) + 64;
+    // x tile and gradient tile [n][kTilePitch]; at least 3 KB (the kernel's final f / unsat exchange)
+    return std::max<size_t>(es * 2 * (size_t)kTilePitch * (size_t)n, 3072);
 }
 
 int tiled_max_n(int precision) {
-    const size_t budget = 227 * 1024;
-    int rows = tiled_stage_rows(precision);
+    const size_t budget = 227 * 1024 - 4608;   // minus the kernel's static stage buffers
     int n = 0;
-    while (tiled_smem_bytes(n + 1, precision, rows) <= budget && n < 32767) ++n;
+    while (tiled_smem_bytes(n + 1, precision) <= budget) ++n;
     return n;
+}
+
+std::vector<int32_t> disjoint_classes(const std::vector<std::vector<int32_t>>& vars, int32_t n, int cap, int window) {
+    const size_t words = ((size_t)n + 63) / 64;
+    std::vector<std::vector<uint64_t>> mask;   // per class
+    std::vector<int32_t> fill;
+    std::vector<int32_t> open;                 // most recent open classes, oldest first
+    std::vector<int32_t> cls(vars.size());
+    for (size_t c = 0; c < vars.size(); ++c) {
+        int32_t got = -1;
+        for (size_t j = 0; j < open.size() && got < 0; ++j) {
+            const std::vector<uint64_t>& mk = mask[(size_t)open[j]];
+            bool ok = true;
+            for (int32_t v : vars[c])
+                if (mk[(size_t)v >> 6] >> (v & 63) & 1ull) { ok = false; break; }
+            if (ok) {
+                got = open[j];
+                if (fill[(size_t)got] + 1 >= cap) open.erase(open.begin() + (long)j);
+            }
+        }
+        if (got < 0) {
+            got = (int32_t)mask.size();
+            mask.emplace_back(words, 0ull);
+            fill.push_back(0);
+            if (cap > 1) open.push_back(got);
+            if ((int)open.size() > window) open.erase(open.begin());
+        }
+        for (int32_t v : vars[c]) mask[(size_t)got][(size_t)v >> 6] |= 1ull << (v & 63);
+        fill[(size_t)got] += 1;
+        cls[c] = got;
+    }
+    return cls;
 }
 
 // ------------------------------------------------------------------------------- A2: layout
@@ -281,6 +310,45 @@ Layout build_layout(const Formula& F, int path, int precision) {
         if (ga != gb) return ga < gb;
         return klen(a) > klen(b);
     });
+
+    // ---- path: tiled (x and gradient tiles in shared memory) when n fits, else global
+    if (path == 0) path = (!fast_ids.empty() && F.n <= tiled_max_n(precision)) ? 1 : 2;
+    if (path == 1 && F.n > tiled_max_n(precision)) throw Error(FFSAT_ERR_ARG, "tiled path needs n <= " + std::to_string(tiled_max_n(precision)));
+    if (path != 1 && path != 2) throw Error(FFSAT_ERR_ARG, "path must be 0, 1 or 2");
+    Lo.path = path;
+
+    // ---- tiled path: within each (k, variant) run, group constraints into var-disjoint classes and make
+    //      each class a contiguous position range (the kernel's warps add a class's terms concurrently)
+    std::vector<int32_t> fast_class;   // class id (global over runs) per fast position
+    if (path == 1) {
+        std::vector<int64_t> reordered;
+        reordered.reserve(fast_ids.size());
+        size_t r0 = 0;
+        int32_t class_base = 0;
+        while (r0 < fast_ids.size()) {
+            size_t r1 = r0;
+            const int k = klen(fast_ids[r0]);
+            while (r1 < fast_ids.size() && klen(fast_ids[r1]) == k && ff[fast_ids[r1]].variant == ff[fast_ids[r0]].variant) ++r1;
+            std::vector<std::vector<int32_t>> vars(r1 - r0);
+            for (size_t j = r0; j < r1; ++j)
+                for (int64_t i = F.offsets[fast_ids[j]]; i < F.offsets[fast_ids[j] + 1]; ++i)
+                    vars[j - r0].push_back((F.lits[i] > 0 ? F.lits[i] : -F.lits[i]) - 1);
+            const int cap = (int)std::max<int64_t>(1, std::min<int64_t>(kClassCap, (int64_t)(0.6 * F.n) / std::max(1, k)));
+            std::vector<int32_t> cls = disjoint_classes(vars, F.n, cap, 64);
+            int32_t ncls = 0;
+            for (int32_t c : cls) ncls = std::max(ncls, c + 1);
+            std::vector<std::vector<int64_t>> members((size_t)ncls);
+            for (size_t j = r0; j < r1; ++j) members[(size_t)cls[j - r0]].push_back(fast_ids[j]);
+            for (int32_t q = 0; q < ncls; ++q)
+                for (int64_t c : members[(size_t)q]) {
+                    reordered.push_back(c);
+                    fast_class.push_back(class_base + q);
+                }
+            class_base += ncls;
+            r0 = r1;
+        }
+        fast_ids.swap(reordered);
+    }
     Lo.order = fast_ids;
     Lo.order.insert(Lo.order.end(), sym_ids.begin(), sym_ids.end());
     Lo.pos_of.assign((size_t)m, 0);
@@ -354,12 +422,6 @@ Layout build_layout(const Formula& F, int path, int precision) {
         else Lo.sym_classes.back().end = s + 1;
     }
 
-    // ---- path
-    if (path == 0) path = (Lo.n_fast > 0 && F.n <= tiled_max_n(precision)) ? 1 : 2;
-    if (path == 1 && F.n > tiled_max_n(precision)) throw Error(FFSAT_ERR_ARG, "tiled path needs n <= " + std::to_string(tiled_max_n(precision)));
-    if (path != 1 && path != 2) throw Error(FFSAT_ERR_ARG, "path must be 0, 1 or 2");
-    Lo.path = path;
-
     // ---- T-buffer slots and occurrence CSR (ascending slot order per variable)
     Lo.tb_fast = path == 2 ? Lo.n_fast_lits : 0;
     Lo.tb_slots = Lo.tb_fast + Lo.n_sym_lits;
@@ -381,46 +443,26 @@ Layout build_layout(const Formula& F, int path, int precision) {
         for (int64_t s = 0; s < Lo.tb_slots; ++s) Lo.occ_slot[(size_t)cur[(size_t)slot_var[(size_t)s]]++] = s;
     }
 
-    // ---- work units (both paths): runs of one bucket with <= unit_rows literals; on the tiled path each
-    //      unit is one shared-memory staging batch with var-sorted rows and per-variable segments
-    Lo.stage_rows = path == 1 ? tiled_stage_rows(precision) : 512;
-    if (path == 1) Lo.tiled_words.assign(Lo.fast_words.size(), 0);
-    std::vector<std::pair<uint32_t, int64_t>> pairs;  // (var, word index)
+    // ---- work units: tiled = the classes; global = runs of one bucket with <= 512 literals
+    if (path == 1) {
+        Lo.tiled_words.assign(Lo.fast_words.size(), 0);
+        for (size_t i = 0; i < Lo.fast_words.size(); ++i) {
+            uint32_t w = Lo.fast_words[i];
+            Lo.tiled_words[i] = (w & 0x7fffffffu) * (uint32_t)kTilePitch | (w & 0x80000000u);
+        }
+    }
     for (size_t bi = 0; bi < Lo.fbuckets.size(); ++bi) {
         const FastBucket& b = Lo.fbuckets[bi];
         int64_t p = b.pos_begin;
         while (p < b.pos_end) {
-            int64_t per = std::max<int64_t>(1, Lo.stage_rows / b.k);
-            int64_t q = std::min(b.pos_end, p + per);
-            SubChunk sc{};
-            sc.bucket = (int32_t)bi;
-            sc.pos_begin = p;
-            sc.pos_end = q;
-            sc.rows = (int32_t)((q - p) * b.k);
-            sc.seg_begin = sc.seg_end = (int32_t)(Lo.segs.size() / 2);
+            int64_t q = p + 1;
             if (path == 1) {
-                pairs.clear();
-                for (int64_t r = p; r < q; ++r)
-                    for (int i = 0; i < b.k; ++i) {
-                        int64_t wi = b.word_off + (r - b.pos_begin) * b.kp + i;
-                        pairs.push_back({Lo.fast_words[(size_t)wi] & 0x7fffffffu, wi});
-                    }
-                std::stable_sort(pairs.begin(), pairs.end(),
-                                 [](const std::pair<uint32_t, int64_t>& a, const std::pair<uint32_t, int64_t>& c) { return a.first < c.first; });
-                int32_t row = 0;
-                for (size_t j = 0; j < pairs.size(); ++j) {
-                    if (j == 0 || pairs[j].first != pairs[j - 1].first) {
-                        Lo.segs.push_back(pairs[j].first);
-                        Lo.segs.push_back((uint32_t)row);
-                    }
-                    uint32_t w = Lo.fast_words[(size_t)pairs[j].second];
-                    Lo.tiled_words[(size_t)pairs[j].second] = (w & 0x7fffffffu) | ((uint32_t)row << 16) | (w & 0x80000000u);
-                    ++row;
-                    Lo.segs[Lo.segs.size() - 1] = (Lo.segs[Lo.segs.size() - 1] & 0xffffu) | ((uint32_t)row << 16);
-                }
-                sc.seg_end = (int32_t)(Lo.segs.size() / 2);
+                while (q < b.pos_end && fast_class[(size_t)q] == fast_class[(size_t)p]) ++q;
+            } else {
+                q = std::min(b.pos_end, p + std::max<int64_t>(1, 512 / b.k));
             }
-            Lo.subchunks.push_back(sc);
+            Lo.units.push_back({(int32_t)bi, (int32_t)(q - p), p});
+            Lo.unit_rows.push_back((q - p) * b.k);
             p = q;
         }
     }

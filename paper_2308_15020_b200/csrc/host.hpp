@@ -63,11 +63,10 @@ struct SymClass {                   // launch class: group size G threads per (c
     int64_t begin, end;             // sym constraint indices
 };
 
-struct SubChunk {                   // tiled path: one smem staging batch
-    int32_t bucket;
-    int32_t seg_begin, seg_end;
-    int64_t pos_begin, pos_end;     // fast constraint positions
-    int32_t rows;                   // staging rows used
+struct WorkUnit {                   // a run of fast constraints of one bucket, contiguous positions
+    int32_t bucket;                 // tiled path: a var-disjoint class (no variable occurs twice in it),
+    int32_t count;                  // so the warps of a CTA can add its terms into the shared gradient
+    int64_t pos_begin;              // tile concurrently and deterministically
 };
 
 int sym_group(int k);               // threads per (constraint, point) on the root path
@@ -95,18 +94,22 @@ struct Layout {
     int64_t tb_fast = 0, tb_slots = 0;
     std::vector<int64_t> occ_off;       // [n + 1]
     std::vector<int64_t> occ_slot;      // ascending slot ids per variable
-    // tiled fast path
-    int32_t stage_rows = 0;
-    std::vector<uint32_t> tiled_words;  // var | row << 16 | neg << 31 (padded rows)
-    std::vector<SubChunk> subchunks;
-    std::vector<uint32_t> segs;         // 2 words per segment: var, row_begin | row_end << 16
+    // work units of the fast kernels (tiled: var-disjoint classes; global: runs of <= 512 literals)
+    std::vector<WorkUnit> units;
+    std::vector<int64_t> unit_rows;     // literals per unit (chunk balancing)
+    std::vector<uint32_t> tiled_words;  // tiled path: (var * kTilePitch) | neg << 31 (padded rows)
 };
+
+constexpr int kTilePitch = 33;      // smem row pitch (points per variable row + 1 pad) of the tiled kernel
+constexpr int kClassCap = 16;       // constraints per var-disjoint class (2 per warp of an 8-warp CTA)
 
 // Build everything; path: 0 auto, 1 tiled, 2 global; precision 0 auto / 32 / 64.
 Layout build_layout(const Formula& F, int path, int precision);
-// Tiled-path admission: staging rows and the max n that fits shared memory for the dtype.
-int tiled_stage_rows(int precision);
+// Tiled-path admission: the max n whose x and gradient tiles fit shared memory for the dtype.
 int tiled_max_n(int precision);
-size_t tiled_smem_bytes(int n, int precision, int stage_rows);
+size_t tiled_smem_bytes(int n, int precision);
+// Greedy partition of one bucket's constraints into var-disjoint classes of at most `cap` members
+// (first fit over the most recent `window` open classes).  Returns class id per constraint.
+std::vector<int32_t> disjoint_classes(const std::vector<std::vector<int32_t>>& vars, int32_t n, int cap, int window);
 
 }  // namespace ffsat

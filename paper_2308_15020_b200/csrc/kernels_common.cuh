@@ -1,0 +1,54 @@
+// kernels_common.cuh -- device helpers shared by the eval and solve kernels.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace ffsat {
+namespace dev {
+
+__device__ __forceinline__ float fmaT(float a, float b, float c) { return fmaf(a, b, c); }
+__device__ __forceinline__ double fmaT(double a, double b, double c) { return ::fma(a, b, c); }
+__device__ __forceinline__ float clamp1(float v) { return fminf(fmaxf(v, -1.0f), 1.0f); }
+__device__ __forceinline__ double clamp1(double v) { return fmin(fmax(v, -1.0), 1.0); }
+
+template <typename T>
+struct cplx {
+    T re, im;
+};
+template <typename T>
+__device__ __forceinline__ cplx<T> cmul(const cplx<T>& a, const cplx<T>& b) {
+    return {fmaT(a.re, b.re, -a.im * b.im), fmaT(a.re, b.im, a.im * b.re)};
+}
+
+__device__ __forceinline__ bool rule_sat(int t, int tmin, int tmax, int parity) {
+    bool ok = t >= tmin && t <= tmax;
+    if (parity == 1) ok = ok && (t & 1);
+    if (parity == 2) ok = ok && !(t & 1);
+    return ok;
+}
+
+// ---- device images of the host layout (uploaded by ffsat.cu)
+struct FastBucketDev {
+    int32_t k, kp, nch, pad0;
+    int64_t pos_begin, word_off, slot_off;
+    double g0;
+    double c0[2], c1[2], g[2];   // channel factor a = c0 + c1 * l, FE += g * prod a
+    int32_t tmin, tmax, parity, pad1;
+};
+
+struct UnitDev {                 // a run of constraints of one bucket at positions [pos_begin, pos_begin + count)
+    int32_t bucket, count;       // (tiled path: a var-disjoint class)
+    int32_t kp, pad;             // literal words per constraint row of the bucket
+    int64_t pos_begin;
+    int64_t word_begin;          // first literal word of the unit (rows of kp words, contiguous)
+};
+
+struct SymSigDev {
+    int32_t k, Mp, tmin, tmax, parity, pad;
+    int64_t coef_off;
+    double g0;
+};
+
+
+}  // namespace dev
+}  // namespace ffsat

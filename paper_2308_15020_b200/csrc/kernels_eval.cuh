@@ -2,10 +2,10 @@
 //
 //   fast_tiled_kernel   A4-A6 (+ fused A9 count) for the product fast paths (OR/AND/NAE/XOR kinds,
 //                       PAPER.md footnote P:964 and App. B) when n fits shared memory: a CTA
-//                       owns 32 points (lane = point) x a range of work units; x tile and gradient
-//                       tile live in smem; per-literal terms are staged in var-sorted rows and summed
-//                       per variable in ascending slot order (deterministic, no float atomics; the
-//                       paper's atomicAdd P:318 is replaced).
+//                       owns 32 points (lane = point) x a range of var-disjoint constraint classes;
+//                       x tile and gradient tile live in smem; warps add literal terms straight into
+//                       the gradient tile, one class at a time (deterministic order, no float atomics;
+//                       the paper's atomicAdd P:318 is replaced).
 //   fast_global_kernel  same products for large n: x transposed [n][B], terms to T[slot][B] in HBM.
 //   sym_kernel<G>       root-of-unity product path (Alg. 2 / Eqs. 7-9, in the probability
 //                       basis of DESIGN.md) with the gradient from exclusive prefix/suffix products
@@ -18,48 +18,10 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 
+#include "kernels_common.cuh"
+
 namespace ffsat {
 namespace dev {
-
-__device__ __forceinline__ float fmaT(float a, float b, float c) { return fmaf(a, b, c); }
-__device__ __forceinline__ double fmaT(double a, double b, double c) { return ::fma(a, b, c); }
-__device__ __forceinline__ float clamp1(float v) { return fminf(fmaxf(v, -1.0f), 1.0f); }
-__device__ __forceinline__ double clamp1(double v) { return fmin(fmax(v, -1.0), 1.0); }
-
-template <typename T>
-struct cplx {
-    T re, im;
-};
-template <typename T>
-__device__ __forceinline__ cplx<T> cmul(const cplx<T>& a, const cplx<T>& b) {
-    return {fmaT(a.re, b.re, -a.im * b.im), fmaT(a.re, b.im, a.im * b.re)};
-}
-
-struct FastBucketDev {
-    int32_t k, kp, nch, pad0;
-    int64_t pos_begin, word_off, slot_off;
-    double g0;
-    double c0[2], c1[2], g[2];   // channel factor a = c0 + c1 * l, FE += g * prod a
-    int32_t tmin, tmax, parity, pad1;
-};
-
-struct UnitDev {                 // a run of constraints of one bucket (tiled: one staging batch)
-    int32_t bucket, seg_begin, seg_end, rows;
-    int64_t pos_begin, pos_end;
-};
-
-struct SymSigDev {
-    int32_t k, Mp, tmin, tmax, parity, pad;
-    int64_t coef_off;
-    double g0;
-};
-
-__device__ __forceinline__ bool rule_sat(int t, int tmin, int tmax, int parity) {
-    bool ok = t >= tmin && t <= tmax;
-    if (parity == 1) ok = ok && (t & 1);
-    if (parity == 2) ok = ok && !(t & 1);
-    return ok;
-}
 
 // ------------------------------------------------------------------------------------------------
 // Per-clause fast products for one lane (= one point).  l_i = s_i x_{v_i}; channel c factor
@@ -93,8 +55,8 @@ __device__ __forceinline__ void fast_terms(const T (&l)[K], const FastBucketDev&
 
 // 16 < k <= 64: literals in register blocks of 16 with a prefix checkpoint per block.
 // getl(i) returns l_i; addterm(i, v, first) stores (first) or accumulates v into literal i's term.
-template <typename T, int NCH, typename GetL, typename AddTerm>
-__device__ __forceinline__ void fast_terms_blocked(int k, const FastBucketDev& bk, GetL getl, AddTerm addterm, T& fe) {
+template <typename T, int NCH, typename BK, typename GetL, typename AddTerm>
+__device__ __forceinline__ void fast_terms_blocked(int k, const BK& bk, GetL getl, AddTerm addterm, T& fe) {
     fe = (T)bk.g0;
 #pragma unroll
     for (int c = 0; c < NCH; ++c) {
@@ -138,15 +100,14 @@ __device__ __forceinline__ void fast_terms_blocked(int k, const FastBucketDev& b
 }
 
 // ------------------------------------------------------------------------------------------------
-// Tiled fast kernel.  grid = (ceil(B/32), n_chunks); block = NT threads (NT/32 warps).
+// Tiled fast kernel: device helpers (the kernel itself and its design notes follow below).
 template <typename T>
 struct TiledArgs {
     const T* x;                  // [B][n]
     int64_t B;
-    int32_t n, stage_rows;
-    const uint32_t* words;       // var | row << 16 | neg << 31, padded rows of kp words
+    int32_t n;
+    const uint32_t* words;       // (var * kTilePitch) | neg << 31, rows of kp words
     const UnitDev* units;
-    const uint2* segs;           // (var, row_begin | row_end << 16)
     const FastBucketDev* buckets;
     const int32_t* chunk_units;  // [n_chunks + 1]
     const T* w_pos;              // weights by constraint position
@@ -155,90 +116,268 @@ struct TiledArgs {
     int32_t* upart;              // [n_chunks][B]
 };
 
+constexpr int kPitch = 33;       // == kTilePitch of host.hpp (row pitch of the smem tiles)
+
+__device__ __forceinline__ float flip_sign(float v, uint32_t w) { return __int_as_float(__float_as_int(v) ^ (int)(w & 0x80000000u)); }
+__device__ __forceinline__ double flip_sign(double v, uint32_t w) {
+    return __longlong_as_double(__double_as_longlong(v) ^ ((long long)(w & 0x80000000u) << 32));
+}
+// 1 iff the literal (variable value xv, sign bit of w) is True: (xv < 0) xor negated.  The tiles hold
+// canonical zeros (-0.0 stored as +0.0), so the sign bit of xv is exactly "xv < 0" (tie rule: x = 0 is False).
+__device__ __forceinline__ uint32_t lit_true(float xv, uint32_t w) { return (__float_as_uint(xv) ^ w) >> 31; }
+__device__ __forceinline__ uint32_t lit_true(double xv, uint32_t w) { return ((uint32_t)__double2hiint(xv) ^ w) >> 31; }
+
+// Bucket constants of one work unit, converted to the path dtype once (registers).
+template <typename T>
+struct BucketReg {
+    T g0, c0[2], c1[2], g[2];
+    int32_t k, kp, tmin, tmax, parity;
+    int64_t pos_begin, word_off;
+};
+template <typename T>
+__device__ __forceinline__ BucketReg<T> load_bucket(const FastBucketDev* p) {
+    BucketReg<T> r;
+    r.g0 = (T)p->g0;
+#pragma unroll
+    for (int c = 0; c < 2; ++c) {
+        r.c0[c] = (T)p->c0[c];
+        r.c1[c] = (T)p->c1[c];
+        r.g[c] = (T)p->g[c];
+    }
+    r.k = p->k; r.kp = p->kp; r.tmin = p->tmin; r.tmax = p->tmax; r.parity = p->parity;
+    r.pos_begin = p->pos_begin; r.word_off = p->word_off;
+    return r;
+}
+
+// Shared-memory element at byte offset (w << log2 sizeof(T)) from a lane's tile base: the 32-bit shift
+// drops the literal's sign bit (bit 31), so one LEA forms the address.
+template <typename T>
+__device__ __forceinline__ const T* tile_at(const T* base, uint32_t w) {
+    return reinterpret_cast<const T*>(reinterpret_cast<const char*>(base) + (uint32_t)(w << (sizeof(T) == 8 ? 3 : 2)));
+}
+template <typename T>
+__device__ __forceinline__ T* tile_at(T* base, uint32_t w) {
+    return reinterpret_cast<T*>(reinterpret_cast<char*>(base) + (uint32_t)(w << (sizeof(T) == 8 ? 3 : 2)));
+}
+
+// One constraint for one lane (= one point), k <= 16 unrolled, literal words already in registers.
+// With c_s = s_i c1 (literal sign folded into the factor slope), a_i = c0 + c_s x_{v_i};
+// FE = g0 + sum_ch g prod_i a_i and d f / d x_{v_i} = w sum_ch g c_s prod_{j != i} a_j (exclusive
+// prefix * suffix products, no division; Prop. 1 / Eq. 10).  The terms are added straight into
+// the shared gradient tile (the unit is var-disjoint, so no other warp touches these rows meanwhile).
 template <typename T, int K, int NCH>
-__device__ __forceinline__ void tiled_clause(const TiledArgs<T>& a, const FastBucketDev& bk, int64_t pos,
-                                             const T* xs, T* Ts, int lane, double& facc, int& uacc) {
-    const uint32_t* wp = a.words + bk.word_off + (pos - bk.pos_begin) * bk.kp;
-    uint32_t w[K];
+__device__ __forceinline__ void tiled_clause(const BucketReg<T>& bk, const uint32_t (&w)[K], T wc, const T* xl, T* gl,
+                                             double& facc, int& uacc) {
+    T xv[K];
+    uint32_t t = 0;
+#pragma unroll
+    for (int i = 0; i < K; ++i) {
+        xv[i] = *tile_at(xl, w[i]);
+        t += lit_true(xv[i], w[i]);
+    }
+    T fe = bk.g0;
+    if (NCH == 1) {
+        T cs[K], av[K], pre[K];
+        T run = (T)1;
+#pragma unroll
+        for (int i = 0; i < K; ++i) {
+            cs[i] = flip_sign(bk.c1[0], w[i]);
+            av[i] = fmaT(cs[i], xv[i], bk.c0[0]);
+            pre[i] = run;
+            run *= av[i];
+        }
+        fe = fmaT(bk.g[0], run, fe);
+        T suf = bk.g[0] * wc;
+#pragma unroll
+        for (int i = K - 1; i >= 0; --i) {
+            T* g = tile_at(gl, w[i]);
+            *g = fmaT(pre[i] * suf, cs[i], *g);
+            suf *= av[i];
+        }
+    } else if (NCH == 2) {
+        T gs[K];
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+            T cs[K], av[K], pre[K];
+            T run = (T)1;
+#pragma unroll
+            for (int i = 0; i < K; ++i) {
+                cs[i] = flip_sign(bk.c1[c], w[i]);
+                av[i] = fmaT(cs[i], xv[i], bk.c0[c]);
+                pre[i] = run;
+                run *= av[i];
+            }
+            fe = fmaT(bk.g[c], run, fe);
+            T suf = bk.g[c] * wc;
+#pragma unroll
+            for (int i = K - 1; i >= 0; --i) {
+                gs[i] = c == 0 ? (pre[i] * suf) * cs[i] : fmaT(pre[i] * suf, cs[i], gs[i]);
+                suf *= av[i];
+            }
+        }
+#pragma unroll
+        for (int i = 0; i < K; ++i) *tile_at(gl, w[i]) += gs[i];
+    }
+    facc += (double)(wc * fe);
+    uacc += rule_sat((int)t, bk.tmin, bk.tmax, bk.parity) ? 0 : 1;
+}
+
+#define K_PAD(K) (((K) + 3) / 4 * 4)
+
+template <int K>
+__device__ __forceinline__ void load_words_smem(const uint32_t* sp, uint32_t (&w)[K]) {
 #pragma unroll
     for (int i = 0; i < K; i += 4) {
-        uint4 q = __ldg(reinterpret_cast<const uint4*>(wp + i));
+        uint4 q = *reinterpret_cast<const uint4*>(sp + i);
         w[i] = q.x;
         if (i + 1 < K) w[i + 1] = q.y;
         if (i + 2 < K) w[i + 2] = q.z;
         if (i + 3 < K) w[i + 3] = q.w;
     }
-    T l[K];
-    int t = 0;
-#pragma unroll
-    for (int i = 0; i < K; ++i) {
-        T xv = xs[(w[i] & 0xffffu) * 33 + lane];
-        bool neg = w[i] >> 31;
-        l[i] = neg ? -xv : xv;
-        t += (int)((xv < (T)0) != neg);
+}
+
+// ---- unit staging: while a unit is processed, the next unit's literal words and weights are copied
+//      global -> shared with cp.async (LDGSTS) into the other half of a double buffer.
+constexpr int kStageWords = 256;   // kClassCap (16) constraints x 16 words (k <= 16)
+constexpr int kStageCons = 16;
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"((uint32_t)__cvta_generic_to_shared(smem)), "l"(gmem));
+}
+template <int BYTES>
+__device__ __forceinline__ void cp_async_small(void* smem, const void* gmem) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], %2;\n" ::"r"((uint32_t)__cvta_generic_to_shared(smem)), "l"(gmem), "n"(BYTES));
+}
+__device__ __forceinline__ void cp_async_commit_wait_all() {
+    asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
+
+template <typename T>
+struct TileStage {
+    uint32_t words[2][kStageWords];
+    T w[2][kStageCons];
+};
+
+template <typename T>
+__device__ __forceinline__ void stage_unit(const TiledArgs<T>& a, const UnitDev& U, TileStage<T>& st, int buf) {
+    const int nwords = min(U.count * U.kp, kStageWords);
+    const int t = threadIdx.x;
+    if (t * 4 < nwords) cp_async16(&st.words[buf][t * 4], a.words + U.word_begin + t * 4);
+    const int c = t - 64;
+    if (c >= 0 && c < min(U.count, kStageCons)) cp_async_small<sizeof(T)>(&st.w[buf][c], a.w_pos + U.pos_begin + c);
+}
+
+// Pipeline state: `cur` is being processed from stage buffer `buf`; `next` is staged (or in flight).
+struct UnitPipe {
+    UnitDev cur, next;
+    int u, buf;
+};
+
+// Advance past `cur`: stage `next`'s successor ... (called by all threads after processing `cur`).
+template <typename T>
+__device__ __forceinline__ void pipe_advance(const TiledArgs<T>& a, UnitPipe& P, int u1, TileStage<T>& st) {
+    cp_async_wait_all();
+    __syncthreads();          // next's words are visible; everybody is done with cur's buffer
+    P.u += 1;
+    P.cur = P.next;
+    P.buf ^= 1;
+    if (P.u + 1 < u1) {
+        P.next = a.units[P.u + 1];
+        stage_unit<T>(a, P.next, st, P.buf ^ 1);
     }
-    T term[K], fe;
-    fast_terms<T, K, NCH>(l, bk, term, fe);
-    const T wc = a.w_pos[pos];
-#pragma unroll
-    for (int i = 0; i < K; ++i) {
-        T v = wc * term[i];
-        Ts[((w[i] >> 16) & 0x7fffu) * 32 + lane] = (w[i] >> 31) ? -v : v;
+    cp_async_commit();
+}
+
+// A run of consecutive units of one bucket: for each unit the warp takes constraints j = warp,
+// warp + nw, ... (two at a time), literal words and weights read from the stage buffer; the pipeline
+// barrier ends the unit.
+template <typename T, int K, int NCH>
+__device__ __forceinline__ void tiled_run(const TiledArgs<T>& a, int bucket, const BucketReg<T>& bk, UnitPipe& P, int u1,
+                                          TileStage<T>& st, const T* xl, T* gl, int warp, int nw, double& facc, int& uacc) {
+    while (P.u < u1 && P.cur.bucket == bucket) {
+        const uint32_t* sw = st.words[P.buf];
+        const T* swt = st.w[P.buf];
+        const int count = P.cur.count;
+        int j = warp;
+        for (; j + nw < count; j += 2 * nw) {
+            uint32_t w0[K], w1[K];
+            load_words_smem<K>(sw + j * K_PAD(K), w0);
+            load_words_smem<K>(sw + (j + nw) * K_PAD(K), w1);
+            tiled_clause<T, K, NCH>(bk, w0, swt[j], xl, gl, facc, uacc);
+            tiled_clause<T, K, NCH>(bk, w1, swt[j + nw], xl, gl, facc, uacc);
+        }
+        if (j < count) {
+            uint32_t w0[K];
+            load_words_smem<K>(sw + j * K_PAD(K), w0);
+            tiled_clause<T, K, NCH>(bk, w0, swt[j], xl, gl, facc, uacc);
+        }
+        pipe_advance<T>(a, P, u1, st);
     }
-    facc += (double)(wc * fe);
-    uacc += rule_sat(t, bk.tmin, bk.tmax, bk.parity) ? 0 : 1;
+}
+
+template <typename T, int NCH>
+__device__ void tiled_run_long(const TiledArgs<T>& a, int bucket, const BucketReg<T>& bk, UnitPipe& P, int u1, TileStage<T>& st,
+                               const T* xl, T* gl, int warp, int nw, double& facc, int& uacc) {
+    const int k = bk.k;
+    while (P.u < u1 && P.cur.bucket == bucket) {
+        for (int j = warp; j < P.cur.count; j += nw) {
+            const int64_t pos = P.cur.pos_begin + j;
+            const uint32_t* wp = a.words + P.cur.word_begin + (int64_t)j * P.cur.kp;
+            uint32_t t = 0;
+            for (int i = 0; i < k; ++i) {
+                uint32_t w = __ldg(wp + i);
+                t += lit_true(*tile_at(xl, w), w);
+            }
+            const T wc = a.w_pos[pos];
+            auto getl = [&](int i) -> T {
+                uint32_t w = __ldg(wp + i);
+                return flip_sign(*tile_at(xl, w), w);
+            };
+            auto addterm = [&](int i, T v, bool) {
+                uint32_t w = __ldg(wp + i);
+                *tile_at(gl, w) += flip_sign(wc * v, w);
+            };
+            T fe;
+            fast_terms_blocked<T, NCH>(k, bk, getl, addterm, fe);
+            facc += (double)(wc * fe);
+            uacc += rule_sat((int)t, bk.tmin, bk.tmax, bk.parity) ? 0 : 1;
+        }
+        pipe_advance<T>(a, P, u1, st);
+    }
 }
 
 template <typename T, int NCH, int KMAX>
-__device__ void tiled_clause_dispatch(const TiledArgs<T>& a, const FastBucketDev& bk, int64_t pos, const T* xs, T* Ts,
-                                      int lane, double& facc, int& uacc) {
+__device__ __forceinline__ void tiled_run_dispatch(const TiledArgs<T>& a, int bucket, const BucketReg<T>& bk, UnitPipe& P, int u1,
+                                                   TileStage<T>& st, const T* xl, T* gl, int warp, int nw, double& facc, int& uacc) {
     switch (bk.k) {
-#define FFSAT_K(KK) case KK: if (KK <= KMAX) { tiled_clause<T, (KK <= KMAX ? KK : 1), NCH>(a, bk, pos, xs, Ts, lane, facc, uacc); return; } break;
+#define FFSAT_K(KK) case KK: if (KK <= KMAX) { tiled_run<T, (KK <= KMAX ? KK : 1), NCH>(a, bucket, bk, P, u1, st, xl, gl, warp, nw, facc, uacc); return; } break;
         FFSAT_K(1) FFSAT_K(2) FFSAT_K(3) FFSAT_K(4) FFSAT_K(5) FFSAT_K(6) FFSAT_K(7) FFSAT_K(8)
         FFSAT_K(9) FFSAT_K(10) FFSAT_K(11) FFSAT_K(12) FFSAT_K(13) FFSAT_K(14) FFSAT_K(15) FFSAT_K(16)
 #undef FFSAT_K
     default: break;
     }
-    if (KMAX <= 16) return;
-    // 16 < k <= 64: literal values re-read from the x tile, terms accumulated in their staging rows
-    const int k = bk.k;
-    const uint32_t* wp = a.words + bk.word_off + (pos - bk.pos_begin) * bk.kp;
-    int t = 0;
-    for (int i = 0; i < k; ++i) {
-        uint32_t w = __ldg(wp + i);
-        T xv = xs[(w & 0xffffu) * 33 + lane];
-        t += (int)((xv < (T)0) != (bool)(w >> 31));
+    if constexpr (KMAX > 16) {
+        tiled_run_long<T, NCH>(a, bucket, bk, P, u1, st, xl, gl, warp, nw, facc, uacc);
+    } else {
+        while (P.u < u1) pipe_advance<T>(a, P, u1, st);   // unreachable (KMAX >= every k); keeps the barriers matched
     }
-    auto getl = [&](int i) -> T {
-        uint32_t w = __ldg(wp + i);
-        T xv = xs[(w & 0xffffu) * 33 + lane];
-        return (w >> 31) ? -xv : xv;
-    };
-    auto addterm = [&](int i, T v, bool first) {
-        uint32_t w = __ldg(wp + i);
-        T* dst = Ts + ((w >> 16) & 0x7fffu) * 32 + lane;
-        *dst = first ? v : *dst + v;
-    };
-    T fe;
-    fast_terms_blocked<T, NCH>(k, bk, getl, addterm, fe);
-    const T wc = a.w_pos[pos];
-    for (int i = 0; i < k; ++i) {
-        uint32_t w = __ldg(wp + i);
-        T* dst = Ts + ((w >> 16) & 0x7fffu) * 32 + lane;
-        T v = wc * *dst;
-        *dst = (w >> 31) ? -v : v;
-    }
-    facc += (double)(wc * fe);
-    uacc += rule_sat(t, bk.tmin, bk.tmax, bk.parity) ? 0 : 1;
 }
 
+// Tiled fast kernel (n small enough for the x and gradient tiles to live in shared memory).
+// grid = (ceil(B/32), n_chunks); block = 256 threads.  lane = point, warp = constraint.  The work units
+// of a chunk are var-disjoint classes (host: disjoint_classes): inside a class no variable occurs twice,
+// so the 8 warps add their literal terms straight into the shared gradient tile without races; a
+// barrier separates classes.  Every (variable, point) entry is therefore accumulated in one fixed order
+// (class order, then literal order) -- deterministic without atomics (the paper's atomicAdd).
 template <typename T, int KMAX>
-__global__ void __launch_bounds__(256) fast_tiled_kernel(TiledArgs<T> a) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
+__global__ void __launch_bounds__(256, (sizeof(T) == 4 ? (KMAX <= 8 ? 4 : 2) : (KMAX <= 8 ? 2 : 1))) fast_tiled_kernel(TiledArgs<T> a) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];   // >= 3 KB (host: tiled_smem_bytes)
+    __shared__ __align__(16) TileStage<T> st;
     const int n = a.n;
-    T* xs = reinterpret_cast<T*>(smem_raw);                 // [n][33]
-    T* Gs = xs + (size_t)n * 33;                            // [n][33]
-    T* Ts = Gs + (size_t)n * 33;                            // [stage_rows][32]
+    T* xs = reinterpret_cast<T*>(smem_raw);                 // [n][kPitch]
+    T* Gs = xs + (size_t)n * kPitch;                        // [n][kPitch]
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
     const int64_t b0 = (int64_t)blockIdx.x * 32;
     const int64_t b = b0 + lane;
@@ -247,38 +386,45 @@ __global__ void __launch_bounds__(256) fast_tiled_kernel(TiledArgs<T> a) {
     for (int idx = threadIdx.x; idx < 32 * n; idx += blockDim.x) {
         int r = idx / n, v = idx - r * n;
         int64_t bb = b0 + r;
-        xs[v * 33 + r] = bb < a.B ? a.x[bb * n + v] : (T)0;
-        Gs[v * 33 + r] = (T)0;
+        xs[v * kPitch + r] = bb < a.B ? a.x[bb * n + v] + (T)0 : (T)0;   // + 0 canonicalises -0.0 to +0.0
+        Gs[v * kPitch + r] = (T)0;
     }
     __syncthreads();
 
     double facc = 0.0;
     int uacc = 0;
+    const T* xl = xs + lane;
+    T* gl = Gs + lane;
     const int u0 = a.chunk_units[chunk], u1 = a.chunk_units[chunk + 1];
-    for (int u = u0; u < u1; ++u) {
-        const UnitDev U = a.units[u];
-        const FastBucketDev bk = a.buckets[U.bucket];
-        for (int64_t pos = U.pos_begin + warp; pos < U.pos_end; pos += nw) {
-            if (bk.nch == 1) tiled_clause_dispatch<T, 1, KMAX>(a, bk, pos, xs, Ts, lane, facc, uacc);
-            else if (bk.nch == 2) tiled_clause_dispatch<T, 2, KMAX>(a, bk, pos, xs, Ts, lane, facc, uacc);
-            else tiled_clause_dispatch<T, 0, KMAX>(a, bk, pos, xs, Ts, lane, facc, uacc);
+    UnitPipe P;
+    P.u = u0;
+    P.buf = 0;
+    if (u0 < u1) {
+        P.cur = a.units[u0];
+        stage_unit<T>(a, P.cur, st, 0);
+        if (u0 + 1 < u1) {
+            P.next = a.units[u0 + 1];
+            stage_unit<T>(a, P.next, st, 1);
         }
-        __syncthreads();
-        for (int s = U.seg_begin + warp; s < U.seg_end; s += nw) {
-            uint2 sg = __ldg(a.segs + s);
-            int rb = sg.y & 0xffffu, re = sg.y >> 16;
-            T acc = (T)0;
-            for (int r = rb; r < re; ++r) acc += Ts[r * 32 + lane];
-            Gs[sg.x * 33 + lane] += acc;
-        }
-        __syncthreads();
+    }
+    cp_async_commit_wait_all();
+    __syncthreads();
+    while (P.u < u1) {
+        const int bucket = P.cur.bucket;
+        const FastBucketDev* bp = a.buckets + bucket;
+        const int nch = bp->nch;
+        const BucketReg<T> bk = load_bucket<T>(bp);
+        if (nch == 1) tiled_run_dispatch<T, 1, KMAX>(a, bucket, bk, P, u1, st, xl, gl, warp, nw, facc, uacc);
+        else if (nch == 2) tiled_run_dispatch<T, 2, KMAX>(a, bucket, bk, P, u1, st, xl, gl, warp, nw, facc, uacc);
+        else tiled_run_dispatch<T, 0, KMAX>(a, bucket, bk, P, u1, st, xl, gl, warp, nw, facc, uacc);
     }
     // outputs: partial gradient tile, partial f / unsat (fixed warp order)
     if (b < a.B) {
-        for (int v = warp; v < n; v += nw) a.P[((int64_t)chunk * n + v) * a.B + b] = Gs[v * 33 + lane];
+        for (int v = warp; v < n; v += nw) a.P[((int64_t)chunk * n + v) * a.B + b] = Gs[v * kPitch + lane];
     }
-    double* fr = reinterpret_cast<double*>(Ts);   // reuse staging
-    int* ur = reinterpret_cast<int*>(fr + nw * 32);
+    __syncthreads();
+    double* fr = reinterpret_cast<double*>(smem_raw);        // [8][32], reuses the tiles
+    int* ur = reinterpret_cast<int*>(fr + 8 * 32);           // [8][32]
     fr[warp * 32 + lane] = facc;
     ur[warp * 32 + lane] = uacc;
     __syncthreads();
@@ -406,7 +552,7 @@ __global__ void __launch_bounds__(256) fast_global_kernel(GlobalArgs<T> a) {
     for (int u = a.chunk_units[chunk]; u < a.chunk_units[chunk + 1]; ++u) {
         const UnitDev U = a.units[u];
         const FastBucketDev bk = a.buckets[U.bucket];
-        for (int64_t pos = U.pos_begin + warp; pos < U.pos_end; pos += nw) {
+        for (int64_t pos = U.pos_begin + warp; pos < U.pos_begin + U.count; pos += nw) {
             if (bk.nch == 1) global_clause_dispatch<T, 1, KMAX>(a, bk, pos, b, bv, facc, uacc);
             else if (bk.nch == 2) global_clause_dispatch<T, 2, KMAX>(a, bk, pos, b, bv, facc, uacc);
             else global_clause_dispatch<T, 0, KMAX>(a, bk, pos, b, bv, facc, uacc);
@@ -646,21 +792,37 @@ struct ReduceFArgs {
     int32_t* unsat;              // [B] or null
 };
 
-__global__ void reduce_f_kernel(ReduceFArgs a) {
-    const int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (b >= a.B) return;
+// one CTA (128 threads) per point: thread t sums rows t, t + 128, ... in ascending order, then a fixed
+// shared-memory tree -- a fixed summation order for any launch (deterministic, no atomics).
+static __global__ void __launch_bounds__(128) reduce_f_kernel(ReduceFArgs a) {
+    __shared__ double sf[128];
+    __shared__ int su[128];
+    const int64_t b = blockIdx.x;
+    const int t = threadIdx.x;
     double f = 0.0;
     int u = 0;
-    for (int c = 0; c < a.n_parts; ++c) {
+    for (int c = t; c < a.n_parts; c += 128) {
         f += a.fpart[(int64_t)c * a.B + b];
         u += a.upart[(int64_t)c * a.B + b];
     }
-    for (int64_t s = 0; s < a.n_sym; ++s) {
+    for (int64_t s = t; s < a.n_sym; s += 128) {
         f += a.fsym[s * a.B + b];
         u += a.usym[s * a.B + b];
     }
-    a.f[b] = f;
-    if (a.unsat) a.unsat[b] = u;
+    sf[t] = f;
+    su[t] = u;
+    __syncthreads();
+    for (int h = 64; h > 0; h >>= 1) {
+        if (t < h) {
+            sf[t] += sf[t + h];
+            su[t] += su[t + h];
+        }
+        __syncthreads();
+    }
+    if (t == 0) {
+        a.f[b] = sf[0];
+        if (a.unsat) a.unsat[b] = su[0];
+    }
 }
 
 // x [B][n] -> xT [n][B]

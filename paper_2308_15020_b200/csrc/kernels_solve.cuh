@@ -13,7 +13,7 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 
-#include "kernels_eval.cuh"
+#include "kernels_common.cuh"
 
 namespace ffsat {
 namespace dev {
