@@ -8,6 +8,28 @@
 
 namespace ffsat {
 
+// k shared by every fast bucket when all of them are single-channel products with k <= 16, else 0.
+inline int uniform_k(const Layout& L) {
+    int k = 0;
+    for (const FastBucket& b : L.fbuckets) {
+        const int nch = (b.gA != 0) + (b.gB != 0) + (b.gX != 0);
+        if (nch != 1 || b.k > 16 || (k != 0 && b.k != k)) return 0;
+        k = b.k;
+    }
+    return k;
+}
+
+template <typename T>
+void launch_tiled_uniform(int k, dim3 grid, size_t smem, cudaStream_t st, const dev::TiledArgs<T>& a) {
+    switch (k) {
+#define FFSAT_KU(K) case K: dev::fast_tiled_kernel<T, (K <= 4 ? 4 : K <= 8 ? 8 : 16), K><<<grid, 256, smem, st>>>(a); break;
+        FFSAT_KU(1) FFSAT_KU(2) FFSAT_KU(3) FFSAT_KU(4) FFSAT_KU(5) FFSAT_KU(6) FFSAT_KU(7) FFSAT_KU(8)
+        FFSAT_KU(9) FFSAT_KU(10) FFSAT_KU(11) FFSAT_KU(12) FFSAT_KU(13) FFSAT_KU(14) FFSAT_KU(15) FFSAT_KU(16)
+#undef FFSAT_KU
+    default: break;
+    }
+}
+
 inline int fast_kmax(const Layout& L) {
     int km = 0;
     for (const FastBucket& b : L.fbuckets) km = std::max(km, b.k);
@@ -49,7 +71,9 @@ void eval_device_t(ffsat_ctx* c, const T* x, int64_t B, double* f, T* grad, int3
             a.P = c->P.as<T>(); a.fpart = c->fpart.as<double>(); a.upart = c->upart.as<int32_t>();
             dim3 grid((unsigned)PT, (unsigned)c->n_chunks);
             const int km = fast_kmax(L);
-            if (km <= 4) dev::fast_tiled_kernel<T, 4><<<grid, 256, c->tiled_smem, st>>>(a);
+            const int ku = uniform_k(L);
+            if (ku > 0) launch_tiled_uniform<T>(ku, grid, c->tiled_smem, st, a);
+            else if (km <= 4) dev::fast_tiled_kernel<T, 4><<<grid, 256, c->tiled_smem, st>>>(a);
             else if (km <= 8) dev::fast_tiled_kernel<T, 8><<<grid, 256, c->tiled_smem, st>>>(a);
             else if (km <= 16) dev::fast_tiled_kernel<T, 16><<<grid, 256, c->tiled_smem, st>>>(a);
             else dev::fast_tiled_kernel<T, 64><<<grid, 256, c->tiled_smem, st>>>(a);
@@ -87,7 +111,7 @@ void eval_device_t(ffsat_ctx* c, const T* x, int64_t B, double* f, T* grad, int3
         dev::ReduceArgs<T> r{};
         r.B = B; r.n = L.n; r.n_chunks = L.path == 1 ? c->n_chunks : 0; r.P = c->P.as<T>(); r.Tb = c->Tb.as<T>();
         r.occ_off = c->occ_off.as<int64_t>(); r.occ_slot = c->occ_slot.as<int32_t>(); r.grad = grad;
-        dim3 grid(blocks_for(B, 32), blocks_for(L.n, 32)), blk(32, 8);
+        dim3 grid(blocks_for(L.n, 8), blocks_for(B, 32)), blk(32, 8);
         dev::reduce_grad_kernel<T><<<grid, blk, 0, st>>>(r);
     }
     mark(3);
@@ -96,7 +120,7 @@ void eval_device_t(ffsat_ctx* c, const T* x, int64_t B, double* f, T* grad, int3
     rf.B = B; rf.n_parts = L.n_fast > 0 ? c->n_chunks : 0; rf.n_sym = L.n_sym;
     rf.fpart = c->fpart.as<double>(); rf.upart = c->upart.as<int32_t>(); rf.fsym = c->fsym.as<double>();
     rf.usym = c->usym.as<int32_t>(); rf.f = f; rf.unsat = unsat;
-    dev::reduce_f_kernel<<<(unsigned)B, 128, 0, st>>>(rf);
+    dev::reduce_f_kernel<<<blocks_for(B, 32), 256, 0, st>>>(rf);
     CK(cudaGetLastError());
     mark(4);
 }
@@ -104,8 +128,13 @@ void eval_device_t(ffsat_ctx* c, const T* x, int64_t B, double* f, T* grad, int3
 
 template <typename T>
 void set_tiled_smem(size_t bytes) {
-    const void* kerns[4] = {(const void*)dev::fast_tiled_kernel<T, 4>, (const void*)dev::fast_tiled_kernel<T, 8>,
-                            (const void*)dev::fast_tiled_kernel<T, 16>, (const void*)dev::fast_tiled_kernel<T, 64>};
+    const void* kerns[4 + 16] = {(const void*)dev::fast_tiled_kernel<T, 4>, (const void*)dev::fast_tiled_kernel<T, 8>,
+                                 (const void*)dev::fast_tiled_kernel<T, 16>, (const void*)dev::fast_tiled_kernel<T, 64>,
+#define FFSAT_KU(K) (const void*)dev::fast_tiled_kernel<T, (K <= 4 ? 4 : K <= 8 ? 8 : 16), K>,
+                                 FFSAT_KU(1) FFSAT_KU(2) FFSAT_KU(3) FFSAT_KU(4) FFSAT_KU(5) FFSAT_KU(6) FFSAT_KU(7) FFSAT_KU(8)
+                                 FFSAT_KU(9) FFSAT_KU(10) FFSAT_KU(11) FFSAT_KU(12) FFSAT_KU(13) FFSAT_KU(14) FFSAT_KU(15) FFSAT_KU(16)
+#undef FFSAT_KU
+    };
     for (const void* k : kerns) CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
 }
 

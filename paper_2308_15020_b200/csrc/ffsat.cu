@@ -34,7 +34,7 @@ struct ffsat_search {
     int64_t B = 0, point0 = 0;
     uint64_t seed = 0;
     ffsat_solve_params P{};
-    DBuf X, Xp, Gx, Gp, fX, fP, dot, eta, done, iters, unsatP, solved, sol, unsat, U, stats;
+    DBuf X, Xp, Gx, Gp, fX, fP, dot, eta, done, iters, unsatP, solved, sol, unsat, U, stats, xT;
     int64_t round = 0, iters_issued = 0;
 };
 
@@ -51,7 +51,10 @@ void upload_layout(ffsat_ctx* c) {
     std::vector<dev::UnitDev> units;
     for (const WorkUnit& u : L.units) {
         const FastBucket& b = L.fbuckets[(size_t)u.bucket];
-        units.push_back({u.bucket, u.count, b.kp, 0, u.pos_begin, b.word_off + (u.pos_begin - b.pos_begin) * b.kp});
+        const int64_t wb = b.word_off + (u.pos_begin - b.pos_begin) * b.kp;
+        if (u.count > 0xffff || b.kp > 0x7fff || u.pos_begin > INT32_MAX || wb > INT32_MAX)
+            throw Error(FFSAT_ERR_ARG, "formula too large for 32-bit work-unit headers");
+        units.push_back({u.bucket, u.count | (b.kp << 16), (int32_t)u.pos_begin, (int32_t)wb});
     }
     upload(c->units, units);
     std::vector<dev::FastBucketDev> bks;
@@ -259,16 +262,46 @@ void search_iterate(ffsat_search* s, int n_iters, cudaStream_t st) {
 }
 
 void search_check(ffsat_search* s, cudaStream_t st) {
-    const Layout& L = s->ctx->Lo;
+    ffsat_ctx* c = s->ctx;
+    const Layout& L = c->Lo;
     CK(cudaMemsetAsync(s->unsat.p, 0, (size_t)s->B * 4, st));
+    if (L.m == 0) return;
+    CK(cudaMemsetAsync(s->U.p, 0, (size_t)L.m * 4, st));
+    const size_t es = c->esize;
+    const size_t tile = (size_t)L.n * 33 * es;
+    const bool smem = tile <= 200 * 1024;
     dev::CheckArgs a{};
-    a.X = s->X.p; a.B = s->B; a.n = L.n; a.m = L.m; a.off = s->ctx->chk_off.as<int64_t>();
-    a.words = s->ctx->chk_words.as<uint32_t>(); a.rule = s->ctx->chk_rule.as<int32_t>();
+    a.B = s->B; a.n = L.n; a.m = L.m; a.off = c->chk_off.as<int64_t>();
+    a.words = c->chk_words.as<uint32_t>(); a.rule = c->chk_rule.as<int32_t>();
     a.U = s->U.as<int32_t>(); a.unsat = s->unsat.as<int32_t>();
-    if (L.m > 0) {
+    const int64_t PT = (s->B + 31) / 32;
+    const int cps = smem ? std::max(1, (int)std::min<size_t>(8, (228 * 1024) / (tile + 2048))) : 8;
+    const int64_t want = std::max<int64_t>(1, (int64_t)c->num_sm * cps * 2 / PT);
+    const int64_t chunks = std::min<int64_t>(std::min<int64_t>(want, 65535), (L.m + 7) / 8);
+    a.cons_per_cta = (L.m + chunks - 1) / chunks;
+    dim3 grid((unsigned)PT, (unsigned)((L.m + a.cons_per_cta - 1) / a.cons_per_cta));
+    if (smem) {
+        a.X = s->X.p;
+        if (L.precision == 64) {
+            CK(cudaFuncSetAttribute(dev::check_kernel<double, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tile));
+            dev::check_kernel<double, true><<<grid, 256, tile, st>>>(a);
+        } else {
+            CK(cudaFuncSetAttribute(dev::check_kernel<float, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tile));
+            dev::check_kernel<float, true><<<grid, 256, tile, st>>>(a);
+        }
         s->ctx->launches += 1;
-        if (L.precision == 64) dev::check_kernel<double><<<blocks_for(L.m, 8), 256, 0, st>>>(a);
-        else dev::check_kernel<float><<<blocks_for(L.m, 8), 256, 0, st>>>(a);
+    } else {
+        s->xT.ensure((size_t)L.n * s->B * es);
+        dim3 tg(blocks_for(L.n, 32), blocks_for(s->B, 32)), tb(32, 8);
+        a.X = s->xT.p;
+        if (L.precision == 64) {
+            dev::transpose_search_kernel<double><<<tg, tb, 0, st>>>(s->X.as<double>(), s->xT.as<double>(), s->B, L.n);
+            dev::check_kernel<double, false><<<grid, 256, 0, st>>>(a);
+        } else {
+            dev::transpose_search_kernel<float><<<tg, tb, 0, st>>>(s->X.as<float>(), s->xT.as<float>(), s->B, L.n);
+            dev::check_kernel<float, false><<<grid, 256, 0, st>>>(a);
+        }
+        s->ctx->launches += 2;
     }
     CK(cudaGetLastError());
 }

@@ -223,7 +223,7 @@ static void sym_coefficients(int k, SatRule r, std::vector<double>& coef, double
 size_t tiled_smem_bytes(int n, int precision) {
     size_t es = precision == 64 ? 8 : 4;
     // x tile and gradient tile [n][kTilePitch]; at least 3 KB (the kernel's final f / unsat exchange)
-    return std::max<size_t>(es * 2 * (size_t)kTilePitch * (size_t)n, 3072);
+    return std::max<size_t>(es * (size_t)kTilePitch * (size_t)n, 3072);
 }
 
 int tiled_max_n(int precision) {

@@ -100,7 +100,7 @@ struct Layout {
     std::vector<uint32_t> tiled_words;  // tiled path: (var * kTilePitch) | neg << 31 (padded rows)
 };
 
-constexpr int kTilePitch = 33;      // smem row pitch (points per variable row + 1 pad) of the tiled kernel
+constexpr int kTilePitch = 66;      // smem row pitch of the tiled kernel: x half-row (32 points + pad) | gradient half-row
 constexpr int kClassCap = 16;       // constraints per var-disjoint class (2 per warp of an 8-warp CTA)
 
 // Build everything; path: 0 auto, 1 tiled, 2 global; precision 0 auto / 32 / 64.

@@ -37,11 +37,13 @@ struct FastBucketDev {
 };
 
 struct UnitDev {                 // a run of constraints of one bucket at positions [pos_begin, pos_begin + count)
-    int32_t bucket, count;       // (tiled path: a var-disjoint class)
-    int32_t kp, pad;             // literal words per constraint row of the bucket
-    int64_t pos_begin;
-    int64_t word_begin;          // first literal word of the unit (rows of kp words, contiguous)
+    int32_t bucket;              // (tiled path: a var-disjoint class); 16 bytes so a header prefetch is 4 registers
+    int32_t count_kp;            // count | kp << 16 (kp = literal words per constraint row of the bucket)
+    int32_t pos_begin;
+    int32_t word_begin;          // first literal word of the unit (rows of kp words, contiguous)
 };
+__device__ __forceinline__ int unit_count(const UnitDev& u) { return u.count_kp & 0xffff; }
+__device__ __forceinline__ int unit_kp(const UnitDev& u) { return u.count_kp >> 16; }
 
 struct SymSigDev {
     int32_t k, Mp, tmin, tmax, parity, pad;

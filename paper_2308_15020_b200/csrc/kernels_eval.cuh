@@ -116,7 +116,9 @@ struct TiledArgs {
     int32_t* upart;              // [n_chunks][B]
 };
 
-constexpr int kPitch = 33;       // == kTilePitch of host.hpp (row pitch of the smem tiles)
+constexpr int kHalf = 33;        // points per tile half-row + 1 pad
+constexpr int kPitch = 2 * kHalf; // == kTilePitch of host.hpp: row v = [x[v][0..32] | G[v][0..32]] (interleaved
+                                  // so a literal's gradient slot is its x slot + kHalf: one address, two offsets)
 
 __device__ __forceinline__ float flip_sign(float v, uint32_t w) { return __int_as_float(__float_as_int(v) ^ (int)(w & 0x80000000u)); }
 __device__ __forceinline__ double flip_sign(double v, uint32_t w) {
@@ -235,6 +237,120 @@ __device__ __forceinline__ void load_words_smem(const uint32_t* sp, uint32_t (&w
         if (i + 3 < K) w[i + 3] = q.w;
     }
 }
+// Same, but an opaque (volatile) shared load the compiler cannot merge with an earlier load of the same
+// words: used to re-read a row instead of keeping it live in registers across the forward pass.
+template <int K>
+__device__ __forceinline__ void reload_words_smem(const uint32_t* sp, uint32_t (&w)[K]) {
+    const uint32_t a = (uint32_t)__cvta_generic_to_shared(sp);
+#pragma unroll
+    for (int i = 0; i < K; i += 4) {
+        uint32_t q0, q1, q2, q3;
+        asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(q0), "=r"(q1), "=r"(q2), "=r"(q3) : "r"(a + 4 * i));
+        w[i] = q0;
+        if (i + 1 < K) w[i + 1] = q1;
+        if (i + 2 < K) w[i + 2] = q2;
+        if (i + 3 < K) w[i + 3] = q3;
+    }
+}
+
+// Two constraints of one (var-disjoint) unit for one lane, fp32: the pair's factor / prefix / suffix
+// chains run side by side in packed f32x2 instructions (FFMA2 / FMUL2, sm_100), which issue two fp32
+// lanes of work per instruction slot.  Arithmetic is element-wise identical to tiled_clause (round-to-
+// nearest fma / mul per element), so results do not depend on how constraints were paired.
+template <int K, int NCH>
+__device__ __forceinline__ void tiled_clause_pair(const BucketReg<float>& bk, const uint32_t* sw0, const uint32_t* sw1,
+                                                  float wc0, float wc1, const float* xl, float* gl, double& facc, int& uacc) {
+    float2 av[K], pre[K];
+    float2 fe = make_float2(bk.g0, bk.g0);
+    uint32_t t0 = 0, t1 = 0;
+    {
+        uint32_t w0[K], w1[K];
+        load_words_smem<K>(sw0, w0);
+        load_words_smem<K>(sw1, w1);
+        float2 xv[K];
+#pragma unroll
+        for (int i = 0; i < K; ++i) {
+            xv[i].x = *tile_at(xl, w0[i]);
+            xv[i].y = *tile_at(xl, w1[i]);
+            t0 += lit_true(xv[i].x, w0[i]);
+            t1 += lit_true(xv[i].y, w1[i]);
+        }
+        if (NCH >= 1) {
+            const float2 c0 = make_float2(bk.c0[0], bk.c0[0]);
+            float2 run = make_float2(1.0f, 1.0f);
+#pragma unroll
+            for (int i = 0; i < K; ++i) {
+                av[i] = __ffma2_rn(make_float2(flip_sign(bk.c1[0], w0[i]), flip_sign(bk.c1[0], w1[i])), xv[i], c0);
+                pre[i] = run;
+                run = __fmul2_rn(run, av[i]);
+            }
+            fe = __ffma2_rn(make_float2(bk.g[0], bk.g[0]), run, fe);
+        }
+        if (NCH == 2) {
+            // second channel: products of (c0' + c1' l) kept as the prefix / factor arrays of channel 1;
+            // channel 0's terms are folded into the gradient tile below before these are overwritten
+            float2 suf = make_float2(bk.g[0] * wc0, bk.g[0] * wc1);
+#pragma unroll
+            for (int i = K - 1; i >= 0; --i) {
+                const float2 cs = make_float2(flip_sign(bk.c1[0], w0[i]), flip_sign(bk.c1[0], w1[i]));
+                float* g0p = tile_at(gl, w0[i]);
+                float* g1p = tile_at(gl, w1[i]);
+                float2 gv = make_float2(*g0p, *g1p);
+                gv = __ffma2_rn(__fmul2_rn(pre[i], suf), cs, gv);
+                *g0p = gv.x;
+                *g1p = gv.y;
+                suf = __fmul2_rn(suf, av[i]);
+            }
+            const float2 c0 = make_float2(bk.c0[1], bk.c0[1]);
+            float2 run = make_float2(1.0f, 1.0f);
+#pragma unroll
+            for (int i = 0; i < K; ++i) {
+                av[i] = __ffma2_rn(make_float2(flip_sign(bk.c1[1], w0[i]), flip_sign(bk.c1[1], w1[i])), xv[i], c0);
+                pre[i] = run;
+                run = __fmul2_rn(run, av[i]);
+            }
+            fe = __ffma2_rn(make_float2(bk.g[1], bk.g[1]), run, fe);
+        }
+    }
+    if (NCH >= 1) {
+        // backward sweep of the last channel: literal words re-read from the stage buffer (broadcast LDS)
+        // so they need not stay live across the forward pass
+        constexpr int c = NCH - 1 > 0 ? NCH - 1 : 0;
+        uint32_t w0[K], w1[K];
+        reload_words_smem<K>(sw0, w0);
+        reload_words_smem<K>(sw1, w1);
+        float2 suf = make_float2(bk.g[c] * wc0, bk.g[c] * wc1);
+#pragma unroll
+        for (int i = K - 1; i >= 0; --i) {
+            const float2 cs = make_float2(flip_sign(bk.c1[c], w0[i]), flip_sign(bk.c1[c], w1[i]));
+            float* g0p = tile_at(gl, w0[i]);
+            float* g1p = tile_at(gl, w1[i]);
+            float2 gv = make_float2(*g0p, *g1p);
+            gv = __ffma2_rn(__fmul2_rn(pre[i], suf), cs, gv);
+            *g0p = gv.x;
+            *g1p = gv.y;
+            suf = __fmul2_rn(suf, av[i]);
+        }
+    }
+    facc += (double)(wc0 * fe.x);
+    facc += (double)(wc1 * fe.y);
+    uacc += rule_sat((int)t0, bk.tmin, bk.tmax, bk.parity) ? 0 : 1;
+    uacc += rule_sat((int)t1, bk.tmin, bk.tmax, bk.parity) ? 0 : 1;
+}
+
+template <typename T, int K, int NCH>
+__device__ __forceinline__ void tiled_pair(const BucketReg<T>& bk, const uint32_t* sw0, const uint32_t* sw1, T wc0, T wc1,
+                                           const T* xl, T* gl, double& facc, int& uacc) {
+    if constexpr (sizeof(T) == 4) {
+        tiled_clause_pair<K, NCH>(bk, sw0, sw1, wc0, wc1, xl, gl, facc, uacc);
+    } else {
+        uint32_t w0[K], w1[K];
+        load_words_smem<K>(sw0, w0);
+        tiled_clause<T, K, NCH>(bk, w0, wc0, xl, gl, facc, uacc);
+        load_words_smem<K>(sw1, w1);
+        tiled_clause<T, K, NCH>(bk, w1, wc1, xl, gl, facc, uacc);
+    }
+}
 
 // ---- unit staging: while a unit is processed, the next unit's literal words and weights are copied
 //      global -> shared with cp.async (LDGSTS) into the other half of a double buffer.
@@ -262,32 +378,33 @@ struct TileStage {
 
 template <typename T>
 __device__ __forceinline__ void stage_unit(const TiledArgs<T>& a, const UnitDev& U, TileStage<T>& st, int buf) {
-    const int nwords = min(U.count * U.kp, kStageWords);
+    const int nwords = min(unit_count(U) * unit_kp(U), kStageWords);
     const int t = threadIdx.x;
-    if (t * 4 < nwords) cp_async16(&st.words[buf][t * 4], a.words + U.word_begin + t * 4);
+    if (t * 4 < nwords) cp_async16(&st.words[buf][t * 4], a.words + (int64_t)U.word_begin + t * 4);
     const int c = t - 64;
-    if (c >= 0 && c < min(U.count, kStageCons)) cp_async_small<sizeof(T)>(&st.w[buf][c], a.w_pos + U.pos_begin + c);
+    if (c >= 0 && c < min(unit_count(U), kStageCons)) cp_async_small<sizeof(T)>(&st.w[buf][c], a.w_pos + (int64_t)U.pos_begin + c);
 }
 
-// Pipeline state: `cur` is being processed from stage buffer `buf`; `next` is staged (or in flight).
+// Pipeline state: unit `u` (header `cur`) is processed from stage buffer `buf`; unit u + 1 (`next`) is
+// staged or in flight into buf ^ 1; the header of unit u + 2 (`after`) is a register prefetch issued a
+// whole unit before it is needed.
 struct UnitPipe {
-    UnitDev cur, next;
+    UnitDev cur, next, after;
     int u, buf;
 };
 
-// Advance past `cur`: stage `next`'s successor ... (called by all threads after processing `cur`).
+// Advance past `cur` (all threads, after processing it).
 template <typename T>
 __device__ __forceinline__ void pipe_advance(const TiledArgs<T>& a, UnitPipe& P, int u1, TileStage<T>& st) {
     cp_async_wait_all();
     __syncthreads();          // next's words are visible; everybody is done with cur's buffer
     P.u += 1;
     P.cur = P.next;
+    P.next = P.after;
     P.buf ^= 1;
-    if (P.u + 1 < u1) {
-        P.next = a.units[P.u + 1];
-        stage_unit<T>(a, P.next, st, P.buf ^ 1);
-    }
+    if (P.u + 1 < u1) stage_unit<T>(a, P.next, st, P.buf ^ 1);
     cp_async_commit();
+    if (P.u + 2 < u1) P.after = a.units[P.u + 2];
 }
 
 // A run of consecutive units of one bucket: for each unit the warp takes constraints j = warp,
@@ -299,15 +416,10 @@ __device__ __forceinline__ void tiled_run(const TiledArgs<T>& a, int bucket, con
     while (P.u < u1 && P.cur.bucket == bucket) {
         const uint32_t* sw = st.words[P.buf];
         const T* swt = st.w[P.buf];
-        const int count = P.cur.count;
+        const int count = unit_count(P.cur);
         int j = warp;
-        for (; j + nw < count; j += 2 * nw) {
-            uint32_t w0[K], w1[K];
-            load_words_smem<K>(sw + j * K_PAD(K), w0);
-            load_words_smem<K>(sw + (j + nw) * K_PAD(K), w1);
-            tiled_clause<T, K, NCH>(bk, w0, swt[j], xl, gl, facc, uacc);
-            tiled_clause<T, K, NCH>(bk, w1, swt[j + nw], xl, gl, facc, uacc);
-        }
+        for (; j + nw < count; j += 2 * nw)
+            tiled_pair<T, K, NCH>(bk, sw + j * K_PAD(K), sw + (j + nw) * K_PAD(K), swt[j], swt[j + nw], xl, gl, facc, uacc);
         if (j < count) {
             uint32_t w0[K];
             load_words_smem<K>(sw + j * K_PAD(K), w0);
@@ -322,9 +434,9 @@ __device__ void tiled_run_long(const TiledArgs<T>& a, int bucket, const BucketRe
                                const T* xl, T* gl, int warp, int nw, double& facc, int& uacc) {
     const int k = bk.k;
     while (P.u < u1 && P.cur.bucket == bucket) {
-        for (int j = warp; j < P.cur.count; j += nw) {
-            const int64_t pos = P.cur.pos_begin + j;
-            const uint32_t* wp = a.words + P.cur.word_begin + (int64_t)j * P.cur.kp;
+        for (int j = warp; j < unit_count(P.cur); j += nw) {
+            const int64_t pos = (int64_t)P.cur.pos_begin + j;
+            const uint32_t* wp = a.words + (int64_t)P.cur.word_begin + (int64_t)j * unit_kp(P.cur);
             uint32_t t = 0;
             for (int i = 0; i < k; ++i) {
                 uint32_t w = __ldg(wp + i);
@@ -371,13 +483,15 @@ __device__ __forceinline__ void tiled_run_dispatch(const TiledArgs<T>& a, int bu
 // so the 8 warps add their literal terms straight into the shared gradient tile without races; a
 // barrier separates classes.  Every (variable, point) entry is therefore accumulated in one fixed order
 // (class order, then literal order) -- deterministic without atomics (the paper's atomicAdd).
-template <typename T, int KMAX>
+// KONLY > 0: every unit has k == KONLY and one product channel (the uniform k-CNF / k-XOR case), so the
+// run loop is instantiated for that k alone (no dispatch; registers sized for one k).
+template <typename T, int KMAX, int KONLY = 0>
 __global__ void __launch_bounds__(256, (sizeof(T) == 4 ? (KMAX <= 8 ? 4 : 2) : (KMAX <= 8 ? 2 : 1))) fast_tiled_kernel(TiledArgs<T> a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];   // >= 3 KB (host: tiled_smem_bytes)
     __shared__ __align__(16) TileStage<T> st;
     const int n = a.n;
-    T* xs = reinterpret_cast<T*>(smem_raw);                 // [n][kPitch]
-    T* Gs = xs + (size_t)n * kPitch;                        // [n][kPitch]
+    T* xs = reinterpret_cast<T*>(smem_raw);                 // [n][kPitch]: x half-rows
+    T* Gs = xs + kHalf;                                     //              gradient half-rows
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
     const int64_t b0 = (int64_t)blockIdx.x * 32;
     const int64_t b = b0 + lane;
@@ -394,7 +508,7 @@ __global__ void __launch_bounds__(256, (sizeof(T) == 4 ? (KMAX <= 8 ? 4 : 2) : (
     double facc = 0.0;
     int uacc = 0;
     const T* xl = xs + lane;
-    T* gl = Gs + lane;
+    T* gl = xs + kHalf + lane;
     const int u0 = a.chunk_units[chunk], u1 = a.chunk_units[chunk + 1];
     UnitPipe P;
     P.u = u0;
@@ -406,14 +520,19 @@ __global__ void __launch_bounds__(256, (sizeof(T) == 4 ? (KMAX <= 8 ? 4 : 2) : (
             P.next = a.units[u0 + 1];
             stage_unit<T>(a, P.next, st, 1);
         }
+        if (u0 + 2 < u1) P.after = a.units[u0 + 2];
     }
     cp_async_commit_wait_all();
     __syncthreads();
     while (P.u < u1) {
         const int bucket = P.cur.bucket;
         const FastBucketDev* bp = a.buckets + bucket;
-        const int nch = bp->nch;
         const BucketReg<T> bk = load_bucket<T>(bp);
+        if constexpr (KONLY > 0) {
+            tiled_run<T, KONLY, 1>(a, bucket, bk, P, u1, st, xl, gl, warp, nw, facc, uacc);
+            continue;
+        }
+        const int nch = bp->nch;
         if (nch == 1) tiled_run_dispatch<T, 1, KMAX>(a, bucket, bk, P, u1, st, xl, gl, warp, nw, facc, uacc);
         else if (nch == 2) tiled_run_dispatch<T, 2, KMAX>(a, bucket, bk, P, u1, st, xl, gl, warp, nw, facc, uacc);
         else tiled_run_dispatch<T, 0, KMAX>(a, bucket, bk, P, u1, st, xl, gl, warp, nw, facc, uacc);
@@ -552,7 +671,7 @@ __global__ void __launch_bounds__(256) fast_global_kernel(GlobalArgs<T> a) {
     for (int u = a.chunk_units[chunk]; u < a.chunk_units[chunk + 1]; ++u) {
         const UnitDev U = a.units[u];
         const FastBucketDev bk = a.buckets[U.bucket];
-        for (int64_t pos = U.pos_begin + warp; pos < U.pos_begin + U.count; pos += nw) {
+        for (int64_t pos = (int64_t)U.pos_begin + warp; pos < (int64_t)U.pos_begin + unit_count(U); pos += nw) {
             if (bk.nch == 1) global_clause_dispatch<T, 1, KMAX>(a, bk, pos, b, bv, facc, uacc);
             else if (bk.nch == 2) global_clause_dispatch<T, 2, KMAX>(a, bk, pos, b, bv, facc, uacc);
             else global_clause_dispatch<T, 0, KMAX>(a, bk, pos, b, bv, facc, uacc);
@@ -752,32 +871,49 @@ struct ReduceArgs {
     T* grad;                     // [B][n]
 };
 
-// block (32, 8): tile of 32 variables x 32 points
+// block (32, 8): 32 points x 8 variables, one (variable, point) sum per thread: the chunk partials in
+// chunk order, then the variable's occurrence slots in ascending order (fp64 accumulator; loads are
+// issued 8 / 4 ahead but added strictly in order, so the sum order is fixed).  Output through smem so
+// each point row gets 8 consecutive gradient entries.
 template <typename T>
 __global__ void __launch_bounds__(256) reduce_grad_kernel(ReduceArgs<T> a) {
-    __shared__ T tile[32][33];
+    __shared__ T tile[8][33];
     const int tx = threadIdx.x, ty = threadIdx.y;
-    const int64_t b0 = (int64_t)blockIdx.x * 32, v0 = (int64_t)blockIdx.y * 32;
-    const int64_t b = b0 + tx;
+    const int64_t b0 = (int64_t)blockIdx.y * 32, v0 = (int64_t)blockIdx.x * 8;   // grid.x over variables (n may exceed 65535 tiles)
+    const int64_t b = b0 + tx, v = v0 + ty;
+    double acc = 0.0;
+    if (v < a.n && b < a.B) {
+        const int64_t stride = (int64_t)a.n * a.B;
+        const T* p = a.P + v * a.B + b;
+        int c = 0;
+        for (; c + 8 <= a.n_chunks; c += 8) {
+            T t[8];
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-        const int vl = ty + 8 * j;
-        const int64_t v = v0 + vl;
-        double acc = 0.0;
-        if (v < a.n && b < a.B) {
-            for (int c = 0; c < a.n_chunks; ++c) acc += (double)a.P[((int64_t)c * a.n + v) * a.B + b];
-            const int64_t e = a.occ_off[v + 1];
-            for (int64_t o = a.occ_off[v]; o < e; ++o) acc += (double)a.Tb[(int64_t)a.occ_slot[o] * a.B + b];
+            for (int j = 0; j < 8; ++j) t[j] = p[(int64_t)(c + j) * stride];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) acc += (double)t[j];
         }
-        tile[vl][tx] = (T)acc;
-    }
-    __syncthreads();
+        for (; c < a.n_chunks; ++c) acc += (double)p[(int64_t)c * stride];
+        int64_t o = a.occ_off[v];
+        const int64_t e = a.occ_off[v + 1];
+        for (; o + 4 <= e; o += 4) {
+            int32_t sl[4];
+            T t[4];
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-        const int bl = ty + 8 * j;
-        const int64_t bb = b0 + bl, v = v0 + tx;
-        if (bb < a.B && v < a.n) a.grad[bb * a.n + v] = tile[tx][bl];
+            for (int j = 0; j < 4; ++j) sl[j] = a.occ_slot[o + j];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) t[j] = a.Tb[(int64_t)sl[j] * a.B + b];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) acc += (double)t[j];
+        }
+        for (; o < e; ++o) acc += (double)a.Tb[(int64_t)a.occ_slot[o] * a.B + b];
     }
+    tile[ty][tx] = (T)acc;
+    __syncthreads();
+    const int t = ty * 32 + tx;
+    const int pl = t >> 3, vl = t & 7;
+    const int64_t bb = b0 + pl, vv = v0 + vl;
+    if (bb < a.B && vv < a.n) a.grad[bb * a.n + vv] = tile[vl][pl];
 }
 
 struct ReduceFArgs {
@@ -792,36 +928,37 @@ struct ReduceFArgs {
     int32_t* unsat;              // [B] or null
 };
 
-// one CTA (128 threads) per point: thread t sums rows t, t + 128, ... in ascending order, then a fixed
-// shared-memory tree -- a fixed summation order for any launch (deterministic, no atomics).
-static __global__ void __launch_bounds__(128) reduce_f_kernel(ReduceFArgs a) {
-    __shared__ double sf[128];
-    __shared__ int su[128];
-    const int64_t b = blockIdx.x;
-    const int t = threadIdx.x;
+// one CTA (256 threads) per 32 points: lane = point, warp w sums rows w, w + 8, ... in ascending order,
+// then the 8 warp sums are added in warp order -- a fixed summation order (deterministic, no atomics).
+static __global__ void __launch_bounds__(256) reduce_f_kernel(ReduceFArgs a) {
+    __shared__ double sf[8][32];
+    __shared__ int su[8][32];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int64_t b = (int64_t)blockIdx.x * 32 + lane;
     double f = 0.0;
     int u = 0;
-    for (int c = t; c < a.n_parts; c += 128) {
-        f += a.fpart[(int64_t)c * a.B + b];
-        u += a.upart[(int64_t)c * a.B + b];
-    }
-    for (int64_t s = t; s < a.n_sym; s += 128) {
-        f += a.fsym[s * a.B + b];
-        u += a.usym[s * a.B + b];
-    }
-    sf[t] = f;
-    su[t] = u;
-    __syncthreads();
-    for (int h = 64; h > 0; h >>= 1) {
-        if (t < h) {
-            sf[t] += sf[t + h];
-            su[t] += su[t + h];
+    if (b < a.B) {
+        for (int c = w; c < a.n_parts; c += 8) {
+            f += a.fpart[(int64_t)c * a.B + b];
+            u += a.upart[(int64_t)c * a.B + b];
         }
-        __syncthreads();
+        for (int64_t s = w; s < a.n_sym; s += 8) {
+            f += a.fsym[s * a.B + b];
+            u += a.usym[s * a.B + b];
+        }
     }
-    if (t == 0) {
-        a.f[b] = sf[0];
-        if (a.unsat) a.unsat[b] = su[0];
+    sf[w][lane] = f;
+    su[w][lane] = u;
+    __syncthreads();
+    if (w == 0 && b < a.B) {
+        double ft = 0.0;
+        int ut = 0;
+        for (int j = 0; j < 8; ++j) {
+            ft += sf[j][lane];
+            ut += su[j][lane];
+        }
+        a.f[b] = ft;
+        if (a.unsat) a.unsat[b] = ut;
     }
 }
 

@@ -142,44 +142,84 @@ __global__ void __launch_bounds__(256) pgd_step_kernel(PgdArgs a) {
     if (threadIdx.x == 0) a.dot[b] = red[0];
 }
 
-// sgn(x) check: one warp per constraint (position order), lanes over points.
+// sgn(x) check (Alg. 1 line 5): exact integer count t of True literals per (constraint, point).
+// CTA = 32 points (lane = point) x a contiguous range of constraints (warp = constraint).  The point
+// values come from a shared-memory tile [n][33] (SMEM = true, small n) or from the transposed copy
+// xT [n][B] (coalesced 128-byte rows, large n).  U[c] += #points of this tile falsifying c (warp ballot +
+// popc, one integer atomic per warp-constraint); unsat[b] += this CTA's count (one integer atomic per
+// point).  Integer atomics: the totals are exact and order-independent.  U and unsat are zeroed before.
 struct CheckArgs {
-    const void* X;      // [B][n]
+    const void* X;      // [B][n] (SMEM) or xT [n][B]
     int64_t B;
     int32_t n;
     int64_t m;
+    int64_t cons_per_cta;
     const int64_t* off;       // [m + 1] position-order literal offsets into words
     const uint32_t* words;    // var | neg << 31
     const int32_t* rule;      // [m][3]
     int32_t* U;               // [m]
-    int32_t* unsat;           // [B] (zeroed before)
+    int32_t* unsat;           // [B]
 };
 
-template <typename T>
+template <typename T, bool SMEM>
 __global__ void __launch_bounds__(256) check_kernel(CheckArgs a) {
-    const int lane = threadIdx.x & 31;
-    const int64_t c = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
-    if (c >= a.m) return;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    __shared__ int ucnt[8][32];
     const T* X = reinterpret_cast<const T*>(a.X);
-    const int64_t lo = a.off[c], hi = a.off[c + 1];
-    const int tmin = a.rule[3 * c], tmax = a.rule[3 * c + 1], par = a.rule[3 * c + 2];
-    int cnt = 0;
-    for (int64_t b0 = 0; b0 < a.B; b0 += 32) {
-        const int64_t b = b0 + lane;
-        bool unsat = false;
-        if (b < a.B) {
-            int t = 0;
-            for (int64_t i = lo; i < hi; ++i) {
-                uint32_t w = __ldg(a.words + i);
-                T xv = X[b * a.n + (w & 0x7fffffffu)];
-                t += (int)((xv < (T)0) != (bool)(w >> 31));
-            }
-            unsat = !rule_sat(t, tmin, tmax, par);
-            if (unsat) atomicAdd(a.unsat + b, 1);
+    T* xs = reinterpret_cast<T*>(smem_raw);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t b0 = (int64_t)blockIdx.x * 32, b = b0 + lane;
+    const bool bv = b < a.B;
+    if (SMEM) {
+        for (int idx = threadIdx.x; idx < 32 * a.n; idx += blockDim.x) {
+            const int r = idx / a.n, v = idx - r * a.n;
+            xs[v * 33 + r] = b0 + r < a.B ? X[(b0 + r) * a.n + v] : (T)0;
         }
-        cnt += __popc(__ballot_sync(0xffffffffu, unsat));
+        __syncthreads();
     }
-    if (lane == 0) a.U[c] = cnt;
+    const int64_t c0 = (int64_t)blockIdx.y * a.cons_per_cta;
+    const int64_t c1 = min(a.m, c0 + a.cons_per_cta);
+    int mine = 0;
+    for (int64_t c = c0 + warp; c < c1; c += 8) {
+        const int64_t lo = a.off[c], hi = a.off[c + 1];
+        int t = 0;
+        for (int64_t i = lo; i < hi; ++i) {
+            const uint32_t w = __ldg(a.words + i);
+            const uint32_t v = w & 0x7fffffffu;
+            const T xv = SMEM ? xs[v * 33 + lane] : (bv ? X[(int64_t)v * a.B + b] : (T)0);
+            t += (int)((xv < (T)0) != ((int)w < 0));
+        }
+        const bool uns = bv && !rule_sat(t, a.rule[3 * c], a.rule[3 * c + 1], a.rule[3 * c + 2]);
+        mine += uns ? 1 : 0;
+        const int cnt = __popc(__ballot_sync(0xffffffffu, uns));
+        if (lane == 0 && cnt) atomicAdd(a.U + c, cnt);
+    }
+    ucnt[warp][lane] = mine;
+    __syncthreads();
+    if (warp == 0 && bv) {
+        int tot = 0;
+        for (int w = 0; w < 8; ++w) tot += ucnt[w][lane];
+        if (tot) atomicAdd(a.unsat + b, tot);
+    }
+}
+
+// X [B][n] -> xT [n][B] for the large-n check (32 x 32 tiles through smem)
+template <typename T>
+__global__ void __launch_bounds__(256) transpose_search_kernel(const T* __restrict__ x, T* __restrict__ xT, int64_t B, int32_t n) {
+    __shared__ T tile[32][33];
+    const int tx = threadIdx.x, ty = threadIdx.y;
+    const int64_t v0 = (int64_t)blockIdx.x * 32, b0 = (int64_t)blockIdx.y * 32;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        const int64_t bb = b0 + ty + 8 * j, v = v0 + tx;
+        if (bb < B && v < n) tile[ty + 8 * j][tx] = x[bb * n + v];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        const int64_t v = v0 + ty + 8 * j, bb = b0 + tx;
+        if (bb < B && v < n) xT[v * B + bb] = tile[tx][ty + 8 * j];
+    }
 }
 
 // ERWA (single block): maxU, then w = (1 - alpha) w + alpha U / maxU

@@ -24,3 +24,21 @@ for what in ("check", "restart", "begin_round"):
     for _ in range(20): getattr(s, what)()
     t1 = time.perf_counter(); e1.record(); torch.cuda.synchronize()
     print(f"{what}: enqueue {1e6*(t1-t0)/20:.1f} us, gpu {1e3*e0.elapsed_time(e1)/20:.1f} us")
+# replicate bench.py's timed loop (flush + per-step events + round end every 10 steps)
+flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
+T = s.tensors()
+flag = torch.zeros(1, dtype=torch.int32, device="cuda")
+for use_flush in (True, False):
+    evs = []
+    torch.cuda.synchronize(); t0 = time.perf_counter()
+    for i in range(50):
+        if use_flush: flush.zero_()
+        a0 = torch.cuda.Event(enable_timing=True); a1 = torch.cuda.Event(enable_timing=True)
+        a0.record()
+        s.iterate(1)
+        if (i + 1) % 10 == 0:
+            s.check(); flag.copy_((T["unsat"].min() == 0).to(torch.int32).view(1)); s.restart(T["U"]); s.begin_round()
+        a1.record(); evs.append((a0, a1))
+    torch.cuda.synchronize(); t1 = time.perf_counter()
+    ev = [x.elapsed_time(y) for x, y in evs]
+    print(f"bench loop flush={use_flush}: events mean {1e3*sum(ev)/len(ev):.1f} us/step (min {1e3*min(ev):.1f} max {1e3*max(ev):.1f}), wall {1e6*(t1-t0)/50:.1f} us/step")
