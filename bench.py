@@ -315,7 +315,7 @@ def main():
         kms = fast_ms
         peak = SM_COUNT * FP32_LANES * 2 * mhz * 1e6 / 1e12 if info["precision"] == 32 else SM_COUNT * FP64_LANES * 2 * mhz * 1e6 / 1e12
     else:
-        kname = "sym_kernel"
+        kname = "sym_group_kernel"
         flops = ROOT_FLOPS_PER_LIT_ROOT * info["sym_root_lits"] * B
         kms = root_ms
         lanes = FP64_LANES if info["precision"] == 64 else FP32_LANES

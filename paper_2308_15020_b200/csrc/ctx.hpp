@@ -56,6 +56,8 @@ inline unsigned blocks_for(int64_t n, int t) { return (unsigned)((n + t - 1) / t
 
 }  // namespace ffsat
 
+#define FFSAT_SIDE_STREAMS 4
+
 struct ffsat_ctx {
     ffsat::Formula F;
     ffsat::Layout Lo;
@@ -74,9 +76,26 @@ struct ffsat_ctx {
     size_t tiled_smem = 0;
     int64_t launches = 0;
     cudaEvent_t ev[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
+    // side streams for the concurrent root-path classes (fork / join through events, graph-capturable)
+    cudaStream_t side[FFSAT_SIDE_STREAMS] = {};
+    cudaEvent_t ev_fork = nullptr, ev_join[FFSAT_SIDE_STREAMS] = {};
+    bool pending_join[FFSAT_SIDE_STREAMS] = {};
+    void ensure_side_streams() {
+        if (ev_fork) return;
+        for (int i = 0; i < FFSAT_SIDE_STREAMS; ++i) {
+            CK(cudaStreamCreateWithFlags(&side[i], cudaStreamNonBlocking));
+            CK(cudaEventCreateWithFlags(&ev_join[i], cudaEventDisableTiming));
+        }
+        CK(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming));
+    }
     ~ffsat_ctx() {
         for (cudaEvent_t& e : ev)
             if (e) cudaEventDestroy(e);
+        for (int i = 0; i < FFSAT_SIDE_STREAMS; ++i) {
+            if (side[i]) cudaStreamDestroy(side[i]);
+            if (ev_join[i]) cudaEventDestroy(ev_join[i]);
+        }
+        if (ev_fork) cudaEventDestroy(ev_fork);
     }
 };
 

@@ -36,16 +36,29 @@ inline int fast_kmax(const Layout& L) {
     return km;
 }
 
+inline void set_sym_smem(const void* kern, size_t bytes) {
+    if (bytes > 48 * 1024) CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+}
+
+// One root-path class launch: a CTA of G threads per (constraint, point) item, C literals per thread.
 template <typename T>
-void launch_sym_class(ffsat_ctx* c, const SymClass& cl, const dev::SymArgs<T>& a, cudaStream_t st) {
-    const int64_t groups = (cl.end - cl.begin) * a.B;
-    switch (cl.G) {
-    case 32: dev::sym_kernel<T, 32><<<blocks_for(groups, 8), 256, 0, st>>>(a, cl.begin, cl.end); break;
-    case 64: dev::sym_kernel<T, 64><<<(unsigned)groups, 64, 0, st>>>(a, cl.begin, cl.end); break;
-    case 128: dev::sym_kernel<T, 128><<<(unsigned)groups, 128, 0, st>>>(a, cl.begin, cl.end); break;
-    case 256: dev::sym_kernel<T, 256><<<(unsigned)groups, 256, 0, st>>>(a, cl.begin, cl.end); break;
-    case 512: dev::sym_kernel<T, 512><<<(unsigned)groups, 512, 0, st>>>(a, cl.begin, cl.end); break;
-    default: throw Error(FFSAT_ERR_ARG, "unsupported group size");
+void launch_sym_class(const SymClass& cl, const dev::SymArgs<T>& a, cudaStream_t st) {
+    const int64_t items = (cl.end - cl.begin) * a.B;
+    if (items == 0) return;
+    if (items > INT32_MAX) throw Error(FFSAT_ERR_ARG, "too many root-path items for one launch");
+    const unsigned g = (unsigned)items;
+    const size_t smem = (size_t)cl.max_mp * 8 * sizeof(T);   // the root table of the longest signature
+    switch (cl.G / 32 * 1000 + cl.C * 10 + cl.R) {
+#define FFSAT_SYM(NW, C, R) case NW * 1000 + C * 10 + R: \
+        set_sym_smem((const void*)dev::sym_item_kernel<T, NW, C, R>, smem); \
+        dev::sym_item_kernel<T, NW, C, R><<<g, 32 * NW, smem, st>>>(a, cl.begin); break;
+        FFSAT_SYM(1, 1, 1) FFSAT_SYM(1, 4, 1)
+        FFSAT_SYM(1, 16, 1) FFSAT_SYM(2, 16, 1) FFSAT_SYM(4, 16, 1) FFSAT_SYM(6, 16, 1) FFSAT_SYM(8, 16, 1)
+        FFSAT_SYM(1, 12, 2) FFSAT_SYM(2, 12, 2) FFSAT_SYM(4, 12, 2) FFSAT_SYM(6, 12, 2) FFSAT_SYM(8, 12, 2)
+        FFSAT_SYM(1, 16, 2) FFSAT_SYM(2, 16, 2) FFSAT_SYM(4, 16, 2) FFSAT_SYM(6, 16, 2) FFSAT_SYM(8, 16, 2)
+        FFSAT_SYM(1, 8, 2) FFSAT_SYM(2, 8, 2) FFSAT_SYM(4, 8, 2) FFSAT_SYM(6, 8, 2) FFSAT_SYM(8, 8, 2)
+#undef FFSAT_SYM
+    default: throw Error(FFSAT_ERR_ARG, "unsupported root-path launch class");
     }
 }
 
@@ -61,6 +74,43 @@ void eval_device_t(ffsat_ctx* c, const T* x, int64_t B, double* f, T* grad, int3
         if (profiled) CK(cudaEventRecord(c->ev[i], st));
     };
     mark(0);
+    // root-path classes are independent of the fast kernel (disjoint outputs): off the profiling path they
+    // run on forked side streams, concurrently with each other and with the fast kernel
+    auto launch_sym_all = [&]() {
+        if (L.n_sym == 0) return;
+        dev::SymArgs<T> a{};
+        a.x = x; a.sb = L.n; a.sv = 1; a.B = B;
+        a.words = c->sym_words.as<uint32_t>(); a.off = c->sym_off.as<int64_t>(); a.sig_of = c->sym_sig.as<int32_t>();
+        a.sigs = c->sigs.as<dev::SymSigDev>(); a.coef = c->coef.as<T>(); a.w_sym = w_pos + L.n_fast;
+        a.tb_fast = L.tb_fast; a.Tb = c->Tb.as<T>(); a.fsym = c->fsym.as<double>(); a.usym = c->usym.as<int32_t>();
+        const size_t ncl = L.sym_classes.size();
+        const bool fork = !profiled && (ncl > 1 || L.n_fast > 0);
+        if (fork) {
+            c->ensure_side_streams();
+            CK(cudaEventRecord(c->ev_fork, st));
+        }
+        for (size_t i = 0; i < ncl; ++i) {
+            cudaStream_t ss = fork ? c->side[i % FFSAT_SIDE_STREAMS] : st;
+            if (fork && i < FFSAT_SIDE_STREAMS) CK(cudaStreamWaitEvent(ss, c->ev_fork, 0));
+            launch_sym_class<T>(L.sym_classes[i], a, ss);
+            c->launches += 1;
+        }
+        CK(cudaGetLastError());
+        if (fork) {
+            for (size_t i = 0; i < std::min<size_t>(ncl, FFSAT_SIDE_STREAMS); ++i) {
+                CK(cudaEventRecord(c->ev_join[i], c->side[i]));
+                c->pending_join[i] = true;
+            }
+        }
+    };
+    auto join_sym = [&]() {
+        for (int i = 0; i < FFSAT_SIDE_STREAMS; ++i)
+            if (c->pending_join[i]) {
+                CK(cudaStreamWaitEvent(st, c->ev_join[i], 0));
+                c->pending_join[i] = false;
+            }
+    };
+    if (!profiled) launch_sym_all();
     if (L.n_fast > 0 && c->n_chunks > 0) {
         c->launches += L.path == 1 ? 1 : 2;
         if (L.path == 1) {
@@ -95,16 +145,8 @@ void eval_device_t(ffsat_ctx* c, const T* x, int64_t B, double* f, T* grad, int3
         CK(cudaGetLastError());
     }
     mark(1);
-    if (L.n_sym > 0) {
-        c->launches += (int64_t)L.sym_classes.size();
-        dev::SymArgs<T> a{};
-        a.x = x; a.sb = L.n; a.sv = 1; a.B = B;
-        a.words = c->sym_words.as<uint32_t>(); a.off = c->sym_off.as<int64_t>(); a.sig_of = c->sym_sig.as<int32_t>();
-        a.sigs = c->sigs.as<dev::SymSigDev>(); a.coef = c->coef.as<T>(); a.w_sym = w_pos + L.n_fast;
-        a.tb_fast = L.tb_fast; a.Tb = c->Tb.as<T>(); a.fsym = c->fsym.as<double>(); a.usym = c->usym.as<int32_t>();
-        for (const SymClass& cl : L.sym_classes) launch_sym_class<T>(c, cl, a, st);
-        CK(cudaGetLastError());
-    }
+    if (profiled) launch_sym_all();
+    join_sym();
     mark(2);
     if (grad) {
         c->launches += 1;

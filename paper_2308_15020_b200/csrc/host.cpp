@@ -7,6 +7,7 @@
 #include <cerrno>
 #include <climits>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <numeric>
 #include <sstream>
@@ -267,11 +268,31 @@ std::vector<int32_t> disjoint_classes(const std::vector<std::vector<int32_t>>& v
 
 // ------------------------------------------------------------------------------- A2: layout
 
+// Root path launch geometry: C literals per thread (1 for k <= 32, 4 for k <= 128, else the long-chunk
+// size) and R roots per pass, groups of 1..8 warps per (constraint, point) item.  Longer chunks amortise
+// the per-root scan across lanes; R = 2 interleaves two independent product chains.
+static int long_variant() {
+    static const int v = [] {
+        const char* e = std::getenv("FFSAT_SYM_VARIANT");   // development hook: 0 = C16/R1, 1 = C12/R2, 2 = C16/R2, 3 = C8/R2
+        return e ? std::atoi(e) : 0;
+    }();
+    return v;
+}
+int sym_chunk(int k) {
+    if (k <= 32) return 1;
+    if (k <= 128) return 4;
+    static const int C[4] = {16, 12, 16, 8};
+    return C[long_variant() & 3];
+}
+int sym_roots(int k) { return k <= 128 ? 1 : (long_variant() & 3) == 0 ? 1 : 2; }
 int sym_group(int k) {
-    int need = (k + 7) / 8;  // CK = 8 literals per thread at most (G <= 512: k <= 4096)
-    int G = 32;
-    while (G < need) G *= 2;
-    return G;
+    const int C = sym_chunk(k);
+    int nw = (k + 32 * C - 1) / (32 * C);
+    if (nw == 3) nw = 4;
+    if (nw == 5) nw = 6;
+    if (nw == 7) nw = 8;
+    if (nw > 8) throw Error(FFSAT_ERR_ARG, "root-path constraint too long for one thread group");
+    return 32 * nw;
 }
 
 Layout build_layout(const Formula& F, int path, int precision) {
@@ -306,8 +327,10 @@ Layout build_layout(const Formula& F, int path, int precision) {
         return ff[a].variant < ff[b].variant;
     });
     std::stable_sort(sym_ids.begin(), sym_ids.end(), [&](int64_t a, int64_t b) {
-        int ga = sym_group(klen(a)), gb = sym_group(klen(b));
-        if (ga != gb) return ga < gb;
+        const int ca = sym_chunk(klen(a)), cb = sym_chunk(klen(b));
+        if (ca != cb) return ca < cb;
+        const int ga = sym_group(klen(a)), gb = sym_group(klen(b));
+        if (ga != gb) return ga > gb;   // largest groups first (longest work first within a launch)
         return klen(a) > klen(b);
     });
 
@@ -417,9 +440,11 @@ Layout build_layout(const Formula& F, int path, int precision) {
         Lo.n_sym_lits += k;
         Lo.sym_root_lits += (int64_t)k * ((k + 1) / 2);
         Lo.sym_off.push_back(Lo.n_sym_lits);
-        int G = sym_group(k);
-        if (Lo.sym_classes.empty() || Lo.sym_classes.back().G != G) Lo.sym_classes.push_back({G, s, s + 1});
+        const int G = sym_group(k), C = sym_chunk(k), R = sym_roots(k);
+        if (Lo.sym_classes.empty() || Lo.sym_classes.back().G != G || Lo.sym_classes.back().C != C)
+            Lo.sym_classes.push_back({G, C, R, s, s + 1, 0});
         else Lo.sym_classes.back().end = s + 1;
+        Lo.sym_classes.back().max_mp = std::max(Lo.sym_classes.back().max_mp, (k + 1) / 2);
     }
 
     // ---- T-buffer slots and occurrence CSR (ascending slot order per variable)

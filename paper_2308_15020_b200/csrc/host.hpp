@@ -58,9 +58,10 @@ struct SymSig {                     // a (k, sat rule) signature with its root t
     double g0;
 };
 
-struct SymClass {                   // launch class: group size G threads per (constraint, point)
-    int32_t G;
+struct SymClass {                   // launch class: G threads per (constraint, point), C literals per thread
+    int32_t G, C, R;                // R roots per pass
     int64_t begin, end;             // sym constraint indices
+    int32_t max_mp;                 // largest M' in the class (root-table size staged in shared memory)
 };
 
 struct WorkUnit {                   // a run of fast constraints of one bucket, contiguous positions
@@ -70,6 +71,8 @@ struct WorkUnit {                   // a run of fast constraints of one bucket, 
 };
 
 int sym_group(int k);               // threads per (constraint, point) on the root path
+int sym_chunk(int k);               // literals per thread on the root path (G * C >= k)
+int sym_roots(int k);               // roots per pass on the root path
 
 struct Layout {
     int32_t n = 0, path = 0, precision = 32, max_k = 0;

@@ -7,7 +7,7 @@
 //                       the gradient tile, one class at a time (deterministic order, no float atomics;
 //                       the paper's atomicAdd P:318 is replaced).
 //   fast_global_kernel  same products for large n: x transposed [n][B], terms to T[slot][B] in HBM.
-//   sym_kernel<G>       root-of-unity product path (Alg. 2 / Eqs. 7-9, in the probability
+//   sym_group_kernel    root-of-unity product path (Alg. 2 / Eqs. 7-9, in the probability
 //                       basis of DESIGN.md) with the gradient from exclusive prefix/suffix products
 //                       (Prop. 1 / Eq. 10); G threads per (constraint, point) own literal
 //                       chunks and scan chunk products across the group (Prop. 2's log-depth schedule).
@@ -728,130 +728,203 @@ __device__ __forceinline__ cplx<T> shfl_c(const cplx<T>& v, int src) {
     return {__shfl_sync(0xffffffffu, v.re, src), __shfl_sync(0xffffffffu, v.im, src)};
 }
 
-template <typename T, int G>
-__global__ void __launch_bounds__(G == 32 ? 256 : G) sym_kernel(SymArgs<T> a, int64_t s_begin, int64_t s_end) {
-    constexpr int CK = 8;
-    constexpr int NWG = G / 32;  // warps per group
-    __shared__ cplx<T> wt[2][NWG > 1 ? NWG : 1];
-    __shared__ int tcnt[NWG > 1 ? NWG : 1];
-    const int lane = threadIdx.x & 31;
-    int64_t gid;
-    int t;
-    if (G == 32) {
-        gid = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
-        t = lane;
-    } else {
-        gid = blockIdx.x;
-        t = threadIdx.x;
-    }
-    const int64_t ncons = s_end - s_begin;
-    if (gid >= ncons * a.B) return;  // G == 32: whole warp exits together; G > 32: whole block
-    const int64_t s = s_begin + gid / a.B;
-    const int64_t b = gid - (gid / a.B) * a.B;
-    const SymSigDev sg = a.sigs[a.sig_of[s]];
-    const int k = sg.k;
-    const int64_t lo = a.off[s];
-    const int ck = (k + G - 1) / G;
-    const int i0 = t * ck;
+// Root path: one CTA of NW warps per (constraint c, point b) item; thread t owns the C consecutive
+// literals [t C, t C + C).  The item index comes from blockIdx alone, so the root loop is uniform and the
+// warp shuffles stay convergent.  Launch classes (NW, C) run on forked streams, concurrently with each
+// other and with the fast-path kernel, so short and long constraints share waves.  Per root m of the
+// Hermitian half spectrum (m = 1..M'):
+//   1. backward sweep in registers: factors phi_j = alpha_m + beta_m l_j (probability basis, #2)
+//      and exclusive in-chunk suffix products insuf_j; the chunk product;
+//   2. exclusive prefix P and suffix S of the chunk products across the group: warp Kogge-Stone scans
+//      with shuffles (Prop. 2's log-depth tree), then a named barrier of the group to
+//      combine warp totals (NW > 1);
+//   3. forward sweep: term_j += Re(A insuf_j) with A = H_m P S prod_{j' < j in chunk} phi_j'.
+// FE = g0 + Re sum_m G_m Q_m.  Each literal's term is owned by one thread: no cross-thread gradient sum.
+__device__ __forceinline__ void opaque(double& v) { asm volatile("" : "+d"(v)); }
+__device__ __forceinline__ void opaque(float& v) { asm volatile("" : "+f"(v)); }
 
-    T l[CK];
-    bool neg[CK];
-    int tc = 0;
+// alpha_m, beta_m of roots m .. m + R - 1 (the last root repeated past Mp; harmless prefetch)
+template <typename T, int R>
+__device__ __forceinline__ void load_ab(const T* cf, int m, int Mp, cplx<T> (&al)[R], cplx<T> (&be)[R]) {
 #pragma unroll
-    for (int j = 0; j < CK; ++j) {
-        int i = i0 + j;
-        l[j] = (T)0;
-        neg[j] = false;
-        if (j < ck && i < k) {
-            uint32_t w = __ldg(a.words + lo + i);
-            T xv = a.x[b * a.sb + (int64_t)(w & 0x7fffffffu) * a.sv];
-            neg[j] = w >> 31;
-            l[j] = neg[j] ? -xv : xv;
-            tc += (int)((xv < (T)0) != neg[j]);
-        }
+    for (int r = 0; r < R; ++r) {
+        const int mm = m + r < Mp ? m + r : Mp - 1;
+        al[r] = {cf[8 * mm + 0], cf[8 * mm + 1]};
+        be[r] = {cf[8 * mm + 2], cf[8 * mm + 3]};
     }
-    T term[CK];
-#pragma unroll
-    for (int j = 0; j < CK; ++j) term[j] = (T)0;
-    double fe_acc = 0.0;
-    const T* cf = a.coef + sg.coef_off * 8;
+}
+
+// R roots m .. m + R - 1 of one item (independent product chains interleaved for instruction-level
+// parallelism).  R == 1 keeps the factors phi_j in registers; R > 1 recomputes them in the forward sweep
+// (the registers go to the second chain instead).
+template <typename T, int NW, int C, int R>
+__device__ __forceinline__ void sym_roots(const T* cf, int m, int Mp, int lane, int warp, int t, const T (&l)[C], T (&term)[C],
+                                          double& fe_acc, cplx<T> (*wtot)[2][NW], cplx<T> (&al)[R], cplx<T> (&be)[R]) {
     const cplx<T> one{(T)1, (T)0};
-    const int warp = t >> 5;
-
-    for (int m = 0; m < sg.Mp; ++m) {
-        const cplx<T> al{__ldg(cf + 8 * m + 0), __ldg(cf + 8 * m + 1)};
-        const cplx<T> be{__ldg(cf + 8 * m + 2), __ldg(cf + 8 * m + 3)};
-        const cplx<T> Gm{__ldg(cf + 8 * m + 4), __ldg(cf + 8 * m + 5)};
-        const cplx<T> Hm{__ldg(cf + 8 * m + 6), __ldg(cf + 8 * m + 7)};
-        // backward within the chunk: insuf_j = prod_{j' > j in chunk} phi_j'
-        cplx<T> insuf[CK];
-        cplx<T> suf = one;
+    const int par = (m / R) & 1;
+    // 1. backward sweep: insuf_j = prod_{j' > j in chunk} phi_j'
+    cplx<T> insuf[R][C], suf[R], ph1[C];
 #pragma unroll
-        for (int j = CK - 1; j >= 0; --j) {
-            insuf[j] = suf;
-            if (j < ck && i0 + j < k) {
-                cplx<T> ph{fmaT(be.re, l[j], al.re), fmaT(be.im, l[j], al.im)};
-                suf = cmul(suf, ph);
-            }
-        }
-        // exclusive prefix / suffix of chunk products across the group (ordered by t)
-        cplx<T> ip = suf, is = suf;
+    for (int r = 0; r < R; ++r) suf[r] = one;
 #pragma unroll
-        for (int d = 1; d < 32; d <<= 1) {
-            cplx<T> y = shfl_up_c(ip, d);
-            if (lane >= d) ip = cmul(y, ip);
-            cplx<T> z = shfl_down_c(is, d);
-            if (lane + d < 32) is = cmul(is, z);
+    for (int j = C - 1; j >= 0; --j) {
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            const cplx<T> ph{fmaT(be[r].re, l[j], al[r].re), fmaT(be[r].im, l[j], al[r].im)};
+            if (R == 1) ph1[j] = ph;
+            insuf[r][j] = suf[r];
+            suf[r] = cmul(suf[r], ph);
         }
-        cplx<T> P = shfl_up_c(ip, 1), S = shfl_down_c(is, 1);
-        if (lane == 0) P = one;
-        if (lane == 31) S = one;
-        cplx<T> Q = shfl_c(ip, 31);
-        if (NWG > 1) {
-            if (lane == 31) wt[m & 1][warp] = ip;
-            __syncthreads();
-            cplx<T> Pw = one, Sw = one, Qa = one;
-            for (int w = 0; w < NWG; ++w) {
-                cplx<T> v = wt[m & 1][w];
-                Qa = cmul(Qa, v);
+    }
+    // next batch's factors, requested early (latency hidden by the scan and the forward sweep)
+    cplx<T> al_n[R], be_n[R];
+    load_ab<T, R>(cf, m + R, Mp, al_n, be_n);
+    // 2. exclusive prefix / suffix of the chunk products across the group
+    cplx<T> ip[R], is[R], P[R], S[R], Q[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) ip[r] = is[r] = suf[r];
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            const cplx<T> y = shfl_up_c(ip[r], d);
+            const cplx<T> z = shfl_down_c(is[r], d);
+            if (lane >= d) ip[r] = cmul(y, ip[r]);
+            if (lane + d < 32) is[r] = cmul(is[r], z);
+        }
+    }
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        P[r] = shfl_up_c(ip[r], 1);
+        S[r] = shfl_down_c(is[r], 1);
+        if (lane == 0) P[r] = one;
+        if (lane == 31) S[r] = one;
+        Q[r] = shfl_c(ip[r], 31);
+    }
+    if (NW > 1) {
+        if (lane == 31) {
+#pragma unroll
+            for (int r = 0; r < R; ++r) wtot[par][r][warp] = ip[r];
+        }
+        __syncthreads();
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            cplx<T> Pw = one, Sw = one;
+#pragma unroll
+            for (int w = 0; w < NW; ++w) {
+                const cplx<T> v = wtot[par][r][w];
                 if (w < warp) Pw = cmul(Pw, v);
                 if (w > warp) Sw = cmul(Sw, v);
             }
-            P = cmul(Pw, P);
-            S = cmul(S, Sw);
-            Q = Qa;
+            Q[r] = cmul(cmul(Pw, Q[r]), Sw);
+            P[r] = cmul(Pw, P[r]);
+            S[r] = cmul(S[r], Sw);
         }
-        // forward: pre = H P S prod_{j' < j in chunk} phi_j'; term_j += Re(pre * insuf_j)
-        cplx<T> pre = cmul(cmul(Hm, P), S);
+    }
+    // 3. forward sweep: term_j += Re(A insuf_j), A = H P S prod_{j' < j} phi_j'
+    cplx<T> A[R], alf[R], bef[R];
 #pragma unroll
-        for (int j = 0; j < CK; ++j) {
-            if (j < ck && i0 + j < k) {
-                term[j] = fmaT(pre.re, insuf[j].re, fmaT(-pre.im, insuf[j].im, term[j]));
-                cplx<T> ph{fmaT(be.re, l[j], al.re), fmaT(be.im, l[j], al.im)};
-                pre = cmul(pre, ph);
-            }
+    for (int r = 0; r < R; ++r) {
+        const cplx<T> Hm{cf[8 * (m + r) + 6], cf[8 * (m + r) + 7]};
+        A[r] = cmul(cmul(Hm, P[r]), S[r]);
+        alf[r] = al[r];
+        bef[r] = be[r];
+        if (R > 1) { opaque(alf[r].re); opaque(alf[r].im); opaque(bef[r].re); opaque(bef[r].im); }
+    }
+#pragma unroll
+    for (int j = 0; j < C; ++j) {
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            term[j] = fmaT(A[r].re, insuf[r][j].re, fmaT(-A[r].im, insuf[r][j].im, term[j]));
+            const cplx<T> ph = R == 1 ? ph1[j] : cplx<T>{fmaT(bef[r].re, l[j], alf[r].re), fmaT(bef[r].im, l[j], alf[r].im)};
+            A[r] = cmul(A[r], ph);
         }
-        if (t == 0) fe_acc += (double)Gm.re * (double)Q.re - (double)Gm.im * (double)Q.im;
+    }
+    if (t == 0) {
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            const T gre = cf[8 * (m + r) + 4], gim = cf[8 * (m + r) + 5];
+            fe_acc += (double)gre * (double)Q[r].re - (double)gim * (double)Q[r].im;
+        }
+    }
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        al[r] = al_n[r];
+        be[r] = be_n[r];
+    }
+}
+
+template <typename T, int NW, int C, int R>
+__global__ void __launch_bounds__(32 * NW, NW >= 8 ? 1 : 8 / NW) sym_item_kernel(SymArgs<T> a, int64_t s_begin) {
+    extern __shared__ __align__(16) unsigned char sym_smem[];   // the signature's root table, M' x 8 T
+    __shared__ cplx<T> wtot[2][2][NW];   // [root-batch parity][root in batch][warp] chunk-product totals
+    __shared__ int tcnt[NW];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int t = threadIdx.x;
+    const int64_t item = blockIdx.x;
+    const bool valid = true;
+    const int64_t s = s_begin + item / a.B;
+    const int64_t b = item - (item / a.B) * a.B;
+    const SymSigDev sg = a.sigs[a.sig_of[s]];
+    const int k = sg.k;
+    const int64_t lo = a.off[s];
+    const int i0 = t * C;
+    // padding literals past k get l = 1 (a certainly-False literal: p = 0), whose factor
+    // alpha + beta = 1 (exactly in real arithmetic, to one rounding in the table), so the sweeps need
+    // no per-literal selects; their terms are never stored
+    T l[C];
+    int tc = 0;
+#pragma unroll
+    for (int j = 0; j < C; ++j) {
+        l[j] = (T)1;
+        if (i0 + j < k) {
+            const uint32_t w = __ldg(a.words + lo + i0 + j);
+            const T xv = a.x[b * a.sb + (int64_t)(w & 0x7fffffffu) * a.sv];
+            l[j] = (int)w < 0 ? -xv : xv;
+            tc += (int)((xv < (T)0) != ((int)w < 0));
+        }
+    }
+    T term[C];
+#pragma unroll
+    for (int j = 0; j < C; ++j) term[j] = (T)0;
+    double fe_acc = 0.0;
+    // root table alpha, beta, G, H (8 T per root) staged in shared memory once per item: the per-root
+    // coefficient reads in the sweeps become broadcast LDS instead of dependent global loads
+    T* cf = reinterpret_cast<T*>(sym_smem);
+    {
+        const T* g = a.coef + sg.coef_off * 8;
+        for (int i = t; i < sg.Mp * 8; i += 32 * NW) cf[i] = g[i];
+        __syncthreads();
+    }
+    const cplx<T> one{(T)1, (T)0};
+    cplx<T> al[R], be[R];
+    load_ab<T, R>(cf, 0, sg.Mp, al, be);
+    int m = 0;
+    for (; m + R <= sg.Mp; m += R) sym_roots<T, NW, C, R>(cf, m, sg.Mp, lane, warp, t, l, term, fe_acc, wtot, al, be);
+    if (R > 1 && m < sg.Mp) {   // odd remainder: one root (al[0], be[0] hold it)
+        cplx<T> al1[1] = {al[0]}, be1[1] = {be[0]};
+        sym_roots<T, NW, C, 1>(cf, m, sg.Mp, lane, warp, t, l, term, fe_acc, wtot, al1, be1);
     }
     const T wc = a.w_sym[s];
 #pragma unroll
-    for (int j = 0; j < CK; ++j) {
-        int i = i0 + j;
-        if (j < ck && i < k) {
-            T v = wc * term[j];
-            a.Tb[(a.tb_fast + lo + i) * a.B + b] = neg[j] ? -v : v;
+    for (int j = 0; j < C; ++j) {
+        const int i = i0 + j;
+        if (valid && i < k) {
+            const uint32_t w = __ldg(a.words + lo + i);
+            const T v = wc * term[j];
+            a.Tb[(a.tb_fast + lo + i) * a.B + b] = (int)w < 0 ? -v : v;
         }
     }
-    // true-literal count of sgn(x) over the group
 #pragma unroll
     for (int d = 16; d >= 1; d >>= 1) tc += __shfl_xor_sync(0xffffffffu, tc, d);
-    if (NWG > 1) {
+    if (NW > 1) {
         if (lane == 0) tcnt[warp] = tc;
         __syncthreads();
         tc = 0;
-        for (int w = 0; w < NWG; ++w) tc += tcnt[w];
+#pragma unroll
+        for (int w = 0; w < NW; ++w) tc += tcnt[w];
     }
-    if (t == 0) {
+    if (valid && t == 0) {
         a.fsym[s * a.B + b] = (double)wc * (sg.g0 + fe_acc);
         a.usym[s * a.B + b] = rule_sat(tc, sg.tmin, sg.tmax, sg.parity) ? 0 : 1;
     }
