@@ -33,12 +33,14 @@ import numpy as np  # noqa: E402
 
 import synth  # noqa: E402
 
+# mode "restart": a step is one CLS iteration of the batch, restart points sharded over ranks (weak scaling);
+# mode "constraint": a step is one batched f + grad evaluation, constraints sharded over ranks + all-reduce
 CONFIGS = {
-    "c2": dict(make=lambda: synth.config2(0), B=1024, desc="c2: uniform random 7-SAT n=200 m=17000 (alpha=85)"),
-    "c1": dict(make=lambda: synth.config1(0), B=1, desc="c1: uniform random 3-SAT n=20 m=91, single point"),
-    "c3": dict(make=lambda: synth.config3(0), B=32, desc="c3: n=4096, 8192 planted 3-SAT + 32 at-most-b k=500..2000, fp64"),
-    "c4": dict(make=lambda: synth.config4_hybrid(0), B=1024, desc="c4: n=1024, 2048 planted 3-CNF + 512 XOR k=3..64"),
-    "c5": dict(make=lambda: synth.config5(0), B=32, desc="c5: uniform random 3-SAT n=1e6 m=4.2e6"),
+    "c2": dict(make=lambda: synth.config2(0), B=1024, mode="restart", desc="c2: uniform random 7-SAT n=200 m=17000 (alpha=85)"),
+    "c1": dict(make=lambda: synth.config1(0), B=1, mode="restart", desc="c1: uniform random 3-SAT n=20 m=91, single point"),
+    "c3": dict(make=lambda: synth.config3(0), B=32, mode="restart", desc="c3: n=4096, 8192 planted 3-SAT + 32 at-most-b k=500..2000, fp64"),
+    "c4": dict(make=lambda: synth.config4_hybrid(0), B=1024, mode="restart", desc="c4: n=1024, 2048 planted 3-CNF + 512 XOR k=3..64"),
+    "c5": dict(make=lambda: synth.config5(0), B=32, mode="constraint", desc="c5: uniform random 3-SAT n=1e6 m=4.2e6, constraint-sharded"),
 }
 SM_COUNT = 148
 FP32_LANES, FP64_LANES = 128, 64  # per SM per clock (B200_PROFILING.md / blackwell guide)
@@ -207,28 +209,31 @@ def main():
         dist.init_process_group("nccl", device_id=dev)
     inst = cfg["make"]()
     B = cfg["B"]
-    ctx = P.Context.from_instance(inst, device=local)
+    from paper_2308_15020_b200 import dist as D
+    if cfg["mode"] == "constraint":
+        se = D.ShardedEval(inst.arrays(), rank, world, device=local)
+        ctx = se.ctx
+    else:
+        ctx = P.Context.from_instance(inst, device=local)
     info = ctx.info
-    L = info["n_lits"]
-    search = ctx.search(B, seed=20230815, point0=rank * B, max_inner=args.round_len, check_every=args.round_len)
-    T = search.tensors()
-    flag = torch.zeros(1, dtype=torch.int32, device=dev)
+    L = inst.n_lits                       # literal-gradient terms per point of the whole formula
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
     stream = torch.cuda.current_stream(dev)
+    dt = torch.float64 if info["precision"] == 64 else torch.float32
 
-    def step(i):
-        search.iterate(1)
-        if (i + 1) % args.round_len == 0:
-            search.check()
-            if world > 1:
-                dist.all_reduce(T["U"], op=dist.ReduceOp.SUM)
-            flag.copy_((T["unsat"].min() == 0).to(torch.int32).view(1))
-            if world > 1:
-                dist.all_reduce(flag, op=dist.ReduceOp.MAX)
-            search.restart(T["U"])
-            search.begin_round()
+    if cfg["mode"] == "constraint":
+        xs = torch.from_numpy(synth.points("U", B, inst.n, 1000, np.float64)).to(dt).to(dev)
 
-    search.begin_round()
+        def step(i):
+            se.eval(xs)
+    else:
+        search = ctx.search(B, seed=20230815, point0=rank * B, max_inner=args.round_len, check_every=args.round_len)
+        rs = D.RestartSharded(search, args.round_len, rank, world)
+        rs.begin()
+
+        def step(i):
+            rs.step(i)
+
     # prime every code path of a step (round end included: CUDA lazy module loading, torch's reduction
     # kernels) so the first timed round end does not pay one-time costs; then the W warm-up steps
     for i in range(args.round_len):
@@ -265,17 +270,29 @@ def main():
     if world > 1:
         dist.all_reduce(t_local, op=dist.ReduceOp.MAX)
     ms_max = float(t_local.item())
-    B_total = B * world
+    B_total = B * world if cfg["mode"] == "restart" else B
     value = L * B_total * args.steps / (ms_max * 1e-3)
 
-    # ---- e2e: the public API with pinned host buffers (H2D of x, D2H of f and grad every step)
-    dt = torch.float64 if info["precision"] == 64 else torch.float32
+    # ---- e2e: the public API with pinned host buffers (H2D of x, D2H of f and grad every step):
+    # ffsat_eval with host pointers (restart mode), or host -> device copy + ShardedEval + device -> host
     xh = torch.from_numpy(synth.points("U", B, inst.n, 1000 + rank, np.float64)).to(dt).pin_memory()
     fh = torch.empty(B, dtype=torch.float64).pin_memory()
     gh = torch.empty((B, inst.n), dtype=dt).pin_memory()
     e2e_steps = max(5, min(args.steps, 50))
+    if cfg["mode"] == "constraint":
+        xdev = torch.empty((B, inst.n), dtype=dt, device=dev)
+
+        def host_eval():
+            xdev.copy_(xh, non_blocking=True)
+            f_, g_, _ = se.eval(xdev)
+            fh.copy_(f_, non_blocking=True)
+            gh.copy_(g_, non_blocking=True)
+            torch.cuda.synchronize()
+    else:
+        def host_eval():
+            P.ffsat_eval(ctx.ptr, xh, B, fh, gh)   # synchronous: H2D, kernels, D2H
     for _ in range(3):
-        P.ffsat_eval(ctx.ptr, xh, B, fh, gh)
+        host_eval()
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
@@ -285,7 +302,7 @@ def main():
             flush.zero_()
             torch.cuda.synchronize()
         t0 = time.perf_counter()
-        P.ffsat_eval(ctx.ptr, xh, B, fh, gh)   # synchronous: H2D, kernels, D2H
+        host_eval()
         e2e_ms.append((time.perf_counter() - t0) * 1e3)
     te = torch.tensor([sum(e2e_ms)], dtype=torch.float64, device=dev)
     if world > 1:
@@ -334,11 +351,11 @@ def main():
         base = None if args.no_cpu_baseline or world > 1 else cpu_baseline(cfg, inst, xd.cpu().numpy())
         line = {"metric": "literal-gradient terms/s", "value": value, "unit": "terms/s", "n_gpus": world,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max / args.steps,
-                "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+                "higher_is_better": True, "scaling": "weak" if cfg["mode"] == "restart" else "strong", "vs_baseline": None,
                 "dtype": "f64" if info["precision"] == 64 else "f32", "data": "synthetic",
                 "config": {"workload": cfg["desc"], "n": inst.n, "m": inst.m, "literals": L,
                            "batch_per_gpu": B, "global_batch": B_total, "round_len": args.round_len,
-                           "parallelism": f"restart-sharded x{world}" if world > 1 else "single GPU",
+                           "parallelism": (f"{cfg['mode']}-sharded x{world}" if world > 1 else "single GPU"),
                            "l2": "flushed between timed steps (256 MiB write, untimed)" if not args.no_flush else "not flushed",
                            "path": "tiled" if info["path"] == 1 else "global"},
                 "evals_per_s": B_total * args.steps / (ms_max * 1e-3),

@@ -1,0 +1,189 @@
+"""Multi-GPU host logic on CPU: world-size-2 gloo process groups.
+
+The library's kernels need a GPU, so the per-rank compute here is the oracle (tests may use it): an
+oracle-backed evaluator for constraint sharding and an oracle-backed search double for restart sharding.
+What is under test is paper_2308_15020_b200/dist.py: the partitions, the collectives and the claim that a
+restart-sharded run is identical to the single-process run of the same global points (F7)."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_2308_15020_b200 import dist as D
+import synth
+from oracle import cdp
+from oracle import solve as osolve
+from oracle.formula import OracleFormula
+
+
+def free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _init(rank, world, port):
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+
+
+# ---------------------------------------------------------------------------------------------- partitions
+
+
+def test_point_ranges_partition():
+    for B in (0, 1, 7, 32, 1000):
+        for world in (1, 2, 3, 8):
+            rs = [D.point_range(B, world, r) for r in range(world)]
+            assert rs[0][0] == 0
+            for (p0, b), (p1, _) in zip(rs, rs[1:]):
+                assert p0 + b == p1
+            assert sum(b for _, b in rs) == B
+            assert max(b for _, b in rs) - min(b for _, b in rs) <= 1
+
+
+def test_constraint_ranges_cover_and_balance():
+    inst = synth.config3(0, n=600, m3=300, n_card=6, kmin=100, kmax=300)
+    cost = D.constraint_cost(inst.kind, inst.bound, inst.offsets)
+    assert np.all(cost[inst.kind == 0] == 3)            # clauses: k
+    assert np.all(cost[inst.kind == 4] > 1000)          # long at-most: 12 k M'
+    for world in (1, 2, 4):
+        rs = D.constraint_ranges(inst.kind, inst.bound, inst.offsets, world)
+        assert rs[0][0] == 0 and rs[-1][1] == inst.m
+        assert all(a[1] == b[0] for a, b in zip(rs, rs[1:]))
+        shares = [cost[c0:c1].sum() for c0, c1 in rs]
+        assert max(shares) <= cost.sum() / world + cost.max()
+
+
+def test_sub_formulas_sum_to_the_formula():
+    inst = synth.random_mixed(n=40, m=120, seed=5, kmax=20)
+    X = synth.points("U", 6, inst.n, 9, np.float64)
+    f_full, g_full = cdp.evaluate(OracleFormula.from_arrays(*inst.arrays()), X)
+    f, g = np.zeros_like(f_full), np.zeros_like(g_full)
+    for c0, c1 in D.constraint_ranges(inst.kind, inst.bound, inst.offsets, 3):
+        fs, gs = cdp.evaluate(OracleFormula.from_arrays(*D.sub_formula(*inst.arrays(), c0, c1)), X)
+        f += fs
+        g += gs
+    assert np.allclose(f, f_full, rtol=0, atol=1e-12) and np.allclose(g, g_full, rtol=0, atol=1e-12)
+
+
+# ---------------------------------------------------------------------------------------------- constraint sharding
+
+
+def _sharded_eval_worker(rank, world, port, out):
+    _init(rank, world, port)
+    inst = synth.random_mixed(n=30, m=90, seed=21, kmax=16)
+    X = synth.points("U", 5, inst.n, 3, np.float64)
+
+    def evaluate(x):
+        Fo = OracleFormula.from_arrays(*se.arrays)
+        f, g = cdp.evaluate(Fo, x)
+        u, _ = cdp.check(Fo, x)
+        return torch.from_numpy(f), torch.from_numpy(g), torch.from_numpy(u.astype(np.int32))
+
+    se = D.ShardedEval(inst.arrays(), rank, world, evaluate=evaluate)
+    f, g, u = se.eval(X)
+    if rank == 0:
+        np.savez(out, f=f.numpy(), g=g.numpy(), u=u.numpy(), r=np.array(se.range))
+    dist.destroy_process_group()
+
+
+def test_constraint_sharded_eval_gloo(tmp_path):
+    out = str(tmp_path / "se.npz")
+    mp.spawn(_sharded_eval_worker, args=(2, free_port(), out), nprocs=2, join=True)
+    r = np.load(out)
+    inst = synth.random_mixed(n=30, m=90, seed=21, kmax=16)
+    X = synth.points("U", 5, inst.n, 3, np.float64)
+    Fo = OracleFormula.from_arrays(*inst.arrays())
+    f, g = cdp.evaluate(Fo, X)
+    u, _ = cdp.check(Fo, X)
+    assert 0 < r["r"][1] < inst.m                     # rank 0 holds a proper part
+    assert np.allclose(r["f"], f, rtol=0, atol=1e-12)
+    assert np.allclose(r["g"], g, rtol=0, atol=1e-12)
+    assert np.array_equal(r["u"], u)
+
+
+# ---------------------------------------------------------------------------------------------- restart sharding
+
+
+class OracleSearch:
+    """Test double of libffsat's Search on the oracle (oracle/solve.py semantics, fp64, CPU tensors)."""
+
+    def __init__(self, F, B, seed, point0, params):
+        self.F, self.B, self.seed, self.point0, self.P = F, B, seed, point0, params
+        self.st = osolve.State(x=osolve.initial_points(seed, range(point0, point0 + B), F.n), f=None, g=None,
+                               eta=None, done=None, iters=None, w=np.ones(F.m), point0=point0)
+        self.unsat = np.zeros(B, np.int32)
+        self.U = np.zeros(F.m, np.int32)
+        self.rnd = 0
+
+    def tensors(self):
+        return {"x": torch.from_numpy(self.st.x), "unsat": torch.from_numpy(self.unsat), "U": torch.from_numpy(self.U)}
+
+    def begin_round(self):
+        osolve.start_round(self.F, self.st, self.P)
+
+    def iterate(self, n):
+        for _ in range(n):
+            osolve.pgd_iteration(self.F, self.st, self.P)
+
+    def check(self):
+        cnt, _, U = cdp.check(self.F, self.st.x, want_U=True)
+        self.unsat[:] = cnt
+        self.U[:] = U
+
+    def restart(self, U_global):
+        if self.P.adaptive_weights:
+            self.st.w = osolve.erwa_update(self.st.w, np.asarray(U_global), self.P.alpha)
+        self.rnd += 1
+        self.st.x[:] = osolve.rephase(self.st.x, self.seed, self.point0, self.rnd, self.P)
+
+    def assignment(self, lp):
+        return np.where(self.st.x[lp] < 0, -1, 1).astype(np.int8)
+
+
+def _run_restart_sharded(rank, world, B_total, rounds, round_len):
+    inst = synth.config1(4)
+    Fo = OracleFormula.from_arrays(*inst.arrays())
+    point0, B = D.point_range(B_total, world, rank)
+    s = OracleSearch(Fo, B, 1234, point0, osolve.Params(max_inner=round_len))
+    rs = D.RestartSharded(s, round_len, rank, world)
+    rs.point0 = point0
+    rs.begin()
+    flags = []
+    for i in range(rounds * round_len):
+        fl = rs.step(i)
+        if fl is not None:
+            flags.append(int(fl.item()))
+    cnt, gp, a = rs.incumbent()
+    return point0, s.st.x.copy(), s.st.w.copy(), flags, (cnt, gp, a)
+
+
+def _restart_worker(rank, world, port, out, B_total, rounds, round_len):
+    _init(rank, world, port)
+    p0, x, w, flags, inc = _run_restart_sharded(rank, world, B_total, rounds, round_len)
+    np.savez(out + f".{rank}.npz", p0=p0, x=x, w=w, flags=np.array(flags), cnt=inc[0], gp=inc[1], a=inc[2])
+    dist.destroy_process_group()
+
+
+def test_restart_sharding_matches_single_process(tmp_path):
+    """G = 2 ranks x 6 points reproduce G = 1 x 12 points exactly: per-point trajectories (Philox keyed by
+    global point), the ERWA weights (global U_c), the any-solved flags and the incumbent."""
+    B_total, rounds, round_len = 12, 3, 4
+    p0, x1, w1, flags1, inc1 = _run_restart_sharded(0, 1, B_total, rounds, round_len)
+    out = str(tmp_path / "rs")
+    mp.spawn(_restart_worker, args=(2, free_port(), out, B_total, rounds, round_len), nprocs=2, join=True)
+    parts = [np.load(out + f".{r}.npz") for r in range(2)]
+    x2 = np.concatenate([p["x"] for p in sorted(parts, key=lambda p: int(p["p0"]))])
+    assert np.array_equal(x1, x2)
+    for p in parts:
+        assert np.array_equal(p["w"], w1)
+        assert list(p["flags"]) == flags1
+        assert (int(p["cnt"]), int(p["gp"])) == (inc1[0], inc1[1])
+        assert np.array_equal(p["a"], inc1[2])
+    # the incumbent is a true minimiser of the falsified count over all global points
+    Fo = OracleFormula.from_arrays(*synth.config1(4).arrays())
+    cnt, _ = cdp.check(Fo, np.where(x1 < 0, -1.0, 1.0))
+    assert inc1[0] == cnt.min() and inc1[1] == int(np.argmin(cnt))
