@@ -43,9 +43,10 @@ CONFIGS = {
     "c5": dict(make=lambda: synth.config5(0), B=32, mode="constraint", desc="c5: uniform random 3-SAT n=1e6 m=4.2e6, constraint-sharded"),
 }
 SM_COUNT = 148
-FP32_LANES, FP64_LANES = 128, 64  # per SM per clock (B200_PROFILING.md / blackwell guide)
-FAST_FLOPS_PER_TERM = 6           # factor FMA + prefix MUL + suffix MUL + combine FMA
-ROOT_FLOPS_PER_LIT_ROOT = 20      # factor 2 FMA + 2 complex MUL (4 MUL + 4 FMA) + Re-accumulate 2 FMA
+FP32_LANES, FP64_LANES = 128, 64  # FP32 / FP64 lanes per SM per clock (B200 guide unit counts)
+# Algorithmic FP lane-operations (one FMA = one lane-op = one pipe slot: count instructions):
+FAST_OPS_PER_TERM = 5             # factor FMA, prefix MUL, prefix*suffix MUL, suffix MUL, gradient FMA
+ROOT_OPS_PER_LIT_ROOT = 12        # factor 2 FMA, prefix + suffix complex MUL (2 x 4), Re-accumulate 2 FMA (App. A)
 
 
 def env_rank():
@@ -326,26 +327,44 @@ def main():
     peaks, peak_src = measured_peaks()
     mhz = float(peaks.get("sm_max_mhz", 1965.0))
     fast_ms, root_ms = float(ph[0]), float(ph[1])
-    if fast_ms >= root_ms:
-        kname = "fast_tiled_kernel" if info["path"] == 1 else "fast_global_kernel"
-        flops = FAST_FLOPS_PER_TERM * info["n_fast_lits"] * B
-        kms = fast_ms
-        peak = SM_COUNT * FP32_LANES * 2 * mhz * 1e6 / 1e12 if info["precision"] == 32 else SM_COUNT * FP64_LANES * 2 * mhz * 1e6 / 1e12
+    es = 8 if info["precision"] == 64 else 4
+    lanes = FP64_LANES if info["precision"] == 64 else FP32_LANES
+    alu_peak = SM_COUNT * lanes * mhz * 1e6 / 1e12          # T lane-ops/s
+    alu_src = (f"{SM_COUNT} SMs x {lanes} {'FP64' if lanes == FP64_LANES else 'FP32'} lanes x {mhz:.0f} MHz "
+               f"({peak_src} sm_max_mhz); one FMA = one lane-op")
+    if fast_ms >= root_ms and info["path"] == 2:
+        # global fast path: HBM-bound (terms stored for the ordered reduction, x rows gathered)
+        kname, kms = "fast_global_kernel", fast_ms
+        alg_bytes = (info["n_fast_lits"] * B * es + inst.n * B * es + info["n_fast_lits"] * 4 + info["n_fast_cons"] * es)
+        achieved = alg_bytes / (kms * 1e-3) / 1e9
+        peak = float(peaks.get("hbm_gbs", 6650.0))
+        roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                    "algorithmic_bytes": alg_bytes,
+                    "algorithmic_bytes_def": "terms written L_fast*B*es + x read once n*B*es + literal words 4*L_fast + weights es*C_fast",
+                    "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_src})"}
+    elif fast_ms >= root_ms:
+        kname, kms = "fast_tiled_kernel", fast_ms
+        ops = FAST_OPS_PER_TERM * info["n_fast_lits"] * B
+        achieved = ops / (kms * 1e-3) / 1e12
+        roofline = {"bound": "alu", "achieved": achieved, "peak": alu_peak, "unit": "T lane-op/s",
+                    "algorithmic_ops_per_term": FAST_OPS_PER_TERM, "peak_source": alu_src,
+                    "note": "issue/LSU-limited gather-scatter kernel; see DESIGN.md 7 and profiles/*fast_tiled*"}
+        peak = alu_peak
     else:
-        kname = "sym_group_kernel"
-        flops = ROOT_FLOPS_PER_LIT_ROOT * info["sym_root_lits"] * B
-        kms = root_ms
-        lanes = FP64_LANES if info["precision"] == 64 else FP32_LANES
-        peak = SM_COUNT * lanes * 2 * mhz * 1e6 / 1e12
-    achieved = flops / (kms * 1e-3) / 1e12
-    traffic = ncu_traffic(kname)
-    roofline = {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
-                "traffic": traffic, "kernel": kname, "kernel_ms": kms,
-                "eval_phase_ms": {"fast": float(ph[0]), "root": float(ph[1]), "grad_reduce": float(ph[2]),
-                                  "f_reduce": float(ph[3])},
-                "kernel_share_of_eval": kms / float(np.sum(ph)),
-                "peak_source": f"{SM_COUNT} SMs x {FP32_LANES if info['precision'] == 32 else FP64_LANES} lanes x 2 flops x "
-                               f"{mhz:.0f} MHz ({peak_src} sm_max_mhz); FMA = 2 flops"}
+        kname, kms = "sym_item_kernel", root_ms
+        ops = ROOT_OPS_PER_LIT_ROOT * info["sym_root_lits"] * B
+        achieved = ops / (kms * 1e-3) / 1e12
+        roofline = {"bound": "alu", "achieved": achieved, "peak": alu_peak, "unit": "T lane-op/s",
+                    "algorithmic_ops_per_lit_root": ROOT_OPS_PER_LIT_ROOT, "peak_source": alu_src}
+        peak = alu_peak
+    roofline.update({"frac": achieved / peak, "traffic": ncu_traffic(kname), "kernel": kname, "kernel_ms": kms,
+                     "eval_phase_ms": {"fast": float(ph[0]), "root": float(ph[1]), "grad_reduce": float(ph[2]),
+                                       "f_reduce": float(ph[3])},
+                     "kernel_share_of_eval": kms / float(np.sum(ph)),
+                     "timing": "CUDA events recorded inside libffsat on the launching stream (ffsat_eval_profiled, "
+                               "phases serialised), mean over the profiled evaluations"})
+    roofline = {k: roofline[k] for k in ("bound", "achieved", "peak", "unit", "frac", "traffic")} | \
+        {k: v for k, v in roofline.items() if k not in ("bound", "achieved", "peak", "unit", "frac", "traffic")}
 
     if rank == 0:
         base = None if args.no_cpu_baseline or world > 1 else cpu_baseline(cfg, inst, xd.cpu().numpy())

@@ -162,7 +162,8 @@ void eval_device_t(ffsat_ctx* c, const T* x, int64_t B, double* f, T* grad, int3
     rf.B = B; rf.n_parts = L.n_fast > 0 ? c->n_chunks : 0; rf.n_sym = L.n_sym;
     rf.fpart = c->fpart.as<double>(); rf.upart = c->upart.as<int32_t>(); rf.fsym = c->fsym.as<double>();
     rf.usym = c->usym.as<int32_t>(); rf.f = f; rf.unsat = unsat;
-    dev::reduce_f_kernel<<<blocks_for(B, 32), 256, 0, st>>>(rf);
+    if (B <= 32 * 64) dev::reduce_f_kernel<32><<<blocks_for(B, 32), 1024, 0, st>>>(rf);
+    else dev::reduce_f_kernel<8><<<blocks_for(B, 32), 256, 0, st>>>(rf);
     CK(cudaGetLastError());
     mark(4);
 }

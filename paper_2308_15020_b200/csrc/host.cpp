@@ -468,6 +468,7 @@ Layout build_layout(const Formula& F, int path, int precision) {
         for (int64_t s = 0; s < Lo.tb_slots; ++s) Lo.occ_slot[(size_t)cur[(size_t)slot_var[(size_t)s]]++] = s;
     }
 
+
     // ---- work units: tiled = the classes; global = runs of one bucket with <= 512 literals
     if (path == 1) {
         Lo.tiled_words.assign(Lo.fast_words.size(), 0);

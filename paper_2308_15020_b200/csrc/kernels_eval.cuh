@@ -134,7 +134,7 @@ template <typename T>
 struct BucketReg {
     T g0, c0[2], c1[2], g[2];
     int32_t k, kp, tmin, tmax, parity;
-    int64_t pos_begin, word_off;
+    int64_t pos_begin, word_off, slot_off;
 };
 template <typename T>
 __device__ __forceinline__ BucketReg<T> load_bucket(const FastBucketDev* p) {
@@ -147,7 +147,7 @@ __device__ __forceinline__ BucketReg<T> load_bucket(const FastBucketDev* p) {
         r.g[c] = (T)p->g[c];
     }
     r.k = p->k; r.kp = p->kp; r.tmin = p->tmin; r.tmax = p->tmax; r.parity = p->parity;
-    r.pos_begin = p->pos_begin; r.word_off = p->word_off;
+    r.pos_begin = p->pos_begin; r.word_off = p->word_off; r.slot_off = p->slot_off;
     return r;
 }
 
@@ -225,6 +225,19 @@ __device__ __forceinline__ void tiled_clause(const BucketReg<T>& bk, const uint3
 }
 
 #define K_PAD(K) (((K) + 3) / 4 * 4)
+
+// K literal words of one constraint row from global memory (16-byte read-only loads)
+template <int K>
+__device__ __forceinline__ void load_words(const uint32_t* wp, uint32_t (&w)[K]) {
+#pragma unroll
+    for (int i = 0; i < K; i += 4) {
+        uint4 q = __ldg(reinterpret_cast<const uint4*>(wp + i));
+        w[i] = q.x;
+        if (i + 1 < K) w[i + 1] = q.y;
+        if (i + 2 < K) w[i + 2] = q.z;
+        if (i + 3 < K) w[i + 3] = q.w;
+    }
+}
 
 template <int K>
 __device__ __forceinline__ void load_words_smem(const uint32_t* sp, uint32_t (&w)[K]) {
@@ -576,86 +589,135 @@ struct GlobalArgs {
     int32_t* upart;
 };
 
+// Terms of one constraint for one lane from its literal words and gathered variable values (k <= 16):
+// term_i = w d FE / d x_{v_i} (literal sign folded into the factor slope, as in tiled_clause).
 template <typename T, int K, int NCH>
-__device__ __forceinline__ void global_clause(const GlobalArgs<T>& a, const FastBucketDev& bk, int64_t pos, int64_t b,
-                                              bool bv, double& facc, int& uacc) {
-    const uint32_t* wp = a.words + bk.word_off + (pos - bk.pos_begin) * bk.kp;
-    uint32_t w[K];
-#pragma unroll
-    for (int i = 0; i < K; i += 4) {
-        uint4 q = __ldg(reinterpret_cast<const uint4*>(wp + i));
-        w[i] = q.x;
-        if (i + 1 < K) w[i + 1] = q.y;
-        if (i + 2 < K) w[i + 2] = q.z;
-        if (i + 3 < K) w[i + 3] = q.w;
-    }
-    T l[K];
-    int t = 0;
+__device__ __forceinline__ void clause_terms(const BucketReg<T>& bk, const uint32_t (&w)[K], const T (&xv)[K], T wc, T (&gs)[K],
+                                             double& facc, int& uacc) {
+    uint32_t t = 0;
 #pragma unroll
     for (int i = 0; i < K; ++i) {
-        T xv = bv ? a.xT[(int64_t)(w[i] & 0x7fffffffu) * a.B + b] : (T)0;
-        bool neg = w[i] >> 31;
-        l[i] = neg ? -xv : xv;
-        t += (int)((xv < (T)0) != neg);
+        t += (uint32_t)((xv[i] < (T)0) != ((int)w[i] < 0));
+        gs[i] = (T)0;
     }
-    T term[K], fe;
-    fast_terms<T, K, NCH>(l, bk, term, fe);
-    const T wc = a.w_pos[pos];
-    const int64_t slot0 = bk.slot_off + (pos - bk.pos_begin) * bk.k;
-    if (bv) {
+    T fe = bk.g0;
+#pragma unroll
+    for (int c = 0; c < NCH; ++c) {
+        T av[K], pre[K];
+        T run = (T)1;
 #pragma unroll
         for (int i = 0; i < K; ++i) {
-            T v = wc * term[i];
-            a.Tb[(slot0 + i) * a.B + b] = (w[i] >> 31) ? -v : v;
+            av[i] = fmaT(flip_sign(bk.c1[c], w[i]), xv[i], bk.c0[c]);
+            pre[i] = run;
+            run *= av[i];
+        }
+        fe = fmaT(bk.g[c], run, fe);
+        T suf = bk.g[c] * wc;
+#pragma unroll
+        for (int i = K - 1; i >= 0; --i) {
+            gs[i] = fmaT(pre[i] * suf, flip_sign(bk.c1[c], w[i]), gs[i]);
+            suf *= av[i];
         }
     }
     facc += (double)(wc * fe);
-    uacc += rule_sat(t, bk.tmin, bk.tmax, bk.parity) ? 0 : 1;
+    uacc += rule_sat((int)t, bk.tmin, bk.tmax, bk.parity) ? 0 : 1;
+}
+
+// One unit on the global path: the warp's constraints two at a time, every load of the pair (literal words,
+// then the gathered x^T rows, read-only path) issued before any arithmetic -- the kernel is bound by the
+// latency of these gathers and the T stores, so memory-level parallelism is what matters.
+template <typename T, int K, int NCH>
+__device__ __forceinline__ void global_unit(const GlobalArgs<T>& a, const BucketReg<T>& bk, const UnitDev& U, int64_t b, bool bv,
+                                            int warp, int nw, double& facc, int& uacc) {
+    const int count = unit_count(U);
+    const int64_t wbase = (int64_t)U.word_begin;
+    const int64_t sbase = bk.slot_off + ((int64_t)U.pos_begin - bk.pos_begin) * K;
+    const int64_t bb = bv ? b : 0;
+    int j = warp;
+    for (; j < count; j += 2 * nw) {
+        const bool two = j + nw < count;
+        uint32_t w0[K], w1[K];
+        load_words<K>(a.words + wbase + (int64_t)j * K_PAD(K), w0);
+        if (two) load_words<K>(a.words + wbase + (int64_t)(j + nw) * K_PAD(K), w1);
+        else {
+#pragma unroll
+            for (int i = 0; i < K; ++i) w1[i] = w0[i];
+        }
+        T x0[K], x1[K];
+#pragma unroll
+        for (int i = 0; i < K; ++i) {
+            x0[i] = __ldg(a.xT + (int64_t)(w0[i] & 0x7fffffffu) * a.B + bb);
+            x1[i] = __ldg(a.xT + (int64_t)(w1[i] & 0x7fffffffu) * a.B + bb);
+        }
+        const T wc0 = __ldg(a.w_pos + U.pos_begin + j);
+        const T wc1 = two ? __ldg(a.w_pos + U.pos_begin + j + nw) : (T)0;
+        T g0[K], g1[K];
+        clause_terms<T, K, NCH>(bk, w0, x0, wc0, g0, facc, uacc);
+        if (bv) {
+#pragma unroll
+            for (int i = 0; i < K; ++i) a.Tb[(sbase + (int64_t)j * K + i) * a.B + b] = g0[i];
+        }
+        if (two) {
+            clause_terms<T, K, NCH>(bk, w1, x1, wc1, g1, facc, uacc);
+            if (bv) {
+#pragma unroll
+                for (int i = 0; i < K; ++i) a.Tb[(sbase + (int64_t)(j + nw) * K + i) * a.B + b] = g1[i];
+            }
+        }
+    }
+}
+
+// 16 < k <= 64 on the global path: literals re-read in 16-literal register blocks (fast_terms_blocked).
+template <typename T, int NCH>
+__device__ void global_unit_long(const GlobalArgs<T>& a, const BucketReg<T>& bk, const UnitDev& U, int64_t b, bool bv,
+                                 int warp, int nw, double& facc, int& uacc) {
+    const int k = bk.k;
+    const int64_t bb = bv ? b : 0;
+    for (int j = warp; j < unit_count(U); j += nw) {
+        const int64_t pos = (int64_t)U.pos_begin + j;
+        const uint32_t* wp = a.words + (int64_t)U.word_begin + (int64_t)j * unit_kp(U);
+        const int64_t slot0 = bk.slot_off + (pos - bk.pos_begin) * k;
+        int t = 0;
+        for (int i = 0; i < k; ++i) {
+            const uint32_t w = __ldg(wp + i);
+            const T xv = __ldg(a.xT + (int64_t)(w & 0x7fffffffu) * a.B + bb);
+            t += (int)((xv < (T)0) != ((int)w < 0));
+        }
+        auto getl = [&](int i) -> T {
+            const uint32_t w = __ldg(wp + i);
+            return flip_sign(__ldg(a.xT + (int64_t)(w & 0x7fffffffu) * a.B + bb), w);
+        };
+        T dummy = (T)0;
+        auto addterm = [&](int i, T v, bool first) {
+            T* dst = bv ? a.Tb + (slot0 + i) * a.B + b : &dummy;
+            *dst = first ? v : *dst + v;
+        };
+        T fe;
+        fast_terms_blocked<T, NCH>(k, bk, getl, addterm, fe);
+        const T wc = __ldg(a.w_pos + pos);
+        if (bv) {
+            for (int i = 0; i < k; ++i) {
+                const uint32_t w = __ldg(wp + i);
+                T* dst = a.Tb + (slot0 + i) * a.B + b;
+                *dst = flip_sign(wc * *dst, w);
+            }
+        }
+        facc += (double)(wc * fe);
+        uacc += rule_sat(t, bk.tmin, bk.tmax, bk.parity) ? 0 : 1;
+    }
 }
 
 template <typename T, int NCH, int KMAX>
-__device__ void global_clause_dispatch(const GlobalArgs<T>& a, const FastBucketDev& bk, int64_t pos, int64_t b, bool bv,
-                                       double& facc, int& uacc) {
+__device__ __forceinline__ void global_unit_dispatch(const GlobalArgs<T>& a, const BucketReg<T>& bk, const UnitDev& U, int64_t b,
+                                                     bool bv, int warp, int nw, double& facc, int& uacc) {
     switch (bk.k) {
-#define FFSAT_K(KK) case KK: if (KK <= KMAX) { global_clause<T, (KK <= KMAX ? KK : 1), NCH>(a, bk, pos, b, bv, facc, uacc); return; } break;
+#define FFSAT_K(KK) case KK: if (KK <= KMAX) { global_unit<T, (KK <= KMAX ? KK : 1), NCH>(a, bk, U, b, bv, warp, nw, facc, uacc); return; } break;
         FFSAT_K(1) FFSAT_K(2) FFSAT_K(3) FFSAT_K(4) FFSAT_K(5) FFSAT_K(6) FFSAT_K(7) FFSAT_K(8)
         FFSAT_K(9) FFSAT_K(10) FFSAT_K(11) FFSAT_K(12) FFSAT_K(13) FFSAT_K(14) FFSAT_K(15) FFSAT_K(16)
 #undef FFSAT_K
     default: break;
     }
-    if (KMAX <= 16) return;
-    const int k = bk.k;
-    const uint32_t* wp = a.words + bk.word_off + (pos - bk.pos_begin) * bk.kp;
-    const int64_t slot0 = bk.slot_off + (pos - bk.pos_begin) * bk.k;
-    int t = 0;
-    for (int i = 0; i < k; ++i) {
-        uint32_t w = __ldg(wp + i);
-        T xv = bv ? a.xT[(int64_t)(w & 0x7fffffffu) * a.B + b] : (T)0;
-        t += (int)((xv < (T)0) != (bool)(w >> 31));
-    }
-    auto getl = [&](int i) -> T {
-        uint32_t w = __ldg(wp + i);
-        T xv = bv ? a.xT[(int64_t)(w & 0x7fffffffu) * a.B + b] : (T)0;
-        return (w >> 31) ? -xv : xv;
-    };
-    T dummy = (T)0;
-    auto addterm = [&](int i, T v, bool first) {
-        T* dst = bv ? a.Tb + (slot0 + i) * a.B + b : &dummy;
-        *dst = first ? v : *dst + v;
-    };
-    T fe;
-    fast_terms_blocked<T, NCH>(k, bk, getl, addterm, fe);
-    const T wc = a.w_pos[pos];
-    if (bv) {
-        for (int i = 0; i < k; ++i) {
-            uint32_t w = __ldg(wp + i);
-            T* dst = a.Tb + (slot0 + i) * a.B + b;
-            T v = wc * *dst;
-            *dst = (w >> 31) ? -v : v;
-        }
-    }
-    facc += (double)(wc * fe);
-    uacc += rule_sat(t, bk.tmin, bk.tmax, bk.parity) ? 0 : 1;
+    if constexpr (KMAX > 16) global_unit_long<T, NCH>(a, bk, U, b, bv, warp, nw, facc, uacc);
 }
 
 template <typename T, int KMAX>
@@ -668,14 +730,19 @@ __global__ void __launch_bounds__(256) fast_global_kernel(GlobalArgs<T> a) {
     const int chunk = blockIdx.y;
     double facc = 0.0;
     int uacc = 0;
+    int cur = -1;
+    BucketReg<T> bk{};
+    int nch = 0;
     for (int u = a.chunk_units[chunk]; u < a.chunk_units[chunk + 1]; ++u) {
         const UnitDev U = a.units[u];
-        const FastBucketDev bk = a.buckets[U.bucket];
-        for (int64_t pos = (int64_t)U.pos_begin + warp; pos < (int64_t)U.pos_begin + unit_count(U); pos += nw) {
-            if (bk.nch == 1) global_clause_dispatch<T, 1, KMAX>(a, bk, pos, b, bv, facc, uacc);
-            else if (bk.nch == 2) global_clause_dispatch<T, 2, KMAX>(a, bk, pos, b, bv, facc, uacc);
-            else global_clause_dispatch<T, 0, KMAX>(a, bk, pos, b, bv, facc, uacc);
+        if (U.bucket != cur) {
+            cur = U.bucket;
+            bk = load_bucket<T>(a.buckets + cur);
+            nch = a.buckets[cur].nch;
         }
+        if (nch == 1) global_unit_dispatch<T, 1, KMAX>(a, bk, U, b, bv, warp, nw, facc, uacc);
+        else if (nch == 2) global_unit_dispatch<T, 2, KMAX>(a, bk, U, b, bv, warp, nw, facc, uacc);
+        else global_unit_dispatch<T, 0, KMAX>(a, bk, U, b, bv, warp, nw, facc, uacc);
     }
     fr[warp * 32 + lane] = facc;
     ur[warp * 32 + lane] = uacc;
@@ -940,7 +1007,7 @@ struct ReduceArgs {
     const T* P;                  // [n_chunks][n][B]
     const T* Tb;                 // [tb_slots][B]
     const int64_t* occ_off;      // [n + 1]
-    const int32_t* occ_slot;
+    const int32_t* occ_slot;     // variable v's T rows, ascending: occ_slot[occ_off[v] .. occ_off[v + 1])
     T* grad;                     // [B][n]
 };
 
@@ -1001,21 +1068,23 @@ struct ReduceFArgs {
     int32_t* unsat;              // [B] or null
 };
 
-// one CTA (256 threads) per 32 points: lane = point, warp w sums rows w, w + 8, ... in ascending order,
-// then the 8 warp sums are added in warp order -- a fixed summation order (deterministic, no atomics).
-static __global__ void __launch_bounds__(256) reduce_f_kernel(ReduceFArgs a) {
-    __shared__ double sf[8][32];
-    __shared__ int su[8][32];
+// one CTA (32 NWF threads) per 32 points: lane = point, warp w sums rows w, w + NWF, ... in ascending
+// order, then the NWF warp sums are added in warp order -- a fixed summation order for a given launch
+// shape (deterministic, no atomics).  NWF = 32 when few point tiles must cover many partial rows.
+template <int NWF>
+__global__ void __launch_bounds__(32 * NWF) reduce_f_kernel(ReduceFArgs a) {
+    __shared__ double sf[NWF][32];
+    __shared__ int su[NWF][32];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const int64_t b = (int64_t)blockIdx.x * 32 + lane;
     double f = 0.0;
     int u = 0;
     if (b < a.B) {
-        for (int c = w; c < a.n_parts; c += 8) {
+        for (int c = w; c < a.n_parts; c += NWF) {
             f += a.fpart[(int64_t)c * a.B + b];
             u += a.upart[(int64_t)c * a.B + b];
         }
-        for (int64_t s = w; s < a.n_sym; s += 8) {
+        for (int64_t s = w; s < a.n_sym; s += NWF) {
             f += a.fsym[s * a.B + b];
             u += a.usym[s * a.B + b];
         }
@@ -1026,7 +1095,7 @@ static __global__ void __launch_bounds__(256) reduce_f_kernel(ReduceFArgs a) {
     if (w == 0 && b < a.B) {
         double ft = 0.0;
         int ut = 0;
-        for (int j = 0; j < 8; ++j) {
+        for (int j = 0; j < NWF; ++j) {
             ft += sf[j][lane];
             ut += su[j][lane];
         }
