@@ -181,6 +181,31 @@ def cpu_baseline(cfg, inst, X):
 # ------------------------------------------------------------------------------------------------ our arm
 
 
+def time_to_solve(P, args, device):
+    """BJ.metric time-to-solve: wall time of ffsat_solve from call to a verified SAT on planted c2
+    instances (random 7-SAT n=200 with a hidden satisfying assignment) at the configured ratio near the threshold
+    (alpha = 87.79) and at alpha = 65; 1024 restart points, ERWA + (ROF) rephasing, 200 PGD trials per round; one
+    run per seed; median and PAR-2 (an unsolved run counts 2 x cap)."""
+    out = []
+    for alpha in (87.79, 65.0):
+        inst = synth.config2(0, planted=True, alpha=alpha)
+        ctx = P.Context.from_instance(inst, device=device)
+        ctx.solve(batch=1024, max_restarts=1, seed=0, max_inner=5)          # warm-up (lazy module loading)
+        times, solved, rounds, best = [], 0, [], []
+        for seed in range(args.tts_seeds):
+            res, a = ctx.solve(batch=1024, max_restarts=10 ** 6, seed=1 + seed, max_inner=200, check_every=10,
+                               timeout_s=args.tts_cap)
+            ok = bool(res["sat"]) and ctx.check(a)[0] == 0
+            solved += ok
+            times.append(res["seconds"] if ok else 2 * args.tts_cap)
+            rounds.append(res["restarts"])
+            best.append(res["best_unsat"])
+        out.append({"instance": f"planted 7-SAT n={inst.n} m={inst.m} (alpha {alpha})", "batch": 1024,
+                    "seeds": args.tts_seeds, "solved": solved, "cap_s": args.tts_cap, "median_s": float(np.median(times)),
+                    "par2_s": float(np.mean(times)), "seconds": times, "restart_rounds": rounds, "best_unsat": best})
+    return {"runs": out, "note": "sat only after the exact host check (ffsat_check); unsolved = 2 x cap"}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -191,6 +216,8 @@ def main():
     ap.add_argument("--round-len", type=int, default=10)
     ap.add_argument("--no-flush", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--tts-seeds", type=int, default=3, help="time-to-solve seeds on the planted c2 instance (0 = skip)")
+    ap.add_argument("--tts-cap", type=float, default=10.0, help="per-seed wall-clock cap in seconds (PAR-2 uses 2x)")
     args = ap.parse_args()
     rank, world, local = env_rank()
     cfg = CONFIGS[args.config]
@@ -366,6 +393,8 @@ def main():
     roofline = {k: roofline[k] for k in ("bound", "achieved", "peak", "unit", "frac", "traffic")} | \
         {k: v for k, v in roofline.items() if k not in ("bound", "achieved", "peak", "unit", "frac", "traffic")}
 
+    tts = time_to_solve(P, args, local) if (rank == 0 and args.config == "c2" and args.tts_seeds > 0) else None
+
     if rank == 0:
         base = None if args.no_cpu_baseline or world > 1 else cpu_baseline(cfg, inst, xd.cpu().numpy())
         line = {"metric": "literal-gradient terms/s", "value": value, "unit": "terms/s", "n_gpus": world,
@@ -381,6 +410,8 @@ def main():
                 "e2e": e2e, "gpu_launches": launches, "roofline": roofline, "clocks": clk}
         if base is not None:
             line["cpu_baseline"] = base
+        if tts is not None:
+            line["time_to_solve"] = tts
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
