@@ -111,5 +111,6 @@ void eval_device_t(ffsat_ctx* c, const T* x, int64_t B, double* f, T* grad, int3
 // allow the tiled kernels of dtype T the dynamic shared memory they need (eval_f32.cu / eval_f64.cu)
 template <typename T>
 void set_tiled_smem(size_t bytes);
+void set_wide_smem(size_t bytes);   // eval_f32.cu
 
 }  // namespace ffsat

@@ -33,10 +33,10 @@ void plan(ffsat_ctx* c, int64_t B) {
     if (c->plan_B == B) return;
     const Layout& L = c->Lo;
     const size_t es = c->esize;
-    const int64_t PT = (B + 31) / 32;
+    const int64_t PT = L.wide ? (B + 63) / 64 : (B + 31) / 32;
     int cps = 8;
     if (L.path == 1) {
-        c->tiled_smem = tiled_smem_bytes(L.n, L.precision);
+        c->tiled_smem = L.wide ? wide_smem_bytes(L.n) : tiled_smem_bytes(L.n, L.precision);
         cps = std::max(1, (int)std::min<size_t>(8, (228 * 1024) / (c->tiled_smem + (L.precision == 64 ? 4352 : 2304) + 1024)));
     }
     const int64_t n_units = (int64_t)L.units.size();
@@ -67,6 +67,7 @@ void plan(ffsat_ctx* c, int64_t B) {
     if (L.path == 1) {
         if (L.precision == 64) set_tiled_smem<double>(c->tiled_smem);
         else set_tiled_smem<float>(c->tiled_smem);
+        if (L.wide) set_wide_smem(c->tiled_smem);
     }
     c->plan_B = B;
 }

@@ -227,6 +227,15 @@ size_t tiled_smem_bytes(int n, int precision) {
     return std::max<size_t>(es * (size_t)kTilePitch * (size_t)n, 3072);
 }
 
+size_t wide_smem_bytes(int n) { return std::max<size_t>(4 * (size_t)kWidePitch * (size_t)n, 6144); }  // >= the final f / unsat exchange (8 x 64 x 12 B)
+
+int wide_max_n() {
+    const size_t budget = 227 * 1024 - 4608;
+    int n = 0;
+    while (wide_smem_bytes(n + 1) <= budget) ++n;
+    return n;
+}
+
 int tiled_max_n(int precision) {
     const size_t budget = 227 * 1024 - 4608;   // minus the kernel's static stage buffers
     int n = 0;
@@ -471,10 +480,18 @@ Layout build_layout(const Formula& F, int path, int precision) {
 
     // ---- work units: tiled = the classes; global = runs of one bucket with <= 512 literals
     if (path == 1) {
+        // wide variant: fp32, every fast bucket one product channel with one shared k <= 16, n small enough
+        bool uniform = !Lo.fbuckets.empty();
+        for (const FastBucket& b : Lo.fbuckets) {
+            const int nch = (b.gA != 0) + (b.gB != 0) + (b.gX != 0);
+            uniform = uniform && nch == 1 && b.k <= 16 && b.k == Lo.fbuckets[0].k;
+        }
+        Lo.wide = precision == 32 && uniform && F.n <= wide_max_n();
+        const uint32_t pitch = Lo.wide ? (uint32_t)kWidePitch : (uint32_t)kTilePitch;
         Lo.tiled_words.assign(Lo.fast_words.size(), 0);
         for (size_t i = 0; i < Lo.fast_words.size(); ++i) {
             uint32_t w = Lo.fast_words[i];
-            Lo.tiled_words[i] = (w & 0x7fffffffu) * (uint32_t)kTilePitch | (w & 0x80000000u);
+            Lo.tiled_words[i] = (w & 0x7fffffffu) * pitch | (w & 0x80000000u);
         }
     }
     for (size_t bi = 0; bi < Lo.fbuckets.size(); ++bi) {

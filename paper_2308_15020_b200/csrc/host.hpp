@@ -76,6 +76,7 @@ int sym_roots(int k);               // roots per pass on the root path
 
 struct Layout {
     int32_t n = 0, path = 0, precision = 32, max_k = 0;
+    bool wide = false;                  // tiled path with 64 points per CTA (fp32, uniform single-channel k <= 16)
     int64_t m = 0, L = 0;
     std::vector<int64_t> order;     // position -> original constraint index (fast first, then sym)
     std::vector<int64_t> pos_of;    // original constraint index -> position
@@ -104,13 +105,16 @@ struct Layout {
 };
 
 constexpr int kTilePitch = 66;      // smem row pitch of the tiled kernel: x half-row (32 points + pad) | gradient half-row
-constexpr int kClassCap = 16;       // constraints per var-disjoint class (2 per warp of an 8-warp CTA)
+constexpr int kClassCap = 16;
+constexpr int kWidePitch = 132;     // wide tiled kernel row: x (64 points + 2 pad) | gradient (64 + 2)       // constraints per var-disjoint class (2 per warp of an 8-warp CTA)
 
 // Build everything; path: 0 auto, 1 tiled, 2 global; precision 0 auto / 32 / 64.
 Layout build_layout(const Formula& F, int path, int precision);
 // Tiled-path admission: the max n whose x and gradient tiles fit shared memory for the dtype.
 int tiled_max_n(int precision);
 size_t tiled_smem_bytes(int n, int precision);
+int wide_max_n();                   // largest n for the wide (64-point) fp32 tiled kernel
+size_t wide_smem_bytes(int n);
 // Greedy partition of one bucket's constraints into var-disjoint classes of at most `cap` members
 // (first fit over the most recent `window` open classes).  Returns class id per constraint.
 std::vector<int32_t> disjoint_classes(const std::vector<std::vector<int32_t>>& vars, int32_t n, int cap, int window);

@@ -573,6 +573,152 @@ __global__ void __launch_bounds__(256, (sizeof(T) == 4 ? (KMAX <= 8 ? 4 : 2) : (
 }
 
 // ------------------------------------------------------------------------------------------------
+// Wide tiled kernel (fp32, every fast constraint a single product channel with the same k <= 16, n <= 430):
+// as fast_tiled_kernel but each lane owns TWO points (b0 + 2 lane, b0 + 2 lane + 1), so a CTA covers 64
+// points.  One literal's address, sign and word serve both points; x and gradient values move as float2
+// (LDS.64 / STS.64) and every product runs as one packed f32x2 instruction (FFMA2 / FMUL2) for the two
+// points.  Row v of the smem tile = [x of 64 points | 2 pad | gradient of 64 points | 2 pad].
+constexpr int kWHalf = 66;
+constexpr int kWPitch = 2 * kWHalf;   // == kWidePitch of host.hpp
+
+template <int K>
+__device__ __forceinline__ void wide_clause(const BucketReg<float>& bk, const uint32_t* sw, float wc, const float* xl,
+                                            double& f0, double& f1, int& u0, int& u1) {
+    uint32_t w[K];
+    load_words_smem<K>(sw, w);
+    float2 xv[K];
+    uint32_t t0 = 0, t1 = 0;
+#pragma unroll
+    for (int i = 0; i < K; ++i) {
+        xv[i] = *reinterpret_cast<const float2*>(tile_at(xl, w[i]));
+        t0 += lit_true(xv[i].x, w[i]);
+        t1 += lit_true(xv[i].y, w[i]);
+    }
+    const float2 c0 = make_float2(bk.c0[0], bk.c0[0]);
+    float2 av[K], pre[K];
+    float2 run = make_float2(1.0f, 1.0f);
+#pragma unroll
+    for (int i = 0; i < K; ++i) {
+        const float cs = flip_sign(bk.c1[0], w[i]);
+        av[i] = __ffma2_rn(make_float2(cs, cs), xv[i], c0);
+        pre[i] = run;
+        run = __fmul2_rn(run, av[i]);
+    }
+    const float2 fe = __ffma2_rn(make_float2(bk.g[0], bk.g[0]), run, make_float2(bk.g0, bk.g0));
+    const float sw0 = bk.g[0] * wc;
+    float2 suf = make_float2(sw0, sw0);
+#pragma unroll
+    for (int i = K - 1; i >= 0; --i) {
+        float2* gp = reinterpret_cast<float2*>(const_cast<float*>(tile_at(xl, w[i])) + kWHalf);
+        const float cs = flip_sign(bk.c1[0], w[i]);
+        *gp = __ffma2_rn(__fmul2_rn(pre[i], suf), make_float2(cs, cs), *gp);
+        suf = __fmul2_rn(suf, av[i]);
+    }
+    f0 += (double)(wc * fe.x);
+    f1 += (double)(wc * fe.y);
+    u0 += rule_sat((int)t0, bk.tmin, bk.tmax, bk.parity) ? 0 : 1;
+    u1 += rule_sat((int)t1, bk.tmin, bk.tmax, bk.parity) ? 0 : 1;
+}
+
+// The staging of the next unit (words + weights) by warp 0 only: lanes copy 16-byte pieces.
+__device__ __forceinline__ void stage_unit_w0(const TiledArgs<float>& a, const UnitDev& U, TileStage<float>& st, int buf, int lane) {
+    const int nwords = min(unit_count(U) * unit_kp(U), kStageWords);
+    for (int q = lane * 4; q < nwords; q += 128) cp_async16(&st.words[buf][q], a.words + (int64_t)U.word_begin + q);
+    if (lane < min(unit_count(U), kStageCons)) cp_async_small<4>(&st.w[buf][lane], a.w_pos + (int64_t)U.pos_begin + lane);
+}
+
+template <int K>
+__global__ void __launch_bounds__(256, 2) fast_wide_kernel(TiledArgs<float> a) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];   // >= 6 KB (host: wide_smem_bytes)
+    __shared__ __align__(16) TileStage<float> st;
+    const int n = a.n;
+    float* xs = reinterpret_cast<float*>(smem_raw);              // [n][kWPitch]
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    const int64_t b0 = (int64_t)blockIdx.x * 64;
+    const int chunk = blockIdx.y;
+
+    for (int idx = threadIdx.x; idx < 64 * n; idx += blockDim.x) {
+        const int r = idx / n, v = idx - r * n;
+        const int64_t bb = b0 + r;
+        xs[v * kWPitch + r] = bb < a.B ? a.x[bb * n + v] + 0.0f : 0.0f;   // + 0 canonicalises -0.0
+        xs[v * kWPitch + kWHalf + r] = 0.0f;
+    }
+    __syncthreads();
+
+    double f0 = 0.0, f1 = 0.0;
+    int uc0 = 0, uc1 = 0;
+    const float* xl = xs + 2 * lane;
+    const int u0 = a.chunk_units[chunk], u1 = a.chunk_units[chunk + 1];
+    UnitDev cur{}, next{}, after{};
+    if (u0 < u1) {
+        cur = a.units[u0];
+        if (warp == 0) stage_unit_w0(a, cur, st, 0, lane);
+        if (u0 + 1 < u1) {
+            next = a.units[u0 + 1];
+            if (warp == 0) stage_unit_w0(a, next, st, 1, lane);
+        }
+        if (u0 + 2 < u1) after = a.units[u0 + 2];
+    }
+    cp_async_commit_wait_all();
+    __syncthreads();
+    int bucket = -1;
+    BucketReg<float> bk{};
+    int buf = 0;
+    for (int u = u0; u < u1; ++u) {
+        if (cur.bucket != bucket) {
+            bucket = cur.bucket;
+            bk = load_bucket<float>(a.buckets + bucket);
+        }
+        const uint32_t* sw = st.words[buf];
+        const float* swt = st.w[buf];
+        const int count = unit_count(cur);
+        for (int j = warp; j < count; j += nw) wide_clause<K>(bk, sw + j * K_PAD(K), swt[j], xl, f0, f1, uc0, uc1);
+        // advance: the next unit's words are ready, everybody is done with this buffer
+        cp_async_wait_all();
+        __syncthreads();
+        cur = next;
+        next = after;
+        buf ^= 1;
+        if (u + 2 < u1 && warp == 0) stage_unit_w0(a, next, st, buf ^ 1, lane);
+        cp_async_commit();
+        if (u + 3 < u1) after = a.units[u + 3];
+    }
+    // outputs: partial gradient tile (float2 per lane), partial f / unsat (fixed warp order)
+    const int64_t b = b0 + 2 * lane;
+    for (int v = warp; v < n; v += nw) {
+        const float2 g = *reinterpret_cast<const float2*>(xs + v * kWPitch + kWHalf + 2 * lane);
+        float* dst = a.P + ((int64_t)chunk * n + v) * a.B + b;
+        if (b + 1 < a.B && ((a.B & 1) == 0)) *reinterpret_cast<float2*>(dst) = g;
+        else {
+            if (b < a.B) dst[0] = g.x;
+            if (b + 1 < a.B) dst[1] = g.y;
+        }
+    }
+    __syncthreads();
+    double* fr = reinterpret_cast<double*>(smem_raw);         // [8][64], reuses the tiles
+    int* ur = reinterpret_cast<int*>(fr + 8 * 64);            // [8][64]
+    fr[warp * 64 + 2 * lane] = f0;
+    fr[warp * 64 + 2 * lane + 1] = f1;
+    ur[warp * 64 + 2 * lane] = uc0;
+    ur[warp * 64 + 2 * lane + 1] = uc1;
+    __syncthreads();
+    if (warp < 2) {
+        const int p = warp * 32 + lane;
+        const int64_t bp = b0 + p;
+        if (bp < a.B) {
+            double f = 0.0;
+            int uc = 0;
+            for (int w = 0; w < nw; ++w) {
+                f += fr[w * 64 + p];
+                uc += ur[w * 64 + p];
+            }
+            a.fpart[(int64_t)chunk * a.B + bp] = f;
+            a.upart[(int64_t)chunk * a.B + bp] = uc;
+        }
+    }
+}
+
+// ------------------------------------------------------------------------------------------------
 // Global fast kernel (large n).  grid = (ceil(B/32), n_chunks); block = 256.  xT [n][B].
 template <typename T>
 struct GlobalArgs {
