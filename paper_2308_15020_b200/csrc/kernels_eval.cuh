@@ -510,11 +510,26 @@ __global__ void __launch_bounds__(256, (sizeof(T) == 4 ? (KMAX <= 8 ? 4 : 2) : (
     const int64_t b = b0 + lane;
     const int chunk = blockIdx.y;
 
-    for (int idx = threadIdx.x; idx < 32 * n; idx += blockDim.x) {
-        int r = idx / n, v = idx - r * n;
-        int64_t bb = b0 + r;
-        xs[v * kPitch + r] = bb < a.B ? a.x[bb * n + v] + (T)0 : (T)0;   // + 0 canonicalises -0.0 to +0.0
-        Gs[v * kPitch + r] = (T)0;
+    {   // x tile load, 8 independent global loads in flight per thread
+        const int tot = 32 * n;
+        for (int base = 0; base < tot; base += 8 * 256) {
+            T v8[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                const int idx = base + q * 256 + (int)threadIdx.x;
+                const int r = idx / n, v = idx - r * n;
+                v8[q] = (idx < tot && b0 + r < a.B) ? __ldg(a.x + (b0 + r) * n + v) : (T)0;
+            }
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                const int idx = base + q * 256 + (int)threadIdx.x;
+                if (idx < tot) {
+                    const int r = idx / n, v = idx - r * n;
+                    xs[v * kPitch + r] = v8[q] + (T)0;   // + 0 canonicalises -0.0 to +0.0
+                    Gs[v * kPitch + r] = (T)0;
+                }
+            }
+        }
     }
     __syncthreads();
 
@@ -607,13 +622,20 @@ __device__ __forceinline__ void wide_clause(const BucketReg<float>& bk, const ui
     const float2 fe = __ffma2_rn(make_float2(bk.g[0], bk.g[0]), run, make_float2(bk.g0, bk.g0));
     const float sw0 = bk.g[0] * wc;
     float2 suf = make_float2(sw0, sw0);
+    // the constraint's variables are distinct, so all gradient entries are read before any is written
+    // (the compiler cannot prove the addresses differ; loading them up front removes the LDS -> FFMA2 -> STS
+    // serialisation per literal)
+    float2 gv[K];
+#pragma unroll
+    for (int i = 0; i < K; ++i) gv[i] = *reinterpret_cast<const float2*>(tile_at(xl, w[i]) + kWHalf);
 #pragma unroll
     for (int i = K - 1; i >= 0; --i) {
-        float2* gp = reinterpret_cast<float2*>(const_cast<float*>(tile_at(xl, w[i])) + kWHalf);
         const float cs = flip_sign(bk.c1[0], w[i]);
-        *gp = __ffma2_rn(__fmul2_rn(pre[i], suf), make_float2(cs, cs), *gp);
+        gv[i] = __ffma2_rn(__fmul2_rn(pre[i], suf), make_float2(cs, cs), gv[i]);
         suf = __fmul2_rn(suf, av[i]);
     }
+#pragma unroll
+    for (int i = 0; i < K; ++i) *reinterpret_cast<float2*>(const_cast<float*>(tile_at(xl, w[i])) + kWHalf) = gv[i];
     f0 += (double)(wc * fe.x);
     f1 += (double)(wc * fe.y);
     u0 += rule_sat((int)t0, bk.tmin, bk.tmax, bk.parity) ? 0 : 1;
@@ -637,11 +659,27 @@ __global__ void __launch_bounds__(256, 2) fast_wide_kernel(TiledArgs<float> a) {
     const int64_t b0 = (int64_t)blockIdx.x * 64;
     const int chunk = blockIdx.y;
 
-    for (int idx = threadIdx.x; idx < 64 * n; idx += blockDim.x) {
-        const int r = idx / n, v = idx - r * n;
-        const int64_t bb = b0 + r;
-        xs[v * kWPitch + r] = bb < a.B ? a.x[bb * n + v] + 0.0f : 0.0f;   // + 0 canonicalises -0.0
-        xs[v * kWPitch + kWHalf + r] = 0.0f;
+    // x tile load: 8 independent global loads in flight per thread (the loop is latency-bound otherwise)
+    {
+        const int tot = 64 * n;
+        for (int base = 0; base < tot; base += 8 * 256) {
+            float v8[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                const int idx = base + q * 256 + (int)threadIdx.x;
+                const int r = idx / n, v = idx - r * n;
+                v8[q] = (idx < tot && b0 + r < a.B) ? __ldg(a.x + (b0 + r) * n + v) : 0.0f;
+            }
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                const int idx = base + q * 256 + (int)threadIdx.x;
+                if (idx < tot) {
+                    const int r = idx / n, v = idx - r * n;
+                    xs[v * kWPitch + r] = v8[q] + 0.0f;   // + 0 canonicalises -0.0
+                    xs[v * kWPitch + kWHalf + r] = 0.0f;
+                }
+            }
+        }
     }
     __syncthreads();
 

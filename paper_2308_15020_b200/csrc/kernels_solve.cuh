@@ -170,10 +170,24 @@ __global__ void __launch_bounds__(256) check_kernel(CheckArgs a) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int64_t b0 = (int64_t)blockIdx.x * 32, b = b0 + lane;
     const bool bv = b < a.B;
-    if (SMEM) {
-        for (int idx = threadIdx.x; idx < 32 * a.n; idx += blockDim.x) {
-            const int r = idx / a.n, v = idx - r * a.n;
-            xs[v * 33 + r] = b0 + r < a.B ? X[(b0 + r) * a.n + v] : (T)0;
+    if (SMEM) {   // x tile, 8 independent loads in flight per thread
+        const int tot = 32 * a.n;
+        for (int base = 0; base < tot; base += 8 * 256) {
+            T v8[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                const int idx = base + q * 256 + (int)threadIdx.x;
+                const int r = idx / a.n, v = idx - r * a.n;
+                v8[q] = (idx < tot && b0 + r < a.B) ? __ldg(X + (b0 + r) * a.n + v) : (T)0;
+            }
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                const int idx = base + q * 256 + (int)threadIdx.x;
+                if (idx < tot) {
+                    const int r = idx / a.n, v = idx - r * a.n;
+                    xs[v * 33 + r] = v8[q];
+                }
+            }
         }
         __syncthreads();
     }
@@ -183,7 +197,21 @@ __global__ void __launch_bounds__(256) check_kernel(CheckArgs a) {
     for (int64_t c = c0 + warp; c < c1; c += 8) {
         const int64_t lo = a.off[c], hi = a.off[c + 1];
         int t = 0;
-        for (int64_t i = lo; i < hi; ++i) {
+        int64_t i = lo;
+        for (; i + 4 <= hi; i += 4) {           // four literals' loads in flight
+            uint32_t w[4];
+            T xv[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) w[q] = __ldg(a.words + i + q);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const uint32_t v = w[q] & 0x7fffffffu;
+                xv[q] = SMEM ? xs[v * 33 + lane] : (bv ? X[(int64_t)v * a.B + b] : (T)0);
+            }
+#pragma unroll
+            for (int q = 0; q < 4; ++q) t += (int)((xv[q] < (T)0) != ((int)w[q] < 0));
+        }
+        for (; i < hi; ++i) {
             const uint32_t w = __ldg(a.words + i);
             const uint32_t v = w & 0x7fffffffu;
             const T xv = SMEM ? xs[v * 33 + lane] : (bv ? X[(int64_t)v * a.B + b] : (T)0);
