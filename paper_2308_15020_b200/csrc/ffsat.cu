@@ -261,6 +261,19 @@ void search_iterate(ffsat_search* s, int n_iters, cudaStream_t st) {
     s->iters_issued += n_iters;
 }
 
+template <typename T>
+void launch_check_uniform(int k, dim3 grid, size_t tile, const dev::CheckArgs& a, cudaStream_t st) {
+    switch (k) {
+#define FFSAT_CK(K) case K: \
+        CK(cudaFuncSetAttribute(dev::check_uniform_kernel<T, K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tile)); \
+        dev::check_uniform_kernel<T, K><<<grid, 256, tile, st>>>(a); break;
+        FFSAT_CK(1) FFSAT_CK(2) FFSAT_CK(3) FFSAT_CK(4) FFSAT_CK(5) FFSAT_CK(6) FFSAT_CK(7) FFSAT_CK(8)
+        FFSAT_CK(9) FFSAT_CK(10) FFSAT_CK(11) FFSAT_CK(12) FFSAT_CK(13) FFSAT_CK(14) FFSAT_CK(15) FFSAT_CK(16)
+#undef FFSAT_CK
+    default: throw Error(FFSAT_ERR_ARG, "uniform check needs k <= 16");
+    }
+}
+
 void search_check(ffsat_search* s, cudaStream_t st) {
     ffsat_ctx* c = s->ctx;
     const Layout& L = c->Lo;
@@ -276,11 +289,19 @@ void search_check(ffsat_search* s, cudaStream_t st) {
     a.U = s->U.as<int32_t>(); a.unsat = s->unsat.as<int32_t>();
     const int64_t PT = (s->B + 31) / 32;
     const int cps = smem ? std::max(1, (int)std::min<size_t>(8, (228 * 1024) / (tile + 2048))) : 8;
-    const int64_t want = std::max<int64_t>(1, (int64_t)c->num_sm * cps * 2 / PT);
+    const int64_t want = std::max<int64_t>(1, (int64_t)c->num_sm * cps / PT);   // one wave: every CTA re-loads the x tile
     const int64_t chunks = std::min<int64_t>(std::min<int64_t>(want, 65535), (L.m + 7) / 8);
     a.cons_per_cta = (L.m + chunks - 1) / chunks;
     dim3 grid((unsigned)PT, (unsigned)((L.m + a.cons_per_cta - 1) / a.cons_per_cta));
-    if (smem) {
+    // uniform k <= 16: the specialised check (offsets c k, sign-bit counts)
+    const int ku = (int)(L.m > 0 ? L.L / L.m : 0);
+    const bool uniform = smem && ku >= 1 && ku <= 16 && (int64_t)ku * L.m == L.L && L.L < INT32_MAX && L.max_k == ku;
+    if (uniform) {
+        a.X = s->X.p;
+        if (L.precision == 64) launch_check_uniform<double>(ku, grid, tile, a, st);
+        else launch_check_uniform<float>(ku, grid, tile, a, st);
+        s->ctx->launches += 1;
+    } else if (smem) {
         a.X = s->X.p;
         if (L.precision == 64) {
             CK(cudaFuncSetAttribute(dev::check_kernel<double, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tile));

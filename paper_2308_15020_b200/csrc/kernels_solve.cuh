@@ -161,6 +161,9 @@ struct CheckArgs {
     int32_t* unsat;           // [B]
 };
 
+__device__ __forceinline__ uint32_t sign_xor(float xv, uint32_t w) { return (__float_as_uint(xv) ^ w) >> 31; }
+__device__ __forceinline__ uint32_t sign_xor(double xv, uint32_t w) { return ((uint32_t)__double2hiint(xv) ^ w) >> 31; }
+
 template <typename T, bool SMEM>
 __global__ void __launch_bounds__(256) check_kernel(CheckArgs a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -218,6 +221,67 @@ __global__ void __launch_bounds__(256) check_kernel(CheckArgs a) {
             t += (int)((xv < (T)0) != ((int)w < 0));
         }
         const bool uns = bv && !rule_sat(t, a.rule[3 * c], a.rule[3 * c + 1], a.rule[3 * c + 2]);
+        mine += uns ? 1 : 0;
+        const int cnt = __popc(__ballot_sync(0xffffffffu, uns));
+        if (lane == 0 && cnt) atomicAdd(a.U + c, cnt);
+    }
+    ucnt[warp][lane] = mine;
+    __syncthreads();
+    if (warp == 0 && bv) {
+        int tot = 0;
+        for (int w = 0; w < 8; ++w) tot += ucnt[w][lane];
+        if (tot) atomicAdd(a.unsat + b, tot);
+    }
+}
+
+// Same check when every constraint has the same length K <= 16 and n fits the smem tile (the uniform k-SAT
+// case): CSR offsets are c K, the K literal words are read as uniform loads, and the True-literal count uses
+// the sign bit of the (canonical-zero) tile value: one LDS, one LOP3 and one LEA.HI per literal.
+template <typename T, int K>
+__global__ void __launch_bounds__(256) check_uniform_kernel(CheckArgs a) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    __shared__ int ucnt[8][32];
+    const T* X = reinterpret_cast<const T*>(a.X);
+    T* xs = reinterpret_cast<T*>(smem_raw);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t b0 = (int64_t)blockIdx.x * 32, b = b0 + lane;
+    const bool bv = b < a.B;
+    {
+        const int tot = 32 * a.n;
+        for (int base = 0; base < tot; base += 8 * 256) {
+            T v8[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                const int idx = base + q * 256 + (int)threadIdx.x;
+                const int r = idx / a.n, v = idx - r * a.n;
+                v8[q] = (idx < tot && b0 + r < a.B) ? __ldg(X + (b0 + r) * a.n + v) : (T)0;
+            }
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                const int idx = base + q * 256 + (int)threadIdx.x;
+                if (idx < tot) {
+                    const int r = idx / a.n, v = idx - r * a.n;
+                    xs[v * 33 + r] = v8[q] + (T)0;   // canonical zero: the sign bit is exactly x < 0
+                }
+            }
+        }
+        __syncthreads();
+    }
+    const int c0 = (int)((int64_t)blockIdx.y * a.cons_per_cta);
+    const int c1 = (int)min(a.m, (int64_t)c0 + a.cons_per_cta);
+    const T* xl = xs + lane;
+    int mine = 0;
+    for (int c = c0 + warp; c < c1; c += 8) {
+        uint32_t w[K];
+#pragma unroll
+        for (int i = 0; i < K; ++i) w[i] = __ldg(a.words + c * K + i);
+        uint32_t t = 0;
+#pragma unroll
+        for (int i = 0; i < K; ++i) {
+            const T xv = xl[(w[i] & 0x7fffffffu) * 33];
+            t += sign_xor(xv, w[i]);
+        }
+        const bool uns = bv && !rule_sat((int)t, __ldg(a.rule + 3 * c), __ldg(a.rule + 3 * c + 1), __ldg(a.rule + 3 * c + 2));
         mine += uns ? 1 : 0;
         const int cnt = __popc(__ballot_sync(0xffffffffu, uns));
         if (lane == 0 && cnt) atomicAdd(a.U + c, cnt);
