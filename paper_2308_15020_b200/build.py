@@ -11,7 +11,8 @@ from concurrent.futures import ThreadPoolExecutor
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
-SRC = [os.path.join(CSRC, f) for f in ("ffsat.cu", "eval.cu", "eval_f32.cu", "eval_f64.cu", "host.cpp")]
+SRC = [os.path.join(CSRC, f) for f in ("ffsat.cu", "eval.cu", "eval_f32.cu", "eval_f64.cu", "sym_f32.cu", "sym_f64.cu",
+                                       "host.cpp")]
 OBJDIR = os.path.join(HERE, "build")
 OUT = os.path.join(HERE, "libffsat.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")

@@ -10,6 +10,10 @@
 #include "host.hpp"
 
 namespace ffsat {
+namespace dev {
+template <typename T>
+struct SymArgs;
+}
 
 #define CK(call)                                                                                     \
     do {                                                                                             \
@@ -56,7 +60,7 @@ inline unsigned blocks_for(int64_t n, int t) { return (unsigned)((n + t - 1) / t
 
 }  // namespace ffsat
 
-#define FFSAT_SIDE_STREAMS 4
+#define FFSAT_SIDE_STREAMS 8
 
 struct ffsat_ctx {
     ffsat::Formula F;
@@ -112,5 +116,8 @@ void eval_device_t(ffsat_ctx* c, const T* x, int64_t B, double* f, T* grad, int3
 template <typename T>
 void set_tiled_smem(size_t bytes);
 void set_wide_smem(size_t bytes);   // eval_f32.cu
+// one root-path launch class (sym_f32.cu / sym_f64.cu)
+template <typename T>
+void launch_sym_class(const SymClass& cl, const dev::SymArgs<T>& a, cudaStream_t st);
 
 }  // namespace ffsat

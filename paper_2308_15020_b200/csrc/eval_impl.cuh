@@ -46,32 +46,6 @@ inline int fast_kmax(const Layout& L) {
     return km;
 }
 
-inline void set_sym_smem(const void* kern, size_t bytes) {
-    if (bytes > 48 * 1024) CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
-}
-
-// One root-path class launch: a CTA of G threads per (constraint, point) item, C literals per thread.
-template <typename T>
-void launch_sym_class(const SymClass& cl, const dev::SymArgs<T>& a, cudaStream_t st) {
-    const int64_t items = (cl.end - cl.begin) * a.B;
-    if (items == 0) return;
-    if (items > INT32_MAX) throw Error(FFSAT_ERR_ARG, "too many root-path items for one launch");
-    const unsigned g = (unsigned)items;
-    const size_t smem = (size_t)cl.max_mp * 8 * sizeof(T);   // the root table of the longest signature
-    switch (cl.G / 32 * 1000 + cl.C * 10 + cl.R) {
-#define FFSAT_SYM(NW, C, R) case NW * 1000 + C * 10 + R: \
-        set_sym_smem((const void*)dev::sym_item_kernel<T, NW, C, R>, smem); \
-        dev::sym_item_kernel<T, NW, C, R><<<g, 32 * NW, smem, st>>>(a, cl.begin); break;
-        FFSAT_SYM(1, 1, 1) FFSAT_SYM(1, 4, 1)
-        FFSAT_SYM(1, 16, 1) FFSAT_SYM(2, 16, 1) FFSAT_SYM(4, 16, 1) FFSAT_SYM(6, 16, 1) FFSAT_SYM(8, 16, 1)
-        FFSAT_SYM(1, 12, 2) FFSAT_SYM(2, 12, 2) FFSAT_SYM(4, 12, 2) FFSAT_SYM(6, 12, 2) FFSAT_SYM(8, 12, 2)
-        FFSAT_SYM(1, 16, 2) FFSAT_SYM(2, 16, 2) FFSAT_SYM(4, 16, 2) FFSAT_SYM(6, 16, 2) FFSAT_SYM(8, 16, 2)
-        FFSAT_SYM(1, 8, 2) FFSAT_SYM(2, 8, 2) FFSAT_SYM(4, 8, 2) FFSAT_SYM(6, 8, 2) FFSAT_SYM(8, 8, 2)
-#undef FFSAT_SYM
-    default: throw Error(FFSAT_ERR_ARG, "unsupported root-path launch class");
-    }
-}
-
 // f (fp64), grad (T, may be null), unsat (int32, may be null) at device points x [B][n]; async on st.
 template <typename T>
 void eval_device_t(ffsat_ctx* c, const T* x, int64_t B, double* f, T* grad, int32_t* unsat, const T* w_pos, cudaStream_t st,
@@ -94,7 +68,7 @@ void eval_device_t(ffsat_ctx* c, const T* x, int64_t B, double* f, T* grad, int3
         a.sigs = c->sigs.as<dev::SymSigDev>(); a.coef = c->coef.as<T>(); a.w_sym = w_pos + L.n_fast;
         a.tb_fast = L.tb_fast; a.Tb = c->Tb.as<T>(); a.fsym = c->fsym.as<double>(); a.usym = c->usym.as<int32_t>();
         const size_t ncl = L.sym_classes.size();
-        const bool fork = !profiled && (ncl > 1 || L.n_fast > 0);
+        const bool fork = ncl > 1 || (!profiled && L.n_fast > 0);
         if (fork) {
             c->ensure_side_streams();
             CK(cudaEventRecord(c->ev_fork, st));

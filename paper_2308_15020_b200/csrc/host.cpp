@@ -7,7 +7,6 @@
 #include <cerrno>
 #include <climits>
 #include <cmath>
-#include <cstdlib>
 #include <cstring>
 #include <numeric>
 #include <sstream>
@@ -277,32 +276,21 @@ std::vector<int32_t> disjoint_classes(const std::vector<std::vector<int32_t>>& v
 
 // ------------------------------------------------------------------------------- A2: layout
 
-// Root path launch geometry: C literals per thread (1 for k <= 32, 4 for k <= 128, else the long-chunk
-// size) and R roots per pass, groups of 1..8 warps per (constraint, point) item.  Longer chunks amortise
-// the per-root scan across lanes; R = 2 interleaves two independent product chains.
-static int long_variant() {
-    static const int v = [] {
-        const char* e = std::getenv("FFSAT_SYM_VARIANT");   // development hook: 0 = C16/R1, 1 = C12/R2, 2 = C16/R2, 3 = C8/R2
-        return e ? std::atoi(e) : 0;
-    }();
-    return v;
+// Root path launch geometry.  k <= 32: one warp, one literal per lane; k <= 128: one warp, four per lane.
+// Longer: the smallest of a short ladder of (NW warps, C literals per thread) capacities 32 NW C that holds
+// k -- padding slots cost full root-sweep work, so the ladder keeps them under ~25% (typically ~10%), while
+// keeping the number of distinct launch classes small (each class is one launch on its own side stream).
+static void sym_geom(int k, int* nw_out, int* c_out) {
+    if (k <= 32) { *nw_out = 1; *c_out = 1; return; }
+    if (k <= 128) { *nw_out = 1; *c_out = 4; return; }
+    static const int ladder[][2] = {{1, 8}, {1, 16}, {2, 12}, {2, 16}, {4, 10}, {3, 16}, {4, 14}, {4, 16}, {6, 16}, {8, 16}};
+    for (const auto& g : ladder)
+        if (32 * g[0] * g[1] >= k) { *nw_out = g[0]; *c_out = g[1]; return; }
+    throw Error(FFSAT_ERR_ARG, "root-path constraint too long for one thread group (k > 4096)");
 }
-int sym_chunk(int k) {
-    if (k <= 32) return 1;
-    if (k <= 128) return 4;
-    static const int C[4] = {16, 12, 16, 8};
-    return C[long_variant() & 3];
-}
-int sym_roots(int k) { return k <= 128 ? 1 : (long_variant() & 3) == 0 ? 1 : 2; }
-int sym_group(int k) {
-    const int C = sym_chunk(k);
-    int nw = (k + 32 * C - 1) / (32 * C);
-    if (nw == 3) nw = 4;
-    if (nw == 5) nw = 6;
-    if (nw == 7) nw = 8;
-    if (nw > 8) throw Error(FFSAT_ERR_ARG, "root-path constraint too long for one thread group");
-    return 32 * nw;
-}
+int sym_chunk(int k) { int nw, c; sym_geom(k, &nw, &c); return c; }
+int sym_roots(int) { return 1; }
+int sym_group(int k) { int nw, c; sym_geom(k, &nw, &c); return 32 * nw; }
 
 Layout build_layout(const Formula& F, int path, int precision) {
     Layout Lo;

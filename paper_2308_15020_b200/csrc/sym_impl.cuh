@@ -1,0 +1,32 @@
+// sym_impl.cuh -- launch of the root-of-unity path classes (sym_item_kernel), instantiated per dtype by
+// sym_f32.cu / sym_f64.cu (separate translation units: the kernel has one instantiation per (NW, C)).
+#pragma once
+#include "ctx.hpp"
+#include "kernels_eval.cuh"
+
+namespace ffsat {
+
+inline void set_sym_smem(const void* kern, size_t bytes) {
+    if (bytes > 48 * 1024) CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+}
+
+// One root-path class launch: a CTA of G threads per (constraint, point) item, C literals per thread.
+template <typename T>
+void launch_sym_class(const SymClass& cl, const dev::SymArgs<T>& a, cudaStream_t st) {
+    const int64_t items = (cl.end - cl.begin) * a.B;
+    if (items == 0) return;
+    if (items > INT32_MAX) throw Error(FFSAT_ERR_ARG, "too many root-path items for one launch");
+    const unsigned g = (unsigned)items;
+    const size_t smem = (size_t)cl.max_mp * 8 * sizeof(T);   // the root table of the longest signature
+    switch (cl.G / 32 * 1000 + cl.C * 10 + cl.R) {
+#define FFSAT_SYM(NW, C) case NW * 1000 + C * 10 + 1: \
+        set_sym_smem((const void*)dev::sym_item_kernel<T, NW, C, 1>, smem); \
+        dev::sym_item_kernel<T, NW, C, 1><<<g, 32 * NW, smem, st>>>(a, cl.begin); break;
+        FFSAT_SYM(1, 1) FFSAT_SYM(1, 4) FFSAT_SYM(1, 8) FFSAT_SYM(1, 16) FFSAT_SYM(2, 12) FFSAT_SYM(2, 16)
+        FFSAT_SYM(4, 10) FFSAT_SYM(3, 16) FFSAT_SYM(4, 14) FFSAT_SYM(4, 16) FFSAT_SYM(6, 16) FFSAT_SYM(8, 16)
+#undef FFSAT_SYM
+    default: throw Error(FFSAT_ERR_ARG, "unsupported root-path launch class");
+    }
+}
+
+}  // namespace ffsat
