@@ -289,6 +289,8 @@ static void sym_geom(int k, int* nw_out, int* c_out) {
     throw Error(FFSAT_ERR_ARG, "root-path constraint too long for one thread group (k > 4096)");
 }
 int sym_chunk(int k) { int nw, c; sym_geom(k, &nw, &c); return c; }
+// roots per pass: 1 with the factors kept in registers (measured faster than recomputing them for a
+// higher occupancy or than two roots per pass: profiles/r01_bench_c3_*.json)
 int sym_roots(int) { return 1; }
 int sym_group(int k) { int nw, c; sym_geom(k, &nw, &c); return 32 * nw; }
 

@@ -1008,7 +1008,7 @@ __device__ __forceinline__ void load_ab(const T* cf, int m, int Mp, cplx<T> (&al
 // R roots m .. m + R - 1 of one item (independent product chains interleaved for instruction-level
 // parallelism).  R == 1 keeps the factors phi_j in registers; R > 1 recomputes them in the forward sweep
 // (the registers go to the second chain instead).
-template <typename T, int NW, int C, int R>
+template <typename T, int NW, int C, int R, bool KEEP = (R == 1)>
 __device__ __forceinline__ void sym_roots(const T* cf, int m, int Mp, int lane, int warp, int t, const T (&l)[C], T (&term)[C],
                                           double& fe_acc, cplx<T> (*wtot)[2][NW], cplx<T> (&al)[R], cplx<T> (&be)[R]) {
     const cplx<T> one{(T)1, (T)0};
@@ -1022,7 +1022,7 @@ __device__ __forceinline__ void sym_roots(const T* cf, int m, int Mp, int lane, 
 #pragma unroll
         for (int r = 0; r < R; ++r) {
             const cplx<T> ph{fmaT(be[r].re, l[j], al[r].re), fmaT(be[r].im, l[j], al[r].im)};
-            if (R == 1) ph1[j] = ph;
+            if (KEEP) ph1[j] = ph;
             insuf[r][j] = suf[r];
             suf[r] = cmul(suf[r], ph);
         }
@@ -1080,14 +1080,14 @@ __device__ __forceinline__ void sym_roots(const T* cf, int m, int Mp, int lane, 
         A[r] = cmul(cmul(Hm, P[r]), S[r]);
         alf[r] = al[r];
         bef[r] = be[r];
-        if (R > 1) { opaque(alf[r].re); opaque(alf[r].im); opaque(bef[r].re); opaque(bef[r].im); }
+        if (!KEEP) { opaque(alf[r].re); opaque(alf[r].im); opaque(bef[r].re); opaque(bef[r].im); }
     }
 #pragma unroll
     for (int j = 0; j < C; ++j) {
 #pragma unroll
         for (int r = 0; r < R; ++r) {
             term[j] = fmaT(A[r].re, insuf[r][j].re, fmaT(-A[r].im, insuf[r][j].im, term[j]));
-            const cplx<T> ph = R == 1 ? ph1[j] : cplx<T>{fmaT(bef[r].re, l[j], alf[r].re), fmaT(bef[r].im, l[j], alf[r].im)};
+            const cplx<T> ph = KEEP ? ph1[j] : cplx<T>{fmaT(bef[r].re, l[j], alf[r].re), fmaT(bef[r].im, l[j], alf[r].im)};
             A[r] = cmul(A[r], ph);
         }
     }
@@ -1105,8 +1105,11 @@ __device__ __forceinline__ void sym_roots(const T* cf, int m, int Mp, int lane, 
     }
 }
 
+// R = 0: one root per pass with the factors recomputed in the forward sweep, fewer registers (3 CTAs of
+// 4 warps per SM); R = 1: factors kept in registers; R = 2: two roots per pass.
 template <typename T, int NW, int C, int R>
-__global__ void __launch_bounds__(32 * NW, NW >= 8 ? 1 : 8 / NW) sym_item_kernel(SymArgs<T> a, int64_t s_begin) {
+__global__ void __launch_bounds__(32 * NW, R == 0 ? (12 / NW > 0 ? 12 / NW : 1) : (NW >= 8 ? 1 : 8 / NW))
+sym_item_kernel(SymArgs<T> a, int64_t s_begin) {
     extern __shared__ __align__(16) unsigned char sym_smem[];   // the signature's root table, M' x 8 T
     __shared__ cplx<T> wtot[2][2][NW];   // [root-batch parity][root in batch][warp] chunk-product totals
     __shared__ int tcnt[NW];
@@ -1148,10 +1151,12 @@ __global__ void __launch_bounds__(32 * NW, NW >= 8 ? 1 : 8 / NW) sym_item_kernel
         __syncthreads();
     }
     const cplx<T> one{(T)1, (T)0};
-    cplx<T> al[R], be[R];
-    load_ab<T, R>(cf, 0, sg.Mp, al, be);
+    cplx<T> al[R == 0 ? 1 : R], be[R == 0 ? 1 : R];
+    load_ab<T, (R == 0 ? 1 : R)>(cf, 0, sg.Mp, al, be);
     int m = 0;
-    for (; m + R <= sg.Mp; m += R) sym_roots<T, NW, C, R>(cf, m, sg.Mp, lane, warp, t, l, term, fe_acc, wtot, al, be);
+    constexpr int RP = R == 0 ? 1 : R;   // roots per pass
+    for (; m + RP <= sg.Mp; m += RP)
+        sym_roots<T, NW, C, RP, (R == 1)>(cf, m, sg.Mp, lane, warp, t, l, term, fe_acc, wtot, al, be);
     if (R > 1 && m < sg.Mp) {   // odd remainder: one root (al[0], be[0] hold it)
         cplx<T> al1[1] = {al[0]}, be1[1] = {be[0]};
         sym_roots<T, NW, C, 1>(cf, m, sg.Mp, lane, warp, t, l, term, fe_acc, wtot, al1, be1);
