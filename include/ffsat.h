@@ -81,7 +81,8 @@ typedef struct {
 typedef struct {
     int32_t precision;  /* 0 = auto (64 iff some non-fast-path constraint has k > 64), 32, 64 */
     int32_t device;     /* CUDA device ordinal; -1 = host-only context (no GPU needed) */
-    int32_t path;       /* 0 = auto, 1 = force on-chip tiled fast path, 2 = force global path */
+    int32_t path;       /* 0 = auto, 1 = force on-chip tiled fast path (64-point kernel when eligible),
+                           2 = force global path, 3 = tiled path with the 32-point kernel only */
     int32_t reserved;
 } ffsat_options;
 
@@ -96,6 +97,7 @@ typedef struct {
     int64_t n_sym_lits;
     int64_t sym_root_lits;  /* sum over sym constraints of k * M', M' = floor((k+1)/2) */
     int32_t path;           /* 1 tiled, 2 global */
+    int32_t wide;           /* 1 if the tiled path uses the 64-point (two points per lane) kernel */
     int32_t max_k;
     int64_t device_bytes;   /* persistent device memory held by the context */
 } ffsat_info_t;

@@ -445,7 +445,7 @@ ffsat_status ffsat_info(const ffsat_ctx* c, ffsat_info_t* o) {
     const Layout& L = c->Lo;
     o->n_vars = L.n; o->precision = L.precision; o->n_cons = L.m; o->n_lits = L.L;
     o->n_fast_cons = L.n_fast; o->n_sym_cons = L.n_sym; o->n_fast_lits = L.n_fast_lits; o->n_sym_lits = L.n_sym_lits;
-    o->sym_root_lits = L.sym_root_lits; o->path = L.path; o->max_k = L.max_k; o->device_bytes = c->persistent_bytes;
+    o->sym_root_lits = L.sym_root_lits; o->path = L.path; o->wide = L.wide ? 1 : 0; o->max_k = L.max_k; o->device_bytes = c->persistent_bytes;
     return FFSAT_OK;
     ABI_CATCH(nullptr)
 }

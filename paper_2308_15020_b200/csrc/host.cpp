@@ -334,9 +334,11 @@ Layout build_layout(const Formula& F, int path, int precision) {
     });
 
     // ---- path: tiled (x and gradient tiles in shared memory) when n fits, else global
+    const bool allow_wide = path != 3;   // 3 = tiled path with the 32-point kernel only (tests)
+    if (path == 3) path = 1;
     if (path == 0) path = (!fast_ids.empty() && F.n <= tiled_max_n(precision)) ? 1 : 2;
     if (path == 1 && F.n > tiled_max_n(precision)) throw Error(FFSAT_ERR_ARG, "tiled path needs n <= " + std::to_string(tiled_max_n(precision)));
-    if (path != 1 && path != 2) throw Error(FFSAT_ERR_ARG, "path must be 0, 1 or 2");
+    if (path != 1 && path != 2) throw Error(FFSAT_ERR_ARG, "path must be 0, 1, 2 or 3");
     Lo.path = path;
 
     // ---- tiled path: within each (k, variant) run, group constraints into var-disjoint classes and make
@@ -476,7 +478,7 @@ Layout build_layout(const Formula& F, int path, int precision) {
             const int nch = (b.gA != 0) + (b.gB != 0) + (b.gX != 0);
             uniform = uniform && nch == 1 && b.k <= 16 && b.k == Lo.fbuckets[0].k;
         }
-        Lo.wide = precision == 32 && uniform && F.n <= wide_max_n();
+        Lo.wide = allow_wide && precision == 32 && uniform && F.n <= wide_max_n();
         const uint32_t pitch = Lo.wide ? (uint32_t)kWidePitch : (uint32_t)kTilePitch;
         Lo.tiled_words.assign(Lo.fast_words.size(), 0);
         for (size_t i = 0; i < Lo.fast_words.size(); ++i) {

@@ -7,7 +7,7 @@
 namespace ffsat {
 
 inline void set_sym_smem(const void* kern, size_t bytes) {
-    if (bytes > 48 * 1024) CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+    if (bytes > 40 * 1024) CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));  // + static smem must fit 48 KB otherwise
 }
 
 // One root-path class launch: a CTA of G threads per (constraint, point) item, C literals per thread.

@@ -326,3 +326,62 @@ def test_solve_planted_hybrid():
     if r["sat"]:
         assert ctx.check(a)[0] == 0
     assert r["best_unsat"] >= 0
+
+
+# ------------------------------------------------------------------ kernel variants and launch geometries
+
+
+@pytest.mark.parametrize("k,kind", [(3, 0), (7, 0), (5, 1), (16, 2)])
+def test_wide_and_narrow_tiled_kernels(k, kind):
+    """Uniform single-channel formulas take the 64-point (two points per lane, f32x2) tiled kernel; path 3
+    forces the 32-point kernel.  Both against the oracle, odd and single-point batches, n at the wide limit."""
+    n = 430
+    rng = np.random.default_rng(5)
+    m = 3 * n
+    lits = []
+    for _ in range(m):
+        vs = rng.choice(n, size=k, replace=False) + 1
+        lits.append(np.where(rng.random(k) < 0.5, -vs, vs))
+    inst = synth._build(f"uniform_k{k}_kind{kind}", n, [kind] * m, [0] * m, lits)
+    for path, wide in ((0, 1), (3, 0)):
+        ctx = P.Context.from_instance(inst, precision=32, path=path, device=0)
+        assert ctx.info["path"] == 1 and ctx.info["wide"] == wide
+        for B, dist in ((65, "U"), (1, "N"), (128, "Z")):
+            compare(inst, synth.points(dist, B, n, 100 + B), ctx=ctx)
+
+
+def test_uniform_check_mixed_rules():
+    """The uniform-k sgn check with different rules per constraint (OR / XOR / XNOR / NAE, k = 5)."""
+    n, m, k = 120, 700, 5
+    rng = np.random.default_rng(9)
+    kinds = rng.choice([0, 1, 2, 5], size=m)
+    lits = []
+    for _ in range(m):
+        vs = rng.choice(n, size=k, replace=False) + 1
+        lits.append(np.where(rng.random(k) < 0.5, -vs, vs))
+    inst = synth._build("uniform_check", n, kinds, [0] * m, lits)
+    ctx = P.Context.from_instance(inst, device=0)
+    s = ctx.search(100, seed=4)
+    s.check()
+    torch.cuda.synchronize()
+    T = s.tensors()
+    x = T["x"].cpu().numpy().astype(np.float64)
+    Fo = oracle_of(inst)
+    cnt, _, U = cdp.check(Fo, x, want_U=True)
+    assert np.array_equal(T["unsat"].cpu().numpy(), cnt)
+    assert np.array_equal(np.sort(T["U"].cpu().numpy()), np.sort(U))
+
+
+@pytest.mark.parametrize("ks", [(129, 256, 257, 512), (513, 768, 769, 1024), (1025, 1280, 1281, 1536), (1537, 1792, 1793, 2048)])
+def test_root_path_geometry_ladder(ks):
+    """Cardinality constraints at every boundary of the root-path launch ladder (C, NW classes), fp64."""
+    n = 2100
+    rng = np.random.default_rng(sum(ks))
+    kinds, bounds, lits = [], [], []
+    for k in ks:
+        vs = rng.choice(n, size=k, replace=False) + 1
+        kinds.append(4); bounds.append(k // 3); lits.append(np.where(rng.random(k) < 0.5, -vs, vs))
+        kinds.append(3); bounds.append(k // 2); lits.append(vs)
+    inst = synth._build("ladder", n, kinds, bounds, lits)
+    compare(inst, synth.points("U", 3, n, 31, np.float64), precision=64)
+    compare(inst, synth.points("N", 2, n, 32, np.float64), precision=64)
