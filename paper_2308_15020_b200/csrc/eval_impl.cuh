@@ -30,9 +30,12 @@ void launch_tiled_uniform(int k, dim3 grid, size_t smem, cudaStream_t st, const 
     }
 }
 
-inline void launch_wide(int k, dim3 grid, size_t smem, cudaStream_t st, const dev::TiledArgs<float>& a) {
-    switch (k) {
-#define FFSAT_KW(K) case K: dev::fast_wide_kernel<K><<<grid, 256, smem, st>>>(a); break;
+inline void launch_wide(int k, int red, dim3 grid, size_t smem, cudaStream_t st, const dev::TiledArgs<float>& a) {
+    switch (k * 4 + red) {
+#define FFSAT_KW(K) case K * 4: dev::fast_wide_kernel<K, 0><<<grid, 256, smem, st>>>(a); break; \
+                    case K * 4 + 1: dev::fast_wide_kernel<K, 1><<<grid, 256, smem, st>>>(a); break; \
+                    case K * 4 + 2: dev::fast_wide_kernel<K, 2><<<grid, 256, smem, st>>>(a); break; \
+                    case K * 4 + 3: dev::fast_wide_kernel<K, 3><<<grid, 256, smem, st>>>(a); break;
         FFSAT_KW(1) FFSAT_KW(2) FFSAT_KW(3) FFSAT_KW(4) FFSAT_KW(5) FFSAT_KW(6) FFSAT_KW(7) FFSAT_KW(8)
         FFSAT_KW(9) FFSAT_KW(10) FFSAT_KW(11) FFSAT_KW(12) FFSAT_KW(13) FFSAT_KW(14) FFSAT_KW(15) FFSAT_KW(16)
 #undef FFSAT_KW
@@ -109,7 +112,7 @@ void eval_device_t(ffsat_ctx* c, const T* x, int64_t B, double* f, T* grad, int3
             if (L.wide) {
                 if constexpr (sizeof(T) == 4) {
                     dim3 gw((unsigned)((B + 63) / 64), (unsigned)c->n_chunks);
-                    launch_wide(ku, gw, c->tiled_smem, st, a);
+                    launch_wide(ku, L.wide_red, gw, c->tiled_smem, st, a);
                 }
             } else if (ku > 0) launch_tiled_uniform<T>(ku, grid, c->tiled_smem, st, a);
             else if (km <= 4) dev::fast_tiled_kernel<T, 4><<<grid, 256, c->tiled_smem, st>>>(a);

@@ -68,6 +68,15 @@ void upload_layout(ffsat_ctx* c) {
         if (b.gX != 0) { d.c0[ch] = 0.0; d.c1[ch] = 1.0; d.g[ch] = b.gX; ++ch; }   // X: l
         d.nch = ch;
         d.tmin = b.rule.tmin; d.tmax = b.rule.tmax; d.parity = b.rule.parity;
+        switch (b.variant) {
+        case V_OR: d.red = 1; break;
+        case V_NOR: d.red = 1 + 4; break;
+        case V_AND: d.red = 2; break;
+        case V_NAND: d.red = 2 + 4; break;
+        case V_XOR: d.red = 3; break;
+        case V_XNOR: d.red = 3 + 4; break;
+        default: d.red = 0;
+        }
         bks.push_back(d);
     }
     upload(c->buckets, bks);

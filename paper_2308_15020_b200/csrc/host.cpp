@@ -479,6 +479,13 @@ Layout build_layout(const Formula& F, int path, int precision) {
             uniform = uniform && nch == 1 && b.k <= 16 && b.k == Lo.fbuckets[0].k;
         }
         Lo.wide = allow_wide && precision == 32 && uniform && F.n <= wide_max_n();
+        auto red_of = [](int variant) {
+            return variant == V_OR || variant == V_NOR ? 1 : variant == V_AND || variant == V_NAND ? 2
+                 : variant == V_XOR || variant == V_XNOR ? 3 : 0;
+        };
+        Lo.wide_red = Lo.fbuckets.empty() ? 0 : red_of(Lo.fbuckets[0].variant);
+        for (const FastBucket& b : Lo.fbuckets)
+            if (red_of(b.variant) != Lo.wide_red) Lo.wide_red = 0;
         const uint32_t pitch = Lo.wide ? (uint32_t)kWidePitch : (uint32_t)kTilePitch;
         Lo.tiled_words.assign(Lo.fast_words.size(), 0);
         for (size_t i = 0; i < Lo.fast_words.size(); ++i) {

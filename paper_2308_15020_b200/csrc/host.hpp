@@ -77,6 +77,7 @@ int sym_roots(int k);               // roots per pass on the root path
 struct Layout {
     int32_t n = 0, path = 0, precision = 32, max_k = 0;
     bool wide = false;                  // tiled path with 64 points per CTA (fp32, uniform single-channel k <= 16)
+    int32_t wide_red = 0;               // the bit reduction (1 OR, 2 AND, 3 XOR) shared by every fast bucket, or 0
     int64_t m = 0, L = 0;
     std::vector<int64_t> order;     // position -> original constraint index (fast first, then sym)
     std::vector<int64_t> pos_of;    // original constraint index -> position

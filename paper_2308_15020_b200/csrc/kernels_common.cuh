@@ -33,7 +33,10 @@ struct FastBucketDev {
     int64_t pos_begin, word_off, slot_off;
     double g0;
     double c0[2], c1[2], g[2];   // channel factor a = c0 + c1 * l, FE += g * prod a
-    int32_t tmin, tmax, parity, pad1;
+    int32_t tmin, tmax, parity;
+    int32_t red;                 // satisfaction as a bit reduction of the literals' truth bits (wide kernel):
+                                 // 1 any-true (OR), 2 all-true (AND), 3 parity (XOR); +4: satisfied iff the
+                                 // reduced bit is 0 (NOR / NAND / XNOR); 0 = count True literals
 };
 
 struct UnitDev {                 // a run of constraints of one bucket at positions [pos_begin, pos_begin + count)

@@ -596,26 +596,43 @@ __global__ void __launch_bounds__(256, (sizeof(T) == 4 ? (KMAX <= 8 ? 4 : 2) : (
 constexpr int kWHalf = 66;
 constexpr int kWPitch = 2 * kWHalf;   // == kWidePitch of host.hpp
 
-template <int K>
-__device__ __forceinline__ void wide_clause(const BucketReg<float>& bk, const uint32_t* sw, float wc, const float* xl,
+// RED != 0: every bucket's satisfaction is one bit reduction of the literals' truth bits (sign of x xor the
+// literal's sign bit, canonical zeros): one LOP3 per literal and point instead of a count (bk.red: +4 =
+// satisfied iff the reduced bit is clear).
+template <int RED>
+__device__ __forceinline__ uint32_t red_init() { return RED == 2 ? 0xffffffffu : 0u; }
+template <int RED>
+__device__ __forceinline__ uint32_t red_step(uint32_t m, float xv, uint32_t w) {
+    const uint32_t bit = __float_as_uint(xv) ^ w;
+    return RED == 1 ? (m | bit) : RED == 2 ? (m & bit) : (m ^ bit);
+}
+
+template <int K, int RED>
+__device__ __forceinline__ void wide_clause(const BucketReg<float>& bk, int redpol, const uint32_t* sw, float wc, const float* xl,
                                             double& f0, double& f1, int& u0, int& u1) {
     uint32_t w[K];
     load_words_smem<K>(sw, w);
     float2 xv[K];
-    uint32_t t0 = 0, t1 = 0;
+    uint32_t t0 = red_init<RED>(), t1 = red_init<RED>();
 #pragma unroll
     for (int i = 0; i < K; ++i) {
         xv[i] = *reinterpret_cast<const float2*>(tile_at(xl, w[i]));
-        t0 += lit_true(xv[i].x, w[i]);
-        t1 += lit_true(xv[i].y, w[i]);
+        if (RED == 0) {
+            t0 += lit_true(xv[i].x, w[i]);
+            t1 += lit_true(xv[i].y, w[i]);
+        } else {
+            t0 = red_step<RED>(t0, xv[i].x, w[i]);
+            t1 = red_step<RED>(t1, xv[i].y, w[i]);
+        }
     }
     const float2 c0 = make_float2(bk.c0[0], bk.c0[0]);
     float2 av[K], pre[K];
+    float cs[K];
     float2 run = make_float2(1.0f, 1.0f);
 #pragma unroll
     for (int i = 0; i < K; ++i) {
-        const float cs = flip_sign(bk.c1[0], w[i]);
-        av[i] = __ffma2_rn(make_float2(cs, cs), xv[i], c0);
+        cs[i] = flip_sign(bk.c1[0], w[i]);
+        av[i] = __ffma2_rn(make_float2(cs[i], cs[i]), xv[i], c0);
         pre[i] = run;
         run = __fmul2_rn(run, av[i]);
     }
@@ -630,16 +647,20 @@ __device__ __forceinline__ void wide_clause(const BucketReg<float>& bk, const ui
     for (int i = 0; i < K; ++i) gv[i] = *reinterpret_cast<const float2*>(tile_at(xl, w[i]) + kWHalf);
 #pragma unroll
     for (int i = K - 1; i >= 0; --i) {
-        const float cs = flip_sign(bk.c1[0], w[i]);
-        gv[i] = __ffma2_rn(__fmul2_rn(pre[i], suf), make_float2(cs, cs), gv[i]);
+        gv[i] = __ffma2_rn(__fmul2_rn(pre[i], suf), make_float2(cs[i], cs[i]), gv[i]);
         suf = __fmul2_rn(suf, av[i]);
     }
 #pragma unroll
     for (int i = 0; i < K; ++i) *reinterpret_cast<float2*>(const_cast<float*>(tile_at(xl, w[i])) + kWHalf) = gv[i];
     f0 += (double)(wc * fe.x);
     f1 += (double)(wc * fe.y);
-    u0 += rule_sat((int)t0, bk.tmin, bk.tmax, bk.parity) ? 0 : 1;
-    u1 += rule_sat((int)t1, bk.tmin, bk.tmax, bk.parity) ? 0 : 1;
+    if (RED == 0) {
+        u0 += rule_sat((int)t0, bk.tmin, bk.tmax, bk.parity) ? 0 : 1;
+        u1 += rule_sat((int)t1, bk.tmin, bk.tmax, bk.parity) ? 0 : 1;
+    } else {   // unsat iff the reduced bit differs from the satisfying value
+        u0 += (int)((t0 >> 31) ^ (uint32_t)redpol);
+        u1 += (int)((t1 >> 31) ^ (uint32_t)redpol);
+    }
 }
 
 // The staging of the next unit (words + weights) by warp 0 only: lanes copy 16-byte pieces.
@@ -649,7 +670,7 @@ __device__ __forceinline__ void stage_unit_w0(const TiledArgs<float>& a, const U
     if (lane < min(unit_count(U), kStageCons)) cp_async_small<4>(&st.w[buf][lane], a.w_pos + (int64_t)U.pos_begin + lane);
 }
 
-template <int K>
+template <int K, int RED>
 __global__ void __launch_bounds__(256, 2) fast_wide_kernel(TiledArgs<float> a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];   // >= 6 KB (host: wide_smem_bytes)
     __shared__ __align__(16) TileStage<float> st;
@@ -701,16 +722,18 @@ __global__ void __launch_bounds__(256, 2) fast_wide_kernel(TiledArgs<float> a) {
     __syncthreads();
     int bucket = -1;
     BucketReg<float> bk{};
+    int redpol = 0;   // 1: satisfied iff the reduced bit is set, so unsat = bit ^ 1
     int buf = 0;
     for (int u = u0; u < u1; ++u) {
         if (cur.bucket != bucket) {
             bucket = cur.bucket;
             bk = load_bucket<float>(a.buckets + bucket);
+            redpol = (a.buckets[bucket].red & 4) ? 0 : 1;
         }
         const uint32_t* sw = st.words[buf];
         const float* swt = st.w[buf];
         const int count = unit_count(cur);
-        for (int j = warp; j < count; j += nw) wide_clause<K>(bk, sw + j * K_PAD(K), swt[j], xl, f0, f1, uc0, uc1);
+        for (int j = warp; j < count; j += nw) wide_clause<K, RED>(bk, redpol, sw + j * K_PAD(K), swt[j], xl, f0, f1, uc0, uc1);
         // advance: the next unit's words are ready, everybody is done with this buffer
         cp_async_wait_all();
         __syncthreads();

@@ -331,10 +331,12 @@ def test_solve_planted_hybrid():
 # ------------------------------------------------------------------ kernel variants and launch geometries
 
 
-@pytest.mark.parametrize("k,kind", [(3, 0), (7, 0), (5, 1), (16, 2)])
-def test_wide_and_narrow_tiled_kernels(k, kind):
+@pytest.mark.parametrize("k,kind,bnd", [(3, 0, 0), (7, 0, 0), (5, 1, 0), (16, 2, 0), (4, 3, 4), (6, 4, 0), (5, 4, 4)])
+def test_wide_and_narrow_tiled_kernels(k, kind, bnd):
     """Uniform single-channel formulas take the 64-point (two points per lane, f32x2) tiled kernel; path 3
-    forces the 32-point kernel.  Both against the oracle, odd and single-point batches, n at the wide limit."""
+    forces the 32-point kernel.  Both against the oracle, odd and single-point batches, n at the wide limit.
+    Kinds cover every truth-bit reduction of the wide kernel: OR, XOR, XNOR, AND (at least k), NOR (at most
+    0), NAND (at most k - 1)."""
     n = 430
     rng = np.random.default_rng(5)
     m = 3 * n
@@ -342,7 +344,7 @@ def test_wide_and_narrow_tiled_kernels(k, kind):
     for _ in range(m):
         vs = rng.choice(n, size=k, replace=False) + 1
         lits.append(np.where(rng.random(k) < 0.5, -vs, vs))
-    inst = synth._build(f"uniform_k{k}_kind{kind}", n, [kind] * m, [0] * m, lits)
+    inst = synth._build(f"uniform_k{k}_kind{kind}", n, [kind] * m, [bnd] * m, lits)
     for path, wide in ((0, 1), (3, 0)):
         ctx = P.Context.from_instance(inst, precision=32, path=path, device=0)
         assert ctx.info["path"] == 1 and ctx.info["wide"] == wide
