@@ -862,13 +862,13 @@ __device__ __forceinline__ void global_unit(const GlobalArgs<T>& a, const Bucket
         clause_terms<T, K, NCH>(bk, w0, x0, wc0, g0, facc, uacc);
         if (bv) {
 #pragma unroll
-            for (int i = 0; i < K; ++i) a.Tb[(sbase + (int64_t)j * K + i) * a.B + b] = g0[i];
+            for (int i = 0; i < K; ++i) __stcs(a.Tb + (sbase + (int64_t)j * K + i) * a.B + b, g0[i]);   // streaming: keep x^T in L2
         }
         if (two) {
             clause_terms<T, K, NCH>(bk, w1, x1, wc1, g1, facc, uacc);
             if (bv) {
 #pragma unroll
-                for (int i = 0; i < K; ++i) a.Tb[(sbase + (int64_t)(j + nw) * K + i) * a.B + b] = g1[i];
+                for (int i = 0; i < K; ++i) __stcs(a.Tb + (sbase + (int64_t)(j + nw) * K + i) * a.B + b, g1[i]);
             }
         }
     }
