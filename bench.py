@@ -370,7 +370,7 @@ def main():
                     "algorithmic_bytes_def": "terms written L_fast*B*es + x read once n*B*es + literal words 4*L_fast + weights es*C_fast",
                     "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_src})"}
     elif fast_ms >= root_ms:
-        kname, kms = "fast_tiled_kernel", fast_ms
+        kname, kms = ("fast_wide_kernel" if info.get("wide") else "fast_tiled_kernel"), fast_ms
         ops = FAST_OPS_PER_TERM * info["n_fast_lits"] * B
         achieved = ops / (kms * 1e-3) / 1e12
         roofline = {"bound": "alu", "achieved": achieved, "peak": alu_peak, "unit": "T lane-op/s",

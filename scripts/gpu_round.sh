@@ -10,7 +10,7 @@ for c in c1 c3 c4 c5; do timeout 600 python bench.py --config $c --steps 30 --wa
 timeout 300 python bench.py --impl reference --steps 3 --warmup 3 > gpurun_out/bench_ref.json 2>gpurun_out/bench_ref.err; echo ref=$?
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches_c2.csv python bench.py --steps 20 --warmup 3 --no-cpu-baseline > /dev/null 2>&1; echo ncu_launch=$?
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches_c3.csv python bench.py --config c3 --steps 10 --warmup 3 --no-cpu-baseline > /dev/null 2>&1; echo ncu_launch3=$?
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:fast_tiled -s 5 -c 1 -o gpurun_out/prof_tiled -f python bench.py --steps 5 --warmup 3 --no-cpu-baseline > /dev/null 2>&1; echo ncu_tiled=$?
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:fast_wide -s 5 -c 1 -o gpurun_out/prof_tiled -f python bench.py --steps 5 --warmup 3 --no-cpu-baseline > /dev/null 2>&1; echo ncu_tiled=$?
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:sym_item -s 2 -c 1 -o gpurun_out/prof_sym -f python bench.py --config c3 --steps 3 --warmup 1 --no-cpu-baseline > /dev/null 2>&1; echo ncu_sym=$?
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:fast_global -s 2 -c 1 -o gpurun_out/prof_global -f python bench.py --config c5 --steps 3 --warmup 1 --no-cpu-baseline > /dev/null 2>&1; echo ncu_global=$?
 for f in gpurun_out/bench_*.json; do echo $f; head -c 600 $f; echo; done

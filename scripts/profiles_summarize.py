@@ -19,7 +19,7 @@ def num(v):
     return float(str(v).replace(",", ""))
 
 
-for rep, kname in (("prof_tiled", "fast_tiled_kernel"), ("prof_sym", "sym_item_kernel"), ("prof_global", "fast_global_kernel")):
+for rep, kname in (("prof_tiled", "fast_wide_kernel"), ("prof_sym", "sym_item_kernel"), ("prof_global", "fast_global_kernel")):
     p = os.path.join(G, rep + ".ncu-rep")
     if not os.path.exists(p):
         continue
