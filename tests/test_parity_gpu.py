@@ -387,3 +387,18 @@ def test_root_path_geometry_ladder(ks):
     inst = synth._build("ladder", n, kinds, bounds, lits)
     compare(inst, synth.points("U", 3, n, 31, np.float64), precision=64)
     compare(inst, synth.points("N", 2, n, 32, np.float64), precision=64)
+
+
+@pytest.mark.parametrize("k", [128, 700, 2000])
+def test_long_cardinality_fp32_probability_basis(k):
+    """in the probability basis the fp32 root path stays within the fp32 tolerance (1e-4) even
+    at k = 2000 (the ESP basis would fail at k ~ 32): forced precision 32, near-corner points."""
+    n = k + 40
+    rng = np.random.default_rng(k + 1)
+    kinds, bounds, lits = [], [], []
+    for kind, b in ((4, k // 4), (3, k // 2)):
+        vs = rng.choice(n, size=k, replace=False) + 1
+        kinds.append(kind); bounds.append(b); lits.append(np.where(rng.random(k) < 0.5, -vs, vs))
+    inst = synth._build(f"fp32_long_k{k}", n, kinds, bounds, lits)
+    compare(inst, synth.points("N", 8, n, 41), precision=32)
+    compare(inst, synth.points("U", 8, n, 42), precision=32)
