@@ -245,3 +245,23 @@ def points(dist: str, B: int, n: int, seed: int, dtype=np.float32) -> np.ndarray
     else:
         raise ValueError(dist)
     return np.ascontiguousarray(x.astype(dtype))
+
+
+def planted_maxcut(l: int, k: int, seed: int = 0) -> Instance:
+    """Benchmark 3: planted-partition graph of l clusters x k vertices; every unordered vertex pair
+    is an edge with probability 1/2 (SPEC S:454 reading of the paper's size remark), weight 1 inside a cluster
+    and 2 between clusters; one weighted XOR (odd) constraint per edge (u, v): satisfied iff u and v land on
+    opposite sides, so the falsified weight is the uncut weight (Max-Cut as 2-XOR).
+    meta: n, edges (u, v, w) arrays (0-based), cluster of each vertex."""
+    rng = np.random.default_rng(np.random.PCG64(seed + 8080))
+    n = l * k
+    cluster = np.repeat(np.arange(l), k)
+    iu, iv = np.triu_indices(n, 1)
+    keep = rng.random(len(iu)) < 0.5
+    u, v = iu[keep], iv[keep]
+    w = np.where(cluster[u] == cluster[v], 1.0, 2.0)
+    m = len(u)
+    lits = np.stack([u + 1, v + 1], axis=1).astype(np.int32).reshape(-1)
+    offsets = np.arange(0, 2 * m + 1, 2, dtype=np.int64)
+    return Instance(f"maxcut_l{l}_k{k}_s{seed}", n, np.full(m, XOR, np.uint8), np.zeros(m, np.int32), w, offsets, lits,
+                    {"edges_u": u, "edges_v": v, "edges_w": w, "cluster": cluster})

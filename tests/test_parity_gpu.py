@@ -402,3 +402,22 @@ def test_long_cardinality_fp32_probability_basis(k):
     inst = synth._build(f"fp32_long_k{k}", n, kinds, bounds, lits)
     compare(inst, synth.points("N", 8, n, 41), precision=32)
     compare(inst, synth.points("U", 8, n, 42), precision=32)
+
+
+def test_maxsat_mode_planted_maxcut_tiny():
+    """f3: optimisation mode (fixed weights, (RF)^inf, incumbent by falsified weight) finds the brute-force
+    optimum of tiny planted Max-Cut instances (SPEC acceptance 7: >= 9 of 10 seeds)."""
+    import itertools
+    from paper_2308_15020_b200.maxsat import solve_maxsat
+    hits = 0
+    for seed in range(10):
+        inst = synth.planted_maxcut(2, 4, seed=seed)
+        Fo = oracle_of(inst)
+        X = np.array(list(itertools.product((-1.0, 1.0), repeat=inst.n)))
+        _, fw = cdp.check(Fo, X)
+        ctx = P.Context.from_instance(inst, device=0)
+        best, a, rounds, secs = solve_maxsat(ctx, batch=32, rounds=50, seed=seed, max_inner=50)
+        assert ctx.check(a)[1] == best
+        assert best >= fw.min() - 1e-12
+        hits += abs(best - fw.min()) < 1e-9
+    assert hits >= 9
