@@ -36,6 +36,15 @@ struct ffsat_search {
     ffsat_solve_params P{};
     DBuf X, Xp, Gx, Gp, fX, fP, dot, eta, done, iters, unsatP, solved, sol, unsat, U, stats, xT;
     int64_t round = 0, iters_issued = 0;
+    // one CLS iteration captured as a CUDA graph (replayed by ffsat_search_iterate)
+    cudaStream_t cap_stream = nullptr;
+    cudaGraphExec_t iter_exec = nullptr;
+    int64_t iter_kernels = 0;     // kernels in one captured iteration (launch accounting)
+    bool graph_failed = false;
+    ~ffsat_search() {
+        if (iter_exec) cudaGraphExecDestroy(iter_exec);
+        if (cap_stream) cudaStreamDestroy(cap_stream);
+    }
 };
 
 namespace {
@@ -253,7 +262,56 @@ void search_begin_round(ffsat_search* s, cudaStream_t st) {
     s->iters_issued = 0;
 }
 
+void search_iterate_direct(ffsat_search* s, int n_iters, cudaStream_t st);
+
+// Capture one iteration (eval + PGD step, forked root-path streams included) into a graph once per search;
+// afterwards each iteration is one cudaGraphLaunch (no per-kernel launch latency on the host or device).
+bool search_capture(ffsat_search* s) {
+    if (s->iter_exec) return true;
+    if (s->graph_failed) return false;
+    if (!s->cap_stream) CK(cudaStreamCreateWithFlags(&s->cap_stream, cudaStreamNonBlocking));
+    plan(s->ctx, s->B);                  // scratch sizing / uploads are synchronous: never inside a capture
+    s->ctx->ensure_side_streams();
+    const int64_t before = s->ctx->launches, iters_before = s->iters_issued;
+    cudaGraph_t g = nullptr;
+    if (cudaStreamBeginCapture(s->cap_stream, cudaStreamCaptureModeThreadLocal) != cudaSuccess) {
+        cudaGetLastError();
+        s->graph_failed = true;
+        return false;
+    }
+    bool ok = true;
+    try {
+        search_iterate_direct(s, 1, s->cap_stream);
+    } catch (const Error&) {
+        ok = false;
+    }
+    const cudaError_t e = cudaStreamEndCapture(s->cap_stream, &g);
+    s->iters_issued = iters_before;
+    if (!ok || e != cudaSuccess || !g || cudaGraphInstantiate(&s->iter_exec, g, 0) != cudaSuccess) {
+        cudaGetLastError();
+        if (g) cudaGraphDestroy(g);
+        s->iter_exec = nullptr;
+        s->graph_failed = true;
+        s->ctx->launches = before;
+        return false;
+    }
+    cudaGraphDestroy(g);
+    s->iter_kernels = s->ctx->launches - before;
+    s->ctx->launches = before;
+    return true;
+}
+
 void search_iterate(ffsat_search* s, int n_iters, cudaStream_t st) {
+    if (n_iters > 0 && search_capture(s)) {
+        for (int i = 0; i < n_iters; ++i) CK(cudaGraphLaunch(s->iter_exec, st));
+        s->ctx->launches += s->iter_kernels * n_iters;
+        s->iters_issued += n_iters;
+        return;
+    }
+    search_iterate_direct(s, n_iters, st);
+}
+
+void search_iterate_direct(ffsat_search* s, int n_iters, cudaStream_t st) {
     const bool f64 = s->ctx->Lo.precision == 64;
     dev::PgdArgs a = pgd_args(s, 1);
     for (int i = 0; i < n_iters; ++i) {
