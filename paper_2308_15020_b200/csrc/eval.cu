@@ -58,7 +58,7 @@ void plan(ffsat_ctx* c, int64_t B) {
     upload(c->chunk_units, cu);
     const int64_t parts = std::max<int64_t>(1, c->n_chunks);
     if (L.path == 1) c->P.ensure(std::max<size_t>(16, (size_t)c->n_chunks * L.n * B * es));
-    if (L.path == 2) c->xT.ensure(std::max<size_t>(16, (size_t)L.n * B * es));
+    if (L.path == 2 || L.sym_lane) c->xT.ensure(std::max<size_t>(16, (size_t)L.n * B * es));
     c->Tb.ensure(std::max<size_t>(16, (size_t)L.tb_slots * B * es));
     c->fpart.ensure((size_t)parts * B * 8);
     c->upart.ensure((size_t)parts * B * 4);

@@ -61,6 +61,13 @@ void eval_device_t(ffsat_ctx* c, const T* x, int64_t B, double* f, T* grad, int3
         if (profiled) CK(cudaEventRecord(c->ev[i], st));
     };
     mark(0);
+    // x^T [n][B] for the global fast kernel and the thread-per-item root classes (coalesced per-point reads)
+    const bool need_xT = L.path == 2 || L.sym_lane;
+    if (need_xT && L.n > 0) {
+        dim3 tg(blocks_for(L.n, 32), blocks_for(B, 32)), tb(32, 8);
+        dev::transpose_kernel<T><<<tg, tb, 0, st>>>(x, c->xT.as<T>(), B, L.n);
+        c->launches += 1;
+    }
     // root-path classes are independent of the fast kernel (disjoint outputs): off the profiling path they
     // run on forked side streams, concurrently with each other and with the fast kernel
     auto launch_sym_all = [&]() {
@@ -76,10 +83,12 @@ void eval_device_t(ffsat_ctx* c, const T* x, int64_t B, double* f, T* grad, int3
             c->ensure_side_streams();
             CK(cudaEventRecord(c->ev_fork, st));
         }
+        dev::SymArgs<T> aT = a;    // thread-per-item classes read x^T
+        aT.x = c->xT.as<T>(); aT.sb = 1; aT.sv = B;
         for (size_t i = 0; i < ncl; ++i) {
             cudaStream_t ss = fork ? c->side[i % FFSAT_SIDE_STREAMS] : st;
             if (fork && i < FFSAT_SIDE_STREAMS) CK(cudaStreamWaitEvent(ss, c->ev_fork, 0));
-            launch_sym_class<T>(L.sym_classes[i], a, ss);
+            launch_sym_class<T>(L.sym_classes[i], L.sym_classes[i].G == 0 ? aT : a, ss);
             c->launches += 1;
         }
         CK(cudaGetLastError());
@@ -99,7 +108,7 @@ void eval_device_t(ffsat_ctx* c, const T* x, int64_t B, double* f, T* grad, int3
     };
     if (!profiled) launch_sym_all();
     if (L.n_fast > 0 && c->n_chunks > 0) {
-        c->launches += L.path == 1 ? 1 : 2;
+        c->launches += 1;
         if (L.path == 1) {
             dev::TiledArgs<T> a{};
             a.x = x; a.B = B; a.n = L.n;
@@ -120,8 +129,6 @@ void eval_device_t(ffsat_ctx* c, const T* x, int64_t B, double* f, T* grad, int3
             else if (km <= 16) dev::fast_tiled_kernel<T, 16><<<grid, 256, c->tiled_smem, st>>>(a);
             else dev::fast_tiled_kernel<T, 64><<<grid, 256, c->tiled_smem, st>>>(a);
         } else {
-            dim3 tg(blocks_for(L.n, 32), blocks_for(B, 32)), tb(32, 8);
-            dev::transpose_kernel<T><<<tg, tb, 0, st>>>(x, c->xT.as<T>(), B, L.n);
             dev::GlobalArgs<T> a{};
             a.xT = c->xT.as<T>(); a.B = B; a.n = L.n; a.words = c->fast_words.as<uint32_t>();
             a.units = c->units.as<dev::UnitDev>(); a.buckets = c->buckets.as<dev::FastBucketDev>();

@@ -276,12 +276,13 @@ std::vector<int32_t> disjoint_classes(const std::vector<std::vector<int32_t>>& v
 
 // ------------------------------------------------------------------------------- A2: layout
 
-// Root path launch geometry.  k <= 32: one warp, one literal per lane; k <= 128: one warp, four per lane.
+// Root path launch geometry.  k <= 32: one thread per item (sym_lane_kernel); k <= 128: one warp, four per lane.
 // Longer: the smallest of a short ladder of (NW warps, C literals per thread) capacities 32 NW C that holds
 // k -- padding slots cost full root-sweep work, so the ladder keeps them under ~25% (typically ~10%), while
 // keeping the number of distinct launch classes small (each class is one launch on its own side stream).
 static void sym_geom(int k, int* nw_out, int* c_out) {
-    if (k <= 32) { *nw_out = 1; *c_out = 1; return; }
+    // k <= 32: thread per (constraint, point) item (sym_lane_kernel), "nw" 0, c = the register bound KMAX
+    if (k <= 32) { *nw_out = 0; *c_out = k <= 8 ? 8 : k <= 16 ? 16 : 32; return; }
     if (k <= 128) { *nw_out = 1; *c_out = 4; return; }
     static const int ladder[][2] = {{1, 8}, {1, 16}, {2, 12}, {2, 16}, {4, 10}, {3, 16}, {4, 14}, {4, 16}, {6, 16}, {8, 16}};
     for (const auto& g : ladder)
@@ -446,6 +447,7 @@ Layout build_layout(const Formula& F, int path, int precision) {
             Lo.sym_classes.push_back({G, C, R, s, s + 1, 0});
         else Lo.sym_classes.back().end = s + 1;
         Lo.sym_classes.back().max_mp = std::max(Lo.sym_classes.back().max_mp, (k + 1) / 2);
+        if (G == 0) Lo.sym_lane = true;
     }
 
     // ---- T-buffer slots and occurrence CSR (ascending slot order per variable)

@@ -59,6 +59,7 @@ struct SymSig {                     // a (k, sat rule) signature with its root t
 };
 
 struct SymClass {                   // launch class: G threads per (constraint, point), C literals per thread
+                                    // (G = 0: one thread per item, C = the literal bound KMAX)
     int32_t G, C, R;                // R roots per pass
     int64_t begin, end;             // sym constraint indices
     int32_t max_mp;                 // largest M' in the class (root-table size staged in shared memory)
@@ -95,6 +96,7 @@ struct Layout {
     std::vector<uint32_t> sym_words;    // var | neg << 31
     std::vector<int32_t> sym_rule;      // 3 ints per sym constraint (tmin, tmax, parity)
     std::vector<SymClass> sym_classes;
+    bool sym_lane = false;              // some root-path class runs thread-per-item on x^T (needs the transpose)
     // T-buffer slots (global path: fast slots then sym slots; tiled path: sym slots only)
     int64_t tb_fast = 0, tb_slots = 0;
     std::vector<int64_t> occ_off;       // [n + 1]

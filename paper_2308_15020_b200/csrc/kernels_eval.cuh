@@ -1209,6 +1209,68 @@ sym_item_kernel(SymArgs<T> a, int64_t s_begin) {
     }
 }
 
+// Root path for short constraints (k <= KMAX <= 32): one thread per (constraint, point) item, lanes over
+// consecutive points of the same constraint (x read from x^T: coalesced), no cross-thread scan at all.  Per
+// root m: backward sweep storing the in-constraint suffix products insuf_j in registers and the total Q_m,
+// then the forward sweep term_j += Re(A insuf_j), A <- A phi_j (phi recomputed), A_0 = H_m.
+// 14 FP lane-ops per (literal, root) and every lane busy (the warp-group kernel would idle lanes at small k).
+template <typename T, int KMAX>
+__global__ void __launch_bounds__(256) sym_lane_kernel(SymArgs<T> a, int64_t s_begin, int64_t n_items) {
+    const int64_t item = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const bool valid = item < n_items;
+    const int64_t it = valid ? item : n_items - 1;
+    const int64_t s = s_begin + it / a.B;
+    const int64_t b = it - (it / a.B) * a.B;
+    const SymSigDev sg = a.sigs[a.sig_of[s]];
+    const int k = sg.k;
+    const int64_t lo = a.off[s];
+    T l[KMAX], term[KMAX];
+    int tc = 0;
+#pragma unroll
+    for (int j = 0; j < KMAX; ++j) {
+        l[j] = (T)1;      // padding literal: p = 0, factor alpha + beta = 1
+        term[j] = (T)0;
+        if (j < k) {
+            const uint32_t w = __ldg(a.words + lo + j);
+            const T xv = a.x[b * a.sb + (int64_t)(w & 0x7fffffffu) * a.sv];
+            l[j] = (int)w < 0 ? -xv : xv;
+            tc += (int)((xv < (T)0) != ((int)w < 0));
+        }
+    }
+    const T* cf = a.coef + sg.coef_off * 8;
+    double fe_acc = 0.0;
+    for (int m = 0; m < sg.Mp; ++m) {
+        const cplx<T> al{__ldg(cf + 8 * m + 0), __ldg(cf + 8 * m + 1)};
+        const cplx<T> be{__ldg(cf + 8 * m + 2), __ldg(cf + 8 * m + 3)};
+        cplx<T> insuf[KMAX];
+        cplx<T> suf{(T)1, (T)0};
+#pragma unroll
+        for (int j = KMAX - 1; j >= 0; --j) {
+            insuf[j] = suf;
+            suf = cmul(suf, cplx<T>{fmaT(be.re, l[j], al.re), fmaT(be.im, l[j], al.im)});
+        }
+        cplx<T> A{__ldg(cf + 8 * m + 6), __ldg(cf + 8 * m + 7)};
+#pragma unroll
+        for (int j = 0; j < KMAX; ++j) {
+            term[j] = fmaT(A.re, insuf[j].re, fmaT(-A.im, insuf[j].im, term[j]));
+            A = cmul(A, cplx<T>{fmaT(be.re, l[j], al.re), fmaT(be.im, l[j], al.im)});
+        }
+        fe_acc += (double)__ldg(cf + 8 * m + 4) * (double)suf.re - (double)__ldg(cf + 8 * m + 5) * (double)suf.im;
+    }
+    if (!valid) return;
+    const T wc = a.w_sym[s];
+#pragma unroll
+    for (int j = 0; j < KMAX; ++j) {
+        if (j < k) {
+            const uint32_t w = __ldg(a.words + lo + j);
+            const T v = wc * term[j];
+            a.Tb[(a.tb_fast + lo + j) * a.B + b] = (int)w < 0 ? -v : v;
+        }
+    }
+    a.fsym[s * a.B + b] = (double)wc * (sg.g0 + fe_acc);
+    a.usym[s * a.B + b] = rule_sat(tc, sg.tmin, sg.tmax, sg.parity) ? 0 : 1;
+}
+
 // ------------------------------------------------------------------------------------------------
 // A7 reductions.
 template <typename T>
