@@ -206,6 +206,12 @@ ffsat_status ffsat_launch_count(const ffsat_ctx* ctx, int64_t* out);
  * path), ms[1] root-path kernels, ms[2] gradient reduction, ms[3] f / unsat reduction. */
 ffsat_status ffsat_eval_profiled(ffsat_ctx* ctx, const void* x, int64_t B, double* f_out, void* grad_out,
                                  int32_t* unsat_out, void* stream, double* ms4);
+/* Layout introspection (tests; works on host-only contexts): the fast-path work units as rows
+ * {bucket, count, first position, tiled (1) / global (0)} and the position -> input-constraint order.  With
+ * units_out NULL only *n_units is written; otherwise cap rows at most are copied.  order_out: [n_cons] or NULL.
+ * On the tiled path every unit is a var-disjoint class: no variable occurs in two of its constraints. */
+ffsat_status ffsat_layout_units(const ffsat_ctx* ctx, int64_t* n_units, int64_t* units_out, int64_t cap,
+                                int64_t* order_out);
 const char* ffsat_last_error(const ffsat_ctx* ctx);
 const char* ffsat_version(void);
 void ffsat_free(ffsat_ctx* ctx);

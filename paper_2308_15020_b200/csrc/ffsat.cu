@@ -801,6 +801,24 @@ ffsat_status ffsat_solve(ffsat_ctx* c, int64_t batch, int64_t max_restarts, uint
     ABI_CATCH(c)
 }
 
+ffsat_status ffsat_layout_units(const ffsat_ctx* c, int64_t* n_units, int64_t* units_out, int64_t cap, int64_t* order_out) {
+    ABI_TRY(nullptr)
+    if (!c || !n_units) throw Error(FFSAT_ERR_ARG, "null argument");
+    const Layout& L = c->Lo;
+    *n_units = (int64_t)L.units.size();
+    if (units_out)
+        for (int64_t u = 0; u < std::min<int64_t>(cap, (int64_t)L.units.size()); ++u) {
+            const WorkUnit& w = L.units[(size_t)u];
+            units_out[4 * u] = w.bucket;
+            units_out[4 * u + 1] = w.count;
+            units_out[4 * u + 2] = w.pos_begin;
+            units_out[4 * u + 3] = L.path == 1 ? 1 : 0;
+        }
+    if (order_out) std::copy(L.order.begin(), L.order.end(), order_out);
+    return FFSAT_OK;
+    ABI_CATCH(nullptr)
+}
+
 ffsat_status ffsat_launch_count(const ffsat_ctx* c, int64_t* out) {
     ABI_TRY(nullptr)
     if (!c || !out) throw Error(FFSAT_ERR_ARG, "null argument");

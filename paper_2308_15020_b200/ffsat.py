@@ -81,7 +81,7 @@ EXPORTS = ["ffsat_load", "ffsat_load_file", "ffsat_info", "ffsat_export", "ffsat
            "ffsat_search_iterate", "ffsat_search_check", "ffsat_search_restart", "ffsat_search_stats_get",
            "ffsat_search_get_buffers", "ffsat_search_assignment", "ffsat_search_free", "ffsat_solve",
            "ffsat_default_params", "ffsat_last_error", "ffsat_version", "ffsat_free", "ffsat_launch_count",
-           "ffsat_eval_profiled"]
+           "ffsat_eval_profiled", "ffsat_layout_units"]
 
 _lib = None
 
@@ -121,6 +121,7 @@ def lib():
         "ffsat_free": ([P], None),
         "ffsat_launch_count": ([P, C.POINTER(I64)], C.c_int),
         "ffsat_eval_profiled": ([P, P, I64, P, P, P, P, C.POINTER(C.c_double)], C.c_int),
+        "ffsat_layout_units": ([P, C.POINTER(I64), P, I64, P], C.c_int),
     }
     for name, (args, res) in sig.items():
         fn = getattr(L, name)
@@ -286,6 +287,16 @@ class Context:
         u = np.zeros(B, np.int32) if unsat else None
         ffsat_eval(self.ptr, x, B, f, g, u, stream)
         return f, g, u
+
+    def layout_units(self):
+        """(units [U][4] = bucket, count, first position, tiled flag; order [m] position -> input constraint)."""
+        nu = C.c_int64()
+        _check(lib().ffsat_layout_units(self.ptr, C.byref(nu), None, 0, None), self.ptr)
+        units = np.zeros((nu.value, 4), np.int64)
+        order = np.zeros(self.m, np.int64)
+        _check(lib().ffsat_layout_units(self.ptr, C.byref(nu), units.ctypes.data_as(C.c_void_p), nu.value,
+                                        order.ctypes.data_as(C.c_void_p)), self.ptr)
+        return units, order
 
     def launch_count(self):
         n = C.c_int64()

@@ -129,3 +129,28 @@ def test_paths_and_sizes():
     assert small.info["n_lits"] == 7 * 17000
     c3 = _ctx(synth.config3(0, n=4096, m3=100, n_card=2, kmin=500, kmax=600))
     assert c3.info["path"] == 2 and c3.info["precision"] == 64 and c3.info["n_sym_cons"] == 2
+
+
+@pytest.mark.parametrize("maker", [lambda: synth.config2(0), lambda: synth.config1(2),
+                                   lambda: synth.random_mixed(n=120, m=600, seed=3, kmax=16),
+                                   lambda: synth.rq1("xor2", seed=1)])
+def test_tiled_units_are_var_disjoint_classes(maker):
+    """The tiled kernels add a unit's literal terms into the shared gradient tile from 8 warps at once; that is
+    race-free and deterministic only because no variable occurs twice in a unit (host: disjoint_classes).
+    Also: units cover every fast constraint exactly once, in position order, with <= 16 members."""
+    inst = maker()
+    ctx = P.Context.from_instance(inst, device=-1)
+    assert ctx.info["path"] == 1
+    units, order = ctx.layout_units()
+    assert sorted(order.tolist()) == list(range(inst.m))
+    covered = 0
+    for bucket, count, p0, tiled in units:
+        assert tiled == 1 and 1 <= count <= 16 and p0 == covered
+        seen = set()
+        for p in range(p0, p0 + count):
+            c = order[p]
+            vs = np.abs(inst.lits[inst.offsets[c]:inst.offsets[c + 1]])
+            assert not (seen & set(vs.tolist())), "variable shared inside a unit"
+            seen |= set(vs.tolist())
+        covered += count
+    assert covered == ctx.info["n_fast_cons"]
