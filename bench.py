@@ -109,15 +109,17 @@ class ClockSampler:
                 "samples": len(sm), "source": "nvml"}
 
 
-def ncu_traffic(kernel_key):
-    """dram bytes per launch of the dominant kernel from the committed ncu --set full summary, or None."""
+def ncu_traffic(kernel_key, config):
+    """dram bytes per launch of the dominant kernel(s) ("a+b": summed) on this config from the committed ncu --set full
+    summary (profiles/ncu_summary.json, keys "<config>:<kernel>"), or None."""
     p = os.path.join(ROOT, "profiles", "ncu_summary.json")
     if not os.path.exists(p):
         return None
     try:
         with open(p) as fh:
             d = json.load(fh)
-        return d.get(kernel_key, {}).get("dram_bytes_per_launch")
+        vals = [d.get(f"{config}:{k}", {}).get("dram_bytes_per_launch") for k in kernel_key.split("+")]
+        return None if any(v is None for v in vals) else float(sum(vals))
     except (OSError, ValueError):
         return None
 
@@ -361,7 +363,8 @@ def main():
                f"({peak_src} sm_max_mhz); one FMA = one lane-op")
     if fast_ms >= root_ms and info["path"] == 2:
         # global fast path: HBM-bound (terms stored for the ordered reduction, x rows gathered)
-        kname, kms = "fast_global_kernel", fast_ms
+        long_fast = any(k > 4 and kd in (0, 1, 2, 5) for k, kd in zip(np.diff(inst.offsets), inst.kind))
+        kname, kms = ("fast_global_kernel+fast_global_long_kernel" if long_fast else "fast_global_kernel"), fast_ms
         alg_bytes = (info["n_fast_lits"] * B * es + inst.n * B * es + info["n_fast_lits"] * 4 + info["n_fast_cons"] * es)
         achieved = alg_bytes / (kms * 1e-3) / 1e9
         peak = float(peaks.get("hbm_gbs", 6650.0))
@@ -384,7 +387,7 @@ def main():
         roofline = {"bound": "alu", "achieved": achieved, "peak": alu_peak, "unit": "T lane-op/s",
                     "algorithmic_ops_per_lit_root": ROOT_OPS_PER_LIT_ROOT, "peak_source": alu_src}
         peak = alu_peak
-    roofline.update({"frac": achieved / peak, "traffic": ncu_traffic(kname), "kernel": kname, "kernel_ms": kms,
+    roofline.update({"frac": achieved / peak, "traffic": ncu_traffic(kname, args.config), "kernel": kname, "kernel_ms": kms,
                      "eval_phase_ms": {"fast": float(ph[0]), "root": float(ph[1]), "grad_reduce": float(ph[2]),
                                        "f_reduce": float(ph[3])},
                      "kernel_share_of_eval": kms / float(np.sum(ph)),

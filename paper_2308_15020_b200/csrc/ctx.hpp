@@ -77,6 +77,9 @@ struct ffsat_ctx {
     ffsat::DBuf xT, Tb, P, fpart, upart, fsym, usym, chunk_units, x_stage, g_stage, f_stage, u_stage, w_stage;
     int64_t plan_B = -1;
     int32_t n_chunks = 0;
+    // global path: chunk groups by bucket length class -- chunks [gchunk[g], gchunk[g + 1]) hold the units with
+    // k <= 4 (g = 0), 4 < k <= 16 (g = 1), 16 < k (g = 2, the long kernel); each group is one launch
+    int32_t gchunk[4] = {0, 0, 0, 0};
     size_t tiled_smem = 0;
     int64_t launches = 0;
     cudaEvent_t ev[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
@@ -116,6 +119,8 @@ void eval_device_t(ffsat_ctx* c, const T* x, int64_t B, double* f, T* grad, int3
 template <typename T>
 void set_tiled_smem(size_t bytes);
 void set_wide_smem(size_t bytes);   // eval_f32.cu
+template <typename T>
+void set_long_smem();              // the long global kernel's dynamic shared memory (eval_f32.cu / eval_f64.cu)
 // one root-path launch class (sym_f32.cu / sym_f64.cu)
 template <typename T>
 void launch_sym_class(const SymClass& cl, const dev::SymArgs<T>& a, cudaStream_t st);

@@ -40,21 +40,48 @@ void plan(ffsat_ctx* c, int64_t B) {
         cps = std::max(1, (int)std::min<size_t>(8, (228 * 1024) / (c->tiled_smem + (L.precision == 64 ? 4352 : 2304) + 1024)));
     }
     const int64_t n_units = (int64_t)L.units.size();
-    c->n_chunks = L.n_fast > 0 ? pick_chunks(PT, cps, c->num_sm, n_units) : 0;
-    // balanced contiguous unit ranges by literal rows
+    // global path: units grouped by length class (buckets ascend in k, so each group is a contiguous unit range):
+    // k <= 4, 4 < k <= 16, k > 16 -- each group gets its own chunks and launch (register bound per class)
+    int64_t ug[4] = {0, n_units, n_units, n_units};
+    if (L.path == 2) {
+        auto kof = [&](int64_t u) { return L.fbuckets[(size_t)L.units[(size_t)u].bucket].k; };
+        int64_t u = 0;
+        while (u < n_units && kof(u) <= 4) ++u;
+        ug[1] = u;
+        while (u < n_units && kof(u) <= 16) ++u;
+        ug[2] = u;
+        // a small 4 < k <= 16 group runs in the long kernel (any k <= 64): a launch of its own would be latency-bound
+        int64_t lits1 = 0;
+        for (int64_t q = ug[1]; q < ug[2]; ++q) lits1 += L.unit_rows[(size_t)q];
+        if (lits1 < 65536) ug[2] = ug[1];
+    }
+    int ncg[3] = {0, 0, 0};
+    if (L.n_fast > 0) {
+        ncg[0] = pick_chunks(PT, cps, c->num_sm, ug[1] - ug[0]);
+        ncg[1] = pick_chunks(PT, cps, c->num_sm, ug[2] - ug[1]);
+        ncg[2] = pick_chunks(PT, 3, c->num_sm, ug[3] - ug[2]);   // long kernel: 64 KB smem per CTA
+    }
+    if (ncg[2] > 0 && (uint64_t)L.n * (uint64_t)B >= (1ull << 32))
+        throw Error(FFSAT_ERR_ARG, "batch too large for the long-constraint kernel (n * B must be < 2^32; split the batch)");
+    c->gchunk[0] = 0;
+    for (int g = 0; g < 3; ++g) c->gchunk[g + 1] = c->gchunk[g] + ncg[g];
+    c->n_chunks = c->gchunk[3];
+    // balanced contiguous unit ranges by literal rows, within each group
     std::vector<int32_t> cu((size_t)c->n_chunks + 1, 0);
-    if (c->n_chunks > 0) {
+    auto split = [&](int64_t ua, int64_t ub, int nc, int j0) {
         int64_t total = 0;
-        for (int64_t r : L.unit_rows) total += r;
+        for (int64_t u = ua; u < ub; ++u) total += L.unit_rows[(size_t)u];
         int64_t acc = 0;
         int j = 1;
-        for (int64_t u = 0; u < n_units && j < c->n_chunks; ++u) {
+        for (int64_t u = ua; u < ub && j < nc; ++u) {
             acc += L.unit_rows[(size_t)u];
-            while (j < c->n_chunks && acc * c->n_chunks >= total * j) cu[j++] = (int32_t)(u + 1);
+            while (j < nc && acc * nc >= total * j) cu[(size_t)(j0 + j++)] = (int32_t)(u + 1);
         }
-        for (; j <= c->n_chunks; ++j) cu[j] = (int32_t)n_units;
-        cu[c->n_chunks] = (int32_t)n_units;
-    }
+        for (; j <= nc; ++j) cu[(size_t)(j0 + j)] = (int32_t)ub;
+        cu[(size_t)j0] = (int32_t)ua;
+    };
+    for (int g = 0; g < 3; ++g)
+        if (ncg[g] > 0) split(ug[g], ug[g + 1], ncg[g], c->gchunk[g]);
     upload(c->chunk_units, cu);
     const int64_t parts = std::max<int64_t>(1, c->n_chunks);
     if (L.path == 1) c->P.ensure(std::max<size_t>(16, (size_t)c->n_chunks * L.n * B * es));
@@ -68,6 +95,10 @@ void plan(ffsat_ctx* c, int64_t B) {
         if (L.precision == 64) set_tiled_smem<double>(c->tiled_smem);
         else set_tiled_smem<float>(c->tiled_smem);
         if (L.wide) set_wide_smem(c->tiled_smem);
+    }
+    if (ncg[2] > 0) {
+        if (L.precision == 64) set_long_smem<double>();
+        else set_long_smem<float>();
     }
     c->plan_B = B;
 }

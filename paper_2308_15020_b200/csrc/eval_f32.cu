@@ -4,6 +4,7 @@
 namespace ffsat {
 template void eval_device_t<float>(ffsat_ctx*, const float*, int64_t, double*, float*, int32_t*, const float*, cudaStream_t, bool);
 template void set_tiled_smem<float>(size_t);
+template void set_long_smem<float>();
 
 void set_wide_smem(size_t bytes) {
 #define FFSAT_KW(K) for (const void* f : {(const void*)dev::fast_wide_kernel<K, 0>, (const void*)dev::fast_wide_kernel<K, 1>, \

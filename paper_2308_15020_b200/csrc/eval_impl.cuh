@@ -48,6 +48,13 @@ inline int fast_kmax(const Layout& L) {
     for (const FastBucket& b : L.fbuckets) km = std::max(km, b.k);
     return km;
 }
+// largest k <= 16 among the fast buckets (the short global kernel's register bound)
+inline int fast_kmax_short(const Layout& L) {
+    int km = 0;
+    for (const FastBucket& b : L.fbuckets)
+        if (b.k <= 16) km = std::max(km, b.k);
+    return km;
+}
 
 // f (fp64), grad (T, may be null), unsat (int32, may be null) at device points x [B][n]; async on st.
 template <typename T>
@@ -129,17 +136,46 @@ void eval_device_t(ffsat_ctx* c, const T* x, int64_t B, double* f, T* grad, int3
             else if (km <= 16) dev::fast_tiled_kernel<T, 16><<<grid, 256, c->tiled_smem, st>>>(a);
             else dev::fast_tiled_kernel<T, 64><<<grid, 256, c->tiled_smem, st>>>(a);
         } else {
+            // chunk groups (plan): k <= 4, 4 < k <= 16 (each with its own register bound), k > 16 (long kernel)
             dev::GlobalArgs<T> a{};
             a.xT = c->xT.as<T>(); a.B = B; a.n = L.n; a.words = c->fast_words.as<uint32_t>();
             a.units = c->units.as<dev::UnitDev>(); a.buckets = c->buckets.as<dev::FastBucketDev>();
             a.chunk_units = c->chunk_units.as<int32_t>(); a.w_pos = w_pos; a.Tb = c->Tb.as<T>();
             a.fpart = c->fpart.as<double>(); a.upart = c->upart.as<int32_t>();
-            dim3 grid((unsigned)PT, (unsigned)c->n_chunks);
-            const int km = fast_kmax(L);
-            if (km <= 4) dev::fast_global_kernel<T, 4><<<grid, 256, 0, st>>>(a);
-            else if (km <= 8) dev::fast_global_kernel<T, 8><<<grid, 256, 0, st>>>(a);
-            else if (km <= 16) dev::fast_global_kernel<T, 16><<<grid, 256, 0, st>>>(a);
-            else dev::fast_global_kernel<T, 64><<<grid, 256, 0, st>>>(a);
+            // several groups: off the profiling path groups 1, 2 run on side streams, concurrently with group 0
+            // (disjoint chunks, T slots and partial rows); joined with the root-path classes below
+            int ngroups = 0;
+            for (int g = 0; g < 3; ++g) ngroups += c->gchunk[g + 1] > c->gchunk[g];
+            const bool gfork = !profiled && ngroups > 1;
+            if (gfork) {
+                c->ensure_side_streams();
+                CK(cudaEventRecord(c->ev_fork, st));
+            }
+            int nl = 0;
+            for (int g = 0; g < 3; ++g) {
+                const int ng = c->gchunk[g + 1] - c->gchunk[g];
+                if (ng == 0) continue;
+                if (nl++ > 0) c->launches += 1;
+                a.chunk_base = c->gchunk[g];
+                dim3 grid((unsigned)PT, (unsigned)ng);
+                const int si = FFSAT_SIDE_STREAMS - g;   // side streams 7, 6 (the root classes start at 0)
+                cudaStream_t gs = st;
+                if (gfork && g > 0) {
+                    gs = c->side[si];
+                    CK(cudaStreamWaitEvent(gs, c->ev_fork, 0));
+                }
+                if (g == 0) dev::fast_global_kernel<T, 4><<<grid, 256, 0, gs>>>(a);
+                else if (g == 1) {
+                    if (fast_kmax_short(L) <= 8) dev::fast_global_kernel<T, 8><<<grid, 256, 0, gs>>>(a);
+                    else dev::fast_global_kernel<T, 16><<<grid, 256, 0, gs>>>(a);
+                } else {
+                    dev::fast_global_long_kernel<T><<<grid, 32 * dev::long_warps<T>(), dev::long_smem_bytes<T>(), gs>>>(a);
+                }
+                if (gs != st) {
+                    CK(cudaEventRecord(c->ev_join[si], gs));
+                    c->pending_join[si] = true;
+                }
+            }
         }
         CK(cudaGetLastError());
     }
@@ -167,6 +203,12 @@ void eval_device_t(ffsat_ctx* c, const T* x, int64_t B, double* f, T* grad, int3
     mark(4);
 }
 
+
+template <typename T>
+void set_long_smem() {
+    CK(cudaFuncSetAttribute((const void*)dev::fast_global_long_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)dev::long_smem_bytes<T>()));
+}
 
 template <typename T>
 void set_tiled_smem(size_t bytes) {

@@ -495,6 +495,9 @@ Layout build_layout(const Formula& F, int path, int precision) {
             Lo.tiled_words[i] = (w & 0x7fffffffu) * pitch | (w & 0x80000000u);
         }
     }
+    // global units hold <= cap literals: 512 for large formulas, smaller for small ones so that the chunk split
+    // (<= one chunk per unit) still yields enough CTAs per point tile to fill the GPU
+    const int64_t gcap = std::min<int64_t>(512, std::max<int64_t>(32, Lo.n_fast_lits / 1024));
     for (size_t bi = 0; bi < Lo.fbuckets.size(); ++bi) {
         const FastBucket& b = Lo.fbuckets[bi];
         int64_t p = b.pos_begin;
@@ -503,7 +506,7 @@ Layout build_layout(const Formula& F, int path, int precision) {
             if (path == 1) {
                 while (q < b.pos_end && fast_class[(size_t)q] == fast_class[(size_t)p]) ++q;
             } else {
-                q = std::min(b.pos_end, p + std::max<int64_t>(1, 512 / b.k));
+                q = std::min(b.pos_end, p + std::max<int64_t>(1, gcap / b.k));
             }
             Lo.units.push_back({(int32_t)bi, (int32_t)(q - p), p});
             Lo.unit_rows.push_back((q - p) * b.k);

@@ -162,6 +162,66 @@ __device__ __forceinline__ T* tile_at(T* base, uint32_t w) {
     return reinterpret_cast<T*>(reinterpret_cast<char*>(base) + (uint32_t)(w << (sizeof(T) == 8 ? 3 : 2)));
 }
 
+// One constraint with 16 < k <= 16 KB (KB = 2..4) for one lane (= one point).  The warp reads the row's literal
+// words once, coalesced (word i in lane i % 32 of register i / 32), takes the negation bits by ballot, and issues
+// all k gathers getx(word) before any arithmetic (all in flight together); the variable values stay in registers
+// (fully unrolled, predicated on the warp-uniform i < k), the exclusive prefix products in registers (SPRE =
+// false) or in a per-lane shared-memory column pre_s[32 i] (SPRE = true, halves the register footprint).
+// emit(i, word, p, cs, first) receives p = pre_i * suf_i (suf seeded with g w_c) and the slope cs = s_i c1: the
+// literal's term is p * cs, to be stored (first channel) or added.
+template <typename T, int KB, int NCH, bool SPRE, typename GetX, typename Emit>
+__device__ __forceinline__ void long_clause(const BucketReg<T>& bk, int k, const uint32_t* wp, T wc, T* pre_s, GetX getx, Emit emit,
+                                            double& facc, int& uacc) {
+    constexpr int KM = 16 * KB, NR = (KM + 31) / 32;
+    const int lane = threadIdx.x & 31;
+    uint32_t wl[NR], neg[NR];
+#pragma unroll
+    for (int r = 0; r < NR; ++r) {
+        wl[r] = lane + 32 * r < k ? __ldg(wp + lane + 32 * r) : 0u;
+        neg[r] = __ballot_sync(0xffffffffu, (int)wl[r] < 0);
+    }
+    T xv[KM];
+#pragma unroll
+    for (int i = 0; i < KM; ++i)
+        if (i < k) xv[i] = getx(__shfl_sync(0xffffffffu, wl[i / 32], i % 32));
+    uint32_t t = 0;
+#pragma unroll
+    for (int i = 0; i < KM; ++i)
+        if (i < k) t += (uint32_t)(xv[i] < (T)0) ^ ((neg[i / 32] >> (i % 32)) & 1u);
+    T fe = bk.g0;
+    T preg[SPRE ? 1 : KM];
+#pragma unroll
+    for (int c = 0; c < NCH; ++c) {
+        const T c0 = bk.c0[c], c1 = bk.c1[c];
+        T run = (T)1;
+#pragma unroll
+        for (int i = 0; i < KM; ++i)
+            if (i < k) {
+                const T cs = flip_sign(c1, neg[i / 32] << (31 - i % 32));
+                if constexpr (SPRE) pre_s[32 * i] = run;
+                else preg[i] = run;
+                run *= fmaT(cs, xv[i], c0);
+            }
+        fe = fmaT(bk.g[c], run, fe);
+        T suf = bk.g[c] * wc;
+#pragma unroll
+        for (int i = KM - 1; i >= 0; --i)
+            if (i < k) {
+                const uint32_t w = __shfl_sync(0xffffffffu, wl[i / 32], i % 32);
+                const T cs = flip_sign(c1, w);
+                T pi;
+                if constexpr (SPRE) pi = pre_s[32 * i];
+                else pi = preg[i];
+                emit(i, w, pi * suf, cs, c == 0);
+                suf *= fmaT(cs, xv[i], c0);
+            }
+    }
+    if (NCH == 0)
+        for (int i = 0; i < k; ++i) emit(i, __ldg(wp + i), (T)0, (T)0, true);
+    facc += (double)(wc * fe);
+    uacc += rule_sat((int)t, bk.tmin, bk.tmax, bk.parity) ? 0 : 1;
+}
+
 // One constraint for one lane (= one point), k <= 16 unrolled, literal words already in registers.
 // With c_s = s_i c1 (literal sign folded into the factor slope), a_i = c0 + c_s x_{v_i};
 // FE = g0 + sum_ch g prod_i a_i and d f / d x_{v_i} = w sum_ch g c_s prod_{j != i} a_j (exclusive
@@ -447,6 +507,22 @@ __device__ void tiled_run_long(const TiledArgs<T>& a, int bucket, const BucketRe
                                const T* xl, T* gl, int warp, int nw, double& facc, int& uacc) {
     const int k = bk.k;
     while (P.u < u1 && P.cur.bucket == bucket) {
+        if constexpr (sizeof(T) == 4) {
+            // fp32: register-resident rows (long_clause); the class is var-disjoint, so terms add straight into the tile
+            for (int j = warp; j < unit_count(P.cur); j += nw) {
+                const int64_t pos = (int64_t)P.cur.pos_begin + j;
+                const uint32_t* wp = a.words + (int64_t)P.cur.word_begin + (int64_t)j * unit_kp(P.cur);
+                auto getx = [&](uint32_t w) { return *tile_at(xl, w); };
+                auto emit = [&](int, uint32_t w, float p, float cs, bool) {
+                    float* g = tile_at(gl, w);
+                    *g = fmaf(p, cs, *g);
+                };
+                const float wc = a.w_pos[pos];
+                if (k <= 32) long_clause<float, 2, NCH, false>(bk, k, wp, wc, nullptr, getx, emit, facc, uacc);
+                else if (k <= 48) long_clause<float, 3, NCH, false>(bk, k, wp, wc, nullptr, getx, emit, facc, uacc);
+                else long_clause<float, 4, NCH, false>(bk, k, wp, wc, nullptr, getx, emit, facc, uacc);
+            }
+        } else {
         for (int j = warp; j < unit_count(P.cur); j += nw) {
             const int64_t pos = (int64_t)P.cur.pos_begin + j;
             const uint32_t* wp = a.words + (int64_t)P.cur.word_begin + (int64_t)j * unit_kp(P.cur);
@@ -468,6 +544,7 @@ __device__ void tiled_run_long(const TiledArgs<T>& a, int bucket, const BucketRe
             fast_terms_blocked<T, NCH>(k, bk, getl, addterm, fe);
             facc += (double)(wc * fe);
             uacc += rule_sat((int)t, bk.tmin, bk.tmax, bk.parity) ? 0 : 1;
+        }
         }
         pipe_advance<T>(a, P, u1, st);
     }
@@ -789,7 +866,8 @@ struct GlobalArgs {
     const uint32_t* words;       // var | neg << 31, padded rows
     const UnitDev* units;
     const FastBucketDev* buckets;
-    const int32_t* chunk_units;
+    const int32_t* chunk_units;  // [n_chunks + 1]; this launch covers chunks chunk_base + blockIdx.y
+    int32_t chunk_base;
     const T* w_pos;
     T* Tb;                       // [tb_slots][B]
     double* fpart;
@@ -874,46 +952,6 @@ __device__ __forceinline__ void global_unit(const GlobalArgs<T>& a, const Bucket
     }
 }
 
-// 16 < k <= 64 on the global path: literals re-read in 16-literal register blocks (fast_terms_blocked).
-template <typename T, int NCH>
-__device__ void global_unit_long(const GlobalArgs<T>& a, const BucketReg<T>& bk, const UnitDev& U, int64_t b, bool bv,
-                                 int warp, int nw, double& facc, int& uacc) {
-    const int k = bk.k;
-    const int64_t bb = bv ? b : 0;
-    for (int j = warp; j < unit_count(U); j += nw) {
-        const int64_t pos = (int64_t)U.pos_begin + j;
-        const uint32_t* wp = a.words + (int64_t)U.word_begin + (int64_t)j * unit_kp(U);
-        const int64_t slot0 = bk.slot_off + (pos - bk.pos_begin) * k;
-        int t = 0;
-        for (int i = 0; i < k; ++i) {
-            const uint32_t w = __ldg(wp + i);
-            const T xv = __ldg(a.xT + (int64_t)(w & 0x7fffffffu) * a.B + bb);
-            t += (int)((xv < (T)0) != ((int)w < 0));
-        }
-        auto getl = [&](int i) -> T {
-            const uint32_t w = __ldg(wp + i);
-            return flip_sign(__ldg(a.xT + (int64_t)(w & 0x7fffffffu) * a.B + bb), w);
-        };
-        T dummy = (T)0;
-        auto addterm = [&](int i, T v, bool first) {
-            T* dst = bv ? a.Tb + (slot0 + i) * a.B + b : &dummy;
-            *dst = first ? v : *dst + v;
-        };
-        T fe;
-        fast_terms_blocked<T, NCH>(k, bk, getl, addterm, fe);
-        const T wc = __ldg(a.w_pos + pos);
-        if (bv) {
-            for (int i = 0; i < k; ++i) {
-                const uint32_t w = __ldg(wp + i);
-                T* dst = a.Tb + (slot0 + i) * a.B + b;
-                *dst = flip_sign(wc * *dst, w);
-            }
-        }
-        facc += (double)(wc * fe);
-        uacc += rule_sat(t, bk.tmin, bk.tmax, bk.parity) ? 0 : 1;
-    }
-}
-
 template <typename T, int NCH, int KMAX>
 __device__ __forceinline__ void global_unit_dispatch(const GlobalArgs<T>& a, const BucketReg<T>& bk, const UnitDev& U, int64_t b,
                                                      bool bv, int warp, int nw, double& facc, int& uacc) {
@@ -922,9 +960,8 @@ __device__ __forceinline__ void global_unit_dispatch(const GlobalArgs<T>& a, con
         FFSAT_K(1) FFSAT_K(2) FFSAT_K(3) FFSAT_K(4) FFSAT_K(5) FFSAT_K(6) FFSAT_K(7) FFSAT_K(8)
         FFSAT_K(9) FFSAT_K(10) FFSAT_K(11) FFSAT_K(12) FFSAT_K(13) FFSAT_K(14) FFSAT_K(15) FFSAT_K(16)
 #undef FFSAT_K
-    default: break;
+    default: break;   // k > 16: fast_global_long_kernel (own chunks)
     }
-    if constexpr (KMAX > 16) global_unit_long<T, NCH>(a, bk, U, b, bv, warp, nw, facc, uacc);
 }
 
 template <typename T, int KMAX>
@@ -934,22 +971,30 @@ __global__ void __launch_bounds__(256) fast_global_kernel(GlobalArgs<T> a) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
     const int64_t b = (int64_t)blockIdx.x * 32 + lane;
     const bool bv = b < a.B;
-    const int chunk = blockIdx.y;
+    const int chunk = a.chunk_base + blockIdx.y;
     double facc = 0.0;
     int uacc = 0;
     int cur = -1;
     BucketReg<T> bk{};
     int nch = 0;
-    for (int u = a.chunk_units[chunk]; u < a.chunk_units[chunk + 1]; ++u) {
-        const UnitDev U = a.units[u];
+    int base = 0;
+    const int ua = a.chunk_units[chunk], ub = a.chunk_units[chunk + 1];
+    UnitDev nextU = ua < ub ? a.units[ua] : UnitDev{};
+    for (int u = ua; u < ub; ++u) {
+        const UnitDev U = nextU;
+        if (u + 1 < ub) nextU = a.units[u + 1];   // header of the next unit in flight during this one
         if (U.bucket != cur) {
             cur = U.bucket;
             bk = load_bucket<T>(a.buckets + cur);
             nch = a.buckets[cur].nch;
         }
-        if (nch == 1) global_unit_dispatch<T, 1, KMAX>(a, bk, U, b, bv, warp, nw, facc, uacc);
-        else if (nch == 2) global_unit_dispatch<T, 2, KMAX>(a, bk, U, b, bv, warp, nw, facc, uacc);
-        else global_unit_dispatch<T, 0, KMAX>(a, bk, U, b, bv, warp, nw, facc, uacc);
+        // the chunk's constraints are dealt to the warps round-robin across unit boundaries (j0 = this warp's
+        // first constraint of the unit), so small units do not idle warps
+        const int j0 = ((warp - base) % nw + nw) % nw;
+        base += unit_count(U);
+        if (nch == 1) global_unit_dispatch<T, 1, KMAX>(a, bk, U, b, bv, j0, nw, facc, uacc);
+        else if (nch == 2) global_unit_dispatch<T, 2, KMAX>(a, bk, U, b, bv, j0, nw, facc, uacc);
+        else global_unit_dispatch<T, 0, KMAX>(a, bk, U, b, bv, j0, nw, facc, uacc);
     }
     fr[warp * 32 + lane] = facc;
     ur[warp * 32 + lane] = uacc;
@@ -958,6 +1003,138 @@ __global__ void __launch_bounds__(256) fast_global_kernel(GlobalArgs<T> a) {
         double f = 0.0;
         int uc = 0;
         for (int w = 0; w < nw; ++w) {
+            f += fr[w * 32 + lane];
+            uc += ur[w * 32 + lane];
+        }
+        a.fpart[(int64_t)chunk * a.B + b] = f;
+        a.upart[(int64_t)chunk * a.B + b] = uc;
+    }
+}
+
+// Long fast constraints (16 < k <= 64) on the global path: their own launch over the chunks that hold the long
+// units (the units are a suffix of the unit list: buckets ascend in k).  Warp = 32 points of one constraint.
+// The warp reads the row's literal words once, coalesced (word i in lane i % 32 of register i / 32), and every
+// lane issues all k gathers x^T[v_i][b] as 4/8-byte cp.async copies into its own shared column xs[i][lane]
+// (no registers held by loads in flight, all k lines requested at once); the exclusive prefixes go to a second
+// column; the backward sweep writes every term once (streaming store).  kLongWarps warps per CTA, 2 x 64 x 32
+// values of shared memory per warp (dynamic: f32 64 KB, f64 64 KB with 2 warps).
+template <typename T>
+__host__ __device__ constexpr int long_warps() { return sizeof(T) == 4 ? 4 : 2; }
+constexpr int kLongKMax = 64;
+template <typename T>
+__host__ __device__ constexpr size_t long_smem_bytes() { return (size_t)long_warps<T>() * 2 * kLongKMax * 32 * sizeof(T); }
+
+template <typename T, int NCH>
+__device__ void global_unit_long_cp(const GlobalArgs<T>& a, const BucketReg<T>& bk, const UnitDev& U, int64_t b, bool bv,
+                                    int j0, T* xs, T* ps, double& facc, int& uacc) {
+    const int k = bk.k;
+    const int lane = threadIdx.x & 31;
+    const T* xb = a.xT + (bv ? b : 0);
+    const uint32_t B32 = (uint32_t)a.B;   // plan() checks n B < 2^32
+    const int k0 = min(k, 32);            // literals [0, k0) have their word in wl0, [32, k) in wl1
+    for (int j = j0; j < unit_count(U); j += long_warps<T>()) {
+        const int64_t pos = (int64_t)U.pos_begin + j;
+        const uint32_t* wp = a.words + (int64_t)U.word_begin + (int64_t)j * unit_kp(U);
+        const uint32_t wl0 = lane < k ? __ldg(wp + lane) : 0u;
+        const uint32_t wl1 = lane + 32 < k ? __ldg(wp + lane + 32) : 0u;
+        const T wc = __ldg(a.w_pos + pos);
+        __syncwarp();   // the previous constraint's reads of xs / ps are done
+#pragma unroll 4
+        for (int i = 0; i < k0; ++i)
+            cp_async_small<sizeof(T)>(xs + 32 * i, xb + (__shfl_sync(0xffffffffu, wl0, i) & 0x7fffffffu) * B32);
+#pragma unroll 4
+        for (int i = 32; i < k; ++i)
+            cp_async_small<sizeof(T)>(xs + 32 * i, xb + (__shfl_sync(0xffffffffu, wl1, i - 32) & 0x7fffffffu) * B32);
+        cp_async_commit_wait_all();
+        T fe = bk.g0;
+        uint32_t t = 0;
+        T* dst = a.Tb + (bk.slot_off + (pos - bk.pos_begin) * k) * a.B + b;
+#pragma unroll
+        for (int c = 0; c < NCH; ++c) {
+            const T c0 = bk.c0[c], c1 = bk.c1[c];
+            T run = (T)1;
+            // forward: exclusive prefixes to ps (channel 0 also counts the True literals)
+            auto fwd = [&](int i, uint32_t w) {
+                const T xv = xs[32 * i];
+                if (c == 0) t += (uint32_t)(xv < (T)0) ^ (w >> 31);
+                ps[32 * i] = run;
+                run *= fmaT(flip_sign(c1, w), xv, c0);
+            };
+#pragma unroll 4
+            for (int i = 0; i < k0; ++i) fwd(i, __shfl_sync(0xffffffffu, wl0, i));
+#pragma unroll 4
+            for (int i = 32; i < k; ++i) fwd(i, __shfl_sync(0xffffffffu, wl1, i - 32));
+            fe = fmaT(bk.g[c], run, fe);
+            T suf = bk.g[c] * wc;
+            // backward: term_i = pre_i suf_i s_i c1, written once (channel 0) or accumulated
+            auto bwd = [&](int i, uint32_t w) {
+                const T cs = flip_sign(c1, w);
+                const T p = ps[32 * i] * suf;
+                if (bv) {
+                    T* d = dst + (uint32_t)i * B32;
+                    if (c == 0) __stcs(d, p * cs);
+                    else *d = fmaT(p, cs, *d);
+                }
+                suf *= fmaT(cs, xs[32 * i], c0);
+            };
+#pragma unroll 4
+            for (int i = k - 1; i >= 32; --i) bwd(i, __shfl_sync(0xffffffffu, wl1, i - 32));
+#pragma unroll 4
+            for (int i = k0 - 1; i >= 0; --i) bwd(i, __shfl_sync(0xffffffffu, wl0, i));
+        }
+        if (NCH == 0) {
+            for (int i = 0; i < k; ++i) {
+                const uint32_t w = __shfl_sync(0xffffffffu, i < 32 ? wl0 : wl1, i & 31);
+                t += (uint32_t)(xs[32 * i] < (T)0) ^ (w >> 31);
+                if (bv) __stcs(dst + (uint32_t)i * B32, (T)0);
+            }
+        }
+        facc += (double)(wc * fe);
+        uacc += rule_sat((int)t, bk.tmin, bk.tmax, bk.parity) ? 0 : 1;
+    }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(32 * long_warps<T>()) fast_global_long_kernel(GlobalArgs<T> a) {
+    constexpr int kLongWarps = long_warps<T>();
+    extern __shared__ __align__(16) unsigned char smem_raw[];   // long_smem_bytes<T>()
+    __shared__ double fr[kLongWarps * 32];
+    __shared__ int ur[kLongWarps * 32];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t b = (int64_t)blockIdx.x * 32 + lane;
+    const bool bv = b < a.B;
+    const int chunk = a.chunk_base + blockIdx.y;
+    T* xs = reinterpret_cast<T*>(smem_raw) + warp * 2 * kLongKMax * 32 + lane;   // per-lane columns, stride 32
+    T* ps = xs + kLongKMax * 32;
+    double facc = 0.0;
+    int uacc = 0;
+    int cur = -1;
+    BucketReg<T> bk{};
+    int nch = 0;
+    int base = 0;
+    const int ua = a.chunk_units[chunk], ub = a.chunk_units[chunk + 1];
+    UnitDev nextU = ua < ub ? a.units[ua] : UnitDev{};
+    for (int u = ua; u < ub; ++u) {
+        const UnitDev U = nextU;
+        if (u + 1 < ub) nextU = a.units[u + 1];   // header of the next unit in flight during this one
+        if (U.bucket != cur) {
+            cur = U.bucket;
+            bk = load_bucket<T>(a.buckets + cur);
+            nch = a.buckets[cur].nch;
+        }
+        const int j0 = ((warp - base) % kLongWarps + kLongWarps) % kLongWarps;   // round-robin across units
+        base += unit_count(U);
+        if (nch == 1) global_unit_long_cp<T, 1>(a, bk, U, b, bv, j0, xs, ps, facc, uacc);
+        else if (nch == 2) global_unit_long_cp<T, 2>(a, bk, U, b, bv, j0, xs, ps, facc, uacc);
+        else global_unit_long_cp<T, 0>(a, bk, U, b, bv, j0, xs, ps, facc, uacc);
+    }
+    fr[warp * 32 + lane] = facc;
+    ur[warp * 32 + lane] = uacc;
+    __syncthreads();
+    if (warp == 0 && bv) {
+        double f = 0.0;
+        int uc = 0;
+        for (int w = 0; w < kLongWarps; ++w) {
             f += fr[w * 32 + lane];
             uc += ur[w * 32 + lane];
         }

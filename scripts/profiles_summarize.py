@@ -19,19 +19,21 @@ def num(v):
     return float(str(v).replace(",", ""))
 
 
-for rep, kname in (("prof_tiled", "fast_wide_kernel"), ("prof_sym", "sym_item_kernel"), ("prof_global", "fast_global_kernel")):
+for rep, cfg, kname in (("prof_tiled", "c2", "fast_wide_kernel"), ("prof_sym", "c3", "sym_item_kernel"),
+                        ("prof_global", "c5", "fast_global_kernel"), ("prof_short", "c4", "fast_global_kernel"),
+                        ("prof_long", "c4", "fast_global_long_kernel")):
     p = os.path.join(G, rep + ".ncu-rep")
     if not os.path.exists(p):
         continue
     txt = subprocess.run([sys.executable, os.path.join(ROOT, "scripts", "ncu_summary.py"), p], capture_output=True, text=True).stdout
-    with open(os.path.join(PR, f"{tag}_ncu_{kname}.txt"), "w") as fh:
+    with open(os.path.join(PR, f"{tag}_ncu_{cfg}_{kname}.txt"), "w") as fh:
         fh.write(f"# ncu --set full --clock-control none, one launch of {kname} ({rep}.ncu-rep)\n" + txt)
     v, u = raw(p)
     scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "B": 1, "KB": 1e3, "MB": 1e6, "GB": 1e9}
     dram = num(v["dram__bytes_read.sum"]) * scale[u["dram__bytes_read.sum"]] + \
         num(v["dram__bytes_write.sum"]) * scale[u["dram__bytes_write.sum"]]
     dur = num(v["gpu__time_duration.sum"]) * {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1, "us": 1, "msecond": 1e3, "ms": 1e3}[u["gpu__time_duration.sum"]]
-    summary[kname] = {"dram_bytes_per_launch": dram, "duration_us_ncu": dur, "round": tag,
+    summary[f"{cfg}:{kname}"] = {"dram_bytes_per_launch": dram, "duration_us_ncu": dur, "round": tag,
                       "grid": v.get("launch__grid_size"), "block": v.get("launch__block_size"),
                       "registers": v.get("launch__registers_per_thread"),
                       "fp64_pipe_pct": v.get("sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active"),
@@ -67,6 +69,8 @@ def launches(src, dst):
 
 launches("launches_c2.csv", f"{tag}_launches_c2.csv")
 launches("launches_c3.csv", f"{tag}_launches_c3.csv")
+launches("launches_c4.csv", f"{tag}_launches_c4.csv")
+launches("launches_c5.csv", f"{tag}_launches_c5.csv")
 for f in sorted(os.listdir(G)):
     if f.startswith("bench_") and f.endswith(".json") and os.path.getsize(os.path.join(G, f)):
         shutil.copy(os.path.join(G, f), os.path.join(PR, f"{tag}_{f}"))

@@ -127,6 +127,33 @@ def test_c4_hybrid_small():
     compare(inst, synth.points("U", 64, inst.n, 26))
 
 
+@pytest.mark.parametrize("precision", [32, 64])
+@pytest.mark.parametrize("dist", ["U", "N", "Z"])
+def test_long_fast_only_global(precision, dist):
+    """Only 16 < k <= 64 fast constraints (XOR / XNOR / OR / NAE / AND kinds): the global path runs the long
+    kernel alone (no short chunks); ragged batch spanning several point tiles."""
+    rng = np.random.default_rng(31)
+    n, kinds, bounds, cl = 200, [], [], []
+    for j in range(90):
+        k = int(rng.integers(17, 65))
+        kd = [synth.OR, synth.XOR, synth.XNOR, synth.NAE, synth.CARD_GE][j % 5]
+        vs = rng.choice(n, size=k, replace=False)
+        neg = rng.random(k) < 0.5
+        kinds.append(kd); bounds.append(k if kd == synth.CARD_GE else 0); cl.append(np.where(neg, -(vs + 1), vs + 1))
+    inst = synth._build("long_fast", n, kinds, bounds, cl)
+    ctx = P.Context.from_instance(inst, precision=precision, path=2, device=0)
+    compare(inst, synth.points(dist, 70, inst.n, 29), precision=precision, ctx=ctx)
+
+
+def test_c4_hybrid_global_full_batch():
+    """c4's shape (3-CNF + XOR k = 3..64, n = 1024) on the global path (short and long kernels) at B = 1024 (the
+    bench launch configuration); oracle on every point of a 1024-point batch."""
+    inst = synth.config4_hybrid(0)
+    ctx = P.Context.from_instance(inst, precision=32, device=0)
+    assert ctx.info["path"] == 2
+    compare(inst, synth.points("U", 1024, inst.n, 30), ctx=ctx)
+
+
 @pytest.mark.parametrize("k", [65, 130, 300, 700])
 def test_long_cardinality_fp64(k):
     """Root path in fp64 at long k (group sizes 32..128), at-most-b, mixed with clauses."""
