@@ -75,6 +75,10 @@ struct ffsat_ctx {
     int64_t persistent_bytes = 0;
     // per-B scratch
     ffsat::DBuf xT, Tb, P, fpart, upart, fsym, usym, chunk_units, x_stage, g_stage, f_stage, u_stage, w_stage;
+    // root splits (plan): effective S per root-path class and its regions of the split partial buffers
+    ffsat::DBuf TbS, fS;                 // [S][class literals][B] terms, [S][class constraints][B] Re sum G Q
+    std::vector<int32_t> sym_S;
+    std::vector<int64_t> sym_offT, sym_offF;
     int64_t plan_B = -1;
     int32_t n_chunks = 0;
     // global path: chunk groups by bucket length class -- chunks [gchunk[g], gchunk[g + 1]) hold the units with

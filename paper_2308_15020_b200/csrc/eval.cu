@@ -90,6 +90,28 @@ void plan(ffsat_ctx* c, int64_t B) {
     c->fpart.ensure((size_t)parts * B * 8);
     c->upart.ensure((size_t)parts * B * 4);
     c->fsym.ensure(std::max<size_t>(16, (size_t)L.n_sym * B * 8));
+    {   // root splits: per-class partial regions (fall back to S = 1 if they would exceed 4 GiB)
+        const size_t ncl = L.sym_classes.size();
+        c->sym_S.assign(ncl, 1);
+        c->sym_offT.assign(ncl, 0);
+        c->sym_offF.assign(ncl, 0);
+        size_t tT = 0, tF = 0;
+        for (size_t i = 0; i < ncl; ++i) {
+            const SymClass& cl = L.sym_classes[i];
+            if (cl.S <= 1) continue;
+            c->sym_S[i] = cl.S;
+            c->sym_offT[i] = (int64_t)tT;
+            c->sym_offF[i] = (int64_t)tF;
+            tT += (size_t)cl.S * (size_t)(cl.lit_end - cl.lit_begin) * (size_t)B;
+            tF += (size_t)cl.S * (size_t)(cl.end - cl.begin) * (size_t)B;
+        }
+        if (tT * es + tF * 8 > (size_t)4 << 30) {
+            c->sym_S.assign(ncl, 1);
+            tT = tF = 0;
+        }
+        c->TbS.ensure(std::max<size_t>(16, tT * es));
+        c->fS.ensure(std::max<size_t>(16, tF * 8));
+    }
     c->usym.ensure(std::max<size_t>(16, (size_t)L.n_sym * B * 4));
     if (L.path == 1) {
         if (L.precision == 64) set_tiled_smem<double>(c->tiled_smem);

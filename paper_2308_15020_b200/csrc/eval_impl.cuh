@@ -95,8 +95,15 @@ void eval_device_t(ffsat_ctx* c, const T* x, int64_t B, double* f, T* grad, int3
         for (size_t i = 0; i < ncl; ++i) {
             cudaStream_t ss = fork ? c->side[i % FFSAT_SIDE_STREAMS] : st;
             if (fork && i < FFSAT_SIDE_STREAMS) CK(cudaStreamWaitEvent(ss, c->ev_fork, 0));
-            launch_sym_class<T>(L.sym_classes[i], L.sym_classes[i].G == 0 ? aT : a, ss);
-            c->launches += 1;
+            const SymClass& cl = L.sym_classes[i];
+            dev::SymArgs<T> ac = cl.G == 0 ? aT : a;
+            ac.S = c->sym_S[i];
+            ac.s_end = cl.end;
+            ac.lit0 = cl.lit_begin;
+            ac.TbS = c->TbS.as<T>() + c->sym_offT[i];
+            ac.fS = c->fS.as<double>() + c->sym_offF[i];
+            launch_sym_class<T>(cl, ac, ss);
+            c->launches += ac.S > 1 ? 2 : 1;   // + the split combine
         }
         CK(cudaGetLastError());
         if (fork) {

@@ -449,6 +449,11 @@ Layout build_layout(const Formula& F, int path, int precision) {
         Lo.sym_classes.back().max_mp = std::max(Lo.sym_classes.back().max_mp, (k + 1) / 2);
         if (G == 0) Lo.sym_lane = true;
     }
+    for (SymClass& cl : Lo.sym_classes) {
+        cl.lit_begin = Lo.sym_off[(size_t)cl.begin];
+        cl.lit_end = Lo.sym_off[(size_t)cl.end];
+        cl.S = cl.G == 0 ? 1 : std::max(1, std::min(32, (cl.max_mp + kRootChunk - 1) / kRootChunk));
+    }
 
     // ---- T-buffer slots and occurrence CSR (ascending slot order per variable)
     Lo.tb_fast = path == 2 ? Lo.n_fast_lits : 0;

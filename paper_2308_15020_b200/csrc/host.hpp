@@ -63,7 +63,10 @@ struct SymClass {                   // launch class: G threads per (constraint, 
     int32_t G, C, R;                // R roots per pass
     int64_t begin, end;             // sym constraint indices
     int32_t max_mp;                 // largest M' in the class (root-table size staged in shared memory)
+    int32_t S = 1;                  // root splits: each item's M' roots are shared by S CTAs (balance; G > 0 only)
+    int64_t lit_begin = 0, lit_end = 0;   // the class's literals in the sym word array
 };
+constexpr int kRootChunk = 64;      // target roots per CTA of the root path (SymClass::S = ceil(max M' / kRootChunk))
 
 struct WorkUnit {                   // a run of fast constraints of one bucket, contiguous positions
     int32_t bucket;                 // tiled path: a var-disjoint class (no variable occurs twice in it),

@@ -1164,6 +1164,12 @@ struct SymArgs {
     T* Tb;                       // [tb_slots][B]
     double* fsym;                // [n_sym][B]  w * FE
     int32_t* usym;               // [n_sym][B]  1 if sgn(x) falsifies
+    // root splits (sym_item_kernel, S > 1): CTA (item, split) covers an even share of the item's roots and
+    // writes partials, summed in split order by sym_combine_kernel
+    int32_t S;
+    int64_t s_end, lit0;         // the class's constraint end and first literal
+    T* TbS;                      // [S][class literals][B]  w s_i (partial dFE/dl_i)
+    double* fS;                  // [S][class constraints][B]  partial Re sum_m G_m Q_m
 };
 
 template <typename T>
@@ -1315,13 +1321,18 @@ sym_item_kernel(SymArgs<T> a, int64_t s_begin) {
     __shared__ int tcnt[NW];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int t = threadIdx.x;
-    const int64_t item = blockIdx.x;
+    const int64_t item = blockIdx.x / a.S;
+    const int split = (int)(blockIdx.x - item * a.S);
     const bool valid = true;
     const int64_t s = s_begin + item / a.B;
     const int64_t b = item - (item / a.B) * a.B;
     const SymSigDev sg = a.sigs[a.sig_of[s]];
     const int k = sg.k;
     const int64_t lo = a.off[s];
+    // this CTA's roots [m0, m0 + Mps) of the item's M' (an even share when split)
+    const int per = (sg.Mp + a.S - 1) / a.S;
+    const int m0 = min(sg.Mp, split * per);
+    const int Mps = min(sg.Mp, m0 + per) - m0;
     const int i0 = t * C;
     // padding literals past k get l = 1 (a certainly-False literal: p = 0), whose factor
     // alpha + beta = 1 (exactly in real arithmetic, to one rounding in the table), so the sweeps need
@@ -1344,28 +1355,42 @@ sym_item_kernel(SymArgs<T> a, int64_t s_begin) {
     double fe_acc = 0.0;
     // root table alpha, beta, G, H (8 T per root) staged in shared memory once per item: the per-root
     // coefficient reads in the sweeps become broadcast LDS instead of dependent global loads
-    T* cf = reinterpret_cast<T*>(sym_smem);
+    T* cf = reinterpret_cast<T*>(sym_smem);   // roots m0 .. m0 + Mps - 1, indexed from 0
     {
-        const T* g = a.coef + sg.coef_off * 8;
-        for (int i = t; i < sg.Mp * 8; i += 32 * NW) cf[i] = g[i];
+        const T* g = a.coef + (sg.coef_off + m0) * 8;
+        for (int i = t; i < Mps * 8; i += 32 * NW) cf[i] = g[i];
         __syncthreads();
     }
     const cplx<T> one{(T)1, (T)0};
     cplx<T> al[R == 0 ? 1 : R], be[R == 0 ? 1 : R];
-    load_ab<T, (R == 0 ? 1 : R)>(cf, 0, sg.Mp, al, be);
+    if (Mps > 0) load_ab<T, (R == 0 ? 1 : R)>(cf, 0, Mps, al, be);
     int m = 0;
     constexpr int RP = R == 0 ? 1 : R;   // roots per pass
-    for (; m + RP <= sg.Mp; m += RP)
-        sym_roots<T, NW, C, RP, (R == 1)>(cf, m, sg.Mp, lane, warp, t, l, term, fe_acc, wtot, al, be);
-    if (R > 1 && m < sg.Mp) {   // odd remainder: one root (al[0], be[0] hold it)
+    for (; m + RP <= Mps; m += RP)
+        sym_roots<T, NW, C, RP, (R == 1)>(cf, m, Mps, lane, warp, t, l, term, fe_acc, wtot, al, be);
+    if (R > 1 && m < Mps) {   // odd remainder: one root (al[0], be[0] hold it)
         cplx<T> al1[1] = {al[0]}, be1[1] = {be[0]};
-        sym_roots<T, NW, C, 1>(cf, m, sg.Mp, lane, warp, t, l, term, fe_acc, wtot, al1, be1);
+        sym_roots<T, NW, C, 1>(cf, m, Mps, lane, warp, t, l, term, fe_acc, wtot, al1, be1);
     }
     const T wc = a.w_sym[s];
+    if (a.S > 1) {   // partials of this root share; the unsat count by split 0
+        const int64_t nlit = a.off[a.s_end] - a.lit0;
+#pragma unroll
+        for (int j = 0; j < C; ++j) {
+            const int i = i0 + j;
+            if (i < k) {
+                const uint32_t w = __ldg(a.words + lo + i);
+                const T v = wc * term[j];
+                a.TbS[((int64_t)split * nlit + (lo - a.lit0) + i) * a.B + b] = (int)w < 0 ? -v : v;
+            }
+        }
+        if (t == 0) a.fS[((int64_t)split * (a.s_end - s_begin) + (s - s_begin)) * a.B + b] = fe_acc;
+        if (split != 0) return;
+    }
 #pragma unroll
     for (int j = 0; j < C; ++j) {
         const int i = i0 + j;
-        if (valid && i < k) {
+        if (a.S == 1 && i < k) {
             const uint32_t w = __ldg(a.words + lo + i);
             const T v = wc * term[j];
             a.Tb[(a.tb_fast + lo + i) * a.B + b] = (int)w < 0 ? -v : v;
@@ -1381,8 +1406,30 @@ sym_item_kernel(SymArgs<T> a, int64_t s_begin) {
         for (int w = 0; w < NW; ++w) tc += tcnt[w];
     }
     if (valid && t == 0) {
-        a.fsym[s * a.B + b] = (double)wc * (sg.g0 + fe_acc);
+        if (a.S == 1) a.fsym[s * a.B + b] = (double)wc * (sg.g0 + fe_acc);
         a.usym[s * a.B + b] = rule_sat(tc, sg.tmin, sg.tmax, sg.parity) ? 0 : 1;
+    }
+}
+
+// Sum of the root-split partials of one class in split order (deterministic): the class's T rows and w (g0 +
+// Re sum_m G_m Q_m) per constraint.  Grid-stride over (class literal, point) then (class constraint, point).
+template <typename T>
+__global__ void __launch_bounds__(256) sym_combine_kernel(SymArgs<T> a, int64_t s_begin) {
+    const int64_t nlit = a.off[a.s_end] - a.lit0, ncons = a.s_end - s_begin;
+    const int64_t nT = nlit * a.B, nF = ncons * a.B;
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < nT + nF; e += (int64_t)gridDim.x * blockDim.x) {
+        if (e < nT) {
+            T v = a.TbS[e];
+            for (int sp = 1; sp < a.S; ++sp) v += a.TbS[(int64_t)sp * nT + e];
+            a.Tb[(a.tb_fast + a.lit0) * a.B + e] = v;
+        } else {
+            const int64_t f = e - nT;
+            double v = a.fS[f];
+            for (int sp = 1; sp < a.S; ++sp) v += a.fS[(int64_t)sp * nF + f];
+            const int64_t s = s_begin + f / a.B;
+            const SymSigDev sg = a.sigs[a.sig_of[s]];
+            a.fsym[s_begin * a.B + f] = (double)a.w_sym[s] * (sg.g0 + v);
+        }
     }
 }
 

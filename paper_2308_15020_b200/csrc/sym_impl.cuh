@@ -16,8 +16,7 @@ void launch_sym_class(const SymClass& cl, const dev::SymArgs<T>& a, cudaStream_t
     const int64_t items = (cl.end - cl.begin) * a.B;
     if (items == 0) return;
     if (items > INT32_MAX) throw Error(FFSAT_ERR_ARG, "too many root-path items for one launch");
-    const unsigned g = (unsigned)items;
-    if (cl.G == 0) {   // thread per item; a.x must be x^T here (sb = 1, sv = B)
+        if (cl.G == 0) {   // thread per item; a.x must be x^T here (sb = 1, sv = B)
         const unsigned nb = (unsigned)((items + 255) / 256);
         switch (cl.C) {
         case 8: dev::sym_lane_kernel<T, 8><<<nb, 256, 0, st>>>(a, cl.begin, items); break;
@@ -27,15 +26,22 @@ void launch_sym_class(const SymClass& cl, const dev::SymArgs<T>& a, cudaStream_t
         }
         return;
     }
-    const size_t smem = (size_t)cl.max_mp * 8 * sizeof(T);   // the root table of the longest signature
+    // root splits: a.S CTAs per item, each staging its share of the root table
+    if ((int64_t)items * a.S > INT32_MAX) throw Error(FFSAT_ERR_ARG, "too many root-path CTAs for one launch");
+    const unsigned gs = (unsigned)(items * a.S);
+    const size_t smem = (size_t)((cl.max_mp + a.S - 1) / a.S) * 8 * sizeof(T);   // the largest root share
     switch (cl.G / 32 * 1000 + cl.C * 10 + cl.R) {
 #define FFSAT_SYM(NW, C) case NW * 1000 + C * 10 + 1: \
         set_sym_smem((const void*)dev::sym_item_kernel<T, NW, C, 1>, smem); \
-        dev::sym_item_kernel<T, NW, C, 1><<<g, 32 * NW, smem, st>>>(a, cl.begin); break;
+        dev::sym_item_kernel<T, NW, C, 1><<<gs, 32 * NW, smem, st>>>(a, cl.begin); break;
         FFSAT_SYM(1, 4) FFSAT_SYM(1, 8) FFSAT_SYM(1, 16) FFSAT_SYM(2, 12) FFSAT_SYM(2, 16)
         FFSAT_SYM(4, 10) FFSAT_SYM(3, 16) FFSAT_SYM(4, 14) FFSAT_SYM(4, 16) FFSAT_SYM(6, 16) FFSAT_SYM(8, 16)
 #undef FFSAT_SYM
     default: throw Error(FFSAT_ERR_ARG, "unsupported root-path launch class");
+    }
+    if (a.S > 1) {
+        const int64_t work = (cl.lit_end - cl.lit_begin + cl.end - cl.begin) * a.B;
+        dev::sym_combine_kernel<T><<<(unsigned)std::min<int64_t>(4 * 148, (work + 255) / 256), 256, 0, st>>>(a, cl.begin);
     }
 }
 
