@@ -45,6 +45,7 @@ CONFIGS = {
 SM_COUNT = 148
 FP32_LANES, FP64_LANES = 128, 64  # FP32 / FP64 lanes per SM per clock (B200 guide unit counts)
 # Algorithmic FP lane-operations (one FMA = one lane-op = one pipe slot: count instructions):
+SMEM_BYTES_PER_TERM = 12   # x tile LDS + gradient tile LDS + STS, 4 B each
 FAST_OPS_PER_TERM = 5             # factor FMA, prefix MUL, prefix*suffix MUL, suffix MUL, gradient FMA
 ROOT_OPS_PER_LIT_ROOT = 12        # factor 2 FMA, prefix + suffix complex MUL (2 x 4), Re-accumulate 2 FMA (App. A)
 
@@ -376,9 +377,17 @@ def main():
         kname, kms = ("fast_wide_kernel" if info.get("wide") else "fast_tiled_kernel"), fast_ms
         ops = FAST_OPS_PER_TERM * info["n_fast_lits"] * B
         achieved = ops / (kms * 1e-3) / 1e12
+        # the resource that binds this kernel (ncu: L1/shared throughput ~74%) is shared-memory bandwidth:
+        # per term the x tile read and the gradient tile read-modify-write, 3 x 4 B, against 128 B/clk/SM
+        smem_bytes = SMEM_BYTES_PER_TERM * info["n_fast_lits"] * B
+        smem_peak = SM_COUNT * 128 * mhz * 1e6 / 1e9   # GB/s
+        smem_ach = smem_bytes / (fast_ms * 1e-3) / 1e9
         roofline = {"bound": "alu", "achieved": achieved, "peak": alu_peak, "unit": "T lane-op/s",
                     "algorithmic_ops_per_term": FAST_OPS_PER_TERM, "peak_source": alu_src,
-                    "note": "issue/LSU-limited gather-scatter kernel; see DESIGN.md 7 and profiles/*fast_tiled*"}
+                    "smem": {"achieved": smem_ach, "peak": smem_peak, "unit": "GB/s", "frac": smem_ach / smem_peak,
+                             "algorithmic_bytes_per_term": SMEM_BYTES_PER_TERM,
+                             "peak_source": f"{SM_COUNT} SMs x 128 B/clk shared-memory bandwidth x {mhz:.0f} MHz"},
+                    "note": "binding resource: shared-memory bandwidth (the smem entry); see DESIGN.md 7"}
         peak = alu_peak
     else:
         kname, kms = "sym_item_kernel", root_ms

@@ -684,16 +684,29 @@ __device__ __forceinline__ uint32_t red_step(uint32_t m, float xv, uint32_t w) {
     return RED == 1 ? (m | bit) : RED == 2 ? (m & bit) : (m ^ bit);
 }
 
+// 32-bit shared-memory float2 access at byte address base + 4 w (the multiply by 4 shifts the literal's
+// sign bit out, so one IMAD forms the address)
+__device__ __forceinline__ float2 lds2(uint32_t addr) {
+    float2 v;
+    asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "r"(addr));
+    return v;
+}
+__device__ __forceinline__ void sts2(uint32_t addr, float2 v) {
+    asm volatile("st.shared.v2.f32 [%0], {%1, %2};" ::"r"(addr), "f"(v.x), "f"(v.y) : "memory");
+}
+
 template <int K, int RED>
-__device__ __forceinline__ void wide_clause(const BucketReg<float>& bk, int redpol, const uint32_t* sw, float wc, const float* xl,
+__device__ __forceinline__ void wide_clause(const BucketReg<float>& bk, int redpol, const uint32_t* sw, float wc, uint32_t xl,
                                             double& f0, double& f1, int& u0, int& u1) {
     uint32_t w[K];
     load_words_smem<K>(sw, w);
+    uint32_t ad[K];
     float2 xv[K];
     uint32_t t0 = red_init<RED>(), t1 = red_init<RED>();
 #pragma unroll
     for (int i = 0; i < K; ++i) {
-        xv[i] = *reinterpret_cast<const float2*>(tile_at(xl, w[i]));
+        ad[i] = xl + (w[i] << 2);
+        xv[i] = lds2(ad[i]);
         if (RED == 0) {
             t0 += lit_true(xv[i].x, w[i]);
             t1 += lit_true(xv[i].y, w[i]);
@@ -705,14 +718,13 @@ __device__ __forceinline__ void wide_clause(const BucketReg<float>& bk, int redp
     const float2 c0 = make_float2(bk.c0[0], bk.c0[0]);
     float2 av[K], pre[K];
     float cs[K];
-    float2 run = make_float2(1.0f, 1.0f);
 #pragma unroll
     for (int i = 0; i < K; ++i) {
         cs[i] = flip_sign(bk.c1[0], w[i]);
         av[i] = __ffma2_rn(make_float2(cs[i], cs[i]), xv[i], c0);
-        pre[i] = run;
-        run = __fmul2_rn(run, av[i]);
+        if (i > 0) pre[i] = i == 1 ? av[0] : __fmul2_rn(pre[i - 1], av[i - 1]);   // pre[0] = 1 is implicit
     }
+    const float2 run = K == 1 ? av[0] : __fmul2_rn(pre[K - 1], av[K - 1]);
     const float2 fe = __ffma2_rn(make_float2(bk.g[0], bk.g[0]), run, make_float2(bk.g0, bk.g0));
     const float sw0 = bk.g[0] * wc;
     float2 suf = make_float2(sw0, sw0);
@@ -721,14 +733,14 @@ __device__ __forceinline__ void wide_clause(const BucketReg<float>& bk, int redp
     // serialisation per literal)
     float2 gv[K];
 #pragma unroll
-    for (int i = 0; i < K; ++i) gv[i] = *reinterpret_cast<const float2*>(tile_at(xl, w[i]) + kWHalf);
+    for (int i = 0; i < K; ++i) gv[i] = lds2(ad[i] + 4 * kWHalf);
 #pragma unroll
     for (int i = K - 1; i >= 0; --i) {
-        gv[i] = __ffma2_rn(__fmul2_rn(pre[i], suf), make_float2(cs[i], cs[i]), gv[i]);
-        suf = __fmul2_rn(suf, av[i]);
+        gv[i] = __ffma2_rn(i == 0 ? suf : __fmul2_rn(pre[i], suf), make_float2(cs[i], cs[i]), gv[i]);
+        if (i > 0) suf = __fmul2_rn(suf, av[i]);
     }
 #pragma unroll
-    for (int i = 0; i < K; ++i) *reinterpret_cast<float2*>(const_cast<float*>(tile_at(xl, w[i])) + kWHalf) = gv[i];
+    for (int i = 0; i < K; ++i) sts2(ad[i] + 4 * kWHalf, gv[i]);
     f0 += (double)(wc * fe.x);
     f1 += (double)(wc * fe.y);
     if (RED == 0) {
@@ -783,7 +795,7 @@ __global__ void __launch_bounds__(256, 2) fast_wide_kernel(TiledArgs<float> a) {
 
     double f0 = 0.0, f1 = 0.0;
     int uc0 = 0, uc1 = 0;
-    const float* xl = xs + 2 * lane;
+    const uint32_t xl32 = (uint32_t)__cvta_generic_to_shared(xs + 2 * lane);   // this lane's x pair in row 0
     const int u0 = a.chunk_units[chunk], u1 = a.chunk_units[chunk + 1];
     UnitDev cur{}, next{}, after{};
     if (u0 < u1) {
@@ -810,7 +822,7 @@ __global__ void __launch_bounds__(256, 2) fast_wide_kernel(TiledArgs<float> a) {
         const uint32_t* sw = st.words[buf];
         const float* swt = st.w[buf];
         const int count = unit_count(cur);
-        for (int j = warp; j < count; j += nw) wide_clause<K, RED>(bk, redpol, sw + j * K_PAD(K), swt[j], xl, f0, f1, uc0, uc1);
+        for (int j = warp; j < count; j += nw) wide_clause<K, RED>(bk, redpol, sw + j * K_PAD(K), swt[j], xl32, f0, f1, uc0, uc1);
         // advance: the next unit's words are ready, everybody is done with this buffer
         cp_async_wait_all();
         __syncthreads();
@@ -914,39 +926,35 @@ __device__ __forceinline__ void clause_terms(const BucketReg<T>& bk, const uint3
 template <typename T, int K, int NCH>
 __device__ __forceinline__ void global_unit(const GlobalArgs<T>& a, const BucketReg<T>& bk, const UnitDev& U, int64_t b, bool bv,
                                             int warp, int nw, double& facc, int& uacc) {
+    // NP constraints of the warp in flight at once (j, j + nw): 2 (4 measured slower on c5: fewer resident warps)
+    constexpr int NP = 2;
     const int count = unit_count(U);
     const int64_t wbase = (int64_t)U.word_begin;
     const int64_t sbase = bk.slot_off + ((int64_t)U.pos_begin - bk.pos_begin) * K;
     const int64_t bb = bv ? b : 0;
-    int j = warp;
-    for (; j < count; j += 2 * nw) {
-        const bool two = j + nw < count;
-        uint32_t w0[K], w1[K];
-        load_words<K>(a.words + wbase + (int64_t)j * K_PAD(K), w0);
-        if (two) load_words<K>(a.words + wbase + (int64_t)(j + nw) * K_PAD(K), w1);
-        else {
+    for (int j = warp; j < count; j += NP * nw) {
+        uint32_t w[NP][K];
 #pragma unroll
-            for (int i = 0; i < K; ++i) w1[i] = w0[i];
+        for (int q = 0; q < NP; ++q) {
+            const int jq = j + q * nw < count ? j + q * nw : j;   // past the unit end: repeat j (not stored)
+            load_words<K>(a.words + wbase + (int64_t)jq * K_PAD(K), w[q]);
         }
-        T x0[K], x1[K];
+        T x[NP][K];
 #pragma unroll
-        for (int i = 0; i < K; ++i) {
-            x0[i] = __ldg(a.xT + (int64_t)(w0[i] & 0x7fffffffu) * a.B + bb);
-            x1[i] = __ldg(a.xT + (int64_t)(w1[i] & 0x7fffffffu) * a.B + bb);
-        }
-        const T wc0 = __ldg(a.w_pos + U.pos_begin + j);
-        const T wc1 = two ? __ldg(a.w_pos + U.pos_begin + j + nw) : (T)0;
-        T g0[K], g1[K];
-        clause_terms<T, K, NCH>(bk, w0, x0, wc0, g0, facc, uacc);
-        if (bv) {
+        for (int q = 0; q < NP; ++q)
 #pragma unroll
-            for (int i = 0; i < K; ++i) __stcs(a.Tb + (sbase + (int64_t)j * K + i) * a.B + b, g0[i]);   // streaming: keep x^T in L2
-        }
-        if (two) {
-            clause_terms<T, K, NCH>(bk, w1, x1, wc1, g1, facc, uacc);
+            for (int i = 0; i < K; ++i) x[q][i] = __ldg(a.xT + (int64_t)(w[q][i] & 0x7fffffffu) * a.B + bb);
+        T wc[NP];
+#pragma unroll
+        for (int q = 0; q < NP; ++q) wc[q] = j + q * nw < count ? __ldg(a.w_pos + U.pos_begin + j + q * nw) : (T)0;
+#pragma unroll
+        for (int q = 0; q < NP; ++q) {
+            if (j + q * nw >= count) break;
+            T g[K];
+            clause_terms<T, K, NCH>(bk, w[q], x[q], wc[q], g, facc, uacc);
             if (bv) {
 #pragma unroll
-                for (int i = 0; i < K; ++i) __stcs(a.Tb + (sbase + (int64_t)(j + nw) * K + i) * a.B + b, g1[i]);
+                for (int i = 0; i < K; ++i) __stcs(a.Tb + (sbase + (int64_t)(j + q * nw) * K + i) * a.B + b, g[i]);   // streaming: keep x^T in L2
             }
         }
     }
