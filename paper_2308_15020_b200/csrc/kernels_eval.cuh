@@ -1034,25 +1034,24 @@ __host__ __device__ constexpr size_t long_smem_bytes() { return (size_t)long_war
 
 template <typename T, int NCH>
 __device__ void global_unit_long_cp(const GlobalArgs<T>& a, const BucketReg<T>& bk, const UnitDev& U, int64_t b, bool bv,
-                                    int j0, T* xs, T* ps, double& facc, int& uacc) {
+                                    int j0, T* xs, T* ps, uint32_t* ws, double& facc, int& uacc) {
     const int k = bk.k;
     const int lane = threadIdx.x & 31;
-    const T* xb = a.xT + (bv ? b : 0);
-    const uint32_t B32 = (uint32_t)a.B;   // plan() checks n B < 2^32
-    const int k0 = min(k, 32);            // literals [0, k0) have their word in wl0, [32, k) in wl1
+    const char* xb = reinterpret_cast<const char*>(a.xT + (bv ? b : 0));
+    const uint32_t rowb = (uint32_t)a.B * (uint32_t)sizeof(T);   // bytes per x^T row (plan(): n B < 2^32)
     for (int j = j0; j < unit_count(U); j += long_warps<T>()) {
         const int64_t pos = (int64_t)U.pos_begin + j;
         const uint32_t* wp = a.words + (int64_t)U.word_begin + (int64_t)j * unit_kp(U);
-        const uint32_t wl0 = lane < k ? __ldg(wp + lane) : 0u;
-        const uint32_t wl1 = lane + 32 < k ? __ldg(wp + lane + 32) : 0u;
         const T wc = __ldg(a.w_pos + pos);
-        __syncwarp();   // the previous constraint's reads of xs / ps are done
+        __syncwarp();   // the previous constraint's reads of ws / xs / ps are done
+        if (lane < k) ws[lane] = __ldg(wp + lane);
+        if (lane + 32 < k) ws[lane + 32] = __ldg(wp + lane + 32);
+        __syncwarp();
+        // every gather in flight at once: 4/8-byte cp.async per literal into this lane's column (broadcast
+        // word reads, one wide multiply-add per address)
 #pragma unroll 4
-        for (int i = 0; i < k0; ++i)
-            cp_async_small<sizeof(T)>(xs + 32 * i, xb + (__shfl_sync(0xffffffffu, wl0, i) & 0x7fffffffu) * B32);
-#pragma unroll 4
-        for (int i = 32; i < k; ++i)
-            cp_async_small<sizeof(T)>(xs + 32 * i, xb + (__shfl_sync(0xffffffffu, wl1, i - 32) & 0x7fffffffu) * B32);
+        for (int i = 0; i < k; ++i)
+            cp_async_small<sizeof(T)>(xs + 32 * i, xb + (size_t)((ws[i] & 0x7fffffffu) * rowb));
         cp_async_commit_wait_all();
         T fe = bk.g0;
         uint32_t t = 0;
@@ -1061,40 +1060,36 @@ __device__ void global_unit_long_cp(const GlobalArgs<T>& a, const BucketReg<T>& 
         for (int c = 0; c < NCH; ++c) {
             const T c0 = bk.c0[c], c1 = bk.c1[c];
             T run = (T)1;
-            // forward: exclusive prefixes to ps (channel 0 also counts the True literals)
-            auto fwd = [&](int i, uint32_t w) {
+            // forward: exclusive prefixes to ps; channel 0 also counts the True literals (x^T holds canonical
+            // zeros, so the sign bit of x is exactly x < 0: tie rule x = 0 -> False)
+#pragma unroll 4
+            for (int i = 0; i < k; ++i) {
+                const uint32_t w = ws[i];
                 const T xv = xs[32 * i];
-                if (c == 0) t += (uint32_t)(xv < (T)0) ^ (w >> 31);
+                if (c == 0) t += lit_true(xv, w);
                 ps[32 * i] = run;
                 run *= fmaT(flip_sign(c1, w), xv, c0);
-            };
-#pragma unroll 4
-            for (int i = 0; i < k0; ++i) fwd(i, __shfl_sync(0xffffffffu, wl0, i));
-#pragma unroll 4
-            for (int i = 32; i < k; ++i) fwd(i, __shfl_sync(0xffffffffu, wl1, i - 32));
+            }
             fe = fmaT(bk.g[c], run, fe);
             T suf = bk.g[c] * wc;
             // backward: term_i = pre_i suf_i s_i c1, written once (channel 0) or accumulated
-            auto bwd = [&](int i, uint32_t w) {
+#pragma unroll 4
+            for (int i = k - 1; i >= 0; --i) {
+                const uint32_t w = ws[i];
                 const T cs = flip_sign(c1, w);
                 const T p = ps[32 * i] * suf;
                 if (bv) {
-                    T* d = dst + (uint32_t)i * B32;
+                    T* d = dst + (size_t)((uint32_t)i * (uint32_t)a.B);
                     if (c == 0) __stcs(d, p * cs);
                     else *d = fmaT(p, cs, *d);
                 }
                 suf *= fmaT(cs, xs[32 * i], c0);
-            };
-#pragma unroll 4
-            for (int i = k - 1; i >= 32; --i) bwd(i, __shfl_sync(0xffffffffu, wl1, i - 32));
-#pragma unroll 4
-            for (int i = k0 - 1; i >= 0; --i) bwd(i, __shfl_sync(0xffffffffu, wl0, i));
+            }
         }
         if (NCH == 0) {
             for (int i = 0; i < k; ++i) {
-                const uint32_t w = __shfl_sync(0xffffffffu, i < 32 ? wl0 : wl1, i & 31);
-                t += (uint32_t)(xs[32 * i] < (T)0) ^ (w >> 31);
-                if (bv) __stcs(dst + (uint32_t)i * B32, (T)0);
+                t += lit_true(xs[32 * i], ws[i]);
+                if (bv) __stcs(dst + (size_t)((uint32_t)i * (uint32_t)a.B), (T)0);
             }
         }
         facc += (double)(wc * fe);
@@ -1114,6 +1109,8 @@ __global__ void __launch_bounds__(32 * long_warps<T>()) fast_global_long_kernel(
     const int chunk = a.chunk_base + blockIdx.y;
     T* xs = reinterpret_cast<T*>(smem_raw) + warp * 2 * kLongKMax * 32 + lane;   // per-lane columns, stride 32
     T* ps = xs + kLongKMax * 32;
+    __shared__ uint32_t wsh[kLongWarps][kLongKMax];                                // the warp's row of words
+    uint32_t* ws = wsh[warp];
     double facc = 0.0;
     int uacc = 0;
     int cur = -1;
@@ -1132,9 +1129,9 @@ __global__ void __launch_bounds__(32 * long_warps<T>()) fast_global_long_kernel(
         }
         const int j0 = ((warp - base) % kLongWarps + kLongWarps) % kLongWarps;   // round-robin across units
         base += unit_count(U);
-        if (nch == 1) global_unit_long_cp<T, 1>(a, bk, U, b, bv, j0, xs, ps, facc, uacc);
-        else if (nch == 2) global_unit_long_cp<T, 2>(a, bk, U, b, bv, j0, xs, ps, facc, uacc);
-        else global_unit_long_cp<T, 0>(a, bk, U, b, bv, j0, xs, ps, facc, uacc);
+        if (nch == 1) global_unit_long_cp<T, 1>(a, bk, U, b, bv, j0, xs, ps, ws, facc, uacc);
+        else if (nch == 2) global_unit_long_cp<T, 2>(a, bk, U, b, bv, j0, xs, ps, ws, facc, uacc);
+        else global_unit_long_cp<T, 0>(a, bk, U, b, bv, j0, xs, ps, ws, facc, uacc);
     }
     fr[warp * 32 + lane] = facc;
     ur[warp * 32 + lane] = uacc;
@@ -1625,7 +1622,7 @@ __global__ void __launch_bounds__(256) transpose_kernel(const T* __restrict__ x,
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
         int64_t v = v0 + ty + 8 * j, b = b0 + tx;
-        if (b < B && v < n) xT[v * B + b] = tile[tx][ty + 8 * j];
+        if (b < B && v < n) xT[v * B + b] = tile[tx][ty + 8 * j] + (T)0;   // + 0: canonical zeros (-0.0 -> +0.0)
     }
 }
 

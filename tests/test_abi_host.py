@@ -154,3 +154,29 @@ def test_tiled_units_are_var_disjoint_classes(maker):
             seen |= set(vs.tolist())
         covered += count
     assert covered == ctx.info["n_fast_cons"]
+
+
+@pytest.mark.parametrize("maker", [lambda: synth.config4_hybrid(0), lambda: synth.random_mixed(n=900, m=700, seed=5, kmax=64)])
+def test_global_units_length_classes(maker):
+    """Global path: units are runs of one bucket in position order covering every fast constraint once, buckets
+    ascend in k so the length classes the kernels split on (k <= 4, 4 < k <= 16, k > 16: the long kernel) are
+    contiguous unit ranges, and a unit holds <= max(1, cap / k) constraints (cap in 32..512 literals)."""
+    inst = maker()
+    ctx = P.Context.from_instance(inst, device=-1, path=2)
+    assert ctx.info["path"] == 2
+    units, order = ctx.layout_units()
+    assert sorted(order.tolist()) == list(range(inst.m))
+    k_of = np.diff(inst.offsets)
+    covered, last_cls, last_k = 0, -1, 0
+    for bucket, count, p0, tiled in units:
+        assert tiled == 0 and p0 == covered and count >= 1
+        ks = {int(k_of[order[p]]) for p in range(p0, p0 + count)}
+        assert len(ks) == 1
+        k = ks.pop()
+        assert count <= max(1, 512 // k)
+        assert k >= last_k
+        cls = 0 if k <= 4 else 1 if k <= 16 else 2
+        assert cls >= last_cls
+        last_cls, last_k = cls, k
+        covered += count
+    assert covered == ctx.info["n_fast_cons"]
