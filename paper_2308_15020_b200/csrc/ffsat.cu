@@ -328,69 +328,37 @@ void search_iterate_direct(ffsat_search* s, int n_iters, cudaStream_t st) {
     s->iters_issued += n_iters;
 }
 
-template <typename T>
-void launch_check_uniform(int k, dim3 grid, size_t tile, const dev::CheckArgs& a, cudaStream_t st) {
-    switch (k) {
-#define FFSAT_CK(K) case K: \
-        CK(cudaFuncSetAttribute(dev::check_uniform_kernel<T, K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tile)); \
-        dev::check_uniform_kernel<T, K><<<grid, 256, tile, st>>>(a); break;
-        FFSAT_CK(1) FFSAT_CK(2) FFSAT_CK(3) FFSAT_CK(4) FFSAT_CK(5) FFSAT_CK(6) FFSAT_CK(7) FFSAT_CK(8)
-        FFSAT_CK(9) FFSAT_CK(10) FFSAT_CK(11) FFSAT_CK(12) FFSAT_CK(13) FFSAT_CK(14) FFSAT_CK(15) FFSAT_CK(16)
-#undef FFSAT_CK
-    default: throw Error(FFSAT_ERR_ARG, "uniform check needs k <= 16");
-    }
-}
-
 void search_check(ffsat_search* s, cudaStream_t st) {
     ffsat_ctx* c = s->ctx;
     const Layout& L = c->Lo;
     CK(cudaMemsetAsync(s->unsat.p, 0, (size_t)s->B * 4, st));
     if (L.m == 0) return;
     CK(cudaMemsetAsync(s->U.p, 0, (size_t)L.m * 4, st));
-    const size_t es = c->esize;
-    const size_t tile = (size_t)L.n * 33 * es;
-    const bool smem = tile <= 200 * 1024;
-    dev::CheckArgs a{};
-    a.B = s->B; a.n = L.n; a.m = L.m; a.off = c->chk_off.as<int64_t>();
+    // sign words S[pt][v] (32 points per word), then one thread per (constraint, 32 points)
+    const int64_t PT = (s->B + 31) / 32;
+    s->xT.ensure(std::max<size_t>(16, (size_t)PT * L.n * 4));
+    uint32_t* S = s->xT.as<uint32_t>();
+    dim3 pg(blocks_for(L.n, 8 * 4), (unsigned)PT);
+    if (L.precision == 64) dev::signpack_kernel<double><<<pg, 256, 0, st>>>(s->X.as<double>(), S, s->B, L.n);
+    else dev::signpack_kernel<float><<<pg, 256, 0, st>>>(s->X.as<float>(), S, s->B, L.n);
+    dev::CheckBitsArgs a{};
+    a.S = S; a.B = s->B; a.n = L.n; a.m = L.m; a.off = c->chk_off.as<int64_t>();
     a.words = c->chk_words.as<uint32_t>(); a.rule = c->chk_rule.as<int32_t>();
     a.U = s->U.as<int32_t>(); a.unsat = s->unsat.as<int32_t>();
-    const int64_t PT = (s->B + 31) / 32;
-    const int cps = smem ? std::max(1, (int)std::min<size_t>(8, (228 * 1024) / (tile + 2048))) : 8;
-    const int64_t want = std::max<int64_t>(1, (int64_t)c->num_sm * cps / PT);   // one wave: every CTA re-loads the x tile
-    const int64_t chunks = std::min<int64_t>(std::min<int64_t>(want, 65535), (L.m + 7) / 8);
+    // chunks: about one wave of CTAs, at least 1024 literals each (each CTA stages the tile's sign words)
+    const int64_t want = std::max<int64_t>(1, (int64_t)c->num_sm * 8 / PT);
+    const int64_t by_work = std::max<int64_t>(1, L.L / 1024);
+    const int64_t chunks = std::min<int64_t>(std::min<int64_t>(want, by_work), std::min<int64_t>(65535, (L.m + 255) / 256));
     a.cons_per_cta = (L.m + chunks - 1) / chunks;
     dim3 grid((unsigned)PT, (unsigned)((L.m + a.cons_per_cta - 1) / a.cons_per_cta));
-    // uniform k <= 16: the specialised check (offsets c k, sign-bit counts)
-    const int ku = (int)(L.m > 0 ? L.L / L.m : 0);
-    const bool uniform = smem && ku >= 1 && ku <= 16 && (int64_t)ku * L.m == L.L && L.L < INT32_MAX && L.max_k == ku;
-    if (uniform) {
-        a.X = s->X.p;
-        if (L.precision == 64) launch_check_uniform<double>(ku, grid, tile, a, st);
-        else launch_check_uniform<float>(ku, grid, tile, a, st);
-        s->ctx->launches += 1;
-    } else if (smem) {
-        a.X = s->X.p;
-        if (L.precision == 64) {
-            CK(cudaFuncSetAttribute(dev::check_kernel<double, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tile));
-            dev::check_kernel<double, true><<<grid, 256, tile, st>>>(a);
-        } else {
-            CK(cudaFuncSetAttribute(dev::check_kernel<float, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tile));
-            dev::check_kernel<float, true><<<grid, 256, tile, st>>>(a);
-        }
-        s->ctx->launches += 1;
+    const size_t tile = (size_t)L.n * 4;
+    if (tile <= 96 * 1024) {
+        if (tile > 48 * 1024) CK(cudaFuncSetAttribute(dev::check_bits_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tile));
+        dev::check_bits_kernel<true><<<grid, 256, tile, st>>>(a);
     } else {
-        s->xT.ensure((size_t)L.n * s->B * es);
-        dim3 tg(blocks_for(L.n, 32), blocks_for(s->B, 32)), tb(32, 8);
-        a.X = s->xT.p;
-        if (L.precision == 64) {
-            dev::transpose_search_kernel<double><<<tg, tb, 0, st>>>(s->X.as<double>(), s->xT.as<double>(), s->B, L.n);
-            dev::check_kernel<double, false><<<grid, 256, 0, st>>>(a);
-        } else {
-            dev::transpose_search_kernel<float><<<tg, tb, 0, st>>>(s->X.as<float>(), s->xT.as<float>(), s->B, L.n);
-            dev::check_kernel<float, false><<<grid, 256, 0, st>>>(a);
-        }
-        s->ctx->launches += 2;
+        dev::check_bits_kernel<false><<<grid, 256, 0, st>>>(a);
     }
+    s->ctx->launches += 2;
     CK(cudaGetLastError());
 }
 

@@ -5,8 +5,9 @@
 //   pgd_step_kernel        Alg. 4: Armijo accept/reject of the trial point just evaluated,
 //                          eta update, convergence (eta < eta_min), solved-trial capture, then
 //                          the next trial x' = clip(x - eta g, -1, 1) and <g, x' - x>; one CTA per point.
-//   check_kernel           Alg. 1 line 5 / Thm. 4: exact integer check of sgn(x) per
-//                          (constraint, point): unsat[b] and U[c].
+//   signpack_kernel,       Alg. 1 line 5 / Thm. 4: exact integer check of sgn(x) per
+//   check_bits_kernel      (constraint, point) on sign words of 32 points: unsat[b] and U[c].
+//                          Integer atomics only: totals are exact and order-independent.
 //   erwa_kernel            Prop. 3: w <- (1-alpha) w + alpha U/max U (skipped if max U = 0).
 //   rephase_kernel         O / F / R phases in the policy cycle, offset by global point.
 #pragma once
@@ -142,177 +143,147 @@ __global__ void __launch_bounds__(256) pgd_step_kernel(PgdArgs a) {
     if (threadIdx.x == 0) a.dot[b] = red[0];
 }
 
-// sgn(x) check (Alg. 1 line 5): exact integer count t of True literals per (constraint, point).
-// CTA = 32 points (lane = point) x a contiguous range of constraints (warp = constraint).  The point
-// values come from a shared-memory tile [n][33] (SMEM = true, small n) or from the transposed copy
-// xT [n][B] (coalesced 128-byte rows, large n).  U[c] += #points of this tile falsifying c (warp ballot +
-// popc, one integer atomic per warp-constraint); unsat[b] += this CTA's count (one integer atomic per
-// point).  Integer atomics: the totals are exact and order-independent.  U and unsat are zeroed before.
-struct CheckArgs {
-    const void* X;      // [B][n] (SMEM) or xT [n][B]
+// ---- bit-packed exact check (A9; Thm. 4, Alg. 1 line 5 P:225): the signs of 32 points of one variable
+//      are one 32-bit word, so one thread checks one constraint for 32 points with one word op per literal.
+// S[pt][v] bit b = 1 iff x[32 pt + b][v] < 0 (the literal "v" is True); points past B have bit 0 and are masked.
+template <typename T>
+__global__ void __launch_bounds__(256) signpack_kernel(const T* __restrict__ X, uint32_t* __restrict__ S, int64_t B, int32_t n) {
+    const int lane = threadIdx.x & 31;
+    const int64_t pt = blockIdx.y;
+    const int64_t b = pt * 32 + lane;
+    const bool bv = b < B;
+    // warp w of block x covers 4 consecutive variables (loads all in flight; a lane's sectors are shared)
+    const int64_t v0 = ((int64_t)blockIdx.x * 8 + (threadIdx.x >> 5)) * 4;
+    T xv[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) xv[j] = (bv && v0 + j < n) ? X[b * n + v0 + j] : (T)0;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        const uint32_t m = __ballot_sync(0xffffffffu, xv[j] < (T)0);   // tie rule: x = 0 (either sign) is False
+        if (lane == j && v0 + j < n) S[pt * n + v0 + j] = m;
+    }
+}
+
+struct CheckBitsArgs {
+    const uint32_t* S;        // [PT][n] sign words
     int64_t B;
     int32_t n;
     int64_t m;
     int64_t cons_per_cta;
     const int64_t* off;       // [m + 1] position-order literal offsets into words
     const uint32_t* words;    // var | neg << 31
-    const int32_t* rule;      // [m][3]
+    const int32_t* rule;      // [m][3] tmin, tmax, parity (1 odd, 2 even)
     int32_t* U;               // [m]
     int32_t* unsat;           // [B]
 };
 
-__device__ __forceinline__ uint32_t sign_xor(float xv, uint32_t w) { return (__float_as_uint(xv) ^ w) >> 31; }
-__device__ __forceinline__ uint32_t sign_xor(double xv, uint32_t w) { return ((uint32_t)__double2hiint(xv) ^ w) >> 31; }
-
-template <typename T, bool SMEM>
-__global__ void __launch_bounds__(256) check_kernel(CheckArgs a) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    __shared__ int ucnt[8][32];
-    const T* X = reinterpret_cast<const T*>(a.X);
-    T* xs = reinterpret_cast<T*>(smem_raw);
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int64_t b0 = (int64_t)blockIdx.x * 32, b = b0 + lane;
-    const bool bv = b < a.B;
-    if (SMEM) {   // x tile, 8 independent loads in flight per thread
-        const int tot = 32 * a.n;
-        for (int base = 0; base < tot; base += 8 * 256) {
-            T v8[8];
-#pragma unroll
-            for (int q = 0; q < 8; ++q) {
-                const int idx = base + q * 256 + (int)threadIdx.x;
-                const int r = idx / a.n, v = idx - r * a.n;
-                v8[q] = (idx < tot && b0 + r < a.B) ? __ldg(X + (b0 + r) * a.n + v) : (T)0;
-            }
-#pragma unroll
-            for (int q = 0; q < 8; ++q) {
-                const int idx = base + q * 256 + (int)threadIdx.x;
-                if (idx < tot) {
-                    const int r = idx / a.n, v = idx - r * a.n;
-                    xs[v * 33 + r] = v8[q];
-                }
-            }
+// Bit-sliced comparison of the per-point counts (planes p[0..P), LSB first) with a constant: gt / eq masks.
+__device__ __forceinline__ void bits_cmp(const uint32_t* p, int P, int c, uint32_t& gt, uint32_t& eq) {
+    gt = 0u;
+    eq = 0xffffffffu;
+    if (c >> P) { eq = 0u; return; }   // c >= 2^P > every count
+    for (int j = P - 1; j >= 0; --j) {
+        if ((c >> j) & 1) eq &= p[j];
+        else {
+            gt |= eq & p[j];
+            eq &= ~p[j];
         }
+    }
+}
+
+// grid (point tiles, constraint chunks), 256 threads; SMEM: the tile's sign words staged in shared memory
+// (n words), else read through the read-only path.  Thread = one constraint for 32 points: literal truth masks
+// L = S[v] ^ (negated ? ~0 : 0); OR / AND / parity rules reduce them with one op each, other rules count them in
+// bit-sliced planes.  U_c: popc of the unsat mask (one integer atomic per constraint with unsat points);
+// unsat[b]: the warp transposes its 32 unsat masks with ballots, lane b keeps point b's count.
+template <bool SMEM>
+__global__ void __launch_bounds__(256) check_bits_kernel(CheckBitsArgs a) {
+    extern __shared__ __align__(16) uint32_t sgn[];
+    __shared__ int ucnt[8][32];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t pt = blockIdx.x, b0 = pt * 32;
+    const uint32_t vm = a.B - b0 >= 32 ? 0xffffffffu : ((1u << (a.B - b0)) - 1u);
+    const uint32_t* S = a.S + pt * a.n;
+    if (SMEM) {
+        for (int v = threadIdx.x; v < a.n; v += 256) sgn[v] = S[v];
         __syncthreads();
+        S = sgn;
     }
     const int64_t c0 = (int64_t)blockIdx.y * a.cons_per_cta;
     const int64_t c1 = min(a.m, c0 + a.cons_per_cta);
-    int mine = 0;
-    for (int64_t c = c0 + warp; c < c1; c += 8) {
-        const int64_t lo = a.off[c], hi = a.off[c + 1];
-        int t = 0;
-        int64_t i = lo;
-        for (; i + 4 <= hi; i += 4) {           // four literals' loads in flight
-            uint32_t w[4];
-            T xv[4];
-#pragma unroll
-            for (int q = 0; q < 4; ++q) w[q] = __ldg(a.words + i + q);
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                const uint32_t v = w[q] & 0x7fffffffu;
-                xv[q] = SMEM ? xs[v * 33 + lane] : (bv ? X[(int64_t)v * a.B + b] : (T)0);
-            }
-#pragma unroll
-            for (int q = 0; q < 4; ++q) t += (int)((xv[q] < (T)0) != ((int)w[q] < 0));
-        }
-        for (; i < hi; ++i) {
-            const uint32_t w = __ldg(a.words + i);
-            const uint32_t v = w & 0x7fffffffu;
-            const T xv = SMEM ? xs[v * 33 + lane] : (bv ? X[(int64_t)v * a.B + b] : (T)0);
-            t += (int)((xv < (T)0) != ((int)w < 0));
-        }
-        const bool uns = bv && !rule_sat(t, a.rule[3 * c], a.rule[3 * c + 1], a.rule[3 * c + 2]);
-        mine += uns ? 1 : 0;
-        const int cnt = __popc(__ballot_sync(0xffffffffu, uns));
-        if (lane == 0 && cnt) atomicAdd(a.U + c, cnt);
-    }
-    ucnt[warp][lane] = mine;
-    __syncthreads();
-    if (warp == 0 && bv) {
-        int tot = 0;
-        for (int w = 0; w < 8; ++w) tot += ucnt[w][lane];
-        if (tot) atomicAdd(a.unsat + b, tot);
-    }
-}
-
-// Same check when every constraint has the same length K <= 16 and n fits the smem tile (the uniform k-SAT
-// case): CSR offsets are c K, the K literal words are read as uniform loads, and the True-literal count uses
-// the sign bit of the (canonical-zero) tile value: one LDS, one LOP3 and one LEA.HI per literal.
-template <typename T, int K>
-__global__ void __launch_bounds__(256) check_uniform_kernel(CheckArgs a) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    __shared__ int ucnt[8][32];
-    const T* X = reinterpret_cast<const T*>(a.X);
-    T* xs = reinterpret_cast<T*>(smem_raw);
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int64_t b0 = (int64_t)blockIdx.x * 32, b = b0 + lane;
-    const bool bv = b < a.B;
-    {
-        const int tot = 32 * a.n;
-        for (int base = 0; base < tot; base += 8 * 256) {
-            T v8[8];
-#pragma unroll
-            for (int q = 0; q < 8; ++q) {
-                const int idx = base + q * 256 + (int)threadIdx.x;
-                const int r = idx / a.n, v = idx - r * a.n;
-                v8[q] = (idx < tot && b0 + r < a.B) ? __ldg(X + (b0 + r) * a.n + v) : (T)0;
-            }
-#pragma unroll
-            for (int q = 0; q < 8; ++q) {
-                const int idx = base + q * 256 + (int)threadIdx.x;
-                if (idx < tot) {
-                    const int r = idx / a.n, v = idx - r * a.n;
-                    xs[v * 33 + r] = v8[q] + (T)0;   // canonical zero: the sign bit is exactly x < 0
+    int mine = 0;   // lane b: unsat constraints of point b seen by this warp
+    for (int64_t cb = c0 + warp * 32; cb < c1; cb += 256) {
+        const int64_t c = cb + lane;
+        uint32_t uns = 0u;
+        if (c < c1) {
+            const int64_t lo = __ldg(a.off + c), hi = __ldg(a.off + c + 1);
+            const int k = (int)(hi - lo);
+            const int tmin = __ldg(a.rule + 3 * c), tmax = __ldg(a.rule + 3 * c + 1), par = __ldg(a.rule + 3 * c + 2);
+            uint32_t sat;
+            if (par == 0 && tmin == 1 && tmax >= k) {            // OR: some literal True
+                sat = 0u;
+                for (int64_t i = lo; i < hi; ++i) {
+                    const uint32_t w = __ldg(a.words + i);
+                    sat |= (SMEM ? S[w & 0x7fffffffu] : __ldg(S + (w & 0x7fffffffu))) ^ (uint32_t)((int)w >> 31);
                 }
+            } else if (par == 0 && tmin >= k && tmax >= k) {     // AND: every literal True
+                sat = 0xffffffffu;
+                for (int64_t i = lo; i < hi; ++i) {
+                    const uint32_t w = __ldg(a.words + i);
+                    sat &= (SMEM ? S[w & 0x7fffffffu] : __ldg(S + (w & 0x7fffffffu))) ^ (uint32_t)((int)w >> 31);
+                }
+                if (tmin > k) sat = 0u;
+            } else if (par != 0 && tmin <= 0 && tmax >= k) {     // XOR / XNOR: parity of the True literals
+                uint32_t x = 0u;
+                for (int64_t i = lo; i < hi; ++i) {
+                    const uint32_t w = __ldg(a.words + i);
+                    x ^= (SMEM ? S[w & 0x7fffffffu] : __ldg(S + (w & 0x7fffffffu))) ^ (uint32_t)((int)w >> 31);
+                }
+                sat = par == 1 ? x : ~x;
+            } else {                                             // counting rules: bit-sliced planes
+                uint32_t p[13];
+                int P = 1;
+                while ((1 << P) <= k) ++P;                       // k <= 4096 -> P <= 13
+#pragma unroll
+                for (int j = 0; j < 13; ++j) p[j] = 0u;
+                for (int64_t i = lo; i < hi; ++i) {
+                    const uint32_t w = __ldg(a.words + i);
+                    uint32_t carry = (SMEM ? S[w & 0x7fffffffu] : __ldg(S + (w & 0x7fffffffu))) ^ (uint32_t)((int)w >> 31);
+#pragma unroll
+                    for (int j = 0; j < 13; ++j) {   // ripple-carry add of one bit per point
+                        if (carry == 0u) break;
+                        const uint32_t t = p[j] & carry;
+                        p[j] ^= carry;
+                        carry = t;
+                    }
+                }
+                uint32_t gtn, eqn, gtx, eqx;
+                bits_cmp(p, P, tmin, gtn, eqn);
+                bits_cmp(p, P, tmax, gtx, eqx);
+                sat = (gtn | eqn) & ~gtx;
+                if (par == 1) sat &= p[0];
+                if (par == 2) sat &= ~p[0];
             }
+            uns = ~sat & vm;
+            const int cnt = __popc(uns);
+            if (cnt) atomicAdd(a.U + c, cnt);
         }
-        __syncthreads();
-    }
-    const int c0 = (int)((int64_t)blockIdx.y * a.cons_per_cta);
-    const int c1 = (int)min(a.m, (int64_t)c0 + a.cons_per_cta);
-    const T* xl = xs + lane;
-    int mine = 0;
-    for (int c = c0 + warp; c < c1; c += 8) {
-        uint32_t w[K];
-#pragma unroll
-        for (int i = 0; i < K; ++i) w[i] = __ldg(a.words + c * K + i);
-        uint32_t t = 0;
-#pragma unroll
-        for (int i = 0; i < K; ++i) {
-            const T xv = xl[(w[i] & 0x7fffffffu) * 33];
-            t += sign_xor(xv, w[i]);
+        // transpose: point b's count over this warp's 32 constraints = popc of the ballot of bit b
+#pragma unroll 8
+        for (int bb = 0; bb < 32; ++bb) {
+            const int cnt = __popc(__ballot_sync(0xffffffffu, (uns >> bb) & 1u));
+            if (lane == bb) mine += cnt;
         }
-        const bool uns = bv && !rule_sat((int)t, __ldg(a.rule + 3 * c), __ldg(a.rule + 3 * c + 1), __ldg(a.rule + 3 * c + 2));
-        mine += uns ? 1 : 0;
-        const int cnt = __popc(__ballot_sync(0xffffffffu, uns));
-        if (lane == 0 && cnt) atomicAdd(a.U + c, cnt);
     }
     ucnt[warp][lane] = mine;
     __syncthreads();
-    if (warp == 0 && bv) {
+    if (warp == 0 && b0 + lane < a.B) {
         int tot = 0;
         for (int w = 0; w < 8; ++w) tot += ucnt[w][lane];
-        if (tot) atomicAdd(a.unsat + b, tot);
+        if (tot) atomicAdd(a.unsat + b0 + lane, tot);
     }
 }
 
-// X [B][n] -> xT [n][B] for the large-n check (32 x 32 tiles through smem)
-template <typename T>
-__global__ void __launch_bounds__(256) transpose_search_kernel(const T* __restrict__ x, T* __restrict__ xT, int64_t B, int32_t n) {
-    __shared__ T tile[32][33];
-    const int tx = threadIdx.x, ty = threadIdx.y;
-    const int64_t v0 = (int64_t)blockIdx.x * 32, b0 = (int64_t)blockIdx.y * 32;
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-        const int64_t bb = b0 + ty + 8 * j, v = v0 + tx;
-        if (bb < B && v < n) tile[ty + 8 * j][tx] = x[bb * n + v];
-    }
-    __syncthreads();
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-        const int64_t v = v0 + ty + 8 * j, bb = b0 + tx;
-        if (bb < B && v < n) xT[v * B + bb] = tile[tx][ty + 8 * j];
-    }
-}
 
 // ERWA (single block): maxU, then w = (1 - alpha) w + alpha U / maxU
 template <typename T>

@@ -448,3 +448,28 @@ def test_maxsat_mode_planted_maxcut_tiny():
         assert best >= fw.min() - 1e-12
         hits += abs(best - fw.min()) < 1e-9
     assert hits >= 9
+
+
+@pytest.mark.parametrize("case", ["mixed", "long_card", "large_n"])
+def test_bit_packed_check_all_rules(case):
+    """The round-end check (sign words of 32 points, OR / AND / parity reductions, bit-sliced counts for the
+    other rules): unsat[b] bit-exact and U_c equal as multisets against the oracle's exact check, on a ragged
+    batch with tie points (x = +-0 is False); large n reads the sign words without the shared tile."""
+    if case == "mixed":
+        inst = synth.random_mixed(n=150, m=900, seed=21, kmax=64)
+    elif case == "long_card":
+        inst = synth.config3(0, n=3000, m3=300, n_card=6, kmin=100, kmax=900)
+    else:
+        inst = synth.random_mixed(n=40000, m=3000, seed=22, kmax=40)
+    ctx = P.Context.from_instance(inst, device=0)
+    B = 77
+    s = ctx.search(B, seed=5)
+    X = synth.points("Z", B, inst.n, 33, np.float64 if ctx.info["precision"] == 64 else np.float32)
+    s.set_x(torch.from_numpy(X).cuda())
+    s.check()
+    torch.cuda.synchronize()
+    T = s.tensors()
+    Fo = oracle_of(inst)
+    cnt, _, U = cdp.check(Fo, X.astype(np.float64), want_U=True)
+    assert np.array_equal(T["unsat"].cpu().numpy(), cnt)
+    assert np.array_equal(np.sort(T["U"].cpu().numpy()), np.sort(U))
