@@ -190,22 +190,29 @@ void eval_device_t(ffsat_ctx* c, const T* x, int64_t B, double* f, T* grad, int3
     if (profiled) launch_sym_all();
     join_sym();
     mark(2);
+    dev::ReduceFArgs rf{};
+    rf.B = B; rf.n_parts = L.n_fast > 0 ? c->n_chunks : 0; rf.n_sym = L.n_sym;
+    rf.fpart = c->fpart.as<double>(); rf.upart = c->upart.as<int32_t>(); rf.fsym = c->fsym.as<double>();
+    rf.usym = c->usym.as<int32_t>(); rf.f = f; rf.unsat = unsat;
+    // with a gradient the f / unsat reduction rides in the gradient reduction (variable tile 0); the profiled
+    // path keeps them apart so the phases can be timed separately
+    const bool fuse = grad && L.n > 0 && !profiled;
     if (grad) {
         c->launches += 1;
         dev::ReduceArgs<T> r{};
         r.B = B; r.n = L.n; r.n_chunks = L.path == 1 ? c->n_chunks : 0; r.P = c->P.as<T>(); r.Tb = c->Tb.as<T>();
         r.occ_off = c->occ_off.as<int64_t>(); r.occ_slot = c->occ_slot.as<int32_t>(); r.grad = grad;
+        r.fuse_f = fuse;
+        r.rf = rf;
         dim3 grid(blocks_for(L.n, 8), blocks_for(B, 32)), blk(32, 8);
         dev::reduce_grad_kernel<T><<<grid, blk, 0, st>>>(r);
     }
     mark(3);
-    c->launches += 1;
-    dev::ReduceFArgs rf{};
-    rf.B = B; rf.n_parts = L.n_fast > 0 ? c->n_chunks : 0; rf.n_sym = L.n_sym;
-    rf.fpart = c->fpart.as<double>(); rf.upart = c->upart.as<int32_t>(); rf.fsym = c->fsym.as<double>();
-    rf.usym = c->usym.as<int32_t>(); rf.f = f; rf.unsat = unsat;
-    if (B <= 32 * 64) dev::reduce_f_kernel<32><<<blocks_for(B, 32), 1024, 0, st>>>(rf);
-    else dev::reduce_f_kernel<8><<<blocks_for(B, 32), 256, 0, st>>>(rf);
+    if (!fuse) {
+        c->launches += 1;
+        if (B <= 32 * 64) dev::reduce_f_kernel<32><<<blocks_for(B, 32), 1024, 0, st>>>(rf);
+        else dev::reduce_f_kernel<8><<<blocks_for(B, 32), 256, 0, st>>>(rf);
+    }
     CK(cudaGetLastError());
     mark(4);
 }

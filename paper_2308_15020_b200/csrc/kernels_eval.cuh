@@ -1502,6 +1502,18 @@ __global__ void __launch_bounds__(256) sym_lane_kernel(SymArgs<T> a, int64_t s_b
 
 // ------------------------------------------------------------------------------------------------
 // A7 reductions.
+struct ReduceFArgs {
+    int64_t B;
+    int32_t n_parts;             // fast partial rows
+    int64_t n_sym;
+    const double* fpart;         // [n_parts][B]
+    const int32_t* upart;
+    const double* fsym;          // [n_sym][B]
+    const int32_t* usym;
+    double* f;                   // [B]
+    int32_t* unsat;              // [B] or null
+};
+
 template <typename T>
 struct ReduceArgs {
     int64_t B;
@@ -1512,6 +1524,8 @@ struct ReduceArgs {
     const int64_t* occ_off;      // [n + 1]
     const int32_t* occ_slot;     // variable v's T rows, ascending: occ_slot[occ_off[v] .. occ_off[v + 1])
     T* grad;                     // [B][n]
+    bool fuse_f;                 // the CTAs of variable tile 0 also reduce f / unsat (rf) for their 32 points
+    ReduceFArgs rf;
 };
 
 // block (32, 8): 32 points x 8 variables, one (variable, point) sum per thread: the chunk partials in
@@ -1524,6 +1538,35 @@ __global__ void __launch_bounds__(256) reduce_grad_kernel(ReduceArgs<T> a) {
     const int tx = threadIdx.x, ty = threadIdx.y;
     const int64_t b0 = (int64_t)blockIdx.y * 32, v0 = (int64_t)blockIdx.x * 8;   // grid.x over variables (n may exceed 65535 tiles)
     const int64_t b = b0 + tx, v = v0 + ty;
+    if (a.fuse_f && blockIdx.x == 0) {   // f / unsat of points b0 .. b0 + 31: warp ty sums rows ty, ty + 8, ... then in order
+        __shared__ double sf[8][32];
+        __shared__ int su[8][32];
+        double f = 0.0;
+        int u = 0;
+        if (b < a.B) {
+            for (int c = ty; c < a.rf.n_parts; c += 8) {
+                f += a.rf.fpart[(int64_t)c * a.B + b];
+                u += a.rf.upart[(int64_t)c * a.B + b];
+            }
+            for (int64_t s = ty; s < a.rf.n_sym; s += 8) {
+                f += a.rf.fsym[s * a.B + b];
+                u += a.rf.usym[s * a.B + b];
+            }
+        }
+        sf[ty][tx] = f;
+        su[ty][tx] = u;
+        __syncthreads();
+        if (ty == 0 && b < a.B) {
+            double ft = 0.0;
+            int ut = 0;
+            for (int j = 0; j < 8; ++j) {
+                ft += sf[j][tx];
+                ut += su[j][tx];
+            }
+            a.rf.f[b] = ft;
+            if (a.rf.unsat) a.rf.unsat[b] = ut;
+        }
+    }
     double acc = 0.0;
     if (v < a.n && b < a.B) {
         const int64_t stride = (int64_t)a.n * a.B;
@@ -1559,17 +1602,6 @@ __global__ void __launch_bounds__(256) reduce_grad_kernel(ReduceArgs<T> a) {
     if (bb < a.B && vv < a.n) a.grad[bb * a.n + vv] = tile[vl][pl];
 }
 
-struct ReduceFArgs {
-    int64_t B;
-    int32_t n_parts;             // fast partial rows
-    int64_t n_sym;
-    const double* fpart;         // [n_parts][B]
-    const int32_t* upart;
-    const double* fsym;          // [n_sym][B]
-    const int32_t* usym;
-    double* f;                   // [B]
-    int32_t* unsat;              // [B] or null
-};
 
 // one CTA (32 NWF threads) per 32 points: lane = point, warp w sums rows w, w + NWF, ... in ascending
 // order, then the NWF warp sums are added in warp order -- a fixed summation order for a given launch
