@@ -234,10 +234,18 @@ def main():
     import torch.distributed as dist
     import paper_2308_15020_b200 as P
 
+    # one GPU per rank; FFSAT_DIST_BACKEND=gloo lets several ranks share a device (host-path smoke test of the
+    # multi-rank step on a single-GPU box; NCCL refuses duplicate devices)
+    backend = os.environ.get("FFSAT_DIST_BACKEND", "nccl")
+    if backend != "nccl":
+        local = local % torch.cuda.device_count()
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
     inst = cfg["make"]()
     B = cfg["B"]
     from paper_2308_15020_b200 import dist as D
