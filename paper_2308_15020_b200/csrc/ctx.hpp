@@ -89,6 +89,11 @@ struct ffsat_ctx {
     cudaEvent_t ev[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
     // side streams for the concurrent root-path classes (fork / join through events, graph-capturable)
     cudaStream_t side[FFSAT_SIDE_STREAMS] = {};
+    // host-buffer evaluation: copy streams (H2D, D2H) and per-chunk events of the pipelined staging
+    cudaStream_t copy_h2d = nullptr, copy_d2h = nullptr;
+    std::vector<cudaEvent_t> ev_h2d, ev_done;
+    ffsat::DBuf nf_flag;
+    int32_t* nf_host = nullptr;   // pinned
     cudaEvent_t ev_fork = nullptr, ev_join[FFSAT_SIDE_STREAMS] = {};
     bool pending_join[FFSAT_SIDE_STREAMS] = {};
     void ensure_side_streams() {
@@ -107,6 +112,11 @@ struct ffsat_ctx {
             if (ev_join[i]) cudaEventDestroy(ev_join[i]);
         }
         if (ev_fork) cudaEventDestroy(ev_fork);
+        if (copy_h2d) cudaStreamDestroy(copy_h2d);
+        if (copy_d2h) cudaStreamDestroy(copy_d2h);
+        for (cudaEvent_t e : ev_h2d) cudaEventDestroy(e);
+        for (cudaEvent_t e : ev_done) cudaEventDestroy(e);
+        if (nf_host) cudaFreeHost(nf_host);
     }
 };
 

@@ -505,30 +505,77 @@ ffsat_status ffsat_eval(ffsat_ctx* c, const void* x, int64_t B, int32_t on_devic
     if (B < 0 || (B > 0 && (!x || !f_out))) throw Error(FFSAT_ERR_ARG, "bad eval arguments");
     if (B > INT32_MAX / 2) throw Error(FFSAT_ERR_ARG, "batch too large");
     cudaStream_t st = S(stream);
-    const size_t es = c->esize, Bn = (size_t)B * c->Lo.n;
+    const size_t es = c->esize;
     if (on_device) {
         eval_device(c, x, B, f_out, grad_out, unsat_out, st);
         return FFSAT_OK;
     }
-    // host buffers: validate, stage, compute, copy back
-    if (es == 8) {
-        const double* xd = (const double*)x;
-        for (size_t i = 0; i < Bn; ++i) if (!std::isfinite(xd[i])) throw Error(FFSAT_ERR_NONFINITE, "non-finite point coordinate");
-    } else {
-        const float* xf = (const float*)x;
-        for (size_t i = 0; i < Bn; ++i) if (!std::isfinite(xf[i])) throw Error(FFSAT_ERR_NONFINITE, "non-finite point coordinate");
+    // host buffers: stage, compute, copy back, pipelined in equal chunks of Bc points (the last one padded with
+    // zero points) so the H2D copy of chunk i + 1 and the D2H copy of chunk i - 1 overlap the evaluation of chunk
+    // i (two copy engines); non-finite coordinates are flagged by a device kernel on the staged copy.
+    // 2 chunks, up to 4 for batches over ~2 MB (smaller chunks multiply the tiled path's partial-tile traffic)
+    const size_t xbytes = (size_t)B * (size_t)c->Lo.n * es;
+    const int64_t nchunk = B < 512 ? 1 : xbytes >= (4u << 20) ? 4 : xbytes >= (2u << 20) ? 3 : 2;
+    const int64_t Bc = nchunk == 1 ? B : ((B + nchunk - 1) / nchunk + 63) / 64 * 64;
+    const int64_t nck = Bc > 0 ? (B + Bc - 1) / Bc : 0;
+    const size_t n = (size_t)c->Lo.n;
+    c->x_stage.ensure(std::max<size_t>(16, (size_t)(nck * Bc) * n * es));
+    c->f_stage.ensure(std::max<size_t>(16, (size_t)(nck * Bc) * 8));
+    c->u_stage.ensure(std::max<size_t>(16, (size_t)(nck * Bc) * 4));
+    if (grad_out) c->g_stage.ensure(std::max<size_t>(16, (size_t)(nck * Bc) * n * es));
+    c->nf_flag.ensure(16);
+    if (!c->copy_h2d) {
+        CK(cudaStreamCreateWithFlags(&c->copy_h2d, cudaStreamNonBlocking));
+        CK(cudaStreamCreateWithFlags(&c->copy_d2h, cudaStreamNonBlocking));
+        CK(cudaMallocHost(&c->nf_host, 16));
     }
-    c->x_stage.ensure(std::max<size_t>(16, Bn * es));
-    c->f_stage.ensure(std::max<size_t>(16, (size_t)B * 8));
-    c->u_stage.ensure(std::max<size_t>(16, (size_t)B * 4));
-    if (grad_out) c->g_stage.ensure(std::max<size_t>(16, Bn * es));
-    if (Bn) CK(cudaMemcpyAsync(c->x_stage.p, x, Bn * es, cudaMemcpyHostToDevice, st));
-    eval_device(c, c->x_stage.p, B, c->f_stage.as<double>(), grad_out ? c->g_stage.p : nullptr,
-                unsat_out ? c->u_stage.as<int32_t>() : nullptr, st);
-    if (B) CK(cudaMemcpyAsync(f_out, c->f_stage.p, (size_t)B * 8, cudaMemcpyDeviceToHost, st));
-    if (grad_out && Bn) CK(cudaMemcpyAsync(grad_out, c->g_stage.p, Bn * es, cudaMemcpyDeviceToHost, st));
-    if (unsat_out && B) CK(cudaMemcpyAsync(unsat_out, c->u_stage.p, (size_t)B * 4, cudaMemcpyDeviceToHost, st));
+    while ((int64_t)c->ev_h2d.size() < nck + 1) {
+        cudaEvent_t e1, e2;
+        CK(cudaEventCreateWithFlags(&e1, cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&e2, cudaEventDisableTiming));
+        c->ev_h2d.push_back(e1);
+        c->ev_done.push_back(e2);
+    }
+    char* xs = c->x_stage.as<char>();
+    char* gs = c->g_stage.as<char>();
+    // the compute stream's prior work is ordered before the copies (ev_done[nck] marks it)
+    CK(cudaEventRecord(c->ev_done[(size_t)nck], st));
+    CK(cudaStreamWaitEvent(c->copy_h2d, c->ev_done[(size_t)nck], 0));
+    CK(cudaMemsetAsync(c->nf_flag.p, 0, 4, c->copy_h2d));
+    if (nck * Bc > B) CK(cudaMemsetAsync(xs + (size_t)B * n * es, 0, (size_t)(nck * Bc - B) * n * es, c->copy_h2d));
+    for (int64_t i = 0; i < nck; ++i) {
+        const int64_t r0 = i * Bc, r1 = std::min(B, r0 + Bc);
+        if (r1 > r0 && n) CK(cudaMemcpyAsync(xs + (size_t)r0 * n * es, (const char*)x + (size_t)r0 * n * es, (size_t)(r1 - r0) * n * es,
+                                             cudaMemcpyHostToDevice, c->copy_h2d));
+        CK(cudaEventRecord(c->ev_h2d[(size_t)i], c->copy_h2d));
+    }
+    for (int64_t i = 0; i < nck; ++i) {
+        const int64_t r0 = i * Bc, r1 = std::min(B, r0 + Bc);
+        CK(cudaStreamWaitEvent(st, c->ev_h2d[(size_t)i], 0));
+        const size_t cnt = (size_t)Bc * n;
+        if (cnt) {
+            if (es == 8) dev::nonfinite_kernel<double><<<(unsigned)std::min<size_t>(1184, (cnt + 255) / 256), 256, 0, st>>>(
+                (const double*)(xs + (size_t)r0 * n * es), (int64_t)cnt, c->nf_flag.as<int32_t>());
+            else dev::nonfinite_kernel<float><<<(unsigned)std::min<size_t>(1184, (cnt + 255) / 256), 256, 0, st>>>(
+                (const float*)(xs + (size_t)r0 * n * es), (int64_t)cnt, c->nf_flag.as<int32_t>());
+            c->launches += 1;
+        }
+        eval_device(c, xs + (size_t)r0 * n * es, Bc, c->f_stage.as<double>() + r0, grad_out ? gs + (size_t)r0 * n * es : nullptr,
+                    unsat_out ? c->u_stage.as<int32_t>() + r0 : nullptr, st);
+        CK(cudaEventRecord(c->ev_done[(size_t)i], st));
+        CK(cudaStreamWaitEvent(c->copy_d2h, c->ev_done[(size_t)i], 0));
+        const int64_t nr = r1 - r0;
+        if (nr > 0) {
+            CK(cudaMemcpyAsync(f_out + r0, c->f_stage.as<double>() + r0, (size_t)nr * 8, cudaMemcpyDeviceToHost, c->copy_d2h));
+            if (grad_out && n) CK(cudaMemcpyAsync((char*)grad_out + (size_t)r0 * n * es, gs + (size_t)r0 * n * es, (size_t)nr * n * es,
+                                                  cudaMemcpyDeviceToHost, c->copy_d2h));
+            if (unsat_out) CK(cudaMemcpyAsync(unsat_out + r0, c->u_stage.as<int32_t>() + r0, (size_t)nr * 4, cudaMemcpyDeviceToHost, c->copy_d2h));
+        }
+    }
+    CK(cudaMemcpyAsync(c->nf_host, c->nf_flag.p, 4, cudaMemcpyDeviceToHost, c->copy_d2h));
+    CK(cudaStreamSynchronize(c->copy_d2h));
     CK(cudaStreamSynchronize(st));
+    if (*c->nf_host) throw Error(FFSAT_ERR_NONFINITE, "non-finite point coordinate");
     return FFSAT_OK;
     ABI_CATCH(c)
 }

@@ -358,6 +358,15 @@ __global__ void __launch_bounds__(1024) stats_kernel(const int32_t* done, const 
     }
 }
 
+// Host-buffer evaluation: flag any non-finite staged coordinate on the device instead of a host scan.
+template <typename T>
+__global__ void __launch_bounds__(256) nonfinite_kernel(const T* __restrict__ x, int64_t count, int32_t* flag) {
+    int bad = 0;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count; i += (int64_t)gridDim.x * blockDim.x)
+        bad |= !isfinite(x[i]);
+    if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(flag, 1);
+}
+
 template <typename T>
 __global__ void permute_weights_kernel(T* w_pos, const double* w_orig, const int64_t* order, int64_t m) {
     const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;

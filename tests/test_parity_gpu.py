@@ -473,3 +473,33 @@ def test_bit_packed_check_all_rules(case):
     cnt, _, U = cdp.check(Fo, X.astype(np.float64), want_U=True)
     assert np.array_equal(T["unsat"].cpu().numpy(), cnt)
     assert np.array_equal(np.sort(T["U"].cpu().numpy()), np.sort(U))
+
+
+@pytest.mark.parametrize("B", [7, 600, 1024, 1030])
+def test_host_buffer_pipeline_matches_device(B):
+    """Host-buffer evaluation is staged in equal padded chunks (H2D / D2H overlapped with the chunk evaluations):
+    f, grad and unsat equal the device-buffer evaluation of the same batch within tolerance (bitwise is not
+    promised: the chunk shapes change the reduction partials), for ragged and exact chunk splits."""
+    inst = synth.random_mixed(n=70, m=300, seed=14, kmax=40)
+    X = synth.points("U", B, inst.n, 15)
+    ctx = P.Context.from_instance(inst, device=0)
+    fh, gh, uh = ctx.eval(X, grad=True, unsat=True)
+    fd, gd, ud = ctx.eval(torch.from_numpy(X).cuda(), grad=True, unsat=True)
+    fd, gd, ud = fd.cpu().numpy(), gd.cpu().numpy(), ud.cpu().numpy()
+    assert np.array_equal(uh, ud)
+    assert np.max(np.abs(fh - fd) / np.maximum(1, np.abs(fd))) <= 1e-5
+    assert np.max(np.abs(gh - gd) / np.maximum(1, np.abs(gd))) <= 1e-5
+
+
+def test_host_buffer_nonfinite_rejected():
+    """a non-finite coordinate in a host batch gives FFSAT_ERR_NONFINITE (flagged on the device)."""
+    inst = synth.config1(0)
+    ctx = P.Context.from_instance(inst, device=0)
+    for bad in (np.nan, np.inf, -np.inf):
+        X = synth.points("U", 700, inst.n, 16)
+        X[613, 7] = bad
+        with pytest.raises(P.FfsatError) as e:
+            ctx.eval(X, grad=True)
+        assert "NONFINITE" in str(e.value)
+    f, g, _ = ctx.eval(synth.points("U", 700, inst.n, 16), grad=True)   # the context stays usable
+    assert np.all(np.isfinite(f))
