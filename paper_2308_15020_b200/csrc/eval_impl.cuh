@@ -194,18 +194,19 @@ void eval_device_t(ffsat_ctx* c, const T* x, int64_t B, double* f, T* grad, int3
     rf.B = B; rf.n_parts = L.n_fast > 0 ? c->n_chunks : 0; rf.n_sym = L.n_sym;
     rf.fpart = c->fpart.as<double>(); rf.upart = c->upart.as<int32_t>(); rf.fsym = c->fsym.as<double>();
     rf.usym = c->usym.as<int32_t>(); rf.f = f; rf.unsat = unsat;
-    // with a gradient the f / unsat reduction rides in the gradient reduction (variable tile 0); the profiled
-    // path keeps them apart so the phases can be timed separately
-    const bool fuse = grad && L.n > 0 && !profiled;
+    // tiled path with a gradient: the f / unsat reduction rides in the gradient reduction (variable tile 0), one
+    // launch fewer per evaluation; the profiled path keeps them apart so the phases can be timed separately, and
+    // the global path keeps them apart (its HBM-bound reduction measured slower with the fused variant, c5)
+    const bool fuse = grad && L.n > 0 && !profiled && L.path == 1;
     if (grad) {
         c->launches += 1;
         dev::ReduceArgs<T> r{};
         r.B = B; r.n = L.n; r.n_chunks = L.path == 1 ? c->n_chunks : 0; r.P = c->P.as<T>(); r.Tb = c->Tb.as<T>();
         r.occ_off = c->occ_off.as<int64_t>(); r.occ_slot = c->occ_slot.as<int32_t>(); r.grad = grad;
-        r.fuse_f = fuse;
         r.rf = rf;
         dim3 grid(blocks_for(L.n, 8), blocks_for(B, 32)), blk(32, 8);
-        dev::reduce_grad_kernel<T><<<grid, blk, 0, st>>>(r);
+        if (fuse) dev::reduce_grad_kernel<T, true><<<grid, blk, 0, st>>>(r);
+        else dev::reduce_grad_kernel<T, false><<<grid, blk, 0, st>>>(r);
     }
     mark(3);
     if (!fuse) {

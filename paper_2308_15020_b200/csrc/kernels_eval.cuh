@@ -1524,21 +1524,20 @@ struct ReduceArgs {
     const int64_t* occ_off;      // [n + 1]
     const int32_t* occ_slot;     // variable v's T rows, ascending: occ_slot[occ_off[v] .. occ_off[v + 1])
     T* grad;                     // [B][n]
-    bool fuse_f;                 // the CTAs of variable tile 0 also reduce f / unsat (rf) for their 32 points
-    ReduceFArgs rf;
+    ReduceFArgs rf;              // reduce_grad_kernel<T, true>: the CTAs of variable tile 0 also reduce f / unsat
 };
 
 // block (32, 8): 32 points x 8 variables, one (variable, point) sum per thread: the chunk partials in
 // chunk order, then the variable's occurrence slots in ascending order (fp64 accumulator; loads are
 // issued 8 / 4 ahead but added strictly in order, so the sum order is fixed).  Output through smem so
 // each point row gets 8 consecutive gradient entries.
-template <typename T>
+template <typename T, bool FUSE_F>
 __global__ void __launch_bounds__(256) reduce_grad_kernel(ReduceArgs<T> a) {
     __shared__ T tile[8][33];
     const int tx = threadIdx.x, ty = threadIdx.y;
     const int64_t b0 = (int64_t)blockIdx.y * 32, v0 = (int64_t)blockIdx.x * 8;   // grid.x over variables (n may exceed 65535 tiles)
     const int64_t b = b0 + tx, v = v0 + ty;
-    if (a.fuse_f && blockIdx.x == 0) {   // f / unsat of points b0 .. b0 + 31: warp ty sums rows ty, ty + 8, ... then in order
+    if (FUSE_F && blockIdx.x == 0) {   // f / unsat of points b0 .. b0 + 31: warp ty sums rows ty, ty + 8, ... then in order
         __shared__ double sf[8][32];
         __shared__ int su[8][32];
         double f = 0.0;
