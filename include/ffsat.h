@@ -115,8 +115,14 @@ ffsat_status ffsat_export(const ffsat_ctx* ctx, uint8_t* kind, int32_t* bound, d
 /* f[b] = sum_c w_c FE_c(x_b) (fp64 accumulation), grad[b][:] = d f / d x at x_b (context dtype),
  * unsat[b] = number of constraints falsified by sgn(x_b) (x < 0 = True, x = 0 = False; exact).
  * x: [B][n] context dtype, coordinates in [-1, 1] (not checked on device; host inputs are
- * checked for NaN/Inf -> FFSAT_ERR_NONFINITE).  f_out [B] double; grad_out [B][n] or NULL;
- * unsat_out [B] int32 or NULL.  Weights: the context's current weights (ffsat_set_weights). */
+ * checked for NaN/Inf -> FFSAT_ERR_NONFINITE, detected by a device kernel on the staged copy: the
+ * outputs are then unspecified).  f_out [B] double; grad_out [B][n] or NULL; unsat_out [B] int32 or
+ * NULL.  Weights: the context's current weights (ffsat_set_weights).
+ * Host buffers (on_device = 0) are staged in 2-4 equal chunks (B >= 512) whose H2D / D2H copies overlap
+ * the chunk evaluations; pinned host memory is needed for the overlap (pageable memory still works).
+ * The call returns when the outputs are in host memory.  Device buffers (on_device = 1) are asynchronous
+ * on `stream`.  Limit: a formula with fast constraints of length 16 < k <= 64 on the global (large-n)
+ * path needs n * B < 2^32 (FFSAT_ERR_ARG otherwise; split the batch). */
 ffsat_status ffsat_eval(ffsat_ctx* ctx, const void* x, int64_t B, int32_t on_device, double* f_out,
                         void* grad_out, int32_t* unsat_out, void* stream);
 
