@@ -1037,7 +1037,10 @@ __device__ void global_unit_long_cp(const GlobalArgs<T>& a, const BucketReg<T>& 
                                     int j0, T* xs, T* ps, uint32_t* ws, double& facc, int& uacc) {
     const int k = bk.k;
     const int lane = threadIdx.x & 31;
-    const char* xb = reinterpret_cast<const char*>(a.xT + (bv ? b : 0));
+    // lanes past the batch end mirror the last point (same inputs, same arithmetic, same stored values), so the
+    // term stores need no predicate: a duplicate lane writes what the last valid lane writes
+    const int64_t bb = bv ? b : a.B - 1;
+    const char* xb = reinterpret_cast<const char*>(a.xT + bb);
     const uint32_t rowb = (uint32_t)a.B * (uint32_t)sizeof(T);   // bytes per x^T row (plan(): n B < 2^32)
     for (int j = j0; j < unit_count(U); j += long_warps<T>()) {
         const int64_t pos = (int64_t)U.pos_begin + j;
@@ -1055,7 +1058,7 @@ __device__ void global_unit_long_cp(const GlobalArgs<T>& a, const BucketReg<T>& 
         cp_async_commit_wait_all();
         T fe = bk.g0;
         uint32_t t = 0;
-        T* dst = a.Tb + (bk.slot_off + (pos - bk.pos_begin) * k) * a.B + b;
+        T* dst = a.Tb + (bk.slot_off + (pos - bk.pos_begin) * k) * a.B + bb;
 #pragma unroll
         for (int c = 0; c < NCH; ++c) {
             const T c0 = bk.c0[c], c1 = bk.c1[c];
@@ -1078,18 +1081,16 @@ __device__ void global_unit_long_cp(const GlobalArgs<T>& a, const BucketReg<T>& 
                 const uint32_t w = ws[i];
                 const T cs = flip_sign(c1, w);
                 const T p = ps[32 * i] * suf;
-                if (bv) {
-                    T* d = dst + (size_t)((uint32_t)i * (uint32_t)a.B);
-                    if (c == 0) __stcs(d, p * cs);
-                    else *d = fmaT(p, cs, *d);
-                }
+                T* d = dst + (size_t)((uint32_t)i * (uint32_t)a.B);
+                if (c == 0) __stcs(d, p * cs);
+                else *d = fmaT(p, cs, *d);
                 suf *= fmaT(cs, xs[32 * i], c0);
             }
         }
         if (NCH == 0) {
             for (int i = 0; i < k; ++i) {
                 t += lit_true(xs[32 * i], ws[i]);
-                if (bv) __stcs(dst + (size_t)((uint32_t)i * (uint32_t)a.B), (T)0);
+                __stcs(dst + (size_t)((uint32_t)i * (uint32_t)a.B), (T)0);
             }
         }
         facc += (double)(wc * fe);
