@@ -177,12 +177,14 @@ struct CheckBitsArgs {
     int32_t* unsat;           // [B]
 };
 
-// Bit-sliced comparison of the per-point counts (planes p[0..P), LSB first) with a constant: gt / eq masks.
-__device__ __forceinline__ void bits_cmp(const uint32_t* p, int P, int c, uint32_t& gt, uint32_t& eq) {
+// Bit-sliced comparison of the per-point counts (planes p[0..13), LSB first, zero above plane P) with a constant:
+// gt / eq masks (fully unrolled so the planes stay in registers).
+__device__ __forceinline__ void bits_cmp(const uint32_t (&p)[13], int c, uint32_t& gt, uint32_t& eq) {
     gt = 0u;
     eq = 0xffffffffu;
-    if (c >> P) { eq = 0u; return; }   // c >= 2^P > every count
-    for (int j = P - 1; j >= 0; --j) {
+    if (c >> 13) { eq = 0u; return; }   // c >= 2^13 > every count
+#pragma unroll
+    for (int j = 12; j >= 0; --j) {
         if ((c >> j) & 1) eq &= p[j];
         else {
             gt |= eq & p[j];
@@ -191,11 +193,78 @@ __device__ __forceinline__ void bits_cmp(const uint32_t* p, int P, int c, uint32
     }
 }
 
+// Satisfied mask of one constraint over the 32 points of a sign tile, from its literals lo + first, lo + first +
+// stride, ... (COOP: the 32 lanes of the warp take interleaved literals and the partial reductions / bit-sliced
+// counts are combined across the warp, every lane ends with the result).  Literal truth masks L = S[v] ^ (negated ?
+// ~0 : 0); OR / AND / parity rules reduce them with one op each, the other rules count them in bit-sliced planes
+// compared with t_min / t_max.
+template <bool SMEM, bool COOP>
+__device__ __forceinline__ uint32_t sat_mask(const CheckBitsArgs& a, const uint32_t* S, int64_t lo, int64_t hi, int tmin, int tmax,
+                                             int par, int first, int stride) {
+    const int k = (int)(hi - lo);
+    auto lit = [&](int64_t i) {
+        const uint32_t w = __ldg(a.words + i);
+        return (SMEM ? S[w & 0x7fffffffu] : __ldg(S + (w & 0x7fffffffu))) ^ (uint32_t)((int)w >> 31);
+    };
+    if (par == 0 && tmin == 1 && tmax >= k) {            // OR: some literal True
+        uint32_t m = 0u;
+        for (int64_t i = lo + first; i < hi; i += stride) m |= lit(i);
+        if (COOP) m = __reduce_or_sync(0xffffffffu, m);
+        return m;
+    }
+    if (par == 0 && tmin >= k && tmax >= k) {            // AND: every literal True
+        uint32_t m = 0xffffffffu;
+        for (int64_t i = lo + first; i < hi; i += stride) m &= lit(i);
+        if (COOP) m = __reduce_and_sync(0xffffffffu, m);
+        return tmin > k ? 0u : m;
+    }
+    if (par != 0 && tmin <= 0 && tmax >= k) {            // XOR / XNOR: parity of the True literals
+        uint32_t x = 0u;
+        for (int64_t i = lo + first; i < hi; i += stride) x ^= lit(i);
+        if (COOP) x = __reduce_xor_sync(0xffffffffu, x);
+        return par == 1 ? x : ~x;
+    }
+    // counting rules: bit-sliced planes (LSB first), k <= 4096 -> 13 planes
+    uint32_t p[13];
+#pragma unroll
+    for (int j = 0; j < 13; ++j) p[j] = 0u;
+    for (int64_t i = lo + first; i < hi; i += stride) {
+        uint32_t carry = lit(i);
+#pragma unroll
+        for (int j = 0; j < 13; ++j) {   // ripple-carry add of one bit per point
+            if (carry == 0u) break;
+            const uint32_t t = p[j] & carry;
+            p[j] ^= carry;
+            carry = t;
+        }
+    }
+    if (COOP) {   // butterfly sum of the 32 lanes' bit-sliced counts
+#pragma unroll
+        for (int d = 16; d >= 1; d >>= 1) {
+            uint32_t carry = 0u;
+#pragma unroll
+            for (int j = 0; j < 13; ++j) {
+                const uint32_t q = __shfl_xor_sync(0xffffffffu, p[j], d);
+                const uint32_t sum = p[j] ^ q ^ carry;
+                carry = (p[j] & q) | (carry & (p[j] ^ q));
+                p[j] = sum;
+            }
+        }
+    }
+    uint32_t gtn, eqn, gtx, eqx;
+    bits_cmp(p, tmin, gtn, eqn);
+    bits_cmp(p, tmax, gtx, eqx);
+    uint32_t sat = (gtn | eqn) & ~gtx;
+    if (par == 1) sat &= p[0];
+    if (par == 2) sat &= ~p[0];
+    return sat;
+}
+
 // grid (point tiles, constraint chunks), 256 threads; SMEM: the tile's sign words staged in shared memory
-// (n words), else read through the read-only path.  Thread = one constraint for 32 points: literal truth masks
-// L = S[v] ^ (negated ? ~0 : 0); OR / AND / parity rules reduce them with one op each, other rules count them in
-// bit-sliced planes.  U_c: popc of the unsat mask (one integer atomic per constraint with unsat points);
-// unsat[b]: the warp transposes its 32 unsat masks with ballots, lane b keeps point b's count.
+// (n words), else read through the read-only path.  Thread = one constraint for 32 points (sat_mask); constraints
+// longer than 128 literals are taken by the whole warp, one after the other (sat_mask<COOP>), so a long
+// cardinality row does not serialise one thread.  U_c: popc of the unsat mask (one integer atomic per constraint
+// with unsat points); unsat[b]: the warp transposes its 32 unsat masks with ballots, lane b keeps point b's count.
 template <bool SMEM>
 __global__ void __launch_bounds__(256) check_bits_kernel(CheckBitsArgs a) {
     extern __shared__ __align__(16) uint32_t sgn[];
@@ -215,59 +284,23 @@ __global__ void __launch_bounds__(256) check_bits_kernel(CheckBitsArgs a) {
     for (int64_t cb = c0 + warp * 32; cb < c1; cb += 256) {
         const int64_t c = cb + lane;
         uint32_t uns = 0u;
+        int64_t lo = 0, hi = 0;
+        int tmin = 0, tmax = 0, par = 0;
         if (c < c1) {
-            const int64_t lo = __ldg(a.off + c), hi = __ldg(a.off + c + 1);
-            const int k = (int)(hi - lo);
-            const int tmin = __ldg(a.rule + 3 * c), tmax = __ldg(a.rule + 3 * c + 1), par = __ldg(a.rule + 3 * c + 2);
-            uint32_t sat;
-            if (par == 0 && tmin == 1 && tmax >= k) {            // OR: some literal True
-                sat = 0u;
-                for (int64_t i = lo; i < hi; ++i) {
-                    const uint32_t w = __ldg(a.words + i);
-                    sat |= (SMEM ? S[w & 0x7fffffffu] : __ldg(S + (w & 0x7fffffffu))) ^ (uint32_t)((int)w >> 31);
-                }
-            } else if (par == 0 && tmin >= k && tmax >= k) {     // AND: every literal True
-                sat = 0xffffffffu;
-                for (int64_t i = lo; i < hi; ++i) {
-                    const uint32_t w = __ldg(a.words + i);
-                    sat &= (SMEM ? S[w & 0x7fffffffu] : __ldg(S + (w & 0x7fffffffu))) ^ (uint32_t)((int)w >> 31);
-                }
-                if (tmin > k) sat = 0u;
-            } else if (par != 0 && tmin <= 0 && tmax >= k) {     // XOR / XNOR: parity of the True literals
-                uint32_t x = 0u;
-                for (int64_t i = lo; i < hi; ++i) {
-                    const uint32_t w = __ldg(a.words + i);
-                    x ^= (SMEM ? S[w & 0x7fffffffu] : __ldg(S + (w & 0x7fffffffu))) ^ (uint32_t)((int)w >> 31);
-                }
-                sat = par == 1 ? x : ~x;
-            } else {                                             // counting rules: bit-sliced planes
-                uint32_t p[13];
-                int P = 1;
-                while ((1 << P) <= k) ++P;                       // k <= 4096 -> P <= 13
-#pragma unroll
-                for (int j = 0; j < 13; ++j) p[j] = 0u;
-                for (int64_t i = lo; i < hi; ++i) {
-                    const uint32_t w = __ldg(a.words + i);
-                    uint32_t carry = (SMEM ? S[w & 0x7fffffffu] : __ldg(S + (w & 0x7fffffffu))) ^ (uint32_t)((int)w >> 31);
-#pragma unroll
-                    for (int j = 0; j < 13; ++j) {   // ripple-carry add of one bit per point
-                        if (carry == 0u) break;
-                        const uint32_t t = p[j] & carry;
-                        p[j] ^= carry;
-                        carry = t;
-                    }
-                }
-                uint32_t gtn, eqn, gtx, eqx;
-                bits_cmp(p, P, tmin, gtn, eqn);
-                bits_cmp(p, P, tmax, gtx, eqx);
-                sat = (gtn | eqn) & ~gtx;
-                if (par == 1) sat &= p[0];
-                if (par == 2) sat &= ~p[0];
-            }
-            uns = ~sat & vm;
-            const int cnt = __popc(uns);
-            if (cnt) atomicAdd(a.U + c, cnt);
+            lo = __ldg(a.off + c);
+            hi = __ldg(a.off + c + 1);
+            tmin = __ldg(a.rule + 3 * c); tmax = __ldg(a.rule + 3 * c + 1); par = __ldg(a.rule + 3 * c + 2);
         }
+        const bool longc = c < c1 && hi - lo > 128;
+        if (c < c1 && !longc) uns = ~sat_mask<SMEM, false>(a, S, lo, hi, tmin, tmax, par, 0, 1) & vm;
+        for (uint32_t lm = __ballot_sync(0xffffffffu, longc); lm; lm &= lm - 1) {
+            const int src = __ffs(lm) - 1;
+            const int64_t lo_s = __shfl_sync(0xffffffffu, lo, src), hi_s = __shfl_sync(0xffffffffu, hi, src);
+            const uint32_t sat = sat_mask<SMEM, true>(a, S, lo_s, hi_s, __shfl_sync(0xffffffffu, tmin, src),
+                                                      __shfl_sync(0xffffffffu, tmax, src), __shfl_sync(0xffffffffu, par, src), lane, 32);
+            if (lane == src) uns = ~sat & vm;
+        }
+        if (uns) atomicAdd(a.U + c, __popc(uns));
         // transpose: point b's count over this warp's 32 constraints = popc of the ballot of bit b
 #pragma unroll 8
         for (int bb = 0; bb < 32; ++bb) {
