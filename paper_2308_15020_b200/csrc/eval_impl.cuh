@@ -205,7 +205,8 @@ void eval_device_t(ffsat_ctx* c, const T* x, int64_t B, double* f, T* grad, int3
         r.occ_off = c->occ_off.as<int64_t>(); r.occ_slot = c->occ_slot.as<int32_t>(); r.grad = grad;
         r.rf = rf;
         dim3 grid(blocks_for(L.n, 8), blocks_for(B, 32)), blk(32, 8);
-        if (fuse) dev::reduce_grad_kernel<T, true><<<grid, blk, 0, st>>>(r);
+        // the fused (tiled-path) reduction follows the product kernel programmatically (PDL)
+        if (fuse) launch_pdl(dev::reduce_grad_kernel<T, true>, grid, blk, 0, st, r);
         else dev::reduce_grad_kernel<T, false><<<grid, blk, 0, st>>>(r);
     }
     mark(3);

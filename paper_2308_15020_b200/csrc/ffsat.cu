@@ -321,7 +321,7 @@ void search_iterate_direct(ffsat_search* s, int n_iters, cudaStream_t st) {
             dev::pgd_step_kernel<double><<<(unsigned)s->B, 256, 0, st>>>(a);
         } else {
             search_eval<float>(s, s->Xp.p, s->fP.as<double>(), s->Gp.p, s->unsatP.as<int32_t>(), st);
-            dev::pgd_step_kernel<float><<<(unsigned)s->B, 256, 0, st>>>(a);
+            launch_pdl(dev::pgd_step_kernel<float>, dim3((unsigned)s->B), dim3(256), 0, st, a);
         }
     }
     CK(cudaGetLastError());

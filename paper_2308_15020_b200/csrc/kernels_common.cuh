@@ -6,6 +6,12 @@
 namespace ffsat {
 namespace dev {
 
+// Programmatic dependent launch (sm_90+): a kernel launched with the programmatic-serialization attribute may
+// start while its predecessor drains; pdl_wait() blocks until the predecessor grid has completed and its memory
+// is visible (a no-op for a normal launch), pdl_trigger() lets this grid's dependents be scheduled early.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 __device__ __forceinline__ float fmaT(float a, float b, float c) { return fmaf(a, b, c); }
 __device__ __forceinline__ double fmaT(double a, double b, double c) { return ::fma(a, b, c); }
 __device__ __forceinline__ float clamp1(float v) { return fminf(fmaxf(v, -1.0f), 1.0f); }

@@ -833,6 +833,7 @@ __global__ void __launch_bounds__(256, 2) fast_wide_kernel(TiledArgs<float> a) {
         cp_async_commit();
         if (u + 3 < u1) after = a.units[u + 3];
     }
+    pdl_trigger();   // the gradient reduction may be scheduled now (it waits for this grid to complete)
     // outputs: partial gradient tile (float2 per lane), partial f / unsat (fixed warp order)
     const int64_t b = b0 + 2 * lane;
     for (int v = warp; v < n; v += nw) {
@@ -1538,6 +1539,8 @@ __global__ void __launch_bounds__(256) reduce_grad_kernel(ReduceArgs<T> a) {
     const int tx = threadIdx.x, ty = threadIdx.y;
     const int64_t b0 = (int64_t)blockIdx.y * 32, v0 = (int64_t)blockIdx.x * 8;   // grid.x over variables (n may exceed 65535 tiles)
     const int64_t b = b0 + tx, v = v0 + ty;
+    pdl_wait();      // launched programmatically after the product kernel: its partials must be complete
+    pdl_trigger();
     if (FUSE_F && blockIdx.x == 0) {   // f / unsat of points b0 .. b0 + 31: warp ty sums rows ty, ty + 8, ... then in order
         __shared__ double sf[8][32];
         __shared__ int su[8][32];

@@ -75,6 +75,7 @@ struct PgdArgs {
 // one CTA (256 threads) per point
 template <typename T>
 __global__ void __launch_bounds__(256) pgd_step_kernel(PgdArgs a) {
+    pdl_wait();   // launched programmatically after the gradient reduction
     __shared__ double red[256];
     __shared__ int s_acc;
     const int64_t b = blockIdx.x;
