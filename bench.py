@@ -177,8 +177,20 @@ def cpu_baseline(cfg, inst, X):
     t0 = time.perf_counter()
     cdp.evaluate(Fo, Xd[:S])
     t = time.perf_counter() - t0
+    # the 1-thread rate on a smaller sample (SURVEY 8(d) oracle timing) and the host CPU model
+    S1 = int(max(1, min(S, 2.0 / max(per_pt, 1e-9))))
+    t0 = time.perf_counter()
+    cdp.evaluate(Fo, Xd[:S1], threads=1)
+    t1 = time.perf_counter() - t0
+    cpu = ""
+    try:
+        with open("/proc/cpuinfo") as fh:
+            cpu = next((ln.split(":", 1)[1].strip() for ln in fh if ln.startswith("model name")), "")
+    except OSError:
+        pass
     return {"value": inst.n_lits * S / t, "unit": "terms/s", "cores": threads, "kind": "oracle",
-            "sample": f"f + grad of {S} of the workload's {len(Xd)} points in fp64 ({t:.1f} s)"}
+            "sample": f"f + grad of {S} of the workload's {len(Xd)} points in fp64 ({t:.1f} s)",
+            "value_1_thread": inst.n_lits * S1 / t1, "sample_1_thread": f"{S1} points ({t1:.1f} s)", "cpu": cpu}
 
 
 # ------------------------------------------------------------------------------------------------ our arm
