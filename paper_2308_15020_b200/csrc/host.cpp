@@ -3,6 +3,7 @@
 #include "host.hpp"
 
 #include <algorithm>
+#include <cstdlib>
 #include <array>
 #include <cerrno>
 #include <climits>
@@ -449,10 +450,13 @@ Layout build_layout(const Formula& F, int path, int precision) {
         Lo.sym_classes.back().max_mp = std::max(Lo.sym_classes.back().max_mp, (k + 1) / 2);
         if (G == 0) Lo.sym_lane = true;
     }
+    // roots per CTA of the root path (FFSAT_ROOT_CHUNK overrides kRootChunk: a tuning knob)
+    int root_chunk = kRootChunk;
+    if (const char* e = std::getenv("FFSAT_ROOT_CHUNK")) root_chunk = std::max(1, std::atoi(e));
     for (SymClass& cl : Lo.sym_classes) {
         cl.lit_begin = Lo.sym_off[(size_t)cl.begin];
         cl.lit_end = Lo.sym_off[(size_t)cl.end];
-        cl.S = cl.G == 0 ? 1 : std::max(1, std::min(32, (cl.max_mp + kRootChunk - 1) / kRootChunk));
+        cl.S = cl.G == 0 ? 1 : std::max(1, std::min(32, (cl.max_mp + root_chunk - 1) / root_chunk));
     }
 
     // ---- T-buffer slots and occurrence CSR (ascending slot order per variable)

@@ -66,7 +66,7 @@ struct SymClass {                   // launch class: G threads per (constraint, 
     int32_t S = 1;                  // root splits: each item's M' roots are shared by S CTAs (balance; G > 0 only)
     int64_t lit_begin = 0, lit_end = 0;   // the class's literals in the sym word array
 };
-constexpr int kRootChunk = 64;      // target roots per CTA of the root path (SymClass::S = ceil(max M' / kRootChunk))
+constexpr int kRootChunk = 256;     // target roots per CTA of the root path (SymClass::S = ceil(max M' / kRootChunk)); c3: 64 -> 1.77 ms, 128 -> 1.69, 256 -> 1.68, unsplit 1.85
 
 struct WorkUnit {                   // a run of fast constraints of one bucket, contiguous positions
     int32_t bucket;                 // tiled path: a var-disjoint class (no variable occurs twice in it),
