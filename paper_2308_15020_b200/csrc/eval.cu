@@ -1,5 +1,6 @@
 // eval.cu -- batch planning of ffsat_eval (chunk split of the fast kernels, scratch sizing).
 #include <algorithm>
+#include <cstdlib>
 
 #include "ctx.hpp"
 
@@ -57,8 +58,10 @@ void plan(ffsat_ctx* c, int64_t B) {
     }
     int ncg[3] = {0, 0, 0};
     if (L.n_fast > 0) {
-        ncg[0] = pick_chunks(PT, cps, c->num_sm, ug[1] - ug[0]);
-        ncg[1] = pick_chunks(PT, cps, c->num_sm, ug[2] - ug[1]);
+        int gcps = cps;   // FFSAT_GLOBAL_CPS: tuning override of the CTAs-per-SM target of the k <= 16 global kernel
+        if (const char* e = std::getenv("FFSAT_GLOBAL_CPS")) if (L.path == 2) gcps = std::max(1, std::atoi(e));
+        ncg[0] = pick_chunks(PT, gcps, c->num_sm, ug[1] - ug[0]);
+        ncg[1] = pick_chunks(PT, gcps, c->num_sm, ug[2] - ug[1]);
         ncg[2] = pick_chunks(PT, 3, c->num_sm, ug[3] - ug[2]);   // long kernel: 64 KB smem per CTA
     }
     if (ncg[2] > 0 && (uint64_t)L.n * (uint64_t)B >= (1ull << 32))

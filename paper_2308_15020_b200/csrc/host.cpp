@@ -506,7 +506,9 @@ Layout build_layout(const Formula& F, int path, int precision) {
     }
     // global units hold <= cap literals: 512 for large formulas, smaller for small ones so that the chunk split
     // (<= one chunk per unit) still yields enough CTAs per point tile to fill the GPU
-    const int64_t gcap = std::min<int64_t>(512, std::max<int64_t>(32, Lo.n_fast_lits / 1024));
+    int64_t gmax = 512;   // FFSAT_GLOBAL_UNIT: tuning override of the largest global unit (literals)
+    if (const char* e = std::getenv("FFSAT_GLOBAL_UNIT")) gmax = std::max(16, std::atoi(e));
+    const int64_t gcap = std::min<int64_t>(gmax, std::max<int64_t>(32, Lo.n_fast_lits / 1024));
     for (size_t bi = 0; bi < Lo.fbuckets.size(); ++bi) {
         const FastBucket& b = Lo.fbuckets[bi];
         int64_t p = b.pos_begin;
