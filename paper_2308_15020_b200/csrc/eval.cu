@@ -13,6 +13,10 @@ int pick_chunks(int64_t point_tiles, int ctas_per_sm, int num_sm, int64_t n_unit
     const int64_t slots = (int64_t)num_sm * std::max(1, ctas_per_sm);
     int best = 1;
     double best_eff = -1;
+    if (const char* e = std::getenv("FFSAT_WAVES")) {   // tuning override: exactly this many waves of CTAs
+        const int64_t nc = std::max<int64_t>(1, (std::max(1, std::atoi(e)) * slots) / point_tiles);
+        return (int)std::min<int64_t>(nc, n_units);
+    }
     for (int w = 1; w <= 4; ++w) {
         int64_t nc = std::max<int64_t>(1, (w * slots) / point_tiles);
         nc = std::min<int64_t>(nc, n_units);
