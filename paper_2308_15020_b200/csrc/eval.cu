@@ -66,7 +66,7 @@ void plan(ffsat_ctx* c, int64_t B) {
         if (const char* e = std::getenv("FFSAT_GLOBAL_CPS")) if (L.path == 2) gcps = std::max(1, std::atoi(e));
         ncg[0] = pick_chunks(PT, gcps, c->num_sm, ug[1] - ug[0]);
         ncg[1] = pick_chunks(PT, gcps, c->num_sm, ug[2] - ug[1]);
-        ncg[2] = pick_chunks(PT, 3, c->num_sm, ug[3] - ug[2]);   // long kernel: 64 KB smem per CTA
+        ncg[2] = pick_chunks(PT, 6, c->num_sm, ug[3] - ug[2]);   // long kernel: 32 KB smem per CTA
     }
     if (ncg[2] > 0 && (uint64_t)L.n * (uint64_t)B >= (1ull << 32))
         throw Error(FFSAT_ERR_ARG, "batch too large for the long-constraint kernel (n * B must be < 2^32; split the batch)");

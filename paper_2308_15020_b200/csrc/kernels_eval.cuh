@@ -1025,10 +1025,10 @@ __global__ void __launch_bounds__(256) fast_global_kernel(GlobalArgs<T> a) {
 // The warp reads the row's literal words once, coalesced (word i in lane i % 32 of register i / 32), and every
 // lane issues all k gathers x^T[v_i][b] as 4/8-byte cp.async copies into its own shared column xs[i][lane]
 // (no registers held by loads in flight, all k lines requested at once); the exclusive prefixes go to a second
-// column; the backward sweep writes every term once (streaming store).  kLongWarps warps per CTA, 2 x 64 x 32
-// values of shared memory per warp (dynamic: f32 64 KB, f64 64 KB with 2 warps).
+// column; the backward sweep writes every term once (streaming store).  2 warps per CTA (smaller CTAs pack 14 warps per SM), 2 x 64 x 32
+// values of shared memory per warp (dynamic: f32 32 KB, f64 64 KB per CTA).
 template <typename T>
-__host__ __device__ constexpr int long_warps() { return sizeof(T) == 4 ? 4 : 2; }
+__host__ __device__ constexpr int long_warps() { return sizeof(T) == 4 ? 2 : 2; }
 constexpr int kLongKMax = 64;
 template <typename T>
 __host__ __device__ constexpr size_t long_smem_bytes() { return (size_t)long_warps<T>() * 2 * kLongKMax * 32 * sizeof(T); }
