@@ -14,6 +14,8 @@ namespace ffsat {
 namespace dev {
 template <typename T>
 struct SymArgs;
+template <typename T>
+struct SymSplit;
 }
 
 #define CK(call)                                                                                     \
@@ -156,6 +158,6 @@ template <typename T>
 void set_long_smem();              // the long global kernel's dynamic shared memory (eval_f32.cu / eval_f64.cu)
 // one root-path launch class (sym_f32.cu / sym_f64.cu)
 template <typename T>
-void launch_sym_class(const SymClass& cl, const dev::SymArgs<T>& a, cudaStream_t st);
+void launch_sym_class(const SymClass& cl, const dev::SymArgs<T>& a, const dev::SymSplit<T>& sp, cudaStream_t st);
 
 }  // namespace ffsat

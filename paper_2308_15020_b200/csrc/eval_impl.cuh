@@ -96,14 +96,14 @@ void eval_device_t(ffsat_ctx* c, const T* x, int64_t B, double* f, T* grad, int3
             cudaStream_t ss = fork ? c->side[i % FFSAT_SIDE_STREAMS] : st;
             if (fork && i < FFSAT_SIDE_STREAMS) CK(cudaStreamWaitEvent(ss, c->ev_fork, 0));
             const SymClass& cl = L.sym_classes[i];
-            dev::SymArgs<T> ac = cl.G == 0 ? aT : a;
-            ac.S = c->sym_S[i];
-            ac.s_end = cl.end;
-            ac.lit0 = cl.lit_begin;
-            ac.TbS = c->TbS.as<T>() + c->sym_offT[i];
-            ac.fS = c->fS.as<double>() + c->sym_offF[i];
-            launch_sym_class<T>(cl, ac, ss);
-            c->launches += ac.S > 1 ? 2 : 1;   // + the split combine
+            dev::SymSplit<T> sp{};
+            sp.S = c->sym_S[i];
+            sp.s_end = cl.end;
+            sp.lit0 = cl.lit_begin;
+            sp.TbS = c->TbS.as<T>() + c->sym_offT[i];
+            sp.fS = c->fS.as<double>() + c->sym_offF[i];
+            launch_sym_class<T>(cl, cl.G == 0 ? aT : a, sp, ss);
+            c->launches += sp.S > 1 ? 2 : 1;   // + the split combine
         }
         CK(cudaGetLastError());
         if (fork) {

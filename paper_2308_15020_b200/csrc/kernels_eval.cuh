@@ -162,66 +162,6 @@ __device__ __forceinline__ T* tile_at(T* base, uint32_t w) {
     return reinterpret_cast<T*>(reinterpret_cast<char*>(base) + (uint32_t)(w << (sizeof(T) == 8 ? 3 : 2)));
 }
 
-// One constraint with 16 < k <= 16 KB (KB = 2..4) for one lane (= one point).  The warp reads the row's literal
-// words once, coalesced (word i in lane i % 32 of register i / 32), takes the negation bits by ballot, and issues
-// all k gathers getx(word) before any arithmetic (all in flight together); the variable values stay in registers
-// (fully unrolled, predicated on the warp-uniform i < k), the exclusive prefix products in registers (SPRE =
-// false) or in a per-lane shared-memory column pre_s[32 i] (SPRE = true, halves the register footprint).
-// emit(i, word, p, cs, first) receives p = pre_i * suf_i (suf seeded with g w_c) and the slope cs = s_i c1: the
-// literal's term is p * cs, to be stored (first channel) or added.
-template <typename T, int KB, int NCH, bool SPRE, typename GetX, typename Emit>
-__device__ __forceinline__ void long_clause(const BucketReg<T>& bk, int k, const uint32_t* wp, T wc, T* pre_s, GetX getx, Emit emit,
-                                            double& facc, int& uacc) {
-    constexpr int KM = 16 * KB, NR = (KM + 31) / 32;
-    const int lane = threadIdx.x & 31;
-    uint32_t wl[NR], neg[NR];
-#pragma unroll
-    for (int r = 0; r < NR; ++r) {
-        wl[r] = lane + 32 * r < k ? __ldg(wp + lane + 32 * r) : 0u;
-        neg[r] = __ballot_sync(0xffffffffu, (int)wl[r] < 0);
-    }
-    T xv[KM];
-#pragma unroll
-    for (int i = 0; i < KM; ++i)
-        if (i < k) xv[i] = getx(__shfl_sync(0xffffffffu, wl[i / 32], i % 32));
-    uint32_t t = 0;
-#pragma unroll
-    for (int i = 0; i < KM; ++i)
-        if (i < k) t += (uint32_t)(xv[i] < (T)0) ^ ((neg[i / 32] >> (i % 32)) & 1u);
-    T fe = bk.g0;
-    T preg[SPRE ? 1 : KM];
-#pragma unroll
-    for (int c = 0; c < NCH; ++c) {
-        const T c0 = bk.c0[c], c1 = bk.c1[c];
-        T run = (T)1;
-#pragma unroll
-        for (int i = 0; i < KM; ++i)
-            if (i < k) {
-                const T cs = flip_sign(c1, neg[i / 32] << (31 - i % 32));
-                if constexpr (SPRE) pre_s[32 * i] = run;
-                else preg[i] = run;
-                run *= fmaT(cs, xv[i], c0);
-            }
-        fe = fmaT(bk.g[c], run, fe);
-        T suf = bk.g[c] * wc;
-#pragma unroll
-        for (int i = KM - 1; i >= 0; --i)
-            if (i < k) {
-                const uint32_t w = __shfl_sync(0xffffffffu, wl[i / 32], i % 32);
-                const T cs = flip_sign(c1, w);
-                T pi;
-                if constexpr (SPRE) pi = pre_s[32 * i];
-                else pi = preg[i];
-                emit(i, w, pi * suf, cs, c == 0);
-                suf *= fmaT(cs, xv[i], c0);
-            }
-    }
-    if (NCH == 0)
-        for (int i = 0; i < k; ++i) emit(i, __ldg(wp + i), (T)0, (T)0, true);
-    facc += (double)(wc * fe);
-    uacc += rule_sat((int)t, bk.tmin, bk.tmax, bk.parity) ? 0 : 1;
-}
-
 // One constraint for one lane (= one point), k <= 16 unrolled, literal words already in registers.
 // With c_s = s_i c1 (literal sign folded into the factor slope), a_i = c0 + c_s x_{v_i};
 // FE = g0 + sum_ch g prod_i a_i and d f / d x_{v_i} = w sum_ch g c_s prod_{j != i} a_j (exclusive
@@ -507,22 +447,6 @@ __device__ void tiled_run_long(const TiledArgs<T>& a, int bucket, const BucketRe
                                const T* xl, T* gl, int warp, int nw, double& facc, int& uacc) {
     const int k = bk.k;
     while (P.u < u1 && P.cur.bucket == bucket) {
-        if constexpr (sizeof(T) == 4) {
-            // fp32: register-resident rows (long_clause); the class is var-disjoint, so terms add straight into the tile
-            for (int j = warp; j < unit_count(P.cur); j += nw) {
-                const int64_t pos = (int64_t)P.cur.pos_begin + j;
-                const uint32_t* wp = a.words + (int64_t)P.cur.word_begin + (int64_t)j * unit_kp(P.cur);
-                auto getx = [&](uint32_t w) { return *tile_at(xl, w); };
-                auto emit = [&](int, uint32_t w, float p, float cs, bool) {
-                    float* g = tile_at(gl, w);
-                    *g = fmaf(p, cs, *g);
-                };
-                const float wc = a.w_pos[pos];
-                if (k <= 32) long_clause<float, 2, NCH, false>(bk, k, wp, wc, nullptr, getx, emit, facc, uacc);
-                else if (k <= 48) long_clause<float, 3, NCH, false>(bk, k, wp, wc, nullptr, getx, emit, facc, uacc);
-                else long_clause<float, 4, NCH, false>(bk, k, wp, wc, nullptr, getx, emit, facc, uacc);
-            }
-        } else {
         for (int j = warp; j < unit_count(P.cur); j += nw) {
             const int64_t pos = (int64_t)P.cur.pos_begin + j;
             const uint32_t* wp = a.words + (int64_t)P.cur.word_begin + (int64_t)j * unit_kp(P.cur);
@@ -544,7 +468,6 @@ __device__ void tiled_run_long(const TiledArgs<T>& a, int bucket, const BucketRe
             fast_terms_blocked<T, NCH>(k, bk, getl, addterm, fe);
             facc += (double)(wc * fe);
             uacc += rule_sat((int)t, bk.tmin, bk.tmax, bk.parity) ? 0 : 1;
-        }
         }
         pipe_advance<T>(a, P, u1, st);
     }
@@ -1171,8 +1094,13 @@ struct SymArgs {
     T* Tb;                       // [tb_slots][B]
     double* fsym;                // [n_sym][B]  w * FE
     int32_t* usym;               // [n_sym][B]  1 if sgn(x) falsifies
-    // root splits (sym_item_kernel, S > 1): CTA (item, split) covers an even share of the item's roots and
-    // writes partials, summed in split order by sym_combine_kernel
+};
+
+// Root splits (sym_item_kernel, S > 1): CTA (item, split) covers an even share of the item's roots and writes
+// partials, summed in split order by sym_combine_kernel.  (A separate kernel argument: growing SymArgs changed
+// the code generated for sym_lane_kernel and slowed it by 40%.)
+template <typename T>
+struct SymSplit {
     int32_t S;
     int64_t s_end, lit0;         // the class's constraint end and first literal
     T* TbS;                      // [S][class literals][B]  w s_i (partial dFE/dl_i)
@@ -1322,14 +1250,14 @@ __device__ __forceinline__ void sym_roots(const T* cf, int m, int Mp, int lane, 
 // 4 warps per SM); R = 1: factors kept in registers; R = 2: two roots per pass.
 template <typename T, int NW, int C, int R>
 __global__ void __launch_bounds__(32 * NW, R == 0 ? (12 / NW > 0 ? 12 / NW : 1) : (NW >= 8 ? 1 : 8 / NW))
-sym_item_kernel(SymArgs<T> a, int64_t s_begin) {
+sym_item_kernel(SymArgs<T> a, SymSplit<T> sp, int64_t s_begin) {
     extern __shared__ __align__(16) unsigned char sym_smem[];   // the signature's root table, M' x 8 T
     __shared__ cplx<T> wtot[2][2][NW];   // [root-batch parity][root in batch][warp] chunk-product totals
     __shared__ int tcnt[NW];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int t = threadIdx.x;
-    const int64_t item = blockIdx.x / a.S;
-    const int split = (int)(blockIdx.x - item * a.S);
+    const int64_t item = blockIdx.x / sp.S;
+    const int split = (int)(blockIdx.x - item * sp.S);
     const bool valid = true;
     const int64_t s = s_begin + item / a.B;
     const int64_t b = item - (item / a.B) * a.B;
@@ -1337,7 +1265,7 @@ sym_item_kernel(SymArgs<T> a, int64_t s_begin) {
     const int k = sg.k;
     const int64_t lo = a.off[s];
     // this CTA's roots [m0, m0 + Mps) of the item's M' (an even share when split)
-    const int per = (sg.Mp + a.S - 1) / a.S;
+    const int per = (sg.Mp + sp.S - 1) / sp.S;
     const int m0 = min(sg.Mp, split * per);
     const int Mps = min(sg.Mp, m0 + per) - m0;
     const int i0 = t * C;
@@ -1380,24 +1308,24 @@ sym_item_kernel(SymArgs<T> a, int64_t s_begin) {
         sym_roots<T, NW, C, 1>(cf, m, Mps, lane, warp, t, l, term, fe_acc, wtot, al1, be1);
     }
     const T wc = a.w_sym[s];
-    if (a.S > 1) {   // partials of this root share; the unsat count by split 0
-        const int64_t nlit = a.off[a.s_end] - a.lit0;
+    if (sp.S > 1) {   // partials of this root share; the unsat count by split 0
+        const int64_t nlit = a.off[sp.s_end] - sp.lit0;
 #pragma unroll
         for (int j = 0; j < C; ++j) {
             const int i = i0 + j;
             if (i < k) {
                 const uint32_t w = __ldg(a.words + lo + i);
                 const T v = wc * term[j];
-                a.TbS[((int64_t)split * nlit + (lo - a.lit0) + i) * a.B + b] = (int)w < 0 ? -v : v;
+                sp.TbS[((int64_t)split * nlit + (lo - sp.lit0) + i) * a.B + b] = (int)w < 0 ? -v : v;
             }
         }
-        if (t == 0) a.fS[((int64_t)split * (a.s_end - s_begin) + (s - s_begin)) * a.B + b] = fe_acc;
+        if (t == 0) sp.fS[((int64_t)split * (sp.s_end - s_begin) + (s - s_begin)) * a.B + b] = fe_acc;
         if (split != 0) return;
     }
 #pragma unroll
     for (int j = 0; j < C; ++j) {
         const int i = i0 + j;
-        if (a.S == 1 && i < k) {
+        if (sp.S == 1 && i < k) {
             const uint32_t w = __ldg(a.words + lo + i);
             const T v = wc * term[j];
             a.Tb[(a.tb_fast + lo + i) * a.B + b] = (int)w < 0 ? -v : v;
@@ -1413,7 +1341,7 @@ sym_item_kernel(SymArgs<T> a, int64_t s_begin) {
         for (int w = 0; w < NW; ++w) tc += tcnt[w];
     }
     if (valid && t == 0) {
-        if (a.S == 1) a.fsym[s * a.B + b] = (double)wc * (sg.g0 + fe_acc);
+        if (sp.S == 1) a.fsym[s * a.B + b] = (double)wc * (sg.g0 + fe_acc);
         a.usym[s * a.B + b] = rule_sat(tc, sg.tmin, sg.tmax, sg.parity) ? 0 : 1;
     }
 }
@@ -1421,18 +1349,18 @@ sym_item_kernel(SymArgs<T> a, int64_t s_begin) {
 // Sum of the root-split partials of one class in split order (deterministic): the class's T rows and w (g0 +
 // Re sum_m G_m Q_m) per constraint.  Grid-stride over (class literal, point) then (class constraint, point).
 template <typename T>
-__global__ void __launch_bounds__(256) sym_combine_kernel(SymArgs<T> a, int64_t s_begin) {
-    const int64_t nlit = a.off[a.s_end] - a.lit0, ncons = a.s_end - s_begin;
+__global__ void __launch_bounds__(256) sym_combine_kernel(SymArgs<T> a, SymSplit<T> sp, int64_t s_begin) {
+    const int64_t nlit = a.off[sp.s_end] - sp.lit0, ncons = sp.s_end - s_begin;
     const int64_t nT = nlit * a.B, nF = ncons * a.B;
     for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < nT + nF; e += (int64_t)gridDim.x * blockDim.x) {
         if (e < nT) {
-            T v = a.TbS[e];
-            for (int sp = 1; sp < a.S; ++sp) v += a.TbS[(int64_t)sp * nT + e];
-            a.Tb[(a.tb_fast + a.lit0) * a.B + e] = v;
+            T v = sp.TbS[e];
+            for (int q = 1; q < sp.S; ++q) v += sp.TbS[(int64_t)q * nT + e];
+            a.Tb[(a.tb_fast + sp.lit0) * a.B + e] = v;
         } else {
             const int64_t f = e - nT;
-            double v = a.fS[f];
-            for (int sp = 1; sp < a.S; ++sp) v += a.fS[(int64_t)sp * nF + f];
+            double v = sp.fS[f];
+            for (int q = 1; q < sp.S; ++q) v += sp.fS[(int64_t)q * nF + f];
             const int64_t s = s_begin + f / a.B;
             const SymSigDev sg = a.sigs[a.sig_of[s]];
             a.fsym[s_begin * a.B + f] = (double)a.w_sym[s] * (sg.g0 + v);

@@ -2,5 +2,5 @@
 #include "sym_impl.cuh"
 
 namespace ffsat {
-template void launch_sym_class<float>(const SymClass&, const dev::SymArgs<float>&, cudaStream_t);
+template void launch_sym_class<float>(const SymClass&, const dev::SymArgs<float>&, const dev::SymSplit<float>&, cudaStream_t);
 }  // namespace ffsat

@@ -2,5 +2,5 @@
 #include "sym_impl.cuh"
 
 namespace ffsat {
-template void launch_sym_class<double>(const SymClass&, const dev::SymArgs<double>&, cudaStream_t);
+template void launch_sym_class<double>(const SymClass&, const dev::SymArgs<double>&, const dev::SymSplit<double>&, cudaStream_t);
 }  // namespace ffsat

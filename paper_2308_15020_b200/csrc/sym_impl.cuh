@@ -12,7 +12,7 @@ inline void set_sym_smem(const void* kern, size_t bytes) {
 
 // One root-path class launch: a CTA of G threads per (constraint, point) item, C literals per thread.
 template <typename T>
-void launch_sym_class(const SymClass& cl, const dev::SymArgs<T>& a, cudaStream_t st) {
+void launch_sym_class(const SymClass& cl, const dev::SymArgs<T>& a, const dev::SymSplit<T>& sp, cudaStream_t st) {
     const int64_t items = (cl.end - cl.begin) * a.B;
     if (items == 0) return;
     if (items > INT32_MAX) throw Error(FFSAT_ERR_ARG, "too many root-path items for one launch");
@@ -26,22 +26,22 @@ void launch_sym_class(const SymClass& cl, const dev::SymArgs<T>& a, cudaStream_t
         }
         return;
     }
-    // root splits: a.S CTAs per item, each staging its share of the root table
-    if ((int64_t)items * a.S > INT32_MAX) throw Error(FFSAT_ERR_ARG, "too many root-path CTAs for one launch");
-    const unsigned gs = (unsigned)(items * a.S);
-    const size_t smem = (size_t)((cl.max_mp + a.S - 1) / a.S) * 8 * sizeof(T);   // the largest root share
+    // root splits: sp.S CTAs per item, each staging its share of the root table
+    if ((int64_t)items * sp.S > INT32_MAX) throw Error(FFSAT_ERR_ARG, "too many root-path CTAs for one launch");
+    const unsigned gs = (unsigned)(items * sp.S);
+    const size_t smem = (size_t)((cl.max_mp + sp.S - 1) / sp.S) * 8 * sizeof(T);   // the largest root share
     switch (cl.G / 32 * 1000 + cl.C * 10 + cl.R) {
 #define FFSAT_SYM(NW, C) case NW * 1000 + C * 10 + 1: \
         set_sym_smem((const void*)dev::sym_item_kernel<T, NW, C, 1>, smem); \
-        dev::sym_item_kernel<T, NW, C, 1><<<gs, 32 * NW, smem, st>>>(a, cl.begin); break;
+        dev::sym_item_kernel<T, NW, C, 1><<<gs, 32 * NW, smem, st>>>(a, sp, cl.begin); break;
         FFSAT_SYM(1, 4) FFSAT_SYM(1, 8) FFSAT_SYM(1, 16) FFSAT_SYM(2, 12) FFSAT_SYM(2, 16)
         FFSAT_SYM(4, 10) FFSAT_SYM(3, 16) FFSAT_SYM(4, 14) FFSAT_SYM(4, 16) FFSAT_SYM(6, 16) FFSAT_SYM(8, 16)
 #undef FFSAT_SYM
     default: throw Error(FFSAT_ERR_ARG, "unsupported root-path launch class");
     }
-    if (a.S > 1) {
+    if (sp.S > 1) {
         const int64_t work = (cl.lit_end - cl.lit_begin + cl.end - cl.begin) * a.B;
-        dev::sym_combine_kernel<T><<<(unsigned)std::min<int64_t>(4 * 148, (work + 255) / 256), 256, 0, st>>>(a, cl.begin);
+        dev::sym_combine_kernel<T><<<(unsigned)std::min<int64_t>(4 * 148, (work + 255) / 256), 256, 0, st>>>(a, sp, cl.begin);
     }
 }
 
