@@ -396,3 +396,84 @@ def test_oracle_solve_semantics():
         assert np.all(st.x <= 1) and np.all(st.x >= -1)
         assert np.all(st.f <= prev + 1e-12)
         prev = st.f.copy()
+
+
+# ---- solve-loop pins written out by hand (rephase and the PGD eta schedule were unpinned)
+
+def _saddle_formula():
+    """f(x) = x1 x2 + x1/4 + x2/4: XOR(x1, x2) has FE = l1 l2 (t odd <=> l1 l2 = -1 at the corners, Thm. 1) and a
+    unit clause (x) has FE = x (OR with k = 1, 2 (1+x)/2 - 1), weighted 1/4 each (Def. 3)."""
+    return OracleFormula.from_constraints(2, [(XOR, 0, 1.0, [1, 2]), (OR, 0, 0.25, [1]), (OR, 0, 0.25, [2])])
+
+
+def test_pgd_eta_schedule_hand_derived():
+    """Alg. 4 in the monotone projected-Armijo reading (#16), worked by hand with dyadic
+    numbers (exact in fp64), under the formula's static weights.  From x = (0, 0): g = (x2 + 1/4, x1 + 1/4) = (1/4, 1/4), eta0 = 4, c1 = 1e-4.
+      1. x' = (-1, -1): f' = 1 - 1/2 = 1/2 > f + c1 <g, x'-x> = -5e-5          reject, eta 4 -> 2
+      2. x' = (-1/2, -1/2): f' = 1/4 - 1/4 = 0 > -2.5e-5                       reject, eta 2 -> 1
+      3. x' = (-1/4, -1/4): f' = 1/16 - 1/8 = -1/16 <= -1.25e-5                accept, eta -> min(2, 4) = 2
+      4. g(-1/4, -1/4) = (0, 0): x' = x, f' = f <= f + 0                       accept, eta -> 4
+    max_inner = 4 then marks the point done: a 5th iteration changes nothing.  With eta_min = 1.5 instead, the
+    second rejection leaves eta = 1 < eta_min and the point is done after iteration 2."""
+    F = _saddle_formula()
+    f0, g0 = cdp.evaluate(F, np.zeros((1, 2)))
+    assert f0[0] == 0.0 and np.array_equal(g0[0], [0.25, 0.25])
+    P = osolve.Params(eta0=4.0, max_inner=4, adaptive_weights=False)
+    st = osolve.State(x=np.zeros((1, 2)), f=None, g=None, eta=None, done=None, iters=None, w=F.weight.copy())
+    osolve.start_round(F, st, P)
+    want = [(False, 2.0, (0.0, 0.0), 0.0), (False, 1.0, (0.0, 0.0), 0.0), (True, 2.0, (-0.25, -0.25), -0.0625),
+            (True, 4.0, (-0.25, -0.25), -0.0625)]
+    for acc_w, eta_w, x_w, f_w in want:
+        _, _, _, acc = osolve.pgd_iteration(F, st, P)
+        assert bool(acc[0]) == acc_w and st.eta[0] == eta_w
+        assert np.array_equal(st.x[0], x_w) and st.f[0] == f_w
+    assert st.done[0] and st.iters[0] == 4
+    osolve.pgd_iteration(F, st, P)
+    assert st.eta[0] == 4.0 and np.array_equal(st.x[0], [-0.25, -0.25]) and st.iters[0] == 4
+    P2 = osolve.Params(eta0=4.0, eta_min=1.5, max_inner=100, adaptive_weights=False)
+    st = osolve.State(x=np.zeros((1, 2)), f=None, g=None, eta=None, done=None, iters=None, w=F.weight.copy())
+    osolve.start_round(F, st, P2)
+    osolve.pgd_iteration(F, st, P2)
+    assert not st.done[0] and st.eta[0] == 2.0
+    osolve.pgd_iteration(F, st, P2)
+    assert st.done[0] and st.eta[0] == 1.0
+    osolve.pgd_iteration(F, st, P2)
+    assert st.eta[0] == 1.0 and np.array_equal(st.x[0], [0.0, 0.0])
+
+
+def test_pgd_projection_arc_armijo():
+    """The sufficient-decrease test uses the PROJECTED step x' - x (the projection arc), not -eta g: from x = (-1, 1)
+    on f = x1 x2 + x1/4 + x2/4, g = (5/4, -3/4); eta = 1 gives x - g = (-9/4, 7/4), clipped to (-1, 1) = x itself, so
+    x' - x = 0, f' = f and the step is accepted with eta -> min(2, eta0) (with -eta g it would need f' <= f - 2.125e-4
+    and be rejected)."""
+    F = _saddle_formula()
+    P = osolve.Params(eta0=1.0, max_inner=10, adaptive_weights=False)
+    st = osolve.State(x=np.array([[-1.0, 1.0]]), f=None, g=None, eta=None, done=None, iters=None, w=F.weight.copy())
+    osolve.start_round(F, st, P)
+    assert np.array_equal(st.g[0], [1.25, -0.75]) and st.f[0] == -1.0
+    xp, fp, _, acc = osolve.pgd_iteration(F, st, P)
+    assert np.array_equal(xp[0], [-1.0, 1.0]) and fp[0] == -1.0 and bool(acc[0]) and st.eta[0] == 1.0
+
+
+def test_rephase_phases_hand_derived():
+    """O / F / R of P:611-615 in the (ROF)^inf cycle, staggered by global point index (reading #20): at new
+    round r the point with global index b takes phase "ROF"[(r - 1 + b) mod 3] -- O keeps x, F is exactly -x, R is a
+    fresh uniform draw of the stream (seed, b, r) (Alg. 1 line 1's sampler, keyed by the NEW round)."""
+    n, seed = 6, 31
+    x = np.array([[0.5, -0.25, 0.125, -1.0, 1.0, 0.0]] * 6) * np.arange(1, 7)[:, None] / 6
+    P = osolve.Params(policy="ROF")
+    # point0 = 0, round 1: b = 0 R, 1 O, 2 F, 3 R, 4 O, 5 F
+    y = osolve.rephase(x, seed, 0, 1, P)
+    assert np.array_equal(y[1], x[1]) and np.array_equal(y[4], x[4])
+    assert np.array_equal(y[2], -x[2]) and np.array_equal(y[5], -x[5])
+    assert np.array_equal(y[0], uniform_pm1(seed, 0, 1, n)) and np.array_equal(y[3], uniform_pm1(seed, 3, 1, n))
+    assert not np.array_equal(y[0], uniform_pm1(seed, 0, 0, n))          # the new round's stream, not round 0's
+    # point0 = 5, round 2: global b = 5..10, (1 + b) mod 3 = 0, 1, 2, 0, 1, 2 -> R O F R O F
+    y = osolve.rephase(x, seed, 5, 2, P)
+    assert np.array_equal(y[0], uniform_pm1(seed, 5, 2, n)) and np.array_equal(y[3], uniform_pm1(seed, 8, 2, n))
+    assert np.array_equal(y[1], x[1]) and np.array_equal(y[2], -x[2]) and np.array_equal(y[5], -x[5])
+    # (RF)^inf (P:1153): b even -> R at odd rounds; R only: every point redrawn
+    y = osolve.rephase(x, seed, 0, 1, osolve.Params(policy="RF"))
+    assert np.array_equal(y[0], uniform_pm1(seed, 0, 1, n)) and np.array_equal(y[1], -x[1])
+    y = osolve.rephase(x, seed, 0, 3, osolve.Params(policy="R"))
+    assert all(np.array_equal(y[i], uniform_pm1(seed, i, 3, n)) for i in range(6))
