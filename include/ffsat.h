@@ -83,7 +83,12 @@ typedef struct {
     int32_t device;     /* CUDA device ordinal; -1 = host-only context (no GPU needed) */
     int32_t path;       /* 0 = auto, 1 = force on-chip tiled fast path (64-point kernel when eligible),
                            2 = force global path, 3 = tiled path with the 32-point kernel only */
-    int32_t reserved;
+    int32_t batch_ref;  /* reference batch of the launch plan, 0 = 1024.  The fast kernels' split of the
+                           constraints into chunks (and so every partial sum) is planned once, at load, for
+                           this batch size and reused for every call: a point's f / grad / unsat bits do not
+                           depend on the batch it is evaluated in (restart sharding over any number of GPUs
+                           reproduces the single-GPU trajectories, F7).  Set it to the batch you
+                           evaluate for best throughput (a much smaller batch than batch_ref underfills the GPU). */
 } ffsat_options;
 
 typedef struct {
@@ -121,8 +126,9 @@ ffsat_status ffsat_export(const ffsat_ctx* ctx, uint8_t* kind, int32_t* bound, d
  * Host buffers (on_device = 0) are staged in 2-4 equal chunks (B >= 512) whose H2D / D2H copies overlap
  * the chunk evaluations; pinned host memory is needed for the overlap (pageable memory still works).
  * The call returns when the outputs are in host memory.  Device buffers (on_device = 1) are asynchronous
- * on `stream`.  Limit: a formula with fast constraints of length 16 < k <= 64 on the global (large-n)
- * path needs n * B < 2^32 (FFSAT_ERR_ARG otherwise; split the batch). */
+ * on `stream`.  B = 0 is a no-op.  Results per point do not depend on B or on the point's position in the
+ * batch (the launch plan is batch-independent, ffsat_options.batch_ref): host and device buffers give the same
+ * bits. */
 ffsat_status ffsat_eval(ffsat_ctx* ctx, const void* x, int64_t B, int32_t on_device, double* f_out,
                         void* grad_out, int32_t* unsat_out, void* stream);
 
@@ -152,19 +158,27 @@ typedef struct {
     int64_t round;           /* restart rounds completed */
     int64_t iterations;      /* PGD iterations issued in the current round */
     int64_t active;          /* points not yet converged in the current round */
-    int64_t solved_point;    /* lowest global point index whose trial sgn(x) satisfied every constraint, -1 none */
+    int64_t solved_point;    /* lowest global point index whose trial or checked sgn(x) satisfied every constraint, -1 none */
     int64_t best_unsat;      /* minimum falsified count over points at the last check */
     int64_t best_point;      /* global index achieving best_unsat */
 } ffsat_search_stats;
 
-typedef struct {             /* device pointers owned by the search (for collectives and tests) */
+/* Device pointers owned by the search (for collectives and tests).  Per-constraint arrays (U, weights) are in the
+ * library's POSITION order, not the input order of the formula: position p holds input constraint order[p], where
+ * order is the map ffsat_layout_units returns (a permutation of 0..n_cons-1).  ffsat_search_restart expects a
+ * U_global in the same position order (e.g. the element-wise SUM of every rank's U: all ranks share one layout). */
+typedef struct {
     void* x;                 /* [B][n] accepted points */
     void* grad;              /* [B][n] gradient at x */
     double* f;               /* [B] f at x */
     double* eta;             /* [B] */
     int32_t* unsat;          /* [B] falsified count of sgn(x) at the last check */
-    int32_t* U;              /* [n_cons] per-constraint falsified count over this batch at the last check */
-    void* weights;           /* [n_cons] current weights (context dtype, context order) */
+    int32_t* U;              /* [n_cons] per-constraint falsified count over this batch at the last check (position order) */
+    void* weights;           /* [n_cons] this search's current weights (context dtype, position order) */
+    int64_t* keys;           /* [2] written by ffsat_search_reduce, MIN-reducible across ranks as they stand:
+                                keys[0] = lowest GLOBAL point index whose solved flag is set, INT64_MAX if none;
+                                keys[1] = (falsified count of sgn(x) at the last check << 32) | global point, minimised */
+    int32_t* solved;         /* [B] 1 once a trial point or a checked point's sgn(x) satisfied every constraint */
 } ffsat_search_buffers;
 
 ffsat_status ffsat_search_create(ffsat_ctx* ctx, int64_t batch, int64_t point0, uint64_t seed,
@@ -175,11 +189,17 @@ ffsat_status ffsat_search_set_x(ffsat_search* s, const void* x, int32_t on_devic
 ffsat_status ffsat_search_begin_round(ffsat_search* s, void* stream);
 /* n PGD iterations (one batched f + grad evaluation each), enqueued on stream. */
 ffsat_status ffsat_search_iterate(ffsat_search* s, int32_t n_iters, void* stream);
-/* Check sgn(x) of every point: unsat[b], U[c] (over this batch) on device. */
+/* Check sgn(x) of every point: unsat[b], U[c] (over this batch, position order) on device; a point with unsat 0 is
+ * marked solved and its assignment kept (ffsat_search_assignment), so a later restart cannot lose it. */
 ffsat_status ffsat_search_check(ffsat_search* s, void* stream);
-/* End the round: ERWA update with U_global (device int32 [n_cons]; NULL = this batch's U) when
- * adaptive, then rephase every point (policy offset = global point index, #20). */
+/* Reduce this batch's state into the device keys of ffsat_search_buffers (asynchronous on stream): the any-solved
+ * key and the incumbent key, both in global point indices (point0 + local index).  Restart sharding MIN-all-reduces
+ * them over ranks (C1, C4 of DESIGN.md section 6) without any host round trip. */
+ffsat_status ffsat_search_reduce(ffsat_search* s, void* stream);
+/* End the round: ERWA update of this search's weights with U_global (device int32 [n_cons], POSITION order; NULL =
+ * this batch's U) when adaptive, then rephase every point (policy offset = global point index, #20). */
 ffsat_status ffsat_search_restart(ffsat_search* s, const int32_t* U_global, void* stream);
+/* ffsat_search_reduce + a synchronous read: solved_point / best_point are global point indices. */
 ffsat_status ffsat_search_stats_get(ffsat_search* s, void* stream, ffsat_search_stats* out);
 ffsat_status ffsat_search_get_buffers(ffsat_search* s, ffsat_search_buffers* out);
 /* Assignment (-1 True / +1 False) of a local point: the solved trial assignment if that point

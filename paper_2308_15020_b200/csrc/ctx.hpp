@@ -83,6 +83,15 @@ void launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cu
 
 #define FFSAT_SIDE_STREAMS 8
 
+namespace ffsat {
+// Per-batch scratch of one evaluation stream: the context's own ffsat_eval calls use ctx->scr, every search owns
+// one (so a search's captured CUDA graph never references buffers another call may resize).
+struct Scratch {
+    DBuf xT, Tb, P, fpart, upart, fsym, usym, TbS, fS;
+    int64_t B = -1;
+};
+}  // namespace ffsat
+
 struct ffsat_ctx {
     ffsat::Formula F;
     ffsat::Layout Lo;
@@ -94,14 +103,21 @@ struct ffsat_ctx {
     ffsat::DBuf fast_words, tiled_words, units, buckets, sym_words, sym_off, sym_sig, sigs, coef, occ_off, occ_slot,
         w_pos, w_static_orig, order, chk_off, chk_words, chk_rule;
     int64_t persistent_bytes = 0;
-    // per-B scratch
-    ffsat::DBuf xT, Tb, P, fpart, upart, fsym, usym, chunk_units, x_stage, g_stage, f_stage, u_stage, w_stage;
-    // root splits (plan): effective S per root-path class and its regions of the split partial buffers
-    ffsat::DBuf TbS, fS;                 // [S][class literals][B] terms, [S][class constraints][B] Re sum G Q
+    // the batch-independent launch plan (plan_chunks, at load): chunk split of the fast kernels and root splits.
+    // It depends on the formula and on batch_ref only -- never on the B of a call -- so every point's f / grad
+    // bits are the same whatever batch it is evaluated in (restart sharding over any number of GPUs, F7).
+    int64_t batch_ref = 1024;
+    ffsat::DBuf chunk_units;
+    // root splits: effective S per root-path class and its regions of the split partial buffers
+    // (TbS: [S][class literals][B] terms, fS: [S][class constraints][B] Re sum G Q)
     std::vector<int32_t> sym_S;
     std::vector<int64_t> sym_offT, sym_offF;
-    int64_t plan_B = -1;
+    int64_t sym_totT = 0, sym_totF = 0;   // per point
     int32_t n_chunks = 0;
+    int32_t f_groups = 8;                 // interleaved groups of the fixed-order f / unsat reduction (8 or 32)
+    // scratch of the context's own evaluations; host-buffer staging
+    ffsat::Scratch scr;
+    ffsat::DBuf x_stage, g_stage, f_stage, u_stage, w_stage;
     // global path: chunk groups by bucket length class -- chunks [gchunk[g], gchunk[g + 1]) hold the units with
     // k <= 4 (g = 0), 4 < k <= 16 (g = 1), 16 < k (g = 2, the long kernel); each group is one launch
     int32_t gchunk[4] = {0, 0, 0, 0};
@@ -143,13 +159,16 @@ struct ffsat_ctx {
 
 namespace ffsat {
 
-// Size the per-batch scratch and the chunk split of the fast kernels for batch B (eval.cu).
-void plan(ffsat_ctx* c, int64_t B);
-// f (fp64), grad (T, may be null), unsat (int32, may be null) at device points x [B][n]; async on st
-// (eval_f32.cu / eval_f64.cu).  profiled: record c->ev[0..4] around the phases.
+// The batch-independent launch plan (eval.cu): chunk split of the fast kernels for the reference batch
+// c->batch_ref, root splits, kernel shared-memory attributes.  Once, at load.
+void plan_chunks(ffsat_ctx* c);
+// Size scratch S for batch B (synchronous allocations: never inside a stream capture).
+void ensure_scratch(const ffsat_ctx* c, Scratch& S, int64_t B);
+// f (fp64), grad (T, may be null), unsat (int32, may be null) at device points x [B][n] under weights w_pos (position
+// order); async on st, scratch S (eval_f32.cu / eval_f64.cu).  profiled: record c->ev[0..4] around the phases.
 template <typename T>
-void eval_device_t(ffsat_ctx* c, const T* x, int64_t B, double* f, T* grad, int32_t* unsat, const T* w_pos, cudaStream_t st,
-                   bool profiled);
+void eval_device_t(ffsat_ctx* c, Scratch& S, const T* x, int64_t B, double* f, T* grad, int32_t* unsat, const T* w_pos,
+                   cudaStream_t st, bool profiled);
 // allow the tiled kernels of dtype T the dynamic shared memory they need (eval_f32.cu / eval_f64.cu)
 template <typename T>
 void set_tiled_smem(size_t bytes);

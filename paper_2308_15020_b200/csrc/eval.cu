@@ -1,4 +1,5 @@
-// eval.cu -- batch planning of ffsat_eval (chunk split of the fast kernels, scratch sizing).
+// eval.cu -- launch planning of ffsat_eval: the batch-independent chunk split of the fast kernels (at load) and the
+// per-batch scratch sizing.
 #include <algorithm>
 #include <cstdlib>
 
@@ -34,10 +35,9 @@ int pick_chunks(int64_t point_tiles, int ctas_per_sm, int num_sm, int64_t n_unit
 
 }  // namespace
 
-void plan(ffsat_ctx* c, int64_t B) {
-    if (c->plan_B == B) return;
+void plan_chunks(ffsat_ctx* c) {
     const Layout& L = c->Lo;
-    const size_t es = c->esize;
+    const int64_t B = std::max<int64_t>(1, c->batch_ref);   // the reference batch: the split never sees a call's B
     const int64_t PT = L.wide ? (B + 63) / 64 : (B + 31) / 32;
     int cps = 8;
     if (L.path == 1) {
@@ -68,8 +68,6 @@ void plan(ffsat_ctx* c, int64_t B) {
         ncg[1] = pick_chunks(PT, gcps, c->num_sm, ug[2] - ug[1]);
         ncg[2] = pick_chunks(PT, 6, c->num_sm, ug[3] - ug[2]);   // long kernel: 32 KB smem per CTA
     }
-    if (ncg[2] > 0 && (uint64_t)L.n * (uint64_t)B >= (1ull << 32))
-        throw Error(FFSAT_ERR_ARG, "batch too large for the long-constraint kernel (n * B must be < 2^32; split the batch)");
     c->gchunk[0] = 0;
     for (int g = 0; g < 3; ++g) c->gchunk[g + 1] = c->gchunk[g] + ncg[g];
     c->n_chunks = c->gchunk[3];
@@ -90,36 +88,33 @@ void plan(ffsat_ctx* c, int64_t B) {
     for (int g = 0; g < 3; ++g)
         if (ncg[g] > 0) split(ug[g], ug[g + 1], ncg[g], c->gchunk[g]);
     upload(c->chunk_units, cu);
-    const int64_t parts = std::max<int64_t>(1, c->n_chunks);
-    if (L.path == 1) c->P.ensure(std::max<size_t>(16, (size_t)c->n_chunks * L.n * B * es));
-    if (L.path == 2 || L.sym_lane) c->xT.ensure(std::max<size_t>(16, (size_t)L.n * B * es));
-    c->Tb.ensure(std::max<size_t>(16, (size_t)L.tb_slots * B * es));
-    c->fpart.ensure((size_t)parts * B * 8);
-    c->upart.ensure((size_t)parts * B * 4);
-    c->fsym.ensure(std::max<size_t>(16, (size_t)L.n_sym * B * 8));
-    {   // root splits: per-class partial regions (fall back to S = 1 if they would exceed 4 GiB)
+    // the fixed f / unsat summation order: rows r = 0 .. R-1 (fast partials, then root-path constraints) summed in
+    // f_groups interleaved groups (r mod f_groups), ascending inside a group, groups in order -- the same order in
+    // reduce_f_kernel and in the gradient reduction's fused variant, for every batch size
+    const int64_t rows = (L.n_fast > 0 ? c->n_chunks : 0) + L.n_sym;
+    c->f_groups = rows > 256 ? 32 : 8;
+    {   // root splits: per-class partial regions (S = 1 everywhere if they would exceed 4 GiB at the reference batch)
         const size_t ncl = L.sym_classes.size();
         c->sym_S.assign(ncl, 1);
         c->sym_offT.assign(ncl, 0);
         c->sym_offF.assign(ncl, 0);
-        size_t tT = 0, tF = 0;
+        int64_t tT = 0, tF = 0;
         for (size_t i = 0; i < ncl; ++i) {
             const SymClass& cl = L.sym_classes[i];
             if (cl.S <= 1) continue;
             c->sym_S[i] = cl.S;
-            c->sym_offT[i] = (int64_t)tT;
-            c->sym_offF[i] = (int64_t)tF;
-            tT += (size_t)cl.S * (size_t)(cl.lit_end - cl.lit_begin) * (size_t)B;
-            tF += (size_t)cl.S * (size_t)(cl.end - cl.begin) * (size_t)B;
+            c->sym_offT[i] = tT;
+            c->sym_offF[i] = tF;
+            tT += (int64_t)cl.S * (cl.lit_end - cl.lit_begin);
+            tF += (int64_t)cl.S * (cl.end - cl.begin);
         }
-        if (tT * es + tF * 8 > (size_t)4 << 30) {
+        if ((size_t)(tT * (int64_t)c->esize + tF * 8) * (size_t)B > (size_t)4 << 30) {
             c->sym_S.assign(ncl, 1);
             tT = tF = 0;
         }
-        c->TbS.ensure(std::max<size_t>(16, tT * es));
-        c->fS.ensure(std::max<size_t>(16, tF * 8));
+        c->sym_totT = tT;
+        c->sym_totF = tF;
     }
-    c->usym.ensure(std::max<size_t>(16, (size_t)L.n_sym * B * 4));
     if (L.path == 1) {
         if (L.precision == 64) set_tiled_smem<double>(c->tiled_smem);
         else set_tiled_smem<float>(c->tiled_smem);
@@ -129,7 +124,23 @@ void plan(ffsat_ctx* c, int64_t B) {
         if (L.precision == 64) set_long_smem<double>();
         else set_long_smem<float>();
     }
-    c->plan_B = B;
+}
+
+void ensure_scratch(const ffsat_ctx* c, Scratch& S, int64_t B) {
+    if (S.B >= B) return;   // buffers sized for a larger batch serve every smaller one (row strides are the call's B)
+    const Layout& L = c->Lo;
+    const size_t es = c->esize, b = (size_t)B;
+    const size_t parts = (size_t)std::max<int64_t>(1, c->n_chunks);
+    if (L.path == 1) S.P.ensure(std::max<size_t>(16, parts * L.n * b * es));
+    if (L.path == 2 || L.sym_lane) S.xT.ensure(std::max<size_t>(16, (size_t)L.n * b * es));
+    S.Tb.ensure(std::max<size_t>(16, (size_t)L.tb_slots * b * es));
+    S.fpart.ensure(parts * b * 8);
+    S.upart.ensure(parts * b * 4);
+    S.fsym.ensure(std::max<size_t>(16, (size_t)L.n_sym * b * 8));
+    S.usym.ensure(std::max<size_t>(16, (size_t)L.n_sym * b * 4));
+    S.TbS.ensure(std::max<size_t>(16, (size_t)c->sym_totT * b * es));
+    S.fS.ensure(std::max<size_t>(16, (size_t)c->sym_totF * b * 8));
+    S.B = B;
 }
 
 

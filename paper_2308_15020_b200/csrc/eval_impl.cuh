@@ -58,11 +58,11 @@ inline int fast_kmax_short(const Layout& L) {
 
 // f (fp64), grad (T, may be null), unsat (int32, may be null) at device points x [B][n]; async on st.
 template <typename T>
-void eval_device_t(ffsat_ctx* c, const T* x, int64_t B, double* f, T* grad, int32_t* unsat, const T* w_pos, cudaStream_t st,
-                   bool profiled) {
+void eval_device_t(ffsat_ctx* c, Scratch& S, const T* x, int64_t B, double* f, T* grad, int32_t* unsat, const T* w_pos,
+                   cudaStream_t st, bool profiled) {
     const Layout& L = c->Lo;
     if (B == 0) return;
-    plan(c, B);
+    ensure_scratch(c, S, B);
     const int64_t PT = (B + 31) / 32;
     auto mark = [&](int i) {
         if (profiled) CK(cudaEventRecord(c->ev[i], st));
@@ -72,7 +72,7 @@ void eval_device_t(ffsat_ctx* c, const T* x, int64_t B, double* f, T* grad, int3
     const bool need_xT = L.path == 2 || L.sym_lane;
     if (need_xT && L.n > 0) {
         dim3 tg(blocks_for(L.n, 32), blocks_for(B, 32)), tb(32, 8);
-        dev::transpose_kernel<T><<<tg, tb, 0, st>>>(x, c->xT.as<T>(), B, L.n);
+        dev::transpose_kernel<T><<<tg, tb, 0, st>>>(x, S.xT.as<T>(), B, L.n);
         c->launches += 1;
     }
     // root-path classes are independent of the fast kernel (disjoint outputs): off the profiling path they
@@ -83,7 +83,7 @@ void eval_device_t(ffsat_ctx* c, const T* x, int64_t B, double* f, T* grad, int3
         a.x = x; a.sb = L.n; a.sv = 1; a.B = B;
         a.words = c->sym_words.as<uint32_t>(); a.off = c->sym_off.as<int64_t>(); a.sig_of = c->sym_sig.as<int32_t>();
         a.sigs = c->sigs.as<dev::SymSigDev>(); a.coef = c->coef.as<T>(); a.w_sym = w_pos + L.n_fast;
-        a.tb_fast = L.tb_fast; a.Tb = c->Tb.as<T>(); a.fsym = c->fsym.as<double>(); a.usym = c->usym.as<int32_t>();
+        a.tb_fast = L.tb_fast; a.Tb = S.Tb.as<T>(); a.fsym = S.fsym.as<double>(); a.usym = S.usym.as<int32_t>();
         const size_t ncl = L.sym_classes.size();
         const bool fork = ncl > 1 || (!profiled && L.n_fast > 0);
         if (fork) {
@@ -91,7 +91,7 @@ void eval_device_t(ffsat_ctx* c, const T* x, int64_t B, double* f, T* grad, int3
             CK(cudaEventRecord(c->ev_fork, st));
         }
         dev::SymArgs<T> aT = a;    // thread-per-item classes read x^T
-        aT.x = c->xT.as<T>(); aT.sb = 1; aT.sv = B;
+        aT.x = S.xT.as<T>(); aT.sb = 1; aT.sv = B;
         for (size_t i = 0; i < ncl; ++i) {
             cudaStream_t ss = fork ? c->side[i % FFSAT_SIDE_STREAMS] : st;
             if (fork && i < FFSAT_SIDE_STREAMS) CK(cudaStreamWaitEvent(ss, c->ev_fork, 0));
@@ -100,8 +100,8 @@ void eval_device_t(ffsat_ctx* c, const T* x, int64_t B, double* f, T* grad, int3
             sp.S = c->sym_S[i];
             sp.s_end = cl.end;
             sp.lit0 = cl.lit_begin;
-            sp.TbS = c->TbS.as<T>() + c->sym_offT[i];
-            sp.fS = c->fS.as<double>() + c->sym_offF[i];
+            sp.TbS = S.TbS.as<T>() + c->sym_offT[i] * B;
+            sp.fS = S.fS.as<double>() + c->sym_offF[i] * B;
             launch_sym_class<T>(cl, cl.G == 0 ? aT : a, sp, ss);
             c->launches += sp.S > 1 ? 2 : 1;   // + the split combine
         }
@@ -128,7 +128,7 @@ void eval_device_t(ffsat_ctx* c, const T* x, int64_t B, double* f, T* grad, int3
             a.x = x; a.B = B; a.n = L.n;
             a.words = c->tiled_words.as<uint32_t>(); a.units = c->units.as<dev::UnitDev>();
             a.buckets = c->buckets.as<dev::FastBucketDev>(); a.chunk_units = c->chunk_units.as<int32_t>(); a.w_pos = w_pos;
-            a.P = c->P.as<T>(); a.fpart = c->fpart.as<double>(); a.upart = c->upart.as<int32_t>();
+            a.P = S.P.as<T>(); a.fpart = S.fpart.as<double>(); a.upart = S.upart.as<int32_t>();
             dim3 grid((unsigned)PT, (unsigned)c->n_chunks);
             const int km = fast_kmax(L);
             const int ku = uniform_k(L);
@@ -145,10 +145,10 @@ void eval_device_t(ffsat_ctx* c, const T* x, int64_t B, double* f, T* grad, int3
         } else {
             // chunk groups (plan): k <= 4, 4 < k <= 16 (each with its own register bound), k > 16 (long kernel)
             dev::GlobalArgs<T> a{};
-            a.xT = c->xT.as<T>(); a.B = B; a.n = L.n; a.words = c->fast_words.as<uint32_t>();
+            a.xT = S.xT.as<T>(); a.B = B; a.n = L.n; a.words = c->fast_words.as<uint32_t>();
             a.units = c->units.as<dev::UnitDev>(); a.buckets = c->buckets.as<dev::FastBucketDev>();
-            a.chunk_units = c->chunk_units.as<int32_t>(); a.w_pos = w_pos; a.Tb = c->Tb.as<T>();
-            a.fpart = c->fpart.as<double>(); a.upart = c->upart.as<int32_t>();
+            a.chunk_units = c->chunk_units.as<int32_t>(); a.w_pos = w_pos; a.Tb = S.Tb.as<T>();
+            a.fpart = S.fpart.as<double>(); a.upart = S.upart.as<int32_t>();
             // several groups: off the profiling path groups 1, 2 run on side streams, concurrently with group 0
             // (disjoint chunks, T slots and partial rows); joined with the root-path classes below
             int ngroups = 0;
@@ -192,16 +192,16 @@ void eval_device_t(ffsat_ctx* c, const T* x, int64_t B, double* f, T* grad, int3
     mark(2);
     dev::ReduceFArgs rf{};
     rf.B = B; rf.n_parts = L.n_fast > 0 ? c->n_chunks : 0; rf.n_sym = L.n_sym;
-    rf.fpart = c->fpart.as<double>(); rf.upart = c->upart.as<int32_t>(); rf.fsym = c->fsym.as<double>();
-    rf.usym = c->usym.as<int32_t>(); rf.f = f; rf.unsat = unsat;
+    rf.fpart = S.fpart.as<double>(); rf.upart = S.upart.as<int32_t>(); rf.fsym = S.fsym.as<double>();
+    rf.usym = S.usym.as<int32_t>(); rf.f = f; rf.unsat = unsat;
     // tiled path with a gradient: the f / unsat reduction rides in the gradient reduction (variable tile 0), one
     // launch fewer per evaluation; the profiled path keeps them apart so the phases can be timed separately, and
     // the global path keeps them apart (its HBM-bound reduction measured slower with the fused variant, c5)
-    const bool fuse = grad && L.n > 0 && !profiled && L.path == 1;
+    const bool fuse = grad && L.n > 0 && !profiled && L.path == 1 && c->f_groups == 8;
     if (grad) {
         c->launches += 1;
         dev::ReduceArgs<T> r{};
-        r.B = B; r.n = L.n; r.n_chunks = L.path == 1 ? c->n_chunks : 0; r.P = c->P.as<T>(); r.Tb = c->Tb.as<T>();
+        r.B = B; r.n = L.n; r.n_chunks = L.path == 1 ? c->n_chunks : 0; r.P = S.P.as<T>(); r.Tb = S.Tb.as<T>();
         r.occ_off = c->occ_off.as<int64_t>(); r.occ_slot = c->occ_slot.as<int32_t>(); r.grad = grad;
         r.rf = rf;
         dim3 grid(blocks_for(L.n, 8), blocks_for(B, 32)), blk(32, 8);
@@ -212,7 +212,8 @@ void eval_device_t(ffsat_ctx* c, const T* x, int64_t B, double* f, T* grad, int3
     mark(3);
     if (!fuse) {
         c->launches += 1;
-        if (B <= 32 * 64) dev::reduce_f_kernel<32><<<blocks_for(B, 32), 1024, 0, st>>>(rf);
+        // one warp per interleaved group: the same summation order as the fused variant for every batch size
+        if (c->f_groups == 32) dev::reduce_f_kernel<32><<<blocks_for(B, 32), 1024, 0, st>>>(rf);
         else dev::reduce_f_kernel<8><<<blocks_for(B, 32), 256, 0, st>>>(rf);
     }
     CK(cudaGetLastError());

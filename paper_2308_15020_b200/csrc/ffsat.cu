@@ -35,6 +35,8 @@ struct ffsat_search {
     uint64_t seed = 0;
     ffsat_solve_params P{};
     DBuf X, Xp, Gx, Gp, fX, fP, dot, eta, done, iters, unsatP, solved, sol, unsat, U, stats, xT;
+    DBuf W;                       // this search's current weights (position order, context dtype): ERWA state
+    Scratch sc;                   // this search's evaluation scratch (referenced by its captured graph)
     int64_t round = 0, iters_issued = 0;
     // one CLS iteration captured as a CUDA graph (replayed by ffsat_search_iterate)
     cudaStream_t cap_stream = nullptr;
@@ -139,11 +141,13 @@ void upload_layout(ffsat_ctx* c) {
 ffsat_ctx* make_ctx(Formula&& F, const ffsat_options* opt) {
     ffsat_options o{0, 0, 0, 0};
     if (opt) o = *opt;
+    if (o.batch_ref < 0) throw Error(FFSAT_ERR_ARG, "batch_ref must be >= 0");
     validate(F);
     std::unique_ptr<ffsat_ctx> c(new ffsat_ctx());
     c->F = std::move(F);
     c->Lo = build_layout(c->F, o.path, o.precision);
     c->device = o.device;
+    c->batch_ref = o.batch_ref > 0 ? o.batch_ref : 1024;
     if (o.device >= 0) {
         int ndev = 0;
         cudaError_t e = cudaGetDeviceCount(&ndev);
@@ -155,6 +159,7 @@ ffsat_ctx* make_ctx(Formula&& F, const ffsat_options* opt) {
         CK(cudaSetDevice(o.device));
         CK(cudaDeviceGetAttribute(&c->num_sm, cudaDevAttrMultiProcessorCount, o.device));
         upload_layout(c.get());
+        plan_chunks(c.get());
     }
     return c.release();
 }
@@ -170,9 +175,9 @@ void need_device(const ffsat_ctx* c) {
 void eval_device(ffsat_ctx* c, const void* x, int64_t B, double* f, void* grad, int32_t* unsat, cudaStream_t st,
                  bool profiled = false) {
     if (c->Lo.precision == 64)
-        eval_device_t<double>(c, (const double*)x, B, f, (double*)grad, unsat, c->w_pos.as<double>(), st, profiled);
+        eval_device_t<double>(c, c->scr, (const double*)x, B, f, (double*)grad, unsat, c->w_pos.as<double>(), st, profiled);
     else
-        eval_device_t<float>(c, (const float*)x, B, f, (float*)grad, unsat, c->w_pos.as<float>(), st, profiled);
+        eval_device_t<float>(c, c->scr, (const float*)x, B, f, (float*)grad, unsat, c->w_pos.as<float>(), st, profiled);
 }
 
 ffsat_status fail(ffsat_ctx* c, const Error& e) {
@@ -220,7 +225,7 @@ int64_t exact_unsat(const Formula& F, const int8_t* a, double* fw) {
 
 template <typename T>
 void search_eval(ffsat_search* s, const void* x, double* f, void* g, int32_t* u, cudaStream_t st) {
-    eval_device_t<T>(s->ctx, (const T*)x, s->B, f, (T*)g, u, s->ctx->w_pos.as<T>(), st, false);
+    eval_device_t<T>(s->ctx, s->sc, (const T*)x, s->B, f, (T*)g, u, s->W.as<T>(), st, false);
 }
 
 void search_alloc(ffsat_search* s) {
@@ -231,7 +236,9 @@ void search_alloc(ffsat_search* s) {
     for (DBuf* d : {&s->done, &s->iters, &s->unsatP, &s->solved, &s->unsat}) d->ensure((size_t)B * 4);
     s->sol.ensure(std::max<size_t>(16, Bn));
     s->U.ensure(std::max<size_t>(16, (size_t)m * 4));
+    s->W.ensure(std::max<size_t>(16, (size_t)m * es));
     s->stats.ensure(64);
+    ensure_scratch(s->ctx, s->sc, B);
     CK(cudaMemset(s->solved.p, 0, (size_t)B * 4));
     CK(cudaMemset(s->unsat.p, 0, (size_t)B * 4));
     CK(cudaMemset(s->U.p, 0, (size_t)std::max<int64_t>(m, 4) * 4));
@@ -270,7 +277,9 @@ bool search_capture(ffsat_search* s) {
     if (s->iter_exec) return true;
     if (s->graph_failed) return false;
     if (!s->cap_stream) CK(cudaStreamCreateWithFlags(&s->cap_stream, cudaStreamNonBlocking));
-    plan(s->ctx, s->B);                  // scratch sizing / uploads are synchronous: never inside a capture
+    // the graph references only this search's buffers (sized at create: allocations never happen inside a
+    // capture) and the context's persistent layout, which is never reallocated after load
+    ensure_scratch(s->ctx, s->sc, s->B);
     s->ctx->ensure_side_streams();
     const int64_t before = s->ctx->launches, iters_before = s->iters_issued;
     cudaGraph_t g = nullptr;
@@ -328,11 +337,23 @@ void search_iterate_direct(ffsat_search* s, int n_iters, cudaStream_t st) {
     s->iters_issued += n_iters;
 }
 
+void check_kernels(ffsat_search* s, cudaStream_t st);
+
 void search_check(ffsat_search* s, cudaStream_t st) {
     ffsat_ctx* c = s->ctx;
     const Layout& L = c->Lo;
     CK(cudaMemsetAsync(s->unsat.p, 0, (size_t)s->B * 4, st));
-    if (L.m == 0) return;
+    if (L.m > 0) check_kernels(s, st);
+    // points whose sgn(x) satisfies every constraint are solved (kept in sol, so a later restart cannot lose them)
+    if (L.precision == 64) dev::mark_solved_kernel<double><<<(unsigned)s->B, 128, 0, st>>>(s->X.as<double>(), s->unsat.as<int32_t>(), s->solved.as<int32_t>(), s->sol.as<int8_t>(), L.n);
+    else dev::mark_solved_kernel<float><<<(unsigned)s->B, 128, 0, st>>>(s->X.as<float>(), s->unsat.as<int32_t>(), s->solved.as<int32_t>(), s->sol.as<int8_t>(), L.n);
+    s->ctx->launches += 1;
+    CK(cudaGetLastError());
+}
+
+void check_kernels(ffsat_search* s, cudaStream_t st) {
+    ffsat_ctx* c = s->ctx;
+    const Layout& L = c->Lo;
     CK(cudaMemsetAsync(s->U.p, 0, (size_t)L.m * 4, st));
     // sign words S[pt][v] (32 points per word), then one thread per (constraint, 32 points)
     const int64_t PT = (s->B + 31) / 32;
@@ -375,8 +396,8 @@ void search_restart(ffsat_search* s, const int32_t* Ug, cudaStream_t st) {
     const int32_t* U = Ug ? Ug : s->U.as<int32_t>();
     if (s->P.adaptive_weights && L.m > 0) {
         s->ctx->launches += 1;
-        if (f64) dev::erwa_kernel<double><<<1, 1024, 0, st>>>(s->ctx->w_pos.as<double>(), U, L.m, s->P.alpha);
-        else dev::erwa_kernel<float><<<1, 1024, 0, st>>>(s->ctx->w_pos.as<float>(), U, L.m, s->P.alpha);
+        if (f64) dev::erwa_kernel<double><<<1, 1024, 0, st>>>(s->W.as<double>(), U, L.m, s->P.alpha);
+        else dev::erwa_kernel<float><<<1, 1024, 0, st>>>(s->W.as<float>(), U, L.m, s->P.alpha);
     }
     int p[3];
     int len = policy_codes(s->P.policy, p);
@@ -391,19 +412,24 @@ void search_restart(ffsat_search* s, const int32_t* Ug, cudaStream_t st) {
     s->round += 1;
 }
 
-void search_stats(ffsat_search* s, cudaStream_t st, ffsat_search_stats* out) {
+void search_reduce(ffsat_search* s, cudaStream_t st) {
     s->ctx->launches += 1;
     dev::stats_kernel<<<1, 1024, 0, st>>>(s->done.as<int32_t>(), s->solved.as<int32_t>(), s->unsat.as<int32_t>(), s->B,
-                                          s->stats.as<int64_t>());
-    int64_t h[4];
+                                          s->point0, s->stats.as<int64_t>());
+    CK(cudaGetLastError());
+}
+
+void search_stats(ffsat_search* s, cudaStream_t st, ffsat_search_stats* out) {
+    search_reduce(s, st);
+    int64_t h[3];
     CK(cudaMemcpyAsync(h, s->stats.p, sizeof(h), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
     out->round = s->round;
     out->iterations = s->iters_issued;
     out->active = h[0];
-    out->solved_point = h[1] >= 0 ? h[1] + s->point0 : -1;
-    out->best_unsat = h[2];
-    out->best_point = h[3] >= 0 ? h[3] + s->point0 : -1;
+    out->solved_point = h[1] != INT64_MAX ? h[1] : -1;
+    out->best_unsat = h[2] != INT64_MAX ? (h[2] >> 32) : -1;
+    out->best_point = h[2] != INT64_MAX ? (h[2] & 0xffffffffLL) : -1;
 }
 
 void search_assignment(ffsat_search* s, int64_t lp, int8_t* out) {
@@ -506,6 +532,7 @@ ffsat_status ffsat_eval(ffsat_ctx* c, const void* x, int64_t B, int32_t on_devic
     if (B > INT32_MAX / 2) throw Error(FFSAT_ERR_ARG, "batch too large");
     cudaStream_t st = S(stream);
     const size_t es = c->esize;
+    if (B == 0) return FFSAT_OK;
     if (on_device) {
         eval_device(c, x, B, f_out, grad_out, unsat_out, st);
         return FFSAT_OK;
@@ -651,11 +678,12 @@ ffsat_status ffsat_search_create(ffsat_ctx* c, int64_t batch, int64_t point0, ui
     if (params) s->P = *params;
     check_params(s->P);
     search_alloc(s.get());
-    // current weights start from the static weights (w0 = 1 for unweighted formulas, #15)
+    // the search's weights start from the formula's static weights (w0 = 1 for unweighted formulas, #15);
+    // they are the search's own ERWA state: the context's weights (ffsat_set_weights) and other searches are untouched
     const int64_t m = c->Lo.m;
     if (m > 0) {
-        if (c->Lo.precision == 64) dev::permute_weights_kernel<double><<<blocks_for(m, 256), 256>>>(c->w_pos.as<double>(), c->w_static_orig.as<double>(), c->order.as<int64_t>(), m);
-        else dev::permute_weights_kernel<float><<<blocks_for(m, 256), 256>>>(c->w_pos.as<float>(), c->w_static_orig.as<double>(), c->order.as<int64_t>(), m);
+        if (c->Lo.precision == 64) dev::permute_weights_kernel<double><<<blocks_for(m, 256), 256>>>(s->W.as<double>(), c->w_static_orig.as<double>(), c->order.as<int64_t>(), m);
+        else dev::permute_weights_kernel<float><<<blocks_for(m, 256), 256>>>(s->W.as<float>(), c->w_static_orig.as<double>(), c->order.as<int64_t>(), m);
     }
     const int64_t tot = batch * c->Lo.n;
     if (tot > 0) {
@@ -721,6 +749,16 @@ ffsat_status ffsat_search_restart(ffsat_search* s, const int32_t* U_global, void
     ABI_CATCH(c)
 }
 
+ffsat_status ffsat_search_reduce(ffsat_search* s, void* stream) {
+    ffsat_ctx* c = s ? s->ctx : nullptr;
+    ABI_TRY(c)
+    if (!s) throw Error(FFSAT_ERR_ARG, "null search");
+    need_device(c);
+    search_reduce(s, S(stream));
+    return FFSAT_OK;
+    ABI_CATCH(c)
+}
+
 ffsat_status ffsat_search_stats_get(ffsat_search* s, void* stream, ffsat_search_stats* out) {
     ffsat_ctx* c = s ? s->ctx : nullptr;
     ABI_TRY(c)
@@ -736,7 +774,8 @@ ffsat_status ffsat_search_get_buffers(ffsat_search* s, ffsat_search_buffers* o) 
     ABI_TRY(c)
     if (!s || !o) throw Error(FFSAT_ERR_ARG, "null argument");
     o->x = s->X.p; o->grad = s->Gx.p; o->f = s->fX.as<double>(); o->eta = s->eta.as<double>();
-    o->unsat = s->unsat.as<int32_t>(); o->U = s->U.as<int32_t>(); o->weights = c->w_pos.p;
+    o->unsat = s->unsat.as<int32_t>(); o->U = s->U.as<int32_t>(); o->weights = s->W.p;
+    o->keys = s->stats.as<int64_t>() + 1; o->solved = s->solved.as<int32_t>();
     return FFSAT_OK;
     ABI_CATCH(c)
 }

@@ -965,7 +965,7 @@ __device__ void global_unit_long_cp(const GlobalArgs<T>& a, const BucketReg<T>& 
     // term stores need no predicate: a duplicate lane writes what the last valid lane writes
     const int64_t bb = bv ? b : a.B - 1;
     const char* xb = reinterpret_cast<const char*>(a.xT + bb);
-    const uint32_t rowb = (uint32_t)a.B * (uint32_t)sizeof(T);   // bytes per x^T row (plan(): n B < 2^32)
+    const size_t rowb = (size_t)a.B * sizeof(T);   // bytes per x^T row (64-bit offsets: any n B)
     for (int j = j0; j < unit_count(U); j += long_warps<T>()) {
         const int64_t pos = (int64_t)U.pos_begin + j;
         const uint32_t* wp = a.words + (int64_t)U.word_begin + (int64_t)j * unit_kp(U);
@@ -978,7 +978,7 @@ __device__ void global_unit_long_cp(const GlobalArgs<T>& a, const BucketReg<T>& 
         // word reads, one wide multiply-add per address)
 #pragma unroll 4
         for (int i = 0; i < k; ++i)
-            cp_async_small<sizeof(T)>(xs + 32 * i, xb + (size_t)((ws[i] & 0x7fffffffu) * rowb));
+            cp_async_small<sizeof(T)>(xs + 32 * i, xb + (size_t)(ws[i] & 0x7fffffffu) * rowb);
         cp_async_commit_wait_all();
         T fe = bk.g0;
         uint32_t t = 0;
@@ -1005,7 +1005,7 @@ __device__ void global_unit_long_cp(const GlobalArgs<T>& a, const BucketReg<T>& 
                 const uint32_t w = ws[i];
                 const T cs = flip_sign(c1, w);
                 const T p = ps[32 * i] * suf;
-                T* d = dst + (size_t)((uint32_t)i * (uint32_t)a.B);
+                T* d = dst + (size_t)i * (size_t)a.B;
                 if (c == 0) __stcs(d, p * cs);
                 else *d = fmaT(p, cs, *d);
                 suf *= fmaT(cs, xs[32 * i], c0);
@@ -1014,7 +1014,7 @@ __device__ void global_unit_long_cp(const GlobalArgs<T>& a, const BucketReg<T>& 
         if (NCH == 0) {
             for (int i = 0; i < k; ++i) {
                 t += lit_true(xs[32 * i], ws[i]);
-                __stcs(dst + (size_t)((uint32_t)i * (uint32_t)a.B), (T)0);
+                __stcs(dst + (size_t)i * (size_t)a.B, (T)0);
             }
         }
         facc += (double)(wc * fe);

@@ -361,15 +361,18 @@ __global__ void reset_round_kernel(double* eta, int32_t* done, int32_t* iters, i
     iters[b] = 0;
 }
 
-// stats: active count, lowest solved index, min unsat and its lowest index (single block)
+// Search statistics (single block) into out[0..2]: out[0] active (not converged) points; out[1] the solved key = lowest
+// GLOBAL point index (point0 + b) whose solved flag is set, INT64_MAX if none; out[2] the incumbent key =
+// (falsified count of sgn(x) at the last check << 32) | global point, minimised (lowest index among equal counts).
+// out[1..2] are MIN-reducible across ranks as they stand (restart sharding, C1 / C4).
 __global__ void __launch_bounds__(1024) stats_kernel(const int32_t* done, const int32_t* solved, const int32_t* unsat,
-                                                     int64_t B, int64_t* out /* [4] */) {
+                                                     int64_t B, int64_t point0, int64_t* out /* [3] */) {
     __shared__ long long s_act[1024], s_sol[1024], s_best[1024];
-    long long act = 0, sol = INT64_MAX, best = INT64_MAX;  // best packs (unsat << 32) | index
+    long long act = 0, sol = INT64_MAX, best = INT64_MAX;
     for (int64_t b = threadIdx.x; b < B; b += blockDim.x) {
         act += done[b] ? 0 : 1;
-        if (solved[b] && b < sol) sol = b;
-        long long key = ((long long)unsat[b] << 32) | (long long)b;
+        if (solved[b] && point0 + b < sol) sol = point0 + b;
+        long long key = ((long long)unsat[b] << 32) | (long long)(point0 + b);
         if (key < best) best = key;
     }
     s_act[threadIdx.x] = act;
@@ -386,10 +389,23 @@ __global__ void __launch_bounds__(1024) stats_kernel(const int32_t* done, const 
     }
     if (threadIdx.x == 0) {
         out[0] = s_act[0];
-        out[1] = s_sol[0] == INT64_MAX ? -1 : s_sol[0];
-        out[2] = s_best[0] == INT64_MAX ? -1 : (s_best[0] >> 32);
-        out[3] = s_best[0] == INT64_MAX ? -1 : (s_best[0] & 0xffffffffLL);
+        out[1] = s_sol[0];
+        out[2] = s_best[0];
     }
+}
+
+// After the round-end check: a point whose rounded assignment sgn(x) falsifies nothing is solved (Thm. 4);
+// record it like a solved trial (first solution kept).  One CTA per point.
+template <typename T>
+__global__ void __launch_bounds__(128) mark_solved_kernel(const T* X, const int32_t* unsat, int32_t* solved, int8_t* sol,
+                                                          int32_t n) {
+    const int64_t b = blockIdx.x;
+    if (unsat[b] != 0 || solved[b]) return;
+    const T* x = X + b * n;
+    int8_t* a = sol + b * n;
+    for (int v = threadIdx.x; v < n; v += blockDim.x) a[v] = x[v] < (T)0 ? (int8_t)-1 : (int8_t)1;
+    __syncthreads();
+    if (threadIdx.x == 0) solved[b] = 1;
 }
 
 // Host-buffer evaluation: flag any non-finite staged coordinate on the device instead of a host scan.

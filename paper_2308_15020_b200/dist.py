@@ -6,8 +6,9 @@ the global points [r B, (r + 1) B) and a full replica of the formula.  Philox st
 point index, so a point's trajectory does not depend on the number of GPUs.  The only exchanges are the
 round-end collectives on library-owned device buffers:
   C2  U_c SUM   -- ERWA (Prop. 3, P:584-605) is defined over all p_t points on all GPUs (P:588);
-  C1  any-solved MAX;
-  C4  incumbent: MIN over (falsified count, global point), then a broadcast of its assignment.
+  C1  any-solved: MIN of the library's solved key (lowest solved global point);
+  C4  incumbent: MIN of the library's key (falsified count << 32 | global point), then a broadcast of its row.
+C1 and C4 travel in one all-reduce of two int64 keys that ffsat_search_reduce writes on the device.
 
 Constraint sharding (config c5, formulas too large for one GPU's throughput).  Each rank evaluates a
 contiguous, cost-balanced range of the constraints for the full batch and the partial f, grad f and unsat
@@ -99,11 +100,17 @@ class ShardedEval:
         return f, g, u
 
 
-class RestartSharded:
-    """Alg. 1 over world x B points, this rank's B at global offset point0 (the search was created with it).
+INT64_MAX = (1 << 63) - 1
 
-    `search` is a libffsat Search (or a test double with the same methods): iterate(n), check(),
-    restart(U_global), begin_round(), tensors() -> {'x', 'unsat', 'U', ...}, assignment(local_point)."""
+
+class RestartSharded:
+    """Alg. 1 over all ranks' points; this rank's B points start at global index point0 (the search was created with
+    it, so its Philox streams and phase offsets are keyed by global point: trajectories do not depend on G).
+
+    `search` is a libffsat Search (or a test double with the same methods): iterate(n), check(), reduce(),
+    restart(U_global), begin_round(), tensors() -> {'x', 'unsat', 'U', 'keys', ...}, assignment(local_point).
+    The any-solved flag and the incumbent are computed by the library (ffsat_search_reduce: device keys in global
+    point indices); this class only moves them through the process group."""
 
     def __init__(self, search, round_len: int, rank: int = 0, world: int = 1, group=None):
         import torch
@@ -113,7 +120,7 @@ class RestartSharded:
         self.rank, self.world, self.group = rank, world, group
         self.T = search.tensors()
         self.point0 = int(getattr(search, "point0", 0))
-        self.flag = torch.zeros(1, dtype=torch.int32, device=self.T["unsat"].device)
+        self.B = int(self.T["unsat"].numel())
         self.rounds = 0
 
     def _all_reduce(self, t, op):
@@ -123,18 +130,30 @@ class RestartSharded:
     def begin(self):
         self.search.begin_round()
 
-    def round_end(self):
-        """Exact check of sgn(x) on every point, global U (C2) and any-solved flag (C1), ERWA + rephase with
-        the global U, start of the next round.  Returns the any-solved flag tensor (not synchronised)."""
+    def exchange(self):
+        """Round-end exchange without a host round trip: exact check of sgn(x) on every point (library; a point
+        with no falsified constraint is marked solved and kept), C2 SUM of U_c over ranks (ERWA is defined over
+        all p_t points), the library's any-solved / incumbent keys, then one MIN all-reduce of both keys
+        (C1 + C4).  Returns the keys tensor [solved global point or INT64_MAX, (unsat << 32) | global point]."""
         s, T = self.search, self.T
         s.check()
         self._all_reduce(T["U"], self.dist.ReduceOp.SUM)
-        self.flag.copy_((T["unsat"].min() == 0).to(self.flag.dtype).view(1))
-        self._all_reduce(self.flag, self.dist.ReduceOp.MAX)
-        s.restart(T["U"])
-        s.begin_round()
+        s.reduce()
+        self._all_reduce(T["keys"], self.dist.ReduceOp.MIN)
+        return T["keys"]
+
+    def restart(self):
+        """ERWA with the global U_c and rephase (library), then the next round's start."""
+        self.search.restart(self.T["U"])
+        self.search.begin_round()
         self.rounds += 1
-        return self.flag
+
+    def round_end(self):
+        """exchange() + restart(), fully asynchronous (the timed bench step).  A solved point's assignment survives
+        the rephase (the library keeps it), so the caller may poll the keys whenever it likes."""
+        keys = self.exchange()
+        self.restart()
+        return keys
 
     def step(self, i: int):
         """One PGD iteration over the local batch; every round_len-th step also ends the round."""
@@ -143,27 +162,71 @@ class RestartSharded:
             return self.round_end()
         return None
 
-    def incumbent(self):
-        """(falsified count, global point, assignment int8 [n]) of the best current point over all ranks
-        (C4): exact check of sgn(x) here, MIN over the packed key count << 32 | global point, then the
-        owner broadcasts its row (lowest global index among equal counts: deterministic for any G)."""
+    def fetch(self, global_point: int):
+        """Assignment int8 [n] (-1 True / +1 False) of a global point, broadcast from the rank that owns it: the
+        solved assignment if that point solved, else sgn of its current x (C4)."""
         torch = self.torch
-        self.search.check()
-        unsat = self.T["unsat"]
-        local = torch.argmin(unsat).item()  # lowest local index among the minima
-        key = torch.tensor([(int(unsat[local].item()) << 32) | (self.point0 + local)], dtype=torch.int64,
-                           device=unsat.device)
-        self._all_reduce(key, self.dist.ReduceOp.MIN)
-        k = int(key.item())
-        cnt, gp = k >> 32, k & 0xFFFFFFFF
-        B = unsat.numel()
-        owner_local = gp - self.point0
-        mine = 0 <= owner_local < B
-        a = torch.zeros(self.T["x"].shape[1], dtype=torch.int8, device=unsat.device)
+        dev = self.T["unsat"].device
+        lp = int(global_point) - self.point0
+        mine = 0 <= lp < self.B
+        n = self.T["x"].shape[1]
+        a = torch.zeros(n, dtype=torch.int8, device=dev)
         if mine:
-            a.copy_(torch.as_tensor(np.asarray(self.search.assignment(owner_local)), device=unsat.device))
+            a.copy_(torch.as_tensor(np.asarray(self.search.assignment(lp)), device=dev))
         if self.world > 1:
-            owner = torch.tensor([self.rank if mine else -1], dtype=torch.int64, device=unsat.device)
+            owner = torch.tensor([self.rank if mine else -1], dtype=torch.int64, device=dev)
             self._all_reduce(owner, self.dist.ReduceOp.MAX)
             self.dist.broadcast(a, src=int(owner.item()), group=self.group)
-        return cnt, gp, a.cpu().numpy()
+        return a.cpu().numpy()
+
+    def incumbent(self):
+        """(falsified count, global point, assignment) of the best point over all ranks at a fresh check (C4): the
+        library's incumbent key, MIN over ranks (lowest global index among equal counts: deterministic for any G),
+        then the owner broadcasts its row."""
+        keys = self.exchange()
+        k = int(keys[1].item())
+        cnt, gp = k >> 32, k & 0xFFFFFFFF
+        return cnt, gp, self.fetch(gp)
+
+
+def solve_sharded(search, check, round_len: int, max_rounds: int, rank: int = 0, world: int = 1, group=None,
+                  timeout_s: float = 0.0):
+    """Restart-sharded Alg. 1 over all ranks: every rank runs its points' PGD rounds; at each round end the
+    ranks exchange U_c (C2) and the library's keys (C1 + C4).  All ranks stop together at the first round end whose
+    any-solved key is set and return the solution of the lowest solved global point, verified by `check`
+    (ffsat_check: the exact host count); otherwise they keep the best incumbent (fetched before the rephase) and
+    return UNKNOWN after max_rounds or timeout_s (the same decision on every rank: rank 0's clock is broadcast).
+
+    Returns dict(sat, assignment, best_unsat, point, rounds, seconds)."""
+    import time
+    import torch
+    import torch.distributed as dist
+    rs = RestartSharded(search, round_len, rank, world, group)
+    t0 = time.perf_counter()
+    best_cnt, best_gp, best_a = None, -1, None
+    rs.begin()
+    rounds = 0
+    stop = torch.zeros(1, dtype=torch.int32, device=rs.T["unsat"].device)
+    for rounds in range(1, max_rounds + 1):
+        search.iterate(round_len)
+        keys = rs.exchange().cpu()          # the one host round trip of a round
+        solved_gp, inc = int(keys[0]), int(keys[1])
+        if solved_gp != INT64_MAX:
+            a = rs.fetch(solved_gp)
+            n_unsat, _ = check(a)
+            if n_unsat == 0:
+                return {"sat": 1, "assignment": a, "best_unsat": 0, "point": solved_gp, "rounds": rounds,
+                        "seconds": time.perf_counter() - t0}
+        cnt, gp = inc >> 32, inc & 0xFFFFFFFF
+        if best_cnt is None or cnt < best_cnt:
+            best_a = rs.fetch(gp)
+            best_cnt, best_gp = check(best_a)[0], gp
+        if timeout_s > 0:
+            stop.fill_(1 if (rank == 0 and time.perf_counter() - t0 > timeout_s) else 0)
+            if world > 1:
+                dist.all_reduce(stop, op=dist.ReduceOp.MAX, group=group)
+            if int(stop.item()):
+                break
+        rs.restart()
+    return {"sat": 0, "assignment": best_a, "best_unsat": best_cnt, "point": best_gp, "rounds": rounds,
+            "seconds": time.perf_counter() - t0}

@@ -36,7 +36,7 @@ class ffsat_formula(C.Structure):
 
 
 class ffsat_options(C.Structure):
-    _fields_ = [("precision", C.c_int32), ("device", C.c_int32), ("path", C.c_int32), ("reserved", C.c_int32)]
+    _fields_ = [("precision", C.c_int32), ("device", C.c_int32), ("path", C.c_int32), ("batch_ref", C.c_int32)]
 
 
 class ffsat_info_t(C.Structure):
@@ -65,7 +65,8 @@ class ffsat_search_stats(C.Structure):
 
 class ffsat_search_buffers(C.Structure):
     _fields_ = [("x", C.c_void_p), ("grad", C.c_void_p), ("f", C.c_void_p), ("eta", C.c_void_p),
-                ("unsat", C.c_void_p), ("U", C.c_void_p), ("weights", C.c_void_p)]
+                ("unsat", C.c_void_p), ("U", C.c_void_p), ("weights", C.c_void_p), ("keys", C.c_void_p),
+                ("solved", C.c_void_p)]
 
 
 class ffsat_result(C.Structure):
@@ -78,7 +79,7 @@ class ffsat_result(C.Structure):
 
 EXPORTS = ["ffsat_load", "ffsat_load_file", "ffsat_info", "ffsat_export", "ffsat_eval", "ffsat_set_weights",
            "ffsat_get_weights", "ffsat_check", "ffsat_search_create", "ffsat_search_set_x", "ffsat_search_begin_round",
-           "ffsat_search_iterate", "ffsat_search_check", "ffsat_search_restart", "ffsat_search_stats_get",
+           "ffsat_search_iterate", "ffsat_search_check", "ffsat_search_reduce", "ffsat_search_restart", "ffsat_search_stats_get",
            "ffsat_search_get_buffers", "ffsat_search_assignment", "ffsat_search_free", "ffsat_solve",
            "ffsat_default_params", "ffsat_last_error", "ffsat_version", "ffsat_free", "ffsat_launch_count",
            "ffsat_eval_profiled", "ffsat_layout_units"]
@@ -109,6 +110,7 @@ def lib():
         "ffsat_search_begin_round": ([P, P], C.c_int),
         "ffsat_search_iterate": ([P, I32, P], C.c_int),
         "ffsat_search_check": ([P, P], C.c_int),
+        "ffsat_search_reduce": ([P, P], C.c_int),
         "ffsat_search_restart": ([P, P, P], C.c_int),
         "ffsat_search_stats_get": ([P, P, C.POINTER(ffsat_search_stats)], C.c_int),
         "ffsat_search_get_buffers": ([P, C.POINTER(ffsat_search_buffers)], C.c_int),
@@ -165,7 +167,7 @@ def _stream(stream, like=None):
 
 # ----------------------------------------------------------------------------- C-ABI mirrors
 
-def ffsat_load(n_vars, kind, bound, weight, offsets, lits, precision=0, device=0, path=0):
+def ffsat_load(n_vars, kind, bound, weight, offsets, lits, precision=0, device=0, path=0, batch_ref=0):
     kind = np.ascontiguousarray(kind, np.uint8)
     m = len(kind)
     bound = np.ascontiguousarray(bound if bound is not None else np.zeros(m), np.int32)
@@ -174,14 +176,14 @@ def ffsat_load(n_vars, kind, bound, weight, offsets, lits, precision=0, device=0
     lits = np.ascontiguousarray(lits, np.int32)
     f = ffsat_formula(int(n_vars), m, kind.ctypes.data, bound.ctypes.data, weight.ctypes.data, offsets.ctypes.data,
                       lits.ctypes.data)
-    o = ffsat_options(int(precision), int(device), int(path), 0)
+    o = ffsat_options(int(precision), int(device), int(path), int(batch_ref))
     out = C.c_void_p()
     _check(lib().ffsat_load(C.byref(f), C.byref(o), C.byref(out)))
     return out
 
 
-def ffsat_load_file(path, precision=0, device=0, opt_path=0):
-    o = ffsat_options(int(precision), int(device), int(opt_path), 0)
+def ffsat_load_file(path, precision=0, device=0, opt_path=0, batch_ref=0):
+    o = ffsat_options(int(precision), int(device), int(opt_path), int(batch_ref))
     out = C.c_void_p()
     _check(lib().ffsat_load_file(str(path).encode(), C.byref(o), C.byref(out)))
     return out
@@ -240,16 +242,16 @@ class Context:
         self.dtype = np.float64 if self.info["precision"] == 64 else np.float32
 
     @classmethod
-    def from_arrays(cls, n, kind, bound, weight, offsets, lits, precision=0, device=0, path=0):
-        return cls(ffsat_load(n, kind, bound, weight, offsets, lits, precision, device, path))
+    def from_arrays(cls, n, kind, bound, weight, offsets, lits, precision=0, device=0, path=0, batch_ref=0):
+        return cls(ffsat_load(n, kind, bound, weight, offsets, lits, precision, device, path, batch_ref))
 
     @classmethod
     def from_instance(cls, inst, **kw):
         return cls.from_arrays(inst.n, inst.kind, inst.bound, inst.weight, inst.offsets, inst.lits, **kw)
 
     @classmethod
-    def from_file(cls, path, precision=0, device=0, opt_path=0):
-        return cls(ffsat_load_file(path, precision, device, opt_path))
+    def from_file(cls, path, precision=0, device=0, opt_path=0, batch_ref=0):
+        return cls(ffsat_load_file(path, precision, device, opt_path, batch_ref))
 
     def close(self):
         if self.ptr:
@@ -297,6 +299,18 @@ class Context:
         _check(lib().ffsat_layout_units(self.ptr, C.byref(nu), units.ctypes.data_as(C.c_void_p), nu.value,
                                         order.ctypes.data_as(C.c_void_p)), self.ptr)
         return units, order
+
+    def order(self):
+        """Position -> input-constraint map of the library's internal constraint order (per-constraint device arrays
+        such as a search's U and weights are in position order: input[order[p]] = position[p])."""
+        return self.layout_units()[1]
+
+    def to_input_order(self, a):
+        """A per-constraint array in position order -> input order."""
+        a = np.asarray(a)
+        out = np.empty_like(a)
+        out[self.order()] = a
+        return out
 
     def launch_count(self):
         n = C.c_int64()
@@ -376,6 +390,10 @@ class Search:
     def check(self, stream=None):
         _check(lib().ffsat_search_check(self.ptr, _stream(stream)), self.ctx.ptr)
 
+    def reduce(self, stream=None):
+        """Device-side any-solved / incumbent keys into tensors()['keys'] (asynchronous)."""
+        _check(lib().ffsat_search_reduce(self.ptr, _stream(stream)), self.ctx.ptr)
+
     def restart(self, U_global=None, stream=None):
         pU = C.c_void_p(U_global.data_ptr()) if U_global is not None else None
         _check(lib().ffsat_search_restart(self.ptr, pU, _stream(stream)), self.ctx.ptr)
@@ -396,7 +414,8 @@ class Search:
         return a
 
     def tensors(self):
-        """torch views of the device buffers (x, grad, f, eta, unsat, U, weights)."""
+        """torch views of the device buffers (x, grad, f, eta, unsat, U, weights, keys, solved); U and weights are in
+        the library's position order (Context.order() maps position -> input constraint)."""
         import torch
         b = self.buffers()
         n, m, B = self.ctx.n, self.ctx.m, self.B
@@ -408,7 +427,8 @@ class Search:
         return {"x": view(b.x, B * n, tdt).view(B, n), "grad": view(b.grad, B * n, tdt).view(B, n),
                 "f": view(b.f, B, torch.float64), "eta": view(b.eta, B, torch.float64),
                 "unsat": view(b.unsat, B, torch.int32), "U": view(b.U, m, torch.int32),
-                "weights": view(b.weights, m, tdt)}
+                "weights": view(b.weights, m, tdt), "keys": view(b.keys, 2, torch.int64),
+                "solved": view(b.solved, B, torch.int32)}
 
 
 def _device_view(ptr, count, dtype, device):
@@ -417,7 +437,7 @@ def _device_view(ptr, count, dtype, device):
 
     class _CAI:
         def __init__(self):
-            typestr = {torch.float32: "<f4", torch.float64: "<f8", torch.int32: "<i4"}[dtype]
+            typestr = {torch.float32: "<f4", torch.float64: "<f8", torch.int32: "<i4", torch.int64: "<i8"}[dtype]
             self.__cuda_array_interface__ = {"shape": (int(count),), "typestr": typestr,
                                              "data": (int(ptr or 0), False), "version": 3, "strides": None}
     return torch.as_tensor(_CAI(), device=device)

@@ -109,7 +109,8 @@ def test_constraint_sharded_eval_gloo(tmp_path):
 
 
 class OracleSearch:
-    """Test double of libffsat's Search on the oracle (oracle/solve.py semantics, fp64, CPU tensors)."""
+    """Test double of libffsat's Search on the oracle (oracle/solve.py semantics, fp64, CPU tensors).  Its reduce()
+    mirrors ffsat_search_reduce's documented keys (include/ffsat.h) so dist.py's collectives can be tested on CPU."""
 
     def __init__(self, F, B, seed, point0, params):
         self.F, self.B, self.seed, self.point0, self.P = F, B, seed, point0, params
@@ -117,10 +118,14 @@ class OracleSearch:
                                eta=None, done=None, iters=None, w=np.ones(F.m), point0=point0)
         self.unsat = np.zeros(B, np.int32)
         self.U = np.zeros(F.m, np.int32)
+        self.keys = np.zeros(2, np.int64)
+        self.solved = np.zeros(B, np.int32)
+        self.sol = np.zeros((B, F.n), np.int8)
         self.rnd = 0
 
     def tensors(self):
-        return {"x": torch.from_numpy(self.st.x), "unsat": torch.from_numpy(self.unsat), "U": torch.from_numpy(self.U)}
+        return {"x": torch.from_numpy(self.st.x), "unsat": torch.from_numpy(self.unsat), "U": torch.from_numpy(self.U),
+                "keys": torch.from_numpy(self.keys), "solved": torch.from_numpy(self.solved)}
 
     def begin_round(self):
         osolve.start_round(self.F, self.st, self.P)
@@ -133,6 +138,14 @@ class OracleSearch:
         cnt, _, U = cdp.check(self.F, self.st.x, want_U=True)
         self.unsat[:] = cnt
         self.U[:] = U
+        for b in np.nonzero((cnt == 0) & (self.solved == 0))[0]:
+            self.solved[b] = 1
+            self.sol[b] = np.where(self.st.x[b] < 0, -1, 1)
+
+    def reduce(self):
+        sol = np.nonzero(self.solved)[0]
+        self.keys[0] = self.point0 + sol[0] if len(sol) else D.INT64_MAX
+        self.keys[1] = min((int(u) << 32) | (self.point0 + b) for b, u in enumerate(self.unsat))
 
     def restart(self, U_global):
         if self.P.adaptive_weights:
@@ -141,6 +154,8 @@ class OracleSearch:
         self.st.x[:] = osolve.rephase(self.st.x, self.seed, self.point0, self.rnd, self.P)
 
     def assignment(self, lp):
+        if self.solved[lp]:
+            return self.sol[lp].copy()
         return np.where(self.st.x[lp] < 0, -1, 1).astype(np.int8)
 
 
@@ -150,29 +165,28 @@ def _run_restart_sharded(rank, world, B_total, rounds, round_len):
     point0, B = D.point_range(B_total, world, rank)
     s = OracleSearch(Fo, B, 1234, point0, osolve.Params(max_inner=round_len))
     rs = D.RestartSharded(s, round_len, rank, world)
-    rs.point0 = point0
     rs.begin()
-    flags = []
+    keys = []
     for i in range(rounds * round_len):
-        fl = rs.step(i)
-        if fl is not None:
-            flags.append(int(fl.item()))
+        k = rs.step(i)
+        if k is not None:
+            keys.append([int(v) for v in k])
     cnt, gp, a = rs.incumbent()
-    return point0, s.st.x.copy(), s.st.w.copy(), flags, (cnt, gp, a)
+    return point0, s.st.x.copy(), s.st.w.copy(), keys, (cnt, gp, a)
 
 
 def _restart_worker(rank, world, port, out, B_total, rounds, round_len):
     _init(rank, world, port)
-    p0, x, w, flags, inc = _run_restart_sharded(rank, world, B_total, rounds, round_len)
-    np.savez(out + f".{rank}.npz", p0=p0, x=x, w=w, flags=np.array(flags), cnt=inc[0], gp=inc[1], a=inc[2])
+    p0, x, w, keys, inc = _run_restart_sharded(rank, world, B_total, rounds, round_len)
+    np.savez(out + f".{rank}.npz", p0=p0, x=x, w=w, keys=np.array(keys), cnt=inc[0], gp=inc[1], a=inc[2])
     dist.destroy_process_group()
 
 
 def test_restart_sharding_matches_single_process(tmp_path):
     """G = 2 ranks x 6 points reproduce G = 1 x 12 points exactly: per-point trajectories (Philox keyed by
-    global point), the ERWA weights (global U_c), the any-solved flags and the incumbent."""
+    global point), the ERWA weights (global U_c), the any-solved / incumbent keys and the incumbent."""
     B_total, rounds, round_len = 12, 3, 4
-    p0, x1, w1, flags1, inc1 = _run_restart_sharded(0, 1, B_total, rounds, round_len)
+    p0, x1, w1, keys1, inc1 = _run_restart_sharded(0, 1, B_total, rounds, round_len)
     out = str(tmp_path / "rs")
     mp.spawn(_restart_worker, args=(2, free_port(), out, B_total, rounds, round_len), nprocs=2, join=True)
     parts = [np.load(out + f".{r}.npz") for r in range(2)]
@@ -180,10 +194,65 @@ def test_restart_sharding_matches_single_process(tmp_path):
     assert np.array_equal(x1, x2)
     for p in parts:
         assert np.array_equal(p["w"], w1)
-        assert list(p["flags"]) == flags1
+        assert p["keys"].tolist() == keys1
         assert (int(p["cnt"]), int(p["gp"])) == (inc1[0], inc1[1])
         assert np.array_equal(p["a"], inc1[2])
     # the incumbent is a true minimiser of the falsified count over all global points
     Fo = OracleFormula.from_arrays(*synth.config1(4).arrays())
     cnt, _ = cdp.check(Fo, np.where(x1 < 0, -1.0, 1.0))
     assert inc1[0] == cnt.min() and inc1[1] == int(np.argmin(cnt))
+
+
+def _solve_worker(rank, world, port, out, B_total):
+    _init(rank, world, port)
+    res = _solve(rank, world, B_total)
+    np.savez(out + f".{rank}.npz", sat=res["sat"], a=res["assignment"], point=res["point"], rounds=res["rounds"],
+             best=res["best_unsat"])
+    dist.destroy_process_group()
+
+
+def _planted():
+    """planted 3-SAT n=40, m=176: the 16-point search needs 3 rounds and solves at global point 12 (rank 1 at G=2)"""
+    z = np.random.default_rng(3).random(40) < 0.5
+    return synth.random_ksat(40, 176, 3, 1, planted=z)
+
+
+def _solve(rank, world, B_total, inst=None):
+    inst = inst or _planted()
+    Fo = OracleFormula.from_arrays(*inst.arrays())
+    point0, B = D.point_range(B_total, world, rank)
+    s = OracleSearch(Fo, B, 99, point0, osolve.Params(max_inner=2))
+
+    def check(a):
+        cnt, fw = cdp.check(Fo, np.where(np.asarray(a) < 0, -1.0, 1.0)[None])
+        return int(cnt[0]), float(fw[0])
+    return D.solve_sharded(s, check, round_len=2, max_rounds=40, rank=rank, world=world)
+
+
+def test_solve_sharded_stops_all_ranks_with_the_same_verified_solution(tmp_path):
+    """The restart-sharded solve loop: both ranks stop at the same round with the lowest solved global point's
+    assignment, which the exact check verifies, and it is the single-process answer (G-independence)."""
+    one = _solve(0, 1, 16)
+    assert one["sat"] == 1 and one["rounds"] > 1 and one["point"] >= 8   # found by rank 1 after restarts
+    out = str(tmp_path / "sv")
+    mp.spawn(_solve_worker, args=(2, free_port(), out, 16), nprocs=2, join=True)
+    parts = [np.load(out + f".{r}.npz") for r in range(2)]
+    Fo = OracleFormula.from_arrays(*_planted().arrays())
+    for p in parts:
+        assert int(p["sat"]) == 1 and int(p["rounds"]) == one["rounds"] and int(p["point"]) == one["point"]
+        assert np.array_equal(p["a"], one["assignment"])
+        assert cdp.check(Fo, np.where(p["a"] < 0, -1.0, 1.0)[None])[0][0] == 0
+
+
+def test_solve_sharded_unsat_returns_unknown_with_incumbent():
+    """{x1, -x1} is unsatisfiable: UNKNOWN (never SAT), incumbent with one falsified clause."""
+    Fo = OracleFormula.from_constraints(1, [(0, 0, 1.0, [1]), (0, 0, 1.0, [-1])])
+    inst = synth.Instance("unsat", 1, Fo.kind, Fo.bound, Fo.weight, Fo.offsets, Fo.lits)
+    s = OracleSearch(Fo, 4, 5, 0, osolve.Params(max_inner=5))
+
+    def check(a):
+        cnt, fw = cdp.check(Fo, np.where(np.asarray(a) < 0, -1.0, 1.0)[None])
+        return int(cnt[0]), float(fw[0])
+    r = D.solve_sharded(s, check, round_len=5, max_rounds=3)
+    assert r["sat"] == 0 and r["best_unsat"] == 1 and r["rounds"] == 3
+    assert inst.m == 2
