@@ -15,6 +15,15 @@ and the next round's start evaluation.  A1-A3 (parse, layout, coefficients) run 
 value = literal-gradient terms per second over all ranks = sum_c k_c * B_total * K / t, with t the
 max over ranks of the summed CUDA-event step times (L2 flushed between steps, untimed).
 `--impl reference` times the oracle (oracle/dp.c, the CPU fp64 GradSAT DP) on the same workload.
+
+`python bench.py --gpus N` without a torchrun environment re-executes itself under torch.distributed.run with N
+ranks (127.0.0.1); with fewer visible GPUs than ranks the ranks share devices over gloo (a functional dry run).
+
+roofline: every resource the dominant kernel (or, for HBM, the evaluation)
+uses is reported under "resources" with its algorithmic count -- fast paths 3 products per term (FP32 pipe) and
+12 B per term of shared-memory traffic on the on-chip path, the root path 12 FP64 slots per (literal, root), HBM
+4L + 8C + 2 es n B + 4B bytes per evaluation -- and the top-level entry is the BINDING one (highest fraction).
+traffic = ncu dram bytes of the same scope; waste = traffic / algorithmic bytes.
 """
 from __future__ import annotations
 
@@ -39,6 +48,8 @@ CONFIGS = {
     "c2": dict(make=lambda: synth.config2(0), B=1024, mode="restart", desc="c2: uniform random 7-SAT n=200 m=17000 (alpha=85)"),
     "c1": dict(make=lambda: synth.config1(0), B=1, mode="restart", desc="c1: uniform random 3-SAT n=20 m=91, single point"),
     "c3": dict(make=lambda: synth.config3(0), B=32, mode="restart", desc="c3: n=4096, 8192 planted 3-SAT + 32 at-most-b k=500..2000, fp64"),
+    "c3b256": dict(make=lambda: synth.config3(0), B=256, mode="restart", desc="c3 at B=256: n=4096, 8192 planted 3-SAT + 32 at-most-b k=500..2000, fp64"),
+    "c4p": dict(make=lambda: synth.config4_parity(0), B=1024, mode="restart", desc="c4(i): parity learning with error N=60, m=120 XOR (P:1066-1071)"),
     "c4": dict(make=lambda: synth.config4_hybrid(0), B=1024, mode="restart", desc="c4: n=1024, 2048 planted 3-CNF + 512 XOR k=3..64"),
     "c5": dict(make=lambda: synth.config5(0), B=32, mode="constraint", desc="c5: uniform random 3-SAT n=1e6 m=4.2e6, constraint-sharded"),
 }
@@ -46,7 +57,7 @@ SM_COUNT = 148
 FP32_LANES, FP64_LANES = 128, 64  # FP32 / FP64 lanes per SM per clock (B200 guide unit counts)
 # Algorithmic FP lane-operations (one FMA = one lane-op = one pipe slot: count instructions):
 SMEM_BYTES_PER_TERM = 12   # x tile LDS + gradient tile LDS + STS, 4 B each
-FAST_OPS_PER_TERM = 5             # factor FMA, prefix MUL, prefix*suffix MUL, suffix MUL, gradient FMA
+FAST_PRODUCTS_PER_TERM = 3       # the fast-path product count per literal and point (prefix, suffix, term)
 ROOT_OPS_PER_LIT_ROOT = 12        # factor 2 FMA, prefix + suffix complex MUL (2 x 4), Re-accumulate 2 FMA (App. A)
 
 
@@ -110,9 +121,10 @@ class ClockSampler:
                 "samples": len(sm), "source": "nvml"}
 
 
-def ncu_traffic(kernel_key, config):
-    """dram bytes per launch of the dominant kernel(s) ("a+b": summed) on this config from the committed ncu --set full
-    summary (profiles/ncu_summary.json, keys "<config>:<kernel>"), or None."""
+def ncu_traffic(kernel_key, config, any_of=False):
+    """dram bytes per launch of the dominant kernel(s) ("a+b": summed) on this config from the committed ncu summary
+    (profiles/ncu_summary.json, keys "<config>:<kernel>" per launch of one evaluation), or None.  any_of: sum the
+    kernels present (an evaluation launches a subset of them), None if none is."""
     p = os.path.join(ROOT, "profiles", "ncu_summary.json")
     if not os.path.exists(p):
         return None
@@ -120,6 +132,9 @@ def ncu_traffic(kernel_key, config):
         with open(p) as fh:
             d = json.load(fh)
         vals = [d.get(f"{config}:{k}", {}).get("dram_bytes_per_launch") for k in kernel_key.split("+")]
+        if any_of:
+            vals = [v for v in vals if v is not None]
+            return float(sum(vals)) if vals else None
         return None if any(v is None for v in vals) else float(sum(vals))
     except (OSError, ValueError):
         return None
@@ -202,29 +217,113 @@ def cpu_baseline(cfg, inst, X):
 # ------------------------------------------------------------------------------------------------ our arm
 
 
-def time_to_solve(P, args, device):
-    """BJ.metric time-to-solve: wall time of ffsat_solve from call to a verified SAT on planted c2
-    instances (random 7-SAT n=200 with a hidden satisfying assignment) at the configured ratio near the threshold
-    (alpha = 87.79) and at alpha = 65; 1024 restart points, ERWA + (ROF) rephasing, 200 PGD trials per round; one
-    run per seed; median and PAR-2 (an unsolved run counts 2 x cap)."""
+def time_to_solve(P, D, args, device, rank, world, dist):
+    """BJ.metric time-to-solve on G = world GPUs: restart-sharded Alg. 1 (dist.solve_sharded: every rank
+    runs 1024 restart points, the ranks exchange U_c and the library's any-solved / incumbent keys at each round end
+    and stop together on the first verified solution) on planted c2 instances (random 7-SAT n=200 with a hidden
+    satisfying assignment) at the threshold ratio alpha = 87.79 and at alpha = 65; ERWA + (ROF) rephasing, 200 PGD
+    trials per round, any-solved polled every 10 iterations.  Wall time of rank 0 from the first iteration to the
+    verified answer, one run per seed; median and PAR-2 (an unsolved run counts 2 x cap)."""
+    import torch
     out = []
     for alpha in (87.79, 65.0):
         inst = synth.config2(0, planted=True, alpha=alpha)
         ctx = P.Context.from_instance(inst, device=device)
-        ctx.solve(batch=1024, max_restarts=1, seed=0, max_inner=5)          # warm-up (lazy module loading)
         times, solved, rounds, best = [], 0, [], []
-        for seed in range(args.tts_seeds):
-            res, a = ctx.solve(batch=1024, max_restarts=10 ** 6, seed=1 + seed, max_inner=200, check_every=10,
-                               timeout_s=args.tts_cap)
-            ok = bool(res["sat"]) and ctx.check(a)[0] == 0
+        for seed in range(-1, args.tts_seeds):                 # seed -1: untimed warm-up (module loading)
+            s = ctx.search(1024, seed=1 + max(seed, 0), point0=rank * 1024, max_inner=200, check_every=200)
+            if world > 1:
+                dist.barrier()
+            torch.cuda.synchronize()
+            r = D.solve_sharded(s, ctx.check, round_len=200, max_rounds=10 ** 6 if seed >= 0 else 1, rank=rank,
+                                world=world, timeout_s=args.tts_cap if seed >= 0 else 0.0, poll_every=10)
+            s.close()
+            if seed < 0:
+                continue
+            ok = bool(r["sat"]) and ctx.check(r["assignment"])[0] == 0
             solved += ok
-            times.append(res["seconds"] if ok else 2 * args.tts_cap)
-            rounds.append(res["restarts"])
-            best.append(res["best_unsat"])
-        out.append({"instance": f"planted 7-SAT n={inst.n} m={inst.m} (alpha {alpha})", "batch": 1024,
-                    "seeds": args.tts_seeds, "solved": solved, "cap_s": args.tts_cap, "median_s": float(np.median(times)),
-                    "par2_s": float(np.mean(times)), "seconds": times, "restart_rounds": rounds, "best_unsat": best})
-    return {"runs": out, "note": "sat only after the exact host check (ffsat_check); unsolved = 2 x cap"}
+            times.append(r["seconds"] if ok else 2 * args.tts_cap)
+            rounds.append(r["rounds"])
+            best.append(int(r["best_unsat"]))
+        out.append({"instance": f"planted 7-SAT n={inst.n} m={inst.m} (alpha {alpha})", "batch_per_gpu": 1024,
+                    "batch_total": 1024 * world, "gpus": world, "seeds": args.tts_seeds, "solved": solved,
+                    "cap_s": args.tts_cap, "median_s": float(np.median(times)), "par2_s": float(np.mean(times)),
+                    "seconds": times, "restart_rounds": rounds, "best_unsat": best})
+        ctx.close()
+    return {"runs": out, "note": "dist.solve_sharded over all ranks; sat only after the exact host check "
+                                 "(ffsat_check); unsolved = 2 x cap"}
+
+
+def roofline_of(info, inst, B, ph, args):
+    """Every resource the hot path uses, with SURVEY 8(d)'s algorithmic counts, and the binding one."""
+    peaks, peak_src = measured_peaks()
+    mhz = float(peaks.get("sm_max_mhz", 1965.0))
+    fast_ms, root_ms = float(ph[0]), float(ph[1])
+    eval_ms = float(np.sum(ph))
+    f64 = info["precision"] == 64
+    es = 8 if f64 else 4
+    terms_fast = info["n_fast_lits"] * B
+    L, C, n = inst.n_lits, inst.m, inst.n
+    alg_bytes = 4 * L + 8 * C + 2 * es * n * B + 4 * B
+    hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
+    lanes = FP64_LANES if f64 else FP32_LANES
+    alu_peak = SM_COUNT * lanes * mhz * 1e6 / 1e12
+    alu_src = (f"{SM_COUNT} SMs x {lanes} {'FP64' if f64 else 'FP32'} lanes x {mhz:.0f} MHz ({peak_src} sm_max_mhz); "
+               "one FMA / MUL = one lane-op")
+    res = {}
+    eval_kernels = ("transpose_kernel+fast_global_kernel+fast_global_long_kernel+reduce_grad_kernel+reduce_f_kernel"
+                    if info["path"] == 2 else "fast_wide_kernel+fast_tiled_kernel+reduce_grad_kernel+reduce_f_kernel")
+    traffic_eval = ncu_traffic(eval_kernels, args.config, any_of=True)
+    res["hbm"] = {"scope": "evaluation (A4-A7, every kernel)", "achieved": alg_bytes / (eval_ms * 1e-3) / 1e9,
+                  "peak": hbm_peak, "unit": "GB/s", "algorithmic_bytes": alg_bytes,
+                  "algorithmic_def": f"4L + 8C + 2*{es}*n*B + 4B (SURVEY 8(d))", "time_ms": eval_ms,
+                  "traffic": traffic_eval, "waste": (traffic_eval / alg_bytes) if traffic_eval else None,
+                  "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_src})"}
+    if fast_ms >= root_ms:
+        kname = ("fast_global_kernel+fast_global_long_kernel" if info["path"] == 2 else
+                 "fast_wide_kernel" if info.get("wide") else "fast_tiled_kernel")
+        res["fp32_pipe" if not f64 else "fp64_pipe"] = {
+            "scope": kname, "achieved": FAST_PRODUCTS_PER_TERM * terms_fast / (fast_ms * 1e-3) / 1e12, "peak": alu_peak,
+            "unit": "T lane-op/s", "algorithmic_def": f"{FAST_PRODUCTS_PER_TERM} products per literal term (SURVEY 8(d))",
+            "time_ms": fast_ms, "peak_source": alu_src}
+        if info["path"] == 1:
+            smem_peak = SM_COUNT * 128 * mhz * 1e6 / 1e9
+            res["smem"] = {"scope": kname, "achieved": SMEM_BYTES_PER_TERM * terms_fast / (fast_ms * 1e-3) / 1e9,
+                           "peak": smem_peak, "unit": "GB/s",
+                           "algorithmic_def": f"{SMEM_BYTES_PER_TERM} B per term: x tile read + gradient tile read and write",
+                           "time_ms": fast_ms, "peak_source": f"{SM_COUNT} SMs x 128 B/clk x {mhz:.0f} MHz"}
+        kms = fast_ms
+    else:
+        kname, kms = "sym_item_kernel", root_ms
+        res["fp64_pipe" if f64 else "fp32_pipe"] = {
+            "scope": kname, "achieved": ROOT_OPS_PER_LIT_ROOT * info["sym_root_lits"] * B / (root_ms * 1e-3) / 1e12,
+            "peak": alu_peak, "unit": "T lane-op/s",
+            "algorithmic_def": f"{ROOT_OPS_PER_LIT_ROOT} slots per (literal, root) (SURVEY App. A)", "time_ms": root_ms,
+            "peak_source": alu_src}
+    for r in res.values():
+        r["frac"] = r["achieved"] / r["peak"]
+    bound = max(res, key=lambda k: res[k]["frac"])
+    top = res[bound]
+    traffic = top.get("traffic") if bound == "hbm" else ncu_traffic(top["scope"], args.config)
+    return {"bound": bound, "achieved": top["achieved"], "peak": top["peak"], "unit": top["unit"], "frac": top["frac"],
+            "traffic": traffic, "kernel": top["scope"], "kernel_ms": top["time_ms"],
+            "waste": res["hbm"]["waste"], "resources": res,
+            "eval_phase_ms": {"fast": float(ph[0]), "root": float(ph[1]), "grad_reduce": float(ph[2]), "f_reduce": float(ph[3])},
+            "kernel_share_of_eval": kms / eval_ms,
+            "timing": "CUDA events recorded inside libffsat on the launching stream (ffsat_eval_profiled, phases "
+                      "serialised), mean over the profiled evaluations"}
+
+
+def reexec_under_torchrun(args):
+    """`bench.py --gpus N` outside torchrun: run this same command under torch.distributed.run with N ranks."""
+    import socket
+    import subprocess
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__), *sys.argv[1:]]
+    sys.exit(subprocess.call(cmd))
 
 
 def main():
@@ -240,7 +339,11 @@ def main():
     ap.add_argument("--tts-seeds", type=int, default=3, help="time-to-solve seeds on the planted c2 instance (0 = skip)")
     ap.add_argument("--tts-cap", type=float, default=10.0, help="per-seed wall-clock cap in seconds (PAR-2 uses 2x)")
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        reexec_under_torchrun(args)
     rank, world, local = env_rank()
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
     cfg = CONFIGS[args.config]
 
     if args.impl == "reference":
@@ -251,12 +354,14 @@ def main():
     import torch
     import torch.distributed as dist
     import paper_2308_15020_b200 as P
+    from paper_2308_15020_b200 import dist as D
 
-    # one GPU per rank; FFSAT_DIST_BACKEND=gloo lets several ranks share a device (host-path smoke test of the
-    # multi-rank step on a single-GPU box; NCCL refuses duplicate devices)
-    backend = os.environ.get("FFSAT_DIST_BACKEND", "nccl")
+    # one GPU per rank over NCCL; with fewer visible GPUs than ranks (a dry run on a 1-GPU box) the ranks share the
+    # devices over gloo (NCCL refuses two ranks on one device); FFSAT_DIST_BACKEND overrides
+    ndev = torch.cuda.device_count()
+    backend = os.environ.get("FFSAT_DIST_BACKEND", "nccl" if ndev >= world else "gloo")
     if backend != "nccl":
-        local = local % torch.cuda.device_count()
+        local = local % ndev
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
@@ -266,12 +371,11 @@ def main():
             dist.init_process_group(backend)
     inst = cfg["make"]()
     B = cfg["B"]
-    from paper_2308_15020_b200 import dist as D
     if cfg["mode"] == "constraint":
-        se = D.ShardedEval(inst.arrays(), rank, world, device=local)
+        se = D.ShardedEval(inst.arrays(), rank, world, device=local, batch_ref=B)
         ctx = se.ctx
     else:
-        ctx = P.Context.from_instance(inst, device=local)
+        ctx = P.Context.from_instance(inst, device=local, batch_ref=B)
     info = ctx.info
     L = inst.n_lits                       # literal-gradient terms per point of the whole formula
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
@@ -291,8 +395,8 @@ def main():
         def step(i):
             rs.step(i)
 
-    # prime every code path of a step (round end included: CUDA lazy module loading, torch's reduction
-    # kernels) so the first timed round end does not pay one-time costs; then the W warm-up steps
+    # prime every code path of a step (round end included: CUDA lazy module loading, the collectives) so the first
+    # timed round end does not pay one-time costs; then the W warm-up steps
     for i in range(args.round_len):
         step(i)
     for i in range(args.warmup):
@@ -380,58 +484,12 @@ def main():
             flush.zero_()
         phases.append(ctx.eval_profiled(xd, fd, gd, ud))
     ph = np.mean(np.array(phases[2:]), axis=0)  # ms: fast, root, grad-reduce, f-reduce
-    peaks, peak_src = measured_peaks()
-    mhz = float(peaks.get("sm_max_mhz", 1965.0))
-    fast_ms, root_ms = float(ph[0]), float(ph[1])
-    es = 8 if info["precision"] == 64 else 4
-    lanes = FP64_LANES if info["precision"] == 64 else FP32_LANES
-    alu_peak = SM_COUNT * lanes * mhz * 1e6 / 1e12          # T lane-ops/s
-    alu_src = (f"{SM_COUNT} SMs x {lanes} {'FP64' if lanes == FP64_LANES else 'FP32'} lanes x {mhz:.0f} MHz "
-               f"({peak_src} sm_max_mhz); one FMA = one lane-op")
-    if fast_ms >= root_ms and info["path"] == 2:
-        # global fast path: HBM-bound (terms stored for the ordered reduction, x rows gathered)
-        long_fast = any(k > 4 and kd in (0, 1, 2, 5) for k, kd in zip(np.diff(inst.offsets), inst.kind))
-        kname, kms = ("fast_global_kernel+fast_global_long_kernel" if long_fast else "fast_global_kernel"), fast_ms
-        alg_bytes = (info["n_fast_lits"] * B * es + inst.n * B * es + info["n_fast_lits"] * 4 + info["n_fast_cons"] * es)
-        achieved = alg_bytes / (kms * 1e-3) / 1e9
-        peak = float(peaks.get("hbm_gbs", 6650.0))
-        roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                    "algorithmic_bytes": alg_bytes,
-                    "algorithmic_bytes_def": "terms written L_fast*B*es + x read once n*B*es + literal words 4*L_fast + weights es*C_fast",
-                    "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_src})"}
-    elif fast_ms >= root_ms:
-        kname, kms = ("fast_wide_kernel" if info.get("wide") else "fast_tiled_kernel"), fast_ms
-        ops = FAST_OPS_PER_TERM * info["n_fast_lits"] * B
-        achieved = ops / (kms * 1e-3) / 1e12
-        # the resource that binds this kernel (ncu: L1/shared throughput ~74%) is shared-memory bandwidth:
-        # per term the x tile read and the gradient tile read-modify-write, 3 x 4 B, against 128 B/clk/SM
-        smem_bytes = SMEM_BYTES_PER_TERM * info["n_fast_lits"] * B
-        smem_peak = SM_COUNT * 128 * mhz * 1e6 / 1e9   # GB/s
-        smem_ach = smem_bytes / (fast_ms * 1e-3) / 1e9
-        roofline = {"bound": "alu", "achieved": achieved, "peak": alu_peak, "unit": "T lane-op/s",
-                    "algorithmic_ops_per_term": FAST_OPS_PER_TERM, "peak_source": alu_src,
-                    "smem": {"achieved": smem_ach, "peak": smem_peak, "unit": "GB/s", "frac": smem_ach / smem_peak,
-                             "algorithmic_bytes_per_term": SMEM_BYTES_PER_TERM,
-                             "peak_source": f"{SM_COUNT} SMs x 128 B/clk shared-memory bandwidth x {mhz:.0f} MHz"},
-                    "note": "binding resource: shared-memory bandwidth (the smem entry); see DESIGN.md 7"}
-        peak = alu_peak
-    else:
-        kname, kms = "sym_item_kernel", root_ms
-        ops = ROOT_OPS_PER_LIT_ROOT * info["sym_root_lits"] * B
-        achieved = ops / (kms * 1e-3) / 1e12
-        roofline = {"bound": "alu", "achieved": achieved, "peak": alu_peak, "unit": "T lane-op/s",
-                    "algorithmic_ops_per_lit_root": ROOT_OPS_PER_LIT_ROOT, "peak_source": alu_src}
-        peak = alu_peak
-    roofline.update({"frac": achieved / peak, "traffic": ncu_traffic(kname, args.config), "kernel": kname, "kernel_ms": kms,
-                     "eval_phase_ms": {"fast": float(ph[0]), "root": float(ph[1]), "grad_reduce": float(ph[2]),
-                                       "f_reduce": float(ph[3])},
-                     "kernel_share_of_eval": kms / float(np.sum(ph)),
-                     "timing": "CUDA events recorded inside libffsat on the launching stream (ffsat_eval_profiled, "
-                               "phases serialised), mean over the profiled evaluations"})
-    roofline = {k: roofline[k] for k in ("bound", "achieved", "peak", "unit", "frac", "traffic")} | \
-        {k: v for k, v in roofline.items() if k not in ("bound", "achieved", "peak", "unit", "frac", "traffic")}
+    roofline = roofline_of(info, inst, B, ph, args)
 
-    tts = time_to_solve(P, args, local) if (rank == 0 and args.config == "c2" and args.tts_seeds > 0) else None
+    tts = None
+    if args.config == "c2" and args.tts_seeds > 0 and cfg["mode"] == "restart":
+        del search, rs
+        tts = time_to_solve(P, D, args, local, rank, world, dist)
 
     if rank == 0:
         base = None if args.no_cpu_baseline or world > 1 else cpu_baseline(cfg, inst, xd.cpu().numpy())
@@ -441,7 +499,7 @@ def main():
                 "dtype": "f64" if info["precision"] == 64 else "f32", "data": "synthetic",
                 "config": {"workload": cfg["desc"], "n": inst.n, "m": inst.m, "literals": L,
                            "batch_per_gpu": B, "global_batch": B_total, "round_len": args.round_len,
-                           "parallelism": (f"{cfg['mode']}-sharded x{world}" if world > 1 else "single GPU"),
+                           "parallelism": (f"{cfg['mode']}-sharded x{world} ({backend})" if world > 1 else "single GPU"),
                            "l2": "flushed between timed steps (256 MiB write, untimed)" if not args.no_flush else "not flushed",
                            "path": "tiled" if info["path"] == 1 else "global"},
                 "evals_per_s": B_total * args.steps / (ms_max * 1e-3),

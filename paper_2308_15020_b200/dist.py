@@ -190,43 +190,75 @@ class RestartSharded:
 
 
 def solve_sharded(search, check, round_len: int, max_rounds: int, rank: int = 0, world: int = 1, group=None,
-                  timeout_s: float = 0.0):
+                  timeout_s: float = 0.0, poll_every: int = 0):
     """Restart-sharded Alg. 1 over all ranks: every rank runs its points' PGD rounds; at each round end the
-    ranks exchange U_c (C2) and the library's keys (C1 + C4).  All ranks stop together at the first round end whose
+    ranks exchange U_c (C2) and the library's keys (C1 + C4).  All ranks stop together at the first poll whose
     any-solved key is set and return the solution of the lowest solved global point, verified by `check`
     (ffsat_check: the exact host count); otherwise they keep the best incumbent (fetched before the rephase) and
     return UNKNOWN after max_rounds or timeout_s (the same decision on every rank: rank 0's clock is broadcast).
+    poll_every > 0 also polls the any-solved key every poll_every PGD iterations inside a round (trial points whose
+    rounded assignment satisfied everything, captured by the library's PGD step).
 
-    Returns dict(sat, assignment, best_unsat, point, rounds, seconds)."""
+    Returns dict(sat, assignment, best_unsat, point, rounds, iterations, seconds)."""
     import time
     import torch
     import torch.distributed as dist
     rs = RestartSharded(search, round_len, rank, world, group)
+    keys_t = rs.T["keys"]
     t0 = time.perf_counter()
     best_cnt, best_gp, best_a = None, -1, None
     rs.begin()
-    rounds = 0
+    rounds = iters = 0
     stop = torch.zeros(1, dtype=torch.int32, device=rs.T["unsat"].device)
+    poll = poll_every if 0 < poll_every < round_len else round_len
+
+    def solved(gp):
+        a = rs.fetch(gp)
+        return a if check(a)[0] == 0 else None
+
+    def out_of_time():
+        if timeout_s <= 0:
+            return False
+        stop.fill_(1 if (rank == 0 and time.perf_counter() - t0 > timeout_s) else 0)
+        if world > 1:
+            dist.all_reduce(stop, op=dist.ReduceOp.MAX, group=group)
+        return bool(int(stop.item()))
+
+    def done(a, gp):
+        return {"sat": 1, "assignment": a, "best_unsat": 0, "point": gp, "rounds": rounds, "iterations": iters,
+                "seconds": time.perf_counter() - t0}
+
     for rounds in range(1, max_rounds + 1):
-        search.iterate(round_len)
-        keys = rs.exchange().cpu()          # the one host round trip of a round
+        it = 0
+        while it + poll < round_len:                 # mid-round polls of the trial captures
+            search.iterate(poll)
+            it += poll
+            iters += poll
+            search.reduce()
+            if world > 1:
+                dist.all_reduce(keys_t, op=dist.ReduceOp.MIN, group=group)
+            gp = int(keys_t[0].item())
+            if gp != INT64_MAX:
+                a = solved(gp)
+                if a is not None:
+                    return done(a, gp)
+            if out_of_time():
+                break
+        else:
+            search.iterate(round_len - it)
+            iters += round_len - it
+        keys = rs.exchange().cpu()                   # round end: exact check, U_c, keys
         solved_gp, inc = int(keys[0]), int(keys[1])
         if solved_gp != INT64_MAX:
-            a = rs.fetch(solved_gp)
-            n_unsat, _ = check(a)
-            if n_unsat == 0:
-                return {"sat": 1, "assignment": a, "best_unsat": 0, "point": solved_gp, "rounds": rounds,
-                        "seconds": time.perf_counter() - t0}
+            a = solved(solved_gp)
+            if a is not None:
+                return done(a, solved_gp)
         cnt, gp = inc >> 32, inc & 0xFFFFFFFF
         if best_cnt is None or cnt < best_cnt:
             best_a = rs.fetch(gp)
             best_cnt, best_gp = check(best_a)[0], gp
-        if timeout_s > 0:
-            stop.fill_(1 if (rank == 0 and time.perf_counter() - t0 > timeout_s) else 0)
-            if world > 1:
-                dist.all_reduce(stop, op=dist.ReduceOp.MAX, group=group)
-            if int(stop.item()):
-                break
+        if out_of_time():
+            break
         rs.restart()
     return {"sat": 0, "assignment": best_a, "best_unsat": best_cnt, "point": best_gp, "rounds": rounds,
-            "seconds": time.perf_counter() - t0}
+            "iterations": iters, "seconds": time.perf_counter() - t0}

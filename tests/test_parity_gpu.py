@@ -363,9 +363,9 @@ def test_pgd_steps_match_oracle(precision):
     inst = synth.config1(3)
     ctx = P.Context.from_instance(inst, precision=precision, device=0)
     B = 64
-    s = ctx.search(B, seed=9, max_inner=500)
+    s = ctx.search(B, seed=9, max_inner=500, eta0=8.0)      # large steps: both accept and reject branches
     Fo = oracle_of(inst)
-    Pp = osolve.Params(max_inner=500)
+    Pp = osolve.Params(max_inner=500, eta0=8.0)
     tol, eps = TOL[precision], EPS[precision]
     s.begin_round()
     T = s.tensors()
