@@ -282,8 +282,8 @@ def roofline_of(info, inst, B, ph, args):
     if fast_ms >= root_ms:
         kname = ("fast_global_kernel+fast_global_long_kernel" if info["path"] == 2 else
                  "fast_wide_kernel" if info.get("wide") else "fast_tiled_kernel")
-        res["fp32_pipe" if not f64 else "fp64_pipe"] = {
-            "scope": kname, "achieved": FAST_PRODUCTS_PER_TERM * terms_fast / (fast_ms * 1e-3) / 1e12, "peak": alu_peak,
+        res["alu"] = {
+            "scope": kname, "pipe": "fp64" if f64 else "fp32", "achieved": FAST_PRODUCTS_PER_TERM * terms_fast / (fast_ms * 1e-3) / 1e12, "peak": alu_peak,
             "unit": "T lane-op/s", "algorithmic_def": f"{FAST_PRODUCTS_PER_TERM} products per literal term (SURVEY 8(d))",
             "time_ms": fast_ms, "peak_source": alu_src}
         if info["path"] == 1:
@@ -295,8 +295,8 @@ def roofline_of(info, inst, B, ph, args):
         kms = fast_ms
     else:
         kname, kms = "sym_item_kernel", root_ms
-        res["fp64_pipe" if f64 else "fp32_pipe"] = {
-            "scope": kname, "achieved": ROOT_OPS_PER_LIT_ROOT * info["sym_root_lits"] * B / (root_ms * 1e-3) / 1e12,
+        res["alu"] = {
+            "scope": kname, "pipe": "fp64" if f64 else "fp32", "achieved": ROOT_OPS_PER_LIT_ROOT * info["sym_root_lits"] * B / (root_ms * 1e-3) / 1e12,
             "peak": alu_peak, "unit": "T lane-op/s",
             "algorithmic_def": f"{ROOT_OPS_PER_LIT_ROOT} slots per (literal, root) (SURVEY App. A)", "time_ms": root_ms,
             "peak_source": alu_src}

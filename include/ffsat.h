@@ -81,8 +81,9 @@ typedef struct {
 typedef struct {
     int32_t precision;  /* 0 = auto (64 iff some non-fast-path constraint has k > 64), 32, 64 */
     int32_t device;     /* CUDA device ordinal; -1 = host-only context (no GPU needed) */
-    int32_t path;       /* 0 = auto, 1 = force on-chip tiled fast path (64-point kernel when eligible),
-                           2 = force global path, 3 = tiled path with the 32-point kernel only */
+    int32_t path;       /* 0 = auto, 1 = force on-chip tiled fast path (64-point kernel when eligible, its TMEM
+                           variant when n <= 256), 2 = force global path, 3 = tiled path with the 32-point kernel
+                           only, 4 = tiled path without the TMEM variant (64-point shared-memory kernel) */
     int32_t batch_ref;  /* reference batch of the launch plan, 0 = 1024.  The fast kernels' split of the
                            constraints into chunks (and so every partial sum) is planned once, at load, for
                            this batch size and reused for every call: a point's f / grad / unsat bits do not
@@ -102,7 +103,8 @@ typedef struct {
     int64_t n_sym_lits;
     int64_t sym_root_lits;  /* sum over sym constraints of k * M', M' = floor((k+1)/2) */
     int32_t path;           /* 1 tiled, 2 global */
-    int32_t wide;           /* 1 if the tiled path uses the 64-point (two points per lane) kernel */
+    int32_t wide;           /* tiled path kernel: 0 = 32-point, 1 = 64-point (two points per lane) with the gradient tile
+                               in shared memory, 2 = 64-point with the gradient tile in tensor memory (TMEM) */
     int32_t max_k;
     int64_t device_bytes;   /* persistent device memory held by the context */
 } ffsat_info_t;
@@ -148,7 +150,9 @@ typedef struct {
     double armijo_c1;        /* sufficient-decrease constant (default 1e-4) */
     double alpha;            /* ERWA decay (default 0.4) */
     int32_t max_inner;       /* PGD trials per restart round (default 500) */
-    int32_t check_every;     /* ffsat_solve polls every this many iterations (default 10) */
+    int32_t check_every;     /* every check_every-th PGD iteration of a round evaluates the trial points with the
+                                fused exact check of their rounded assignment (A9; a satisfying trial is captured
+                                as solved); the others skip it.  ffsat_solve polls after those iterations (default 10) */
     int32_t policy;          /* rephasing cycle: 0 = ROF, 1 = RF, 2 = R */
     int32_t adaptive_weights;/* 1 = ERWA (decision mode), 0 = fixed weights */
     double timeout_s;        /* ffsat_solve wall-clock limit, <= 0 = none */

@@ -2,7 +2,8 @@
 
 The product is libffsat.so (csrc/, sm_100a CUDA + C++ host layer) behind the C-ABI in
 include/ffsat.h; ffsat.py is its ctypes binding (argument marshalling only) and
-parallel.py the torch.distributed orchestration for restart / constraint sharding.
+dist.py the torch.distributed orchestration for restart / constraint sharding (RestartSharded,
+solve_sharded, ShardedEval).
 """
 from .ffsat import (Context, FfsatError, Search, ffsat_check, ffsat_default_params, ffsat_eval, ffsat_free,
                     ffsat_info, ffsat_load, ffsat_load_file, ffsat_version, lib, LIB_PATH, EXPORTS)

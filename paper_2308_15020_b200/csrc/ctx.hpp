@@ -173,6 +173,7 @@ void eval_device_t(ffsat_ctx* c, Scratch& S, const T* x, int64_t B, double* f, T
 template <typename T>
 void set_tiled_smem(size_t bytes);
 void set_wide_smem(size_t bytes);   // eval_f32.cu
+void set_tmem_smem(size_t bytes);   // eval_f32.cu
 template <typename T>
 void set_long_smem();              // the long global kernel's dynamic shared memory (eval_f32.cu / eval_f64.cu)
 // one root-path launch class (sym_f32.cu / sym_f64.cu)

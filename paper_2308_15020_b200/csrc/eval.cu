@@ -41,8 +41,9 @@ void plan_chunks(ffsat_ctx* c) {
     const int64_t PT = L.wide ? (B + 63) / 64 : (B + 31) / 32;
     int cps = 8;
     if (L.path == 1) {
-        c->tiled_smem = L.wide ? wide_smem_bytes(L.n) : tiled_smem_bytes(L.n, L.precision);
-        cps = std::max(1, (int)std::min<size_t>(8, (228 * 1024) / (c->tiled_smem + (L.precision == 64 ? 4352 : 2304) + 1024)));
+        c->tiled_smem = L.tmem ? tmem_smem_bytes(L.n) : L.wide ? wide_smem_bytes(L.n) : tiled_smem_bytes(L.n, L.precision);
+        cps = L.tmem ? 1   // one CTA per SM: 16 warps, the TMEM allocation
+                     : std::max(1, (int)std::min<size_t>(8, (228 * 1024) / (c->tiled_smem + (L.precision == 64 ? 4352 : 2304) + 1024)));
     }
     const int64_t n_units = (int64_t)L.units.size();
     // global path: units grouped by length class (buckets ascend in k, so each group is a contiguous unit range):
@@ -119,6 +120,7 @@ void plan_chunks(ffsat_ctx* c) {
         if (L.precision == 64) set_tiled_smem<double>(c->tiled_smem);
         else set_tiled_smem<float>(c->tiled_smem);
         if (L.wide) set_wide_smem(c->tiled_smem);
+        if (L.tmem) set_tmem_smem(c->tiled_smem);
     }
     if (ncg[2] > 0) {
         if (L.precision == 64) set_long_smem<double>();

@@ -30,16 +30,34 @@ void launch_tiled_uniform(int k, dim3 grid, size_t smem, cudaStream_t st, const 
     }
 }
 
-inline void launch_wide(int k, int red, dim3 grid, size_t smem, cudaStream_t st, const dev::TiledArgs<float>& a) {
-    switch (k * 4 + red) {
-#define FFSAT_KW(K) case K * 4: dev::fast_wide_kernel<K, 0><<<grid, 256, smem, st>>>(a); break; \
-                    case K * 4 + 1: dev::fast_wide_kernel<K, 1><<<grid, 256, smem, st>>>(a); break; \
-                    case K * 4 + 2: dev::fast_wide_kernel<K, 2><<<grid, 256, smem, st>>>(a); break; \
-                    case K * 4 + 3: dev::fast_wide_kernel<K, 3><<<grid, 256, smem, st>>>(a); break;
+inline void launch_wide(int k, int red, bool check, dim3 grid, size_t smem, cudaStream_t st, const dev::TiledArgs<float>& a) {
+    const int sel = check ? red : 4;   // 0-3: truth reduction of the fused check; 4: no check
+    switch (k * 8 + sel) {
+#define FFSAT_KW(K) case K * 8: dev::fast_wide_kernel<K, 0, true><<<grid, 256, smem, st>>>(a); break; \
+                    case K * 8 + 1: dev::fast_wide_kernel<K, 1, true><<<grid, 256, smem, st>>>(a); break; \
+                    case K * 8 + 2: dev::fast_wide_kernel<K, 2, true><<<grid, 256, smem, st>>>(a); break; \
+                    case K * 8 + 3: dev::fast_wide_kernel<K, 3, true><<<grid, 256, smem, st>>>(a); break; \
+                    case K * 8 + 4: dev::fast_wide_kernel<K, 0, false><<<grid, 256, smem, st>>>(a); break;
         FFSAT_KW(1) FFSAT_KW(2) FFSAT_KW(3) FFSAT_KW(4) FFSAT_KW(5) FFSAT_KW(6) FFSAT_KW(7) FFSAT_KW(8)
         FFSAT_KW(9) FFSAT_KW(10) FFSAT_KW(11) FFSAT_KW(12) FFSAT_KW(13) FFSAT_KW(14) FFSAT_KW(15) FFSAT_KW(16)
 #undef FFSAT_KW
     default: throw Error(FFSAT_ERR_ARG, "wide tiled kernel needs k <= 16");
+    }
+}
+
+inline void launch_tmem(int k, int red, bool check, dim3 grid, size_t smem, uint32_t cols, cudaStream_t st,
+                        const dev::TiledArgs<float>& a) {
+    const int sel = check ? red : 4;
+    switch (k * 8 + sel) {
+#define FFSAT_KT(K) case K * 8: dev::fast_tmem_kernel<K, 0, true><<<grid, 32 * dev::kTmemWarps, smem, st>>>(a, cols); break; \
+                    case K * 8 + 1: dev::fast_tmem_kernel<K, 1, true><<<grid, 32 * dev::kTmemWarps, smem, st>>>(a, cols); break; \
+                    case K * 8 + 2: dev::fast_tmem_kernel<K, 2, true><<<grid, 32 * dev::kTmemWarps, smem, st>>>(a, cols); break; \
+                    case K * 8 + 3: dev::fast_tmem_kernel<K, 3, true><<<grid, 32 * dev::kTmemWarps, smem, st>>>(a, cols); break; \
+                    case K * 8 + 4: dev::fast_tmem_kernel<K, 0, false><<<grid, 32 * dev::kTmemWarps, smem, st>>>(a, cols); break;
+        FFSAT_KT(1) FFSAT_KT(2) FFSAT_KT(3) FFSAT_KT(4) FFSAT_KT(5) FFSAT_KT(6) FFSAT_KT(7) FFSAT_KT(8)
+        FFSAT_KT(9) FFSAT_KT(10) FFSAT_KT(11) FFSAT_KT(12) FFSAT_KT(13) FFSAT_KT(14) FFSAT_KT(15) FFSAT_KT(16)
+#undef FFSAT_KT
+    default: throw Error(FFSAT_ERR_ARG, "TMEM tiled kernel needs k <= 16");
     }
 }
 
@@ -132,10 +150,17 @@ void eval_device_t(ffsat_ctx* c, Scratch& S, const T* x, int64_t B, double* f, T
             dim3 grid((unsigned)PT, (unsigned)c->n_chunks);
             const int km = fast_kmax(L);
             const int ku = uniform_k(L);
-            if (L.wide) {
+            if (L.tmem) {
                 if constexpr (sizeof(T) == 4) {
                     dim3 gw((unsigned)((B + 63) / 64), (unsigned)c->n_chunks);
-                    launch_wide(ku, L.wide_red, gw, c->tiled_smem, st, a);
+                    dev::TiledArgs<float> at = a;
+                    at.words = c->fast_words.as<uint32_t>();   // var | neg << 31 (the TMEM column is 2 var)
+                    launch_tmem(ku, L.wide_red, unsat != nullptr, gw, c->tiled_smem, tmem_cols(L.n), st, at);
+                }
+            } else if (L.wide) {
+                if constexpr (sizeof(T) == 4) {
+                    dim3 gw((unsigned)((B + 63) / 64), (unsigned)c->n_chunks);
+                    launch_wide(ku, L.wide_red, unsat != nullptr, gw, c->tiled_smem, st, a);
                 }
             } else if (ku > 0) launch_tiled_uniform<T>(ku, grid, c->tiled_smem, st, a);
             else if (km <= 4) dev::fast_tiled_kernel<T, 4><<<grid, 256, c->tiled_smem, st>>>(a);

@@ -38,15 +38,18 @@ struct ffsat_search {
     DBuf W;                       // this search's current weights (position order, context dtype): ERWA state
     Scratch sc;                   // this search's evaluation scratch (referenced by its captured graph)
     int64_t round = 0, iters_issued = 0;
-    // one CLS iteration captured as a CUDA graph (replayed by ffsat_search_iterate)
+    // one CLS iteration captured as a CUDA graph (replayed by ffsat_search_iterate), in two variants: [1] with the
+    // fused check of the trial points (every check_every-th iteration of a round), [0] without
     cudaStream_t cap_stream = nullptr;
-    cudaGraphExec_t iter_exec = nullptr;
-    int64_t iter_kernels = 0;     // kernels in one captured iteration (launch accounting)
+    cudaGraphExec_t iter_exec[2] = {nullptr, nullptr};
+    int64_t iter_kernels[2] = {0, 0};   // kernels in one captured iteration (launch accounting)
     bool graph_failed = false;
     ~ffsat_search() {
-        if (iter_exec) cudaGraphExecDestroy(iter_exec);
+        for (cudaGraphExec_t& g : iter_exec)
+            if (g) cudaGraphExecDestroy(g);
         if (cap_stream) cudaStreamDestroy(cap_stream);
     }
+    bool checked_next() const { return (iters_issued + 1) % P.check_every == 0; }
 };
 
 namespace {
@@ -245,13 +248,13 @@ void search_alloc(ffsat_search* s) {
     CK(cudaMemset(s->done.p, 0, (size_t)B * 4));
 }
 
-dev::PgdArgs pgd_args(ffsat_search* s, int mode) {
+dev::PgdArgs pgd_args(ffsat_search* s, int mode, bool checked) {
     dev::PgdArgs a{};
     a.B = s->B; a.n = s->ctx->Lo.n; a.eta0 = s->P.eta0; a.eta_min = s->P.eta_min; a.c1 = s->P.armijo_c1;
     a.max_inner = s->P.max_inner; a.X = s->X.p; a.Xp = s->Xp.p; a.Gx = s->Gx.p; a.Gp = s->Gp.p;
     a.fX = s->fX.as<double>(); a.fP = s->fP.as<double>(); a.dot = s->dot.as<double>(); a.eta = s->eta.as<double>();
     a.done = s->done.as<int32_t>(); a.iters = s->iters.as<int32_t>(); a.unsatP = s->unsatP.as<int32_t>();
-    a.solved = s->solved.as<int32_t>(); a.sol = s->sol.as<int8_t>(); a.mode = mode;
+    a.solved = s->solved.as<int32_t>(); a.sol = s->sol.as<int8_t>(); a.mode = mode; a.checked = checked ? 1 : 0;
     return a;
 }
 
@@ -262,79 +265,86 @@ void search_begin_round(ffsat_search* s, cudaStream_t st) {
                                                                     s->iters.as<int32_t>(), s->B, s->P.eta0);
     if (f64) search_eval<double>(s, s->X.p, s->fX.as<double>(), s->Gx.p, s->unsatP.as<int32_t>(), st);
     else search_eval<float>(s, s->X.p, s->fX.as<double>(), s->Gx.p, s->unsatP.as<int32_t>(), st);
-    dev::PgdArgs a = pgd_args(s, 0);
+    dev::PgdArgs a = pgd_args(s, 0, true);
     if (f64) dev::pgd_step_kernel<double><<<(unsigned)s->B, 256, 0, st>>>(a);
     else dev::pgd_step_kernel<float><<<(unsigned)s->B, 256, 0, st>>>(a);
     CK(cudaGetLastError());
     s->iters_issued = 0;
 }
 
-void search_iterate_direct(ffsat_search* s, int n_iters, cudaStream_t st);
+void search_iterate_one(ffsat_search* s, bool checked, cudaStream_t st);
 
-// Capture one iteration (eval + PGD step, forked root-path streams included) into a graph once per search;
-// afterwards each iteration is one cudaGraphLaunch (no per-kernel launch latency on the host or device).
+// Capture one iteration of each variant (eval + PGD step, forked root-path streams included) into a graph once per
+// search; afterwards each iteration is one cudaGraphLaunch (no per-kernel launch latency on the host or device).
 bool search_capture(ffsat_search* s) {
-    if (s->iter_exec) return true;
+    if (s->iter_exec[0] && s->iter_exec[1]) return true;
     if (s->graph_failed) return false;
     if (!s->cap_stream) CK(cudaStreamCreateWithFlags(&s->cap_stream, cudaStreamNonBlocking));
-    // the graph references only this search's buffers (sized at create: allocations never happen inside a
+    // the graphs reference only this search's buffers (sized at create: allocations never happen inside a
     // capture) and the context's persistent layout, which is never reallocated after load
     ensure_scratch(s->ctx, s->sc, s->B);
     s->ctx->ensure_side_streams();
-    const int64_t before = s->ctx->launches, iters_before = s->iters_issued;
-    cudaGraph_t g = nullptr;
-    if (cudaStreamBeginCapture(s->cap_stream, cudaStreamCaptureModeThreadLocal) != cudaSuccess) {
-        cudaGetLastError();
-        s->graph_failed = true;
-        return false;
+    const int64_t before = s->ctx->launches;
+    for (int v = 0; v < 2; ++v) {
+        cudaGraph_t g = nullptr;
+        if (cudaStreamBeginCapture(s->cap_stream, cudaStreamCaptureModeThreadLocal) != cudaSuccess) {
+            cudaGetLastError();
+            s->graph_failed = true;
+            return false;
+        }
+        const int64_t l0 = s->ctx->launches;
+        bool ok = true;
+        try {
+            search_iterate_one(s, v == 1, s->cap_stream);
+        } catch (const Error&) {
+            ok = false;
+        }
+        const cudaError_t e = cudaStreamEndCapture(s->cap_stream, &g);
+        s->iter_kernels[v] = s->ctx->launches - l0;
+        if (!ok || e != cudaSuccess || !g || cudaGraphInstantiate(&s->iter_exec[v], g, 0) != cudaSuccess) {
+            cudaGetLastError();
+            if (g) cudaGraphDestroy(g);
+            for (cudaGraphExec_t& x : s->iter_exec)
+                if (x) { cudaGraphExecDestroy(x); x = nullptr; }
+            s->graph_failed = true;
+            s->ctx->launches = before;
+            return false;
+        }
+        cudaGraphDestroy(g);
     }
-    bool ok = true;
-    try {
-        search_iterate_direct(s, 1, s->cap_stream);
-    } catch (const Error&) {
-        ok = false;
-    }
-    const cudaError_t e = cudaStreamEndCapture(s->cap_stream, &g);
-    s->iters_issued = iters_before;
-    if (!ok || e != cudaSuccess || !g || cudaGraphInstantiate(&s->iter_exec, g, 0) != cudaSuccess) {
-        cudaGetLastError();
-        if (g) cudaGraphDestroy(g);
-        s->iter_exec = nullptr;
-        s->graph_failed = true;
-        s->ctx->launches = before;
-        return false;
-    }
-    cudaGraphDestroy(g);
-    s->iter_kernels = s->ctx->launches - before;
     s->ctx->launches = before;
     return true;
 }
 
 void search_iterate(ffsat_search* s, int n_iters, cudaStream_t st) {
-    if (n_iters > 0 && search_capture(s)) {
-        for (int i = 0; i < n_iters; ++i) CK(cudaGraphLaunch(s->iter_exec, st));
-        s->ctx->launches += s->iter_kernels * n_iters;
-        s->iters_issued += n_iters;
-        return;
+    const bool graphs = n_iters > 0 && search_capture(s);
+    for (int i = 0; i < n_iters; ++i) {
+        const bool chk = s->checked_next();
+        if (graphs) {
+            CK(cudaGraphLaunch(s->iter_exec[chk ? 1 : 0], st));
+            s->ctx->launches += s->iter_kernels[chk ? 1 : 0];
+        } else {
+            search_iterate_one(s, chk, st);
+        }
+        s->iters_issued += 1;
     }
-    search_iterate_direct(s, n_iters, st);
 }
 
-void search_iterate_direct(ffsat_search* s, int n_iters, cudaStream_t st) {
+// One PGD iteration: evaluate the trial points (with the fused check of their rounded assignment when `checked`),
+// then the Armijo accept / eta update / next trial point.
+void search_iterate_one(ffsat_search* s, bool checked, cudaStream_t st) {
     const bool f64 = s->ctx->Lo.precision == 64;
-    dev::PgdArgs a = pgd_args(s, 1);
-    for (int i = 0; i < n_iters; ++i) {
-        s->ctx->launches += 1;
-        if (f64) {
-            search_eval<double>(s, s->Xp.p, s->fP.as<double>(), s->Gp.p, s->unsatP.as<int32_t>(), st);
-            dev::pgd_step_kernel<double><<<(unsigned)s->B, 256, 0, st>>>(a);
-        } else {
-            search_eval<float>(s, s->Xp.p, s->fP.as<double>(), s->Gp.p, s->unsatP.as<int32_t>(), st);
-            launch_pdl(dev::pgd_step_kernel<float>, dim3((unsigned)s->B), dim3(256), 0, st, a);
-        }
+    dev::PgdArgs a = pgd_args(s, 1, checked);
+    int32_t* u = checked ? s->unsatP.as<int32_t>() : nullptr;
+    s->ctx->launches += 1;
+    if (f64) {
+        search_eval<double>(s, s->Xp.p, s->fP.as<double>(), s->Gp.p, u, st);
+        dev::pgd_step_kernel<double><<<(unsigned)s->B, 256, 0, st>>>(a);
+    } else {
+        search_eval<float>(s, s->Xp.p, s->fP.as<double>(), s->Gp.p, u, st);
+        launch_pdl(dev::pgd_step_kernel<float>, dim3((unsigned)s->B), dim3(256), 0, st, a);
     }
     CK(cudaGetLastError());
-    s->iters_issued += n_iters;
 }
 
 void check_kernels(ffsat_search* s, cudaStream_t st);
@@ -506,7 +516,7 @@ ffsat_status ffsat_info(const ffsat_ctx* c, ffsat_info_t* o) {
     const Layout& L = c->Lo;
     o->n_vars = L.n; o->precision = L.precision; o->n_cons = L.m; o->n_lits = L.L;
     o->n_fast_cons = L.n_fast; o->n_sym_cons = L.n_sym; o->n_fast_lits = L.n_fast_lits; o->n_sym_lits = L.n_sym_lits;
-    o->sym_root_lits = L.sym_root_lits; o->path = L.path; o->wide = L.wide ? 1 : 0; o->max_k = L.max_k; o->device_bytes = c->persistent_bytes;
+    o->sym_root_lits = L.sym_root_lits; o->path = L.path; o->wide = L.tmem ? 2 : L.wide ? 1 : 0; o->max_k = L.max_k; o->device_bytes = c->persistent_bytes;
     return FFSAT_OK;
     ABI_CATCH(nullptr)
 }

@@ -228,6 +228,12 @@ size_t tiled_smem_bytes(int n, int precision) {
 }
 
 size_t wide_smem_bytes(int n) { return std::max<size_t>(4 * (size_t)kWidePitch * (size_t)n, 6144); }  // >= the final f / unsat exchange (8 x 64 x 12 B)
+size_t tmem_smem_bytes(int n) { return std::max<size_t>(2 * 256 * (size_t)n, 12288); }   // x tile + 2nd sum tile; >= 16 x 64 x 12 B
+uint32_t tmem_cols(int n) {
+    uint32_t c = 32;
+    while (c < 2u * (uint32_t)n) c <<= 1;
+    return c;
+}
 
 int wide_max_n() {
     const size_t budget = 227 * 1024 - 4608;
@@ -337,10 +343,11 @@ Layout build_layout(const Formula& F, int path, int precision) {
 
     // ---- path: tiled (x and gradient tiles in shared memory) when n fits, else global
     const bool allow_wide = path != 3;   // 3 = tiled path with the 32-point kernel only (tests)
-    if (path == 3) path = 1;
+    const bool allow_tmem = path != 4;   // 4 = tiled path without the TMEM kernel (the shared-memory 64-point kernel)
+    if (path == 3 || path == 4) path = 1;
     if (path == 0) path = (!fast_ids.empty() && F.n <= tiled_max_n(precision)) ? 1 : 2;
     if (path == 1 && F.n > tiled_max_n(precision)) throw Error(FFSAT_ERR_ARG, "tiled path needs n <= " + std::to_string(tiled_max_n(precision)));
-    if (path != 1 && path != 2) throw Error(FFSAT_ERR_ARG, "path must be 0, 1, 2 or 3");
+    if (path != 1 && path != 2) throw Error(FFSAT_ERR_ARG, "path must be 0 .. 4");
     Lo.path = path;
 
     // ---- tiled path: within each (k, variant) run, group constraints into var-disjoint classes and make
@@ -490,6 +497,7 @@ Layout build_layout(const Formula& F, int path, int precision) {
             uniform = uniform && nch == 1 && b.k <= 16 && b.k == Lo.fbuckets[0].k;
         }
         Lo.wide = allow_wide && precision == 32 && uniform && F.n <= wide_max_n();
+        Lo.tmem = Lo.wide && allow_tmem && F.n <= kTmemMaxN && kClassCap <= 16;
         auto red_of = [](int variant) {
             return variant == V_OR || variant == V_NOR ? 1 : variant == V_AND || variant == V_NAND ? 2
                  : variant == V_XOR || variant == V_XNOR ? 3 : 0;

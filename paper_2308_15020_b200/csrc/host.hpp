@@ -81,6 +81,7 @@ int sym_roots(int k);               // roots per pass on the root path
 struct Layout {
     int32_t n = 0, path = 0, precision = 32, max_k = 0;
     bool wide = false;                  // tiled path with 64 points per CTA (fp32, uniform single-channel k <= 16)
+    bool tmem = false;                  // ... with the gradient tile in tensor memory (n <= 256; else shared memory)
     int32_t wide_red = 0;               // the bit reduction (1 OR, 2 AND, 3 XOR) shared by every fast bucket, or 0
     int64_t m = 0, L = 0;
     std::vector<int64_t> order;     // position -> original constraint index (fast first, then sym)
@@ -121,6 +122,9 @@ int tiled_max_n(int precision);
 size_t tiled_smem_bytes(int n, int precision);
 int wide_max_n();                   // largest n for the wide (64-point) fp32 tiled kernel
 size_t wide_smem_bytes(int n);
+size_t tmem_smem_bytes(int n);      // the TMEM kernel's dynamic shared memory: x tile [n][64] fp32 (>= the f / unsat exchange)
+uint32_t tmem_cols(int n);          // TMEM columns it allocates: the power of two >= 2 n (>= 32)
+constexpr int kTmemMaxN = 256;
 // Greedy partition of one bucket's constraints into var-disjoint classes of at most `cap` members
 // (first fit over the most recent `window` open classes).  Returns class id per constraint.
 std::vector<int32_t> disjoint_classes(const std::vector<std::vector<int32_t>>& vars, int32_t n, int cap, int window);

@@ -618,79 +618,137 @@ __device__ __forceinline__ void sts2(uint32_t addr, float2 v) {
     asm volatile("st.shared.v2.f32 [%0], {%1, %2};" ::"r"(addr), "f"(v.x), "f"(v.y) : "memory");
 }
 
-template <int K, int RED>
-__device__ __forceinline__ void wide_clause(const BucketReg<float>& bk, int redpol, const uint32_t* sw, float wc, uint32_t xl,
-                                            double& f0, double& f1, int& u0, int& u1) {
-    uint32_t w[K];
-    load_words_smem<K>(sw, w);
-    uint32_t ad[K];
-    float2 xv[K];
-    uint32_t t0 = red_init<RED>(), t1 = red_init<RED>();
+// NC (1 or 2) clauses of one var-disjoint class for the lane's two points, interleaved: every shared-memory load
+// of both clauses is issued before the arithmetic (the clauses share no variable, so the gradient entries of the
+// second cannot alias the first's stores) and the two prefix / suffix chains run side by side -- twice the
+// instruction-level parallelism of one clause between the class barriers.  CHECK: also the satisfaction bit of
+// the rounded points (A9, fused), one LOP3 per literal and point.  fe2 accumulates w * FE of the two points.
+template <int K, int RED, bool CHECK, int NC>
+__device__ __forceinline__ void wide_clauses(const BucketReg<float>& bk, int redpol, const uint32_t* sw0, const uint32_t* sw1,
+                                             float wc0, float wc1, uint32_t xl, float2& fe2, int& u0, int& u1) {
+    uint32_t ad[NC][K];
+    float cs[NC][K];
+    float2 xv[NC][K];
 #pragma unroll
-    for (int i = 0; i < K; ++i) {
-        ad[i] = xl + (w[i] << 2);
-        xv[i] = lds2(ad[i]);
-        if (RED == 0) {
-            t0 += lit_true(xv[i].x, w[i]);
-            t1 += lit_true(xv[i].y, w[i]);
-        } else {
-            t0 = red_step<RED>(t0, xv[i].x, w[i]);
-            t1 = red_step<RED>(t1, xv[i].y, w[i]);
+    for (int c = 0; c < NC; ++c) {
+        uint32_t w[K];
+        load_words_smem<K>(c == 0 ? sw0 : sw1, w);
+#pragma unroll
+        for (int i = 0; i < K; ++i) {
+            ad[c][i] = xl + (w[i] << 2);
+            cs[c][i] = flip_sign(bk.c1[0], w[i]);
+        }
+    }
+#pragma unroll
+    for (int c = 0; c < NC; ++c)
+#pragma unroll
+        for (int i = 0; i < K; ++i) xv[c][i] = lds2(ad[c][i]);
+    float2 gv[NC][K];
+#pragma unroll
+    for (int c = 0; c < NC; ++c)
+#pragma unroll
+        for (int i = 0; i < K; ++i) gv[c][i] = lds2(ad[c][i] + 4 * kWHalf);
+    if (CHECK) {
+#pragma unroll
+        for (int c = 0; c < NC; ++c) {
+            uint32_t t0 = red_init<RED>(), t1 = red_init<RED>();
+#pragma unroll
+            for (int i = 0; i < K; ++i) {
+                // the literal's sign bit is the sign bit of cs (c1 > 0 is flipped iff negated): cs ^ c1 recovers it
+                const uint32_t wneg = __float_as_uint(cs[c][i]) ^ __float_as_uint(bk.c1[0]);
+                if (RED == 0) {
+                    t0 += lit_true(xv[c][i].x, wneg);
+                    t1 += lit_true(xv[c][i].y, wneg);
+                } else {
+                    t0 = red_step<RED>(t0, xv[c][i].x, wneg);
+                    t1 = red_step<RED>(t1, xv[c][i].y, wneg);
+                }
+            }
+            if (RED == 0) {
+                u0 += rule_sat((int)t0, bk.tmin, bk.tmax, bk.parity) ? 0 : 1;
+                u1 += rule_sat((int)t1, bk.tmin, bk.tmax, bk.parity) ? 0 : 1;
+            } else {   // unsat iff the reduced bit differs from the satisfying value
+                u0 += (int)((t0 >> 31) ^ (uint32_t)redpol);
+                u1 += (int)((t1 >> 31) ^ (uint32_t)redpol);
+            }
         }
     }
     const float2 c0 = make_float2(bk.c0[0], bk.c0[0]);
-    float2 av[K], pre[K];
-    float cs[K];
+    float2 av[NC][K], pre[NC][K];
 #pragma unroll
-    for (int i = 0; i < K; ++i) {
-        cs[i] = flip_sign(bk.c1[0], w[i]);
-        av[i] = __ffma2_rn(make_float2(cs[i], cs[i]), xv[i], c0);
-        if (i > 0) pre[i] = i == 1 ? av[0] : __fmul2_rn(pre[i - 1], av[i - 1]);   // pre[0] = 1 is implicit
+    for (int i = 0; i < K; ++i)
+#pragma unroll
+        for (int c = 0; c < NC; ++c) {
+            av[c][i] = __ffma2_rn(make_float2(cs[c][i], cs[c][i]), xv[c][i], c0);
+            if (i > 0) pre[c][i] = i == 1 ? av[c][0] : __fmul2_rn(pre[c][i - 1], av[c][i - 1]);   // pre[0] = 1 implicit
+        }
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+        const float wc = c == 0 ? wc0 : wc1;
+        const float2 run = K == 1 ? av[c][0] : __fmul2_rn(pre[c][K - 1], av[c][K - 1]);
+        const float2 fe = __ffma2_rn(make_float2(bk.g[0], bk.g[0]), run, make_float2(bk.g0, bk.g0));
+        fe2 = __ffma2_rn(make_float2(wc, wc), fe, fe2);
     }
-    const float2 run = K == 1 ? av[0] : __fmul2_rn(pre[K - 1], av[K - 1]);
-    const float2 fe = __ffma2_rn(make_float2(bk.g[0], bk.g[0]), run, make_float2(bk.g0, bk.g0));
-    const float sw0 = bk.g[0] * wc;
-    float2 suf = make_float2(sw0, sw0);
-    // the constraint's variables are distinct, so all gradient entries are read before any is written
-    // (the compiler cannot prove the addresses differ; loading them up front removes the LDS -> FFMA2 -> STS
-    // serialisation per literal)
-    float2 gv[K];
+    float2 suf[NC];
 #pragma unroll
-    for (int i = 0; i < K; ++i) gv[i] = lds2(ad[i] + 4 * kWHalf);
-#pragma unroll
-    for (int i = K - 1; i >= 0; --i) {
-        gv[i] = __ffma2_rn(i == 0 ? suf : __fmul2_rn(pre[i], suf), make_float2(cs[i], cs[i]), gv[i]);
-        if (i > 0) suf = __fmul2_rn(suf, av[i]);
+    for (int c = 0; c < NC; ++c) {
+        const float sw = bk.g[0] * (c == 0 ? wc0 : wc1);
+        suf[c] = make_float2(sw, sw);
     }
 #pragma unroll
-    for (int i = 0; i < K; ++i) sts2(ad[i] + 4 * kWHalf, gv[i]);
-    f0 += (double)(wc * fe.x);
-    f1 += (double)(wc * fe.y);
-    if (RED == 0) {
-        u0 += rule_sat((int)t0, bk.tmin, bk.tmax, bk.parity) ? 0 : 1;
-        u1 += rule_sat((int)t1, bk.tmin, bk.tmax, bk.parity) ? 0 : 1;
-    } else {   // unsat iff the reduced bit differs from the satisfying value
-        u0 += (int)((t0 >> 31) ^ (uint32_t)redpol);
-        u1 += (int)((t1 >> 31) ^ (uint32_t)redpol);
-    }
+    for (int i = K - 1; i >= 0; --i)
+#pragma unroll
+        for (int c = 0; c < NC; ++c) {
+            gv[c][i] = __ffma2_rn(i == 0 ? suf[c] : __fmul2_rn(pre[c][i], suf[c]), make_float2(cs[c][i], cs[c][i]), gv[c][i]);
+            if (i > 0) suf[c] = __fmul2_rn(suf[c], av[c][i]);
+        }
+#pragma unroll
+    for (int c = 0; c < NC; ++c)
+#pragma unroll
+        for (int i = 0; i < K; ++i) sts2(ad[c][i] + 4 * kWHalf, gv[c][i]);
 }
 
-// The staging of the next unit (words + weights) by warp 0 only: lanes copy 16-byte pieces.
-__device__ __forceinline__ void stage_unit_w0(const TiledArgs<float>& a, const UnitDev& U, TileStage<float>& st, int buf, int lane) {
-    const int nwords = min(unit_count(U) * unit_kp(U), kStageWords);
-    for (int q = lane * 4; q < nwords; q += 128) cp_async16(&st.words[buf][q], a.words + (int64_t)U.word_begin + q);
-    if (lane < min(unit_count(U), kStageCons)) cp_async_small<4>(&st.w[buf][lane], a.w_pos + (int64_t)U.pos_begin + lane);
+// The staging of a class (literal words + weights) spread over the CTA: lane l < 8 of warp w copies 16-byte word
+// chunk 8 w + l (a class holds <= 16 rows of <= 16 words = 64 chunks), lanes 8, 9 copy weights 2 w, 2 w + 1; lane
+// 10 of warp 0 copies the header of the class after it into the header ring.
+template <int K>
+__device__ __forceinline__ void stage_class(const TiledArgs<float>& a, const UnitDev& U, int u, int u1, TileStage<float>& st,
+                                            UnitDev* hdr, int buf, int warp, int lane) {
+    constexpr int KP = K_PAD(K);
+    const int count = unit_count(U);
+    const int q = warp * 8 + lane;
+    if (lane < 8 && q * 4 < count * KP) cp_async16(&st.words[buf][q * 4], a.words + (int64_t)U.word_begin + q * 4);
+    const int j = warp * 2 + (lane - 8);
+    if (lane >= 8 && lane < 10 && j < count) cp_async_small<4>(&st.w[buf][j], a.w_pos + (int64_t)U.pos_begin + j);
+    if (warp == 0 && lane == 10 && u + 1 < u1) cp_async16(&hdr[(u + 1) & 3], a.units + u + 1);
 }
 
-template <int K, int RED>
+// Wide tiled kernel: 8 warps x 2 points per lane = 64 points per CTA; the chunk's var-disjoint classes (<= 16
+// clauses, host kClassCap) one after the other, warp w taking clauses w and w + 8 of a class together, a barrier
+// between classes (the gradient tile's fixed accumulation order).  Class headers come through a 4-entry ring in
+// shared memory (cp.async two classes ahead), so no register waits on a header load.  CHECK = false: the evaluation
+// does not count falsified constraints (PGD iterations between checks), which removes the truth reductions.
+template <int K, int RED, bool CHECK>
 __global__ void __launch_bounds__(256, 2) fast_wide_kernel(TiledArgs<float> a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];   // >= 6 KB (host: wide_smem_bytes)
     __shared__ __align__(16) TileStage<float> st;
+    __shared__ __align__(16) UnitDev hdr[4];                     // header ring: class u at hdr[u & 3]
     const int n = a.n;
     float* xs = reinterpret_cast<float*>(smem_raw);              // [n][kWPitch]
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int64_t b0 = (int64_t)blockIdx.x * 64;
     const int chunk = blockIdx.y;
+    const int u0 = a.chunk_units[chunk], u1 = a.chunk_units[chunk + 1];
+    if (u0 < u1) {   // the first two classes' staging overlaps the x tile load
+        const UnitDev h0 = a.units[u0];
+        if (threadIdx.x == 0) hdr[u0 & 3] = h0;
+        stage_class<K>(a, h0, u0, u1, st, hdr, 0, warp, lane);
+        if (u0 + 1 < u1) {
+            const UnitDev h1 = a.units[u0 + 1];
+            stage_class<K>(a, h1, u0 + 1, u1, st, hdr, 1, warp, lane);
+        }
+    }
+    cp_async_commit();
 
     // x tile load: 8 independent global loads in flight per thread (the loop is latency-bound otherwise)
     {
@@ -714,29 +772,18 @@ __global__ void __launch_bounds__(256, 2) fast_wide_kernel(TiledArgs<float> a) {
             }
         }
     }
+    cp_async_wait_all();
     __syncthreads();
 
     double f0 = 0.0, f1 = 0.0;
     int uc0 = 0, uc1 = 0;
     const uint32_t xl32 = (uint32_t)__cvta_generic_to_shared(xs + 2 * lane);   // this lane's x pair in row 0
-    const int u0 = a.chunk_units[chunk], u1 = a.chunk_units[chunk + 1];
-    UnitDev cur{}, next{}, after{};
-    if (u0 < u1) {
-        cur = a.units[u0];
-        if (warp == 0) stage_unit_w0(a, cur, st, 0, lane);
-        if (u0 + 1 < u1) {
-            next = a.units[u0 + 1];
-            if (warp == 0) stage_unit_w0(a, next, st, 1, lane);
-        }
-        if (u0 + 2 < u1) after = a.units[u0 + 2];
-    }
-    cp_async_commit_wait_all();
-    __syncthreads();
     int bucket = -1;
     BucketReg<float> bk{};
     int redpol = 0;   // 1: satisfied iff the reduced bit is set, so unsat = bit ^ 1
     int buf = 0;
     for (int u = u0; u < u1; ++u) {
+        const UnitDev cur = hdr[u & 3];
         if (cur.bucket != bucket) {
             bucket = cur.bucket;
             bk = load_bucket<float>(a.buckets + bucket);
@@ -745,21 +792,25 @@ __global__ void __launch_bounds__(256, 2) fast_wide_kernel(TiledArgs<float> a) {
         const uint32_t* sw = st.words[buf];
         const float* swt = st.w[buf];
         const int count = unit_count(cur);
-        for (int j = warp; j < count; j += nw) wide_clause<K, RED>(bk, redpol, sw + j * K_PAD(K), swt[j], xl32, f0, f1, uc0, uc1);
-        // advance: the next unit's words are ready, everybody is done with this buffer
+        float2 fe2 = make_float2(0.0f, 0.0f);
+        if (warp + 8 < count)
+            wide_clauses<K, RED, CHECK, 2>(bk, redpol, sw + warp * K_PAD(K), sw + (warp + 8) * K_PAD(K), swt[warp],
+                                           swt[warp + 8], xl32, fe2, uc0, uc1);
+        else if (warp < count)
+            wide_clauses<K, RED, CHECK, 1>(bk, redpol, sw + warp * K_PAD(K), sw, swt[warp], 0.0f, xl32, fe2, uc0, uc1);
+        f0 += (double)fe2.x;
+        f1 += (double)fe2.y;
+        // advance: class u + 1's words and header u + 2 are in shared memory, everybody is done with this buffer
         cp_async_wait_all();
         __syncthreads();
-        cur = next;
-        next = after;
         buf ^= 1;
-        if (u + 2 < u1 && warp == 0) stage_unit_w0(a, next, st, buf ^ 1, lane);
+        if (u + 2 < u1) stage_class<K>(a, hdr[(u + 2) & 3], u + 2, u1, st, hdr, buf ^ 1, warp, lane);
         cp_async_commit();
-        if (u + 3 < u1) after = a.units[u + 3];
     }
     pdl_trigger();   // the gradient reduction may be scheduled now (it waits for this grid to complete)
     // outputs: partial gradient tile (float2 per lane), partial f / unsat (fixed warp order)
     const int64_t b = b0 + 2 * lane;
-    for (int v = warp; v < n; v += nw) {
+    for (int v = warp; v < n; v += 8) {
         const float2 g = *reinterpret_cast<const float2*>(xs + v * kWPitch + kWHalf + 2 * lane);
         float* dst = a.P + ((int64_t)chunk * n + v) * a.B + b;
         if (b + 1 < a.B && ((a.B & 1) == 0)) *reinterpret_cast<float2*>(dst) = g;
@@ -782,12 +833,323 @@ __global__ void __launch_bounds__(256, 2) fast_wide_kernel(TiledArgs<float> a) {
         if (bp < a.B) {
             double f = 0.0;
             int uc = 0;
-            for (int w = 0; w < nw; ++w) {
+            for (int w = 0; w < 8; ++w) {
                 f += fr[w * 64 + p];
                 uc += ur[w * 64 + p];
             }
             a.fpart[(int64_t)chunk * a.B + bp] = f;
-            a.upart[(int64_t)chunk * a.B + bp] = uc;
+            if (CHECK) a.upart[(int64_t)chunk * a.B + bp] = uc;
+        }
+    }
+}
+
+// ------------------------------------------------------------------------------------------------
+// TMEM tiled kernel (fp32, uniform single-channel k <= 16, n <= 256): the wide kernel's arithmetic with the
+// gradient tile in TENSOR MEMORY instead of shared memory.  The gradient read-modify-write of every literal term
+// (8 of the 12 bytes per term) leaves the shared-memory pipe, which bound the wide kernel (ncu: L1/TEX ~80 % busy),
+// for TMEM's own datapath (tcgen05.ld / tcgen05.st, measured 2.5 SM-cycles per 32-lane x 2-column RMW against 4.0
+// for LDS.64 + STS.64, scripts/tmem_probe.cu); shared memory keeps only the x tile reads.
+//
+// A CTA = 16 warps over 64 points (lane = points 2 l, 2 l + 1, as in the wide kernel).  TMEM lane quadrant q
+// (lanes 32 q .. 32 q + 31, reachable only from warps w with w % 4 == q) holds warp group q's private partial gradient
+// tile of those 64 points: column 2 v + j = variable v, point 2 l + j of lane l.  Group q (warps q, q + 4, q + 8,
+// q + 12) takes classes q, q + 4, q + 8, ... of the chunk; a class's <= 16 clauses go 4 per warp (two interleaved
+// pairs) and a named barrier of the group (128 threads) separates its classes -- the fixed accumulation order of
+// the tile, deterministic without atomics.  At the end the four quadrant tiles are summed in quadrant order into
+// the chunk's partial tile.  One CTA per SM (the allocation is the whole 512-column TMEM when n > 128).
+constexpr int kTmemWarps = 16;
+
+__device__ __forceinline__ void tmem_ld2(uint32_t taddr, float2& v) {
+    uint32_t r0, r1;
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x2.b32 {%0, %1}, [%2];" : "=r"(r0), "=r"(r1) : "r"(taddr));
+    v = make_float2(__uint_as_float(r0), __uint_as_float(r1));
+}
+__device__ __forceinline__ void tmem_st2(uint32_t taddr, float2 v) {
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x2.b32 [%0], {%1, %2};" ::"r"(taddr), "r"(__float_as_uint(v.x)),
+                 "r"(__float_as_uint(v.y)) : "memory");
+}
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ void tmem_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tmem_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void named_bar(int id, int threads) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory"); }
+
+// NC (1 or 2) clauses of a var-disjoint class for the lane's two points; words are var | neg << 31.  x from the
+// shared tile (row v at xbase + 256 v), the gradient from / to the quadrant's TMEM columns (tq + 2 v).
+template <int K, int RED, bool CHECK, int NC>
+__device__ __forceinline__ void tmem_clauses(const BucketReg<float>& bk, int redpol, const uint32_t* sw0, const uint32_t* sw1,
+                                             float wc0, float wc1, uint32_t xl, uint32_t tq, float2& fe2, int& u0, int& u1) {
+    uint32_t w[NC][K];
+#pragma unroll
+    for (int c = 0; c < NC; ++c) load_words_smem<K>(c == 0 ? sw0 : sw1, w[c]);
+    float2 xv[NC][K], gv[NC][K];
+#pragma unroll
+    for (int c = 0; c < NC; ++c)
+#pragma unroll
+        for (int i = 0; i < K; ++i) tmem_ld2(tq + (w[c][i] << 1), gv[c][i]);   // the shift drops the sign bit
+#pragma unroll
+    for (int c = 0; c < NC; ++c)
+#pragma unroll
+        for (int i = 0; i < K; ++i) xv[c][i] = lds2(xl + (w[c][i] << 8));
+    float cs[NC][K];
+#pragma unroll
+    for (int c = 0; c < NC; ++c)
+#pragma unroll
+        for (int i = 0; i < K; ++i) cs[c][i] = flip_sign(bk.c1[0], w[c][i]);
+    if (CHECK) {
+#pragma unroll
+        for (int c = 0; c < NC; ++c) {
+            uint32_t t0 = red_init<RED>(), t1 = red_init<RED>();
+#pragma unroll
+            for (int i = 0; i < K; ++i) {
+                if (RED == 0) {
+                    t0 += lit_true(xv[c][i].x, w[c][i]);
+                    t1 += lit_true(xv[c][i].y, w[c][i]);
+                } else {
+                    t0 = red_step<RED>(t0, xv[c][i].x, w[c][i]);
+                    t1 = red_step<RED>(t1, xv[c][i].y, w[c][i]);
+                }
+            }
+            if (RED == 0) {
+                u0 += rule_sat((int)t0, bk.tmin, bk.tmax, bk.parity) ? 0 : 1;
+                u1 += rule_sat((int)t1, bk.tmin, bk.tmax, bk.parity) ? 0 : 1;
+            } else {
+                u0 += (int)((t0 >> 31) ^ (uint32_t)redpol);
+                u1 += (int)((t1 >> 31) ^ (uint32_t)redpol);
+            }
+        }
+    }
+    const float2 c0 = make_float2(bk.c0[0], bk.c0[0]);
+    float2 av[NC][K], pre[NC][K];
+#pragma unroll
+    for (int i = 0; i < K; ++i)
+#pragma unroll
+        for (int c = 0; c < NC; ++c) {
+            av[c][i] = __ffma2_rn(make_float2(cs[c][i], cs[c][i]), xv[c][i], c0);
+            if (i > 0) pre[c][i] = i == 1 ? av[c][0] : __fmul2_rn(pre[c][i - 1], av[c][i - 1]);
+        }
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+        const float wc = c == 0 ? wc0 : wc1;
+        const float2 run = K == 1 ? av[c][0] : __fmul2_rn(pre[c][K - 1], av[c][K - 1]);
+        const float2 fe = __ffma2_rn(make_float2(bk.g[0], bk.g[0]), run, make_float2(bk.g0, bk.g0));
+        fe2 = __ffma2_rn(make_float2(wc, wc), fe, fe2);
+    }
+    float2 suf[NC];
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+        const float sv = bk.g[0] * (c == 0 ? wc0 : wc1);
+        suf[c] = make_float2(sv, sv);
+    }
+    tmem_wait_ld();
+    // the loaded registers are valid only after the wait: pin every use behind it (asm volatile keeps the order)
+#pragma unroll
+    for (int c = 0; c < NC; ++c)
+#pragma unroll
+        for (int i = 0; i < K; ++i) asm volatile("" : "+f"(gv[c][i].x), "+f"(gv[c][i].y));
+#pragma unroll
+    for (int i = K - 1; i >= 0; --i)
+#pragma unroll
+        for (int c = 0; c < NC; ++c) {
+            gv[c][i] = __ffma2_rn(i == 0 ? suf[c] : __fmul2_rn(pre[c][i], suf[c]), make_float2(cs[c][i], cs[c][i]), gv[c][i]);
+            if (i > 0) suf[c] = __fmul2_rn(suf[c], av[c][i]);
+        }
+#pragma unroll
+    for (int c = 0; c < NC; ++c)
+#pragma unroll
+        for (int i = 0; i < K; ++i) tmem_st2(tq + (w[c][i] << 1), gv[c][i]);
+}
+
+struct TmemStage {
+    uint32_t words[4][2][kStageWords];   // [group][buffer]
+    float w[4][2][kStageCons];
+    UnitDev hdr[4][4];                   // [group][ring]
+    uint32_t tbase;
+};
+
+// Staging of one class by its group's 4 warps: lane l < 16 of group member r copies 16-byte word chunk 16 r + l,
+// lanes 16..19 weights 4 r .. 4 r + 3; lane 20 of member 0 copies the header of the group's class after it.
+template <int K>
+__device__ __forceinline__ void tmem_stage(const TiledArgs<float>& a, const UnitDev& U, int u, int i, int u1, TmemStage& st, int q,
+                                           int r, int buf, int lane) {
+    constexpr int KP = K_PAD(K);
+    const int count = unit_count(U);
+    const int ch = r * 16 + lane;
+    if (lane < 16 && ch * 4 < count * KP) cp_async16(&st.words[q][buf][ch * 4], a.words + (int64_t)U.word_begin + ch * 4);
+    const int j = r * 4 + (lane - 16);
+    if (lane >= 16 && lane < 20 && j < count) cp_async_small<4>(&st.w[q][buf][j], a.w_pos + (int64_t)U.pos_begin + j);
+    if (r == 0 && lane == 20 && u + 4 < u1) cp_async16(&st.hdr[q][(i + 1) & 3], a.units + u + 4);   // group class i + 1
+}
+
+template <int K, int RED, bool CHECK>
+__global__ void __launch_bounds__(32 * kTmemWarps, 1) fast_tmem_kernel(TiledArgs<float> a, uint32_t tcols) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];   // x tile [n][64] (host: tmem_smem_bytes)
+    __shared__ __align__(16) TmemStage st;
+    const int n = a.n;
+    float* xs = reinterpret_cast<float*>(smem_raw);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int q = warp & 3, r = warp >> 2;   // TMEM lane quadrant / warp group, member of the group
+    const int64_t b0 = (int64_t)blockIdx.x * 64;
+    const int chunk = blockIdx.y;
+    const int u0 = a.chunk_units[chunk], u1 = a.chunk_units[chunk + 1];
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                         (uint32_t)__cvta_generic_to_shared(&st.tbase)), "r"(tcols));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    // group q's classes: u = u0 + q + 4 i.  The first two classes' staging (and their headers) overlap the x tile load.
+    {
+        const int ua = u0 + q, ub = u0 + q + 4;
+        if (ua < u1) {
+            const UnitDev h = a.units[ua];
+            if (r == 0 && lane == 0) st.hdr[q][0] = h;
+            tmem_stage<K>(a, h, ua, 0, u1, st, q, r, 0, lane);   // also copies the header of ub into ring slot 1
+            if (ub < u1) tmem_stage<K>(a, a.units[ub], ub, 1, u1, st, q, r, 1, lane);
+        }
+    }
+    cp_async_commit();
+    {   // x tile [n][64]: row v = 64 points (256 B).  Thread t covers point t % 64, so a warp's 32 stores of one row are
+        // 32 consecutive words (bank-conflict-free; the row-major mapping would put a warp's stores 256 B apart, one
+        // bank: 32-way conflicts); 16-byte loads of 4 consecutive variables when the rows allow it.
+        const int p = (int)threadIdx.x & 63, g0 = (int)threadIdx.x >> 6;   // 8 variable groups per pass
+        const bool pv = b0 + p < a.B;
+        const float* xr = a.x + (b0 + p) * n;
+        if ((n & 3) == 0) {
+            for (int v4 = g0; v4 < (n >> 2); v4 += 8) {
+                const float4 q4 = pv ? __ldg(reinterpret_cast<const float4*>(xr) + v4) : make_float4(0.f, 0.f, 0.f, 0.f);
+                xs[(4 * v4 + 0) * 64 + p] = q4.x + 0.0f;   // + 0 canonicalises -0.0
+                xs[(4 * v4 + 1) * 64 + p] = q4.y + 0.0f;
+                xs[(4 * v4 + 2) * 64 + p] = q4.z + 0.0f;
+                xs[(4 * v4 + 3) * 64 + p] = q4.w + 0.0f;
+            }
+        } else {
+            for (int v = g0; v < n; v += 8) xs[v * 64 + p] = (pv ? __ldg(xr + v) : 0.0f) + 0.0f;
+        }
+    }
+    tmem_fence_before();
+    __syncthreads();
+    tmem_fence_after();
+    const uint32_t tq = st.tbase + ((uint32_t)(32 * q) << 16);
+    // zero the quadrant's 2 n columns (member r takes columns r, r + 4, ... in pairs)
+    for (int v = r; v < n; v += 4) tmem_st2(tq + 2 * v, make_float2(0.0f, 0.0f));
+    tmem_wait_st();
+    cp_async_wait_all();
+    tmem_fence_before();
+    __syncthreads();
+    tmem_fence_after();
+
+    double f0 = 0.0, f1 = 0.0;
+    int uc0 = 0, uc1 = 0;
+    const uint32_t xl32 = (uint32_t)__cvta_generic_to_shared(xs + 2 * lane);
+    int bucket = -1;
+    BucketReg<float> bk{};
+    int redpol = 0;
+    int buf = 0;
+    for (int i = 0, u = u0 + q; u < u1; ++i, u += 4) {
+        const UnitDev cur = st.hdr[q][i & 3];
+        if (cur.bucket != bucket) {
+            bucket = cur.bucket;
+            bk = load_bucket<float>(a.buckets + bucket);
+            redpol = (a.buckets[bucket].red & 4) ? 0 : 1;
+        }
+        const uint32_t* sw = st.words[q][buf];
+        const float* swt = st.w[q][buf];
+        const int count = unit_count(cur);
+        float2 fe2 = make_float2(0.0f, 0.0f);
+#pragma unroll
+        for (int pr = 0; pr < 2; ++pr) {   // clauses r + 8 pr and r + 8 pr + 4
+            const int j0 = r + 8 * pr, j1 = j0 + 4;
+            if (j1 < count)
+                tmem_clauses<K, RED, CHECK, 2>(bk, redpol, sw + j0 * K_PAD(K), sw + j1 * K_PAD(K), swt[j0], swt[j1], xl32, tq,
+                                               fe2, uc0, uc1);
+            else if (j0 < count)
+                tmem_clauses<K, RED, CHECK, 1>(bk, redpol, sw + j0 * K_PAD(K), sw, swt[j0], 0.0f, xl32, tq, fe2, uc0, uc1);
+        }
+        f0 += (double)fe2.x;
+        f1 += (double)fe2.y;
+        // end of the class: my TMEM stores are complete, the group's next class words / header are in shared memory
+        tmem_wait_st();
+        cp_async_wait_all();
+        tmem_fence_before();
+        named_bar(1 + q, 128);
+        tmem_fence_after();
+        buf ^= 1;
+        if (u + 8 < u1) tmem_stage<K>(a, st.hdr[q][(i + 2) & 3], u + 8, i + 2, u1, st, q, r, buf ^ 1, lane);
+        cp_async_commit();
+    }
+    pdl_trigger();
+    // the four quadrant tiles summed in a fixed order, (q0 + q2) + (q1 + q3), through two shared tiles T0 = x tile
+    // region, T1 after it: round 1 q0 -> T0 and q1 -> T1, round 2 q2 += T0 and q3 += T1, then T0 + T1.  Each warp moves 8
+    // variables (16 columns) per tcgen05.ld.
+    __syncthreads();
+    float* T0 = xs;             // [n][64]
+    float* T1 = xs + n * 64;    // [n][64]
+    for (int round = 0; round < 2; ++round) {
+        if ((q >> 1) == round) {
+            float* T = (q & 1) ? T1 : T0;
+            for (int v8 = r * 8; v8 < n; v8 += 32) {   // variables v8 .. v8 + 7 (columns 2 v8 .. 2 v8 + 15)
+                uint32_t g[16];
+                asm volatile("tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+                             : "=r"(g[0]), "=r"(g[1]), "=r"(g[2]), "=r"(g[3]), "=r"(g[4]), "=r"(g[5]), "=r"(g[6]), "=r"(g[7]),
+                               "=r"(g[8]), "=r"(g[9]), "=r"(g[10]), "=r"(g[11]), "=r"(g[12]), "=r"(g[13]), "=r"(g[14]), "=r"(g[15])
+                             : "r"(tq + 2 * v8));
+                tmem_wait_ld();
+#pragma unroll
+                for (int j = 0; j < 16; ++j) asm volatile("" : "+r"(g[j]));
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    if (v8 + j < n) {
+                        float2* dst = reinterpret_cast<float2*>(T + (v8 + j) * 64) + lane;
+                        const float2 gv = make_float2(__uint_as_float(g[2 * j]), __uint_as_float(g[2 * j + 1]));
+                        if (round == 0) *dst = gv;
+                        else {
+                            const float2 o = *dst;
+                            *dst = make_float2(o.x + gv.x, o.y + gv.y);
+                        }
+                    }
+                }
+            }
+        }
+        tmem_fence_before();
+        __syncthreads();
+    }
+    if (warp == 0) {   // every TMEM access of the CTA is ordered before the deallocation (fence - barrier - fence)
+        tmem_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(st.tbase), "r"(tcols));
+    }
+    float* G = T0;
+    const int64_t b = b0 + 2 * lane;
+    for (int v = warp; v < n; v += kTmemWarps) {
+        const float2 g0 = reinterpret_cast<const float2*>(G + v * 64)[lane];
+        const float2 g1 = reinterpret_cast<const float2*>(T1 + v * 64)[lane];
+        const float2 g = make_float2(g0.x + g1.x, g0.y + g1.y);
+        float* dst = a.P + ((int64_t)chunk * n + v) * a.B + b;
+        if (b + 1 < a.B && ((a.B & 1) == 0)) *reinterpret_cast<float2*>(dst) = g;
+        else {
+            if (b < a.B) dst[0] = g.x;
+            if (b + 1 < a.B) dst[1] = g.y;
+        }
+    }
+    __syncthreads();
+    double* fr = reinterpret_cast<double*>(smem_raw);         // [16][64]
+    int* ur = reinterpret_cast<int*>(fr + kTmemWarps * 64);   // [16][64]
+    fr[warp * 64 + 2 * lane] = f0;
+    fr[warp * 64 + 2 * lane + 1] = f1;
+    ur[warp * 64 + 2 * lane] = uc0;
+    ur[warp * 64 + 2 * lane + 1] = uc1;
+    __syncthreads();
+    if (warp < 2) {
+        const int p = warp * 32 + lane;
+        const int64_t bp = b0 + p;
+        if (bp < a.B) {
+            double f = 0.0;
+            int uc = 0;
+            for (int w = 0; w < kTmemWarps; ++w) {
+                f += fr[w * 64 + p];
+                uc += ur[w * 64 + p];
+            }
+            a.fpart[(int64_t)chunk * a.B + bp] = f;
+            if (CHECK) a.upart[(int64_t)chunk * a.B + bp] = uc;
         }
     }
 }
@@ -1475,13 +1837,14 @@ __global__ void __launch_bounds__(256) reduce_grad_kernel(ReduceArgs<T> a) {
         double f = 0.0;
         int u = 0;
         if (b < a.B) {
+            const bool cu = a.rf.unsat != nullptr;   // the unsat partials exist only when the evaluation counted them
             for (int c = ty; c < a.rf.n_parts; c += 8) {
                 f += a.rf.fpart[(int64_t)c * a.B + b];
-                u += a.rf.upart[(int64_t)c * a.B + b];
+                if (cu) u += a.rf.upart[(int64_t)c * a.B + b];
             }
             for (int64_t s = ty; s < a.rf.n_sym; s += 8) {
                 f += a.rf.fsym[s * a.B + b];
-                u += a.rf.usym[s * a.B + b];
+                if (cu) u += a.rf.usym[s * a.B + b];
             }
         }
         sf[ty][tx] = f;
@@ -1546,13 +1909,14 @@ __global__ void __launch_bounds__(32 * NWF) reduce_f_kernel(ReduceFArgs a) {
     double f = 0.0;
     int u = 0;
     if (b < a.B) {
+        const bool cu = a.unsat != nullptr;   // the unsat partials exist only when the evaluation counted them
         for (int c = w; c < a.n_parts; c += NWF) {
             f += a.fpart[(int64_t)c * a.B + b];
-            u += a.upart[(int64_t)c * a.B + b];
+            if (cu) u += a.upart[(int64_t)c * a.B + b];
         }
         for (int64_t s = w; s < a.n_sym; s += NWF) {
             f += a.fsym[s * a.B + b];
-            u += a.usym[s * a.B + b];
+            if (cu) u += a.usym[s * a.B + b];
         }
     }
     sf[w][lane] = f;

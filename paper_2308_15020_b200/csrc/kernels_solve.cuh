@@ -70,6 +70,7 @@ struct PgdArgs {
     int32_t* solved;   // per point: 1 once a trial satisfied everything
     int8_t* sol;       // [B][n] the first satisfying trial's assignment (-1 True / +1 False)
     int32_t mode;      // 0 = propose only (round start), 1 = accept then propose
+    int32_t checked;   // 1: unsatP holds the fused check of the evaluated point (check iterations only)
 };
 
 // one CTA (256 threads) per point
@@ -88,7 +89,7 @@ __global__ void __launch_bounds__(256) pgd_step_kernel(PgdArgs a) {
     if (a.mode == 0) {
         // round start: the evaluated point is x itself
         if (threadIdx.x == 0) {
-            int newly = (a.unsatP[b] == 0 && !a.solved[b]) ? 1 : 0;
+            int newly = (a.checked && a.unsatP[b] == 0 && !a.solved[b]) ? 1 : 0;
             if (newly) a.solved[b] = 1;
             s_acc = newly << 1;
         }
@@ -109,8 +110,8 @@ __global__ void __launch_bounds__(256) pgd_step_kernel(PgdArgs a) {
                 if (acc) a.fX[b] = a.fP[b];
                 if (eta < a.eta_min || it >= a.max_inner) a.done[b] = 1;
             }
-            // any trial whose rounded assignment satisfies every constraint is a solution (Thm. 4)
-            int newly = (a.unsatP[b] == 0 && !a.solved[b]) ? 1 : 0;
+            // any checked trial whose rounded assignment satisfies every constraint is a solution (Thm. 4)
+            int newly = (a.checked && a.unsatP[b] == 0 && !a.solved[b]) ? 1 : 0;
             if (newly) a.solved[b] = 1;
             s_acc = acc | (newly << 1);
         }
