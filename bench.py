@@ -57,6 +57,7 @@ SM_COUNT = 148
 FP32_LANES, FP64_LANES = 128, 64  # FP32 / FP64 lanes per SM per clock (B200 guide unit counts)
 # Algorithmic FP lane-operations (one FMA = one lane-op = one pipe slot: count instructions):
 SMEM_BYTES_PER_TERM = 12   # x tile LDS + gradient tile LDS + STS, 4 B each
+TMEM_RMW_BYTES_PER_CLK = 213   # per SM: 16 warps of 32x32b.x2 tcgen05.ld + tcgen05.st (profiles/r02_tmem_probe.txt)
 FAST_PRODUCTS_PER_TERM = 3       # the fast-path product count per literal and point (prefix, suffix, term)
 ROOT_OPS_PER_LIT_ROOT = 12        # factor 2 FMA, prefix + suffix complex MUL (2 x 4), Re-accumulate 2 FMA (App. A)
 
@@ -271,7 +272,7 @@ def roofline_of(info, inst, B, ph, args):
     alu_src = (f"{SM_COUNT} SMs x {lanes} {'FP64' if f64 else 'FP32'} lanes x {mhz:.0f} MHz ({peak_src} sm_max_mhz); "
                "one FMA / MUL = one lane-op")
     res = {}
-    eval_kernels = ("transpose_kernel+fast_global_kernel+fast_global_long_kernel+reduce_grad_kernel+reduce_f_kernel"
+    eval_kernels = ("transpose_kernel+fast_global_kernel+fast_global_long_kernel+owner_grad_kernel+reduce_grad_kernel+reduce_f_kernel"
                     if info["path"] == 2 else "fast_wide_kernel+fast_tiled_kernel+reduce_grad_kernel+reduce_f_kernel")
     traffic_eval = ncu_traffic(eval_kernels, args.config, any_of=True)
     res["hbm"] = {"scope": "evaluation (A4-A7, every kernel)", "achieved": alg_bytes / (eval_ms * 1e-3) / 1e9,
@@ -279,8 +280,19 @@ def roofline_of(info, inst, B, ph, args):
                   "algorithmic_def": f"4L + 8C + 2*{es}*n*B + 4B (SURVEY 8(d))", "time_ms": eval_ms,
                   "traffic": traffic_eval, "waste": (traffic_eval / alg_bytes) if traffic_eval else None,
                   "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_src})"}
-    if fast_ms >= root_ms:
+    grad_ms = float(ph[2])
+    own = info.get("n_own_lits", 0) > 0
+    if own and grad_ms >= max(fast_ms, root_ms):
+        # global path, owner-computes: the short constraints' products are formed in owner_grad_kernel
+        res["alu"] = {
+            "scope": "owner_grad_kernel", "pipe": "fp64" if f64 else "fp32",
+            "achieved": FAST_PRODUCTS_PER_TERM * terms_fast / (grad_ms * 1e-3) / 1e12, "peak": alu_peak,
+            "unit": "T lane-op/s", "algorithmic_def": f"{FAST_PRODUCTS_PER_TERM} products per literal term (SURVEY 8(d))",
+            "time_ms": grad_ms, "peak_source": alu_src}
+        kms = grad_ms
+    elif fast_ms >= root_ms:
         kname = ("fast_global_kernel+fast_global_long_kernel" if info["path"] == 2 else
+                 "fast_tmem_kernel" if info.get("wide") == 2 else
                  "fast_wide_kernel" if info.get("wide") else "fast_tiled_kernel")
         res["alu"] = {
             "scope": kname, "pipe": "fp64" if f64 else "fp32", "achieved": FAST_PRODUCTS_PER_TERM * terms_fast / (fast_ms * 1e-3) / 1e12, "peak": alu_peak,
@@ -288,10 +300,20 @@ def roofline_of(info, inst, B, ph, args):
             "time_ms": fast_ms, "peak_source": alu_src}
         if info["path"] == 1:
             smem_peak = SM_COUNT * 128 * mhz * 1e6 / 1e9
-            res["smem"] = {"scope": kname, "achieved": SMEM_BYTES_PER_TERM * terms_fast / (fast_ms * 1e-3) / 1e9,
+            tm = info.get("wide") == 2
+            sb = 4 if tm else SMEM_BYTES_PER_TERM
+            res["smem"] = {"scope": kname, "achieved": sb * terms_fast / (fast_ms * 1e-3) / 1e9,
                            "peak": smem_peak, "unit": "GB/s",
-                           "algorithmic_def": f"{SMEM_BYTES_PER_TERM} B per term: x tile read + gradient tile read and write",
+                           "algorithmic_def": (f"{sb} B per term: x tile read" if tm else
+                                               f"{sb} B per term: x tile read + gradient tile read and write"),
                            "time_ms": fast_ms, "peak_source": f"{SM_COUNT} SMs x 128 B/clk x {mhz:.0f} MHz"}
+            if tm:
+                tmem_peak = SM_COUNT * TMEM_RMW_BYTES_PER_CLK * mhz * 1e6 / 1e9
+                res["tmem"] = {"scope": kname, "achieved": 8 * terms_fast / (fast_ms * 1e-3) / 1e9, "peak": tmem_peak,
+                               "unit": "GB/s", "algorithmic_def": "8 B per term: gradient tile read and write in TMEM",
+                               "time_ms": fast_ms,
+                               "peak_source": f"{SM_COUNT} SMs x {TMEM_RMW_BYTES_PER_CLK} B/clk (tcgen05.ld + st read-modify-"
+                                              f"write, measured by scripts/tmem_probe.cu) x {mhz:.0f} MHz"}
         kms = fast_ms
     else:
         kname, kms = "sym_item_kernel", root_ms

@@ -107,6 +107,8 @@ typedef struct {
                                in shared memory, 2 = 64-point with the gradient tile in tensor memory (TMEM) */
     int32_t max_k;
     int64_t device_bytes;   /* persistent device memory held by the context */
+    int64_t n_own_lits;     /* global path: literals of the short constraints whose gradient terms the owner-computes
+                               kernel forms per variable (no T-buffer round trip); 0 otherwise */
 } ffsat_info_t;
 
 /* Build a context from arrays (validates, buckets, precomputes coefficients, uploads). */

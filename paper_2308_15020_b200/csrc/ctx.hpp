@@ -101,7 +101,7 @@ struct ffsat_ctx {
     std::string err;
     // persistent device layout
     ffsat::DBuf fast_words, tiled_words, units, buckets, sym_words, sym_off, sym_sig, sigs, coef, occ_off, occ_slot,
-        w_pos, w_static_orig, order, chk_off, chk_words, chk_rule;
+        w_pos, w_static_orig, order, chk_off, chk_words, chk_rule, own_off, own_rec;
     int64_t persistent_bytes = 0;
     // the batch-independent launch plan (plan_chunks, at load): chunk split of the fast kernels and root splits.
     // It depends on the formula and on batch_ref only -- never on the B of a call -- so every point's f / grad
@@ -114,6 +114,8 @@ struct ffsat_ctx {
     std::vector<int64_t> sym_offT, sym_offF;
     int64_t sym_totT = 0, sym_totF = 0;   // per point
     int32_t n_chunks = 0;
+    int32_t n_vtiles = 0;                 // owner-computes: 8-variable tiles (their partial f rows, folded to n_fold rows)
+    int32_t n_fold = 0;
     int32_t f_groups = 8;                 // interleaved groups of the fixed-order f / unsat reduction (8 or 32)
     // scratch of the context's own evaluations; host-buffer staging
     ffsat::Scratch scr;

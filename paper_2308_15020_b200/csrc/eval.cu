@@ -52,6 +52,10 @@ void plan_chunks(ffsat_ctx* c) {
     if (L.path == 2) {
         auto kof = [&](int64_t u) { return L.fbuckets[(size_t)L.units[(size_t)u].bucket].k; };
         int64_t u = 0;
+        // owner-computes buckets (the shortest, a prefix of the units) take no fast-kernel pass: owner_grad_kernel
+        // forms their terms per variable
+        while (u < n_units && L.fbuckets[(size_t)L.units[(size_t)u].bucket].own) ++u;
+        ug[0] = u;
         while (u < n_units && kof(u) <= 4) ++u;
         ug[1] = u;
         while (u < n_units && kof(u) <= 16) ++u;
@@ -92,7 +96,11 @@ void plan_chunks(ffsat_ctx* c) {
     // the fixed f / unsat summation order: rows r = 0 .. R-1 (fast partials, then root-path constraints) summed in
     // f_groups interleaved groups (r mod f_groups), ascending inside a group, groups in order -- the same order in
     // reduce_f_kernel and in the gradient reduction's fused variant, for every batch size
-    const int64_t rows = (L.n_fast > 0 ? c->n_chunks : 0) + L.n_sym;
+    // owner_grad_kernel's f / unsat partial rows, one per 8-variable tile, folded 256 to a row (fold_rows_kernel);
+    // partial row layout: [chunk rows | folded rows | variable-tile rows]
+    c->n_vtiles = L.own ? (L.n + 7) / 8 : 0;
+    c->n_fold = (c->n_vtiles + 255) / 256;
+    const int64_t rows = (L.n_fast > 0 ? c->n_chunks + c->n_fold : 0) + L.n_sym;
     c->f_groups = rows > 256 ? 32 : 8;
     {   // root splits: per-class partial regions (S = 1 everywhere if they would exceed 4 GiB at the reference batch)
         const size_t ncl = L.sym_classes.size();
@@ -132,7 +140,7 @@ void ensure_scratch(const ffsat_ctx* c, Scratch& S, int64_t B) {
     if (S.B >= B) return;   // buffers sized for a larger batch serve every smaller one (row strides are the call's B)
     const Layout& L = c->Lo;
     const size_t es = c->esize, b = (size_t)B;
-    const size_t parts = (size_t)std::max<int64_t>(1, c->n_chunks);
+    const size_t parts = (size_t)std::max<int64_t>(1, c->n_chunks + c->n_fold + c->n_vtiles);
     if (L.path == 1) S.P.ensure(std::max<size_t>(16, parts * L.n * b * es));
     if (L.path == 2 || L.sym_lane) S.xT.ensure(std::max<size_t>(16, (size_t)L.n * b * es));
     S.Tb.ensure(std::max<size_t>(16, (size_t)L.tb_slots * b * es));

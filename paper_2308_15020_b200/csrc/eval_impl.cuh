@@ -216,14 +216,29 @@ void eval_device_t(ffsat_ctx* c, Scratch& S, const T* x, int64_t B, double* f, T
     join_sym();
     mark(2);
     dev::ReduceFArgs rf{};
-    rf.B = B; rf.n_parts = L.n_fast > 0 ? c->n_chunks : 0; rf.n_sym = L.n_sym;
+    rf.B = B; rf.n_parts = L.n_fast > 0 ? c->n_chunks + c->n_fold : 0; rf.n_sym = L.n_sym;
     rf.fpart = S.fpart.as<double>(); rf.upart = S.upart.as<int32_t>(); rf.fsym = S.fsym.as<double>();
     rf.usym = S.usym.as<int32_t>(); rf.f = f; rf.unsat = unsat;
     // tiled path with a gradient: the f / unsat reduction rides in the gradient reduction (variable tile 0), one
     // launch fewer per evaluation; the profiled path keeps them apart so the phases can be timed separately, and
     // the global path keeps them apart (its HBM-bound reduction measured slower with the fused variant, c5)
     const bool fuse = grad && L.n > 0 && !profiled && L.path == 1 && c->f_groups == 8;
-    if (grad) {
+    if (L.own && L.n > 0) {
+        // global path with owner-computes buckets: one kernel forms their terms per variable and adds the T slots
+        // (replaces the gradient reduction); it also writes the short constraints' f / unsat partial rows
+        c->launches += 1;
+        dev::OwnerArgs<T> o{};
+        o.xT = S.xT.as<T>(); o.B = B; o.n = L.n; o.own_off = c->own_off.as<int64_t>(); o.own_rec = c->own_rec.as<uint4>();
+        o.buckets = c->buckets.as<dev::FastBucketDev>(); o.w_pos = w_pos;
+        o.Tb = S.Tb.as<T>(); o.occ_off = c->occ_off.as<int64_t>(); o.occ_slot = c->occ_slot.as<int32_t>(); o.grad = grad;
+        o.fpart = S.fpart.as<double>(); o.upart = unsat ? S.upart.as<int32_t>() : nullptr;
+        o.row0 = c->n_chunks + c->n_fold;
+        dim3 grid(blocks_for(L.n, 8), blocks_for(B, 32)), blk(32, 8);
+        dev::owner_grad_kernel<T><<<grid, blk, 0, st>>>(o);
+        dev::fold_rows_kernel<8><<<dim3((unsigned)c->n_fold, blocks_for(B, 32)), 256, 0, st>>>(
+            S.fpart.as<double>(), unsat ? S.upart.as<int32_t>() : nullptr, B, o.row0, c->n_vtiles, c->n_chunks);
+        c->launches += 1;
+    } else if (grad) {
         c->launches += 1;
         dev::ReduceArgs<T> r{};
         r.B = B; r.n = L.n; r.n_chunks = L.path == 1 ? c->n_chunks : 0; r.P = S.P.as<T>(); r.Tb = S.Tb.as<T>();

@@ -115,6 +115,10 @@ void upload_layout(ffsat_ctx* c) {
         upload(c->w_pos, w);
     }
     upload(c->w_static_orig, c->F.weight);
+    if (L.own) {
+        upload(c->own_off, L.own_off);
+        upload(c->own_rec, L.own_rec);
+    }
     upload(c->order, L.order);
     // unified position-order CSR for the exact check kernel
     std::vector<int64_t> off{0};
@@ -137,7 +141,7 @@ void upload_layout(ffsat_ctx* c) {
     upload(c->chk_rule, rule);
     for (DBuf* d : {&c->fast_words, &c->tiled_words, &c->units, &c->buckets, &c->sym_words, &c->sym_off,
                     &c->sym_sig, &c->sigs, &c->coef, &c->occ_off, &c->occ_slot, &c->w_pos, &c->w_static_orig, &c->order,
-                    &c->chk_off, &c->chk_words, &c->chk_rule})
+                    &c->chk_off, &c->chk_words, &c->chk_rule, &c->own_off, &c->own_rec})
         c->persistent_bytes += (int64_t)d->bytes;
 }
 
@@ -517,6 +521,7 @@ ffsat_status ffsat_info(const ffsat_ctx* c, ffsat_info_t* o) {
     o->n_vars = L.n; o->precision = L.precision; o->n_cons = L.m; o->n_lits = L.L;
     o->n_fast_cons = L.n_fast; o->n_sym_cons = L.n_sym; o->n_fast_lits = L.n_fast_lits; o->n_sym_lits = L.n_sym_lits;
     o->sym_root_lits = L.sym_root_lits; o->path = L.path; o->wide = L.tmem ? 2 : L.wide ? 1 : 0; o->max_k = L.max_k; o->device_bytes = c->persistent_bytes;
+    o->n_own_lits = L.n_own_lits;
     return FFSAT_OK;
     ABI_CATCH(nullptr)
 }

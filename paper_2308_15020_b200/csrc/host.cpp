@@ -466,12 +466,61 @@ Layout build_layout(const Formula& F, int path, int precision) {
         cl.S = cl.G == 0 ? 1 : std::max(1, std::min(32, (cl.max_mp + root_chunk - 1) / root_chunk));
     }
 
+    // ---- owner-computes buckets (global path): no T slots; the other fast buckets' slots are renumbered densely
+    // off by default: measured slower than the T-buffer path on c5 (2.65 vs 1.34 ms per evaluation, the per-variable
+    // occurrence loops are latency-bound and x^T still misses L2); FFSAT_OWN=1 enables it
+    int own_kmax = 0;
+    if (const char* e = std::getenv("FFSAT_OWN")) if (path == 2 && std::atoi(e) != 0) own_kmax = kOwnKMax;
+    {
+        int64_t ts = 0;
+        for (FastBucket& b : Lo.fbuckets) {
+            b.own = b.k <= own_kmax;
+            b.slot_off = b.own ? 0 : ts;
+            if (!b.own) ts += (b.pos_end - b.pos_begin) * b.k;
+            else Lo.n_own_lits += (b.pos_end - b.pos_begin) * b.k;
+        }
+        if (path == 2) Lo.tb_fast = ts;
+        Lo.own = Lo.n_own_lits > 0;
+    }
+    if (Lo.own) {
+        if (Lo.fbuckets.size() > 0xffffff) throw Error(FFSAT_ERR_ARG, "too many fast buckets");
+        Lo.own_off.assign((size_t)F.n + 1, 0);
+        for (const FastBucket& b : Lo.fbuckets)
+            if (b.own)
+                for (int64_t p = b.pos_begin; p < b.pos_end; ++p)
+                    for (int i = 0; i < b.k; ++i)
+                        Lo.own_off[(size_t)(Lo.fast_words[(size_t)(b.word_off + (p - b.pos_begin) * b.kp + i)] & 0x7fffffffu) + 1]++;
+        for (int32_t v = 0; v < F.n; ++v) Lo.own_off[(size_t)v + 1] += Lo.own_off[(size_t)v];
+        Lo.own_rec.assign((size_t)(4 * Lo.n_own_lits), 0);
+        std::vector<int64_t> cur(Lo.own_off.begin(), Lo.own_off.end() - 1);
+        for (size_t bi = 0; bi < Lo.fbuckets.size(); ++bi) {
+            const FastBucket& b = Lo.fbuckets[bi];
+            if (!b.own) continue;
+            for (int64_t p = b.pos_begin; p < b.pos_end; ++p) {
+                const uint32_t* wr = &Lo.fast_words[(size_t)(b.word_off + (p - b.pos_begin) * b.kp)];
+                for (int i = 0; i < b.k; ++i) {
+                    const uint32_t v = wr[i] & 0x7fffffffu;
+                    const int64_t o = cur[v]++;
+                    if (p > INT32_MAX) throw Error(FFSAT_ERR_ARG, "formula too large for 32-bit owner records");
+                    uint32_t* rec = &Lo.own_rec[(size_t)(4 * o)];
+                    rec[0] = (uint32_t)p;
+                    int q = 1;
+                    for (int j = 0; j < b.k; ++j)
+                        if (j != i) rec[q++] = wr[j];
+                    while (q < 3) rec[q++] = 0;   // padding (k < 3): never read
+                    rec[3] = ((uint32_t)bi << 8) | ((uint32_t)i << 1) | (wr[i] >> 31);
+                }
+            }
+        }
+    }
+
     // ---- T-buffer slots and occurrence CSR (ascending slot order per variable)
-    Lo.tb_fast = path == 2 ? Lo.n_fast_lits : 0;
+    if (path != 2) Lo.tb_fast = 0;
     Lo.tb_slots = Lo.tb_fast + Lo.n_sym_lits;
     std::vector<int32_t> slot_var((size_t)Lo.tb_slots);
     if (path == 2) {
         for (const FastBucket& b : Lo.fbuckets)
+            if (!b.own)
             for (int64_t p = b.pos_begin; p < b.pos_end; ++p)
                 for (int i = 0; i < b.k; ++i)
                     slot_var[(size_t)(b.slot_off + (p - b.pos_begin) * b.k + i)] =

@@ -43,6 +43,7 @@ bool fast_form(int kind, int k, int bound, FastForm* out);
 
 struct FastBucket {
     int32_t variant, k, kp;        // kp = k rounded up to a multiple of 4 (16-byte literal rows)
+    bool own = false;              // global path, k <= kOwnKMax: gradient by owner-computes (no T slots)
     int64_t pos_begin, pos_end;    // constraint positions (layout order)
     int64_t word_off;              // first padded literal word of the bucket
     int64_t slot_off;              // first (unpadded) literal slot of the bucket
@@ -101,8 +102,15 @@ struct Layout {
     std::vector<int32_t> sym_rule;      // 3 ints per sym constraint (tmin, tmax, parity)
     std::vector<SymClass> sym_classes;
     bool sym_lane = false;              // some root-path class runs thread-per-item on x^T (needs the transpose)
-    // T-buffer slots (global path: fast slots then sym slots; tiled path: sym slots only)
+    // T-buffer slots (global path: non-owner fast slots then sym slots; tiled path: sym slots only)
     int64_t tb_fast = 0, tb_slots = 0;
+    // owner-computes (global path, fast buckets with k <= kOwnKMax): per variable its occurrences in those
+    // constraints, ascending position, as self-contained 16-byte records {position, the other literals' words (in
+    // literal order, padded with the first), bucket << 8 | literal index << 1 | own literal negated}
+    bool own = false;
+    int64_t n_own_lits = 0;
+    std::vector<int64_t> own_off;       // [n + 1]
+    std::vector<uint32_t> own_rec;      // 4 per occurrence
     std::vector<int64_t> occ_off;       // [n + 1]
     std::vector<int64_t> occ_slot;      // ascending slot ids per variable
     // work units of the fast kernels (tiled: var-disjoint classes; global: runs of <= 512 literals)
@@ -111,6 +119,7 @@ struct Layout {
     std::vector<uint32_t> tiled_words;  // tiled path: (var * kTilePitch) | neg << 31 (padded rows)
 };
 
+constexpr int kOwnKMax = 3;         // global path, FFSAT_OWN=1: constraints this short take the owner-computes gradient
 constexpr int kTilePitch = 66;      // smem row pitch of the tiled kernel: x half-row (32 points + pad) | gradient half-row
 constexpr int kClassCap = 16;
 constexpr int kWidePitch = 132;     // wide tiled kernel row: x (64 points + 2 pad) | gradient (64 + 2)       // constraints per var-disjoint class (2 per warp of an 8-warp CTA)

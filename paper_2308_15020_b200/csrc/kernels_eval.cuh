@@ -1897,6 +1897,199 @@ __global__ void __launch_bounds__(256) reduce_grad_kernel(ReduceArgs<T> a) {
 }
 
 
+// Owner-computes gradient for the short fast constraints of the global path (k <= 3, SURVEY 8(e) "owner-computes"):
+// thread (variable v, point b) forms every term of v's occurrences in those constraints itself -- the constraint's
+// other literals gathered from x^T (coalesced: lanes = points), the exclusive product of their factors, Prop. 1 --
+// and sums them in ascending position order, then adds v's remaining T slots (long fast and root-path constraints)
+// in ascending slot order (fp64 accumulation): no term round trip through HBM for the short constraints.  The
+// occurrence at literal index 0 also contributes the constraint's w FE and its fused check to the tile's partial
+// f / unsat row (row0 + variable tile), so every constraint is counted once.  Occurrence records are
+// self-contained (the other literals' words inline) and processed four at a time with every load in flight.
+// Block (32 points, 8 variables).
+template <typename T>
+struct OwnerArgs {
+    const T* xT;                 // [n][B] (canonical zeros)
+    int64_t B;
+    int32_t n;
+    const int64_t* own_off;      // [n + 1]
+    const uint4* own_rec;        // {position, other word A, other word B, bucket << 8 | i << 1 | own negated}
+    const FastBucketDev* buckets;
+    const T* w_pos;
+    const T* Tb;                 // [tb_slots][B]
+    const int64_t* occ_off;      // [n + 1] the remaining (T-slot) occurrences
+    const int32_t* occ_slot;
+    T* grad;                     // [B][n] or null (f / unsat only)
+    double* fpart;               // rows [row0 + variable tile][B]
+    int32_t* upart;              // same rows, or null
+    int32_t row0;
+};
+
+// L2 cache policies (createpolicy): x^T rows are gathered many times (keep them: evict_last), the occurrence records
+// are read once (evict_first) -- so the streamed records do not displace x^T from L2.
+__device__ __forceinline__ uint64_t l2_policy_last() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ uint64_t l2_policy_first() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ uint4 ld_stream16(const uint4* p, uint64_t pol) {
+    uint4 v;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0, %1, %2, %3}, [%4], %5;"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p), "l"(pol));
+    return v;
+}
+template <typename T>
+__device__ __forceinline__ T ld_keep(const T* p, uint64_t pol) {
+    T v;
+    if constexpr (sizeof(T) == 4) asm volatile("ld.global.nc.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(v) : "l"(p), "l"(pol));
+    else asm volatile("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol));
+    return v;
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256) owner_grad_kernel(OwnerArgs<T> a) {
+    __shared__ T tile[8][33];
+    __shared__ double sf[8][32];
+    __shared__ int su[8][32];
+    const int tx = threadIdx.x, ty = threadIdx.y;
+    const int64_t b0 = (int64_t)blockIdx.y * 32, v0 = (int64_t)blockIdx.x * 8;   // grid.x over variable tiles
+    const int64_t b = b0 + tx, v = v0 + ty;
+    const bool bv = b < a.B;
+    const int64_t bb = bv ? b : a.B - 1;   // lanes past the batch mirror the last point (in-bounds loads, nothing stored)
+    const bool want_term = a.grad != nullptr, want_unsat = a.upart != nullptr;
+    double acc = 0.0, facc = 0.0;
+    int uacc = 0;
+    if (v < a.n) {
+        const uint64_t keep = l2_policy_last(), stream = l2_policy_first();
+        const T* xTb = a.xT + bb;
+        const T xv = ld_keep(xTb + v * a.B, keep);
+        int cur = -1, nch = 0;
+        BucketReg<T> bk{};
+        const int64_t o1 = a.own_off[v + 1];
+        for (int64_t o = a.own_off[v]; o < o1; o += 4) {
+            constexpr int NB = 4;
+            uint4 rc[NB];
+#pragma unroll
+            for (int q = 0; q < NB; ++q) rc[q] = o + q < o1 ? ld_stream16(a.own_rec + o + q, stream) : make_uint4(0, 0, 0, 0);
+            T xa[NB], xb[NB], wc[NB];
+#pragma unroll
+            for (int q = 0; q < NB; ++q) {   // every gather of the batch in flight (padding words read variable 0)
+                xa[q] = ld_keep(xTb + (int64_t)(rc[q].y & 0x7fffffffu) * a.B, keep);
+                xb[q] = ld_keep(xTb + (int64_t)(rc[q].z & 0x7fffffffu) * a.B, keep);
+                wc[q] = __ldg(a.w_pos + rc[q].x);
+            }
+#pragma unroll
+            for (int q = 0; q < NB; ++q) {
+                if (o + q >= o1) break;
+                const int bucket = (int)(rc[q].w >> 8), i = (int)((rc[q].w >> 1) & 3);
+                if (bucket != cur) {
+                    cur = bucket;
+                    bk = load_bucket<T>(a.buckets + bucket);
+                    nch = a.buckets[bucket].nch;
+                }
+                const int k = bk.k;
+                const uint32_t wown = rc[q].w << 31;   // the own literal's sign bit
+                T term = (T)0, fe = bk.g0;
+#pragma unroll
+                for (int c = 0; c < 2; ++c) {
+                    if (c >= nch) break;
+                    const T ao = fmaT(flip_sign(bk.c1[c], wown), xv, bk.c0[c]);
+                    const T aa = k >= 2 ? fmaT(flip_sign(bk.c1[c], rc[q].y), xa[q], bk.c0[c]) : (T)1;
+                    const T ab = k >= 3 ? fmaT(flip_sign(bk.c1[c], rc[q].z), xb[q], bk.c0[c]) : (T)1;
+                    const T ex = aa * ab;                                   // the other factors, in literal order
+                    // all factors in literal order: own first when it is literal 0 (the only case FE is used)
+                    fe = fmaT(bk.g[c], ao * ex, fe);
+                    term = fmaT(bk.g[c] * flip_sign(bk.c1[c], wown), ex, term);
+                }
+                if (want_term) acc += (double)(wc[q] * term);
+                if (i == 0) {   // the constraint's f and check, counted once (by its first literal's owner)
+                    facc += (double)(wc[q] * fe);
+                    if (want_unsat) {
+                        uint32_t t = lit_true(xv, wown);
+                        if (k >= 2) t += lit_true(xa[q], rc[q].y);
+                        if (k >= 3) t += lit_true(xb[q], rc[q].z);
+                        uacc += rule_sat((int)t, bk.tmin, bk.tmax, bk.parity) ? 0 : 1;
+                    }
+                }
+            }
+        }
+        if (want_term) {   // the remaining occurrences' T slots, ascending (loads issued 4 ahead, added in order)
+            int64_t q = a.occ_off[v];
+            const int64_t e = a.occ_off[v + 1];
+            for (; q + 4 <= e; q += 4) {
+                int32_t sl[4];
+                T t[4];
+#pragma unroll
+                for (int j = 0; j < 4; ++j) sl[j] = a.occ_slot[q + j];
+#pragma unroll
+                for (int j = 0; j < 4; ++j) t[j] = a.Tb[(int64_t)sl[j] * a.B + bb];
+#pragma unroll
+                for (int j = 0; j < 4; ++j) acc += (double)t[j];
+            }
+            for (; q < e; ++q) acc += (double)a.Tb[(int64_t)a.occ_slot[q] * a.B + bb];
+        }
+    }
+    // partial f / unsat of this variable tile: warp (variable) order
+    sf[ty][tx] = facc;
+    su[ty][tx] = uacc;
+    tile[ty][tx] = (T)acc;
+    __syncthreads();
+    if (ty == 0 && bv) {
+        double f = 0.0;
+        int u = 0;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            f += sf[j][tx];
+            u += su[j][tx];
+        }
+        a.fpart[((int64_t)a.row0 + blockIdx.x) * a.B + b] = f;
+        if (want_unsat) a.upart[((int64_t)a.row0 + blockIdx.x) * a.B + b] = u;
+    }
+    if (want_term) {   // transposed write: each point row gets 8 consecutive gradient entries
+        const int t = ty * 32 + tx;
+        const int pl = t >> 3, vl = t & 7;
+        const int64_t pb = b0 + pl, vv = v0 + vl;
+        if (pb < a.B && vv < a.n) a.grad[pb * a.n + vv] = tile[vl][pl];
+    }
+}
+
+// Fold partial rows [src, src + nrows) into rows [dst, dst + ceil(nrows / 256)): group g = rows 256 g .. 256 g + 255,
+// warp w sums its rows w, w + 8, ... in ascending order, then the 8 warp sums in warp order (a fixed tree: the f /
+// unsat totals stay deterministic for any batch).  grid (groups, point tiles), block 256.
+template <int NW>   // NW = 8 (a template so that every translation unit may include this header)
+__global__ void __launch_bounds__(32 * NW) fold_rows_kernel(double* fpart, int32_t* upart, int64_t B, int64_t src, int64_t nrows,
+                                                        int64_t dst) {
+    __shared__ double sf[8][32];
+    __shared__ int su[8][32];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int64_t b = (int64_t)blockIdx.y * 32 + lane;
+    const int64_t r0 = (int64_t)blockIdx.x * 256, r1 = min(nrows, r0 + 256);
+    double f = 0.0;
+    int u = 0;
+    if (b < B)
+        for (int64_t r = r0 + w; r < r1; r += 8) {
+            f += fpart[(src + r) * B + b];
+            if (upart) u += upart[(src + r) * B + b];
+        }
+    sf[w][lane] = f;
+    su[w][lane] = u;
+    __syncthreads();
+    if (w == 0 && b < B) {
+        double t = 0.0;
+        int tu = 0;
+        for (int j = 0; j < 8; ++j) {
+            t += sf[j][lane];
+            tu += su[j][lane];
+        }
+        fpart[(dst + blockIdx.x) * B + b] = t;
+        if (upart) upart[(dst + blockIdx.x) * B + b] = tu;
+    }
+}
+
 // one CTA (32 NWF threads) per 32 points: lane = point, warp w sums rows w, w + NWF, ... in ascending
 // order, then the NWF warp sums are added in warp order -- a fixed summation order for a given launch
 // shape (deterministic, no atomics).  NWF = 32 when few point tiles must cover many partial rows.

@@ -39,7 +39,7 @@ def test_our_arm_json_line():
     assert line["n_gpus"] == 1 and line["steps"] == 3 and line["warmup"] == 3 and line["value"] > 0
     assert line["gpu_launches"] > 0
     rf = line["roofline"]
-    assert rf["bound"] in ("hbm", "tensor", "alu", "smem") and 0 < rf["frac"] < 1 and rf["peak"] > 0
+    assert rf["bound"] in ("hbm", "tensor", "alu", "smem", "tmem") and 0 < rf["frac"] < 1 and rf["peak"] > 0
     assert line["e2e"]["h2d_bytes_per_step"] > 0 and line["e2e"]["value"] > 0
     assert line["cpu_baseline"]["kind"] == "oracle" and line["cpu_baseline"]["value"] > 0
     assert line["clocks"]["sm_mhz"] is not None

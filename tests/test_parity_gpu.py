@@ -204,6 +204,23 @@ def test_long_kernel_64bit_gather_offsets():
     torch.cuda.empty_cache()
 
 
+@pytest.mark.parametrize("precision", [32, 64])
+def test_owner_computes_option(precision, monkeypatch):
+    """FFSAT_OWN=1 (global path): constraints with k <= 3 take the owner-computes gradient (owner_grad_kernel: per
+    variable, no T-buffer round trip), the rest the T buffer; f, grad, unsat against the oracle, mixed kinds incl.
+    NAE (two product channels) and constant constraints, ragged batch; and bit-identical across batch splits."""
+    monkeypatch.setenv("FFSAT_OWN", "1")
+    inst = synth.random_mixed(n=90, m=400, seed=11, kmax=64)
+    ctx = P.Context.from_instance(inst, precision=precision, path=2, device=0)
+    assert ctx.info["n_own_lits"] > 0
+    compare(inst, synth.points("U", 77, inst.n, 3), precision=precision, ctx=ctx)
+    compare(inst, synth.points("Z", 40, inst.n, 4), precision=precision, ctx=ctx)
+    X = torch.from_numpy(synth.points("U", 70, inst.n, 5, ctx.dtype)).cuda()
+    f, g, u = ctx.eval(X, grad=True, unsat=True)
+    f2, g2, u2 = ctx.eval(X[33:50].contiguous(), grad=True, unsat=True)
+    assert torch.equal(f2, f[33:50]) and torch.equal(g2, g[33:50]) and torch.equal(u2, u[33:50])
+
+
 def test_c4_hybrid_global_full_batch():
     """c4's shape (3-CNF + XOR k = 3..64, n = 1024) on the global path (short and long kernels) at B = 1024 (the
     bench launch configuration); oracle on every point of a 1024-point batch."""
