@@ -262,3 +262,102 @@ def solve_sharded(search, check, round_len: int, max_rounds: int, rank: int = 0,
         rs.restart()
     return {"sat": 0, "assignment": best_a, "best_unsat": best_cnt, "point": best_gp, "rounds": rounds,
             "iterations": iters, "seconds": time.perf_counter() - t0}
+
+
+def portfolio_groups(world: int, n_strategies: int, dist=None):
+    """Strategy of each rank and the process groups of the portfolio ("employing multiple GPUs to
+    simultaneously attempt different search strategies"): with world >= n_strategies, rank r runs strategy r mod n
+    and strategy s's U_c are summed over the ranks running it (its own group); with fewer ranks than strategies
+    every rank runs every strategy on a share of its points (groups None = the whole world).  Returns
+    (strategies of this rank as a list of (strategy, group)) for every rank, in rank order."""
+    if world >= n_strategies:
+        groups = [None] * n_strategies
+        if dist is not None and world > 1:
+            # every rank must create every group, in the same order
+            groups = [dist.new_group([r for r in range(world) if r % n_strategies == s]) for s in range(n_strategies)]
+        return [[(r % n_strategies, groups[r % n_strategies])] for r in range(world)]
+    return [[(s, None) for s in range(n_strategies)] for _ in range(world)]
+
+
+def solve_portfolio(searches, check, round_len: int, max_rounds: int, rank: int = 0, world: int = 1, timeout_s: float = 0.0):
+    """Portfolio of restart-sharded searches (Table 2 "Portfolio"): `searches` is
+    this rank's list of (strategy, search, group) -- each search with its own strategy parameters (e.g. ERWA + (ROF) rephasing
+    vs fixed weights + fresh random restarts) and point0 range disjoint from every other search of any rank (keys are
+    global point indices); group is the process group over which that strategy's U_c are summed (None = this rank
+    alone when world == 1, else the world).  Every round all searches run round_len PGD iterations, exchange U_c
+    within their strategy, and the library's keys are MIN-reduced over this rank's searches and then over the world:
+    the first solution of ANY strategy stops every rank (C1), verified by `check`.
+
+    Returns dict(sat, assignment, best_unsat, point, strategy, rounds, seconds)."""
+    import time
+    import torch
+    import torch.distributed as dist
+    t0 = time.perf_counter()
+    runs, strategies = [], []
+    for strat, s, g in searches:
+        T = s.tensors()
+        runs.append((s, g, T, int(getattr(s, "point0", 0)), int(T["unsat"].numel())))
+        strategies.append(int(strat))
+        s.begin_round()
+    dev = runs[0][2]["unsat"].device
+    keys = torch.empty(2, dtype=torch.int64, device=dev)
+    stop = torch.zeros(1, dtype=torch.int32, device=dev)
+    best_cnt, best_gp, best_a = None, -1, None
+
+    def owner_of(gp):
+        for i, (s, g, T, p0, B) in enumerate(runs):
+            if 0 <= gp - p0 < B:
+                return i
+        return -1
+
+    def fetch(gp):
+        i = owner_of(gp)
+        n = runs[0][2]["x"].shape[1]
+        a = torch.zeros(n, dtype=torch.int8, device=dev)
+        if i >= 0:
+            s, g, T, p0, B = runs[i]
+            a.copy_(torch.as_tensor(np.asarray(s.assignment(gp - p0)), device=dev))
+        if world > 1:
+            owner = torch.tensor([rank if i >= 0 else -1], dtype=torch.int64, device=dev)
+            dist.all_reduce(owner, op=dist.ReduceOp.MAX)
+            dist.broadcast(a, src=int(owner.item()))
+        return a.cpu().numpy()
+
+    rounds = 0
+    for rounds in range(1, max_rounds + 1):
+        keys.fill_(INT64_MAX)
+        for s, g, T, p0, B in runs:
+            s.iterate(round_len)
+            s.check()
+            if world > 1:
+                dist.all_reduce(T["U"], op=dist.ReduceOp.SUM, group=g)
+            s.reduce()
+            torch.minimum(keys, T["keys"], out=keys)
+        if world > 1:
+            dist.all_reduce(keys, op=dist.ReduceOp.MIN)
+        k = keys.cpu()
+        solved_gp, inc = int(k[0]), int(k[1])
+        if solved_gp != INT64_MAX:
+            a = fetch(solved_gp)
+            if check(a)[0] == 0:
+                i = owner_of(solved_gp)
+                strat = torch.tensor([strategies[i] if i >= 0 else -1], dtype=torch.int64, device=dev)
+                if world > 1:
+                    dist.all_reduce(strat, op=dist.ReduceOp.MAX)
+                return {"sat": 1, "assignment": a, "best_unsat": 0, "point": solved_gp, "strategy": int(strat.item()),
+                        "rounds": rounds, "seconds": time.perf_counter() - t0}
+        cnt, gp = inc >> 32, inc & 0xFFFFFFFF
+        if best_cnt is None or cnt < best_cnt:
+            best_a = fetch(gp)
+            best_cnt, best_gp = check(best_a)[0], gp
+        if timeout_s > 0:
+            stop.fill_(1 if (rank == 0 and time.perf_counter() - t0 > timeout_s) else 0)
+            if world > 1:
+                dist.all_reduce(stop, op=dist.ReduceOp.MAX)
+            if int(stop.item()):
+                break
+        for s, g, T, p0, B in runs:
+            s.restart(T["U"])
+            s.begin_round()
+    return {"sat": 0, "assignment": best_a, "best_unsat": best_cnt, "point": best_gp, "strategy": -1, "rounds": rounds,
+            "seconds": time.perf_counter() - t0}

@@ -168,3 +168,38 @@ def test_solve_sharded_real_library(tmp_path):
         assert int(p["sat"]) == 1 and int(p["rounds"]) == one["rounds"] and int(p["point"]) == one["point"]
         assert np.array_equal(p["a"], one["assignment"])
         assert cdp.check(Fo, np.where(p["a"] < 0, -1.0, 1.0)[None])[0][0] == 0
+
+
+# ------------------------------------------------------------------------------------------ portfolio (f1)
+
+PF_STRATS = [dict(policy="ROF", adaptive_weights=1), dict(policy="R", adaptive_weights=0)]
+
+
+def _portfolio(rank, world):
+    inst = _solve_inst()
+    ctx = P.Context.from_instance(inst, device=0)
+    mine = D.portfolio_groups(world, 2, dist if world > 1 else None)[rank]
+    searches = [(s, ctx.search(64, seed=3, point0=64 * s, max_inner=30, **PF_STRATS[s]), g) for s, g in mine]
+    return D.solve_portfolio(searches, ctx.check, round_len=30, max_rounds=200, rank=rank, world=world)
+
+
+def _portfolio_worker(rank, world, port, out):
+    _init(rank, world, port)
+    r = _portfolio(rank, world)
+    np.savez(out + f".{rank}.npz", sat=r["sat"], a=r["assignment"], point=r["point"], rounds=r["rounds"],
+             strategy=r["strategy"])
+    dist.destroy_process_group()
+
+
+def test_portfolio_real_library(tmp_path):
+    """Both strategies on one GPU (two searches) vs one strategy per rank: the same round, point, strategy and
+    verified assignment."""
+    torch.cuda.set_device(0)
+    one = _portfolio(0, 1)
+    assert one["sat"] == 1
+    out = str(tmp_path / "pf")
+    mp.spawn(_portfolio_worker, args=(2, free_port(), out), nprocs=2, join=True)
+    for r in range(2):
+        p = np.load(out + f".{r}.npz")
+        assert int(p["sat"]) == 1 and int(p["rounds"]) == one["rounds"] and int(p["point"]) == one["point"]
+        assert int(p["strategy"]) == one["strategy"] and np.array_equal(p["a"], one["assignment"])

@@ -256,3 +256,60 @@ def test_solve_sharded_unsat_returns_unknown_with_incumbent():
     r = D.solve_sharded(s, check, round_len=5, max_rounds=3)
     assert r["sat"] == 0 and r["best_unsat"] == 1 and r["rounds"] == 3
     assert inst.m == 2
+
+
+# ---------------------------------------------------------------------------------------------- portfolio (f1)
+
+STRATS = [osolve.Params(max_inner=2, policy="ROF", adaptive_weights=True),   # heuristics
+          osolve.Params(max_inner=2, policy="R", adaptive_weights=False)]    # fresh random restarts, fixed weights
+
+
+def _portfolio(rank, world, B=8):
+    Fo = OracleFormula.from_arrays(*_planted().arrays())
+    mine = D.portfolio_groups(world, 2, dist if world > 1 else None)[rank]
+    searches = [(s, OracleSearch(Fo, B, 99, s * B, STRATS[s]), g) for s, g in mine]
+
+    def check(a):
+        cnt, fw = cdp.check(Fo, np.where(np.asarray(a) < 0, -1.0, 1.0)[None])
+        return int(cnt[0]), float(fw[0])
+    return D.solve_portfolio(searches, check, round_len=2, max_rounds=40, rank=rank, world=world)
+
+
+def _portfolio_worker(rank, world, port, out):
+    _init(rank, world, port)
+    r = _portfolio(rank, world)
+    np.savez(out + f".{rank}.npz", sat=r["sat"], a=r["assignment"], point=r["point"], rounds=r["rounds"],
+             strategy=r["strategy"])
+    dist.destroy_process_group()
+
+
+def test_portfolio_groups_layout():
+    assert D.portfolio_groups(1, 2) == [[(0, None), (1, None)]]
+    lay = D.portfolio_groups(4, 2)
+    assert [[s for s, _ in r] for r in lay] == [[0], [1], [0], [1]]
+
+
+def test_portfolio_one_process_equals_one_strategy_per_rank(tmp_path):
+    """f1 portfolio: both strategies on one process (one GPU, two searches) and one strategy per rank (two GPUs,
+    "heuristics on / off per GPU group") stop at the same round with the same verified solution, because every point
+    is keyed by its global index and each strategy's U_c stays within its group; the winner is at least as fast as
+    either strategy alone."""
+    one = _portfolio(0, 1)
+    assert one["sat"] == 1
+    out = str(tmp_path / "pf")
+    mp.spawn(_portfolio_worker, args=(2, free_port(), out), nprocs=2, join=True)
+    Fo = OracleFormula.from_arrays(*_planted().arrays())
+    for r in range(2):
+        p = np.load(out + f".{r}.npz")
+        assert int(p["sat"]) == 1 and int(p["rounds"]) == one["rounds"] and int(p["point"]) == one["point"]
+        assert int(p["strategy"]) == one["strategy"] and np.array_equal(p["a"], one["assignment"])
+        assert cdp.check(Fo, np.where(p["a"] < 0, -1.0, 1.0)[None])[0][0] == 0
+    for s in range(2):   # each strategy alone (same points, same keys) never beats the portfolio
+        Fo2 = OracleFormula.from_arrays(*_planted().arrays())
+
+        def check(a):
+            cnt, fw = cdp.check(Fo2, np.where(np.asarray(a) < 0, -1.0, 1.0)[None])
+            return int(cnt[0]), float(fw[0])
+        alone = D.solve_portfolio([(s, OracleSearch(Fo2, 8, 99, s * 8, STRATS[s]), None)], check, round_len=2,
+                                  max_rounds=40)
+        assert (not alone["sat"]) or alone["rounds"] >= one["rounds"]
