@@ -127,7 +127,7 @@ ffsat_status ffsat_export(const ffsat_ctx* ctx, uint8_t* kind, int32_t* bound, d
  * checked for NaN/Inf -> FFSAT_ERR_NONFINITE, detected by a device kernel on the staged copy: the
  * outputs are then unspecified).  f_out [B] double; grad_out [B][n] or NULL; unsat_out [B] int32 or
  * NULL.  Weights: the context's current weights (ffsat_set_weights).
- * Host buffers (on_device = 0) are staged in 2-4 equal chunks (B >= 512) whose H2D / D2H copies overlap
+ * Host buffers (on_device = 0) are staged in up to 4 equal chunks of at least batch_ref points whose H2D / D2H copies overlap
  * the chunk evaluations; pinned host memory is needed for the overlap (pageable memory still works).
  * The call returns when the outputs are in host memory.  Device buffers (on_device = 1) are asynchronous
  * on `stream`.  B = 0 is a no-op.  Results per point do not depend on B or on the point's position in the

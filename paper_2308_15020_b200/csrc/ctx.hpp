@@ -168,9 +168,17 @@ void plan_chunks(ffsat_ctx* c);
 void ensure_scratch(const ffsat_ctx* c, Scratch& S, int64_t B);
 // f (fp64), grad (T, may be null), unsat (int32, may be null) at device points x [B][n] under weights w_pos (position
 // order); async on st, scratch S (eval_f32.cu / eval_f64.cu).  profiled: record c->ev[0..4] around the phases.
+// partials_only: stop before the reductions (the search's fused PGD step reduces the point-major partials itself).
 template <typename T>
 void eval_device_t(ffsat_ctx* c, Scratch& S, const T* x, int64_t B, double* f, T* grad, int32_t* unsat, const T* w_pos,
-                   cudaStream_t st, bool profiled);
+                   cudaStream_t st, bool profiled, bool partials_only = false);
+namespace dev {
+template <typename T>
+struct PmReduce;
+}
+// the reduction arguments of the point-major partials of scratch S (tiled TMEM path)
+template <typename T>
+dev::PmReduce<T> pm_reduce_args(const ffsat_ctx* c, const Scratch& S, int64_t B, bool unsat);
 // allow the tiled kernels of dtype T the dynamic shared memory they need (eval_f32.cu / eval_f64.cu)
 template <typename T>
 void set_tiled_smem(size_t bytes);

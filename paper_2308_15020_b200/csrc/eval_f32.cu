@@ -2,7 +2,8 @@
 #include "eval_impl.cuh"
 
 namespace ffsat {
-template void eval_device_t<float>(ffsat_ctx*, Scratch&, const float*, int64_t, double*, float*, int32_t*, const float*, cudaStream_t, bool);
+template void eval_device_t<float>(ffsat_ctx*, Scratch&, const float*, int64_t, double*, float*, int32_t*, const float*, cudaStream_t, bool, bool);
+template dev::PmReduce<float> pm_reduce_args<float>(const ffsat_ctx*, const Scratch&, int64_t, bool);
 template void set_tiled_smem<float>(size_t);
 template void set_long_smem<float>();
 

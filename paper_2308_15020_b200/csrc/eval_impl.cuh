@@ -76,8 +76,19 @@ inline int fast_kmax_short(const Layout& L) {
 
 // f (fp64), grad (T, may be null), unsat (int32, may be null) at device points x [B][n]; async on st.
 template <typename T>
+dev::PmReduce<T> pm_reduce_args(const ffsat_ctx* c, const Scratch& S, int64_t B, bool unsat) {
+    const Layout& L = c->Lo;
+    dev::PmReduce<T> r{};
+    r.B = B; r.n = L.n; r.n_chunks = L.n_fast > 0 ? c->n_chunks : 0; r.groups = c->f_groups; r.n_sym = L.n_sym;
+    r.P = S.P.as<T>(); r.Tb = S.Tb.as<T>(); r.occ_off = c->occ_off.as<int64_t>(); r.occ_slot = c->occ_slot.as<int32_t>();
+    r.fpart = S.fpart.as<double>(); r.upart = unsat ? S.upart.as<int32_t>() : nullptr; r.fsym = S.fsym.as<double>();
+    r.usym = S.usym.as<int32_t>();
+    return r;
+}
+
+template <typename T>
 void eval_device_t(ffsat_ctx* c, Scratch& S, const T* x, int64_t B, double* f, T* grad, int32_t* unsat, const T* w_pos,
-                   cudaStream_t st, bool profiled) {
+                   cudaStream_t st, bool profiled, bool partials_only) {
     const Layout& L = c->Lo;
     if (B == 0) return;
     ensure_scratch(c, S, B);
@@ -214,7 +225,20 @@ void eval_device_t(ffsat_ctx* c, Scratch& S, const T* x, int64_t B, double* f, T
     mark(1);
     if (profiled) launch_sym_all();
     join_sym();
+    if (partials_only) return;
     mark(2);
+    if (L.tmem) {
+        // point-major partials of the TMEM kernel: gradient (optional), f and unsat in one reduction kernel, programmatic
+        // after the product kernel
+        c->launches += 1;
+        const dev::PmReduce<T> r = pm_reduce_args<T>(c, S, B, unsat != nullptr);
+        const unsigned threads = (unsigned)std::min(256, std::max(32, (L.n + 31) / 32 * 32));
+        launch_pdl(dev::reduce_pm_kernel<T>, dim3((unsigned)B), dim3(threads), 0, st, r, grad, f, unsat);
+        CK(cudaGetLastError());
+        mark(3);
+        mark(4);
+        return;
+    }
     dev::ReduceFArgs rf{};
     rf.B = B; rf.n_parts = L.n_fast > 0 ? c->n_chunks + c->n_fold : 0; rf.n_sym = L.n_sym;
     rf.fpart = S.fpart.as<double>(); rf.upart = S.upart.as<int32_t>(); rf.fsym = S.fsym.as<double>();

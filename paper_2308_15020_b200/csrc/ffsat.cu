@@ -36,6 +36,7 @@ struct ffsat_search {
     ffsat_solve_params P{};
     DBuf X, Xp, Gx, Gp, fX, fP, dot, eta, done, iters, unsatP, solved, sol, unsat, U, stats, xT;
     DBuf W;                       // this search's current weights (position order, context dtype): ERWA state
+    DBuf umax;                    // max U_c of the ERWA update
     Scratch sc;                   // this search's evaluation scratch (referenced by its captured graph)
     int64_t round = 0, iters_issued = 0;
     // one CLS iteration captured as a CUDA graph (replayed by ffsat_search_iterate), in two variants: [1] with the
@@ -244,6 +245,7 @@ void search_alloc(ffsat_search* s) {
     s->sol.ensure(std::max<size_t>(16, Bn));
     s->U.ensure(std::max<size_t>(16, (size_t)m * 4));
     s->W.ensure(std::max<size_t>(16, (size_t)m * es));
+    s->umax.ensure(16);
     s->stats.ensure(64);
     ensure_scratch(s->ctx, s->sc, B);
     CK(cudaMemset(s->solved.p, 0, (size_t)B * 4));
@@ -267,11 +269,18 @@ void search_begin_round(ffsat_search* s, cudaStream_t st) {
     s->ctx->launches += 2;
     dev::reset_round_kernel<<<blocks_for(s->B, 256), 256, 0, st>>>(s->eta.as<double>(), s->done.as<int32_t>(),
                                                                     s->iters.as<int32_t>(), s->B, s->P.eta0);
-    if (f64) search_eval<double>(s, s->X.p, s->fX.as<double>(), s->Gx.p, s->unsatP.as<int32_t>(), st);
-    else search_eval<float>(s, s->X.p, s->fX.as<double>(), s->Gx.p, s->unsatP.as<int32_t>(), st);
-    dev::PgdArgs a = pgd_args(s, 0, true);
-    if (f64) dev::pgd_step_kernel<double><<<(unsigned)s->B, 256, 0, st>>>(a);
-    else dev::pgd_step_kernel<float><<<(unsigned)s->B, 256, 0, st>>>(a);
+    // the round's start point x (rephased): f and gradient, no check (the round-end check catches solutions)
+    dev::PgdArgs a = pgd_args(s, 0, false);
+    if (!f64 && s->ctx->Lo.tmem) {
+        eval_device_t<float>(s->ctx, s->sc, s->X.as<float>(), s->B, nullptr, nullptr, nullptr, s->W.as<float>(), st, false, true);
+        const dev::PmReduce<float> r = pm_reduce_args<float>(s->ctx, s->sc, s->B, false);
+        launch_pdl(dev::pgd_fused_kernel<float>, dim3((unsigned)s->B), dim3(256), 0, st, a, r);
+    } else {
+        if (f64) search_eval<double>(s, s->X.p, s->fX.as<double>(), s->Gx.p, nullptr, st);
+        else search_eval<float>(s, s->X.p, s->fX.as<double>(), s->Gx.p, nullptr, st);
+        if (f64) dev::pgd_step_kernel<double><<<(unsigned)s->B, 256, 0, st>>>(a);
+        else dev::pgd_step_kernel<float><<<(unsigned)s->B, 256, 0, st>>>(a);
+    }
     CK(cudaGetLastError());
     s->iters_issued = 0;
 }
@@ -341,7 +350,12 @@ void search_iterate_one(ffsat_search* s, bool checked, cudaStream_t st) {
     dev::PgdArgs a = pgd_args(s, 1, checked);
     int32_t* u = checked ? s->unsatP.as<int32_t>() : nullptr;
     s->ctx->launches += 1;
-    if (f64) {
+    if (!f64 && s->ctx->Lo.tmem) {
+        // tiled TMEM path: the evaluation stops at its point-major partials; the PGD step reduces them itself
+        eval_device_t<float>(s->ctx, s->sc, s->Xp.as<float>(), s->B, nullptr, nullptr, u, s->W.as<float>(), st, false, true);
+        const dev::PmReduce<float> r = pm_reduce_args<float>(s->ctx, s->sc, s->B, checked);
+        launch_pdl(dev::pgd_fused_kernel<float>, dim3((unsigned)s->B), dim3(256), 0, st, a, r);
+    } else if (f64) {
         search_eval<double>(s, s->Xp.p, s->fP.as<double>(), s->Gp.p, u, st);
         dev::pgd_step_kernel<double><<<(unsigned)s->B, 256, 0, st>>>(a);
     } else {
@@ -380,6 +394,14 @@ void check_kernels(ffsat_search* s, cudaStream_t st) {
     a.S = S; a.B = s->B; a.n = L.n; a.m = L.m; a.off = c->chk_off.as<int64_t>();
     a.words = c->chk_words.as<uint32_t>(); a.rule = c->chk_rule.as<int32_t>();
     a.U = s->U.as<int32_t>(); a.unsat = s->unsat.as<int32_t>();
+    if (L.max_k <= 64) {   // short rows: thread per constraint over 8 point tiles
+        constexpr int TPC = 8;
+        dim3 grid(blocks_for(L.m, 256), (unsigned)((PT + TPC - 1) / TPC));
+        dev::check_rows_kernel<TPC><<<grid, 256, 0, st>>>(a);
+        s->ctx->launches += 2;
+        CK(cudaGetLastError());
+        return;
+    }
     // chunks: about one wave of CTAs, at least 1024 literals each (each CTA stages the tile's sign words)
     const int64_t want = std::max<int64_t>(1, (int64_t)c->num_sm * 8 / PT);
     const int64_t by_work = std::max<int64_t>(1, L.L / 1024);
@@ -410,8 +432,12 @@ void search_restart(ffsat_search* s, const int32_t* Ug, cudaStream_t st) {
     const int32_t* U = Ug ? Ug : s->U.as<int32_t>();
     if (s->P.adaptive_weights && L.m > 0) {
         s->ctx->launches += 1;
-        if (f64) dev::erwa_kernel<double><<<1, 1024, 0, st>>>(s->W.as<double>(), U, L.m, s->P.alpha);
-        else dev::erwa_kernel<float><<<1, 1024, 0, st>>>(s->W.as<float>(), U, L.m, s->P.alpha);
+        const unsigned g = (unsigned)std::min<int64_t>(4 * 148, (L.m + 255) / 256);
+        CK(cudaMemsetAsync(s->umax.p, 0, 4, st));
+        dev::umax_kernel<<<g, 256, 0, st>>>(U, L.m, s->umax.as<int32_t>());
+        if (f64) dev::erwa_kernel<double><<<g, 256, 0, st>>>(s->W.as<double>(), U, L.m, s->P.alpha, s->umax.as<int32_t>());
+        else dev::erwa_kernel<float><<<g, 256, 0, st>>>(s->W.as<float>(), U, L.m, s->P.alpha, s->umax.as<int32_t>());
+        s->ctx->launches += 1;
     }
     int p[3];
     int len = policy_codes(s->P.policy, p);
@@ -557,7 +583,9 @@ ffsat_status ffsat_eval(ffsat_ctx* c, const void* x, int64_t B, int32_t on_devic
     // i (two copy engines); non-finite coordinates are flagged by a device kernel on the staged copy.
     // 2 chunks, up to 4 for batches over ~2 MB (smaller chunks multiply the tiled path's partial-tile traffic)
     const size_t xbytes = (size_t)B * (size_t)c->Lo.n * es;
-    const int64_t nchunk = B < 512 ? 1 : xbytes >= (4u << 20) ? 4 : xbytes >= (2u << 20) ? 3 : 2;
+    // chunks of at least batch_ref points: the launch plan is sized for batch_ref, a smaller chunk underfills the GPU
+    int64_t nchunk = B < 512 ? 1 : xbytes >= (4u << 20) ? 4 : xbytes >= (2u << 20) ? 3 : 2;
+    nchunk = std::max<int64_t>(1, std::min<int64_t>(nchunk, B / std::max<int64_t>(1, c->batch_ref)));
     const int64_t Bc = nchunk == 1 ? B : ((B + nchunk - 1) / nchunk + 63) / 64 * 64;
     const int64_t nck = Bc > 0 ? (B + Bc - 1) / Bc : 0;
     const size_t n = (size_t)c->Lo.n;

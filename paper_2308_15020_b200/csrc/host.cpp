@@ -228,7 +228,7 @@ size_t tiled_smem_bytes(int n, int precision) {
 }
 
 size_t wide_smem_bytes(int n) { return std::max<size_t>(4 * (size_t)kWidePitch * (size_t)n, 6144); }  // >= the final f / unsat exchange (8 x 64 x 12 B)
-size_t tmem_smem_bytes(int n) { return std::max<size_t>(2 * 256 * (size_t)n, 12288); }   // x tile + 2nd sum tile; >= 16 x 64 x 12 B
+size_t tmem_smem_bytes(int n) { return std::max<size_t>(2 * 260 * (size_t)n, 12288); }   // 2 sum tiles [n][65] (the x tile is the first); >= 16 x 64 x 12 B
 uint32_t tmem_cols(int n) {
     uint32_t c = 32;
     while (c < 2u * (uint32_t)n) c <<= 1;

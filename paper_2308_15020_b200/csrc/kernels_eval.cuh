@@ -1079,11 +1079,13 @@ __global__ void __launch_bounds__(32 * kTmemWarps, 1) fast_tmem_kernel(TiledArgs
     }
     pdl_trigger();
     // the four quadrant tiles summed in a fixed order, (q0 + q2) + (q1 + q3), through two shared tiles T0 = x tile
-    // region, T1 after it: round 1 q0 -> T0 and q1 -> T1, round 2 q2 += T0 and q3 += T1, then T0 + T1.  Each warp moves 8
-    // variables (16 columns) per tcgen05.ld.
+    // region, T1 after it (rows of 65 floats: the point-major write-out below reads them conflict-free): round 1
+    // q0 -> T0 and q1 -> T1, round 2 q2 += T0 and q3 += T1, then T0 + T1.  Each warp moves 8 variables (16 columns)
+    // per tcgen05.ld.
     __syncthreads();
-    float* T0 = xs;             // [n][64]
-    float* T1 = xs + n * 64;    // [n][64]
+    constexpr int TP = 65;
+    float* T0 = xs;              // [n][65]
+    float* T1 = xs + n * TP;     // [n][65]
     for (int round = 0; round < 2; ++round) {
         if ((q >> 1) == round) {
             float* T = (q & 1) ? T1 : T0;
@@ -1099,12 +1101,14 @@ __global__ void __launch_bounds__(32 * kTmemWarps, 1) fast_tmem_kernel(TiledArgs
 #pragma unroll
                 for (int j = 0; j < 8; ++j) {
                     if (v8 + j < n) {
-                        float2* dst = reinterpret_cast<float2*>(T + (v8 + j) * 64) + lane;
-                        const float2 gv = make_float2(__uint_as_float(g[2 * j]), __uint_as_float(g[2 * j + 1]));
-                        if (round == 0) *dst = gv;
-                        else {
-                            const float2 o = *dst;
-                            *dst = make_float2(o.x + gv.x, o.y + gv.y);
+                        float* dst = T + (v8 + j) * TP + 2 * lane;
+                        const float gx = __uint_as_float(g[2 * j]), gy = __uint_as_float(g[2 * j + 1]);
+                        if (round == 0) {
+                            dst[0] = gx;
+                            dst[1] = gy;
+                        } else {
+                            dst[0] += gx;
+                            dst[1] += gy;
                         }
                     }
                 }
@@ -1117,18 +1121,13 @@ __global__ void __launch_bounds__(32 * kTmemWarps, 1) fast_tmem_kernel(TiledArgs
         tmem_fence_after();
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(st.tbase), "r"(tcols));
     }
-    float* G = T0;
-    const int64_t b = b0 + 2 * lane;
-    for (int v = warp; v < n; v += kTmemWarps) {
-        const float2 g0 = reinterpret_cast<const float2*>(G + v * 64)[lane];
-        const float2 g1 = reinterpret_cast<const float2*>(T1 + v * 64)[lane];
-        const float2 g = make_float2(g0.x + g1.x, g0.y + g1.y);
-        float* dst = a.P + ((int64_t)chunk * n + v) * a.B + b;
-        if (b + 1 < a.B && ((a.B & 1) == 0)) *reinterpret_cast<float2*>(dst) = g;
-        else {
-            if (b < a.B) dst[0] = g.x;
-            if (b + 1 < a.B) dst[1] = g.y;
-        }
+    // the chunk's partial gradient, POINT-major: P[chunk][b][v] (a point's row is contiguous, so the reduction -- or
+    // the fused PGD step, one CTA per point -- reads it coalesced); warp w writes points w, w + 16, ..., lanes over v
+    for (int p = warp; p < 64; p += kTmemWarps) {
+        const int64_t bp = b0 + p;
+        if (bp >= a.B) break;
+        float* dst = a.P + ((int64_t)chunk * a.B + bp) * n;
+        for (int v = lane; v < n; v += 32) dst[v] = T0[v * TP + p] + T1[v * TP + p];
     }
     __syncthreads();
     double* fr = reinterpret_cast<double*>(smem_raw);         // [16][64]
@@ -2087,6 +2086,86 @@ __global__ void __launch_bounds__(32 * NW) fold_rows_kernel(double* fpart, int32
         }
         fpart[(dst + blockIdx.x) * B + b] = t;
         if (upart) upart[(dst + blockIdx.x) * B + b] = tu;
+    }
+}
+
+// ---- reductions of POINT-major partials (the TMEM kernel writes P[chunk][b][v]): one warp per point, lanes over
+//      variables.  Sums in the same fixed orders as reduce_grad_kernel / reduce_f_kernel (so the result bits do not
+//      depend on which kernel reduced them): gradient = chunk partials in chunk order, then the variable's T slots
+//      ascending (fp64); f / unsat = `groups` interleaved row groups (rows j, j + groups, ... of the chunk partials,
+//      then of the root-path constraints), groups added in order.
+template <typename T>
+struct PmReduce {
+    int64_t B;
+    int32_t n, n_chunks, groups;
+    int64_t n_sym;
+    const T* P;                  // [n_chunks][B][n]
+    const T* Tb;                 // [tb_slots][B]
+    const int64_t* occ_off;
+    const int32_t* occ_slot;
+    const double* fpart;         // [n_chunks][B]
+    const int32_t* upart;        // or null (no check)
+    const double* fsym;          // [n_sym][B]
+    const int32_t* usym;
+};
+
+template <typename T>
+__device__ __forceinline__ double pm_grad(const PmReduce<T>& a, int64_t b, int v) {
+    double acc = 0.0;
+    const T* p = a.P + b * a.n + v;
+    const int64_t stride = a.B * a.n;
+    int c = 0;
+    for (; c + 4 <= a.n_chunks; c += 4) {
+        T t[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) t[j] = p[(int64_t)(c + j) * stride];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc += (double)t[j];
+    }
+    for (; c < a.n_chunks; ++c) acc += (double)p[(int64_t)c * stride];
+    for (int64_t o = a.occ_off[v]; o < a.occ_off[v + 1]; ++o) acc += (double)a.Tb[(int64_t)a.occ_slot[o] * a.B + b];
+    return acc;
+}
+
+// f / unsat of point b by one whole warp: lane j < groups sums group j (chunk rows j, j + groups, ... then root-path
+// rows j, j + groups, ..., ascending), then the group sums are added in group order (moved by shuffles) -- the order
+// of reduce_f_kernel, bit for bit.  Every lane returns the result.
+template <typename T>
+__device__ __forceinline__ double pm_f_warp(const PmReduce<T>& a, int64_t b, int* unsat) {
+    const int lane = threadIdx.x & 31;
+    double fj = 0.0;
+    int u = 0;
+    if (lane < a.groups) {
+        for (int c = lane; c < a.n_chunks; c += a.groups) {
+            fj += a.fpart[(int64_t)c * a.B + b];
+            if (a.upart) u += a.upart[(int64_t)c * a.B + b];
+        }
+        for (int64_t s = lane; s < a.n_sym; s += a.groups) {
+            fj += a.fsym[s * a.B + b];
+            if (a.upart) u += a.usym[s * a.B + b];
+        }
+    }
+    double f = 0.0;
+    for (int j = 0; j < a.groups; ++j) f += __shfl_sync(0xffffffffu, fj, j);
+    *unsat = __reduce_add_sync(0xffffffffu, u);
+    return f;
+}
+
+// grad [B][n] (or null), f [B], unsat [B] (or null): one CTA per point, one thread per variable (n <= 256 on the TMEM
+// path; blockDim = n rounded up to a warp), so every partial of the point is loaded in one round trip.
+template <typename T>
+__global__ void __launch_bounds__(256) reduce_pm_kernel(PmReduce<T> a, T* grad, double* f, int32_t* unsat) {
+    pdl_wait();
+    const int64_t b = blockIdx.x;
+    if (grad)
+        for (int v = threadIdx.x; v < a.n; v += blockDim.x) grad[b * a.n + v] = (T)pm_grad(a, b, v);
+    if (threadIdx.x < 32) {
+        int u = 0;
+        const double fb = pm_f_warp(a, b, &u);
+        if (threadIdx.x == 0) {
+            f[b] = fb;
+            if (unsat) unsat[b] = u;
+        }
     }
 }
 

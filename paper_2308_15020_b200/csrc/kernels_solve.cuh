@@ -8,13 +8,15 @@
 //   signpack_kernel,       Alg. 1 line 5 / Thm. 4: exact integer check of sgn(x) per
 //   check_bits_kernel      (constraint, point) on sign words of 32 points: unsat[b] and U[c].
 //                          Integer atomics only: totals are exact and order-independent.
-//   erwa_kernel            Prop. 3: w <- (1-alpha) w + alpha U/max U (skipped if max U = 0).
+//   umax_kernel,           Prop. 3: w <- (1-alpha) w + alpha U/max U (skipped if max U = 0).
+//   erwa_kernel
 //   rephase_kernel         O / F / R phases in the policy cycle, offset by global point.
 #pragma once
 #include <cstdint>
 #include <cuda_runtime.h>
 
 #include "kernels_common.cuh"
+#include "kernels_eval.cuh"
 
 namespace ffsat {
 namespace dev {
@@ -135,6 +137,93 @@ __global__ void __launch_bounds__(256) pgd_step_kernel(PgdArgs a) {
         T xn = act ? clamp1(xv - eta * g) : xv;
         Xp[v] = xn;
         d += (double)g * (double)(xn - xv);
+    }
+    red[threadIdx.x] = d;
+    __syncthreads();
+    for (int s = 128; s > 0; s >>= 1) {
+        if (threadIdx.x < s) red[threadIdx.x] += red[threadIdx.x + s];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) a.dot[b] = red[0];
+}
+
+// The PGD step fused with the reduction of point-major partials (tiled TMEM path, n <= 256 <= blockDim): per point
+// b the CTA sums its gradient (one variable per thread) and f / unsat from the evaluation's partials in the fixed
+// orders of reduce_pm_kernel (the same bits), then takes the Armijo decision and proposes the next trial exactly as
+// pgd_step_kernel -- the gradient of the trial never round-trips through HBM.  mode 0 (round start): the evaluated
+// point is x itself (f and gradient at x, first trial).  One CTA per point.
+template <typename T>
+__global__ void __launch_bounds__(256) pgd_fused_kernel(PgdArgs a, PmReduce<T> r) {
+    pdl_wait();
+    __shared__ double red[256];
+    __shared__ int s_acc;
+    __shared__ double s_f;
+    __shared__ int s_u;
+    const int64_t b = blockIdx.x;
+    const int n = a.n;
+    const int v = threadIdx.x;
+    T* X = reinterpret_cast<T*>(a.X) + b * n;
+    T* Xp = reinterpret_cast<T*>(a.Xp) + b * n;
+    T* Gx = reinterpret_cast<T*>(a.Gx) + b * n;
+    int8_t* sol = a.sol + b * n;
+    const T g = v < n ? (T)pm_grad(r, b, v) : (T)0;   // gradient at the trial point
+    if (threadIdx.x < 32) {
+        int u = 0;
+        const double fb = pm_f_warp(r, b, &u);
+        if (threadIdx.x == 0) {
+            s_f = fb;
+            s_u = u;
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0 && a.mode == 0) {   // round start: the evaluated point is x itself
+        a.fX[b] = s_f;
+        const int newly = (a.checked && s_u == 0 && !a.solved[b]) ? 1 : 0;
+        if (newly) a.solved[b] = 1;
+        s_acc = 1 | (newly << 1);   // "accept": Gx <- g below (X is unchanged)
+    } else if (threadIdx.x == 0) {
+        const double fp = s_f;
+        a.fP[b] = fp;
+        if (a.checked) a.unsatP[b] = s_u;
+        int acc = 0;
+        if (!a.done[b]) {
+            acc = fp <= a.fX[b] + a.c1 * a.dot[b];
+            double eta = a.eta[b];
+            eta = acc ? fmin(2.0 * eta, a.eta0) : 0.5 * eta;
+            a.eta[b] = eta;
+            const int it = a.iters[b] + 1;
+            a.iters[b] = it;
+            if (acc) a.fX[b] = fp;
+            if (eta < a.eta_min || it >= a.max_inner) a.done[b] = 1;
+        }
+        const int newly = (a.checked && s_u == 0 && !a.solved[b]) ? 1 : 0;
+        if (newly) a.solved[b] = 1;
+        s_acc = acc | (newly << 1);
+    }
+    __syncthreads();
+    const int flags = s_acc;
+    T xv = (T)0, gv = (T)0;
+    if (v < n) {
+        const T xp = a.mode == 0 ? X[v] : Xp[v];   // the evaluated point
+        if (flags & 2) sol[v] = xp < (T)0 ? (int8_t)-1 : (int8_t)1;
+        if (flags & 1) {
+            if (a.mode != 0) X[v] = xp;
+            Gx[v] = g;
+            xv = xp;
+            gv = g;
+        } else {
+            xv = X[v];
+            gv = Gx[v];
+        }
+    }
+    // next trial point
+    const bool act = !a.done[b];
+    const T eta = (T)a.eta[b];
+    double d = 0.0;
+    if (v < n) {
+        const T xn = act ? clamp1(xv - eta * gv) : xv;
+        Xp[v] = xn;
+        d = (double)gv * (double)(xn - xv);
     }
     red[threadIdx.x] = d;
     __syncthreads();
@@ -320,22 +409,69 @@ __global__ void __launch_bounds__(256) check_bits_kernel(CheckBitsArgs a) {
 }
 
 
-// ERWA (single block): maxU, then w = (1 - alpha) w + alpha U / maxU
-template <typename T>
-__global__ void __launch_bounds__(1024) erwa_kernel(T* w, const int32_t* U, int64_t m, double alpha) {
-    __shared__ int red[1024];
-    int mx = 0;
-    for (int64_t c = threadIdx.x; c < m; c += blockDim.x) mx = max(mx, U[c]);
-    red[threadIdx.x] = mx;
+// Round-end check for formulas without long rows (k <= 64): one thread per constraint over a group of TPC point
+// tiles (blockIdx.y), so U_c is counted in a register (one integer atomic per constraint and tile group instead of
+// one per constraint and tile) and the per-point counts of the CTA's tiles are accumulated in shared memory (ballot
+// transposition per warp and tile), then added to unsat[] once per CTA.  Integer sums: exact, order-free.
+template <int TPC>
+__global__ void __launch_bounds__(256) check_rows_kernel(CheckBitsArgs a) {
+    __shared__ int cnt[TPC * 32];
+    const int lane = threadIdx.x & 31;
+    const int64_t pt0 = (int64_t)blockIdx.y * TPC;
+    const int64_t PT = (a.B + 31) / 32;
+    const int ntile = (int)min((int64_t)TPC, PT - pt0);
+    for (int i = threadIdx.x; i < TPC * 32; i += blockDim.x) cnt[i] = 0;
     __syncthreads();
-    for (int s = 512; s > 0; s >>= 1) {
-        if ((int)threadIdx.x < s) red[threadIdx.x] = max(red[threadIdx.x], red[threadIdx.x + s]);
-        __syncthreads();
+    const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const bool cv = c < a.m;
+    int64_t lo = 0, hi = 0;
+    int tmin = 0, tmax = 0, par = 0;
+    if (cv) {
+        lo = __ldg(a.off + c);
+        hi = __ldg(a.off + c + 1);
+        tmin = __ldg(a.rule + 3 * c); tmax = __ldg(a.rule + 3 * c + 1); par = __ldg(a.rule + 3 * c + 2);
     }
-    mx = red[0];
+    int uc = 0;
+    for (int t = 0; t < ntile; ++t) {
+        const int64_t pt = pt0 + t, b0 = pt * 32;
+        const uint32_t vm = a.B - b0 >= 32 ? 0xffffffffu : ((1u << (a.B - b0)) - 1u);
+        uint32_t uns = 0u;
+        if (cv) uns = ~sat_mask<false, false>(a, a.S + pt * a.n, lo, hi, tmin, tmax, par, 0, 1) & vm;
+        uc += __popc(uns);
+#pragma unroll 8
+        for (int bb = 0; bb < 32; ++bb) {
+            const int k = __popc(__ballot_sync(0xffffffffu, (uns >> bb) & 1u));
+            if (lane == bb && k) atomicAdd(&cnt[t * 32 + bb], k);
+        }
+    }
+    if (cv && uc) atomicAdd(a.U + c, uc);
+    __syncthreads();
+    for (int i = threadIdx.x; i < ntile * 32; i += blockDim.x)
+        if (cnt[i] && pt0 * 32 + i < a.B) atomicAdd(a.unsat + pt0 * 32 + i, cnt[i]);
+}
+
+// ERWA (Prop. 3) in two grid-wide kernels: max U_c (block maxima, one integer atomicMax each: exact and
+// order-free), then w = (1 - alpha) w + alpha U / max U (skipped when max U = 0).
+__global__ void __launch_bounds__(256) umax_kernel(const int32_t* U, int64_t m, int32_t* umax) {
+    int mx = 0;
+    for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < m; c += (int64_t)gridDim.x * blockDim.x) mx = max(mx, U[c]);
+    mx = __reduce_max_sync(0xffffffffu, mx);
+    __shared__ int wm[8];
+    if ((threadIdx.x & 31) == 0) wm[threadIdx.x >> 5] = mx;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int t = 0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t = max(t, wm[w]);
+        if (t > 0) atomicMax(umax, t);
+    }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256) erwa_kernel(T* w, const int32_t* U, int64_t m, double alpha, const int32_t* umax) {
+    const int mx = *umax;
     if (mx == 0) return;
     const double inv = 1.0 / (double)mx;
-    for (int64_t c = threadIdx.x; c < m; c += blockDim.x)
+    for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < m; c += (int64_t)gridDim.x * blockDim.x)
         w[c] = (T)((1.0 - alpha) * (double)w[c] + alpha * ((double)U[c] * inv));
 }
 
