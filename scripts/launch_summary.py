@@ -11,7 +11,8 @@ rows = list(csv.reader(l for l in open(sys.argv[1]) if not l.startswith("==")))
 hdr = rows[0]
 ki, mi, vi, ui = hdr.index("Kernel Name"), hdr.index("Metric Name"), hdr.index("Metric Value"), hdr.index("Metric Unit")
 idi = hdr.index("ID")
-SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3}
+SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0,
+         "msecond": 1e3, "ms": 1e3}
 t = collections.defaultdict(dict)
 names = {}
 for r in rows[1:]:

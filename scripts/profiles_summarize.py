@@ -19,9 +19,10 @@ def num(v):
     return float(str(v).replace(",", ""))
 
 
-for rep, cfg, kname in (("prof_tiled", "c2", "fast_wide_kernel"), ("prof_sym", "c3", "sym_item_kernel"),
+for rep, cfg, kname in (("prof_tmem", "c2", "fast_tmem_kernel"), ("prof_tmem_chk", "c2", "fast_tmem_kernel_check"),
+                        ("prof_tiled", "c2", "fast_wide_kernel"), ("prof_sym", "c3", "sym_item_kernel"),
                         ("prof_global", "c5", "fast_global_kernel"), ("prof_short", "c4", "fast_global_kernel"),
-                        ("prof_long", "c4", "fast_global_long_kernel")):
+                        ("prof_long", "c4", "fast_global_long_kernel"), ("prof_reduce5", "c5", "reduce_grad_kernel")):
     p = os.path.join(G, rep + ".ncu-rep")
     if not os.path.exists(p):
         continue
@@ -67,11 +68,15 @@ def launches(src, dst):
             fh.write(f"{k},{n},{t:.1f},{t / n:.2f},{t / tot:.3f}\n")
 
 
-launches("launches_c2.csv", f"{tag}_launches_c2.csv")
-launches("launches_c3.csv", f"{tag}_launches_c3.csv")
-launches("launches_c4.csv", f"{tag}_launches_c4.csv")
-launches("launches_c5.csv", f"{tag}_launches_c5.csv")
+for c in ("c2", "c3", "c4", "c5"):   # per-kernel launch summaries written by scripts/gpu_launches.sh (time + DRAM bytes)
+    src = os.path.join(G, f"launch_summary_{c}.csv")
+    if os.path.exists(src):
+        with open(os.path.join(PR, f"{tag}_launches_{c}.csv"), "w") as fh:
+            fh.write("# ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none "
+                     "(cold-cache, serialised launches; bench.py --config " + c + " --steps 20 --warmup 3)\n")
+            fh.write(open(src).read())
 for f in sorted(os.listdir(G)):
-    if f.startswith("bench_") and f.endswith(".json") and os.path.getsize(os.path.join(G, f)):
+    if (f.startswith("bench") or f in ("table2_portfolio.json", "rq1_suite.json")) and f.endswith(".json") and \
+            os.path.getsize(os.path.join(G, f)):
         shutil.copy(os.path.join(G, f), os.path.join(PR, f"{tag}_{f}"))
 print(json.dumps(summary, indent=1))
