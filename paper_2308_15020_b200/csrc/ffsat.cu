@@ -266,9 +266,7 @@ dev::PgdArgs pgd_args(ffsat_search* s, int mode, bool checked) {
 
 void search_begin_round(ffsat_search* s, cudaStream_t st) {
     const bool f64 = s->ctx->Lo.precision == 64;
-    s->ctx->launches += 2;
-    dev::reset_round_kernel<<<blocks_for(s->B, 256), 256, 0, st>>>(s->eta.as<double>(), s->done.as<int32_t>(),
-                                                                    s->iters.as<int32_t>(), s->B, s->P.eta0);
+    s->ctx->launches += 1;   // eta / done / iterations are reset by the round-start PGD step itself
     // the round's start point x (rephased): f and gradient, no check (the round-end check catches solutions)
     dev::PgdArgs a = pgd_args(s, 0, false);
     if (!f64 && s->ctx->Lo.tmem) {

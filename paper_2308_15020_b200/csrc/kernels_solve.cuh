@@ -89,8 +89,11 @@ __global__ void __launch_bounds__(256) pgd_step_kernel(PgdArgs a) {
     const T* Gp = reinterpret_cast<const T*>(a.Gp) + b * n;
     int8_t* sol = a.sol + b * n;
     if (a.mode == 0) {
-        // round start: the evaluated point is x itself
+        // round start: the evaluated point is x itself; eta, done, iteration count restart
         if (threadIdx.x == 0) {
+            a.eta[b] = a.eta0;
+            a.done[b] = 0;
+            a.iters[b] = 0;
             int newly = (a.checked && a.unsatP[b] == 0 && !a.solved[b]) ? 1 : 0;
             if (newly) a.solved[b] = 1;
             s_acc = newly << 1;
@@ -176,7 +179,10 @@ __global__ void __launch_bounds__(256) pgd_fused_kernel(PgdArgs a, PmReduce<T> r
         }
     }
     __syncthreads();
-    if (threadIdx.x == 0 && a.mode == 0) {   // round start: the evaluated point is x itself
+    if (threadIdx.x == 0 && a.mode == 0) {   // round start: the evaluated point is x itself; eta, done, iterations restart
+        a.eta[b] = a.eta0;
+        a.done[b] = 0;
+        a.iters[b] = 0;
         a.fX[b] = s_f;
         const int newly = (a.checked && s_u == 0 && !a.solved[b]) ? 1 : 0;
         if (newly) a.solved[b] = 1;
