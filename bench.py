@@ -512,7 +512,9 @@ def main():
     for i in range(max(5, min(args.steps, 50))):
         if not args.no_flush:
             flush.zero_()
-        phases.append(ctx.eval_profiled(xd, fd, gd, ud))
+        # the evaluation of a PGD iteration between checks (no fused check: 9 of every 10 iterations at round_len 10;
+        # bench's check iterations and the ffsat_eval API count unsat as well)
+        phases.append(ctx.eval_profiled(xd, fd, gd, None if cfg["mode"] == "restart" else ud))
     ph = np.mean(np.array(phases[2:]), axis=0)  # ms: fast, root, grad-reduce, f-reduce
     roofline = roofline_of(info, inst, B, ph, args)
 
