@@ -158,9 +158,9 @@ __global__ void __launch_bounds__(256) pgd_step_kernel(PgdArgs a) {
 template <typename T>
 __global__ void __launch_bounds__(256) pgd_fused_kernel(PgdArgs a, PmReduce<T> r) {
     pdl_wait();
-    __shared__ double red[256];
-    __shared__ int s_acc;
-    __shared__ double s_f;
+    __shared__ double s_red[8];
+    __shared__ int s_acc, s_done;
+    __shared__ double s_f, s_eta;
     __shared__ int s_u;
     const int64_t b = blockIdx.x;
     const int n = a.n;
@@ -169,7 +169,21 @@ __global__ void __launch_bounds__(256) pgd_fused_kernel(PgdArgs a, PmReduce<T> r
     T* Xp = reinterpret_cast<T*>(a.Xp) + b * n;
     T* Gx = reinterpret_cast<T*>(a.Gx) + b * n;
     int8_t* sol = a.sol + b * n;
-    const T g = v < n ? (T)pm_grad(r, b, v) : (T)0;   // gradient at the trial point
+    // every load of the step first (they are independent, so one memory latency instead of a chain): the point's
+    // rows, the search state of the point, its partials
+    T x0 = (T)0, xp0 = (T)0, g0 = (T)0;
+    if (v < n) {
+        x0 = X[v];
+        if (a.mode != 0) xp0 = Xp[v];
+        g0 = Gx[v];
+    }
+    double st_fX = 0.0, st_dot = 0.0, st_eta = 0.0;
+    int st_done = 0, st_iters = 0, st_solved = 0;
+    if (threadIdx.x == 0) {
+        st_fX = a.fX[b]; st_dot = a.dot[b]; st_eta = a.eta[b];
+        st_done = a.done[b]; st_iters = a.iters[b]; st_solved = a.solved[b];
+    }
+    const T g = v < n ? (T)pm_grad(r, b, v) : (T)0;   // gradient at the evaluated point
     if (threadIdx.x < 32) {
         int u = 0;
         const double fb = pm_f_warp(r, b, &u);
@@ -179,65 +193,64 @@ __global__ void __launch_bounds__(256) pgd_fused_kernel(PgdArgs a, PmReduce<T> r
         }
     }
     __syncthreads();
-    if (threadIdx.x == 0 && a.mode == 0) {   // round start: the evaluated point is x itself; eta, done, iterations restart
-        a.eta[b] = a.eta0;
-        a.done[b] = 0;
-        a.iters[b] = 0;
-        a.fX[b] = s_f;
-        const int newly = (a.checked && s_u == 0 && !a.solved[b]) ? 1 : 0;
-        if (newly) a.solved[b] = 1;
-        s_acc = 1 | (newly << 1);   // "accept": Gx <- g below (X is unchanged)
-    } else if (threadIdx.x == 0) {
+    if (threadIdx.x == 0) {
         const double fp = s_f;
-        a.fP[b] = fp;
-        if (a.checked) a.unsatP[b] = s_u;
-        int acc = 0;
-        if (!a.done[b]) {
-            acc = fp <= a.fX[b] + a.c1 * a.dot[b];
-            double eta = a.eta[b];
-            eta = acc ? fmin(2.0 * eta, a.eta0) : 0.5 * eta;
-            a.eta[b] = eta;
-            const int it = a.iters[b] + 1;
-            a.iters[b] = it;
-            if (acc) a.fX[b] = fp;
-            if (eta < a.eta_min || it >= a.max_inner) a.done[b] = 1;
+        int acc = 0, done = st_done;
+        double eta = st_eta;
+        if (a.mode == 0) {   // round start: the evaluated point is x itself; eta, done, iterations restart
+            eta = a.eta0;
+            done = 0;
+            a.iters[b] = 0;
+            a.fX[b] = fp;
+            acc = 1;         // "accept": Gx <- g below (X is unchanged)
+        } else {
+            a.fP[b] = fp;
+            if (a.checked) a.unsatP[b] = s_u;
+            if (!done) {
+                acc = fp <= st_fX + a.c1 * st_dot;
+                eta = acc ? fmin(2.0 * eta, a.eta0) : 0.5 * eta;
+                const int it = st_iters + 1;
+                a.iters[b] = it;
+                if (acc) a.fX[b] = fp;
+                if (eta < a.eta_min || it >= a.max_inner) done = 1;
+            }
         }
-        const int newly = (a.checked && s_u == 0 && !a.solved[b]) ? 1 : 0;
+        a.eta[b] = eta;
+        a.done[b] = done;
+        const int newly = (a.checked && s_u == 0 && !st_solved) ? 1 : 0;
         if (newly) a.solved[b] = 1;
         s_acc = acc | (newly << 1);
+        s_eta = eta;
+        s_done = done;
     }
     __syncthreads();
     const int flags = s_acc;
-    T xv = (T)0, gv = (T)0;
-    if (v < n) {
-        const T xp = a.mode == 0 ? X[v] : Xp[v];   // the evaluated point
-        if (flags & 2) sol[v] = xp < (T)0 ? (int8_t)-1 : (int8_t)1;
-        if (flags & 1) {
-            if (a.mode != 0) X[v] = xp;
-            Gx[v] = g;
-            xv = xp;
-            gv = g;
-        } else {
-            xv = X[v];
-            gv = Gx[v];
-        }
-    }
-    // next trial point
-    const bool act = !a.done[b];
-    const T eta = (T)a.eta[b];
     double d = 0.0;
     if (v < n) {
-        const T xn = act ? clamp1(xv - eta * gv) : xv;
+        const T xe = a.mode == 0 ? x0 : xp0;   // the evaluated point
+        if (flags & 2) sol[v] = xe < (T)0 ? (int8_t)-1 : (int8_t)1;
+        T xv = x0, gv = g0;
+        if (flags & 1) {
+            if (a.mode != 0) X[v] = xe;
+            Gx[v] = g;
+            xv = xe;
+            gv = g;
+        }
+        // next trial point
+        const T xn = s_done ? xv : clamp1(xv - (T)s_eta * gv);
         Xp[v] = xn;
         d = (double)gv * (double)(xn - xv);
     }
-    red[threadIdx.x] = d;
+    // <g, x' - x>: warp sums, then the 8 warp sums in order (a fixed order)
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) d += __shfl_xor_sync(0xffffffffu, d, o);
+    if ((threadIdx.x & 31) == 0) s_red[threadIdx.x >> 5] = d;
     __syncthreads();
-    for (int s = 128; s > 0; s >>= 1) {
-        if (threadIdx.x < s) red[threadIdx.x] += red[threadIdx.x + s];
-        __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += s_red[w];
+        a.dot[b] = t;
     }
-    if (threadIdx.x == 0) a.dot[b] = red[0];
 }
 
 // ---- bit-packed exact check (A9; Thm. 4, Alg. 1 line 5 P:225): the signs of 32 points of one variable

@@ -18,7 +18,7 @@ names = {}
 for r in rows[1:]:
     if len(r) <= vi:
         continue
-    names[r[idi]] = r[ki].split("(")[0].replace("void ", "").replace("ffsat::dev::", "")
+    names[r[idi]] = r[ki].split("(")[0].replace("void ", "").replace("ffsat::dev::", "").replace("ffsat::", "")
     t[r[idi]][r[mi]] = float(r[vi].replace(",", "")) * SCALE.get(r[ui], 1.0)
 agg = collections.defaultdict(lambda: [0, 0.0, 0.0])
 for i, m in t.items():
