@@ -392,10 +392,17 @@ void check_kernels(ffsat_search* s, cudaStream_t st) {
     a.S = S; a.B = s->B; a.n = L.n; a.m = L.m; a.off = c->chk_off.as<int64_t>();
     a.words = c->chk_words.as<uint32_t>(); a.rule = c->chk_rule.as<int32_t>();
     a.U = s->U.as<int32_t>(); a.unsat = s->unsat.as<int32_t>();
-    if (L.max_k <= 64) {   // short rows: thread per constraint over 8 point tiles
-        constexpr int TPC = 8;
-        dim3 grid(blocks_for(L.m, 256), (unsigned)((PT + TPC - 1) / TPC));
-        dev::check_rows_kernel<TPC><<<grid, 256, 0, st>>>(a);
+    if (L.max_k <= 64) {   // short rows: thread per constraint over TPC point tiles (the largest TPC with >= 2 waves)
+        const int64_t cx = blocks_for(L.m, 256);
+        int tpc = 8;
+        while (tpc > 1 && cx * ((PT + tpc - 1) / tpc) < 2 * c->num_sm) tpc >>= 1;
+        dim3 grid((unsigned)cx, (unsigned)((PT + tpc - 1) / tpc));
+        switch (tpc) {
+        case 8: dev::check_rows_kernel<8><<<grid, 256, 0, st>>>(a); break;
+        case 4: dev::check_rows_kernel<4><<<grid, 256, 0, st>>>(a); break;
+        case 2: dev::check_rows_kernel<2><<<grid, 256, 0, st>>>(a); break;
+        default: dev::check_rows_kernel<1><<<grid, 256, 0, st>>>(a); break;
+        }
         s->ctx->launches += 2;
         CK(cudaGetLastError());
         return;

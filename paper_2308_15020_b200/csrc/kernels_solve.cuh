@@ -75,12 +75,15 @@ struct PgdArgs {
     int32_t checked;   // 1: unsatP holds the fused check of the evaluated point (check iterations only)
 };
 
-// one CTA (256 threads) per point
+// one CTA (256 threads) per point.  The point's search state is loaded first (one latency), the decision is thread 0's,
+// then one pass over the point's row: accept (x <- x', g <- g') and the next trial x'' = clip(x - eta g) with
+// <g, x'' - x> (warp sums, then the warp sums in order: a fixed order).
 template <typename T>
 __global__ void __launch_bounds__(256) pgd_step_kernel(PgdArgs a) {
     pdl_wait();   // launched programmatically after the gradient reduction
-    __shared__ double red[256];
-    __shared__ int s_acc;
+    __shared__ double s_red[8];
+    __shared__ int s_acc, s_done;
+    __shared__ double s_eta;
     const int64_t b = blockIdx.x;
     const int n = a.n;
     T* X = reinterpret_cast<T*>(a.X) + b * n;
@@ -88,66 +91,63 @@ __global__ void __launch_bounds__(256) pgd_step_kernel(PgdArgs a) {
     T* Gx = reinterpret_cast<T*>(a.Gx) + b * n;
     const T* Gp = reinterpret_cast<const T*>(a.Gp) + b * n;
     int8_t* sol = a.sol + b * n;
-    if (a.mode == 0) {
-        // round start: the evaluated point is x itself; eta, done, iteration count restart
-        if (threadIdx.x == 0) {
-            a.eta[b] = a.eta0;
-            a.done[b] = 0;
+    if (threadIdx.x == 0) {
+        const double fX = a.fX[b], fP = a.fP[b], dot = a.dot[b];
+        double eta = a.eta[b];
+        int done = a.done[b], iters = a.iters[b];
+        const int unsatP = a.unsatP[b], solved = a.solved[b];
+        int acc = 0;
+        if (a.mode == 0) {   // round start: the evaluated point is x itself; eta, done, iteration count restart
+            eta = a.eta0;
+            done = 0;
             a.iters[b] = 0;
-            int newly = (a.checked && a.unsatP[b] == 0 && !a.solved[b]) ? 1 : 0;
-            if (newly) a.solved[b] = 1;
-            s_acc = newly << 1;
+        } else if (!done) {
+            acc = fP <= fX + a.c1 * dot;
+            eta = acc ? fmin(2.0 * eta, a.eta0) : 0.5 * eta;
+            const int it = iters + 1;
+            a.iters[b] = it;
+            if (acc) a.fX[b] = fP;
+            if (eta < a.eta_min || it >= a.max_inner) done = 1;
         }
-        __syncthreads();
-        if (s_acc & 2)
-            for (int v = threadIdx.x; v < n; v += blockDim.x) sol[v] = X[v] < (T)0 ? (int8_t)-1 : (int8_t)1;
+        a.eta[b] = eta;
+        a.done[b] = done;
+        // any checked trial whose rounded assignment satisfies every constraint is a solution (Thm. 4)
+        const int newly = (a.checked && unsatP == 0 && !solved) ? 1 : 0;
+        if (newly) a.solved[b] = 1;
+        s_acc = acc | (newly << 1);
+        s_eta = eta;
+        s_done = done;
     }
-    if (a.mode == 1) {
-        if (threadIdx.x == 0) {
-            int acc = 0;
-            if (!a.done[b]) {
-                acc = a.fP[b] <= a.fX[b] + a.c1 * a.dot[b];
-                double eta = a.eta[b];
-                eta = acc ? fmin(2.0 * eta, a.eta0) : 0.5 * eta;
-                a.eta[b] = eta;
-                int it = a.iters[b] + 1;
-                a.iters[b] = it;
-                if (acc) a.fX[b] = a.fP[b];
-                if (eta < a.eta_min || it >= a.max_inner) a.done[b] = 1;
-            }
-            // any checked trial whose rounded assignment satisfies every constraint is a solution (Thm. 4)
-            int newly = (a.checked && a.unsatP[b] == 0 && !a.solved[b]) ? 1 : 0;
-            if (newly) a.solved[b] = 1;
-            s_acc = acc | (newly << 1);
-        }
-        __syncthreads();
-        const int flags = s_acc;
-        if (flags & 2)
-            for (int v = threadIdx.x; v < n; v += blockDim.x) sol[v] = Xp[v] < (T)0 ? (int8_t)-1 : (int8_t)1;
-        if (flags & 1)
-            for (int v = threadIdx.x; v < n; v += blockDim.x) {
-                X[v] = Xp[v];
-                Gx[v] = Gp[v];
-            }
-    }
-    // next trial point
-    const bool act = !a.done[b];
-    const T eta = (T)a.eta[b];
+    __syncthreads();
+    const int flags = s_acc;
+    const bool act = !s_done;
+    const T eta = (T)s_eta;
     double d = 0.0;
     for (int v = threadIdx.x; v < n; v += blockDim.x) {
-        T xv = X[v];
-        T g = Gx[v];
-        T xn = act ? clamp1(xv - eta * g) : xv;
+        T xv, g;
+        if (a.mode == 1 && (flags & 1)) {
+            xv = Xp[v];
+            g = Gp[v];
+            X[v] = xv;
+            Gx[v] = g;
+        } else {
+            xv = X[v];
+            g = Gx[v];
+        }
+        if (flags & 2) sol[v] = (a.mode == 0 ? xv : Xp[v]) < (T)0 ? (int8_t)-1 : (int8_t)1;
+        const T xn = act ? clamp1(xv - eta * g) : xv;
         Xp[v] = xn;
         d += (double)g * (double)(xn - xv);
     }
-    red[threadIdx.x] = d;
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) d += __shfl_xor_sync(0xffffffffu, d, o);
+    if ((threadIdx.x & 31) == 0) s_red[threadIdx.x >> 5] = d;
     __syncthreads();
-    for (int s = 128; s > 0; s >>= 1) {
-        if (threadIdx.x < s) red[threadIdx.x] += red[threadIdx.x + s];
-        __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += s_red[w];
+        a.dot[b] = t;
     }
-    if (threadIdx.x == 0) a.dot[b] = red[0];
 }
 
 // The PGD step fused with the reduction of point-major partials (tiled TMEM path, n <= 256 <= blockDim): per point
@@ -334,18 +334,28 @@ __device__ __forceinline__ uint32_t sat_mask(const CheckBitsArgs& a, const uint3
         if (COOP) x = __reduce_xor_sync(0xffffffffu, x);
         return par == 1 ? x : ~x;
     }
-    // counting rules: bit-sliced planes (LSB first), k <= 4096 -> 13 planes
+    // counting rules: bit-sliced planes (LSB first), k <= 4096 -> 13 planes.  The literal masks are loaded 8 at a time
+    // (all in flight) before they are added: the ripple-carry adds would otherwise serialise one load latency per literal
     uint32_t p[13];
 #pragma unroll
     for (int j = 0; j < 13; ++j) p[j] = 0u;
-    for (int64_t i = lo + first; i < hi; i += stride) {
-        uint32_t carry = lit(i);
+    for (int64_t i0 = lo + first; i0 < hi; i0 += 8 * (int64_t)stride) {
+        uint32_t mk[8];
 #pragma unroll
-        for (int j = 0; j < 13; ++j) {   // ripple-carry add of one bit per point
-            if (carry == 0u) break;
-            const uint32_t t = p[j] & carry;
-            p[j] ^= carry;
-            carry = t;
+        for (int q = 0; q < 8; ++q) {
+            const int64_t i = i0 + q * (int64_t)stride;
+            mk[q] = i < hi ? lit(i) : 0u;
+        }
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            uint32_t carry = mk[q];
+#pragma unroll
+            for (int j = 0; j < 13; ++j) {   // ripple-carry add of one bit per point
+                if (carry == 0u) break;
+                const uint32_t t = p[j] & carry;
+                p[j] ^= carry;
+                carry = t;
+            }
         }
     }
     if (COOP) {   // butterfly sum of the 32 lanes' bit-sliced counts
