@@ -80,6 +80,91 @@ def pgd_iteration(F: OracleFormula, st: State, P: Params):
     return xp, fp, gp, acc
 
 
+# ---- accelerated projected gradient (FISTA, Beck & Teboulle 2009) with backtracking: the paper's solver runs
+#      jaxopt's projected gradient with FISTA acceleration and a line search; reading #16b.
+#      Per point, one evaluation per iteration, a two-phase machine:
+#        phase 1 (a trial x+ = clip(y - eta g_y) was evaluated): accept iff f(x+) <= f(y) + <g_y, x+ - y>
+#                 + |x+ - y|^2 / (2 eta) (the quadratic upper bound); accept: x_prev, x <- x, x+; t <- (1 +
+#                 sqrt(1 + 4 t^2)) / 2, beta = (t_old - 1) / t; eta <- min(2 eta, eta0); if beta = 0 the new y is
+#                 x+ itself (its f, g are at hand) and the next trial is proposed, else the next evaluation is
+#                 y = x + beta (x - x_prev) (phase 0); reject: eta <- eta / 2, next trial from the same y.
+#        phase 0 (y was evaluated): f_y, g_y <- f(y), grad f(y); the next trial is proposed (phase 1).
+#      Every evaluation counts as an iteration; done at eta < eta_min or max_inner iterations.
+
+
+@dataclass
+class FistaState:
+    x: np.ndarray            # [B][n] accepted x_k
+    f: np.ndarray            # f(x_k)
+    g: np.ndarray            # grad f(x_k)
+    xm: np.ndarray           # x_{k-1}
+    y: np.ndarray            # current extrapolation point
+    fy: np.ndarray
+    gy: np.ndarray
+    xp: np.ndarray           # the next point to evaluate
+    t: np.ndarray
+    eta: np.ndarray
+    phase: np.ndarray        # 1: xp is a trial from y; 0: xp is the next y
+    done: np.ndarray
+    iters: np.ndarray
+    w: np.ndarray
+
+
+def fista_propose(st: FistaState, b: int):
+    st.xp[b] = np.clip(st.y[b] - st.eta[b] * st.gy[b], -1.0, 1.0)
+    st.phase[b] = 1
+
+
+def fista_start_round(F: OracleFormula, x: np.ndarray, w: np.ndarray, P: Params) -> FistaState:
+    f, g = cdp.evaluate_weighted(F, w, x)
+    B = len(f)
+    st = FistaState(x=x.copy(), f=f, g=g, xm=x.copy(), y=x.copy(), fy=f.copy(), gy=g.copy(), xp=x.copy(),
+                    t=np.ones(B), eta=np.full(B, P.eta0), phase=np.ones(B, np.int64), done=np.zeros(B, bool),
+                    iters=np.zeros(B, np.int64), w=w)
+    for b in range(B):
+        fista_propose(st, b)
+    return st
+
+
+def fista_iteration(F: OracleFormula, st: FistaState, P: Params):
+    """One evaluation for every point, then each point's phase step (see above).  Returns per-point actions:
+    'y' (phase 0 consumed), 'accept', 'reject', or None (done)."""
+    fp, gp = cdp.evaluate_weighted(F, st.w, st.xp)
+    acts = []
+    for b in range(len(fp)):
+        if st.done[b]:
+            acts.append(None)
+            continue
+        if st.phase[b] == 0:
+            st.y[b], st.fy[b], st.gy[b] = st.xp[b], fp[b], gp[b]
+            fista_propose(st, b)
+            acts.append("y")
+        else:
+            dx = st.xp[b] - st.y[b]
+            q = st.fy[b] + np.dot(st.gy[b], dx) + np.dot(dx, dx) / (2.0 * st.eta[b])
+            if fp[b] <= q:
+                st.xm[b], st.x[b], st.f[b], st.g[b] = st.x[b].copy(), st.xp[b].copy(), fp[b], gp[b]
+                t_new = (1.0 + np.sqrt(1.0 + 4.0 * st.t[b] ** 2)) / 2.0
+                beta = (st.t[b] - 1.0) / t_new
+                st.t[b] = t_new
+                st.eta[b] = min(2.0 * st.eta[b], P.eta0)
+                if beta == 0.0:
+                    st.y[b], st.fy[b], st.gy[b] = st.x[b].copy(), fp[b], gp[b]
+                    fista_propose(st, b)
+                else:
+                    st.xp[b] = st.x[b] + beta * (st.x[b] - st.xm[b])
+                    st.phase[b] = 0
+                acts.append("accept")
+            else:
+                st.eta[b] = 0.5 * st.eta[b]
+                fista_propose(st, b)
+                acts.append("reject")
+        st.iters[b] += 1
+        if st.eta[b] < P.eta_min or st.iters[b] >= P.max_inner:
+            st.done[b] = True
+    return acts
+
+
 def erwa_update(w: np.ndarray, U: np.ndarray, alpha: float) -> np.ndarray:
     """Prop. 3: w <- (1-alpha) w + alpha r, r_c = U_c / max U; skipped when max U = 0."""
     mx = int(U.max()) if len(U) else 0

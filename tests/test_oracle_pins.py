@@ -477,3 +477,42 @@ def test_rephase_phases_hand_derived():
     assert np.array_equal(y[0], uniform_pm1(seed, 0, 1, n)) and np.array_equal(y[1], -x[1])
     y = osolve.rephase(x, seed, 0, 3, osolve.Params(policy="R"))
     assert all(np.array_equal(y[i], uniform_pm1(seed, i, 3, n)) for i in range(6))
+
+
+def test_fista_schedule_hand_derived():
+    """The FISTA reading (#16b; P:939 names jaxopt's accelerated projected gradient) worked by hand on
+    f = x1 x2 + x1/4 + x2/4 from x = (0, 0), eta0 = 4, with dyadic values (exact in fp64):
+      y = (0, 0), f_y = 0, g_y = (1/4, 1/4)
+      1. x+ = (-1, -1): f+ = 1/2 > f_y + <g_y, x+ - y> + |x+ - y|^2 / 8 = -1/2 + 1/4 = -1/4        reject, eta -> 2
+      2. x+ = (-1/2, -1/2): f+ = 0 > -1/4 + 1/8 = -1/8                                              reject, eta -> 1
+      3. x+ = (-1/4, -1/4): f+ = -1/16 <= -1/8 + 1/16 = -1/16 (equality)                             accept, t: 1 -> (1 + 5^.5) / 2,
+         beta = 0, so y = x+ (its f and gradient (0, 0) are at hand), eta -> 2, next trial x+ = y
+      4. x+ = y: f+ = f_y <= f_y                                                                     accept, beta = (t - 1) / t' != 0:
+         the next evaluation is y' = x + beta (x - x_prev) = x (x_prev = x): phase 0
+      5. the y evaluation: f_y = -1/16, g_y = 0; the next trial is x+ = y."""
+    F = _saddle_formula()
+    P = osolve.Params(eta0=4.0, max_inner=50, adaptive_weights=False)
+    st = osolve.fista_start_round(F, np.zeros((1, 2)), F.weight.copy(), P)
+    assert np.array_equal(st.xp[0], [-1.0, -1.0]) and st.phase[0] == 1
+    want = [("reject", 2.0, (-0.5, -0.5)), ("reject", 1.0, (-0.25, -0.25)), ("accept", 2.0, (-0.25, -0.25)),
+            ("accept", 4.0, (-0.25, -0.25)), ("y", 4.0, (-0.25, -0.25))]
+    for k, (act_w, eta_w, xp_w) in enumerate(want):
+        acts = osolve.fista_iteration(F, st, P)
+        assert acts[0] == act_w and st.eta[0] == eta_w and np.array_equal(st.xp[0], xp_w), k
+    assert np.array_equal(st.x[0], [-0.25, -0.25]) and st.f[0] == -0.0625
+    assert abs(st.t[0] - (1 + np.sqrt(1 + 4 * ((1 + 5 ** 0.5) / 2) ** 2)) / 2) < 1e-15
+    assert st.iters[0] == 5 and st.phase[0] == 1
+
+
+def test_fista_descends_and_stays_feasible():
+    """On a random 3-SAT instance every accepted x stays in the box (trials are projected; only the extrapolation
+    points y may leave it) and after 60 evaluations the accepted f is below the start for every point."""
+    inst = synth.config1(3)
+    Fo = OracleFormula.from_arrays(*inst.arrays())
+    P = osolve.Params(eta0=8.0, max_inner=60)
+    st = osolve.fista_start_round(Fo, osolve.initial_points(5, range(8), Fo.n), np.ones(Fo.m), P)
+    f0 = st.f.copy()
+    for _ in range(60):
+        osolve.fista_iteration(Fo, st, P)
+        assert np.all(np.abs(st.x) <= 1)
+    assert np.all(st.f <= f0 + 1e-12) and np.mean(st.f) < np.mean(f0)
