@@ -158,6 +158,12 @@ typedef struct {
     int32_t policy;          /* rephasing cycle: 0 = ROF, 1 = RF, 2 = R */
     int32_t adaptive_weights;/* 1 = ERWA (decision mode), 0 = fixed weights */
     double timeout_s;        /* ffsat_solve wall-clock limit, <= 0 = none */
+    int32_t accel;           /* 0 = monotone projected Armijo backtracking, one trial per iteration (#16);
+                                1 = FISTA: accelerated projected gradient with backtracking on the quadratic upper
+                                bound ("FISTA", #16b), one evaluation (trial or extrapolation point)
+                                per iteration.  In this mode ffsat_search_buffers.grad holds the gradient at the
+                                extrapolation point y, f and x the last accepted iterate (default 0) */
+    int32_t reserved;        /* must be 0 */
 } ffsat_solve_params;
 
 typedef struct {
@@ -185,6 +191,13 @@ typedef struct {
                                 keys[0] = lowest GLOBAL point index whose solved flag is set, INT64_MAX if none;
                                 keys[1] = (falsified count of sgn(x) at the last check << 32) | global point, minimised */
     int32_t* solved;         /* [B] 1 once a trial point or a checked point's sgn(x) satisfied every constraint */
+    void* xp;                /* [B][n] the next point to evaluate (the trial; in FISTA mode possibly the point y) */
+    /* FISTA state (params.accel = 1; NULL otherwise): */
+    void* x_prev;            /* [B][n] x_{k-1} */
+    void* y;                 /* [B][n] the extrapolation point whose gradient is in grad */
+    double* f_y;             /* [B] f(y) */
+    double* t;               /* [B] momentum t_k */
+    int32_t* phase;          /* [B] 1: xp is a trial from y; 0: xp is the next y */
 } ffsat_search_buffers;
 
 ffsat_status ffsat_search_create(ffsat_ctx* ctx, int64_t batch, int64_t point0, uint64_t seed,

@@ -37,6 +37,7 @@ struct ffsat_search {
     DBuf X, Xp, Gx, Gp, fX, fP, dot, eta, done, iters, unsatP, solved, sol, unsat, U, stats, xT;
     DBuf W;                       // this search's current weights (position order, context dtype): ERWA state
     DBuf umax;                    // max U_c of the ERWA update
+    DBuf Xm, Y, fy, tmom, phase;  // FISTA state (P.accel = 1): x_{k-1}, y, f(y), momentum t, phase
     Scratch sc;                   // this search's evaluation scratch (referenced by its captured graph)
     int64_t round = 0, iters_issued = 0;
     // one CLS iteration captured as a CUDA graph (replayed by ffsat_search_iterate), in two variants: [1] with the
@@ -247,6 +248,11 @@ void search_alloc(ffsat_search* s) {
     s->W.ensure(std::max<size_t>(16, (size_t)m * es));
     s->umax.ensure(16);
     s->stats.ensure(64);
+    if (s->P.accel) {
+        for (DBuf* d : {&s->Xm, &s->Y}) d->ensure(std::max<size_t>(16, Bn * es));
+        for (DBuf* d : {&s->fy, &s->tmom}) d->ensure((size_t)B * 8);
+        s->phase.ensure((size_t)B * 4);
+    }
     ensure_scratch(s->ctx, s->sc, B);
     CK(cudaMemset(s->solved.p, 0, (size_t)B * 4));
     CK(cudaMemset(s->unsat.p, 0, (size_t)B * 4));
@@ -264,9 +270,44 @@ dev::PgdArgs pgd_args(ffsat_search* s, int mode, bool checked) {
     return a;
 }
 
+dev::FistaArgs fista_args(ffsat_search* s, int mode, bool checked) {
+    dev::FistaArgs f{};
+    f.p = pgd_args(s, mode, checked);
+    f.Xm = s->Xm.p; f.Y = s->Y.p; f.fy = s->fy.as<double>(); f.t = s->tmom.as<double>(); f.phase = s->phase.as<int32_t>();
+    return f;
+}
+
+// FISTA mode (P.accel = 1): evaluate the point (X at a round start, else Xp) and take the FISTA step; the TMEM path
+// fuses the reduction of its point-major partials into the step as pgd_fused_kernel does.
+void fista_round_step(ffsat_search* s, int mode, bool checked, cudaStream_t st) {
+    ffsat_ctx* c = s->ctx;
+    const bool f64 = c->Lo.precision == 64;
+    const dev::FistaArgs a = fista_args(s, mode, checked);
+    const void* xe = mode == 0 ? s->X.p : s->Xp.p;
+    int32_t* u = checked ? s->unsatP.as<int32_t>() : nullptr;
+    const unsigned B = (unsigned)s->B;
+    if (!f64 && c->Lo.tmem) {
+        eval_device_t<float>(c, s->sc, (const float*)xe, s->B, nullptr, nullptr, u, s->W.as<float>(), st, false, true);
+        const dev::PmReduce<float> r = pm_reduce_args<float>(c, s->sc, s->B, checked);
+        launch_pdl(dev::fista_step_kernel<float, true>, dim3(B), dim3(256), 0, st, a, r);
+    } else if (f64) {
+        search_eval<double>(s, xe, s->fP.as<double>(), s->Gp.p, u, st);
+        dev::fista_step_kernel<double, false><<<B, 256, 0, st>>>(a, dev::PmReduce<double>{});
+    } else {
+        search_eval<float>(s, xe, s->fP.as<double>(), s->Gp.p, u, st);
+        launch_pdl(dev::fista_step_kernel<float, false>, dim3(B), dim3(256), 0, st, a, dev::PmReduce<float>{});
+    }
+    CK(cudaGetLastError());
+}
+
 void search_begin_round(ffsat_search* s, cudaStream_t st) {
     const bool f64 = s->ctx->Lo.precision == 64;
     s->ctx->launches += 1;   // eta / done / iterations are reset by the round-start PGD step itself
+    if (s->P.accel) {
+        fista_round_step(s, 0, false, st);
+        s->iters_issued = 0;
+        return;
+    }
     // the round's start point x (rephased): f and gradient, no check (the round-end check catches solutions)
     dev::PgdArgs a = pgd_args(s, 0, false);
     if (!f64 && s->ctx->Lo.tmem) {
@@ -345,6 +386,11 @@ void search_iterate(ffsat_search* s, int n_iters, cudaStream_t st) {
 // then the Armijo accept / eta update / next trial point.
 void search_iterate_one(ffsat_search* s, bool checked, cudaStream_t st) {
     const bool f64 = s->ctx->Lo.precision == 64;
+    if (s->P.accel) {
+        s->ctx->launches += 1;
+        fista_round_step(s, 1, checked, st);
+        return;
+    }
     dev::PgdArgs a = pgd_args(s, 1, checked);
     int32_t* u = checked ? s->unsatP.as<int32_t>() : nullptr;
     s->ctx->launches += 1;
@@ -496,7 +542,7 @@ void search_assignment(ffsat_search* s, int64_t lp, int8_t* out) {
 
 void check_params(const ffsat_solve_params& p) {
     if (!(p.eta0 > 0) || !(p.eta_min >= 0) || !(p.armijo_c1 >= 0 && p.armijo_c1 < 1) || !(p.alpha >= 0 && p.alpha <= 1) ||
-        p.max_inner < 1 || p.check_every < 1 || p.policy < 0 || p.policy > 2)
+        p.max_inner < 1 || p.check_every < 1 || p.policy < 0 || p.policy > 2 || p.accel < 0 || p.accel > 1 || p.reserved != 0)
         throw Error(FFSAT_ERR_ARG, "invalid solve parameters");
 }
 
@@ -517,6 +563,8 @@ void ffsat_default_params(ffsat_solve_params* p) {
     p->policy = 0;
     p->adaptive_weights = 1;
     p->timeout_s = 0;
+    p->accel = 0;
+    p->reserved = 0;
 }
 
 const char* ffsat_version(void) { return "ffsat-b200 1 (sm_100a)"; }
@@ -824,6 +872,9 @@ ffsat_status ffsat_search_get_buffers(ffsat_search* s, ffsat_search_buffers* o) 
     o->x = s->X.p; o->grad = s->Gx.p; o->f = s->fX.as<double>(); o->eta = s->eta.as<double>();
     o->unsat = s->unsat.as<int32_t>(); o->U = s->U.as<int32_t>(); o->weights = s->W.p;
     o->keys = s->stats.as<int64_t>() + 1; o->solved = s->solved.as<int32_t>();
+    o->xp = s->Xp.p;
+    o->x_prev = s->Xm.p; o->y = s->Y.p; o->f_y = s->fy.as<double>(); o->t = s->tmom.as<double>();
+    o->phase = s->phase.as<int32_t>();
     return FFSAT_OK;
     ABI_CATCH(c)
 }

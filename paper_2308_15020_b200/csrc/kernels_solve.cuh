@@ -253,6 +253,174 @@ __global__ void __launch_bounds__(256) pgd_fused_kernel(PgdArgs a, PmReduce<T> r
     }
 }
 
+// ---- accelerated projected gradient (FISTA with backtracking; "FISTA ... line search", reading #16b).
+//      Per point a two-phase machine with ONE evaluation per iteration (the evaluated point is Xp, or X at a round
+//      start):
+//        phase 1 (Xp = clip(y - eta g_y) is a trial): accept iff f(Xp) <= f_y + <g_y, Xp - y> + |Xp - y|^2 / (2 eta)
+//                (the quadratic upper bound; its right-hand side minus f_y is stored in dot[] when the trial is
+//                proposed).  accept: x_prev, x <- x, Xp; t <- (1 + sqrt(1 + 4 t^2)) / 2; beta = (t_old - 1) / t;
+//                eta <- min(2 eta, eta0); beta = 0: y <- Xp (f and gradient at hand), next trial; else the next
+//                evaluation is y = x + beta (x - x_prev), not projected (phase 0).  reject: eta <- eta / 2, next
+//                trial from the same y.
+//        phase 0 (y evaluated): f_y, g_y <- f(y), grad f(y); next trial (phase 1).
+//      Every evaluation counts toward max_inner; done at eta < eta_min or max_inner.  Buffers: X = x_k,
+//      Xm = x_{k-1}, Y = y, Gx = g_y (the gradient at y in this mode), fX = f(x_k), fy = f(y).
+struct FistaArgs {
+    PgdArgs p;         // mode 0: round start (the evaluated point is X); p.dot holds <g_y, dx> + |dx|^2 / (2 eta)
+    void* Xm;          // [B][n] x_{k-1}
+    void* Y;           // [B][n] y
+    double* fy;        // [B] f(y)
+    double* t;         // [B] momentum t_k
+    int32_t* phase;    // [B] 1: Xp is a trial from y; 0: Xp is the next y
+};
+
+// actions (thread 0's decision, then one pass over the point's row)
+enum : int { FA_NONE = 0, FA_SETY = 1, FA_EXTRAP = 2, FA_REJECT = 3 };
+
+// One CTA (256 threads) per point.  FUSED: the gradient / f / unsat of the evaluated point come from the TMEM path's
+// point-major partials (n <= 256 = blockDim, one variable per thread); otherwise from Gp / fP / unsatP.
+template <typename T, bool FUSED>
+__global__ void __launch_bounds__(256) fista_step_kernel(FistaArgs fa, PmReduce<T> r) {
+    pdl_wait();
+    const PgdArgs& a = fa.p;
+    __shared__ double s_gd[8], s_dd[8];
+    __shared__ int s_act, s_flags;
+    __shared__ double s_eta, s_beta, s_f;
+    __shared__ int s_u;
+    const int64_t b = blockIdx.x;
+    const int n = a.n;
+    T* X = reinterpret_cast<T*>(a.X) + b * n;
+    T* Xp = reinterpret_cast<T*>(a.Xp) + b * n;
+    T* Gy = reinterpret_cast<T*>(a.Gx) + b * n;
+    const T* Gp = reinterpret_cast<const T*>(a.Gp) + b * n;
+    T* Xm = reinterpret_cast<T*>(fa.Xm) + b * n;
+    T* Y = reinterpret_cast<T*>(fa.Y) + b * n;
+    int8_t* sol = a.sol + b * n;
+    T gf = (T)0;
+    if (FUSED) {
+        if ((int)threadIdx.x < n) gf = (T)pm_grad(r, b, threadIdx.x);
+        if (threadIdx.x < 32) {
+            int u = 0;
+            const double fb = pm_f_warp(r, b, &u);
+            if (threadIdx.x == 0) {
+                s_f = fb;
+                s_u = u;
+            }
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        const double fe = FUSED ? s_f : a.fP[b];
+        const int ue = FUSED ? s_u : a.unsatP[b];
+        double eta = a.eta[b], t = fa.t[b], beta = 0.0;
+        int done = a.done[b], act = FA_NONE, acc = 0;
+        if (FUSED) {
+            a.fP[b] = fe;
+            if (a.checked) a.unsatP[b] = ue;
+        }
+        if (a.mode == 0) {   // round start: the evaluated point is x itself
+            eta = a.eta0;
+            t = 1.0;
+            done = 0;
+            a.iters[b] = 0;
+            a.fX[b] = fe;
+            fa.fy[b] = fe;
+            fa.phase[b] = 1;
+            act = FA_SETY;
+        } else if (!done) {
+            if (fa.phase[b] == 0) {
+                fa.fy[b] = fe;
+                fa.phase[b] = 1;
+                act = FA_SETY;
+            } else if (fe <= fa.fy[b] + a.dot[b]) {
+                acc = 1;
+                a.fX[b] = fe;
+                const double tn = (1.0 + sqrt(1.0 + 4.0 * t * t)) / 2.0;
+                beta = (t - 1.0) / tn;
+                t = tn;
+                eta = fmin(2.0 * eta, a.eta0);
+                if (beta == 0.0) {
+                    fa.fy[b] = fe;
+                    act = FA_SETY;
+                } else {
+                    fa.phase[b] = 0;
+                    act = FA_EXTRAP;
+                }
+            } else {
+                eta = 0.5 * eta;
+                fa.phase[b] = 1;
+                act = FA_REJECT;
+            }
+            const int it = a.iters[b] + 1;
+            a.iters[b] = it;
+            if (eta < a.eta_min || it >= a.max_inner) done = 1;
+        }
+        a.eta[b] = eta;
+        a.done[b] = done;
+        fa.t[b] = t;
+        const int newly = (a.checked && ue == 0 && !a.solved[b]) ? 1 : 0;
+        if (newly) a.solved[b] = 1;
+        s_act = act;
+        s_flags = acc | (newly << 1);
+        s_eta = eta;
+        s_beta = beta;
+    }
+    __syncthreads();
+    const int act = s_act, flags = s_flags;
+    const T eta = (T)s_eta, beta = (T)s_beta;
+    double gd = 0.0, dd = 0.0;
+    for (int v = threadIdx.x; v < n; v += blockDim.x) {
+        const T xe = a.mode == 0 ? X[v] : Xp[v];   // the evaluated point
+        if (flags & 2) sol[v] = xe < (T)0 ? (int8_t)-1 : (int8_t)1;
+        if (act == FA_NONE) continue;
+        if (act == FA_EXTRAP) {
+            const T xo = X[v];
+            Xm[v] = xo;
+            X[v] = xe;
+            Xp[v] = xe + beta * (xe - xo);
+            continue;
+        }
+        T y, gy;
+        if (act == FA_SETY) {
+            y = xe;
+            gy = FUSED ? gf : Gp[v];
+            Y[v] = y;
+            Gy[v] = gy;
+            if (a.mode == 0) Xm[v] = xe;
+            else if (flags & 1) {   // accept with beta = 0
+                Xm[v] = X[v];
+                X[v] = xe;
+            }
+        } else {   // FA_REJECT: the next trial from the same y
+            y = Y[v];
+            gy = Gy[v];
+        }
+        const T xn = clamp1(y - eta * gy);
+        Xp[v] = xn;
+        const T dx = xn - y;
+        gd += (double)gy * (double)dx;
+        dd += (double)dx * (double)dx;
+    }
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) {
+        gd += __shfl_xor_sync(0xffffffffu, gd, o);
+        dd += __shfl_xor_sync(0xffffffffu, dd, o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        s_gd[threadIdx.x >> 5] = gd;
+        s_dd[threadIdx.x >> 5] = dd;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0 && (act == FA_SETY || act == FA_REJECT)) {
+        double tg = 0.0, td = 0.0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
+            tg += s_gd[w];
+            td += s_dd[w];
+        }
+        a.dot[b] = tg + td / (2.0 * s_eta);
+    }
+}
+
 // ---- bit-packed exact check (A9; Thm. 4, Alg. 1 line 5 P:225): the signs of 32 points of one variable
 //      are one 32-bit word, so one thread checks one constraint for 32 points with one word op per literal.
 // S[pt][v] bit b = 1 iff x[32 pt + b][v] < 0 (the literal "v" is True); points past B have bit 0 and are masked.

@@ -52,7 +52,8 @@ class ffsat_info_t(C.Structure):
 class ffsat_solve_params(C.Structure):
     _fields_ = [("eta0", C.c_double), ("eta_min", C.c_double), ("armijo_c1", C.c_double), ("alpha", C.c_double),
                 ("max_inner", C.c_int32), ("check_every", C.c_int32), ("policy", C.c_int32),
-                ("adaptive_weights", C.c_int32), ("timeout_s", C.c_double)]
+                ("adaptive_weights", C.c_int32), ("timeout_s", C.c_double), ("accel", C.c_int32),
+                ("reserved", C.c_int32)]
 
 
 class ffsat_search_stats(C.Structure):
@@ -66,7 +67,8 @@ class ffsat_search_stats(C.Structure):
 class ffsat_search_buffers(C.Structure):
     _fields_ = [("x", C.c_void_p), ("grad", C.c_void_p), ("f", C.c_void_p), ("eta", C.c_void_p),
                 ("unsat", C.c_void_p), ("U", C.c_void_p), ("weights", C.c_void_p), ("keys", C.c_void_p),
-                ("solved", C.c_void_p)]
+                ("solved", C.c_void_p), ("xp", C.c_void_p), ("x_prev", C.c_void_p), ("y", C.c_void_p),
+                ("f_y", C.c_void_p), ("t", C.c_void_p), ("phase", C.c_void_p)]
 
 
 class ffsat_result(C.Structure):
@@ -414,7 +416,8 @@ class Search:
         return a
 
     def tensors(self):
-        """torch views of the device buffers (x, grad, f, eta, unsat, U, weights, keys, solved); U and weights are in
+        """torch views of the device buffers (x, grad, f, eta, unsat, U, weights, keys, solved, xp; in FISTA mode also
+        x_prev, y, f_y, t, phase -- grad is then the gradient at y); U and weights are in
         the library's position order (Context.order() maps position -> input constraint)."""
         import torch
         b = self.buffers()
@@ -424,11 +427,16 @@ class Search:
 
         def view(ptr, count, dtype):
             return _device_view(ptr, count, dtype, dev)
-        return {"x": view(b.x, B * n, tdt).view(B, n), "grad": view(b.grad, B * n, tdt).view(B, n),
+        out = {"x": view(b.x, B * n, tdt).view(B, n), "grad": view(b.grad, B * n, tdt).view(B, n),
                 "f": view(b.f, B, torch.float64), "eta": view(b.eta, B, torch.float64),
                 "unsat": view(b.unsat, B, torch.int32), "U": view(b.U, m, torch.int32),
                 "weights": view(b.weights, m, tdt), "keys": view(b.keys, 2, torch.int64),
-                "solved": view(b.solved, B, torch.int32)}
+                "solved": view(b.solved, B, torch.int32), "xp": view(b.xp, B * n, tdt).view(B, n)}
+        if b.y:   # FISTA state (accel = 1)
+            out.update({"x_prev": view(b.x_prev, B * n, tdt).view(B, n), "y": view(b.y, B * n, tdt).view(B, n),
+                        "f_y": view(b.f_y, B, torch.float64), "t": view(b.t, B, torch.float64),
+                        "phase": view(b.phase, B, torch.int32)})
+        return out
 
 
 def _device_view(ptr, count, dtype, device):

@@ -448,6 +448,138 @@ def test_pgd_eta_schedule_hand_derived_on_gpu(precision):
     assert s.stats()["active"] == 0
 
 
+@pytest.mark.parametrize("precision", [32, 64])
+def test_fista_schedule_hand_derived_on_gpu(precision):
+    """The hand-derived FISTA sequence of tests/test_oracle_pins.py::test_fista_schedule_hand_derived (reading #16b,
+    P:939) on the GPU, dyadic values (exact in fp32 and fp64): from x = (0, 0), eta0 = 4 the first trial is (-1, -1);
+    reject (eta 4 -> 2, trial (-1/2, -1/2)), reject (-> 1, trial (-1/4, -1/4)), accept with beta = 0 (-> 2, y = x+,
+    next trial = y), accept with beta != 0 (-> 4, the next evaluation is y = x + beta (x - x_prev) = x, phase 0), then
+    the y evaluation (phase 1 again)."""
+    cons = [(1, 0, 1.0, [1, 2]), (0, 0, 0.25, [1]), (0, 0, 0.25, [2])]
+    Fo = OracleFormula.from_constraints(2, cons)
+    ctx = P.Context.from_arrays(2, Fo.kind, Fo.bound, Fo.weight, Fo.offsets, Fo.lits, precision=precision, device=0)
+    s = ctx.search(3, seed=1, eta0=4.0, max_inner=50, accel=1, adaptive_weights=0)
+    s.set_x(torch.zeros((3, 2), dtype=torch.float32 if precision == 32 else torch.float64, device="cuda"))
+    s.begin_round()
+    T = s.tensors()
+    torch.cuda.synchronize()
+    assert np.all(T["xp"].cpu().numpy() == -1.0) and np.all(T["phase"].cpu().numpy() == 1)
+    want = [(2.0, -0.5, 1, 0.0), (1.0, -0.25, 1, 0.0), (2.0, -0.25, 1, -0.25), (4.0, -0.25, 0, -0.25),
+            (4.0, -0.25, 1, -0.25)]
+    for k, (eta_w, xp_w, ph_w, x_w) in enumerate(want):
+        s.iterate(1)
+        torch.cuda.synchronize()
+        assert np.all(T["eta"].cpu().numpy() == eta_w), k
+        assert np.all(T["xp"].cpu().numpy() == xp_w), k
+        assert np.all(T["phase"].cpu().numpy() == ph_w), k
+        assert np.all(T["x"].cpu().numpy() == x_w), k
+    assert np.all(T["f"].cpu().numpy() == -0.0625) and np.all(T["f_y"].cpu().numpy() == -0.0625)
+    t2 = (1 + np.sqrt(1 + 4 * ((1 + 5 ** 0.5) / 2) ** 2)) / 2
+    assert np.all(np.abs(T["t"].cpu().numpy() - t2) < 1e-15)
+    assert np.all(T["grad"].cpu().numpy() == 0.0)   # the gradient at y = the stationary point (Eg. 7)
+
+
+@pytest.mark.parametrize("precision,path", [(32, 0), (32, 4), (64, 0)])
+def test_fista_steps_match_oracle(precision, path):
+    """Per-step parity of the FISTA mode (reading #16b) against oracle/solve.py:fista_iteration: before every iteration
+    the oracle is re-synchronised to the GPU's state (x, x_prev, y, the point to evaluate, t, eta, phase) and evaluates
+    f, grad at y and at that point itself (T2 DP); both take one step.  Then:
+      * the action (y consumed / accept / reject) agrees wherever the oracle's margin against the quadratic upper
+        bound exceeds what the evaluation tolerance can move, eta and t follow exactly;
+      * accepted points: x is the evaluated point bit-exactly and x_prev the old x; the next point agrees within the
+        update's bound -- a projected trial clip(y - eta g_y): eta tol max(1, |g|) + rounding; an extrapolation
+        x + beta (x - x_prev): rounding only;
+      * rejected points keep x bit-exactly.
+    path 0 in fp32 is the TMEM kernel with the reduction fused into the FISTA step; path 4 the shared-memory tiled
+    kernel with the separate step; fp64 the general path."""
+    inst = synth.config1(3)
+    ctx = P.Context.from_instance(inst, precision=precision, device=0, path=path)
+    if precision == 32:
+        assert ctx.info["wide"] == (2 if path == 0 else 1)
+    B = 64
+    s = ctx.search(B, seed=9, max_inner=500, eta0=8.0, accel=1)
+    Fo = oracle_of(inst)
+    Pp = osolve.Params(max_inner=500, eta0=8.0)
+    tol, eps = TOL[precision], EPS[precision]
+    s.begin_round()
+    T = s.tensors()
+    w = ctx.to_input_order(T["weights"].cpu().numpy().astype(np.float64))
+    seen = {"y": 0, "accept": 0, "reject": 0}
+    n_tie = 0
+    get = lambda k: T[k].cpu().numpy().astype(np.float64)
+    for it in range(16):
+        torch.cuda.synchronize()
+        x, xm, y, xp = get("x"), get("x_prev"), get("y"), get("xp")
+        t, eta, phase = get("t"), get("eta"), T["phase"].cpu().numpy().copy()
+        fy_o, gy_o = cdp.evaluate_weighted(Fo, w, y)
+        f_o, g_o = cdp.evaluate_weighted(Fo, w, x)
+        st = osolve.FistaState(x=x.copy(), f=f_o, g=g_o, xm=xm.copy(), y=y.copy(), fy=fy_o, gy=gy_o, xp=xp.copy(),
+                               t=t.copy(), eta=eta.copy(), phase=phase.astype(np.int64), done=np.zeros(B, bool),
+                               iters=np.zeros(B, np.int64), w=w)
+        fp_o, gp_o = cdp.evaluate_weighted(Fo, w, xp)
+        acts = osolve.fista_iteration(Fo, st, Pp)
+        s.iterate(1)
+        torch.cuda.synchronize()
+        x2, xm2, xp2 = get("x"), get("x_prev"), get("xp")
+        eta2, t2 = get("eta"), get("t")
+        dx = xp - y
+        margin = fp_o - (fy_o + np.einsum("bn,bn->b", gy_o, dx) + np.einsum("bn,bn->b", dx, dx) / (2 * eta))
+        for b in range(B):
+            if phase[b] == 0:
+                act = "y"
+                assert eta2[b] == eta[b] and t2[b] == t[b]
+            elif eta2[b] == min(2 * eta[b], Pp.eta0) and t2[b] != t[b]:
+                act = "accept"
+            else:
+                act = "reject"
+                assert eta2[b] == 0.5 * eta[b] and t2[b] == t[b]
+            clear = phase[b] == 0 or abs(margin[b]) > 4 * tol * max(1.0, abs(fy_o[b]))
+            if not clear:
+                n_tie += 1
+                continue
+            assert act == acts[b], f"iteration {it} point {b}: GPU {act}, oracle {acts[b]}"
+            seen[act] += 1
+            assert eta2[b] == st.eta[b] and t2[b] == st.t[b]
+            if act == "accept":
+                assert np.array_equal(x2[b], xp[b]) and np.array_equal(xm2[b], x[b])
+                if st.phase[b] == 0:   # extrapolation point: rounding of x + beta (x - x_prev) only
+                    assert np.all(np.abs(xp2[b] - st.xp[b]) <= 8 * eps * (1 + np.abs(st.xp[b])))
+                    continue
+            else:
+                assert np.array_equal(x2[b], x[b])
+            # a new trial clip(y - eta g_y): y is the evaluated point after consuming y or a beta = 0 accept (its
+            # gradient comes from this evaluation), the old y after a reject; the GPU's g_y differs from the
+            # oracle's within the evaluation tolerance
+            g_new = gy_o[b] if act == "reject" else gp_o[b]
+            gmax = max(1.0, float(np.max(np.abs(g_new))))
+            trial_bound = st.eta[b] * (tol * gmax + 2 * eps * (1 + gmax)) + 2 * eps
+            assert np.all(np.abs(xp2[b] - st.xp[b]) <= trial_bound), f"trial differs at iteration {it} point {b}"
+    assert all(v > 0 for v in seen.values()), seen
+    assert n_tie <= 16 * B // 4, "most decisions must be clear of the tolerance band (the test has teeth)"
+
+
+def test_fista_solve_small_formulas():
+    """ffsat_solve with accel = 1: the Eg. 7 formula and uniform random 3-SAT (c1) solve, every SAT answer verified by
+    the exact check and the oracle; the UNSAT pair {x1, -x1} stays UNKNOWN."""
+    ctx = P.Context.from_file(golden("eg7_saddle.hnf"), device=0)
+    r, a = ctx.solve(batch=8, max_restarts=5, seed=1, max_inner=50, accel=1)
+    assert r["sat"] == 1 and ctx.check(a)[0] == 0
+    Fo = OracleFormula.from_constraints(1, [(0, 0, 1.0, [1]), (0, 0, 1.0, [-1])])
+    ctx = P.Context.from_arrays(1, Fo.kind, Fo.bound, Fo.weight, Fo.offsets, Fo.lits, device=0)
+    r, a = ctx.solve(batch=8, max_restarts=3, seed=1, max_inner=30, accel=1)
+    assert r["sat"] == 0 and r["best_unsat"] == 1
+    solved = 0
+    for seed in range(3):
+        inst = synth.config1(seed)
+        ctx = P.Context.from_instance(inst, device=0)
+        r, a = ctx.solve(batch=256, max_restarts=20, seed=seed, max_inner=100, accel=1)
+        if r["sat"]:
+            solved += 1
+            assert ctx.check(a)[0] == 0
+            assert cdp.check(oracle_of(inst), np.where(a < 0, -1.0, 1.0)[None])[0][0] == 0
+    assert solved >= 1
+
+
 def test_check_U_and_erwa_match_oracle():
     """Round-end check (A9) and ERWA (A10): unsat[b] exact; U_c exact PER CONSTRAINT (the device array is in
     position order, mapped back with Context.order()); the search's weights after the restart equal Prop. 3's
