@@ -92,6 +92,38 @@ void plan_chunks(ffsat_ctx* c) {
     };
     for (int g = 0; g < 3; ++g)
         if (ncg[g] > 0) split(ug[g], ug[g + 1], ncg[g], c->gchunk[g]);
+    if (L.tmem && ncg[0] > 0) {
+        // the TMEM kernel keeps its chunk's class data (headers, literal words, weights) resident in shared memory
+        // after the x tile: more chunks until the largest fits (228 KB per CTA minus the tile and the static part)
+        auto res_bytes = [&](int64_t ua, int64_t ub) -> size_t {
+            if (ua >= ub) return 0;
+            auto wb = [&](int64_t u) {
+                const WorkUnit& w = L.units[(size_t)u];
+                const FastBucket& b = L.fbuckets[(size_t)w.bucket];
+                return b.word_off + (w.pos_begin - b.pos_begin) * b.kp;
+            };
+            const WorkUnit& wl = L.units[(size_t)ub - 1];
+            const int64_t words = wb(ub - 1) + (int64_t)wl.count * L.fbuckets[(size_t)wl.bucket].kp - wb(ua);
+            const int64_t cons = wl.pos_begin + wl.count - L.units[(size_t)ua].pos_begin;
+            return (size_t)(16 * (ub - ua) + 4 * words + 4 * cons);
+        };
+        const size_t budget = (size_t)227 * 1024 - (size_t)256 * L.n - 1024;
+        for (;;) {
+            size_t mx = 0;
+            for (int j = 0; j < ncg[0]; ++j) mx = std::max(mx, res_bytes(cu[(size_t)j], cu[(size_t)j + 1]));
+            if (mx <= budget) {
+                c->tiled_smem = std::max(tmem_smem_bytes(L.n), (size_t)256 * L.n + mx);
+                break;
+            }
+            if (ncg[0] >= ug[1] - ug[0]) throw Error(FFSAT_ERR_ARG, "TMEM kernel: a class does not fit in shared memory");
+            ncg[0] = (int)std::min<int64_t>(ug[1] - ug[0], (int64_t)ncg[0] * mx / budget + 1);
+            c->gchunk[1] = ncg[0];
+            c->gchunk[2] = c->gchunk[3] = ncg[0];
+            c->n_chunks = ncg[0];
+            cu.assign((size_t)c->n_chunks + 1, 0);
+            split(ug[0], ug[1], ncg[0], 0);
+        }
+    }
     upload(c->chunk_units, cu);
     // the fixed f / unsat summation order: rows r = 0 .. R-1 (fast partials, then root-path constraints) summed in
     // f_groups interleaved groups (r mod f_groups), ascending inside a group, groups in order -- the same order in
@@ -125,10 +157,10 @@ void plan_chunks(ffsat_ctx* c) {
         c->sym_totF = tF;
     }
     if (L.path == 1) {
-        if (L.precision == 64) set_tiled_smem<double>(c->tiled_smem);
-        else set_tiled_smem<float>(c->tiled_smem);
-        if (L.wide) set_wide_smem(c->tiled_smem);
         if (L.tmem) set_tmem_smem(c->tiled_smem);
+        else if (L.wide) set_wide_smem(c->tiled_smem);
+        else if (L.precision == 64) set_tiled_smem<double>(c->tiled_smem);
+        else set_tiled_smem<float>(c->tiled_smem);
     }
     if (ncg[2] > 0) {
         if (L.precision == 64) set_long_smem<double>();

@@ -960,31 +960,12 @@ __device__ __forceinline__ void tmem_clauses(const BucketReg<float>& bk, int red
         for (int i = 0; i < K; ++i) tmem_st2(tq + (w[c][i] << 1), gv[c][i]);
 }
 
-struct TmemStage {
-    uint32_t words[4][2][kStageWords];   // [group][buffer]
-    float w[4][2][kStageCons];
-    UnitDev hdr[4][4];                   // [group][ring]
-    uint32_t tbase;
-};
-
-// Staging of one class by its group's 4 warps: lane l < 16 of group member r copies 16-byte word chunk 16 r + l,
-// lanes 16..19 weights 4 r .. 4 r + 3; lane 20 of member 0 copies the header of the group's class after it.
-template <int K>
-__device__ __forceinline__ void tmem_stage(const TiledArgs<float>& a, const UnitDev& U, int u, int i, int u1, TmemStage& st, int q,
-                                           int r, int buf, int lane) {
-    constexpr int KP = K_PAD(K);
-    const int count = unit_count(U);
-    const int ch = r * 16 + lane;
-    if (lane < 16 && ch * 4 < count * KP) cp_async16(&st.words[q][buf][ch * 4], a.words + (int64_t)U.word_begin + ch * 4);
-    const int j = r * 4 + (lane - 16);
-    if (lane >= 16 && lane < 20 && j < count) cp_async_small<4>(&st.w[q][buf][j], a.w_pos + (int64_t)U.pos_begin + j);
-    if (r == 0 && lane == 20 && u + 4 < u1) cp_async16(&st.hdr[q][(i + 1) & 3], a.units + u + 4);   // group class i + 1
-}
-
 template <int K, int RED, bool CHECK>
 __global__ void __launch_bounds__(32 * kTmemWarps, 1) fast_tmem_kernel(TiledArgs<float> a, uint32_t tcols) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];   // x tile [n][64] (host: tmem_smem_bytes)
-    __shared__ __align__(16) TmemStage st;
+    // dynamic shared memory: x tile [n][64] fp32, then the chunk's RESIDENT class data -- unit headers, literal words,
+    // weights -- staged once (the host sizes the chunks so they fit: plan_chunks); the epilogue tiles reuse it all
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    __shared__ uint32_t s_tbase;
     const int n = a.n;
     float* xs = reinterpret_cast<float*>(smem_raw);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -994,18 +975,23 @@ __global__ void __launch_bounds__(32 * kTmemWarps, 1) fast_tmem_kernel(TiledArgs
     const int u0 = a.chunk_units[chunk], u1 = a.chunk_units[chunk + 1];
     if (warp == 0) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
-                         (uint32_t)__cvta_generic_to_shared(&st.tbase)), "r"(tcols));
+                         (uint32_t)__cvta_generic_to_shared(&s_tbase)), "r"(tcols));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
-    // group q's classes: u = u0 + q + 4 i.  The first two classes' staging (and their headers) overlap the x tile load.
-    {
-        const int ua = u0 + q, ub = u0 + q + 4;
-        if (ua < u1) {
-            const UnitDev h = a.units[ua];
-            if (r == 0 && lane == 0) st.hdr[q][0] = h;
-            tmem_stage<K>(a, h, ua, 0, u1, st, q, r, 0, lane);   // also copies the header of ub into ring slot 1
-            if (ub < u1) tmem_stage<K>(a, a.units[ub], ub, 1, u1, st, q, r, 1, lane);
-        }
+    UnitDev* hdr_s = reinterpret_cast<UnitDev*>(smem_raw + (size_t)n * 256);
+    uint32_t* words_s = reinterpret_cast<uint32_t*>(hdr_s + (u1 - u0));
+    float* w_s = nullptr;
+    int wbase = 0, pbase = 0;
+    if (u0 < u1) {   // the chunk's units are contiguous in positions and literal words (host layout)
+        const UnitDev uf = a.units[u0], ul = a.units[u1 - 1];
+        wbase = uf.word_begin;
+        pbase = uf.pos_begin;
+        const int nwords = ul.word_begin + unit_count(ul) * unit_kp(ul) - wbase;   // a multiple of 4
+        const int ncons = ul.pos_begin + unit_count(ul) - pbase;
+        w_s = reinterpret_cast<float*>(words_s + nwords);
+        for (int i = threadIdx.x; i < u1 - u0; i += blockDim.x) cp_async16(&hdr_s[i], a.units + u0 + i);
+        for (int i = threadIdx.x; 4 * i < nwords; i += blockDim.x) cp_async16(&words_s[4 * i], a.words + wbase + 4 * i);
+        for (int i = threadIdx.x; i < ncons; i += blockDim.x) cp_async_small<4>(&w_s[i], a.w_pos + pbase + i);
     }
     cp_async_commit();
     {   // x tile [n][64]: row v = 64 points (256 B).  Thread t covers point t % 64, so a warp's 32 stores of one row are
@@ -1029,7 +1015,8 @@ __global__ void __launch_bounds__(32 * kTmemWarps, 1) fast_tmem_kernel(TiledArgs
     tmem_fence_before();
     __syncthreads();
     tmem_fence_after();
-    const uint32_t tq = st.tbase + ((uint32_t)(32 * q) << 16);
+    const uint32_t tbase = s_tbase;
+    const uint32_t tq = tbase + ((uint32_t)(32 * q) << 16);
     // zero the quadrant's 2 n columns (member r takes columns r, r + 4, ... in pairs)
     for (int v = r; v < n; v += 4) tmem_st2(tq + 2 * v, make_float2(0.0f, 0.0f));
     tmem_wait_st();
@@ -1044,16 +1031,17 @@ __global__ void __launch_bounds__(32 * kTmemWarps, 1) fast_tmem_kernel(TiledArgs
     int bucket = -1;
     BucketReg<float> bk{};
     int redpol = 0;
-    int buf = 0;
-    for (int i = 0, u = u0 + q; u < u1; ++i, u += 4) {
-        const UnitDev cur = st.hdr[q][i & 3];
+    // group q takes classes u0 + q, u0 + q + 4, ...; 4 clauses per warp per class as two interleaved pairs; a named
+    // barrier per group (128 threads) separates its classes (var-disjoint inside a class: fixed accumulation order)
+    for (int u = u0 + q; u < u1; u += 4) {
+        const UnitDev cur = hdr_s[u - u0];
         if (cur.bucket != bucket) {
             bucket = cur.bucket;
             bk = load_bucket<float>(a.buckets + bucket);
             redpol = (a.buckets[bucket].red & 4) ? 0 : 1;
         }
-        const uint32_t* sw = st.words[q][buf];
-        const float* swt = st.w[q][buf];
+        const uint32_t* sw = words_s + (cur.word_begin - wbase);
+        const float* swt = w_s + (cur.pos_begin - pbase);
         const int count = unit_count(cur);
         float2 fe2 = make_float2(0.0f, 0.0f);
 #pragma unroll
@@ -1067,15 +1055,11 @@ __global__ void __launch_bounds__(32 * kTmemWarps, 1) fast_tmem_kernel(TiledArgs
         }
         f0 += (double)fe2.x;
         f1 += (double)fe2.y;
-        // end of the class: my TMEM stores are complete, the group's next class words / header are in shared memory
+        // end of the class: my TMEM stores are complete before the group's next class
         tmem_wait_st();
-        cp_async_wait_all();
         tmem_fence_before();
         named_bar(1 + q, 128);
         tmem_fence_after();
-        buf ^= 1;
-        if (u + 8 < u1) tmem_stage<K>(a, st.hdr[q][(i + 2) & 3], u + 8, i + 2, u1, st, q, r, buf ^ 1, lane);
-        cp_async_commit();
     }
     pdl_trigger();
     // the four quadrant tiles summed in a fixed order, (q0 + q2) + (q1 + q3), through two shared tiles T0 = x tile
@@ -1119,7 +1103,7 @@ __global__ void __launch_bounds__(32 * kTmemWarps, 1) fast_tmem_kernel(TiledArgs
     }
     if (warp == 0) {   // every TMEM access of the CTA is ordered before the deallocation (fence - barrier - fence)
         tmem_fence_after();
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(st.tbase), "r"(tcols));
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tbase), "r"(tcols));
     }
     // the chunk's partial gradient, POINT-major: P[chunk][b][v] (a point's row is contiguous, so the reduction -- or
     // the fused PGD step, one CTA per point -- reads it coalesced); warp w writes points w, w + 16, ..., lanes over v
