@@ -109,6 +109,8 @@ typedef struct {
     int64_t device_bytes;   /* persistent device memory held by the context */
     int64_t n_own_lits;     /* global path: literals of the short constraints whose gradient terms the owner-computes
                                kernel forms per variable (no T-buffer round trip); 0 otherwise */
+    int64_t n_tree_cons;    /* fp64 symmetric constraints on the product-tree path (long k) */
+    int64_t tree_work;      /* their FP64 instructions per point (the tree path's algorithmic count) */
 } ffsat_info_t;
 
 /* Build a context from arrays (validates, buckets, precomputes coefficients, uploads). */

@@ -88,6 +88,7 @@ namespace ffsat {
 // one (so a search's captured CUDA graph never references buffers another call may resize).
 struct Scratch {
     DBuf xT, Tb, P, fpart, upart, fsym, usym, TbS, fS;
+    DBuf tree_ctr;                // work counters of the product-tree classes (one int32 per sym class)
     int64_t B = -1;
 };
 }  // namespace ffsat
@@ -184,6 +185,8 @@ template <typename T>
 void set_tiled_smem(size_t bytes);
 void set_wide_smem(size_t bytes);   // eval_f32.cu
 void set_tmem_smem(size_t bytes);   // eval_f32.cu
+void launch_tree_class(const SymClass& cl, const dev::SymArgs<double>& a, int max_k, int32_t* counter, int num_sm,
+                       cudaStream_t st);   // sym_f64.cu
 template <typename T>
 void set_long_smem();              // the long global kernel's dynamic shared memory (eval_f32.cu / eval_f64.cu)
 // one root-path launch class (sym_f32.cu / sym_f64.cu)

@@ -182,6 +182,7 @@ void ensure_scratch(const ffsat_ctx* c, Scratch& S, int64_t B) {
     S.usym.ensure(std::max<size_t>(16, (size_t)L.n_sym * b * 4));
     S.TbS.ensure(std::max<size_t>(16, (size_t)c->sym_totT * b * es));
     S.fS.ensure(std::max<size_t>(16, (size_t)c->sym_totF * b * 8));
+    S.tree_ctr.ensure(std::max<size_t>(16, L.sym_classes.size() * 4));
     S.B = B;
 }
 

@@ -131,6 +131,16 @@ void eval_device_t(ffsat_ctx* c, Scratch& S, const T* x, int64_t B, double* f, T
             sp.lit0 = cl.lit_begin;
             sp.TbS = S.TbS.as<T>() + c->sym_offT[i] * B;
             sp.fS = S.fS.as<double>() + c->sym_offF[i] * B;
+            if (cl.G == kTreeClass) {
+                if constexpr (sizeof(T) == 8) {
+                    const int max_k = (int)(L.sym_off[(size_t)cl.begin + 1] - L.sym_off[(size_t)cl.begin]);   // sorted longest first
+                    launch_tree_class(cl, a, max_k, S.tree_ctr.as<int32_t>() + i, c->num_sm, ss);
+                } else {
+                    throw Error(FFSAT_ERR_ARG, "product-tree class in an fp32 context");
+                }
+                c->launches += 1;
+                continue;
+            }
             launch_sym_class<T>(cl, cl.G == 0 ? aT : a, sp, ss);
             c->launches += sp.S > 1 ? 2 : 1;   // + the split combine
         }

@@ -601,6 +601,7 @@ ffsat_status ffsat_info(const ffsat_ctx* c, ffsat_info_t* o) {
     o->n_fast_cons = L.n_fast; o->n_sym_cons = L.n_sym; o->n_fast_lits = L.n_fast_lits; o->n_sym_lits = L.n_sym_lits;
     o->sym_root_lits = L.sym_root_lits; o->path = L.path; o->wide = L.tmem ? 2 : L.wide ? 1 : 0; o->max_k = L.max_k; o->device_bytes = c->persistent_bytes;
     o->n_own_lits = L.n_own_lits;
+    o->n_tree_cons = L.n_tree_cons; o->tree_work = L.tree_work;
     return FFSAT_OK;
     ABI_CATCH(nullptr)
 }

@@ -1,6 +1,7 @@
 // host.cpp -- host formula layer of libffsat: A1 parse/validate, A2 bucketing and CSR layouts,
 // A3 coefficient tables.  See host.hpp and DESIGN.md.
 #include "host.hpp"
+#include "tree_geom.hpp"
 
 #include <algorithm>
 #include <cstdlib>
@@ -297,6 +298,16 @@ static void sym_geom(int k, int* nw_out, int* c_out) {
     throw Error(FFSAT_ERR_ARG, "root-path constraint too long for one thread group (k > 4096)");
 }
 int sym_chunk(int k) { int nw, c; sym_geom(k, &nw, &c); return c; }
+// Product-tree path (kernels_tree.cuh): fp64 symmetric constraints of at least FFSAT_TREE_KMIN literals (default 256;
+// FFSAT_TREE=0 keeps every constraint on the root-of-unity path) whose tree fits in one CTA's shared memory.
+bool tree_path(int k, int precision) {
+    if (precision != 64) return false;
+    const char* e0 = std::getenv("FFSAT_TREE");
+    const char* e1 = std::getenv("FFSAT_TREE_KMIN");
+    const bool on = !(e0 && std::atoi(e0) == 0);
+    const int kmin = e1 ? std::max(33, std::atoi(e1)) : 256;
+    return on && k >= kmin && (size_t)tree::tree_geom(k).total * 8 <= tree::kTreeSmemMax;
+}
 // roots per pass: 1 with the factors kept in registers (measured faster than recomputing them for a
 // higher occupancy or than two roots per pass: profiles/r01_bench_c3_*.json)
 int sym_roots(int) { return 1; }
@@ -333,10 +344,17 @@ Layout build_layout(const Formula& F, int path, int precision) {
         if (ka != kb) return ka < kb;
         return ff[a].variant < ff[b].variant;
     });
+    // launch geometry of a sym constraint: the product-tree class (G = kTreeClass, sorted last) or a root-path class
+    auto sgeom = [&](int k, int* G, int* C) {
+        if (tree_path(k, precision)) { *G = kTreeClass; *C = 1 << 20; return; }
+        *G = sym_group(k);
+        *C = sym_chunk(k);
+    };
     std::stable_sort(sym_ids.begin(), sym_ids.end(), [&](int64_t a, int64_t b) {
-        const int ca = sym_chunk(klen(a)), cb = sym_chunk(klen(b));
+        int ga, gb, ca, cb;
+        sgeom(klen(a), &ga, &ca);
+        sgeom(klen(b), &gb, &cb);
         if (ca != cb) return ca < cb;
-        const int ga = sym_group(klen(a)), gb = sym_group(klen(b));
         if (ga != gb) return ga > gb;   // largest groups first (longest work first within a launch)
         return klen(a) > klen(b);
     });
@@ -450,7 +468,13 @@ Layout build_layout(const Formula& F, int path, int precision) {
         Lo.n_sym_lits += k;
         Lo.sym_root_lits += (int64_t)k * ((k + 1) / 2);
         Lo.sym_off.push_back(Lo.n_sym_lits);
-        const int G = sym_group(k), C = sym_chunk(k), R = sym_roots(k);
+        int G, C;
+        sgeom(k, &G, &C);
+        const int R = G == kTreeClass ? 0 : sym_roots(k);
+        if (G == kTreeClass) {
+            Lo.n_tree_cons += 1;
+            Lo.tree_work += tree::tree_fp64_work(k);
+        }
         if (Lo.sym_classes.empty() || Lo.sym_classes.back().G != G || Lo.sym_classes.back().C != C)
             Lo.sym_classes.push_back({G, C, R, s, s + 1, 0});
         else Lo.sym_classes.back().end = s + 1;
@@ -463,7 +487,7 @@ Layout build_layout(const Formula& F, int path, int precision) {
     for (SymClass& cl : Lo.sym_classes) {
         cl.lit_begin = Lo.sym_off[(size_t)cl.begin];
         cl.lit_end = Lo.sym_off[(size_t)cl.end];
-        cl.S = cl.G == 0 ? 1 : std::max(1, std::min(32, (cl.max_mp + root_chunk - 1) / root_chunk));
+        cl.S = cl.G <= 0 ? 1 : std::max(1, std::min(32, (cl.max_mp + root_chunk - 1) / root_chunk));
     }
 
     // ---- owner-computes buckets (global path): no T slots; the other fast buckets' slots are renumbered densely

@@ -75,6 +75,8 @@ struct WorkUnit {                   // a run of fast constraints of one bucket, 
     int64_t pos_begin;              // tile concurrently and deterministically
 };
 
+constexpr int kTreeClass = -1;      // SymClass::G of the product-tree path
+bool tree_path(int k, int precision);   // fp64 long symmetric constraints whose tree fits in shared memory
 int sym_group(int k);               // threads per (constraint, point) on the root path
 int sym_chunk(int k);               // literals per thread on the root path (G * C >= k)
 int sym_roots(int k);               // roots per pass on the root path
@@ -102,6 +104,8 @@ struct Layout {
     std::vector<int32_t> sym_rule;      // 3 ints per sym constraint (tmin, tmax, parity)
     std::vector<SymClass> sym_classes;
     bool sym_lane = false;              // some root-path class runs thread-per-item on x^T (needs the transpose)
+    int64_t n_tree_cons = 0;            // sym constraints on the product-tree path (kernels_tree.cuh; SymClass G = kTreeClass)
+    int64_t tree_work = 0;              // its FP64 instructions per point (tree::tree_fp64_work summed)
     // T-buffer slots (global path: non-owner fast slots then sym slots; tiled path: sym slots only)
     int64_t tb_fast = 0, tb_slots = 0;
     // owner-computes (global path, fast buckets with k <= kOwnKMax): per variable its occurrences in those

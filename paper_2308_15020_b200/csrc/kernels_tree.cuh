@@ -1,0 +1,367 @@
+// kernels_tree.cuh -- product-tree path for long symmetric constraints (fp64): f and the exact gradient of
+// FE = sum_t f(t) P(T = t) through a binary tree of Poisson-binomial polynomials, the work-efficient form of
+// Prop. 2's log-depth product tree that the paper names as future work for long constraints.
+//
+// Per (constraint c, point b) item, with p_i = (1 - l_i) / 2 and the literal generating polynomials
+// f_i(z) = (1 - p_i) + p_i z (so prod_i f_i = sum_t P(T = t) z^t, T = number of True literals):
+//   bottom-up   node polynomial P_S = P_left * P_right (schoolbook convolution; leaves are blocks of 16 literals,
+//               computed by the sequential Bernoulli recurrence of Alg. 5's forward pass);
+//   root        FE = sum_t f(t) P_root[t] (Def. 3 / Thm. 1: the multilinear extension of the truth-by-count table);
+//   top-down    the linear functional L(g) = sum_t f(t) [z^t] g pushed down the tree: lambda_root = f, and for a
+//               node S with children L, R: lambda_L[t] = sum_s lambda_S[t + s] P_R[s] (the functional g ->
+//               L(g * prod_{j not in L} f_j) restricted to L's degree), symmetrically for R;
+//   leaves      for literal i in block g: dFE/dp_i = L(prod_{j != i} f_j (z - 1)) = sum_s delta_g[s] Q_i[s] with
+//               delta_g[s] = lambda_g[s + 1] - lambda_g[s] and Q_i = prod_{j in g, j != i} f_j; dFE/dl_i = -dFE/dp_i / 2.
+// Every quantity is a probability vector or a functional bounded by max |f| = 1 combined with convex weights, so the
+// fp64 result is accurate to a few ulps times the tree depth.  Work per item ~ k^2 / 2 (bottom-up) + k^2 (top-down)
+// fused multiply-adds, against 12 k M' (~6 k^2) FP64 instruction slots of the root-of-unity path.
+//
+// Mapping: one CTA of 512 threads per item (persistent CTAs take items from an atomic counter, longest constraints
+// first; results do not depend on the assignment).  The polynomials of every tree level and two functional buffers
+// live in shared memory.  A work unit computes R = 9 consecutive outputs of one node over a share of the inner index
+// (the share's partial sums are combined with warp shuffles in a fixed order): one operand is read as a broadcast,
+// the other through a register ring (one new element per step: 9 FMAs per 2 shared loads); R odd keeps the windowed
+// loads of 32 lanes (stride R doubles) bank-conflict-free.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "kernels_common.cuh"
+#include "kernels_eval.cuh"
+#include "tree_geom.hpp"
+
+namespace ffsat {
+namespace dev {
+
+constexpr int kTreeThreads = 512;
+using tree::kTreeLeaf;
+using tree::kTreeR;
+using tree::kTreePF;
+using tree::kTreeNR;
+using tree::kTreePad;
+using tree::TreeGeom;
+using tree::tree_nodes;
+using tree::tree_level_size;
+using tree::tree_geom;
+// first coefficient of node j at level l
+__device__ __forceinline__ int tree_node(const TreeGeom& g, int base, int l, int j) {
+    return base + kTreePad + j * ((kTreeLeaf << l) + 1 + kTreePad);
+}
+// number of real literals of node j at level l (its polynomial degree); <= 0 if the node does not exist
+__device__ __forceinline__ int tree_deg(const TreeGeom& g, int l, int j) {
+    const int D = kTreeLeaf << l;
+    return min(D, g.k - j * D);
+}
+
+// acc[r] += sum_{s = sa}^{sb - 1} A[s] W[t0 + r - s] (CONV) or A[s] W[t0 + r + s] (CORR), r = 0..R-1.  A is read as
+// a (mostly) broadcast operand, W through a register ring of R + PF elements (one new element per step); the loads
+// may run up to R + PF elements past the window's range on either side (the zero guards).
+template <bool CONV>
+__device__ __forceinline__ void tree_unit(const double* A, const double* W, int t0, int sa, int sb, double (&acc)[kTreeR]) {
+    constexpr int R = kTreeR, PF = kTreePF, NR = kTreeNR;
+    double ring[NR];
+    // window element e' (relative): CONV index t0 - sa + e' with e' = r - u; CORR index t0 + sa + e' with e' = r + u
+    const double* wp = W + (CONV ? t0 - sa : t0 + sa);
+#pragma unroll
+    for (int e = 0; e < R; ++e) ring[e] = wp[e];
+#pragma unroll
+    for (int e = 1; e < PF; ++e) {
+        if (CONV) ring[NR - e] = wp[-e];
+        else ring[R + e - 1] = wp[R + e - 1];
+    }
+    const int n = sb - sa;
+    const double* ap = A + sa;
+    int u0 = 0;
+    for (; u0 + NR <= n; u0 += NR) {
+        double av[NR];
+#pragma unroll
+        for (int u = 0; u < NR; ++u) av[u] = ap[u0 + u];
+#pragma unroll
+        for (int u = 0; u < NR; ++u) {
+            if (CONV) ring[(NR - ((u + PF) % NR)) % NR] = wp[-(u0 + u) - PF];
+            else ring[(u + R + PF - 1) % NR] = wp[u0 + u + R + PF - 1];
+#pragma unroll
+            for (int r = 0; r < R; ++r) acc[r] = fma(av[u], ring[CONV ? (r - u + NR * 2) % NR : (r + u) % NR], acc[r]);
+        }
+    }
+    const int rem = n - u0;
+    if (rem > 0) {
+        double av[NR];
+#pragma unroll
+        for (int u = 0; u < NR; ++u) av[u] = u < rem ? ap[u0 + u] : 0.0;
+#pragma unroll
+        for (int u = 0; u < NR; ++u) {
+            if (u < rem) {
+                if (CONV) ring[(NR - ((u + PF) % NR)) % NR] = wp[-(u0 + u) - PF];
+                else ring[(u + R + PF - 1) % NR] = wp[u0 + u + R + PF - 1];
+#pragma unroll
+                for (int r = 0; r < R; ++r) acc[r] = fma(av[u], ring[CONV ? (r - u + NR * 2) % NR : (r + u) % NR], acc[r]);
+            }
+        }
+    }
+}
+
+// inner-index shares per unit: the smallest count that gives the CTA's threads work
+__device__ __forceinline__ int tree_shares(int units) {
+    int best = 1;
+    double be = 0.0;
+    for (int P = 1; P <= 8; P *= 2) {
+        const int items = units * P;
+        const int rounds = (items + kTreeThreads - 1) / kTreeThreads;
+        const double eff = (double)items / ((double)rounds * kTreeThreads);
+        if (eff > be + 0.02) {
+            be = eff;
+            best = P;
+        }
+    }
+    return best;
+}
+
+// sum of the P partials of a unit held by P consecutive lanes (butterfly: every lane ends with the same, fixed-order sum)
+__device__ __forceinline__ void tree_combine(double (&acc)[kTreeR], int P) {
+#pragma unroll
+    for (int o = 1; o < 8; o <<= 1) {
+        if (o >= P) break;
+#pragma unroll
+        for (int r = 0; r < kTreeR; ++r) acc[r] += __shfl_xor_sync(0xffffffffu, acc[r], o);
+    }
+}
+
+// leaf block polynomial: prod_{i in block} ((1 - p_i) + p_i z), p[] padded with zeros past k (identity factors);
+// skip = the literal left out (-1: none).  Alg. 5's forward recurrence, coefficients in registers.
+__device__ __forceinline__ void tree_leaf_poly(const double* p, int skip, double (&q)[kTreeLeaf + 1]) {
+    q[0] = 1.0;
+#pragma unroll
+    for (int t = 1; t <= kTreeLeaf; ++t) q[t] = 0.0;
+#pragma unroll
+    for (int i = 0; i < kTreeLeaf; ++i) {
+        const double pi = i == skip ? 0.0 : p[i];
+        const double qi = 1.0 - pi;
+#pragma unroll
+        for (int t = i + 1; t >= 1; --t) q[t] = fma(pi, q[t - 1], qi * q[t]);
+        q[0] *= qi;
+    }
+}
+
+__device__ __forceinline__ double tree_f(int t, const SymSigDev& sg) { return rule_sat(t, sg.tmin, sg.tmax, sg.parity) ? -1.0 : 1.0; }
+
+// fixed-order CTA sums (warp butterflies, then the warps in order)
+__device__ __forceinline__ double tree_block_sum(double v, double* red) {
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    __syncthreads();
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+    __syncthreads();
+    double t = 0.0;
+    for (int w = 0; w < kTreeThreads / 32; ++w) t += red[w];
+    return t;
+}
+
+__global__ void __launch_bounds__(kTreeThreads, 1) sym_tree_kernel(SymArgs<double> a, int64_t s_begin, int64_t n_items, int32_t* counter) {
+    extern __shared__ __align__(16) double sm[];
+    __shared__ double s_red[kTreeThreads / 32];
+    __shared__ int s_item;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    for (;;) {
+        if (tid == 0) s_item = atomicAdd(counter, 1);
+        __syncthreads();
+        const int64_t item = s_item;
+        if (item >= n_items) break;
+        const int64_t s = s_begin + item / a.B, b = item - (item / a.B) * a.B;   // the class is sorted by k, longest first
+        const SymSigDev sg = a.sigs[a.sig_of[s]];
+        const TreeGeom g = tree_geom(sg.k);
+        const int k = g.k;
+        const int64_t lo = a.off[s];
+        // zero everything past p (the guards and the unused tails must read as 0), then p_i = (1 - l_i) / 2
+        for (int i = g.kp + tid; i < g.total; i += kTreeThreads) sm[i] = 0.0;
+        double* p = sm;
+        int tc = 0;
+        for (int i = tid; i < g.kp; i += kTreeThreads) {
+            double pi = 0.0;
+            if (i < k) {
+                const uint32_t w = __ldg(a.words + lo + i);
+                const double xv = a.x[b * a.sb + (int64_t)(w & 0x7fffffffu) * a.sv];
+                const double l = (int)w < 0 ? -xv : xv;
+                pi = 0.5 - 0.5 * l;
+                tc += (int)((xv < 0.0) != ((int)w < 0));   // the literal is True (sgn rounding, x = 0 -> False)
+            }
+            p[i] = pi;
+        }
+        __syncthreads();
+        if (tid == 0) sm[g.one + kTreePad] = 1.0;
+        // ---- bottom-up, level 1 (32 literals): warp per node, lanes 0 / 1 form the two leaf polynomials
+        double* tmp = sm + g.lamY;   // 16 warps x 34 doubles of scratch (the functional buffers are free until the root)
+        const int n1 = tree_nodes(k, 1);
+        for (int j = warp; j < n1; j += kTreeThreads / 32) {
+            double* tw = tmp + warp * 2 * (kTreeLeaf + 1);
+            if (lane < 2) {
+                double q[kTreeLeaf + 1];
+                tree_leaf_poly(p + 32 * j + 16 * lane, -1, q);
+#pragma unroll
+                for (int t = 0; t <= kTreeLeaf; ++t) tw[lane * (kTreeLeaf + 1) + t] = q[t];
+            }
+            __syncwarp();
+            double* dst = sm + tree_node(g, g.off[1], 1, j);
+            const int d = tree_deg(g, 1, j);
+            for (int t = lane; t <= d; t += 32) {
+                double c = 0.0;
+                for (int u = max(0, t - kTreeLeaf); u <= min(kTreeLeaf, t); ++u) c = fma(tw[u], tw[kTreeLeaf + 1 + t - u], c);
+                dst[t] = c;
+            }
+            __syncwarp();
+        }
+        // ---- bottom-up, levels 2..Lv: node j = child 2j * child 2j+1 (a missing right child is the polynomial 1)
+        for (int l = 2; l <= g.Lv; ++l) {
+            __syncthreads();
+            const int nl = tree_nodes(k, l), D = kTreeLeaf << l;
+            const int nbF = (D + 1 + kTreeR - 1) / kTreeR;
+            const int units = nl * nbF;
+            const int P = tree_shares(units);
+            const int items = (units * P + 31) / 32 * 32;
+            for (int w = tid; w < items; w += kTreeThreads) {
+                const int q = w / P, h = w - q * P;
+                const int j = q / nbF, t0 = (q - j * nbF) * kTreeR;
+                const bool ok = j < nl && t0 <= tree_deg(g, l, j);
+                int dA = 0, dB = 0, sa = 0, sb = 0;
+                const double *A = sm, *W = sm;
+                if (ok) {
+                    dA = tree_deg(g, l - 1, 2 * j);
+                    const int dR = tree_deg(g, l - 1, 2 * j + 1);
+                    A = sm + tree_node(g, g.off[l - 1], l - 1, 2 * j);
+                    W = dR > 0 ? sm + tree_node(g, g.off[l - 1], l - 1, 2 * j + 1) : sm + g.one + kTreePad;
+                    dB = max(dR, 0);
+                    const int lo_s = max(0, t0 - dB), hi_s = min(dA, t0 + kTreeR - 1);
+                    const int per = (hi_s - lo_s + P) / P;
+                    sa = min(hi_s + 1, lo_s + h * per);
+                    sb = min(hi_s + 1, sa + per);
+                }
+                double acc[kTreeR];
+#pragma unroll
+                for (int r = 0; r < kTreeR; ++r) acc[r] = 0.0;
+                if (sa < sb) tree_unit<true>(A, W, t0, sa, sb, acc);
+                tree_combine(acc, P);
+                if (ok && h == 0) {
+                    double* dst = sm + tree_node(g, g.off[l], l, j);
+                    const int d = tree_deg(g, l, j);
+#pragma unroll
+                    for (int r = 0; r < kTreeR; ++r)
+                        if (t0 + r <= d) dst[t0 + r] = acc[r];
+                }
+            }
+        }
+        __syncthreads();
+        // ---- root: lambda = f, FE = sum_t f(t) P_root[t]
+        const double* Proot = sm + tree_node(g, g.off[g.Lv], g.Lv, 0);
+        double* lam = sm + g.lamX;   // level Lv functional (node 0 at the level layout)
+        double fe = 0.0;
+        for (int t = tid; t <= k; t += kTreeThreads) {
+            const double ft = tree_f(t, sg);
+            fe = fma(ft, Proot[t], fe);
+            lam[kTreePad + t] = ft;
+        }
+        fe = tree_block_sum(fe, s_red);
+        // ---- top-down, levels Lv..2 -> 1: lambda_L = corr(lambda_S, P_R), lambda_R = corr(lambda_S, P_L)
+        int cur = g.lamX, nxt = g.lamY;
+        for (int l = g.Lv; l >= 2; --l) {
+            // the next buffer: zero it (its guards are read by the windows of the next level), except on the first
+            // pass where it still holds the level-1 scratch (already consumed)
+            for (int i = tid; i < g.lamSize; i += kTreeThreads) sm[nxt + i] = 0.0;
+            __syncthreads();
+            const int nl = tree_nodes(k, l), Dc = kTreeLeaf << (l - 1);
+            const int nbF = (Dc + 1 + kTreeR - 1) / kTreeR;
+            const int units = nl * 2 * nbF;
+            const int P = tree_shares(units);
+            const int items = (units * P + 31) / 32 * 32;
+            // level l functional of node j starts at the same offset as the level-l node layout, relative to cur
+            for (int w = tid; w < items; w += kTreeThreads) {
+                const int q = w / P, h = w - q * P;
+                const int j = q / (2 * nbF), rq = q - j * 2 * nbF, side = rq / nbF, t0 = (rq - side * nbF) * kTreeR;
+                const int child = 2 * j + side;
+                bool ok = j < nl && t0 <= tree_deg(g, l - 1, child);
+                int sa = 0, sb = 0;
+                const double *A = sm, *W = sm;
+                if (ok) {
+                    const int sib = 2 * j + 1 - side;
+                    const int dS = tree_deg(g, l - 1, sib);
+                    A = dS > 0 ? sm + tree_node(g, g.off[l - 1], l - 1, sib) : sm + g.one + kTreePad;
+                    W = sm + cur + kTreePad + j * ((kTreeLeaf << l) + 1 + kTreePad);
+                    const int hi_s = max(dS, 0);
+                    const int per = (hi_s + P) / P;
+                    sa = min(hi_s + 1, h * per);
+                    sb = min(hi_s + 1, sa + per);
+                }
+                double acc[kTreeR];
+#pragma unroll
+                for (int r = 0; r < kTreeR; ++r) acc[r] = 0.0;
+                if (sa < sb) tree_unit<false>(A, W, t0, sa, sb, acc);
+                tree_combine(acc, P);
+                if (ok && h == 0) {
+                    double* dst = sm + nxt + kTreePad + child * (Dc + 1 + kTreePad);
+                    const int d = tree_deg(g, l - 1, child);
+#pragma unroll
+                    for (int r = 0; r < kTreeR; ++r)
+                        if (t0 + r <= d) dst[t0 + r] = acc[r];
+                }
+            }
+            __syncthreads();
+            const int tsw = cur;
+            cur = nxt;
+            nxt = tsw;
+        }
+        // ---- leaves: warp per level-1 node (lambda at cur), lane = literal 32 j + lane
+        const double wc = a.w_sym[s];
+        for (int j = warp; j < n1; j += kTreeThreads / 32) {
+            const double* lam1 = sm + cur + kTreePad + j * (32 + 1 + kTreePad);
+            double* tw = sm + nxt + warp * 4 * (kTreeLeaf + 1);   // P_L, P_R, then delta_L, delta_R
+            if (lane < 2) {
+                double q[kTreeLeaf + 1];
+                tree_leaf_poly(p + 32 * j + 16 * lane, -1, q);
+#pragma unroll
+                for (int t = 0; t <= kTreeLeaf; ++t) tw[lane * (kTreeLeaf + 1) + t] = q[t];
+            }
+            __syncwarp();
+            // lambda_L[t] = sum_s lam1[t + s] P_R[s], lambda_R[t] = sum_s lam1[t + s] P_L[s], t = 0..16
+            if (lane <= kTreeLeaf) {
+                double vl = 0.0, vr = 0.0;
+                for (int u = 0; u <= kTreeLeaf; ++u) {
+                    vl = fma(lam1[lane + u], tw[kTreeLeaf + 1 + u], vl);
+                    vr = fma(lam1[lane + u], tw[u], vr);
+                }
+                tw[2 * (kTreeLeaf + 1) + lane] = vl;
+                tw[3 * (kTreeLeaf + 1) + lane] = vr;
+            }
+            __syncwarp();
+            const int i = 32 * j + lane;
+            const int blk = lane >> 4;
+            double qi[kTreeLeaf + 1];
+            tree_leaf_poly(p + 32 * j + 16 * blk, lane & 15, qi);
+            const double* lb = tw + (2 + blk) * (kTreeLeaf + 1);
+            double dp = 0.0;   // dFE/dp_i = sum_s (lambda[s + 1] - lambda[s]) Q_i[s]
+#pragma unroll
+            for (int u = 0; u < kTreeLeaf; ++u) dp = fma(lb[u + 1] - lb[u], qi[u], dp);
+            if (i < k) {
+                const uint32_t w = __ldg(a.words + lo + i);
+                const double v = wc * (-0.5 * dp);   // dFE/dl_i = -dFE/dp_i / 2
+                a.Tb[(a.tb_fast + lo + i) * a.B + b] = (int)w < 0 ? -v : v;
+            }
+            __syncwarp();
+        }
+        // unsat count (integer, exact), f
+        int tcs = tc;
+#pragma unroll
+        for (int o = 16; o >= 1; o >>= 1) tcs += __shfl_xor_sync(0xffffffffu, tcs, o);
+        __syncthreads();
+        if (lane == 0) reinterpret_cast<int*>(s_red)[warp] = tcs;
+        __syncthreads();
+        if (tid == 0) {
+            int t = 0;
+            for (int w = 0; w < kTreeThreads / 32; ++w) t += reinterpret_cast<int*>(s_red)[w];
+            a.fsym[s * a.B + b] = wc * fe;
+            a.usym[s * a.B + b] = rule_sat(t, sg.tmin, sg.tmax, sg.parity) ? 0 : 1;
+        }
+        __syncthreads();
+    }
+}
+
+}  // namespace dev
+}  // namespace ffsat

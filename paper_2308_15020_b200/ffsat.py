@@ -43,7 +43,8 @@ class ffsat_info_t(C.Structure):
     _fields_ = [("n_vars", C.c_int32), ("precision", C.c_int32), ("n_cons", C.c_int64), ("n_lits", C.c_int64),
                 ("n_fast_cons", C.c_int64), ("n_sym_cons", C.c_int64), ("n_fast_lits", C.c_int64),
                 ("n_sym_lits", C.c_int64), ("sym_root_lits", C.c_int64), ("path", C.c_int32), ("wide", C.c_int32),
-                ("max_k", C.c_int32), ("pad", C.c_int32), ("device_bytes", C.c_int64), ("n_own_lits", C.c_int64)]
+                ("max_k", C.c_int32), ("pad", C.c_int32), ("device_bytes", C.c_int64), ("n_own_lits", C.c_int64),
+                ("n_tree_cons", C.c_int64), ("tree_work", C.c_int64)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}

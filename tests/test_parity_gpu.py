@@ -238,6 +238,50 @@ def test_long_cardinality_fp64(k):
     compare(inst, synth.points("N", 3, inst.n, 28))
 
 
+@pytest.mark.parametrize("k", [256, 257, 300, 511, 512, 513, 1000, 2000, 2048])
+def test_product_tree_path(k):
+    """fp64 symmetric constraints of k >= 256 literals take the product-tree kernel (kernels_tree.cuh, ffsat_info
+    n_tree_cons): f and the gradient against the T2 oracle at the fp64 tolerance on uniform, near-corner, corner and
+    tie points, unsat exact; every kind of truth table (at-least-b, at-most-b with mixed signs, XOR / XNOR parity, OR,
+    NAE), tree sizes around the powers of two (levels with and without a right child, partial leaf blocks)."""
+    n = k + 40
+    rng = np.random.default_rng(k)
+    cons = []
+    for kind, bnd in ((3, k // 3), (4, k // 2), (1, 0), (2, 0), (0, 0), (5, 0), (4, k - 1)):
+        vs = rng.choice(n, size=k, replace=False) + 1
+        lits = np.where(rng.random(k) < 0.5, -vs, vs).tolist()
+        cons.append((kind, bnd, float(rng.uniform(0.5, 2.0)), lits))
+    for _ in range(20):   # some short clauses on other paths alongside
+        vs = rng.choice(n, size=3, replace=False) + 1
+        cons.append((0, 0, 1.0, np.where(rng.random(3) < 0.5, -vs, vs).tolist()))
+    Fo = OracleFormula.from_constraints(n, cons)
+    inst = synth.Instance(f"tree{k}", n, Fo.kind, Fo.bound, Fo.weight, Fo.offsets, Fo.lits)
+    ctx = P.Context.from_instance(inst, precision=64, device=0)
+    assert ctx.info["n_tree_cons"] == 7 and ctx.info["tree_work"] > 0
+    for B, dist in ((5, "U"), (3, "N"), (2, "C"), (3, "Z")):
+        compare(inst, synth.points(dist, B, n, 300 + k + B), ctx=ctx)
+
+
+def test_product_tree_matches_root_path(monkeypatch):
+    """The same long constraints through the product tree and through the root-of-unity path (FFSAT_TREE=0): f and the
+    gradient agree to 1e-12 (both fp64), unsat identical; and the tree path is deterministic bit for bit."""
+    inst = synth.config3(0, n=3000, m3=300, n_card=6, kmin=400, kmax=1800)
+    X = torch.from_numpy(synth.points("U", 8, inst.n, 41, np.float64)).cuda()
+    ctx_t = P.Context.from_instance(inst, device=0)
+    assert ctx_t.info["n_tree_cons"] == 6
+    monkeypatch.setenv("FFSAT_TREE", "0")
+    ctx_r = P.Context.from_instance(inst, device=0)
+    assert ctx_r.info["n_tree_cons"] == 0
+    ft, gt, ut = ctx_t.eval(X, unsat=True)
+    fr, gr, ur = ctx_r.eval(X, unsat=True)
+    ft2, gt2, _ = ctx_t.eval(X, unsat=True)
+    torch.cuda.synchronize()
+    assert torch.max(torch.abs(ft - fr) / torch.clamp(torch.abs(fr), min=1)).item() <= 1e-12
+    assert torch.max(torch.abs(gt - gr) / torch.clamp(torch.abs(gr), min=1)).item() <= 1e-12
+    assert torch.equal(ut, ur)
+    assert torch.equal(ft, ft2) and torch.equal(gt, gt2)
+
+
 def test_long_xor_or_root_path():
     """Fast kinds longer than 64 go to the root path (general truth table incl. parity)."""
     cons = [(1, 0, 1.0, list(range(1, 101))), (0, 0, 2.0, [-v for v in range(20, 120)]),
