@@ -101,7 +101,7 @@ typedef struct {
     int64_t n_sym_cons;     /* constraints on the root-of-unity product path */
     int64_t n_fast_lits;
     int64_t n_sym_lits;
-    int64_t sym_root_lits;  /* sum over sym constraints of k * M', M' = floor((k+1)/2) */
+    int64_t sym_root_lits;  /* sum over root-of-unity-path sym constraints of k * M', M' = floor((k+1)/2) */
     int32_t path;           /* 1 tiled, 2 global */
     int32_t wide;           /* tiled path kernel: 0 = 32-point, 1 = 64-point (two points per lane) with the gradient tile
                                in shared memory, 2 = 64-point with the gradient tile in tensor memory (TMEM) */

@@ -466,7 +466,7 @@ Layout build_layout(const Formula& F, int path, int precision) {
             Lo.sym_words.push_back((uint32_t)((lit > 0 ? lit : -lit) - 1) | (lit < 0 ? 0x80000000u : 0u));
         }
         Lo.n_sym_lits += k;
-        Lo.sym_root_lits += (int64_t)k * ((k + 1) / 2);
+        if (!tree_path(k, precision)) Lo.sym_root_lits += (int64_t)k * ((k + 1) / 2);   // root-of-unity path only
         Lo.sym_off.push_back(Lo.n_sym_lits);
         int G, C;
         sgeom(k, &G, &C);

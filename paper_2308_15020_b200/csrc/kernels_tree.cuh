@@ -40,17 +40,21 @@ using tree::kTreePF;
 using tree::kTreeNR;
 using tree::kTreePad;
 using tree::TreeGeom;
-using tree::tree_nodes;
 using tree::tree_level_size;
 using tree::tree_geom;
-// first coefficient of node j at level l
-__device__ __forceinline__ int tree_node(const TreeGeom& g, int base, int l, int j) {
-    return base + kTreePad + j * ((kTreeLeaf << l) + 1 + kTreePad);
-}
-// number of real literals of node j at level l (its polynomial degree); <= 0 if the node does not exist
-__device__ __forceinline__ int tree_deg(const TreeGeom& g, int l, int j) {
-    const int D = kTreeLeaf << l;
-    return min(D, g.k - j * D);
+// node j of level l: first pair, pair end, degree (real literals; -1 for an empty level-1 slot), first coefficient
+// (relative to a level base)
+struct TreeNode {
+    int a, b, deg, pos;
+};
+__device__ __forceinline__ TreeNode tree_node(const TreeGeom& g, const short* hs, int l, int j) {
+    const int h = (1 << (g.Lv - l)) + j;
+    TreeNode nd;
+    nd.a = hs[h];
+    nd.b = (((h + 1) & h) == 0) ? g.nu : hs[h + 1];   // the last node of a level ends at nu
+    nd.deg = nd.b > nd.a ? min(g.k, 2 * kTreeLeaf * nd.b) - 2 * kTreeLeaf * nd.a : -1;
+    nd.pos = (j + 1) * kTreePad + 2 * kTreeLeaf * nd.a + j;
+    return nd;
 }
 
 // acc[r] += sum_{s = sa}^{sb - 1} A[s] W[t0 + r - s] (CONV) or A[s] W[t0 + r + s] (CORR), r = 0..R-1.  A is read as
@@ -143,6 +147,25 @@ __device__ __forceinline__ void tree_leaf_poly(const double* p, int skip, double
     }
 }
 
+// The two leaf-block polynomials of a level-1 node by the whole warp: half-warp hw (lanes 16 hw .. 16 hw + 15) forms
+// block `a + hw`'s 17 coefficients (lane t of the half holds q[t], its lane 15 also q[16]) with one shuffle per literal
+// (the same recurrence, q_t <- (1 - p_i) q_t + p_i q_{t-1}); an absent block (present = false) is the polynomial 1.
+// Written to out[hw * 17 + t].
+__device__ __forceinline__ void tree_leaf_pair(const double* p, bool present, double* out) {
+    const int lane = threadIdx.x & 31, t = lane & 15, hw = lane >> 4;
+    double q = t == 0 ? 1.0 : 0.0, q16 = 0.0;
+#pragma unroll
+    for (int i = 0; i < kTreeLeaf; ++i) {
+        const double pi = present ? p[i] : 0.0;
+        const double qm = __shfl_up_sync(0xffffffffu, q, 1, 16);
+        const double q15 = q;
+        q = fma(pi, t == 0 ? 0.0 : qm, (1.0 - pi) * q);
+        q16 = fma(pi, q15, (1.0 - pi) * q16);
+    }
+    out[hw * (kTreeLeaf + 1) + t] = q;
+    if (t == 15) out[hw * (kTreeLeaf + 1) + 16] = q16;
+}
+
 __device__ __forceinline__ double tree_f(int t, const SymSigDev& sg) { return rule_sat(t, sg.tmin, sg.tmax, sg.parity) ? -1.0 : 1.0; }
 
 // fixed-order CTA sums (warp butterflies, then the warps in order)
@@ -160,6 +183,7 @@ __device__ __forceinline__ double tree_block_sum(double v, double* red) {
 __global__ void __launch_bounds__(kTreeThreads, 1) sym_tree_kernel(SymArgs<double> a, int64_t s_begin, int64_t n_items, int32_t* counter) {
     extern __shared__ __align__(16) double sm[];
     __shared__ double s_red[kTreeThreads / 32];
+    __shared__ short s_hs[512];    // first pair of each tree node, heap order (root 1, children 2h, 2h + 1)
     __shared__ int s_item;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     for (;;) {
@@ -187,51 +211,64 @@ __global__ void __launch_bounds__(kTreeThreads, 1) sym_tree_kernel(SymArgs<doubl
             }
             p[i] = pi;
         }
-        __syncthreads();
-        if (tid == 0) sm[g.one + kTreePad] = 1.0;
-        // ---- bottom-up, level 1 (32 literals): warp per node, lanes 0 / 1 form the two leaf polynomials
-        double* tmp = sm + g.lamY;   // 16 warps x 34 doubles of scratch (the functional buffers are free until the root)
-        const int n1 = tree_nodes(k, 1);
-        for (int j = warp; j < n1; j += kTreeThreads / 32) {
-            double* tw = tmp + warp * 2 * (kTreeLeaf + 1);
-            if (lane < 2) {
-                double q[kTreeLeaf + 1];
-                tree_leaf_poly(p + 32 * j + 16 * lane, -1, q);
-#pragma unroll
-                for (int t = 0; t <= kTreeLeaf; ++t) tw[lane * (kTreeLeaf + 1) + t] = q[t];
+        // balanced node ranges, level by level from the root
+        if (tid == 0) {
+            s_hs[1] = 0;
+            sm[g.one + kTreePad] = 1.0;
+        }
+        for (int l = g.Lv; l >= 2; --l) {
+            __syncthreads();
+            const int h0 = 1 << (g.Lv - l);
+            for (int h = h0 + tid; h < 2 * h0; h += kTreeThreads) {
+                const int na = s_hs[h], nbb = (((h + 1) & h) == 0) ? g.nu : s_hs[h + 1];
+                s_hs[2 * h] = (short)na;
+                s_hs[2 * h + 1] = (short)(na + (nbb - na + 1) / 2);
             }
+        }
+        __syncthreads();
+        // ---- bottom-up, level 1 (two leaf blocks, the second possibly partial or empty): warp per node
+        double* tmp = sm + g.lamY;   // 16 warps x 34 doubles of scratch (the functional buffers are free until the root)
+        const int n1 = 1 << (g.Lv - 1);
+        for (int j = warp; j < n1; j += kTreeThreads / 32) {
+            const TreeNode nd = tree_node(g, s_hs, 1, j);
+            if (nd.deg < 0) continue;   // an empty slot (warp-uniform)
+            double* tw = tmp + warp * 2 * (kTreeLeaf + 1);
+            tree_leaf_pair(p + 2 * kTreeLeaf * nd.a + kTreeLeaf * (lane >> 4), true, tw);   // p is zero past k
             __syncwarp();
-            double* dst = sm + tree_node(g, g.off[1], 1, j);
-            const int d = tree_deg(g, 1, j);
-            for (int t = lane; t <= d; t += 32) {
+            double* dst = sm + g.off[1] + nd.pos;
+            for (int t = lane; t <= nd.deg; t += 32) {
                 double c = 0.0;
                 for (int u = max(0, t - kTreeLeaf); u <= min(kTreeLeaf, t); ++u) c = fma(tw[u], tw[kTreeLeaf + 1 + t - u], c);
                 dst[t] = c;
             }
             __syncwarp();
         }
-        // ---- bottom-up, levels 2..Lv: node j = child 2j * child 2j+1 (a missing right child is the polynomial 1)
+        // ---- bottom-up, levels 2..Lv: node j = child 2j * child 2j+1 (an empty right child is the polynomial 1)
         for (int l = 2; l <= g.Lv; ++l) {
             __syncthreads();
-            const int nl = tree_nodes(k, l), D = kTreeLeaf << l;
-            const int nbF = (D + 1 + kTreeR - 1) / kTreeR;
+            const int nl = 1 << (g.Lv - l);
+            const int maxdeg = 2 * kTreeLeaf * ((g.nu + nl - 1) / nl);
+            const int nbF = (maxdeg + 1 + kTreeR - 1) / kTreeR;
             const int units = nl * nbF;
             const int P = tree_shares(units);
             const int items = (units * P + 31) / 32 * 32;
             for (int w = tid; w < items; w += kTreeThreads) {
                 const int q = w / P, h = w - q * P;
                 const int j = q / nbF, t0 = (q - j * nbF) * kTreeR;
-                const bool ok = j < nl && t0 <= tree_deg(g, l, j);
-                int dA = 0, dB = 0, sa = 0, sb = 0;
+                TreeNode nd{0, 0, -1, 0}, cA{}, cB{};
+                if (j < nl) nd = tree_node(g, s_hs, l, j);
+                const bool ok = t0 <= nd.deg;
+                int sa = 0, sb = 0;
                 const double *A = sm, *W = sm;
                 if (ok) {
-                    dA = tree_deg(g, l - 1, 2 * j);
-                    const int dR = tree_deg(g, l - 1, 2 * j + 1);
-                    A = sm + tree_node(g, g.off[l - 1], l - 1, 2 * j);
-                    W = dR > 0 ? sm + tree_node(g, g.off[l - 1], l - 1, 2 * j + 1) : sm + g.one + kTreePad;
-                    dB = max(dR, 0);
-                    const int lo_s = max(0, t0 - dB), hi_s = min(dA, t0 + kTreeR - 1);
-                    const int per = (hi_s - lo_s + P) / P;
+                    cA = tree_node(g, s_hs, l - 1, 2 * j);
+                    cB = tree_node(g, s_hs, l - 1, 2 * j + 1);
+                    if (cB.deg < 0) cB.deg = 0;   // an empty right child (level 1 only): the polynomial 1
+                    A = sm + g.off[l - 1] + cA.pos;
+                    W = cB.b > cB.a ? sm + g.off[l - 1] + cB.pos : sm + g.one + kTreePad;
+                    const int lo_s = max(0, t0 - cB.deg), hi_s = min(cA.deg, t0 + kTreeR - 1);
+                    int per = (hi_s - lo_s + P) / P;
+                    per += P > 1 ? 1 - (per & 1) : 0;   // odd: the P shares' broadcast reads fall in distinct banks
                     sa = min(hi_s + 1, lo_s + h * per);
                     sb = min(hi_s + 1, sa + per);
                 }
@@ -241,52 +278,54 @@ __global__ void __launch_bounds__(kTreeThreads, 1) sym_tree_kernel(SymArgs<doubl
                 if (sa < sb) tree_unit<true>(A, W, t0, sa, sb, acc);
                 tree_combine(acc, P);
                 if (ok && h == 0) {
-                    double* dst = sm + tree_node(g, g.off[l], l, j);
-                    const int d = tree_deg(g, l, j);
+                    double* dst = sm + g.off[l] + nd.pos;
 #pragma unroll
                     for (int r = 0; r < kTreeR; ++r)
-                        if (t0 + r <= d) dst[t0 + r] = acc[r];
+                        if (t0 + r <= nd.deg) dst[t0 + r] = acc[r];
                 }
             }
         }
         __syncthreads();
         // ---- root: lambda = f, FE = sum_t f(t) P_root[t]
-        const double* Proot = sm + tree_node(g, g.off[g.Lv], g.Lv, 0);
-        double* lam = sm + g.lamX;   // level Lv functional (node 0 at the level layout)
+        const double* Proot = sm + g.off[g.Lv] + kTreePad;
+        double* lam = sm + g.lamX + kTreePad;
         double fe = 0.0;
         for (int t = tid; t <= k; t += kTreeThreads) {
             const double ft = tree_f(t, sg);
             fe = fma(ft, Proot[t], fe);
-            lam[kTreePad + t] = ft;
+            lam[t] = ft;
         }
         fe = tree_block_sum(fe, s_red);
         // ---- top-down, levels Lv..2 -> 1: lambda_L = corr(lambda_S, P_R), lambda_R = corr(lambda_S, P_L)
         int cur = g.lamX, nxt = g.lamY;
         for (int l = g.Lv; l >= 2; --l) {
-            // the next buffer: zero it (its guards are read by the windows of the next level), except on the first
-            // pass where it still holds the level-1 scratch (already consumed)
+            // the next buffer is zeroed first (its guards are read by the next level's windows; on the first pass it
+            // still holds the consumed level-1 scratch)
             for (int i = tid; i < g.lamSize; i += kTreeThreads) sm[nxt + i] = 0.0;
             __syncthreads();
-            const int nl = tree_nodes(k, l), Dc = kTreeLeaf << (l - 1);
-            const int nbF = (Dc + 1 + kTreeR - 1) / kTreeR;
+            const int nl = 1 << (g.Lv - l);
+            const int maxdeg = 2 * kTreeLeaf * ((g.nu + 2 * nl - 1) / (2 * nl));   // of a child
+            const int nbF = (maxdeg + 1 + kTreeR - 1) / kTreeR;
             const int units = nl * 2 * nbF;
             const int P = tree_shares(units);
             const int items = (units * P + 31) / 32 * 32;
-            // level l functional of node j starts at the same offset as the level-l node layout, relative to cur
             for (int w = tid; w < items; w += kTreeThreads) {
                 const int q = w / P, h = w - q * P;
                 const int j = q / (2 * nbF), rq = q - j * 2 * nbF, side = rq / nbF, t0 = (rq - side * nbF) * kTreeR;
                 const int child = 2 * j + side;
-                bool ok = j < nl && t0 <= tree_deg(g, l - 1, child);
+                TreeNode cd{0, 0, -1, 0}, sib{}, par{};
+                if (j < nl) cd = tree_node(g, s_hs, l - 1, child);
+                const bool ok = t0 <= cd.deg;
                 int sa = 0, sb = 0;
                 const double *A = sm, *W = sm;
                 if (ok) {
-                    const int sib = 2 * j + 1 - side;
-                    const int dS = tree_deg(g, l - 1, sib);
-                    A = dS > 0 ? sm + tree_node(g, g.off[l - 1], l - 1, sib) : sm + g.one + kTreePad;
-                    W = sm + cur + kTreePad + j * ((kTreeLeaf << l) + 1 + kTreePad);
-                    const int hi_s = max(dS, 0);
-                    const int per = (hi_s + P) / P;
+                    sib = tree_node(g, s_hs, l - 1, 2 * j + 1 - side);
+                    par = tree_node(g, s_hs, l, j);
+                    A = sib.deg >= 0 ? sm + g.off[l - 1] + sib.pos : sm + g.one + kTreePad;   // empty sibling: 1
+                    W = sm + cur + par.pos;
+                    const int hi_s = max(sib.deg, 0);
+                    int per = (hi_s + P) / P;
+                    per += P > 1 ? 1 - (per & 1) : 0;
                     sa = min(hi_s + 1, h * per);
                     sb = min(hi_s + 1, sa + per);
                 }
@@ -296,11 +335,10 @@ __global__ void __launch_bounds__(kTreeThreads, 1) sym_tree_kernel(SymArgs<doubl
                 if (sa < sb) tree_unit<false>(A, W, t0, sa, sb, acc);
                 tree_combine(acc, P);
                 if (ok && h == 0) {
-                    double* dst = sm + nxt + kTreePad + child * (Dc + 1 + kTreePad);
-                    const int d = tree_deg(g, l - 1, child);
+                    double* dst = sm + nxt + cd.pos;
 #pragma unroll
                     for (int r = 0; r < kTreeR; ++r)
-                        if (t0 + r <= d) dst[t0 + r] = acc[r];
+                        if (t0 + r <= cd.deg) dst[t0 + r] = acc[r];
                 }
             }
             __syncthreads();
@@ -308,17 +346,14 @@ __global__ void __launch_bounds__(kTreeThreads, 1) sym_tree_kernel(SymArgs<doubl
             cur = nxt;
             nxt = tsw;
         }
-        // ---- leaves: warp per level-1 node (lambda at cur), lane = literal 32 j + lane
+        // ---- leaves: warp per level-1 node (lambda at cur), lane = literal 32 a + lane of its two blocks
         const double wc = a.w_sym[s];
         for (int j = warp; j < n1; j += kTreeThreads / 32) {
-            const double* lam1 = sm + cur + kTreePad + j * (32 + 1 + kTreePad);
-            double* tw = sm + nxt + warp * 4 * (kTreeLeaf + 1);   // P_L, P_R, then delta_L, delta_R
-            if (lane < 2) {
-                double q[kTreeLeaf + 1];
-                tree_leaf_poly(p + 32 * j + 16 * lane, -1, q);
-#pragma unroll
-                for (int t = 0; t <= kTreeLeaf; ++t) tw[lane * (kTreeLeaf + 1) + t] = q[t];
-            }
+            const TreeNode nd = tree_node(g, s_hs, 1, j);
+            if (nd.deg < 0) continue;   // an empty slot (warp-uniform)
+            const double* lam1 = sm + cur + nd.pos;
+            double* tw = sm + nxt + warp * 4 * (kTreeLeaf + 1);   // P_L, P_R, then lambda_L, lambda_R
+            tree_leaf_pair(p + 2 * kTreeLeaf * nd.a + kTreeLeaf * (lane >> 4), true, tw);
             __syncwarp();
             // lambda_L[t] = sum_s lam1[t + s] P_R[s], lambda_R[t] = sum_s lam1[t + s] P_L[s], t = 0..16
             if (lane <= kTreeLeaf) {
@@ -331,15 +366,15 @@ __global__ void __launch_bounds__(kTreeThreads, 1) sym_tree_kernel(SymArgs<doubl
                 tw[3 * (kTreeLeaf + 1) + lane] = vr;
             }
             __syncwarp();
-            const int i = 32 * j + lane;
             const int blk = lane >> 4;
-            double qi[kTreeLeaf + 1];
-            tree_leaf_poly(p + 32 * j + 16 * blk, lane & 15, qi);
-            const double* lb = tw + (2 + blk) * (kTreeLeaf + 1);
-            double dp = 0.0;   // dFE/dp_i = sum_s (lambda[s + 1] - lambda[s]) Q_i[s]
-#pragma unroll
-            for (int u = 0; u < kTreeLeaf; ++u) dp = fma(lb[u + 1] - lb[u], qi[u], dp);
+            const int i = 2 * kTreeLeaf * nd.a + lane;
             if (i < k) {
+                double qi[kTreeLeaf + 1];
+                tree_leaf_poly(p + 2 * kTreeLeaf * nd.a + kTreeLeaf * blk, lane & 15, qi);
+                const double* lb = tw + (2 + blk) * (kTreeLeaf + 1);
+                double dp = 0.0;   // dFE/dp_i = sum_s (lambda[s + 1] - lambda[s]) Q_i[s]
+#pragma unroll
+                for (int u = 0; u < kTreeLeaf; ++u) dp = fma(lb[u + 1] - lb[u], qi[u], dp);
                 const uint32_t w = __ldg(a.words + lo + i);
                 const double v = wc * (-0.5 * dp);   // dFE/dl_i = -dFE/dp_i / 2
                 a.Tb[(a.tb_fast + lo + i) * a.B + b] = (int)w < 0 ? -v : v;

@@ -17,31 +17,35 @@ constexpr int kTreeR = 9;        // outputs per work unit
 constexpr int kTreePF = 3;       // window elements loaded ahead
 constexpr int kTreeNR = kTreeR + kTreePF;
 constexpr int kTreePad = 16;     // zero guard before / after every node (>= kTreeR + kTreePF)
-constexpr size_t kTreeSmemMax = 226 * 1024;   // dynamic shared memory of one tree CTA (227 KB minus the static part)
+constexpr size_t kTreeSmemMax = 224 * 1024;   // dynamic shared memory of one tree CTA (227 KB minus the static part, 2.2 KB)
 
-// Shared-memory layout of one item (doubles), a function of k only (host: tree_smem_doubles mirrors it).
+// Shared-memory layout of one item (doubles), a function of k only.  Level-1 nodes are pairs of 16-literal leaf blocks
+// (32 literals, the last one partial); above them the tree is BALANCED over the nu = ceil(k / 32) pairs: a node
+// covering pairs [a, b) splits at a + ceil((b - a) / 2), so siblings differ by at most one pair (uniform work per
+// level).  Level l (1..Lv, Lv = 1 + ceil(log2 nu)) has 2^(Lv - l) node slots; every node above level 1 holds >= 1
+// pair, a level-1 slot holds 1 or 0 (an empty right child).  Node j of level l is stored compactly: its deg + 1
+// coefficients at off[l] + (j + 1) kTreePad + 32 start_j + j, zero guards between.
 struct TreeGeom {
-    int k, kp, Lv;               // kp = k rounded up to 32; levels 1..Lv (level l node = 16 << l literals)
-    int off[12];                 // level l polynomial region (l = 1..Lv); off[0] = the p array
+    int k, kp, nu, Lv;           // kp = 32 nu (the p array, zero past k)
+    int off[12];                 // level l polynomial region (l = 1..Lv)
     int lamX, lamY, lamSize;     // the two functional buffers (each sized for the largest level)
     int one;                     // the constant polynomial 1 surrounded by zeros
     int total;
 };
 
-FFSAT_HD inline int tree_nodes(int k, int l) { const int D = kTreeLeaf << l; return (k + D - 1) / D; }
 FFSAT_HD inline int tree_level_size(int k, int l, int Lv) {
-    const int D = kTreeLeaf << l;
-    return l == Lv ? 2 * kTreePad + k + 1 : kTreePad + tree_nodes(k, l) * (D + 1 + kTreePad);
+    const int nl = 1 << (Lv - l);
+    return (nl + 1) * kTreePad + k + nl;
 }
 FFSAT_HD inline TreeGeom tree_geom(int k) {
     TreeGeom g{};
     g.k = k;
-    g.kp = (k + 31) / 32 * 32;
+    g.nu = (k + 2 * kTreeLeaf - 1) / (2 * kTreeLeaf);
+    g.kp = 2 * kTreeLeaf * g.nu;
     int Lv = 1;
-    while (tree_nodes(k, Lv) > 1) ++Lv;
+    while ((1 << (Lv - 1)) < g.nu) ++Lv;
     g.Lv = Lv;
     int o = g.kp;
-    g.off[0] = 0;
     for (int l = 1; l <= Lv; ++l) {
         g.off[l] = o;
         o += tree_level_size(k, l, Lv);
@@ -61,19 +65,27 @@ FFSAT_HD inline TreeGeom tree_geom(int k) {
 // real degrees, plus the level-1 / leaf stage.
 inline int64_t tree_fp64_work(int k) {
     const TreeGeom g = tree_geom(k);
-    auto deg = [&](int l, int j) { const int D = kTreeLeaf << l; const int d = k - j * D; return d < D ? d : D; };
+    // node pair ranges, heap order (root 1, children 2h, 2h + 1), as the kernel builds them
+    int64_t start[1 << 10], endb[1 << 10];
+    start[1] = 0;
+    endb[1] = g.nu;
+    for (int h = 1; h < (1 << (g.Lv - 1)); ++h) {
+        const int64_t a = start[h], b = endb[h];
+        start[2 * h] = a;
+        endb[2 * h] = a + (b - a + 1) / 2;
+        start[2 * h + 1] = endb[2 * h];
+        endb[2 * h + 1] = b;
+    }
+    auto deg = [&](int h) { const int64_t e = endb[h] * 2 * kTreeLeaf < k ? endb[h] * 2 * kTreeLeaf : k; const int64_t d = e - start[h] * 2 * kTreeLeaf; return d > 0 ? d : 0; };
     int64_t w = 0;
-    const int n1 = tree_nodes(k, 1);
     // per level-1 node: the two leaf recurrences twice (bottom-up and leaf stage; 136 updates of 2 slots each), the
     // 17 x 17 product, the two 17 x 17 leaf functionals; per literal: its leave-one-out recurrence and 16-term dot
-    w += (int64_t)n1 * (4 * 2 * 136 + 17 * 17 + 2 * 17 * 17);
+    w += (int64_t)g.nu * (4 * 2 * 136 + 17 * 17 + 2 * 17 * 17);
     w += (int64_t)k * (2 * 136 + 2 * 16);
-    for (int l = 2; l <= g.Lv; ++l)
-        for (int j = 0; j < tree_nodes(k, l); ++j) {
-            const int dA = deg(l - 1, 2 * j), dB = deg(l - 1, 2 * j + 1);
-            if (dB <= 0) continue;
-            w += (int64_t)(dA + 1) * (dB + 1) * 3;   // bottom-up product + the two top-down correlations
-        }
+    for (int h = 1; h < (1 << (g.Lv - 1)); ++h) {   // nodes of levels 2..Lv
+        const int64_t dA = deg(2 * h), dB = deg(2 * h + 1);
+        if (dB > 0) w += (dA + 1) * (dB + 1) * 3;   // bottom-up product + the two top-down correlations
+    }
     return w;
 }
 

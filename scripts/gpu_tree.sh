@@ -20,5 +20,7 @@ PY
 if [ -n "$3" ]; then
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:sym_tree_kernel -s 2 -c 1 -o gpurun_out/prof_tree -f python bench.py --config c3 --steps 3 --warmup 1 --no-cpu-baseline > gpurun_out/ncu_tree.log 2>&1; echo ncu=$?
   python scripts/ncu_summary.py gpurun_out/prof_tree.ncu-rep > gpurun_out/ncu_tree_summary.txt 2>&1; head -60 gpurun_out/ncu_tree_summary.txt
+  ncu -i gpurun_out/prof_tree.ncu-rep --page source --csv --print-source cuda > gpurun_out/prof_tree_cuda.csv 2>/dev/null
+  ncu -i gpurun_out/prof_tree.ncu-rep --page source --csv --print-source sass > gpurun_out/prof_tree_sass.csv 2>/dev/null
   rm -f gpurun_out/prof_tree.ncu-rep
 fi
