@@ -105,14 +105,14 @@ __device__ __forceinline__ void tree_unit(const double* A, const double* W, int 
     }
 }
 
-// inner-index shares per unit: the smallest count that gives the CTA's threads work
-__device__ __forceinline__ int tree_shares(int units) {
+// inner-index shares per unit: the count that keeps nt threads busiest
+__device__ __forceinline__ int tree_shares(int units, int nt) {
     int best = 1;
     double be = 0.0;
     for (int P = 1; P <= 8; P *= 2) {
         const int items = units * P;
-        const int rounds = (items + kTreeThreads - 1) / kTreeThreads;
-        const double eff = (double)items / ((double)rounds * kTreeThreads);
+        const int rounds = (items + nt - 1) / nt;
+        const double eff = (double)items / ((double)rounds * nt);
         if (eff > be + 0.02) {
             be = eff;
             best = P;
@@ -180,12 +180,157 @@ __device__ __forceinline__ double tree_block_sum(double v, double* red) {
     return t;
 }
 
-__global__ void __launch_bounds__(kTreeThreads, 1) sym_tree_kernel(SymArgs<double> a, int64_t s_begin, int64_t n_items, int32_t* counter) {
+// Bottom-up level l >= 2: the polynomials of nodes [j0, j1) from their children, by threads ti of nt (nt a multiple of
+// 32; whole warps take part: the share sums use shuffles).  Units of kTreeR outputs x P inner-index shares.
+__device__ __forceinline__ void tree_up_level(const TreeGeom& g, const short* hs, double* sm, int l, int j0, int j1, int ti, int nt) {
+    const int nl = j1 - j0;
+    const int maxdeg = 2 * kTreeLeaf * ((g.nu + (1 << (g.Lv - l)) - 1) >> (g.Lv - l));
+    const int nbF = (maxdeg + 1 + kTreeR - 1) / kTreeR;
+    const int units = nl * nbF;
+    const int P = tree_shares(units, nt);
+    const int items = (units * P + 31) / 32 * 32;
+    for (int w = ti; w < items; w += nt) {
+        const int q = w / P, h = w - q * P;
+        const int jr = q / nbF, t0 = (q - jr * nbF) * kTreeR, j = j0 + jr;
+        TreeNode nd{0, 0, -1, 0};
+        if (jr < nl) nd = tree_node(g, hs, l, j);
+        const bool ok = t0 <= nd.deg;
+        int sa = 0, sb = 0;
+        const double *A = sm, *W = sm;
+        if (ok) {
+            const TreeNode cA = tree_node(g, hs, l - 1, 2 * j);
+            TreeNode cB = tree_node(g, hs, l - 1, 2 * j + 1);
+            if (cB.deg < 0) cB.deg = 0;   // an empty right child (level 1 only): the polynomial 1
+            A = sm + g.off[l - 1] + cA.pos;
+            W = cB.b > cB.a ? sm + g.off[l - 1] + cB.pos : sm + g.one + kTreePad;
+            const int lo_s = max(0, t0 - cB.deg), hi_s = min(cA.deg, t0 + kTreeR - 1);
+            int per = (hi_s - lo_s + P) / P;
+            per += P > 1 ? 1 - (per & 1) : 0;   // odd: the P shares' broadcast reads fall in distinct banks
+            sa = min(hi_s + 1, lo_s + h * per);
+            sb = min(hi_s + 1, sa + per);
+        }
+        double acc[kTreeR];
+#pragma unroll
+        for (int r = 0; r < kTreeR; ++r) acc[r] = 0.0;
+        if (sa < sb) tree_unit<true>(A, W, t0, sa, sb, acc);
+        tree_combine(acc, P);
+        if (ok && h == 0) {
+            double* dst = sm + g.off[l] + nd.pos;
+#pragma unroll
+            for (int r = 0; r < kTreeR; ++r)
+                if (t0 + r <= nd.deg) dst[t0 + r] = acc[r];
+        }
+    }
+}
+
+// Top-down from level l >= 2: the functionals of the children of nodes [j0, j1) (parents in buffer cur, children into
+// nxt): lambda_L = corr(lambda_S, P_R), lambda_R = corr(lambda_S, P_L).  Reads past a parent's end only feed outputs
+// past the child's degree, which are not stored (the buffers hold finite values: zeroed at kernel start).
+__device__ __forceinline__ void tree_down_level(const TreeGeom& g, const short* hs, double* sm, int l, int j0, int j1, int cur, int nxt,
+                                                int ti, int nt) {
+    const int nl = j1 - j0;
+    const int maxdeg = 2 * kTreeLeaf * ((g.nu + (2 << (g.Lv - l)) - 1) >> (g.Lv - l + 1));   // of a child
+    const int nbF = (maxdeg + 1 + kTreeR - 1) / kTreeR;
+    const int units = nl * 2 * nbF;
+    const int P = tree_shares(units, nt);
+    const int items = (units * P + 31) / 32 * 32;
+    for (int w = ti; w < items; w += nt) {
+        const int q = w / P, h = w - q * P;
+        const int jr = q / (2 * nbF), rq = q - jr * 2 * nbF, side = rq / nbF, t0 = (rq - side * nbF) * kTreeR;
+        const int j = j0 + jr, child = 2 * j + side;
+        TreeNode cd{0, 0, -1, 0};
+        if (jr < nl) cd = tree_node(g, hs, l - 1, child);
+        const bool ok = t0 <= cd.deg;
+        int sa = 0, sb = 0;
+        const double *A = sm, *W = sm;
+        if (ok) {
+            const TreeNode sib = tree_node(g, hs, l - 1, 2 * j + 1 - side);
+            const TreeNode par = tree_node(g, hs, l, j);
+            A = sib.deg >= 0 ? sm + g.off[l - 1] + sib.pos : sm + g.one + kTreePad;   // empty sibling: 1
+            W = sm + cur + par.pos;
+            const int hi_s = max(sib.deg, 0);
+            int per = (hi_s + P) / P;
+            per += P > 1 ? 1 - (per & 1) : 0;
+            sa = min(hi_s + 1, h * per);
+            sb = min(hi_s + 1, sa + per);
+        }
+        double acc[kTreeR];
+#pragma unroll
+        for (int r = 0; r < kTreeR; ++r) acc[r] = 0.0;
+        if (sa < sb) tree_unit<false>(A, W, t0, sa, sb, acc);
+        tree_combine(acc, P);
+        if (ok && h == 0) {
+            double* dst = sm + nxt + cd.pos;
+#pragma unroll
+            for (int r = 0; r < kTreeR; ++r)
+                if (t0 + r <= cd.deg) dst[t0 + r] = acc[r];
+        }
+    }
+}
+
+// Level-1 node j (one warp): its polynomial = (block 0 poly) * (block 1 poly) of its 32 literals (p is zero past k).
+__device__ __forceinline__ void tree_leaf_up(const TreeGeom& g, const short* hs, double* sm, const double* p, int j, double* tw) {
+    const int lane = threadIdx.x & 31;
+    const TreeNode nd = tree_node(g, hs, 1, j);
+    if (nd.deg < 0) return;   // an empty slot (warp-uniform)
+    tree_leaf_pair(p + 2 * kTreeLeaf * nd.a + kTreeLeaf * (lane >> 4), true, tw);
+    __syncwarp();
+    double* dst = sm + g.off[1] + nd.pos;
+    for (int t = lane; t <= nd.deg; t += 32) {
+        double c = 0.0;
+        for (int u = max(0, t - kTreeLeaf); u <= min(kTreeLeaf, t); ++u) c = fma(tw[u], tw[kTreeLeaf + 1 + t - u], c);
+        dst[t] = c;
+    }
+    __syncwarp();
+}
+
+// Leaf stage of level-1 node j (one warp, lane = literal 32 a + lane): the two block functionals from the node's
+// functional (at lam), then per literal dFE/dp_i = sum_s (lambda[s + 1] - lambda[s]) Q_i[s]; terms into Tb.
+__device__ __forceinline__ void tree_leaf_down(const TreeGeom& g, const short* hs, const double* lamb, const double* p, int j,
+                                               double* tw, const SymArgs<double>& a, int64_t lo, int64_t b, double wc) {
+    const int lane = threadIdx.x & 31;
+    const TreeNode nd = tree_node(g, hs, 1, j);
+    if (nd.deg < 0) return;
+    const double* lam1 = lamb + nd.pos;
+    tree_leaf_pair(p + 2 * kTreeLeaf * nd.a + kTreeLeaf * (lane >> 4), true, tw);   // P_L, P_R
+    __syncwarp();
+    // lambda_L[t] = sum_s lam1[t + s] P_R[s], lambda_R[t] = sum_s lam1[t + s] P_L[s], t = 0..16
+    if (lane <= kTreeLeaf) {
+        double vl = 0.0, vr = 0.0;
+        for (int u = 0; u <= kTreeLeaf; ++u) {
+            vl = fma(lam1[lane + u], tw[kTreeLeaf + 1 + u], vl);
+            vr = fma(lam1[lane + u], tw[u], vr);
+        }
+        tw[2 * (kTreeLeaf + 1) + lane] = vl;
+        tw[3 * (kTreeLeaf + 1) + lane] = vr;
+    }
+    __syncwarp();
+    const int blk = lane >> 4;
+    const int i = 2 * kTreeLeaf * nd.a + lane;
+    if (i < g.k) {
+        double qi[kTreeLeaf + 1];
+        tree_leaf_poly(p + 2 * kTreeLeaf * nd.a + kTreeLeaf * blk, lane & 15, qi);
+        const double* lb = tw + (2 + blk) * (kTreeLeaf + 1);
+        double dp = 0.0;
+#pragma unroll
+        for (int u = 0; u < kTreeLeaf; ++u) dp = fma(lb[u + 1] - lb[u], qi[u], dp);
+        const uint32_t w = __ldg(a.words + lo + i);
+        const double v = wc * (-0.5 * dp);   // dFE/dl_i = -dFE/dp_i / 2
+        a.Tb[(a.tb_fast + lo + i) * a.B + b] = (int)w < 0 ? -v : v;
+    }
+    __syncwarp();
+}
+
+__global__ void __launch_bounds__(kTreeThreads, 1) sym_tree_kernel(SymArgs<double> a, int64_t s_begin, int64_t n_items, int32_t* counter,
+                                                                    int32_t smem_doubles) {
     extern __shared__ __align__(16) double sm[];
     __shared__ double s_red[kTreeThreads / 32];
     __shared__ short s_hs[512];    // first pair of each tree node, heap order (root 1, children 2h, 2h + 1)
     __shared__ int s_item;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    constexpr int NW = kTreeThreads / 32;
+    // every buffer starts finite (the functional buffers are never re-zeroed: see tree_down_level)
+    for (int i = tid; i < smem_doubles; i += kTreeThreads) sm[i] = 0.0;
     for (;;) {
         if (tid == 0) s_item = atomicAdd(counter, 1);
         __syncthreads();
@@ -196,8 +341,9 @@ __global__ void __launch_bounds__(kTreeThreads, 1) sym_tree_kernel(SymArgs<doubl
         const TreeGeom g = tree_geom(sg.k);
         const int k = g.k;
         const int64_t lo = a.off[s];
-        // zero everything past p (the guards and the unused tails must read as 0), then p_i = (1 - l_i) / 2
-        for (int i = g.kp + tid; i < g.total; i += kTreeThreads) sm[i] = 0.0;
+        // the polynomial levels (guards and unused tails must read as 0), the constant 1; then p_i = (1 - l_i) / 2
+        for (int i = g.kp + tid; i < g.lamX; i += kTreeThreads) sm[i] = 0.0;
+        for (int i = g.one + tid; i < g.scr; i += kTreeThreads) sm[i] = 0.0;
         double* p = sm;
         int tc = 0;
         for (int i = tid; i < g.kp; i += kTreeThreads) {
@@ -211,79 +357,35 @@ __global__ void __launch_bounds__(kTreeThreads, 1) sym_tree_kernel(SymArgs<doubl
             }
             p[i] = pi;
         }
-        // balanced node ranges, level by level from the root
-        if (tid == 0) {
-            s_hs[1] = 0;
-            sm[g.one + kTreePad] = 1.0;
-        }
-        for (int l = g.Lv; l >= 2; --l) {
-            __syncthreads();
-            const int h0 = 1 << (g.Lv - l);
-            for (int h = h0 + tid; h < 2 * h0; h += kTreeThreads) {
-                const int na = s_hs[h], nbb = (((h + 1) & h) == 0) ? g.nu : s_hs[h + 1];
-                s_hs[2 * h] = (short)na;
-                s_hs[2 * h + 1] = (short)(na + (nbb - na + 1) / 2);
+        // balanced node ranges, level by level from the root (one warp)
+        if (warp == 0) {
+            if (lane == 0) s_hs[1] = 0;
+            for (int l = g.Lv; l >= 2; --l) {
+                __syncwarp();
+                const int h0 = 1 << (g.Lv - l);
+                for (int h = h0 + lane; h < 2 * h0; h += 32) {
+                    const int na = s_hs[h], nbb = (((h + 1) & h) == 0) ? g.nu : s_hs[h + 1];
+                    s_hs[2 * h] = (short)na;
+                    s_hs[2 * h + 1] = (short)(na + (nbb - na + 1) / 2);
+                }
             }
         }
         __syncthreads();
-        // ---- bottom-up, level 1 (two leaf blocks, the second possibly partial or empty): warp per node
-        double* tmp = sm + g.lamY;   // 16 warps x 34 doubles of scratch (the functional buffers are free until the root)
-        const int n1 = 1 << (g.Lv - 1);
-        for (int j = warp; j < n1; j += kTreeThreads / 32) {
-            const TreeNode nd = tree_node(g, s_hs, 1, j);
-            if (nd.deg < 0) continue;   // an empty slot (warp-uniform)
-            double* tw = tmp + warp * 2 * (kTreeLeaf + 1);
-            tree_leaf_pair(p + 2 * kTreeLeaf * nd.a + kTreeLeaf * (lane >> 4), true, tw);   // p is zero past k
-            __syncwarp();
-            double* dst = sm + g.off[1] + nd.pos;
-            for (int t = lane; t <= nd.deg; t += 32) {
-                double c = 0.0;
-                for (int u = max(0, t - kTreeLeaf); u <= min(kTreeLeaf, t); ++u) c = fma(tw[u], tw[kTreeLeaf + 1 + t - u], c);
-                dst[t] = c;
+        if (tid == 0) sm[g.one + kTreePad] = 1.0;   // (ordered after the zeroing above; read after the next barrier)
+        // warp-local subtrees: rooted at level lw = Lv - 4 (16 of them, one per warp), or at level 1 for small trees
+        const int lw = max(1, g.Lv - 4), nsub = 1 << (g.Lv - lw), w1 = 1 << (lw - 1);
+        double* tw = sm + g.scr + warp * 4 * (kTreeLeaf + 1);
+        // ---- bottom-up: levels 1..lw per warp, then lw+1..Lv by the CTA
+        for (int r = warp; r < nsub; r += NW) {
+            for (int j = r * w1; j < (r + 1) * w1; ++j) tree_leaf_up(g, s_hs, sm, p, j, tw);
+            for (int l = 2; l <= lw; ++l) {
+                tree_up_level(g, s_hs, sm, l, r << (lw - l), (r + 1) << (lw - l), lane, 32);
+                __syncwarp();
             }
-            __syncwarp();
         }
-        // ---- bottom-up, levels 2..Lv: node j = child 2j * child 2j+1 (an empty right child is the polynomial 1)
-        for (int l = 2; l <= g.Lv; ++l) {
+        for (int l = lw + 1; l <= g.Lv; ++l) {
             __syncthreads();
-            const int nl = 1 << (g.Lv - l);
-            const int maxdeg = 2 * kTreeLeaf * ((g.nu + nl - 1) / nl);
-            const int nbF = (maxdeg + 1 + kTreeR - 1) / kTreeR;
-            const int units = nl * nbF;
-            const int P = tree_shares(units);
-            const int items = (units * P + 31) / 32 * 32;
-            for (int w = tid; w < items; w += kTreeThreads) {
-                const int q = w / P, h = w - q * P;
-                const int j = q / nbF, t0 = (q - j * nbF) * kTreeR;
-                TreeNode nd{0, 0, -1, 0}, cA{}, cB{};
-                if (j < nl) nd = tree_node(g, s_hs, l, j);
-                const bool ok = t0 <= nd.deg;
-                int sa = 0, sb = 0;
-                const double *A = sm, *W = sm;
-                if (ok) {
-                    cA = tree_node(g, s_hs, l - 1, 2 * j);
-                    cB = tree_node(g, s_hs, l - 1, 2 * j + 1);
-                    if (cB.deg < 0) cB.deg = 0;   // an empty right child (level 1 only): the polynomial 1
-                    A = sm + g.off[l - 1] + cA.pos;
-                    W = cB.b > cB.a ? sm + g.off[l - 1] + cB.pos : sm + g.one + kTreePad;
-                    const int lo_s = max(0, t0 - cB.deg), hi_s = min(cA.deg, t0 + kTreeR - 1);
-                    int per = (hi_s - lo_s + P) / P;
-                    per += P > 1 ? 1 - (per & 1) : 0;   // odd: the P shares' broadcast reads fall in distinct banks
-                    sa = min(hi_s + 1, lo_s + h * per);
-                    sb = min(hi_s + 1, sa + per);
-                }
-                double acc[kTreeR];
-#pragma unroll
-                for (int r = 0; r < kTreeR; ++r) acc[r] = 0.0;
-                if (sa < sb) tree_unit<true>(A, W, t0, sa, sb, acc);
-                tree_combine(acc, P);
-                if (ok && h == 0) {
-                    double* dst = sm + g.off[l] + nd.pos;
-#pragma unroll
-                    for (int r = 0; r < kTreeR; ++r)
-                        if (t0 + r <= nd.deg) dst[t0 + r] = acc[r];
-                }
-            }
+            tree_up_level(g, s_hs, sm, l, 0, 1 << (g.Lv - l), tid, kTreeThreads);
         }
         __syncthreads();
         // ---- root: lambda = f, FE = sum_t f(t) P_root[t]
@@ -295,91 +397,27 @@ __global__ void __launch_bounds__(kTreeThreads, 1) sym_tree_kernel(SymArgs<doubl
             fe = fma(ft, Proot[t], fe);
             lam[t] = ft;
         }
-        fe = tree_block_sum(fe, s_red);
-        // ---- top-down, levels Lv..2 -> 1: lambda_L = corr(lambda_S, P_R), lambda_R = corr(lambda_S, P_L)
+        fe = tree_block_sum(fe, s_red);   // (its barriers also publish lambda_root)
+        // ---- top-down: levels Lv..lw+1 by the CTA, then lw..2 and the leaves per warp
         int cur = g.lamX, nxt = g.lamY;
-        for (int l = g.Lv; l >= 2; --l) {
-            // the next buffer is zeroed first (its guards are read by the next level's windows; on the first pass it
-            // still holds the consumed level-1 scratch)
-            for (int i = tid; i < g.lamSize; i += kTreeThreads) sm[nxt + i] = 0.0;
-            __syncthreads();
-            const int nl = 1 << (g.Lv - l);
-            const int maxdeg = 2 * kTreeLeaf * ((g.nu + 2 * nl - 1) / (2 * nl));   // of a child
-            const int nbF = (maxdeg + 1 + kTreeR - 1) / kTreeR;
-            const int units = nl * 2 * nbF;
-            const int P = tree_shares(units);
-            const int items = (units * P + 31) / 32 * 32;
-            for (int w = tid; w < items; w += kTreeThreads) {
-                const int q = w / P, h = w - q * P;
-                const int j = q / (2 * nbF), rq = q - j * 2 * nbF, side = rq / nbF, t0 = (rq - side * nbF) * kTreeR;
-                const int child = 2 * j + side;
-                TreeNode cd{0, 0, -1, 0}, sib{}, par{};
-                if (j < nl) cd = tree_node(g, s_hs, l - 1, child);
-                const bool ok = t0 <= cd.deg;
-                int sa = 0, sb = 0;
-                const double *A = sm, *W = sm;
-                if (ok) {
-                    sib = tree_node(g, s_hs, l - 1, 2 * j + 1 - side);
-                    par = tree_node(g, s_hs, l, j);
-                    A = sib.deg >= 0 ? sm + g.off[l - 1] + sib.pos : sm + g.one + kTreePad;   // empty sibling: 1
-                    W = sm + cur + par.pos;
-                    const int hi_s = max(sib.deg, 0);
-                    int per = (hi_s + P) / P;
-                    per += P > 1 ? 1 - (per & 1) : 0;
-                    sa = min(hi_s + 1, h * per);
-                    sb = min(hi_s + 1, sa + per);
-                }
-                double acc[kTreeR];
-#pragma unroll
-                for (int r = 0; r < kTreeR; ++r) acc[r] = 0.0;
-                if (sa < sb) tree_unit<false>(A, W, t0, sa, sb, acc);
-                tree_combine(acc, P);
-                if (ok && h == 0) {
-                    double* dst = sm + nxt + cd.pos;
-#pragma unroll
-                    for (int r = 0; r < kTreeR; ++r)
-                        if (t0 + r <= cd.deg) dst[t0 + r] = acc[r];
-                }
-            }
+        for (int l = g.Lv; l > lw; --l) {
+            tree_down_level(g, s_hs, sm, l, 0, 1 << (g.Lv - l), cur, nxt, tid, kTreeThreads);
             __syncthreads();
             const int tsw = cur;
             cur = nxt;
             nxt = tsw;
         }
-        // ---- leaves: warp per level-1 node (lambda at cur), lane = literal 32 a + lane of its two blocks
         const double wc = a.w_sym[s];
-        for (int j = warp; j < n1; j += kTreeThreads / 32) {
-            const TreeNode nd = tree_node(g, s_hs, 1, j);
-            if (nd.deg < 0) continue;   // an empty slot (warp-uniform)
-            const double* lam1 = sm + cur + nd.pos;
-            double* tw = sm + nxt + warp * 4 * (kTreeLeaf + 1);   // P_L, P_R, then lambda_L, lambda_R
-            tree_leaf_pair(p + 2 * kTreeLeaf * nd.a + kTreeLeaf * (lane >> 4), true, tw);
-            __syncwarp();
-            // lambda_L[t] = sum_s lam1[t + s] P_R[s], lambda_R[t] = sum_s lam1[t + s] P_L[s], t = 0..16
-            if (lane <= kTreeLeaf) {
-                double vl = 0.0, vr = 0.0;
-                for (int u = 0; u <= kTreeLeaf; ++u) {
-                    vl = fma(lam1[lane + u], tw[kTreeLeaf + 1 + u], vl);
-                    vr = fma(lam1[lane + u], tw[u], vr);
-                }
-                tw[2 * (kTreeLeaf + 1) + lane] = vl;
-                tw[3 * (kTreeLeaf + 1) + lane] = vr;
+        for (int r = warp; r < nsub; r += NW) {
+            int c = cur, x = nxt;
+            for (int l = lw; l >= 2; --l) {
+                tree_down_level(g, s_hs, sm, l, r << (lw - l), (r + 1) << (lw - l), c, x, lane, 32);
+                __syncwarp();
+                const int tsw = c;
+                c = x;
+                x = tsw;
             }
-            __syncwarp();
-            const int blk = lane >> 4;
-            const int i = 2 * kTreeLeaf * nd.a + lane;
-            if (i < k) {
-                double qi[kTreeLeaf + 1];
-                tree_leaf_poly(p + 2 * kTreeLeaf * nd.a + kTreeLeaf * blk, lane & 15, qi);
-                const double* lb = tw + (2 + blk) * (kTreeLeaf + 1);
-                double dp = 0.0;   // dFE/dp_i = sum_s (lambda[s + 1] - lambda[s]) Q_i[s]
-#pragma unroll
-                for (int u = 0; u < kTreeLeaf; ++u) dp = fma(lb[u + 1] - lb[u], qi[u], dp);
-                const uint32_t w = __ldg(a.words + lo + i);
-                const double v = wc * (-0.5 * dp);   // dFE/dl_i = -dFE/dp_i / 2
-                a.Tb[(a.tb_fast + lo + i) * a.B + b] = (int)w < 0 ? -v : v;
-            }
-            __syncwarp();
+            for (int j = r * w1; j < (r + 1) * w1; ++j) tree_leaf_down(g, s_hs, sm + c, p, j, tw, a, lo, b, wc);
         }
         // unsat count (integer, exact), f
         int tcs = tc;
@@ -390,7 +428,7 @@ __global__ void __launch_bounds__(kTreeThreads, 1) sym_tree_kernel(SymArgs<doubl
         __syncthreads();
         if (tid == 0) {
             int t = 0;
-            for (int w = 0; w < kTreeThreads / 32; ++w) t += reinterpret_cast<int*>(s_red)[w];
+            for (int w = 0; w < NW; ++w) t += reinterpret_cast<int*>(s_red)[w];
             a.fsym[s * a.B + b] = wc * fe;
             a.usym[s * a.B + b] = rule_sat(t, sg.tmin, sg.tmax, sg.parity) ? 0 : 1;
         }

@@ -19,6 +19,6 @@ void launch_tree_class(const SymClass& cl, const dev::SymArgs<double>& a, int ma
     }
     CK(cudaMemsetAsync(counter, 0, sizeof(int32_t), st));
     const unsigned grid = (unsigned)std::min<int64_t>(items, num_sm);
-    dev::sym_tree_kernel<<<grid, dev::kTreeThreads, smem, st>>>(a, cl.begin, items, counter);
+    dev::sym_tree_kernel<<<grid, dev::kTreeThreads, smem, st>>>(a, cl.begin, items, counter, (int32_t)(smem / sizeof(double)));
 }
 }  // namespace ffsat

@@ -30,6 +30,7 @@ struct TreeGeom {
     int off[12];                 // level l polynomial region (l = 1..Lv)
     int lamX, lamY, lamSize;     // the two functional buffers (each sized for the largest level)
     int one;                     // the constant polynomial 1 surrounded by zeros
+    int scr;                     // per-warp scratch
     int total;
 };
 
@@ -50,13 +51,14 @@ FFSAT_HD inline TreeGeom tree_geom(int k) {
         g.off[l] = o;
         o += tree_level_size(k, l, Lv);
     }
-    // the functional buffers hold any level's functionals, and the per-warp scratch of the leaf phase (16 x 68)
-    g.lamSize = 16 * 4 * (kTreeLeaf + 1);
+    // the functional buffers hold any level's functionals
+    g.lamSize = 0;
     for (int l = 1; l <= Lv; ++l) g.lamSize = g.lamSize > tree_level_size(k, l, Lv) ? g.lamSize : tree_level_size(k, l, Lv);
     g.lamX = o;
     g.lamY = o + g.lamSize;
     g.one = g.lamY + g.lamSize;
-    g.total = g.one + 2 * kTreePad + 1;
+    g.scr = g.one + 2 * kTreePad + 1;          // per-warp scratch of the level-1 / leaf stage: 16 x 4 x 17
+    g.total = g.scr + 16 * 4 * (kTreeLeaf + 1);
     return g;
 }
 
