@@ -101,7 +101,8 @@ void eval_device_t(ffsat_ctx* c, Scratch& S, const T* x, int64_t B, double* f, T
     const bool need_xT = L.path == 2 || L.sym_lane;
     if (need_xT && L.n > 0) {
         dim3 tg(blocks_for(L.n, 32), blocks_for(B, 32)), tb(32, 8);
-        dev::transpose_kernel<T><<<tg, tb, 0, st>>>(x, S.xT.as<T>(), B, L.n);
+        if (L.own_sliced) dev::transpose_kernel<T, kOwnSlice><<<tg, tb, 0, st>>>(x, S.xT.as<T>(), B, L.n);
+        else dev::transpose_kernel<T, 0><<<tg, tb, 0, st>>>(x, S.xT.as<T>(), B, L.n);
         c->launches += 1;
     }
     // root-path classes are independent of the fast kernel (disjoint outputs): off the profiling path they
@@ -263,12 +264,30 @@ void eval_device_t(ffsat_ctx* c, Scratch& S, const T* x, int64_t B, double* f, T
         c->launches += 1;
         dev::OwnerArgs<T> o{};
         o.xT = S.xT.as<T>(); o.B = B; o.n = L.n; o.own_off = c->own_off.as<int64_t>(); o.own_rec = c->own_rec.as<uint4>();
+        o.row_stride = L.own_sliced ? kOwnSlice : B;
+        o.slice_stride = L.own_sliced ? kOwnSlice * (int64_t)L.n : 32;
         o.buckets = c->buckets.as<dev::FastBucketDev>(); o.w_pos = w_pos;
         o.Tb = S.Tb.as<T>(); o.occ_off = c->occ_off.as<int64_t>(); o.occ_slot = c->occ_slot.as<int32_t>(); o.grad = grad;
         o.fpart = S.fpart.as<double>(); o.upart = unsat ? S.upart.as<int32_t>() : nullptr;
         o.row0 = c->n_chunks + c->n_fold;
-        dim3 grid(blocks_for(L.n, 8), blocks_for(B, 32)), blk(32, 8);
-        dev::owner_grad_kernel<T><<<grid, blk, 0, st>>>(o);
+        if (L.own_sliced && L.own_uni >= 0) {   // one owner bucket: coefficients once, branch-free records
+            dim3 grid(blocks_for(L.n, 256 / kOwnSlice), blocks_for(B, kOwnSlice));
+            const int key = L.fbuckets[(size_t)L.own_uni].k * 10 + fast_nch(L.fbuckets[(size_t)L.own_uni]);
+            switch (key) {
+            case 11: dev::owner_uni_kernel<T, kOwnSlice, 1, 1><<<grid, 256, 0, st>>>(o, L.own_uni); break;
+            case 12: dev::owner_uni_kernel<T, kOwnSlice, 1, 2><<<grid, 256, 0, st>>>(o, L.own_uni); break;
+            case 21: dev::owner_uni_kernel<T, kOwnSlice, 2, 1><<<grid, 256, 0, st>>>(o, L.own_uni); break;
+            case 22: dev::owner_uni_kernel<T, kOwnSlice, 2, 2><<<grid, 256, 0, st>>>(o, L.own_uni); break;
+            case 31: dev::owner_uni_kernel<T, kOwnSlice, 3, 1><<<grid, 256, 0, st>>>(o, L.own_uni); break;
+            default: dev::owner_uni_kernel<T, kOwnSlice, 3, 2><<<grid, 256, 0, st>>>(o, L.own_uni); break;
+            }
+        } else if (L.own_sliced) {   // kOwnSlice points x 256 / kOwnSlice variables per block
+            dim3 grid(blocks_for(L.n, 256 / kOwnSlice), blocks_for(B, kOwnSlice));
+            dev::owner_grad_kernel<T, kOwnSlice><<<grid, 256, 0, st>>>(o);
+        } else {
+            dim3 grid(blocks_for(L.n, 8), blocks_for(B, 32));
+            dev::owner_grad_kernel<T, 32><<<grid, 256, 0, st>>>(o);
+        }
         dev::fold_rows_kernel<8><<<dim3((unsigned)c->n_fold, blocks_for(B, 32)), 256, 0, st>>>(
             S.fpart.as<double>(), unsat ? S.upart.as<int32_t>() : nullptr, B, o.row0, c->n_vtiles, c->n_chunks);
         c->launches += 1;

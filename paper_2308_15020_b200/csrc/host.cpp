@@ -490,11 +490,18 @@ Layout build_layout(const Formula& F, int path, int precision) {
         cl.S = cl.G <= 0 ? 1 : std::max(1, std::min(32, (cl.max_mp + root_chunk - 1) / root_chunk));
     }
 
-    // ---- owner-computes buckets (global path): no T slots; the other fast buckets' slots are renumbered densely
-    // off by default: measured slower than the T-buffer path on c5 (2.65 vs 1.34 ms per evaluation, the per-variable
-    // occurrence loops are latency-bound and x^T still misses L2); FFSAT_OWN=1 enables it
+    // ---- owner-computes buckets (global path, FFSAT_OWN=1): no T slots; the other fast buckets' slots are renumbered
+    // densely.  Off by default: measured slower than the T-buffer path on c5 (round 1 2.65 vs
+    // 1.34 ms; round 2, x^T in L2-resident 8-point slices and one branch-free kernel for a single owner bucket, 1.71 vs
+    // 1.34 ms at 1.2 GB of DRAM traffic instead of 4.5 GB -- instruction-bound: the per-record work is repeated per
+    // slice).  When every fast constraint is short and no root-path class reads x^T, x^T is sliced (own_sliced).
     int own_kmax = 0;
-    if (const char* e = std::getenv("FFSAT_OWN")) if (path == 2 && std::atoi(e) != 0) own_kmax = kOwnKMax;
+    {
+        bool short_only = path == 2 && !Lo.fbuckets.empty();
+        for (const FastBucket& b : Lo.fbuckets) short_only = short_only && b.k <= kOwnKMax;
+        if (const char* e = std::getenv("FFSAT_OWN")) own_kmax = (path == 2 && std::atoi(e) != 0) ? kOwnKMax : 0;
+        Lo.own_sliced = own_kmax > 0 && short_only && !Lo.sym_lane;
+    }
     {
         int64_t ts = 0;
         for (FastBucket& b : Lo.fbuckets) {
@@ -505,6 +512,13 @@ Layout build_layout(const Formula& F, int path, int precision) {
         }
         if (path == 2) Lo.tb_fast = ts;
         Lo.own = Lo.n_own_lits > 0;
+        int nown = 0;
+        for (size_t bi = 0; bi < Lo.fbuckets.size(); ++bi)
+            if (Lo.fbuckets[bi].own) {
+                ++nown;
+                Lo.own_uni = (int32_t)bi;
+            }
+        if (nown != 1 || !Lo.own_sliced) Lo.own_uni = -1;
     }
     if (Lo.own) {
         if (Lo.fbuckets.size() > 0xffffff) throw Error(FFSAT_ERR_ARG, "too many fast buckets");

@@ -51,6 +51,7 @@ struct FastBucket {
     SatRule rule;
 };
 
+inline int fast_nch(const FastBucket& b) { return (b.gA != 0) + (b.gB != 0) + (b.gX != 0); }   // product channels
 constexpr int kFastKMax = 64;       // fast product paths handle k <= 64; longer constraints use roots
 
 struct SymSig {                     // a (k, sat rule) signature with its root table
@@ -111,7 +112,10 @@ struct Layout {
     // owner-computes (global path, fast buckets with k <= kOwnKMax): per variable its occurrences in those
     // constraints, ascending position, as self-contained 16-byte records {position, the other literals' words (in
     // literal order, padded with the first), bucket << 8 | literal index << 1 | own literal negated}
+    bool own_sliced = false;        // every fast constraint is owner-computed and nothing else reads x^T: x^T is laid out in
+                                    // 16-point slices [B/16][n][16] so one slice (n x 64 B) stays L2-resident per pass
     bool own = false;
+    int32_t own_uni = -1;               // the single owner bucket when there is exactly one (owner_uni_kernel), else -1
     int64_t n_own_lits = 0;
     std::vector<int64_t> own_off;       // [n + 1]
     std::vector<uint32_t> own_rec;      // 4 per occurrence
@@ -123,6 +127,7 @@ struct Layout {
     std::vector<uint32_t> tiled_words;  // tiled path: (var * kTilePitch) | neg << 31 (padded rows)
 };
 
+constexpr int kOwnSlice = 8;       // points per x^T slice of the sliced owner-computes path (one slice's x^T stays in L2)
 constexpr int kOwnKMax = 3;         // global path, FFSAT_OWN=1: constraints this short take the owner-computes gradient
 constexpr int kTilePitch = 66;      // smem row pitch of the tiled kernel: x half-row (32 points + pad) | gradient half-row
 constexpr int kClassCap = 16;

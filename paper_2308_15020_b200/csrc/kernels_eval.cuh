@@ -1891,7 +1891,8 @@ __global__ void __launch_bounds__(256) reduce_grad_kernel(ReduceArgs<T> a) {
 // Block (32 points, 8 variables).
 template <typename T>
 struct OwnerArgs {
-    const T* xT;                 // [n][B] (canonical zeros)
+    const T* xT;                 // x^T (canonical zeros): element (v, b) at xT[(b / SB) slice_stride + v row_stride + b % SB]
+    int64_t row_stride, slice_stride;   // [n][B]: B, 32 (SB = 32); 16-point slices [B/16][n][16]: 16, 16 n (SB = 16)
     int64_t B;
     int32_t n;
     const int64_t* own_off;      // [n + 1]
@@ -1933,13 +1934,15 @@ __device__ __forceinline__ T ld_keep(const T* p, uint64_t pol) {
     return v;
 }
 
-template <typename T>
+// Block = SB points x (256 / SB) variables (thread (tx = point, ty = variable)); grid (variable tiles, point slices).
+template <typename T, int SB>
 __global__ void __launch_bounds__(256) owner_grad_kernel(OwnerArgs<T> a) {
-    __shared__ T tile[8][33];
-    __shared__ double sf[8][32];
-    __shared__ int su[8][32];
-    const int tx = threadIdx.x, ty = threadIdx.y;
-    const int64_t b0 = (int64_t)blockIdx.y * 32, v0 = (int64_t)blockIdx.x * 8;   // grid.x over variable tiles
+    constexpr int NV = 256 / SB;   // variables per block
+    __shared__ T tile[NV][SB + 1];
+    __shared__ double sf[NV][SB];
+    __shared__ int su[NV][SB];
+    const int tx = threadIdx.x % SB, ty = threadIdx.x / SB;
+    const int64_t b0 = (int64_t)blockIdx.y * SB, v0 = (int64_t)blockIdx.x * NV;   // grid.x over variable tiles
     const int64_t b = b0 + tx, v = v0 + ty;
     const bool bv = b < a.B;
     const int64_t bb = bv ? b : a.B - 1;   // lanes past the batch mirror the last point (in-bounds loads, nothing stored)
@@ -1948,8 +1951,8 @@ __global__ void __launch_bounds__(256) owner_grad_kernel(OwnerArgs<T> a) {
     int uacc = 0;
     if (v < a.n) {
         const uint64_t keep = l2_policy_last(), stream = l2_policy_first();
-        const T* xTb = a.xT + bb;
-        const T xv = ld_keep(xTb + v * a.B, keep);
+        const T* xTb = a.xT + (bb / SB) * a.slice_stride + bb % SB;
+        const T xv = ld_keep(xTb + v * a.row_stride, keep);
         int cur = -1, nch = 0;
         BucketReg<T> bk{};
         const int64_t o1 = a.own_off[v + 1];
@@ -1961,8 +1964,8 @@ __global__ void __launch_bounds__(256) owner_grad_kernel(OwnerArgs<T> a) {
             T xa[NB], xb[NB], wc[NB];
 #pragma unroll
             for (int q = 0; q < NB; ++q) {   // every gather of the batch in flight (padding words read variable 0)
-                xa[q] = ld_keep(xTb + (int64_t)(rc[q].y & 0x7fffffffu) * a.B, keep);
-                xb[q] = ld_keep(xTb + (int64_t)(rc[q].z & 0x7fffffffu) * a.B, keep);
+                xa[q] = ld_keep(xTb + (int64_t)(rc[q].y & 0x7fffffffu) * a.row_stride, keep);
+                xb[q] = ld_keep(xTb + (int64_t)(rc[q].z & 0x7fffffffu) * a.row_stride, keep);
                 wc[q] = __ldg(a.w_pos + rc[q].x);
             }
 #pragma unroll
@@ -2016,7 +2019,7 @@ __global__ void __launch_bounds__(256) owner_grad_kernel(OwnerArgs<T> a) {
             for (; q < e; ++q) acc += (double)a.Tb[(int64_t)a.occ_slot[q] * a.B + bb];
         }
     }
-    // partial f / unsat of this variable tile: warp (variable) order
+    // partial f / unsat of this variable tile: variable order
     sf[ty][tx] = facc;
     su[ty][tx] = uacc;
     tile[ty][tx] = (T)acc;
@@ -2025,18 +2028,103 @@ __global__ void __launch_bounds__(256) owner_grad_kernel(OwnerArgs<T> a) {
         double f = 0.0;
         int u = 0;
 #pragma unroll
-        for (int j = 0; j < 8; ++j) {
+        for (int j = 0; j < NV; ++j) {
             f += sf[j][tx];
             u += su[j][tx];
         }
         a.fpart[((int64_t)a.row0 + blockIdx.x) * a.B + b] = f;
         if (want_unsat) a.upart[((int64_t)a.row0 + blockIdx.x) * a.B + b] = u;
     }
-    if (want_term) {   // transposed write: each point row gets 8 consecutive gradient entries
-        const int t = ty * 32 + tx;
-        const int pl = t >> 3, vl = t & 7;
+    if (want_term) {   // transposed write: each point row gets NV consecutive gradient entries
+        const int t = threadIdx.x;
+        const int pl = t / NV, vl = t % NV;
         const int64_t pb = b0 + pl, vv = v0 + vl;
-        if (pb < a.B && vv < a.n) a.grad[pb * a.n + vv] = tile[vl][pl];
+        // streaming store (evict-first): the gradient is written once and must not displace the x^T slice from L2
+        if (pb < a.B && vv < a.n) __stcs(a.grad + pb * a.n + vv, tile[vl][pl]);
+    }
+}
+
+// The same for the common case of ONE owner bucket (uniform short constraints, e.g. random 3-SAT): the bucket's
+// coefficients are loaded once and the per-record work is branch-free with the length K and the product channels
+// NCH fixed at compile time.  Same records, same summation orders (bit-identical to owner_grad_kernel).
+template <typename T, int SB, int K, int NCH>
+__global__ void __launch_bounds__(256) owner_uni_kernel(OwnerArgs<T> a, int32_t bucket) {
+    constexpr int NV = 256 / SB;
+    __shared__ T tile[NV][SB + 1];
+    __shared__ double sf[NV][SB];
+    __shared__ int su[NV][SB];
+    const int tx = threadIdx.x % SB, ty = threadIdx.x / SB;
+    const int64_t b0 = (int64_t)blockIdx.y * SB, v0 = (int64_t)blockIdx.x * NV;
+    const int64_t b = b0 + tx, v = v0 + ty;
+    const bool bv = b < a.B;
+    const int64_t bb = bv ? b : a.B - 1;
+    const bool want_term = a.grad != nullptr, want_unsat = a.upart != nullptr;
+    const BucketReg<T> bk = load_bucket<T>(a.buckets + bucket);
+    double acc = 0.0, facc = 0.0;
+    int uacc = 0;
+    if (v < a.n) {
+        const T* xTb = a.xT + (bb / SB) * a.slice_stride + bb % SB;
+        const T xv = __ldg(xTb + v * a.row_stride);
+        const int64_t o1 = a.own_off[v + 1];
+        for (int64_t o = a.own_off[v]; o < o1; o += 4) {
+            constexpr int NB = 4;
+            uint4 rc[NB];
+#pragma unroll
+            for (int q = 0; q < NB; ++q) rc[q] = o + q < o1 ? __ldcs(a.own_rec + o + q) : make_uint4(0, 0, 0, 0);
+            T xa[NB], xb[NB], wc[NB];
+#pragma unroll
+            for (int q = 0; q < NB; ++q) {
+                xa[q] = K >= 2 ? __ldg(xTb + (int64_t)(rc[q].y & 0x7fffffffu) * a.row_stride) : (T)0;
+                xb[q] = K >= 3 ? __ldg(xTb + (int64_t)(rc[q].z & 0x7fffffffu) * a.row_stride) : (T)0;
+                wc[q] = __ldg(a.w_pos + rc[q].x);
+            }
+#pragma unroll
+            for (int q = 0; q < NB; ++q) {
+                if (o + q >= o1) break;
+                const uint32_t wown = rc[q].w << 31;
+                T term = (T)0, fe = bk.g0;
+#pragma unroll
+                for (int c = 0; c < NCH; ++c) {
+                    const T ao = fmaT(flip_sign(bk.c1[c], wown), xv, bk.c0[c]);
+                    const T aa = K >= 2 ? fmaT(flip_sign(bk.c1[c], rc[q].y), xa[q], bk.c0[c]) : (T)1;
+                    const T ab = K >= 3 ? fmaT(flip_sign(bk.c1[c], rc[q].z), xb[q], bk.c0[c]) : (T)1;
+                    const T ex = aa * ab;
+                    fe = fmaT(bk.g[c], ao * ex, fe);
+                    term = fmaT(bk.g[c] * flip_sign(bk.c1[c], wown), ex, term);
+                }
+                if (want_term) acc += (double)(wc[q] * term);
+                if (((rc[q].w >> 1) & 3) == 0) {   // the constraint's f and check, counted once (first literal's owner)
+                    facc += (double)(wc[q] * fe);
+                    if (want_unsat) {
+                        uint32_t t = lit_true(xv, wown);
+                        if (K >= 2) t += lit_true(xa[q], rc[q].y);
+                        if (K >= 3) t += lit_true(xb[q], rc[q].z);
+                        uacc += rule_sat((int)t, bk.tmin, bk.tmax, bk.parity) ? 0 : 1;
+                    }
+                }
+            }
+        }
+    }
+    sf[ty][tx] = facc;
+    su[ty][tx] = uacc;
+    tile[ty][tx] = (T)acc;
+    __syncthreads();
+    if (ty == 0 && bv) {
+        double f = 0.0;
+        int u = 0;
+#pragma unroll
+        for (int j = 0; j < NV; ++j) {
+            f += sf[j][tx];
+            u += su[j][tx];
+        }
+        a.fpart[((int64_t)a.row0 + blockIdx.x) * a.B + b] = f;
+        if (want_unsat) a.upart[((int64_t)a.row0 + blockIdx.x) * a.B + b] = u;
+    }
+    if (want_term) {
+        const int t = threadIdx.x;
+        const int pl = t / NV, vl = t % NV;
+        const int64_t pb = b0 + pl, vv = v0 + vl;
+        if (pb < a.B && vv < a.n) __stcs(a.grad + pb * a.n + vv, tile[vl][pl]);
     }
 }
 
@@ -2191,7 +2279,8 @@ __global__ void __launch_bounds__(32 * NWF) reduce_f_kernel(ReduceFArgs a) {
 }
 
 // x [B][n] -> xT [n][B]
-template <typename T>
+// x [B][n] -> x^T: W = 0 [n][B]; W > 0: W-point slices [B/W][n][W] (each slice contiguous).
+template <typename T, int W = 0>
 __global__ void __launch_bounds__(256) transpose_kernel(const T* __restrict__ x, T* __restrict__ xT, int64_t B, int32_t n) {
     __shared__ T tile[32][33];
     const int tx = threadIdx.x, ty = threadIdx.y;
@@ -2205,7 +2294,10 @@ __global__ void __launch_bounds__(256) transpose_kernel(const T* __restrict__ x,
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
         int64_t v = v0 + ty + 8 * j, b = b0 + tx;
-        if (b < B && v < n) xT[v * B + b] = tile[tx][ty + 8 * j] + (T)0;   // + 0: canonical zeros (-0.0 -> +0.0)
+        if (b < B && v < n) {
+            const int64_t o = W > 0 ? (b / W) * W * (int64_t)n + v * W + (b % W) : v * B + b;
+            xT[o] = tile[tx][ty + 8 * j] + (T)0;   // + 0: canonical zeros (-0.0 -> +0.0)
+        }
     }
 }
 

@@ -221,6 +221,23 @@ def test_owner_computes_option(precision, monkeypatch):
     assert torch.equal(f2, f[33:50]) and torch.equal(g2, g[33:50]) and torch.equal(u2, u[33:50])
 
 
+@pytest.mark.parametrize("precision", [32, 64])
+def test_owner_computes_sliced_uniform(precision, monkeypatch):
+    """FFSAT_OWN=1 on a formula whose fast constraints are ALL short (uniform random 3-SAT on the global path): x^T in
+    8-point slices and the single-bucket owner kernel (owner_uni_kernel); f, grad, unsat against the oracle on a ragged
+    batch (a partial last slice), and bit-identical when a point is evaluated in another batch / slice position."""
+    monkeypatch.setenv("FFSAT_OWN", "1")
+    inst = synth.random_ksat(3000, 12600, 3, 5)
+    ctx = P.Context.from_instance(inst, precision=precision, path=2, device=0)
+    assert ctx.info["n_own_lits"] == ctx.info["n_lits"]
+    compare(inst, synth.points("U", 21, inst.n, 6), precision=precision, ctx=ctx)
+    compare(inst, synth.points("Z", 9, inst.n, 7), precision=precision, ctx=ctx)
+    X = torch.from_numpy(synth.points("U", 37, inst.n, 8, ctx.dtype)).cuda()
+    f, g, u = ctx.eval(X, grad=True, unsat=True)
+    f2, g2, u2 = ctx.eval(X[5:30].contiguous(), grad=True, unsat=True)
+    assert torch.equal(f2, f[5:30]) and torch.equal(g2, g[5:30]) and torch.equal(u2, u[5:30])
+
+
 def test_c4_hybrid_global_full_batch():
     """c4's shape (3-CNF + XOR k = 3..64, n = 1024) on the global path (short and long kernels) at B = 1024 (the
     bench launch configuration); oracle on every point of a 1024-point batch."""
