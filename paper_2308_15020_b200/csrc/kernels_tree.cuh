@@ -131,22 +131,6 @@ __device__ __forceinline__ void tree_combine(double (&acc)[kTreeR], int P) {
     }
 }
 
-// leaf block polynomial: prod_{i in block} ((1 - p_i) + p_i z), p[] padded with zeros past k (identity factors);
-// skip = the literal left out (-1: none).  Alg. 5's forward recurrence, coefficients in registers.
-__device__ __forceinline__ void tree_leaf_poly(const double* p, int skip, double (&q)[kTreeLeaf + 1]) {
-    q[0] = 1.0;
-#pragma unroll
-    for (int t = 1; t <= kTreeLeaf; ++t) q[t] = 0.0;
-#pragma unroll
-    for (int i = 0; i < kTreeLeaf; ++i) {
-        const double pi = i == skip ? 0.0 : p[i];
-        const double qi = 1.0 - pi;
-#pragma unroll
-        for (int t = i + 1; t >= 1; --t) q[t] = fma(pi, q[t - 1], qi * q[t]);
-        q[0] *= qi;
-    }
-}
-
 // The two leaf-block polynomials of a level-1 node by the whole warp: half-warp hw (lanes 16 hw .. 16 hw + 15) forms
 // block `a + hw`'s 17 coefficients (lane t of the half holds q[t], its lane 15 also q[16]) with one shuffle per literal
 // (the same recurrence, q_t <- (1 - p_i) q_t + p_i q_{t-1}); an absent block (present = false) is the polynomial 1.
@@ -268,11 +252,13 @@ __device__ __forceinline__ void tree_down_level(const TreeGeom& g, const short* 
     }
 }
 
-// Level-1 node j (one warp): its polynomial = (block 0 poly) * (block 1 poly) of its 32 literals (p is zero past k).
-__device__ __forceinline__ void tree_leaf_up(const TreeGeom& g, const short* hs, double* sm, const double* p, int j, double* tw) {
+// Level-1 node j (one warp): the two leaf-block polynomials (kept at g.leaf for the leaf stage) and their product,
+// the node's polynomial (p is zero past k, so a missing or partial second block is exact).
+__device__ __forceinline__ void tree_leaf_up(const TreeGeom& g, const short* hs, double* sm, const double* p, int j) {
     const int lane = threadIdx.x & 31;
     const TreeNode nd = tree_node(g, hs, 1, j);
     if (nd.deg < 0) return;   // an empty slot (warp-uniform)
+    double* tw = sm + g.leaf + j * 2 * (kTreeLeaf + 1);
     tree_leaf_pair(p + 2 * kTreeLeaf * nd.a + kTreeLeaf * (lane >> 4), true, tw);
     __syncwarp();
     double* dst = sm + g.off[1] + nd.pos;
@@ -285,35 +271,55 @@ __device__ __forceinline__ void tree_leaf_up(const TreeGeom& g, const short* hs,
 }
 
 // Leaf stage of level-1 node j (one warp, lane = literal 32 a + lane): the two block functionals from the node's
-// functional (at lam), then per literal dFE/dp_i = sum_s (lambda[s + 1] - lambda[s]) Q_i[s]; terms into Tb.
-__device__ __forceinline__ void tree_leaf_down(const TreeGeom& g, const short* hs, const double* lamb, const double* p, int j,
-                                               double* tw, const SymArgs<double>& a, int64_t lo, int64_t b, double wc) {
+// functional (at lamb), then per literal dFE/dp_i = sum_s (lambda[s + 1] - lambda[s]) Q_i[s], where the block's
+// leave-one-out polynomial Q_i = P_block / f_i comes from ONE synthetic division by the linear factor f_i = (1 - p_i)
+// + p_i z, run in the stable direction: ascending when p_i <= 1/2 (each step multiplies the carried error by
+// p_i / (1 - p_i) <= 1), descending from the top otherwise ((1 - p_i) / p_i <= 1); terms into Tb.
+__device__ __forceinline__ void tree_leaf_down(const TreeGeom& g, const short* hs, double* sm, const double* lamb, const double* p,
+                                               int j, double* tw, const SymArgs<double>& a, int64_t lo, int64_t b, double wc) {
     const int lane = threadIdx.x & 31;
     const TreeNode nd = tree_node(g, hs, 1, j);
     if (nd.deg < 0) return;
     const double* lam1 = lamb + nd.pos;
-    tree_leaf_pair(p + 2 * kTreeLeaf * nd.a + kTreeLeaf * (lane >> 4), true, tw);   // P_L, P_R
-    __syncwarp();
+    const double* PL = sm + g.leaf + j * 2 * (kTreeLeaf + 1);   // P_L, P_R (from the bottom-up pass)
     // lambda_L[t] = sum_s lam1[t + s] P_R[s], lambda_R[t] = sum_s lam1[t + s] P_L[s], t = 0..16
     if (lane <= kTreeLeaf) {
         double vl = 0.0, vr = 0.0;
         for (int u = 0; u <= kTreeLeaf; ++u) {
-            vl = fma(lam1[lane + u], tw[kTreeLeaf + 1 + u], vl);
-            vr = fma(lam1[lane + u], tw[u], vr);
+            vl = fma(lam1[lane + u], PL[kTreeLeaf + 1 + u], vl);
+            vr = fma(lam1[lane + u], PL[u], vr);
         }
-        tw[2 * (kTreeLeaf + 1) + lane] = vl;
-        tw[3 * (kTreeLeaf + 1) + lane] = vr;
+        tw[lane] = vl;
+        tw[kTreeLeaf + 1 + lane] = vr;
     }
     __syncwarp();
     const int blk = lane >> 4;
     const int i = 2 * kTreeLeaf * nd.a + lane;
     if (i < g.k) {
-        double qi[kTreeLeaf + 1];
-        tree_leaf_poly(p + 2 * kTreeLeaf * nd.a + kTreeLeaf * blk, lane & 15, qi);
-        const double* lb = tw + (2 + blk) * (kTreeLeaf + 1);
+        const double* P = PL + blk * (kTreeLeaf + 1);
+        const double pi = p[i];
+        double q[kTreeLeaf];
+        if (pi <= 0.5) {
+            const double r = 1.0 / (1.0 - pi);
+            double prev = 0.0;
+#pragma unroll
+            for (int t = 0; t < kTreeLeaf; ++t) {
+                q[t] = fma(-pi, prev, P[t]) * r;
+                prev = q[t];
+            }
+        } else {
+            const double r = 1.0 / pi, qi = 1.0 - pi;
+            double nxt = 0.0;
+#pragma unroll
+            for (int t = kTreeLeaf; t >= 1; --t) {
+                q[t - 1] = fma(-qi, nxt, P[t]) * r;
+                nxt = q[t - 1];
+            }
+        }
+        const double* lb = tw + blk * (kTreeLeaf + 1);
         double dp = 0.0;
 #pragma unroll
-        for (int u = 0; u < kTreeLeaf; ++u) dp = fma(lb[u + 1] - lb[u], qi[u], dp);
+        for (int u = 0; u < kTreeLeaf; ++u) dp = fma(lb[u + 1] - lb[u], q[u], dp);
         const uint32_t w = __ldg(a.words + lo + i);
         const double v = wc * (-0.5 * dp);   // dFE/dl_i = -dFE/dp_i / 2
         a.Tb[(a.tb_fast + lo + i) * a.B + b] = (int)w < 0 ? -v : v;
@@ -374,10 +380,10 @@ __global__ void __launch_bounds__(kTreeThreads, 1) sym_tree_kernel(SymArgs<doubl
         if (tid == 0) sm[g.one + kTreePad] = 1.0;   // (ordered after the zeroing above; read after the next barrier)
         // warp-local subtrees: rooted at level lw = Lv - 4 (16 of them, one per warp), or at level 1 for small trees
         const int lw = max(1, g.Lv - 4), nsub = 1 << (g.Lv - lw), w1 = 1 << (lw - 1);
-        double* tw = sm + g.scr + warp * 4 * (kTreeLeaf + 1);
+        double* tw = sm + g.scr + warp * 2 * (kTreeLeaf + 1);
         // ---- bottom-up: levels 1..lw per warp, then lw+1..Lv by the CTA
         for (int r = warp; r < nsub; r += NW) {
-            for (int j = r * w1; j < (r + 1) * w1; ++j) tree_leaf_up(g, s_hs, sm, p, j, tw);
+            for (int j = r * w1; j < (r + 1) * w1; ++j) tree_leaf_up(g, s_hs, sm, p, j);
             for (int l = 2; l <= lw; ++l) {
                 tree_up_level(g, s_hs, sm, l, r << (lw - l), (r + 1) << (lw - l), lane, 32);
                 __syncwarp();
@@ -417,7 +423,7 @@ __global__ void __launch_bounds__(kTreeThreads, 1) sym_tree_kernel(SymArgs<doubl
                 c = x;
                 x = tsw;
             }
-            for (int j = r * w1; j < (r + 1) * w1; ++j) tree_leaf_down(g, s_hs, sm + c, p, j, tw, a, lo, b, wc);
+            for (int j = r * w1; j < (r + 1) * w1; ++j) tree_leaf_down(g, s_hs, sm, sm + c, p, j, tw, a, lo, b, wc);
         }
         // unsat count (integer, exact), f
         int tcs = tc;

@@ -31,6 +31,7 @@ struct TreeGeom {
     int lamX, lamY, lamSize;     // the two functional buffers (each sized for the largest level)
     int one;                     // the constant polynomial 1 surrounded by zeros
     int scr;                     // per-warp scratch
+    int leaf;                    // leaf-block polynomials (kept from the bottom-up pass for the leaf stage)
     int total;
 };
 
@@ -57,8 +58,9 @@ FFSAT_HD inline TreeGeom tree_geom(int k) {
     g.lamX = o;
     g.lamY = o + g.lamSize;
     g.one = g.lamY + g.lamSize;
-    g.scr = g.one + 2 * kTreePad + 1;          // per-warp scratch of the level-1 / leaf stage: 16 x 4 x 17
-    g.total = g.scr + 16 * 4 * (kTreeLeaf + 1);
+    g.scr = g.one + 2 * kTreePad + 1;          // per-warp scratch of the leaf stage: 16 x 2 x 17
+    g.leaf = g.scr + 16 * 2 * (kTreeLeaf + 1);  // the two leaf-block polynomials of every level-1 slot (34 each)
+    g.total = g.leaf + (1 << (Lv - 1)) * 2 * (kTreeLeaf + 1);
     return g;
 }
 
@@ -80,10 +82,11 @@ inline int64_t tree_fp64_work(int k) {
     }
     auto deg = [&](int h) { const int64_t e = endb[h] * 2 * kTreeLeaf < k ? endb[h] * 2 * kTreeLeaf : k; const int64_t d = e - start[h] * 2 * kTreeLeaf; return d > 0 ? d : 0; };
     int64_t w = 0;
-    // per level-1 node: the two leaf recurrences twice (bottom-up and leaf stage; 136 updates of 2 slots each), the
-    // 17 x 17 product, the two 17 x 17 leaf functionals; per literal: its leave-one-out recurrence and 16-term dot
-    w += (int64_t)g.nu * (4 * 2 * 136 + 17 * 17 + 2 * 17 * 17);
-    w += (int64_t)k * (2 * 136 + 2 * 16);
+    // per level-1 node: the two leaf recurrences (136 updates of 2 slots each), the 17 x 17 product, the two 17 x 17
+    // leaf functionals; per literal: its leave-one-out polynomial by one 16-step division (2 slots a step) and the
+    // 16-term dot (2 slots a term)
+    w += (int64_t)g.nu * (2 * 2 * 136 + 17 * 17 + 2 * 17 * 17);
+    w += (int64_t)k * (2 * 16 + 2 * 16);
     for (int h = 1; h < (1 << (g.Lv - 1)); ++h) {   // nodes of levels 2..Lv
         const int64_t dA = deg(2 * h), dB = deg(2 * h + 1);
         if (dB > 0) w += (dA + 1) * (dB + 1) * 3;   // bottom-up product + the two top-down correlations
