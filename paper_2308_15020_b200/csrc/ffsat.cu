@@ -141,9 +141,14 @@ void upload_layout(ffsat_ctx* c) {
     upload(c->chk_off, off);
     upload(c->chk_words, words);
     upload(c->chk_rule, rule);
+    std::vector<int32_t> longs;
+    for (int64_t p = 0; p < L.m; ++p)
+        if (off[(size_t)p + 1] - off[(size_t)p] > dev::kCheckLong) longs.push_back((int32_t)p);
+    c->n_chk_long = (int32_t)longs.size();
+    if (!longs.empty()) upload(c->chk_long, longs);
     for (DBuf* d : {&c->fast_words, &c->tiled_words, &c->units, &c->buckets, &c->sym_words, &c->sym_off,
                     &c->sym_sig, &c->sigs, &c->coef, &c->occ_off, &c->occ_slot, &c->w_pos, &c->w_static_orig, &c->order,
-                    &c->chk_off, &c->chk_words, &c->chk_rule, &c->own_off, &c->own_rec})
+                    &c->chk_off, &c->chk_words, &c->chk_rule, &c->chk_long, &c->own_off, &c->own_rec})
         c->persistent_bytes += (int64_t)d->bytes;
 }
 
@@ -460,6 +465,7 @@ void check_kernels(ffsat_search* s, cudaStream_t st) {
     a.cons_per_cta = (L.m + chunks - 1) / chunks;
     dim3 grid((unsigned)PT, (unsigned)((L.m + a.cons_per_cta - 1) / a.cons_per_cta));
     const size_t tile = (size_t)L.n * 4;
+    a.skip_long = c->n_chk_long > 0 ? 1 : 0;
     if (tile <= 96 * 1024) {
         if (tile > 48 * 1024) CK(cudaFuncSetAttribute(dev::check_bits_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tile));
         dev::check_bits_kernel<true><<<grid, 256, tile, st>>>(a);
@@ -467,6 +473,16 @@ void check_kernels(ffsat_search* s, cudaStream_t st) {
         dev::check_bits_kernel<false><<<grid, 256, 0, st>>>(a);
     }
     s->ctx->launches += 2;
+    if (c->n_chk_long > 0) {   // the long rows: one warp per (row, 32-point tile)
+        dim3 lg((unsigned)PT, (unsigned)((c->n_chk_long + 7) / 8));
+        if (tile <= 96 * 1024) {
+            if (tile > 48 * 1024) CK(cudaFuncSetAttribute(dev::check_long_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tile));
+            dev::check_long_kernel<true><<<lg, 256, tile, st>>>(a, c->chk_long.as<int32_t>(), c->n_chk_long);
+        } else {
+            dev::check_long_kernel<false><<<lg, 256, 0, st>>>(a, c->chk_long.as<int32_t>(), c->n_chk_long);
+        }
+        s->ctx->launches += 1;
+    }
     CK(cudaGetLastError());
 }
 

@@ -453,7 +453,9 @@ struct CheckBitsArgs {
     const int32_t* rule;      // [m][3] tmin, tmax, parity (1 odd, 2 even)
     int32_t* U;               // [m]
     int32_t* unsat;           // [B]
+    int32_t skip_long;        // rows longer than kCheckLong are left to check_long_kernel
 };
+constexpr int kCheckLong = 128;
 
 // Bit-sliced comparison of the per-point counts (planes p[0..13), LSB first, zero above plane P) with a constant:
 // gt / eq masks (fully unrolled so the planes stay in registers).
@@ -579,8 +581,9 @@ __global__ void __launch_bounds__(256) check_bits_kernel(CheckBitsArgs a) {
             hi = __ldg(a.off + c + 1);
             tmin = __ldg(a.rule + 3 * c); tmax = __ldg(a.rule + 3 * c + 1); par = __ldg(a.rule + 3 * c + 2);
         }
-        const bool longc = c < c1 && hi - lo > 128;
-        if (c < c1 && !longc) uns = ~sat_mask<SMEM, false>(a, S, lo, hi, tmin, tmax, par, 0, 1) & vm;
+        const bool longc = c < c1 && hi - lo > kCheckLong && !a.skip_long;
+        const bool skipped = c < c1 && hi - lo > kCheckLong && a.skip_long;
+        if (c < c1 && !longc && !skipped) uns = ~sat_mask<SMEM, false>(a, S, lo, hi, tmin, tmax, par, 0, 1) & vm;
         for (uint32_t lm = __ballot_sync(0xffffffffu, longc); lm; lm &= lm - 1) {
             const int src = __ffs(lm) - 1;
             const int64_t lo_s = __shfl_sync(0xffffffffu, lo, src), hi_s = __shfl_sync(0xffffffffu, hi, src);
@@ -605,6 +608,32 @@ __global__ void __launch_bounds__(256) check_bits_kernel(CheckBitsArgs a) {
     }
 }
 
+
+// Long rows (k > kCheckLong) of the round-end check, spread out: one warp per (long constraint, 32-point tile), the
+// 32 lanes interleaving its literals (sat_mask COOP); U_c and the per-point counts by integer atomics (exact, order
+// free).  check_bits_kernel skips these rows (a.skip_long), so a few thousand-literal rows no longer serialise on the
+// one warp whose constraint range holds them.  grid (tiles, ceil(n_long / 8)), 256 threads.
+template <bool SMEM>
+__global__ void __launch_bounds__(256) check_long_kernel(CheckBitsArgs a, const int32_t* longs, int32_t n_long) {
+    extern __shared__ __align__(16) uint32_t sgn[];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t pt = blockIdx.x, b0 = pt * 32;
+    const uint32_t vm = a.B - b0 >= 32 ? 0xffffffffu : ((1u << (a.B - b0)) - 1u);
+    const uint32_t* S = a.S + pt * a.n;
+    if (SMEM) {
+        for (int v = threadIdx.x; v < a.n; v += 256) sgn[v] = S[v];
+        __syncthreads();
+        S = sgn;
+    }
+    const int j = blockIdx.y * 8 + warp;
+    if (j >= n_long) return;
+    const int64_t c = longs[j];
+    const int64_t lo = __ldg(a.off + c), hi = __ldg(a.off + c + 1);
+    const int tmin = __ldg(a.rule + 3 * c), tmax = __ldg(a.rule + 3 * c + 1), par = __ldg(a.rule + 3 * c + 2);
+    const uint32_t uns = ~sat_mask<SMEM, true>(a, S, lo, hi, tmin, tmax, par, lane, 32) & vm;
+    if (lane == 0 && uns) atomicAdd(a.U + c, __popc(uns));
+    if ((uns >> lane) & 1u) atomicAdd(a.unsat + b0 + lane, 1);
+}
 
 // Round-end check for formulas without long rows (k <= 64): one thread per constraint over a group of TPC point
 // tiles (blockIdx.y), so U_c is counted in a register (one integer atomic per constraint and tile group instead of

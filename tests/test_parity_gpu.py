@@ -841,7 +841,7 @@ def test_maxsat_mode_planted_maxcut_tiny():
     assert hits >= 9
 
 
-@pytest.mark.parametrize("case", ["mixed", "long_card", "large_n"])
+@pytest.mark.parametrize("case", ["mixed", "long_card", "large_n", "large_n_long"])
 def test_bit_packed_check_all_rules(case):
     """The round-end check (sign words of 32 points, OR / AND / parity reductions, bit-sliced counts for the
     other rules): unsat[b] and U_c (per constraint) bit-exact against the oracle's exact check, on a ragged
@@ -850,8 +850,10 @@ def test_bit_packed_check_all_rules(case):
         inst = synth.random_mixed(n=150, m=900, seed=21, kmax=64)
     elif case == "long_card":
         inst = synth.config3(0, n=3000, m3=300, n_card=6, kmin=100, kmax=900)
-    else:
+    elif case == "large_n":
         inst = synth.random_mixed(n=40000, m=3000, seed=22, kmax=40)
+    else:   # rows longer than 128 literals (check_long_kernel) with the sign words read without the shared tile
+        inst = synth.config3(1, n=30000, m3=300, n_card=5, kmin=150, kmax=700)
     ctx = P.Context.from_instance(inst, device=0)
     B = 77
     s = ctx.search(B, seed=5)
