@@ -275,6 +275,23 @@ dev::PgdArgs pgd_args(ffsat_search* s, int mode, bool checked) {
     return a;
 }
 
+// The (non-fused) PGD step: one CTA per point, 1024 threads when n >= 2048 (the per-point row loop is the latency),
+// else 256 -- chosen from n only (batch-independent bits); fp32 follows the gradient reduction programmatically.
+void launch_pgd_step(ffsat_search* s, const dev::PgdArgs& a, cudaStream_t st, bool pdl) {
+    const bool f64 = s->ctx->Lo.precision == 64, wide = s->ctx->Lo.n >= 2048;
+    const dim3 g((unsigned)s->B);
+    if (f64) {
+        if (wide) dev::pgd_step_kernel<double, 1024><<<g, 1024, 0, st>>>(a);
+        else dev::pgd_step_kernel<double, 256><<<g, 256, 0, st>>>(a);
+    } else if (pdl) {
+        if (wide) launch_pdl(dev::pgd_step_kernel<float, 1024>, g, dim3(1024), 0, st, a);
+        else launch_pdl(dev::pgd_step_kernel<float, 256>, g, dim3(256), 0, st, a);
+    } else {
+        if (wide) dev::pgd_step_kernel<float, 1024><<<g, 1024, 0, st>>>(a);
+        else dev::pgd_step_kernel<float, 256><<<g, 256, 0, st>>>(a);
+    }
+}
+
 dev::FistaArgs fista_args(ffsat_search* s, int mode, bool checked) {
     dev::FistaArgs f{};
     f.p = pgd_args(s, mode, checked);
@@ -322,8 +339,7 @@ void search_begin_round(ffsat_search* s, cudaStream_t st) {
     } else {
         if (f64) search_eval<double>(s, s->X.p, s->fX.as<double>(), s->Gx.p, nullptr, st);
         else search_eval<float>(s, s->X.p, s->fX.as<double>(), s->Gx.p, nullptr, st);
-        if (f64) dev::pgd_step_kernel<double><<<(unsigned)s->B, 256, 0, st>>>(a);
-        else dev::pgd_step_kernel<float><<<(unsigned)s->B, 256, 0, st>>>(a);
+        launch_pgd_step(s, a, st, false);
     }
     CK(cudaGetLastError());
     s->iters_issued = 0;
@@ -406,10 +422,10 @@ void search_iterate_one(ffsat_search* s, bool checked, cudaStream_t st) {
         launch_pdl(dev::pgd_fused_kernel<float>, dim3((unsigned)s->B), dim3(256), 0, st, a, r);
     } else if (f64) {
         search_eval<double>(s, s->Xp.p, s->fP.as<double>(), s->Gp.p, u, st);
-        dev::pgd_step_kernel<double><<<(unsigned)s->B, 256, 0, st>>>(a);
+        launch_pgd_step(s, a, st, false);
     } else {
         search_eval<float>(s, s->Xp.p, s->fP.as<double>(), s->Gp.p, u, st);
-        launch_pdl(dev::pgd_step_kernel<float>, dim3((unsigned)s->B), dim3(256), 0, st, a);
+        launch_pgd_step(s, a, st, true);
     }
     CK(cudaGetLastError());
 }

@@ -78,10 +78,11 @@ struct PgdArgs {
 // one CTA (256 threads) per point.  The point's search state is loaded first (one latency), the decision is thread 0's,
 // then one pass over the point's row: accept (x <- x', g <- g') and the next trial x'' = clip(x - eta g) with
 // <g, x'' - x> (warp sums, then the warp sums in order: a fixed order).
-template <typename T>
-__global__ void __launch_bounds__(256) pgd_step_kernel(PgdArgs a) {
+// NT threads per CTA (a function of n only, so a point's bits never depend on the batch: 1024 for n >= 2048)
+template <typename T, int NT = 256>
+__global__ void __launch_bounds__(NT) pgd_step_kernel(PgdArgs a) {
     pdl_wait();   // launched programmatically after the gradient reduction
-    __shared__ double s_red[8];
+    __shared__ double s_red[NT / 32];
     __shared__ int s_acc, s_done;
     __shared__ double s_eta;
     const int64_t b = blockIdx.x;
