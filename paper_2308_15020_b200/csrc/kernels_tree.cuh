@@ -6,7 +6,8 @@
 // f_i(z) = (1 - p_i) + p_i z (so prod_i f_i = sum_t P(T = t) z^t, T = number of True literals):
 //   bottom-up   node polynomial P_S = P_left * P_right (schoolbook convolution; leaves are blocks of 16 literals,
 //               computed by the sequential Bernoulli recurrence of Alg. 5's forward pass);
-//   root        FE = sum_t f(t) P_root[t] (Def. 3 / Thm. 1: the multilinear extension of the truth-by-count table);
+//   root        FE = sum_t f(t) P_root[t] (Def. 3 / Thm. 1: the multilinear extension of the truth-by-count table)
+//               = sum_s P_L[s] lambda_L[s] with the root's left child: the root product itself is never formed;
 //   top-down    the linear functional L(g) = sum_t f(t) [z^t] g pushed down the tree: lambda_root = f, and for a
 //               node S with children L, R: lambda_L[t] = sum_s lambda_S[t + s] P_R[s] (the functional g ->
 //               L(g * prod_{j not in L} f_j) restricted to L's degree), symmetrically for R;
@@ -389,26 +390,30 @@ __global__ void __launch_bounds__(kTreeThreads, 1) sym_tree_kernel(SymArgs<doubl
                 __syncwarp();
             }
         }
-        for (int l = lw + 1; l <= g.Lv; ++l) {
+        // (the root's own product is never formed: FE comes from its left child below)
+        for (int l = lw + 1; l < g.Lv; ++l) {
             __syncthreads();
             tree_up_level(g, s_hs, sm, l, 0, 1 << (g.Lv - l), tid, kTreeThreads);
         }
         __syncthreads();
-        // ---- root: lambda = f, FE = sum_t f(t) P_root[t]
-        const double* Proot = sm + g.off[g.Lv] + kTreePad;
+        // ---- root functional lambda = f
         double* lam = sm + g.lamX + kTreePad;
-        double fe = 0.0;
-        for (int t = tid; t <= k; t += kTreeThreads) {
-            const double ft = tree_f(t, sg);
-            fe = fma(ft, Proot[t], fe);
-            lam[t] = ft;
-        }
-        fe = tree_block_sum(fe, s_red);   // (its barriers also publish lambda_root)
+        for (int t = tid; t <= k; t += kTreeThreads) lam[t] = tree_f(t, sg);
+        __syncthreads();
         // ---- top-down: levels Lv..lw+1 by the CTA, then lw..2 and the leaves per warp
         int cur = g.lamX, nxt = g.lamY;
+        double fe = 0.0;
         for (int l = g.Lv; l > lw; --l) {
             tree_down_level(g, s_hs, sm, l, 0, 1 << (g.Lv - l), cur, nxt, tid, kTreeThreads);
             __syncthreads();
+            if (l == g.Lv) {   // FE = L(P_L P_R) = sum_s P_L[s] lambda_L[s] (lambda_L = corr(f, P_R), just formed)
+                const TreeNode cl = tree_node(g, s_hs, g.Lv - 1, 0);
+                const double* pl = sm + g.off[g.Lv - 1] + cl.pos;
+                const double* ll = sm + nxt + cl.pos;
+                double v = 0.0;
+                for (int t = tid; t <= cl.deg; t += kTreeThreads) v = fma(pl[t], ll[t], v);
+                fe = tree_block_sum(v, s_red);
+            }
             const int tsw = cur;
             cur = nxt;
             nxt = tsw;

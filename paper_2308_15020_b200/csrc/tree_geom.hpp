@@ -89,7 +89,8 @@ inline int64_t tree_fp64_work(int k) {
     w += (int64_t)k * (2 * 16 + 2 * 16);
     for (int h = 1; h < (1 << (g.Lv - 1)); ++h) {   // nodes of levels 2..Lv
         const int64_t dA = deg(2 * h), dB = deg(2 * h + 1);
-        if (dB > 0) w += (dA + 1) * (dB + 1) * 3;   // bottom-up product + the two top-down correlations
+        // bottom-up product (not for the root: FE comes from its left child's functional) + the two top-down correlations
+        if (dB > 0) w += (dA + 1) * (dB + 1) * (h == 1 ? 2 : 3) + (h == 1 ? dA + 1 : 0);
     }
     return w;
 }
