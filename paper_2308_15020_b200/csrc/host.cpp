@@ -473,7 +473,7 @@ Layout build_layout(const Formula& F, int path, int precision) {
         const int R = G == kTreeClass ? 0 : sym_roots(k);
         if (G == kTreeClass) {
             Lo.n_tree_cons += 1;
-            Lo.tree_work += tree::tree_fp64_work(k);
+            Lo.tree_work += tree::tree_fp64_work(k, r.parity);
         }
         if (Lo.sym_classes.empty() || Lo.sym_classes.back().G != G || Lo.sym_classes.back().C != C)
             Lo.sym_classes.push_back({G, C, R, s, s + 1, 0});

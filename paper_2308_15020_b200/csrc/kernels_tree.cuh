@@ -165,6 +165,32 @@ __device__ __forceinline__ double tree_block_sum(double v, double* red) {
     return t;
 }
 
+// Inclusive prefix sums out[i] = in[0] + ... + in[i], i < len, by the CTA in a fixed order (each thread a contiguous
+// segment, then the segment totals scanned by warp shuffles and the warps in order): deterministic.
+__device__ __forceinline__ void tree_block_scan(const double* in, double* out, int len, double* s_tot) {
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int seg = (len + kTreeThreads - 1) / kTreeThreads;
+    const int i0 = tid * seg, i1 = min(len, i0 + seg);
+    double run = 0.0;
+    for (int i = i0; i < i1; ++i) run += in[i];
+    double inc = run;   // warp-inclusive scan of the segment totals
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const double y = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += y;
+    }
+    __syncthreads();
+    if (lane == 31) s_tot[warp] = inc;
+    __syncthreads();
+    double off = inc - run;
+    for (int w = 0; w < warp; ++w) off += s_tot[w];
+    for (int i = i0; i < i1; ++i) {
+        off += in[i];
+        out[i] = off;
+    }
+    __syncthreads();
+}
+
 // Bottom-up level l >= 2: the polynomials of nodes [j0, j1) from their children, by threads ti of nt (nt a multiple of
 // 32; whole warps take part: the share sums use shuffles).  Units of kTreeR outputs x P inner-index shares.
 __device__ __forceinline__ void tree_up_level(const TreeGeom& g, const short* hs, double* sm, int l, int j0, int j1, int ti, int nt) {
@@ -404,7 +430,24 @@ __global__ void __launch_bounds__(kTreeThreads, 1) sym_tree_kernel(SymArgs<doubl
         int cur = g.lamX, nxt = g.lamY;
         double fe = 0.0;
         for (int l = g.Lv; l > lw; --l) {
-            tree_down_level(g, s_hs, sm, l, 0, 1 << (g.Lv - l), cur, nxt, tid, kTreeThreads);
+            if (l == g.Lv && sg.parity == 0) {
+                // root of an interval rule (satisfied iff tmin <= t <= tmax: f = 1 - 2 [tmin <= t <= tmax]): the root's
+                // correlations in O(k) from the children's cumulative sums, lambda_L[s] = sum_u f(s + u) P_R[u] =
+                // T_R - 2 (C_R(tmax - s) - C_R(tmin - s - 1)) (C_R(i) = sum_{u <= i} P_R[u], 0 for i < 0), likewise R
+                const TreeNode cl = tree_node(g, s_hs, g.Lv - 1, 0), cr = tree_node(g, s_hs, g.Lv - 1, 1);
+                double* CL = sm + cur;                     // lambda_root = f is not needed on this path: scratch
+                double* CR = sm + cur + cl.deg + 1;
+                tree_block_scan(sm + g.off[g.Lv - 1] + cl.pos, CL, cl.deg + 1, s_red);
+                tree_block_scan(sm + g.off[g.Lv - 1] + cr.pos, CR, cr.deg + 1, s_red);
+                const double TL = CL[cl.deg], TR = CR[cr.deg];
+                auto cdf = [](const double* C, int d, int i) { return i < 0 ? 0.0 : C[min(i, d)]; };
+                for (int t = tid; t <= cl.deg; t += kTreeThreads)
+                    sm[nxt + cl.pos + t] = TR - 2.0 * (cdf(CR, cr.deg, sg.tmax - t) - cdf(CR, cr.deg, sg.tmin - t - 1));
+                for (int t = tid; t <= cr.deg; t += kTreeThreads)
+                    sm[nxt + cr.pos + t] = TL - 2.0 * (cdf(CL, cl.deg, sg.tmax - t) - cdf(CL, cl.deg, sg.tmin - t - 1));
+            } else {
+                tree_down_level(g, s_hs, sm, l, 0, 1 << (g.Lv - l), cur, nxt, tid, kTreeThreads);
+            }
             __syncthreads();
             if (l == g.Lv) {   // FE = L(P_L P_R) = sum_s P_L[s] lambda_L[s] (lambda_L = corr(f, P_R), just formed)
                 const TreeNode cl = tree_node(g, s_hs, g.Lv - 1, 0);

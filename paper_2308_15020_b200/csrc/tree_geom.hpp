@@ -67,7 +67,7 @@ FFSAT_HD inline TreeGeom tree_geom(int k) {
 // FP64 instructions of one item on the tree path (the algorithmic count of the roofline): one DFMA per
 // multiply-add of the level convolutions (bottom-up, levels 2..Lv) and correlations (top-down, levels Lv..2) over the
 // real degrees, plus the level-1 / leaf stage.
-inline int64_t tree_fp64_work(int k) {
+inline int64_t tree_fp64_work(int k, int parity) {
     const TreeGeom g = tree_geom(k);
     // node pair ranges, heap order (root 1, children 2h, 2h + 1), as the kernel builds them
     int64_t start[1 << 10], endb[1 << 10];
@@ -89,8 +89,12 @@ inline int64_t tree_fp64_work(int k) {
     w += (int64_t)k * (2 * 16 + 2 * 16);
     for (int h = 1; h < (1 << (g.Lv - 1)); ++h) {   // nodes of levels 2..Lv
         const int64_t dA = deg(2 * h), dB = deg(2 * h + 1);
-        // bottom-up product (not for the root: FE comes from its left child's functional) + the two top-down correlations
-        if (dB > 0) w += (dA + 1) * (dB + 1) * (h == 1 ? 2 : 3) + (h == 1 ? dA + 1 : 0);
+        // bottom-up product + the two top-down correlations; at the root no product (FE comes from its left child's
+        // functional: dA + 1 FMAs) and, for an interval rule (parity 0), the correlations from cumulative sums (~4 k)
+        if (dB > 0) {
+            if (h != 1) w += (dA + 1) * (dB + 1) * 3;
+            else w += (parity == 0 ? 4 * (dA + dB + 2) : (dA + 1) * (dB + 1) * 2) + dA + 1;
+        }
     }
     return w;
 }
