@@ -180,3 +180,31 @@ def test_global_units_length_classes(maker):
         last_cls, last_k = cls, k
         covered += count
     assert covered == ctx.info["n_fast_cons"]
+
+
+def test_product_tree_classification(monkeypatch):
+    """fp64 symmetric constraints of 256..2048 literals take the product-tree path (ffsat_info n_tree_cons, its FP64
+    instruction count tree_work, the root path's k M' count sym_root_lits only for the others); FFSAT_TREE=0 keeps
+    them on the root path; fp32 contexts never use the tree."""
+    inst = synth.config3(0, n=3000, m3=50, n_card=4, kmin=300, kmax=2000)
+    c = _ctx(inst)
+    assert c.info["n_tree_cons"] == 4 and c.info["tree_work"] > 0 and c.info["sym_root_lits"] == 0
+    ks = [len(set(inst.lits[inst.offsets[i]:inst.offsets[i + 1]])) for i in range(inst.m - 4, inst.m)]
+    # the tree's FP64 count is far below the root path's 12 k M' (about k^2 / 1.3 vs 6 k^2)
+    assert c.info["tree_work"] < sum(12 * k * ((k + 1) // 2) for k in ks) / 5
+    monkeypatch.setenv("FFSAT_TREE", "0")
+    r = _ctx(inst)
+    assert r.info["n_tree_cons"] == 0 and r.info["sym_root_lits"] == sum(k * ((k + 1) // 2) for k in ks)
+    monkeypatch.delenv("FFSAT_TREE")
+    f32 = P.Context.from_instance(inst, precision=32, device=-1)
+    assert f32.info["n_tree_cons"] == 0
+
+
+def test_solve_params_defaults_and_fista_flag():
+    """ffsat_default_params: the documented defaults, accel = 0 (monotone Armijo, reading #16); accel = 1
+    selects FISTA (reading #16b)."""
+    p = P.ffsat_default_params()
+    assert (p.eta0, p.eta_min, p.armijo_c1, p.alpha, p.max_inner, p.check_every, p.policy, p.adaptive_weights) == \
+        (1.0, 1e-12, 1e-4, 0.4, 500, 10, 0, 1)
+    assert p.accel == 0 and p.reserved == 0
+    assert P.ffsat_default_params(accel=1).accel == 1
