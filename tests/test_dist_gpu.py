@@ -203,3 +203,42 @@ def test_portfolio_real_library(tmp_path):
         p = np.load(out + f".{r}.npz")
         assert int(p["sat"]) == 1 and int(p["rounds"]) == one["rounds"] and int(p["point"]) == one["point"]
         assert int(p["strategy"]) == one["strategy"] and np.array_equal(p["a"], one["assignment"])
+
+
+# ------------------------------------------------------------------------------------------ NCCL on the library's buffers
+
+def test_nccl_collectives_on_library_buffers():
+    """The collectives dist.py issues, over an NCCL process group (one rank: the box has one GPU), on the library's own
+    device buffers (zero-copy views of ffsat_search_get_buffers / the ShardedEval outputs): U_c SUM (int32), the keys
+    MIN (int64), f / grad / unsat SUM (fp64 / fp32 / int32) and the assignment broadcast (int8) -- NCCL accepts
+    every buffer and dtype, and a one-rank reduction leaves the values unchanged."""
+    torch.cuda.set_device(0)
+    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{free_port()}", rank=0, world_size=1)
+    try:
+        inst = _restart_inst()
+        ctx = P.Context.from_instance(inst, device=0)
+        s = ctx.search(64, seed=SEED, max_inner=ROUND_LEN)
+        s.begin_round()
+        s.iterate(3)
+        s.check()
+        s.reduce()
+        T = s.tensors()
+        torch.cuda.synchronize()
+        U0, k0 = T["U"].clone(), T["keys"].clone()
+        dist.all_reduce(T["U"], op=dist.ReduceOp.SUM)
+        dist.all_reduce(T["keys"], op=dist.ReduceOp.MIN)
+        a = torch.as_tensor(s.assignment(0), device="cuda")
+        a0 = a.clone()
+        dist.broadcast(a, src=0)
+        torch.cuda.synchronize()
+        assert torch.equal(T["U"], U0) and torch.equal(T["keys"], k0) and torch.equal(a, a0)
+        se = D.ShardedEval(inst.arrays(), 0, 1, device=0, precision=32)
+        X = torch.from_numpy(synth.points("U", 32, inst.n, 5)).cuda()
+        f, g, u = se.eval(X)
+        f0, g0, u0 = f.clone(), g.clone(), u.clone()
+        for t in (f, g, u):
+            dist.all_reduce(t, op=dist.ReduceOp.SUM)
+        torch.cuda.synchronize()
+        assert torch.equal(f, f0) and torch.equal(g, g0) and torch.equal(u, u0)
+    finally:
+        dist.destroy_process_group()
