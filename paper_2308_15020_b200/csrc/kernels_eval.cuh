@@ -2254,7 +2254,23 @@ __global__ void __launch_bounds__(32 * NWF) reduce_f_kernel(ReduceFArgs a) {
     int u = 0;
     if (b < a.B) {
         const bool cu = a.unsat != nullptr;   // the unsat partials exist only when the evaluation counted them
-        for (int c = w; c < a.n_parts; c += NWF) {
+        // rows w, w + NWF, ...: loads issued 8 at a time (one latency per batch), added strictly in row order
+        int c = w;
+        for (; c + 7 * NWF < a.n_parts; c += 8 * NWF) {
+            double fv[8];
+            int uv[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                fv[j] = a.fpart[(int64_t)(c + j * NWF) * a.B + b];
+                uv[j] = cu ? a.upart[(int64_t)(c + j * NWF) * a.B + b] : 0;
+            }
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                f += fv[j];
+                u += uv[j];
+            }
+        }
+        for (; c < a.n_parts; c += NWF) {
             f += a.fpart[(int64_t)c * a.B + b];
             if (cu) u += a.upart[(int64_t)c * a.B + b];
         }
