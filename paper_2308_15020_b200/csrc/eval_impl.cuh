@@ -195,6 +195,8 @@ void eval_device_t(ffsat_ctx* c, Scratch& S, const T* x, int64_t B, double* f, T
             a.xT = S.xT.as<T>(); a.B = B; a.n = L.n; a.words = c->fast_words.as<uint32_t>();
             a.units = c->units.as<dev::UnitDev>(); a.buckets = c->buckets.as<dev::FastBucketDev>();
             a.chunk_units = c->chunk_units.as<int32_t>(); a.w_pos = w_pos; a.Tb = S.Tb.as<T>();
+            // the fast terms' T rows fit in L2 (126 MB): plain stores, the reduction reads them back from L2
+            a.t_keep = (double)L.tb_fast * (double)B * sizeof(T) <= 100.0 * (1 << 20) ? 1 : 0;
             a.fpart = S.fpart.as<double>(); a.upart = S.upart.as<int32_t>();
             // several groups: off the profiling path groups 1, 2 run on side streams, concurrently with group 0
             // (disjoint chunks, T slots and partial rows); joined with the root-path classes below

@@ -1153,7 +1153,16 @@ struct GlobalArgs {
     T* Tb;                       // [tb_slots][B]
     double* fpart;
     int32_t* upart;
+    int32_t t_keep;              // 1: the term buffer fits in L2 -- plain stores (the reduction reads it back from L2);
+                                 // 0: streaming stores (keep x^T in L2 instead)
 };
+
+// T-buffer store: streaming (evict-first) unless the whole buffer fits in L2 and is read back right away
+template <typename T>
+__device__ __forceinline__ void t_store(T* p, T v, int keep) {
+    if (keep) *p = v;
+    else __stcs(p, v);
+}
 
 // Terms of one constraint for one lane from its literal words and gathered variable values (k <= 16):
 // term_i = w d FE / d x_{v_i} (literal sign folded into the factor slope, as in tiled_clause).
@@ -1223,7 +1232,7 @@ __device__ __forceinline__ void global_unit(const GlobalArgs<T>& a, const Bucket
             clause_terms<T, K, NCH>(bk, w[q], x[q], wc[q], g, facc, uacc);
             if (bv) {
 #pragma unroll
-                for (int i = 0; i < K; ++i) __stcs(a.Tb + (sbase + (int64_t)(j + q * nw) * K + i) * a.B + b, g[i]);   // streaming: keep x^T in L2
+                for (int i = 0; i < K; ++i) t_store(a.Tb + (sbase + (int64_t)(j + q * nw) * K + i) * a.B + b, g[i], a.t_keep);
             }
         }
     }
@@ -1351,7 +1360,7 @@ __device__ void global_unit_long_cp(const GlobalArgs<T>& a, const BucketReg<T>& 
                 const T cs = flip_sign(c1, w);
                 const T p = ps[32 * i] * suf;
                 T* d = dst + (size_t)i * (size_t)a.B;
-                if (c == 0) __stcs(d, p * cs);
+                if (c == 0) t_store(d, p * cs, a.t_keep);
                 else *d = fmaT(p, cs, *d);
                 suf *= fmaT(cs, xs[32 * i], c0);
             }
@@ -1359,7 +1368,7 @@ __device__ void global_unit_long_cp(const GlobalArgs<T>& a, const BucketReg<T>& 
         if (NCH == 0) {
             for (int i = 0; i < k; ++i) {
                 t += lit_true(xs[32 * i], ws[i]);
-                __stcs(dst + (size_t)i * (size_t)a.B, (T)0);
+                t_store(dst + (size_t)i * (size_t)a.B, (T)0, a.t_keep);
             }
         }
         facc += (double)(wc * fe);
