@@ -12,10 +12,12 @@ void launch_tree_class(const SymClass& cl, const dev::SymArgs<double>& a, int ma
     if (items == 0) return;
     const size_t smem = (size_t)tree::tree_geom(max_k).total * sizeof(double);
     if (smem > tree::kTreeSmemMax) throw Error(FFSAT_ERR_ARG, "product-tree constraint does not fit in shared memory");
-    static size_t set_bytes = 0;
-    if (smem > set_bytes) {
+    static bool set_on[64] = {};   // the attribute is per device
+    int devi = 0;
+    CK(cudaGetDevice(&devi));
+    if (devi < 0 || devi >= 64 || !set_on[devi]) {
         CK(cudaFuncSetAttribute(dev::sym_tree_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tree::kTreeSmemMax));
-        set_bytes = tree::kTreeSmemMax;
+        if (devi >= 0 && devi < 64) set_on[devi] = true;
     }
     CK(cudaMemsetAsync(counter, 0, sizeof(int32_t), st));
     const unsigned grid = (unsigned)std::min<int64_t>(items, num_sm);
