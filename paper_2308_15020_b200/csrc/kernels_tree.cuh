@@ -10,16 +10,20 @@
 //               = sum_s P_L[s] lambda_L[s] with the root's left child: the root product itself is never formed;
 //   top-down    the linear functional L(g) = sum_t f(t) [z^t] g pushed down the tree: lambda_root = f, and for a
 //               node S with children L, R: lambda_L[t] = sum_s lambda_S[t + s] P_R[s] (the functional g ->
-//               L(g * prod_{j not in L} f_j) restricted to L's degree), symmetrically for R;
+//               L(g * prod_{j not in L} f_j) restricted to L's degree), symmetrically for R; at the root of an
+//               interval rule (f = 1 - 2 [tmin <= t <= tmax]) from the children's cumulative sums in O(k);
 //   leaves      for literal i in block g: dFE/dp_i = L(prod_{j != i} f_j (z - 1)) = sum_s delta_g[s] Q_i[s] with
-//               delta_g[s] = lambda_g[s + 1] - lambda_g[s] and Q_i = prod_{j in g, j != i} f_j; dFE/dl_i = -dFE/dp_i / 2.
+//               delta_g[s] = lambda_g[s + 1] - lambda_g[s] and Q_i = P_g / f_i (one stable synthetic division);
+//               dFE/dl_i = -dFE/dp_i / 2.
 // Every quantity is a probability vector or a functional bounded by max |f| = 1 combined with convex weights, so the
-// fp64 result is accurate to a few ulps times the tree depth.  Work per item ~ k^2 / 2 (bottom-up) + k^2 (top-down)
-// fused multiply-adds, against 12 k M' (~6 k^2) FP64 instruction slots of the root-of-unity path.
+// fp64 result is accurate to a few ulps times the tree depth.  Work per item ~ k^2 / 4 (bottom-up below the root) +
+// k^2 / 2 (top-down below the root) fused multiply-adds, against 12 k M' (~6 k^2) FP64 instruction slots of the
+// root-of-unity path.
 //
 // Mapping: one CTA of 512 threads per item (persistent CTAs take items from an atomic counter, longest constraints
 // first; results do not depend on the assignment).  The polynomials of every tree level and two functional buffers
-// live in shared memory.  A work unit computes R = 9 consecutive outputs of one node over a share of the inner index
+// live in shared memory (k <= 2048); the tree is balanced over 32-literal pairs; the levels below Lv - 4 run as 16
+// warp-local subtrees.  A work unit computes R = 9 consecutive outputs of one node over a share of the inner index
 // (the share's partial sums are combined with warp shuffles in a fixed order): one operand is read as a broadcast,
 // the other through a register ring (one new element per step: 9 FMAs per 2 shared loads); R odd keeps the windowed
 // loads of 32 lanes (stride R doubles) bank-conflict-free.
