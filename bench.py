@@ -422,9 +422,12 @@ def main():
 
     if cfg["mode"] == "constraint":
         xs = torch.from_numpy(synth.points("U", B, inst.n, 1000, np.float64)).to(dt).to(dev)
+        # over several ranks the C3 all-reduce of one half of the batch overlaps the evaluation of the other half
+        # (ShardedEval chunks; the same bits as one block); FFSAT_C3_CHUNKS overrides
+        c3_chunks = int(os.environ.get("FFSAT_C3_CHUNKS", "2" if world > 1 else "1"))
 
         def step(i):
-            se.eval(xs)
+            se.eval(xs, chunks=c3_chunks)
     else:
         search = ctx.search(B, seed=20230815, point0=rank * B, max_inner=args.round_len, check_every=args.round_len)
         rs = D.RestartSharded(search, args.round_len, rank, world)
@@ -483,7 +486,7 @@ def main():
 
         def host_eval():
             xdev.copy_(xh, non_blocking=True)
-            f_, g_, _ = se.eval(xdev)
+            f_, g_, _ = se.eval(xdev, chunks=c3_chunks)
             fh.copy_(f_, non_blocking=True)
             gh.copy_(g_, non_blocking=True)
             torch.cuda.synchronize()

@@ -92,12 +92,28 @@ class ShardedEval:
                 return self.ctx.eval(x, grad=True, unsat=True)
         self._evaluate = evaluate
 
-    def eval(self, x):
-        f, g, u = self._evaluate(x)
-        if self.world > 1:
-            for t in (f, g, u):
-                self.dist.all_reduce(t, op=self.dist.ReduceOp.SUM, group=self.group)
-        return f, g, u
+    def eval(self, x, chunks: int = 1):
+        """chunks > 1 (and world > 1): the batch in `chunks` row blocks, the all-reduce of block i issued
+        asynchronously so it overlaps the evaluation of block i + 1; the library's launch plan is
+        batch-independent, so the results are the same bits as one block."""
+        if self.world <= 1 or chunks <= 1 or x.shape[0] < 2 * chunks:
+            f, g, u = self._evaluate(x)
+            if self.world > 1:
+                for t in (f, g, u):
+                    self.dist.all_reduce(t, op=self.dist.ReduceOp.SUM, group=self.group)
+            return f, g, u
+        import torch
+        B = x.shape[0]
+        cuts = [B * i // chunks for i in range(chunks + 1)]
+        parts, works = [], []
+        for i in range(chunks):
+            fi, gi, ui = self._evaluate(x[cuts[i]:cuts[i + 1]])
+            for t in (fi, gi, ui):
+                works.append(self.dist.all_reduce(t, op=self.dist.ReduceOp.SUM, group=self.group, async_op=True))
+            parts.append((fi, gi, ui))
+        for w in works:
+            w.wait()
+        return tuple(torch.cat([p[j] for p in parts]) for j in range(3))
 
 
 INT64_MAX = (1 << 63) - 1

@@ -55,10 +55,14 @@ def _sharded_worker(rank, world, port, out):
     _init(rank, world, port)
     inst = _sharded_inst()
     X = synth.points("U", 96, inst.n, 43)
-    se = D.ShardedEval(inst.arrays(), rank, world, device=0, precision=32)
+    se = D.ShardedEval(inst.arrays(), rank, world, device=0, precision=32, batch_ref=96)
     f, g, u = se.eval(torch.from_numpy(X).cuda())
+    # the overlapped C3 (two row blocks, the all-reduce of the first during the evaluation of the second)
+    f2, g2, u2 = se.eval(torch.from_numpy(X).cuda(), chunks=2)
     torch.cuda.synchronize()
-    np.savez(out + f".{rank}.npz", f=f.cpu().numpy(), g=g.cpu().numpy(), u=u.cpu().numpy(), r=np.array(se.range))
+    same = bool(torch.equal(f, f2) and torch.equal(g, g2) and torch.equal(u, u2))
+    np.savez(out + f".{rank}.npz", f=f.cpu().numpy(), g=g.cpu().numpy(), u=u.cpu().numpy(), r=np.array(se.range),
+             same=same)
     dist.destroy_process_group()
 
 
@@ -76,6 +80,7 @@ def test_constraint_sharded_eval_real_library(tmp_path):
         assert np.max(np.abs(p["f"] - fo) / np.maximum(1, np.abs(fo))) <= 1e-4
         assert np.max(np.abs(p["g"] - go) / np.maximum(1, np.abs(go))) <= 1e-4
         assert np.array_equal(p["u"], uo)
+        assert bool(p["same"])                          # chunked / overlapped: the same bits
 
 
 # ------------------------------------------------------------------------------------------ restart sharding

@@ -85,8 +85,11 @@ def _sharded_eval_worker(rank, world, port, out):
 
     se = D.ShardedEval(inst.arrays(), rank, world, evaluate=evaluate)
     f, g, u = se.eval(X)
+    # the overlapped variant (row blocks, asynchronous all-reduce of block i during block i + 1): the same bits
+    f2, g2, u2 = se.eval(torch.from_numpy(X), chunks=2)
+    same = bool(torch.equal(f2, f) and torch.equal(g2, g) and torch.equal(u2, u))
     if rank == 0:
-        np.savez(out, f=f.numpy(), g=g.numpy(), u=u.numpy(), r=np.array(se.range))
+        np.savez(out, f=f.numpy(), g=g.numpy(), u=u.numpy(), r=np.array(se.range), same=same)
     dist.destroy_process_group()
 
 
@@ -103,6 +106,7 @@ def test_constraint_sharded_eval_gloo(tmp_path):
     assert np.allclose(r["f"], f, rtol=0, atol=1e-12)
     assert np.allclose(r["g"], g, rtol=0, atol=1e-12)
     assert np.array_equal(r["u"], u)
+    assert bool(r["same"])
 
 
 # ---------------------------------------------------------------------------------------------- restart sharding
