@@ -366,15 +366,17 @@ def test_c2_full_size_sampled(dist):
     assert np.array_equal(u[idx], uo)
 
 
-def test_c3_full_size_sampled():
-    """c3 at full size (n=4096, 8192 clauses, 32 at-most-b of length 500..2000, fp64, B=32)."""
+@pytest.mark.parametrize("B", [32, 256])
+def test_c3_full_size_sampled(B):
+    """c3 at full size (n=4096, 8192 clauses, 32 at-most-b of length 500..2000, fp64) at both bench batch sizes
+    (B = 32: c3, B = 256: c3b256; the long constraints on the product tree), sampled points against the oracle."""
     inst = synth.config3(0)
-    X = synth.points("U", 32, inst.n, 1000, np.float64)
+    X = synth.points("U", B, inst.n, 1000, np.float64)
     ctx = P.Context.from_instance(inst, device=0)
     assert ctx.info["precision"] == 64
     f, g, u = ctx.eval(torch.from_numpy(X).cuda(), unsat=True)
     f, g, u = f.cpu().numpy(), g.cpu().numpy(), u.cpu().numpy()
-    idx = np.array([0, 17, 31])
+    idx = np.array([0, 17, 31]) if B == 32 else np.array([0, 100, 199, 255])
     Fo = oracle_of(inst)
     fo, go = cdp.evaluate(Fo, X[idx])
     uo, _ = cdp.check(Fo, X[idx])
