@@ -121,6 +121,8 @@ struct ffsat_ctx {
     int32_t f_groups = 8;                 // interleaved groups of the fixed-order f / unsat reduction (8 or 32)
     // scratch of the context's own evaluations; host-buffer staging
     ffsat::Scratch scr;
+    ffsat::Scratch scr2;                  // host-buffer evaluations: the second concurrent chunk's scratch
+    cudaStream_t comp2 = nullptr;         // ... and its compute stream
     ffsat::DBuf x_stage, g_stage, f_stage, u_stage, w_stage;
     // global path: chunk groups by bucket length class -- chunks [gchunk[g], gchunk[g + 1]) hold the units with
     // k <= 4 (g = 0), 4 < k <= 16 (g = 1), 16 < k (g = 2, the long kernel); each group is one launch
@@ -155,6 +157,7 @@ struct ffsat_ctx {
         if (ev_fork) cudaEventDestroy(ev_fork);
         if (copy_h2d) cudaStreamDestroy(copy_h2d);
         if (copy_d2h) cudaStreamDestroy(copy_d2h);
+        if (comp2) cudaStreamDestroy(comp2);
         for (cudaEvent_t e : ev_h2d) cudaEventDestroy(e);
         for (cudaEvent_t e : ev_done) cudaEventDestroy(e);
         if (nf_host) cudaFreeHost(nf_host);

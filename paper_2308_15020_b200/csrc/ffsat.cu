@@ -187,11 +187,12 @@ void need_device(const ffsat_ctx* c) {
 // ------------------------------------------------------------------------------------------------ eval
 
 void eval_device(ffsat_ctx* c, const void* x, int64_t B, double* f, void* grad, int32_t* unsat, cudaStream_t st,
-                 bool profiled = false) {
+                 bool profiled = false, Scratch* scr = nullptr) {
+    Scratch& S = scr ? *scr : c->scr;
     if (c->Lo.precision == 64)
-        eval_device_t<double>(c, c->scr, (const double*)x, B, f, (double*)grad, unsat, c->w_pos.as<double>(), st, profiled);
+        eval_device_t<double>(c, S, (const double*)x, B, f, (double*)grad, unsat, c->w_pos.as<double>(), st, profiled);
     else
-        eval_device_t<float>(c, c->scr, (const float*)x, B, f, (float*)grad, unsat, c->w_pos.as<float>(), st, profiled);
+        eval_device_t<float>(c, S, (const float*)x, B, f, (float*)grad, unsat, c->w_pos.as<float>(), st, profiled);
 }
 
 ffsat_status fail(ffsat_ctx* c, const Error& e) {
@@ -672,6 +673,10 @@ ffsat_status ffsat_eval(ffsat_ctx* c, const void* x, int64_t B, int32_t on_devic
     // chunks of at least batch_ref points: the launch plan is sized for batch_ref, a smaller chunk underfills the GPU
     int64_t nchunk = B < 512 ? 1 : xbytes >= (4u << 20) ? 4 : xbytes >= (2u << 20) ? 3 : 2;
     nchunk = std::max<int64_t>(1, std::min<int64_t>(nchunk, B / std::max<int64_t>(1, c->batch_ref)));
+    // tiled formulas without forked root-path work: two half-batch chunks evaluated CONCURRENTLY on two compute
+    // streams with their own scratch (each fills half the GPU; the copies of one overlap the other's evaluation)
+    const bool dual = nchunk == 1 && B >= 512 && c->Lo.path == 1 && c->Lo.n_sym == 0;
+    if (dual) nchunk = 2;
     const int64_t Bc = nchunk == 1 ? B : ((B + nchunk - 1) / nchunk + 63) / 64 * 64;
     const int64_t nck = Bc > 0 ? (B + Bc - 1) / Bc : 0;
     const size_t n = (size_t)c->Lo.n;
@@ -685,6 +690,7 @@ ffsat_status ffsat_eval(ffsat_ctx* c, const void* x, int64_t B, int32_t on_devic
         CK(cudaStreamCreateWithFlags(&c->copy_d2h, cudaStreamNonBlocking));
         CK(cudaMallocHost(&c->nf_host, 16));
     }
+    if (dual && !c->comp2) CK(cudaStreamCreateWithFlags(&c->comp2, cudaStreamNonBlocking));
     while ((int64_t)c->ev_h2d.size() < nck + 1) {
         cudaEvent_t e1, e2;
         CK(cudaEventCreateWithFlags(&e1, cudaEventDisableTiming));
@@ -705,20 +711,25 @@ ffsat_status ffsat_eval(ffsat_ctx* c, const void* x, int64_t B, int32_t on_devic
                                              cudaMemcpyHostToDevice, c->copy_h2d));
         CK(cudaEventRecord(c->ev_h2d[(size_t)i], c->copy_h2d));
     }
+    if (dual) {
+        ensure_scratch(c, c->scr, Bc);
+        ensure_scratch(c, c->scr2, Bc);
+    }
     for (int64_t i = 0; i < nck; ++i) {
         const int64_t r0 = i * Bc, r1 = std::min(B, r0 + Bc);
-        CK(cudaStreamWaitEvent(st, c->ev_h2d[(size_t)i], 0));
+        cudaStream_t cs = dual && i == 1 ? c->comp2 : st;
+        CK(cudaStreamWaitEvent(cs, c->ev_h2d[(size_t)i], 0));   // (also orders comp2 after st's prior work)
         const size_t cnt = (size_t)Bc * n;
         if (cnt) {
-            if (es == 8) dev::nonfinite_kernel<double><<<(unsigned)std::min<size_t>(1184, (cnt + 255) / 256), 256, 0, st>>>(
+            if (es == 8) dev::nonfinite_kernel<double><<<(unsigned)std::min<size_t>(1184, (cnt + 255) / 256), 256, 0, cs>>>(
                 (const double*)(xs + (size_t)r0 * n * es), (int64_t)cnt, c->nf_flag.as<int32_t>());
-            else dev::nonfinite_kernel<float><<<(unsigned)std::min<size_t>(1184, (cnt + 255) / 256), 256, 0, st>>>(
+            else dev::nonfinite_kernel<float><<<(unsigned)std::min<size_t>(1184, (cnt + 255) / 256), 256, 0, cs>>>(
                 (const float*)(xs + (size_t)r0 * n * es), (int64_t)cnt, c->nf_flag.as<int32_t>());
             c->launches += 1;
         }
         eval_device(c, xs + (size_t)r0 * n * es, Bc, c->f_stage.as<double>() + r0, grad_out ? gs + (size_t)r0 * n * es : nullptr,
-                    unsat_out ? c->u_stage.as<int32_t>() + r0 : nullptr, st);
-        CK(cudaEventRecord(c->ev_done[(size_t)i], st));
+                    unsat_out ? c->u_stage.as<int32_t>() + r0 : nullptr, cs, false, dual && i == 1 ? &c->scr2 : nullptr);
+        CK(cudaEventRecord(c->ev_done[(size_t)i], cs));
         CK(cudaStreamWaitEvent(c->copy_d2h, c->ev_done[(size_t)i], 0));
         const int64_t nr = r1 - r0;
         if (nr > 0) {
@@ -730,6 +741,7 @@ ffsat_status ffsat_eval(ffsat_ctx* c, const void* x, int64_t B, int32_t on_devic
     }
     CK(cudaMemcpyAsync(c->nf_host, c->nf_flag.p, 4, cudaMemcpyDeviceToHost, c->copy_d2h));
     CK(cudaStreamSynchronize(c->copy_d2h));
+    if (dual) CK(cudaStreamSynchronize(c->comp2));
     CK(cudaStreamSynchronize(st));
     if (*c->nf_host) throw Error(FFSAT_ERR_NONFINITE, "non-finite point coordinate");
     return FFSAT_OK;

@@ -885,6 +885,21 @@ def test_host_buffer_pipeline_matches_device(B):
     assert np.array_equal(fh, fd.cpu().numpy()) and np.array_equal(gh, gd.cpu().numpy())
 
 
+@pytest.mark.parametrize("B", [600, 1024, 1030])
+def test_host_buffer_dual_stream_matches_device(B):
+    """Host-buffer evaluation of a pure-CNF (tiled-path) formula: the batch splits into two half chunks evaluated
+    concurrently on two compute streams with separate scratch; against the oracle, and bit-identical to the
+    single-stream device-buffer evaluation."""
+    inst = synth.random_ksat(n=120, m=3000, k=7, seed=23)
+    X = synth.points("U", B, inst.n, 17)
+    ctx, _, _ = compare(inst, X, device_path=False)
+    assert ctx.info["path"] == 1
+    fh, gh, uh = ctx.eval(X, grad=True, unsat=True)
+    fd, gd, ud = ctx.eval(torch.from_numpy(X).cuda(), grad=True, unsat=True)
+    assert np.array_equal(uh, ud.cpu().numpy())
+    assert np.array_equal(fh, fd.cpu().numpy()) and np.array_equal(gh, gd.cpu().numpy())
+
+
 def test_host_buffer_nonfinite_rejected():
     """a non-finite coordinate in a host batch gives FFSAT_ERR_NONFINITE (flagged on the device)."""
     inst = synth.config1(0)
