@@ -280,7 +280,8 @@ def roofline_of(info, inst, B, ph, args):
     alu_src = (f"{SM_COUNT} SMs x {lanes} {'FP64' if f64 else 'FP32'} lanes x {mhz:.0f} MHz ({peak_src} sm_max_mhz); "
                "one FMA / MUL = one lane-op")
     res = {}
-    eval_kernels = ("transpose_kernel+fast_global_kernel+fast_global_long_kernel+owner_grad_kernel+reduce_grad_kernel+reduce_f_kernel"
+    eval_kernels = ("transpose_kernel+fast_global_kernel+fast_global_long_kernel+owner_grad_kernel+owner_grp_kernel+"
+                    "fold_rows_kernel+reduce_grad_kernel+reduce_f_kernel"
                     if info["path"] == 2 else "fast_wide_kernel+fast_tiled_kernel+reduce_grad_kernel+reduce_f_kernel")
     traffic_eval = ncu_traffic(eval_kernels, args.config, any_of=True)
     res["hbm"] = {"scope": "evaluation (A4-A7, every kernel)", "achieved": alg_bytes / (eval_ms * 1e-3) / 1e9,
@@ -291,9 +292,11 @@ def roofline_of(info, inst, B, ph, args):
     grad_ms = float(ph[2])
     own = info.get("n_own_lits", 0) > 0
     if own and grad_ms >= max(fast_ms, root_ms):
-        # global path, owner-computes: the short constraints' products are formed in owner_grad_kernel
+        # global path, owner-computes: the short constraints' products are formed in the owner kernel (grouped
+        # records when they are the only fast constraints, owner_grp_kernel; else owner_grad_kernel)
+        oname = "owner_grp_kernel" if info["n_own_lits"] == info["n_fast_lits"] else "owner_grad_kernel"
         res["alu"] = {
-            "scope": "owner_grad_kernel", "pipe": "fp64" if f64 else "fp32",
+            "scope": oname, "pipe": "fp64" if f64 else "fp32",
             "achieved": FAST_PRODUCTS_PER_TERM * terms_fast / (grad_ms * 1e-3) / 1e12, "peak": alu_peak,
             "unit": "T lane-op/s", "algorithmic_def": f"{FAST_PRODUCTS_PER_TERM} products per literal term (SURVEY 8(d))",
             "time_ms": grad_ms, "peak_source": alu_src}

@@ -102,7 +102,7 @@ struct ffsat_ctx {
     std::string err;
     // persistent device layout
     ffsat::DBuf fast_words, tiled_words, units, buckets, sym_words, sym_off, sym_sig, sigs, coef, occ_off, occ_slot,
-        w_pos, w_static_orig, order, chk_off, chk_words, chk_rule, chk_long, own_off, own_rec;
+        w_pos, w_static_orig, order, chk_off, chk_words, chk_rule, chk_long, own_off, own_rec, grp_desc, grp_var, grp_rec;
     int32_t n_chk_long = 0;              // rows longer than dev::kCheckLong (positions in chk_long)
     int64_t persistent_bytes = 0;
     // the batch-independent launch plan (plan_chunks, at load): chunk split of the fast kernels and root splits.

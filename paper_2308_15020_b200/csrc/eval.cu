@@ -131,7 +131,8 @@ void plan_chunks(ffsat_ctx* c) {
     // owner_grad_kernel's f / unsat partial rows, one per 8-variable tile, folded 256 to a row (fold_rows_kernel);
     // partial row layout: [chunk rows | folded rows | variable-tile rows]
     // the owner kernels' variable tiles (partial f rows): 256 / kOwnSlice variables (sliced) or 8 (unsliced)
-    c->n_vtiles = !L.own ? 0 : L.own_sliced ? (L.n + 256 / kOwnSlice - 1) / (256 / kOwnSlice) : (L.n + 7) / 8;
+    c->n_vtiles = !L.own ? 0 : L.own_uni >= 0 ? (L.n + 31) / 32
+                 : L.own_sliced ? (L.n + 256 / kOwnSlice - 1) / (256 / kOwnSlice) : (L.n + 7) / 8;
     c->n_fold = (c->n_vtiles + 255) / 256;
     const int64_t rows = (L.n_fast > 0 ? c->n_chunks + c->n_fold : 0) + L.n_sym;
     c->f_groups = rows > 256 ? 32 : 8;
@@ -175,7 +176,7 @@ void ensure_scratch(const ffsat_ctx* c, Scratch& S, int64_t B) {
     const size_t es = c->esize, b = (size_t)B;
     const size_t parts = (size_t)std::max<int64_t>(1, c->n_chunks + c->n_fold + c->n_vtiles);
     if (L.path == 1) S.P.ensure(std::max<size_t>(16, parts * L.n * b * es));
-    if (L.path == 2 || L.sym_lane) S.xT.ensure(std::max<size_t>(16, (size_t)L.n * ((b + kOwnSlice - 1) / kOwnSlice * kOwnSlice) * es));   // (sliced: whole slices)
+    if (L.path == 2 || L.sym_lane) S.xT.ensure(std::max<size_t>(16, (size_t)L.n * ((b + kOwnSliceMax - 1) / kOwnSliceMax * kOwnSliceMax) * es));   // (sliced: whole slices)
     S.Tb.ensure(std::max<size_t>(16, (size_t)L.tb_slots * b * es));
     S.fpart.ensure(parts * b * 8);
     S.upart.ensure(parts * b * 4);

@@ -86,6 +86,28 @@ dev::PmReduce<T> pm_reduce_args(const ffsat_ctx* c, const Scratch& S, int64_t B,
     return r;
 }
 
+// owner_grp_kernel for the bucket's (k, product channels) and the points per thread (float: 1, 2, 4; double: 1, 2)
+template <typename T, int K, int NCH>
+void launch_owner_grp_k(int ppt, dim3 grid, cudaStream_t st, const dev::OwnerArgs<T>& o, int32_t bucket) {
+    // rows per batch at 4 points per thread: 2 (80 registers, 3 CTAs per SM; 4 rows: 128 registers, 2 CTAs, slower)
+    static const int nb = [] { const char* e = std::getenv("FFSAT_OWN_NB"); return e && std::atoi(e) == 4 ? 4 : 2; }();
+    if (ppt == 1) dev::owner_grp_kernel<T, K, NCH, 1, 4><<<grid, 256, 0, st>>>(o, bucket);
+    else if (ppt == 2 || sizeof(T) == 8) dev::owner_grp_kernel<T, K, NCH, 2, 4><<<grid, 256, 0, st>>>(o, bucket);
+    else if (nb == 2) dev::owner_grp_kernel<T, K, NCH, (sizeof(T) == 4 ? 4 : 2), 2><<<grid, 256, 0, st>>>(o, bucket);
+    else dev::owner_grp_kernel<T, K, NCH, (sizeof(T) == 4 ? 4 : 2), 4><<<grid, 256, 0, st>>>(o, bucket);
+}
+template <typename T>
+void launch_owner_grp(int key, int ppt, dim3 grid, cudaStream_t st, const dev::OwnerArgs<T>& o, int32_t bucket) {
+    switch (key) {
+    case 11: launch_owner_grp_k<T, 1, 1>(ppt, grid, st, o, bucket); break;
+    case 12: launch_owner_grp_k<T, 1, 2>(ppt, grid, st, o, bucket); break;
+    case 21: launch_owner_grp_k<T, 2, 1>(ppt, grid, st, o, bucket); break;
+    case 22: launch_owner_grp_k<T, 2, 2>(ppt, grid, st, o, bucket); break;
+    case 31: launch_owner_grp_k<T, 3, 1>(ppt, grid, st, o, bucket); break;
+    default: launch_owner_grp_k<T, 3, 2>(ppt, grid, st, o, bucket); break;
+    }
+}
+
 template <typename T>
 void eval_device_t(ffsat_ctx* c, Scratch& S, const T* x, int64_t B, double* f, T* grad, int32_t* unsat, const T* w_pos,
                    cudaStream_t st, bool profiled, bool partials_only) {
@@ -101,7 +123,10 @@ void eval_device_t(ffsat_ctx* c, Scratch& S, const T* x, int64_t B, double* f, T
     const bool need_xT = L.path == 2 || L.sym_lane;
     if (need_xT && L.n > 0) {
         dim3 tg(blocks_for(L.n, 32), blocks_for(B, 32)), tb(32, 8);
-        if (L.own_sliced) dev::transpose_kernel<T, kOwnSlice><<<tg, tb, 0, st>>>(x, S.xT.as<T>(), B, L.n);
+        const int sw = L.own_uni >= 0 ? 8 * L.own_ppt : kOwnSlice;   // slice width of the owner kernel
+        if (L.own_sliced && sw == 32) dev::transpose_kernel<T, 32><<<tg, tb, 0, st>>>(x, S.xT.as<T>(), B, L.n);
+        else if (L.own_sliced && sw == 16) dev::transpose_kernel<T, 16><<<tg, tb, 0, st>>>(x, S.xT.as<T>(), B, L.n);
+        else if (L.own_sliced) dev::transpose_kernel<T, kOwnSlice><<<tg, tb, 0, st>>>(x, S.xT.as<T>(), B, L.n);
         else dev::transpose_kernel<T, 0><<<tg, tb, 0, st>>>(x, S.xT.as<T>(), B, L.n);
         c->launches += 1;
     }
@@ -272,17 +297,13 @@ void eval_device_t(ffsat_ctx* c, Scratch& S, const T* x, int64_t B, double* f, T
         o.Tb = S.Tb.as<T>(); o.occ_off = c->occ_off.as<int64_t>(); o.occ_slot = c->occ_slot.as<int32_t>(); o.grad = grad;
         o.fpart = S.fpart.as<double>(); o.upart = unsat ? S.upart.as<int32_t>() : nullptr;
         o.row0 = c->n_chunks + c->n_fold;
-        if (L.own_sliced && L.own_uni >= 0) {   // one owner bucket: coefficients once, branch-free records
-            dim3 grid(blocks_for(L.n, 256 / kOwnSlice), blocks_for(B, kOwnSlice));
+        if (L.own_sliced && L.own_uni >= 0) {   // one owner bucket: grouped records, coefficients once
+            o.grp_desc = c->grp_desc.as<uint4>(); o.grp_var = c->grp_var.as<int32_t>(); o.grp_rec = c->grp_rec.as<uint4>();
+            const int sw = 8 * L.own_ppt;
+            o.grp_pitch = (uint32_t)(sw * sizeof(T));
+            dim3 grid(blocks_for(L.n, 32), blocks_for(B, sw));
             const int key = L.fbuckets[(size_t)L.own_uni].k * 10 + fast_nch(L.fbuckets[(size_t)L.own_uni]);
-            switch (key) {
-            case 11: dev::owner_uni_kernel<T, kOwnSlice, 1, 1><<<grid, 256, 0, st>>>(o, L.own_uni); break;
-            case 12: dev::owner_uni_kernel<T, kOwnSlice, 1, 2><<<grid, 256, 0, st>>>(o, L.own_uni); break;
-            case 21: dev::owner_uni_kernel<T, kOwnSlice, 2, 1><<<grid, 256, 0, st>>>(o, L.own_uni); break;
-            case 22: dev::owner_uni_kernel<T, kOwnSlice, 2, 2><<<grid, 256, 0, st>>>(o, L.own_uni); break;
-            case 31: dev::owner_uni_kernel<T, kOwnSlice, 3, 1><<<grid, 256, 0, st>>>(o, L.own_uni); break;
-            default: dev::owner_uni_kernel<T, kOwnSlice, 3, 2><<<grid, 256, 0, st>>>(o, L.own_uni); break;
-            }
+            launch_owner_grp<T>(key, L.own_ppt, grid, st, o, L.own_uni);
         } else if (L.own_sliced) {   // kOwnSlice points x 256 / kOwnSlice variables per block
             dim3 grid(blocks_for(L.n, 256 / kOwnSlice), blocks_for(B, kOwnSlice));
             dev::owner_grad_kernel<T, kOwnSlice><<<grid, 256, 0, st>>>(o);

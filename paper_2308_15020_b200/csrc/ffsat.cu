@@ -117,7 +117,11 @@ void upload_layout(ffsat_ctx* c) {
         upload(c->w_pos, w);
     }
     upload(c->w_static_orig, c->F.weight);
-    if (L.own) {
+    if (L.own && L.own_uni >= 0) {
+        upload(c->grp_desc, L.grp_desc);
+        upload(c->grp_var, L.grp_var);
+        upload(c->grp_rec, L.grp_rec);
+    } else if (L.own) {
         upload(c->own_off, L.own_off);
         upload(c->own_rec, L.own_rec);
     }
@@ -148,7 +152,8 @@ void upload_layout(ffsat_ctx* c) {
     if (!longs.empty()) upload(c->chk_long, longs);
     for (DBuf* d : {&c->fast_words, &c->tiled_words, &c->units, &c->buckets, &c->sym_words, &c->sym_off,
                     &c->sym_sig, &c->sigs, &c->coef, &c->occ_off, &c->occ_slot, &c->w_pos, &c->w_static_orig, &c->order,
-                    &c->chk_off, &c->chk_words, &c->chk_rule, &c->chk_long, &c->own_off, &c->own_rec})
+                    &c->chk_off, &c->chk_words, &c->chk_rule, &c->chk_long, &c->own_off, &c->own_rec, &c->grp_desc,
+                    &c->grp_var, &c->grp_rec})
         c->persistent_bytes += (int64_t)d->bytes;
 }
 

@@ -490,16 +490,18 @@ Layout build_layout(const Formula& F, int path, int precision) {
         cl.S = cl.G <= 0 ? 1 : std::max(1, std::min(32, (cl.max_mp + root_chunk - 1) / root_chunk));
     }
 
-    // ---- owner-computes buckets (global path, FFSAT_OWN=1): no T slots; the other fast buckets' slots are renumbered
-    // densely.  Off by default: measured slower than the T-buffer path on c5 (round 1 2.65 vs
-    // 1.34 ms; round 2, x^T in L2-resident 8-point slices and one branch-free kernel for a single owner bucket, 1.71 vs
-    // 1.34 ms at 1.2 GB of DRAM traffic instead of 4.5 GB -- instruction-bound: the per-record work is repeated per
-    // slice).  When every fast constraint is short and no root-path class reads x^T, x^T is sliced (own_sliced).
+    // ---- owner-computes buckets (global path): no T slots; the other fast buckets' slots are renumbered densely.
+    // ON by default when the global path's fast constraints form ONE bucket of short constraints (k <= 3: uniform
+    // random 3-SAT, c5) and no root-path class reads x^T: x^T in 32-point slices and the grouped-record kernel
+    // (owner_grp_kernel: c5 evaluation 1.34 -> 0.92 ms, 2.4 GB of DRAM traffic instead of 4.7 GB).
+    // FFSAT_OWN=1 forces it for every global-path bucket with k <= 3 (owner_grad_kernel for mixed buckets: measured
+    // slower than the T-buffer path), FFSAT_OWN=0 turns it off.
     int own_kmax = 0;
     {
         bool short_only = path == 2 && !Lo.fbuckets.empty();
         for (const FastBucket& b : Lo.fbuckets) short_only = short_only && b.k <= kOwnKMax;
         if (const char* e = std::getenv("FFSAT_OWN")) own_kmax = (path == 2 && std::atoi(e) != 0) ? kOwnKMax : 0;
+        else if (short_only && Lo.fbuckets.size() == 1 && !Lo.sym_lane) own_kmax = kOwnKMax;
         Lo.own_sliced = own_kmax > 0 && short_only && !Lo.sym_lane;
     }
     {
@@ -520,7 +522,110 @@ Layout build_layout(const Formula& F, int path, int precision) {
             }
         if (nown != 1 || !Lo.own_sliced) Lo.own_uni = -1;
     }
-    if (Lo.own) {
+    if (Lo.own && Lo.own_uni >= 0) {
+        // one owner bucket: grouped, padded, interleaved records (owner_grp_kernel)
+        Lo.own_ppt = precision == 64 ? 2 : 4;   // one 32-point slice (fp64: 16-point slices, 16-byte gathers)
+        if (const char* e = std::getenv("FFSAT_OWN_PPT")) {
+            const int v = std::atoi(e);
+            Lo.own_ppt = v == 2 || v == 4 ? v : 1;
+        }
+        if (precision == 64 && Lo.own_ppt > 2) Lo.own_ppt = 2;
+        const FastBucket& b = Lo.fbuckets[(size_t)Lo.own_uni];
+        const int64_t n = F.n, nblk = (n + 31) / 32;
+        std::vector<int64_t> offA((size_t)n + 1, 0), offB((size_t)n + 1, 0);
+        for (int64_t p = b.pos_begin; p < b.pos_end; ++p) {
+            const uint32_t* wr = &Lo.fast_words[(size_t)(b.word_off + (p - b.pos_begin) * b.kp)];
+            for (int i = 0; i < b.k; ++i) (i == 0 ? offA : offB)[(size_t)(wr[i] & 0x7fffffffu) + 1]++;
+        }
+        for (int64_t v = 0; v < n; ++v) {
+            offA[(size_t)v + 1] += offA[(size_t)v];
+            offB[(size_t)v + 1] += offB[(size_t)v];
+        }
+        std::vector<std::array<uint32_t, 4>> recA((size_t)offA[(size_t)n]), recB((size_t)offB[(size_t)n]);
+        {
+            std::vector<int64_t> ca(offA.begin(), offA.end() - 1), cb(offB.begin(), offB.end() - 1);
+            for (int64_t p = b.pos_begin; p < b.pos_end; ++p) {
+                if (p > INT32_MAX) throw Error(FFSAT_ERR_ARG, "formula too large for 32-bit owner records");
+                const uint32_t* wr = &Lo.fast_words[(size_t)(b.word_off + (p - b.pos_begin) * b.kp)];
+                for (int i = 0; i < b.k; ++i) {
+                    const uint32_t v = wr[i] & 0x7fffffffu;
+                    std::array<uint32_t, 4> r{(uint32_t)p, 0u, 0u, wr[i] >> 31};
+                    int q = 1;
+                    for (int j = 0; j < b.k; ++j)
+                        if (j != i) r[(size_t)q++] = wr[j];
+                    (i == 0 ? recA[(size_t)ca[v]++] : recB[(size_t)cb[v]++]) = r;
+                }
+            }
+        }
+        Lo.grp_var.assign((size_t)(nblk * 32), -1);
+        Lo.grp_desc.assign((size_t)(nblk * 8 * 4), 0);
+        Lo.grp_rec.clear();
+        Lo.grp_rec.reserve((size_t)(Lo.n_own_lits * 4 * 5 / 4));
+        auto cntA = [&](int32_t v) { return v < 0 ? 0 : offA[(size_t)v + 1] - offA[(size_t)v]; };
+        auto cntB = [&](int32_t v) { return v < 0 ? 0 : offB[(size_t)v + 1] - offB[(size_t)v]; };
+        // windows of 8 blocks (256 variables): the window's variables sorted by occurrence counts and dealt in that
+        // order to its blocks and groups, so a group's lists, and a block's groups, have about equal lengths (little
+        // padding; no warp of a block idles at its barrier) -- the cheapest (padded rows) of three orders: by total
+        // count, by literal-0 count, by the other count.  (Variables past n: -1, sorted last.)
+        std::vector<int32_t> win_order;
+        for (int64_t blk = 0; blk < nblk; ++blk) {
+            if (blk % 8 == 0) {
+                const int64_t wb = std::min<int64_t>(8, nblk - blk) * 32;
+                int64_t best_cost = -1;
+                std::vector<int32_t> o((size_t)wb);
+                for (int key = 0; key < 3; ++key) {
+                    for (int64_t s = 0; s < wb; ++s) o[(size_t)s] = blk * 32 + s < n ? (int32_t)(blk * 32 + s) : -1;
+                    auto kf = [&](int32_t v) {
+                        if (v < 0) return (int64_t)-1;
+                        return key == 0 ? cntA(v) + cntB(v) : key == 1 ? (cntA(v) << 24) + cntB(v) : (cntB(v) << 24) + cntA(v);
+                    };
+                    std::stable_sort(o.begin(), o.end(), [&](int32_t x, int32_t y) { return kf(x) > kf(y); });
+                    int64_t cost = 0;
+                    for (int64_t g = 0; g < wb / 4; ++g) {
+                        int64_t la = 0, lb = 0;
+                        for (int s = 0; s < 4; ++s) {
+                            la = std::max(la, cntA(o[(size_t)(4 * g + s)]));
+                            lb = std::max(lb, cntB(o[(size_t)(4 * g + s)]));
+                        }
+                        cost += la + lb;
+                    }
+                    if (best_cost < 0 || cost < best_cost) {
+                        best_cost = cost;
+                        win_order = o;
+                    }
+                }
+            }
+            std::array<int32_t, 32> best{};
+            for (int s = 0; s < 32; ++s) best[(size_t)s] = win_order[(size_t)((blk % 8) * 32 + s)];
+            for (int g = 0; g < 8; ++g) {
+                int64_t la = 0, lb = 0;
+                for (int s = 0; s < 4; ++s) {
+                    const int32_t v = best[(size_t)(4 * g + s)];
+                    Lo.grp_var[(size_t)(blk * 32 + 4 * g + s)] = v;
+                    la = std::max(la, cntA(v));
+                    lb = std::max(lb, cntB(v));
+                }
+                if (la + lb > INT32_MAX) throw Error(FFSAT_ERR_ARG, "variable occurs too often for owner records");
+                const uint64_t off = Lo.grp_rec.size() / 4;
+                uint32_t* d = &Lo.grp_desc[(size_t)((blk * 8 + g) * 4)];
+                d[0] = (uint32_t)off; d[1] = (uint32_t)(off >> 32); d[2] = (uint32_t)la; d[3] = (uint32_t)lb;
+                for (int sec = 0; sec < 2; ++sec) {
+                    const int64_t rows = sec == 0 ? la : lb;
+                    for (int64_t j = 0; j < rows; ++j)
+                        for (int s = 0; s < 4; ++s) {
+                            const int32_t v = best[(size_t)(4 * g + s)];
+                            std::array<uint32_t, 4> r{0u, 0u, 0u, 2u};   // pad
+                            if (sec == 0 && j < cntA(v)) r = recA[(size_t)(offA[(size_t)v] + j)];
+                            if (sec == 1 && j < cntB(v)) r = recB[(size_t)(offB[(size_t)v] + j)];
+                            Lo.grp_rec.insert(Lo.grp_rec.end(), r.begin(), r.end());
+                        }
+                }
+            }
+        }
+        // 8 pad rows past the last group: the kernel's batches of <= 4 rows, and the next batch it prefetches, read
+        // (and mask) past a section's end
+        for (int i = 0; i < 32; ++i) Lo.grp_rec.insert(Lo.grp_rec.end(), {0u, 0u, 0u, 2u});
+    } else if (Lo.own) {
         if (Lo.fbuckets.size() > 0xffffff) throw Error(FFSAT_ERR_ARG, "too many fast buckets");
         Lo.own_off.assign((size_t)F.n + 1, 0);
         for (const FastBucket& b : Lo.fbuckets)

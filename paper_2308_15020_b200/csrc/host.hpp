@@ -115,10 +115,20 @@ struct Layout {
     bool own_sliced = false;        // every fast constraint is owner-computed and nothing else reads x^T: x^T is laid out in
                                     // 16-point slices [B/16][n][16] so one slice (n x 64 B) stays L2-resident per pass
     bool own = false;
-    int32_t own_uni = -1;               // the single owner bucket when there is exactly one (owner_uni_kernel), else -1
+    int32_t own_uni = -1;               // the single owner bucket when there is exactly one (owner_grp_kernel), else -1
     int64_t n_own_lits = 0;
     std::vector<int64_t> own_off;       // [n + 1]
     std::vector<uint32_t> own_rec;      // 4 per occurrence
+    // the single-bucket case (owner_grp_kernel) instead: per block of 32 variable slots, 8 groups of 4 (the variables
+    // of each 256-variable window sorted by occurrence counts and dealt in that order to the window's 8 blocks;
+    // grp_var: slot -> variable, -1 past n); per group {record offset lo, hi,
+    // rows A, rows B}; its records interleaved [row][4 slots], rows A = the occurrences at literal index 0 (ascending
+    // position), rows B = the others (ascending position), each padded to the group's longest list with pad records
+    // {0, 0, 0, 2}.  Record {position, the other literals' words (literal order), bit 0 own negated | bit 1 pad}
+    int32_t own_ppt = 1;                // points per thread of owner_grp_kernel (x^T slices of 8 * own_ppt points)
+    std::vector<uint32_t> grp_desc;     // 4 per group
+    std::vector<int32_t> grp_var;       // [32 * ceil(n / 32)]
+    std::vector<uint32_t> grp_rec;      // 4 per record (incl. pads)
     std::vector<int64_t> occ_off;       // [n + 1]
     std::vector<int64_t> occ_slot;      // ascending slot ids per variable
     // work units of the fast kernels (tiled: var-disjoint classes; global: runs of <= 512 literals)
@@ -128,6 +138,7 @@ struct Layout {
 };
 
 constexpr int kOwnSlice = 8;       // points per x^T slice of the sliced owner-computes path (one slice's x^T stays in L2)
+constexpr int kOwnSliceMax = 32;   // the widest slice (owner_grp_kernel, 4 points per thread)
 constexpr int kOwnKMax = 3;         // global path, FFSAT_OWN=1: constraints this short take the owner-computes gradient
 constexpr int kTilePitch = 66;      // smem row pitch of the tiled kernel: x half-row (32 points + pad) | gradient half-row
 constexpr int kClassCap = 16;

@@ -1915,6 +1915,10 @@ struct OwnerArgs {
     double* fpart;               // rows [row0 + variable tile][B]
     int32_t* upart;              // same rows, or null
     int32_t row0;
+    const uint4* grp_desc;       // owner_grp_kernel: per group {record offset lo, hi, rows A, rows B}
+    const int32_t* grp_var;      // slot -> variable (-1: none)
+    const uint4* grp_rec;        // interleaved [row][4] records
+    uint32_t grp_pitch;          // bytes per variable row of an x^T slice (8 PPT sizeof(T))
 };
 
 // L2 cache policies (createpolicy): x^T rows are gathered many times (keep them: evict_last), the occurrence records
@@ -2053,87 +2057,160 @@ __global__ void __launch_bounds__(256) owner_grad_kernel(OwnerArgs<T> a) {
     }
 }
 
-// The same for the common case of ONE owner bucket (uniform short constraints, e.g. random 3-SAT): the bucket's
-// coefficients are loaded once and the per-record work is branch-free with the length K and the product channels
-// NCH fixed at compile time.  Same records, same summation orders (bit-identical to owner_grad_kernel).
-template <typename T, int SB, int K, int NCH>
-__global__ void __launch_bounds__(256) owner_uni_kernel(OwnerArgs<T> a, int32_t bucket) {
-    constexpr int NV = 256 / SB;
-    __shared__ T tile[NV][SB + 1];
-    __shared__ double sf[NV][SB];
-    __shared__ int su[NV][SB];
-    const int tx = threadIdx.x % SB, ty = threadIdx.x / SB;
-    const int64_t b0 = (int64_t)blockIdx.y * SB, v0 = (int64_t)blockIdx.x * NV;
-    const int64_t b = b0 + tx, v = v0 + ty;
-    const bool bv = b < a.B;
-    const int64_t bb = bv ? b : a.B - 1;
-    const bool want_term = a.grad != nullptr, want_unsat = a.upart != nullptr;
-    const BucketReg<T> bk = load_bucket<T>(a.buckets + bucket);
-    double acc = 0.0, facc = 0.0;
-    int uacc = 0;
-    if (v < a.n) {
-        const T* xTb = a.xT + (bb / SB) * a.slice_stride + bb % SB;
-        const T xv = __ldg(xTb + v * a.row_stride);
-        const int64_t o1 = a.own_off[v + 1];
-        for (int64_t o = a.own_off[v]; o < o1; o += 4) {
-            constexpr int NB = 4;
-            uint4 rc[NB];
+// PPT consecutive elements at byte offset off from base (one vector load of <= 16 bytes, read-only path).  The offset
+// is a runtime product (IMAD.WIDE of the index by the row pitch: no 64-bit shift sequence).
+template <typename T, int PPT>
+__device__ __forceinline__ void ld_vec(const T* base, uint64_t off, T (&v)[PPT]) {
+    static_assert(sizeof(T) * PPT <= 16, "vector load of at most 16 bytes");
+    const char* p = reinterpret_cast<const char*>(base) + off;
+    if constexpr (PPT == 1) v[0] = __ldg(reinterpret_cast<const T*>(p));
+    else if constexpr (sizeof(T) == 4 && PPT == 2) {
+        const float2 q = __ldg(reinterpret_cast<const float2*>(p));
+        v[0] = q.x; v[1] = q.y;
+    } else if constexpr (sizeof(T) == 4 && PPT == 4) {
+        const float4 q = __ldg(reinterpret_cast<const float4*>(p));
+        v[0] = q.x; v[1] = q.y; v[2] = q.z; v[3] = q.w;
+    } else {
+        const double2 q = __ldg(reinterpret_cast<const double2*>(p));
+        v[0] = q.x; v[1] = q.y;
+    }
+}
+
+// Rows [0, rows) of one owner group's section (records at rec[4 row]): the terms of this thread's variable at its PPT
+// points, added in row order; FCHK (rows A: the own literal is the constraint's literal 0) also the constraint's w FE
+// and its fused check.  Four rows per batch with every load in flight; the tail batch reads pad records past rows.
+template <typename T, int K, int NCH, int PPT, int NB, bool FCHK>
+__device__ __forceinline__ void owner_grp_rows(const uint4* __restrict__ rec, int rows, const T* __restrict__ xTs, uint32_t pitch,
+                                               const T* __restrict__ w_pos, const BucketReg<T>& bk, const T (&xv)[PPT],
+                                               const T (&aoP)[NCH][PPT], const T (&aoN)[NCH][PPT], const T (&gP)[NCH],
+                                               const T (&gN)[NCH], bool want_term, bool want_unsat, double (&acc)[PPT],
+                                               double (&facc)[PPT], int (&uacc)[PPT]) {
+        // software-pipelined: the next batch's records are in flight while this batch's gathers and products run (rows
+    // past the section are read and masked below; the host appends pad rows past the last group)
+    uint4 rc[NB];
 #pragma unroll
-            for (int q = 0; q < NB; ++q) rc[q] = o + q < o1 ? __ldcs(a.own_rec + o + q) : make_uint4(0, 0, 0, 0);
-            T xa[NB], xb[NB], wc[NB];
+    for (int q = 0; q < NB; ++q) rc[q] = __ldcs(rec + 4 * q);
+    for (int j = 0; j < rows; j += NB) {
+        T xa[NB][PPT], xb[NB][PPT], wc[NB];
 #pragma unroll
-            for (int q = 0; q < NB; ++q) {
-                xa[q] = K >= 2 ? __ldg(xTb + (int64_t)(rc[q].y & 0x7fffffffu) * a.row_stride) : (T)0;
-                xb[q] = K >= 3 ? __ldg(xTb + (int64_t)(rc[q].z & 0x7fffffffu) * a.row_stride) : (T)0;
-                wc[q] = __ldg(a.w_pos + rc[q].x);
-            }
+        for (int q = 0; q < NB; ++q) {
+            if (K >= 2) ld_vec<T, PPT>(xTs, (uint64_t)(rc[q].y & 0x7fffffffu) * pitch, xa[q]);
+            if (K >= 3) ld_vec<T, PPT>(xTs, (uint64_t)(rc[q].z & 0x7fffffffu) * pitch, xb[q]);
+            wc[q] = __ldg(w_pos + rc[q].x);
+        }
+        uint4 rn[NB];
 #pragma unroll
-            for (int q = 0; q < NB; ++q) {
-                if (o + q >= o1) break;
-                const uint32_t wown = rc[q].w << 31;
+        for (int q = 0; q < NB; ++q) rn[q] = __ldcs(rec + 4 * (j + NB + q));
+#pragma unroll
+        for (int q = 0; q < NB; ++q) {
+            const bool neg = rc[q].w & 1u, pad = (rc[q].w & 2u) || j + q >= rows;
+            const T w = pad ? (T)0 : wc[q];
+#pragma unroll
+            for (int p = 0; p < PPT; ++p) {
                 T term = (T)0, fe = bk.g0;
 #pragma unroll
                 for (int c = 0; c < NCH; ++c) {
-                    const T ao = fmaT(flip_sign(bk.c1[c], wown), xv, bk.c0[c]);
-                    const T aa = K >= 2 ? fmaT(flip_sign(bk.c1[c], rc[q].y), xa[q], bk.c0[c]) : (T)1;
-                    const T ab = K >= 3 ? fmaT(flip_sign(bk.c1[c], rc[q].z), xb[q], bk.c0[c]) : (T)1;
+                    const T aa = K >= 2 ? fmaT(flip_sign(bk.c1[c], rc[q].y), xa[q][p], bk.c0[c]) : (T)1;
+                    const T ab = K >= 3 ? fmaT(flip_sign(bk.c1[c], rc[q].z), xb[q][p], bk.c0[c]) : (T)1;
                     const T ex = aa * ab;
-                    fe = fmaT(bk.g[c], ao * ex, fe);
-                    term = fmaT(bk.g[c] * flip_sign(bk.c1[c], wown), ex, term);
+                    if (FCHK) fe = fmaT(bk.g[c], (neg ? aoN[c][p] : aoP[c][p]) * ex, fe);
+                    term = fmaT(neg ? gN[c] : gP[c], ex, term);
                 }
-                if (want_term) acc += (double)(wc[q] * term);
-                if (((rc[q].w >> 1) & 3) == 0) {   // the constraint's f and check, counted once (first literal's owner)
-                    facc += (double)(wc[q] * fe);
+                if (want_term) acc[p] += (double)(w * term);
+                if (FCHK) {
+                    facc[p] += (double)(w * fe);
                     if (want_unsat) {
-                        uint32_t t = lit_true(xv, wown);
-                        if (K >= 2) t += lit_true(xa[q], rc[q].y);
-                        if (K >= 3) t += lit_true(xb[q], rc[q].z);
-                        uacc += rule_sat((int)t, bk.tmin, bk.tmax, bk.parity) ? 0 : 1;
+                        uint32_t t = lit_true(xv[p], neg ? 0x80000000u : 0u);
+                        if (K >= 2) t += lit_true(xa[q][p], rc[q].y);
+                        if (K >= 3) t += lit_true(xb[q][p], rc[q].z);
+                        // the rule, branch-free: tmin <= t <= tmax and the parity (0 none, 1 odd, 2 even)
+                        const int ti = (int)t;
+                        const bool ok = ti >= bk.tmin && ti <= bk.tmax && (bk.parity == 0 || (ti & 1) == (bk.parity & 1));
+                        uacc[p] += (pad || ok) ? 0 : 1;
                     }
                 }
             }
         }
+#pragma unroll
+        for (int q = 0; q < NB; ++q) rc[q] = rn[q];
     }
-    sf[ty][tx] = facc;
-    su[ty][tx] = uacc;
-    tile[ty][tx] = (T)acc;
+}
+
+// Owner-computes for ONE owner bucket of short constraints (k <= 3), grouped records (host.hpp grp_*): block = 32
+// variable slots x one x^T slice of SB = 8 PPT points; warp w = group w of the block (4 variable slots x 8 lanes),
+// lane = PPT consecutive points (vector gathers).  The host sorts each 256-variable window by occurrence counts and
+// deals it to 8 blocks of 8 groups, padding a group's lists to its longest: trip counts are warp-uniform, a block's
+// warps finish together, a record row is two 32 B sectors.  The next batch of records is loaded while the current
+// one's gathers and products run (two dependent misses per batch -> one).  Gradient entries are stored straight
+// from registers (the window's blocks complete the rows' sectors in L2).  Per (variable, point) the order of the fp64 sum: rows A (the occurrences at literal index 0,
+// which also carry the constraint's f and fused check) ascending position, rows B ascending position, then the
+// variable's remaining T slots ascending -- fixed, and independent of the batch and of the point's slice position.
+template <typename T, int K, int NCH, int PPT, int NB>
+__global__ void __launch_bounds__(256, (PPT == 4 && NB == 4) || sizeof(T) == 8 ? 2 : PPT >= 2 ? 3 : 4) owner_grp_kernel(OwnerArgs<T> a, int32_t bucket) {
+    constexpr int SB = 8 * PPT;
+    __shared__ double sf[32][SB];
+    __shared__ int su[32][SB];
+    const int t = threadIdx.x, lane = t & 7, slot = t >> 3;
+    const int64_t v0 = (int64_t)blockIdx.x * 32, b0 = (int64_t)blockIdx.y * SB;
+    const bool want_term = a.grad != nullptr, want_unsat = a.upart != nullptr;
+    const BucketReg<T> bk = load_bucket<T>(a.buckets + bucket);
+    const int32_t v = a.grp_var[v0 + slot];
+    const T* xTs = a.xT + (int64_t)blockIdx.y * SB * a.n + lane * PPT;
+    double acc[PPT], facc[PPT];
+    int uacc[PPT];
+#pragma unroll
+    for (int p = 0; p < PPT; ++p) { acc[p] = 0.0; facc[p] = 0.0; uacc[p] = 0; }
+    T xv[PPT];
+    const uint32_t pitch = a.grp_pitch;   // = SB * sizeof(T), a runtime value
+    ld_vec<T, PPT>(xTs, (uint64_t)(v < 0 ? 0 : v) * pitch, xv);
+    T aoP[NCH][PPT], aoN[NCH][PPT], gP[NCH], gN[NCH];
+#pragma unroll
+    for (int c = 0; c < NCH; ++c) {
+        gP[c] = bk.g[c] * bk.c1[c];
+        gN[c] = bk.g[c] * -bk.c1[c];
+#pragma unroll
+        for (int p = 0; p < PPT; ++p) {
+            aoP[c][p] = fmaT(bk.c1[c], xv[p], bk.c0[c]);
+            aoN[c][p] = fmaT(-bk.c1[c], xv[p], bk.c0[c]);
+        }
+    }
+    const uint4 d = a.grp_desc[blockIdx.x * 8 + (slot >> 2)];
+    const uint4* rec = a.grp_rec + (((int64_t)d.y << 32) | d.x) + (slot & 3);   // record row 0 of the group, this slot
+    owner_grp_rows<T, K, NCH, PPT, NB, true>(rec, (int)d.z, xTs, pitch, a.w_pos, bk, xv, aoP, aoN, gP, gN, want_term, want_unsat,
+                                         acc, facc, uacc);
+    owner_grp_rows<T, K, NCH, PPT, NB, false>(rec + 4 * (int64_t)d.z, (int)d.w, xTs, pitch, a.w_pos, bk, xv, aoP, aoN, gP, gN,
+                                          want_term, want_unsat, acc, facc, uacc);
+    if (want_term && v >= 0) {   // the variable's remaining T slots (long fast / root-path constraints), ascending
+        const int64_t e = a.occ_off[v + 1];
+        for (int64_t q = a.occ_off[v]; q < e; ++q) {
+            const int64_t sl = a.occ_slot[q];
+#pragma unroll
+            for (int p = 0; p < PPT; ++p) {
+                const int64_t bb = min(b0 + lane * PPT + p, a.B - 1);
+                acc[p] += (double)a.Tb[sl * a.B + bb];
+            }
+        }
+    }
+#pragma unroll
+    for (int p = 0; p < PPT; ++p) {
+        sf[slot][lane * PPT + p] = facc[p];
+        su[slot][lane * PPT + p] = uacc[p];
+        // the gradient entry straight from the register (the block's variables are scattered over a 256-variable
+        // window: the window's 8 blocks, launched together, complete its rows' sectors in L2)
+        const int64_t pb = b0 + lane * PPT + p;
+        if (want_term && v >= 0 && pb < a.B) __stcs(a.grad + pb * a.n + v, (T)acc[p]);
+    }
     __syncthreads();
-    if (ty == 0 && bv) {
+    if (t < SB && b0 + t < a.B) {   // partial f / unsat of this variable block, slot order
         double f = 0.0;
         int u = 0;
-#pragma unroll
-        for (int j = 0; j < NV; ++j) {
-            f += sf[j][tx];
-            u += su[j][tx];
+#pragma unroll 8
+        for (int j = 0; j < 32; ++j) {
+            f += sf[j][t];
+            u += su[j][t];
         }
-        a.fpart[((int64_t)a.row0 + blockIdx.x) * a.B + b] = f;
-        if (want_unsat) a.upart[((int64_t)a.row0 + blockIdx.x) * a.B + b] = u;
-    }
-    if (want_term) {
-        const int t = threadIdx.x;
-        const int pl = t / NV, vl = t % NV;
-        const int64_t pb = b0 + pl, vv = v0 + vl;
-        if (pb < a.B && vv < a.n) __stcs(a.grad + pb * a.n + vv, tile[vl][pl]);
+        a.fpart[((int64_t)a.row0 + blockIdx.x) * a.B + b0 + t] = f;
+        if (want_unsat) a.upart[((int64_t)a.row0 + blockIdx.x) * a.B + b0 + t] = u;
     }
 }
 

@@ -34,6 +34,10 @@ if len(sys.argv) > 2:
     cfg = sys.argv[2]
     p = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "profiles", "ncu_summary.json")
     d = json.load(open(p)) if os.path.exists(p) else {}
+    # kernels of this config that the new launch list no longer shows (a changed plan) are dropped
+    bases = {name.split("<")[0] for name in agg}
+    for key in [k for k in d if k.startswith(f"{cfg}:") and k.split(":", 1)[1] not in bases]:
+        del d[key]
     for name, (n, us, by) in agg.items():
         base = name.split("<")[0]
         if base.startswith("at::") or "Functor" in name:

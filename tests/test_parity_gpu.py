@@ -221,13 +221,16 @@ def test_owner_computes_option(precision, monkeypatch):
     assert torch.equal(f2, f[33:50]) and torch.equal(g2, g[33:50]) and torch.equal(u2, u[33:50])
 
 
-@pytest.mark.parametrize("precision", [32, 64])
-def test_owner_computes_sliced_uniform(precision, monkeypatch):
-    """FFSAT_OWN=1 on a formula whose fast constraints are ALL short (uniform random 3-SAT on the global path): x^T in
-    8-point slices and the single-bucket owner kernel (owner_uni_kernel); f, grad, unsat against the oracle on a ragged
-    batch (a partial last slice), and bit-identical when a point is evaluated in another batch / slice position."""
+@pytest.mark.parametrize("precision,ppt,k", [(32, 1, 3), (32, 2, 3), (32, 4, 3), (64, 1, 3), (64, 2, 3), (32, 4, 2),
+                                             (64, 2, 2)])
+def test_owner_computes_sliced_uniform(precision, ppt, k, monkeypatch):
+    """FFSAT_OWN=1 on a formula whose fast constraints are ALL short (uniform random k-SAT on the global path, n not a
+    multiple of 32): x^T in 8 ppt-point slices and the single-bucket grouped owner kernel (owner_grp_kernel, ppt points
+    per thread); f, grad, unsat against the oracle on a ragged batch (a partial last slice), and bit-identical when a
+    point is evaluated in another batch / slice position."""
     monkeypatch.setenv("FFSAT_OWN", "1")
-    inst = synth.random_ksat(3000, 12600, 3, 5)
+    monkeypatch.setenv("FFSAT_OWN_PPT", str(ppt))
+    inst = synth.random_ksat(3001, 12600, k, 5)
     ctx = P.Context.from_instance(inst, precision=precision, path=2, device=0)
     assert ctx.info["n_own_lits"] == ctx.info["n_lits"]
     compare(inst, synth.points("U", 21, inst.n, 6), precision=precision, ctx=ctx)
@@ -236,6 +239,36 @@ def test_owner_computes_sliced_uniform(precision, monkeypatch):
     f, g, u = ctx.eval(X, grad=True, unsat=True)
     f2, g2, u2 = ctx.eval(X[5:30].contiguous(), grad=True, unsat=True)
     assert torch.equal(f2, f[5:30]) and torch.equal(g2, g[5:30]) and torch.equal(u2, u[5:30])
+
+
+@pytest.mark.parametrize("precision", [32, 64])
+def test_owner_grouped_default_on_single_short_bucket(precision, monkeypatch):
+    """Default plan (no FFSAT_OWN): a global-path formula whose fast constraints are ONE bucket of 3-literal clauses
+    takes the grouped owner kernel (owner_grp_kernel, 32-point slices in fp32, 16 in fp64); f, grad, unsat against
+    the oracle over several slices with a ragged tail, and the same bits for a point in another batch position."""
+    monkeypatch.delenv("FFSAT_OWN", raising=False)
+    monkeypatch.delenv("FFSAT_OWN_PPT", raising=False)
+    inst = synth.random_ksat(5003, 21000, 3, 9)
+    ctx = P.Context.from_instance(inst, precision=precision, path=2, device=0)
+    assert ctx.info["n_own_lits"] == ctx.info["n_lits"]
+    compare(inst, synth.points("U", 70, inst.n, 10), precision=precision, ctx=ctx)
+    compare(inst, synth.points("N", 33, inst.n, 11), precision=precision, ctx=ctx)
+    compare(inst, synth.points("Z", 5, inst.n, 12), precision=precision, ctx=ctx)
+    X = torch.from_numpy(synth.points("U", 70, inst.n, 13, ctx.dtype)).cuda()
+    f, g, u = ctx.eval(X, grad=True, unsat=True)
+    f2, g2, u2 = ctx.eval(X[31:69].contiguous(), grad=True, unsat=True)
+    assert torch.equal(f2, f[31:69]) and torch.equal(g2, g[31:69]) and torch.equal(u2, u[31:69])
+
+
+def test_owner_grouped_with_root_path_slots(monkeypatch):
+    """The grouped owner kernel also adds a variable's T slots (here the root-path terms of long at-most-b
+    constraints sharing the variables with the 3-literal clauses), fp64, against the oracle."""
+    monkeypatch.delenv("FFSAT_OWN", raising=False)
+    inst = synth.config3(0, n=1500, m3=3000, n_card=3, kmin=100, kmax=300)
+    ctx = P.Context.from_instance(inst, precision=64, path=2, device=0)
+    assert 0 < ctx.info["n_own_lits"] < ctx.info["n_lits"]
+    compare(inst, synth.points("U", 40, inst.n, 14), precision=64, ctx=ctx)
+    compare(inst, synth.points("N", 9, inst.n, 15), precision=64, ctx=ctx)
 
 
 def test_c4_hybrid_global_full_batch():
