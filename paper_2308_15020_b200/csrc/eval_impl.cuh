@@ -86,25 +86,30 @@ dev::PmReduce<T> pm_reduce_args(const ffsat_ctx* c, const Scratch& S, int64_t B,
     return r;
 }
 
-// owner_grp_kernel for the bucket's (k, product channels) and the points per thread (float: 1, 2, 4; double: 1, 2)
+// owner_grp_kernel for the bucket's (k, product channels), threads per variable and points per thread (fp32: 4 or 2,
+// fp64: 2; 16- or 8-byte gathers)
 template <typename T, int K, int NCH>
-void launch_owner_grp_k(int ppt, dim3 grid, cudaStream_t st, const dev::OwnerArgs<T>& o, int32_t bucket) {
-    // rows per batch at 4 points per thread: 2 (80 registers, 3 CTAs per SM; 4 rows: 128 registers, 2 CTAs, slower)
-    static const int nb = [] { const char* e = std::getenv("FFSAT_OWN_NB"); return e && std::atoi(e) == 4 ? 4 : 2; }();
-    if (ppt == 1) dev::owner_grp_kernel<T, K, NCH, 1, 4><<<grid, 256, 0, st>>>(o, bucket);
-    else if (ppt == 2 || sizeof(T) == 8) dev::owner_grp_kernel<T, K, NCH, 2, 4><<<grid, 256, 0, st>>>(o, bucket);
-    else if (nb == 2) dev::owner_grp_kernel<T, K, NCH, (sizeof(T) == 4 ? 4 : 2), 2><<<grid, 256, 0, st>>>(o, bucket);
-    else dev::owner_grp_kernel<T, K, NCH, (sizeof(T) == 4 ? 4 : 2), 4><<<grid, 256, 0, st>>>(o, bucket);
+void launch_owner_grp_k(int lanes, int ppt, dim3 grid, cudaStream_t st, const dev::OwnerArgs<T>& o, int32_t bucket) {
+    constexpr int P4 = sizeof(T) == 4 ? 4 : 2;
+    if (ppt == 2 || sizeof(T) == 8) {
+        if (lanes == 2) dev::owner_grp_kernel<T, K, NCH, 2, 2><<<grid, 256, 0, st>>>(o, bucket);
+        else if (lanes == 4) dev::owner_grp_kernel<T, K, NCH, 4, 2><<<grid, 256, 0, st>>>(o, bucket);
+        else dev::owner_grp_kernel<T, K, NCH, 8, 2><<<grid, 256, 0, st>>>(o, bucket);
+    } else {
+        if (lanes == 2) dev::owner_grp_kernel<T, K, NCH, 2, P4><<<grid, 256, 0, st>>>(o, bucket);
+        else if (lanes == 4) dev::owner_grp_kernel<T, K, NCH, 4, P4><<<grid, 256, 0, st>>>(o, bucket);
+        else dev::owner_grp_kernel<T, K, NCH, 8, P4><<<grid, 256, 0, st>>>(o, bucket);
+    }
 }
 template <typename T>
-void launch_owner_grp(int key, int ppt, dim3 grid, cudaStream_t st, const dev::OwnerArgs<T>& o, int32_t bucket) {
+void launch_owner_grp(int key, int lanes, int ppt, dim3 grid, cudaStream_t st, const dev::OwnerArgs<T>& o, int32_t bucket) {
     switch (key) {
-    case 11: launch_owner_grp_k<T, 1, 1>(ppt, grid, st, o, bucket); break;
-    case 12: launch_owner_grp_k<T, 1, 2>(ppt, grid, st, o, bucket); break;
-    case 21: launch_owner_grp_k<T, 2, 1>(ppt, grid, st, o, bucket); break;
-    case 22: launch_owner_grp_k<T, 2, 2>(ppt, grid, st, o, bucket); break;
-    case 31: launch_owner_grp_k<T, 3, 1>(ppt, grid, st, o, bucket); break;
-    default: launch_owner_grp_k<T, 3, 2>(ppt, grid, st, o, bucket); break;
+    case 11: launch_owner_grp_k<T, 1, 1>(lanes, ppt, grid, st, o, bucket); break;
+    case 12: launch_owner_grp_k<T, 1, 2>(lanes, ppt, grid, st, o, bucket); break;
+    case 21: launch_owner_grp_k<T, 2, 1>(lanes, ppt, grid, st, o, bucket); break;
+    case 22: launch_owner_grp_k<T, 2, 2>(lanes, ppt, grid, st, o, bucket); break;
+    case 31: launch_owner_grp_k<T, 3, 1>(lanes, ppt, grid, st, o, bucket); break;
+    default: launch_owner_grp_k<T, 3, 2>(lanes, ppt, grid, st, o, bucket); break;
     }
 }
 
@@ -123,9 +128,10 @@ void eval_device_t(ffsat_ctx* c, Scratch& S, const T* x, int64_t B, double* f, T
     const bool need_xT = L.path == 2 || L.sym_lane;
     if (need_xT && L.n > 0) {
         dim3 tg(blocks_for(L.n, 32), blocks_for(B, 32)), tb(32, 8);
-        const int sw = L.own_uni >= 0 ? 8 * L.own_ppt : kOwnSlice;   // slice width of the owner kernel
+        const int sw = L.own_uni >= 0 ? L.own_lanes * L.own_ppt : kOwnSlice;   // slice width of the owner kernel
         if (L.own_sliced && sw == 32) dev::transpose_kernel<T, 32><<<tg, tb, 0, st>>>(x, S.xT.as<T>(), B, L.n);
         else if (L.own_sliced && sw == 16) dev::transpose_kernel<T, 16><<<tg, tb, 0, st>>>(x, S.xT.as<T>(), B, L.n);
+        else if (L.own_sliced && sw == 4) dev::transpose_kernel<T, 4><<<tg, tb, 0, st>>>(x, S.xT.as<T>(), B, L.n);
         else if (L.own_sliced) dev::transpose_kernel<T, kOwnSlice><<<tg, tb, 0, st>>>(x, S.xT.as<T>(), B, L.n);
         else dev::transpose_kernel<T, 0><<<tg, tb, 0, st>>>(x, S.xT.as<T>(), B, L.n);
         c->launches += 1;
@@ -299,11 +305,11 @@ void eval_device_t(ffsat_ctx* c, Scratch& S, const T* x, int64_t B, double* f, T
         o.row0 = c->n_chunks + c->n_fold;
         if (L.own_sliced && L.own_uni >= 0) {   // one owner bucket: grouped records, coefficients once
             o.grp_desc = c->grp_desc.as<uint4>(); o.grp_var = c->grp_var.as<int32_t>(); o.grp_rec = c->grp_rec.as<uint4>();
-            const int sw = 8 * L.own_ppt;
+            const int sw = L.own_lanes * L.own_ppt;
             o.grp_pitch = (uint32_t)(sw * sizeof(T));
-            dim3 grid(blocks_for(L.n, 32), blocks_for(B, sw));
+            dim3 grid(blocks_for(L.n, 256 / L.own_lanes), blocks_for(B, sw));
             const int key = L.fbuckets[(size_t)L.own_uni].k * 10 + fast_nch(L.fbuckets[(size_t)L.own_uni]);
-            launch_owner_grp<T>(key, L.own_ppt, grid, st, o, L.own_uni);
+            launch_owner_grp<T>(key, L.own_lanes, L.own_ppt, grid, st, o, L.own_uni);
         } else if (L.own_sliced) {   // kOwnSlice points x 256 / kOwnSlice variables per block
             dim3 grid(blocks_for(L.n, 256 / kOwnSlice), blocks_for(B, kOwnSlice));
             dev::owner_grad_kernel<T, kOwnSlice><<<grid, 256, 0, st>>>(o);

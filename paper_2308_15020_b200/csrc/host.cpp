@@ -524,14 +524,17 @@ Layout build_layout(const Formula& F, int path, int precision) {
     }
     if (Lo.own && Lo.own_uni >= 0) {
         // one owner bucket: grouped, padded, interleaved records (owner_grp_kernel)
-        Lo.own_ppt = precision == 64 ? 2 : 4;   // one 32-point slice (fp64: 16-point slices, 16-byte gathers)
-        if (const char* e = std::getenv("FFSAT_OWN_PPT")) {
+        // 16-byte gathers: 4 fp32 / 2 fp64 points per thread; threads per variable (FFSAT_OWN_LANES 2, 4 or 8)
+        Lo.own_ppt = precision == 64 ? 2 : 4;
+        Lo.own_lanes = kOwnLanes;
+        if (const char* e = std::getenv("FFSAT_OWN_PPT")) Lo.own_ppt = std::atoi(e) == 2 ? 2 : Lo.own_ppt;
+        if (const char* e = std::getenv("FFSAT_OWN_LANES")) {
             const int v = std::atoi(e);
-            Lo.own_ppt = v == 2 || v == 4 ? v : 1;
+            Lo.own_lanes = v == 2 || v == 4 ? v : 8;
         }
-        if (precision == 64 && Lo.own_ppt > 2) Lo.own_ppt = 2;
+        const int G = 32 / Lo.own_lanes, NS = 8 * G;   // variable slots per group (warp) and per block
         const FastBucket& b = Lo.fbuckets[(size_t)Lo.own_uni];
-        const int64_t n = F.n, nblk = (n + 31) / 32;
+        const int64_t n = F.n, nblk = (n + NS - 1) / NS;
         std::vector<int64_t> offA((size_t)n + 1, 0), offB((size_t)n + 1, 0);
         for (int64_t p = b.pos_begin; p < b.pos_end; ++p) {
             const uint32_t* wr = &Lo.fast_words[(size_t)(b.word_off + (p - b.pos_begin) * b.kp)];
@@ -557,35 +560,35 @@ Layout build_layout(const Formula& F, int path, int precision) {
                 }
             }
         }
-        Lo.grp_var.assign((size_t)(nblk * 32), -1);
+        Lo.grp_var.assign((size_t)(nblk * NS), -1);
         Lo.grp_desc.assign((size_t)(nblk * 8 * 4), 0);
         Lo.grp_rec.clear();
         Lo.grp_rec.reserve((size_t)(Lo.n_own_lits * 4 * 5 / 4));
         auto cntA = [&](int32_t v) { return v < 0 ? 0 : offA[(size_t)v + 1] - offA[(size_t)v]; };
         auto cntB = [&](int32_t v) { return v < 0 ? 0 : offB[(size_t)v + 1] - offB[(size_t)v]; };
-        // windows of 8 blocks (256 variables): the window's variables sorted by occurrence counts and dealt in that
-        // order to its blocks and groups, so a group's lists, and a block's groups, have about equal lengths (little
-        // padding; no warp of a block idles at its barrier) -- the cheapest (padded rows) of three orders: by total
-        // count, by literal-0 count, by the other count.  (Variables past n: -1, sorted last.)
-        std::vector<int32_t> win_order;
+        // windows of 8 blocks: the window's variables sorted by occurrence counts and dealt in that order to its
+        // blocks and groups, so a group's lists, and a block's groups, have about equal lengths (little padding; no
+        // warp of a block idles at its barrier) -- the cheapest (padded rows) of three orders: by total count, by
+        // literal-0 count, by the other count.  (Slots past n: -1, sorted last.)
+        std::vector<int32_t> win_order, o;
         for (int64_t blk = 0; blk < nblk; ++blk) {
             if (blk % 8 == 0) {
-                const int64_t wb = std::min<int64_t>(8, nblk - blk) * 32;
+                const int64_t wb = std::min<int64_t>(8, nblk - blk) * NS;
                 int64_t best_cost = -1;
-                std::vector<int32_t> o((size_t)wb);
+                o.assign((size_t)wb, -1);
                 for (int key = 0; key < 3; ++key) {
-                    for (int64_t s = 0; s < wb; ++s) o[(size_t)s] = blk * 32 + s < n ? (int32_t)(blk * 32 + s) : -1;
+                    for (int64_t s = 0; s < wb; ++s) o[(size_t)s] = blk * NS + s < n ? (int32_t)(blk * NS + s) : -1;
                     auto kf = [&](int32_t v) {
                         if (v < 0) return (int64_t)-1;
                         return key == 0 ? cntA(v) + cntB(v) : key == 1 ? (cntA(v) << 24) + cntB(v) : (cntB(v) << 24) + cntA(v);
                     };
                     std::stable_sort(o.begin(), o.end(), [&](int32_t x, int32_t y) { return kf(x) > kf(y); });
                     int64_t cost = 0;
-                    for (int64_t g = 0; g < wb / 4; ++g) {
+                    for (int64_t g = 0; g < wb / G; ++g) {
                         int64_t la = 0, lb = 0;
-                        for (int s = 0; s < 4; ++s) {
-                            la = std::max(la, cntA(o[(size_t)(4 * g + s)]));
-                            lb = std::max(lb, cntB(o[(size_t)(4 * g + s)]));
+                        for (int s = 0; s < G; ++s) {
+                            la = std::max(la, cntA(o[(size_t)(G * g + s)]));
+                            lb = std::max(lb, cntB(o[(size_t)(G * g + s)]));
                         }
                         cost += la + lb;
                     }
@@ -595,15 +598,13 @@ Layout build_layout(const Formula& F, int path, int precision) {
                     }
                 }
             }
-            std::array<int32_t, 32> best{};
-            for (int s = 0; s < 32; ++s) best[(size_t)s] = win_order[(size_t)((blk % 8) * 32 + s)];
             for (int g = 0; g < 8; ++g) {
+                const int32_t* grp = &win_order[(size_t)((blk % 8) * NS + g * G)];
                 int64_t la = 0, lb = 0;
-                for (int s = 0; s < 4; ++s) {
-                    const int32_t v = best[(size_t)(4 * g + s)];
-                    Lo.grp_var[(size_t)(blk * 32 + 4 * g + s)] = v;
-                    la = std::max(la, cntA(v));
-                    lb = std::max(lb, cntB(v));
+                for (int s = 0; s < G; ++s) {
+                    Lo.grp_var[(size_t)(blk * NS + g * G + s)] = grp[s];
+                    la = std::max(la, cntA(grp[s]));
+                    lb = std::max(lb, cntB(grp[s]));
                 }
                 if (la + lb > INT32_MAX) throw Error(FFSAT_ERR_ARG, "variable occurs too often for owner records");
                 const uint64_t off = Lo.grp_rec.size() / 4;
@@ -612,8 +613,8 @@ Layout build_layout(const Formula& F, int path, int precision) {
                 for (int sec = 0; sec < 2; ++sec) {
                     const int64_t rows = sec == 0 ? la : lb;
                     for (int64_t j = 0; j < rows; ++j)
-                        for (int s = 0; s < 4; ++s) {
-                            const int32_t v = best[(size_t)(4 * g + s)];
+                        for (int s = 0; s < G; ++s) {
+                            const int32_t v = grp[s];
                             std::array<uint32_t, 4> r{0u, 0u, 0u, 2u};   // pad
                             if (sec == 0 && j < cntA(v)) r = recA[(size_t)(offA[(size_t)v] + j)];
                             if (sec == 1 && j < cntB(v)) r = recB[(size_t)(offB[(size_t)v] + j)];
@@ -624,7 +625,7 @@ Layout build_layout(const Formula& F, int path, int precision) {
         }
         // 8 pad rows past the last group: the kernel's batches of <= 4 rows, and the next batch it prefetches, read
         // (and mask) past a section's end
-        for (int i = 0; i < 32; ++i) Lo.grp_rec.insert(Lo.grp_rec.end(), {0u, 0u, 0u, 2u});
+        for (int i = 0; i < 8 * G; ++i) Lo.grp_rec.insert(Lo.grp_rec.end(), {0u, 0u, 0u, 2u});
     } else if (Lo.own) {
         if (Lo.fbuckets.size() > 0xffffff) throw Error(FFSAT_ERR_ARG, "too many fast buckets");
         Lo.own_off.assign((size_t)F.n + 1, 0);

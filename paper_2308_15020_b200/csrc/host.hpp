@@ -119,13 +119,15 @@ struct Layout {
     int64_t n_own_lits = 0;
     std::vector<int64_t> own_off;       // [n + 1]
     std::vector<uint32_t> own_rec;      // 4 per occurrence
-    // the single-bucket case (owner_grp_kernel) instead: per block of 32 variable slots, 8 groups of 4 (the variables
-    // of each 256-variable window sorted by occurrence counts and dealt in that order to the window's 8 blocks;
-    // grp_var: slot -> variable, -1 past n); per group {record offset lo, hi,
-    // rows A, rows B}; its records interleaved [row][4 slots], rows A = the occurrences at literal index 0 (ascending
+    // the single-bucket case (owner_grp_kernel) instead: per block of 8 G variable slots (G = 32 / own_lanes), 8 groups
+    // of G (the variables of each 8-block window sorted by occurrence counts and dealt in that order to the window's
+    // blocks; grp_var: slot -> variable, -1 past n); per group {record offset lo, hi,
+    // rows A, rows B}; its records interleaved [row][G slots], rows A = the occurrences at literal index 0 (ascending
     // position), rows B = the others (ascending position), each padded to the group's longest list with pad records
     // {0, 0, 0, 2}.  Record {position, the other literals' words (literal order), bit 0 own negated | bit 1 pad}
-    int32_t own_ppt = 1;                // points per thread of owner_grp_kernel (x^T slices of 8 * own_ppt points)
+    int32_t own_ppt = 4;                // owner_grp_kernel: points per thread,
+    int32_t own_lanes = 8;              // ... threads per variable (x^T slices of own_lanes * own_ppt points; groups of
+                                        // 32 / own_lanes variables, blocks of 8 groups, windows of 8 blocks)
     std::vector<uint32_t> grp_desc;     // 4 per group
     std::vector<int32_t> grp_var;       // [32 * ceil(n / 32)]
     std::vector<uint32_t> grp_rec;      // 4 per record (incl. pads)
@@ -138,7 +140,8 @@ struct Layout {
 };
 
 constexpr int kOwnSlice = 8;       // points per x^T slice of the sliced owner-computes path (one slice's x^T stays in L2)
-constexpr int kOwnSliceMax = 32;   // the widest slice (owner_grp_kernel, 4 points per thread)
+constexpr int kOwnSliceMax = 32;   // the widest slice (owner_grp_kernel, 8 lanes x 4 points per thread)
+constexpr int kOwnLanes = 8;       // owner_grp_kernel: threads per variable (default; FFSAT_OWN_LANES)
 constexpr int kOwnKMax = 3;         // global path, FFSAT_OWN=1: constraints this short take the owner-computes gradient
 constexpr int kTilePitch = 66;      // smem row pitch of the tiled kernel: x half-row (32 points + pad) | gradient half-row
 constexpr int kClassCap = 16;

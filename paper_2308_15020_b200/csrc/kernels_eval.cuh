@@ -2079,7 +2079,7 @@ __device__ __forceinline__ void ld_vec(const T* base, uint64_t off, T (&v)[PPT])
 // Rows [0, rows) of one owner group's section (records at rec[4 row]): the terms of this thread's variable at its PPT
 // points, added in row order; FCHK (rows A: the own literal is the constraint's literal 0) also the constraint's w FE
 // and its fused check.  Four rows per batch with every load in flight; the tail batch reads pad records past rows.
-template <typename T, int K, int NCH, int PPT, int NB, bool FCHK>
+template <typename T, int K, int NCH, int PPT, int NB, int G, bool FCHK>
 __device__ __forceinline__ void owner_grp_rows(const uint4* __restrict__ rec, int rows, const T* __restrict__ xTs, uint32_t pitch,
                                                const T* __restrict__ w_pos, const BucketReg<T>& bk, const T (&xv)[PPT],
                                                const T (&aoP)[NCH][PPT], const T (&aoN)[NCH][PPT], const T (&gP)[NCH],
@@ -2089,7 +2089,7 @@ __device__ __forceinline__ void owner_grp_rows(const uint4* __restrict__ rec, in
     // past the section are read and masked below; the host appends pad rows past the last group)
     uint4 rc[NB];
 #pragma unroll
-    for (int q = 0; q < NB; ++q) rc[q] = __ldcs(rec + 4 * q);
+    for (int q = 0; q < NB; ++q) rc[q] = __ldcs(rec + G * q);
     for (int j = 0; j < rows; j += NB) {
         T xa[NB][PPT], xb[NB][PPT], wc[NB];
 #pragma unroll
@@ -2100,7 +2100,7 @@ __device__ __forceinline__ void owner_grp_rows(const uint4* __restrict__ rec, in
         }
         uint4 rn[NB];
 #pragma unroll
-        for (int q = 0; q < NB; ++q) rn[q] = __ldcs(rec + 4 * (j + NB + q));
+        for (int q = 0; q < NB; ++q) rn[q] = __ldcs(rec + G * (j + NB + q));
 #pragma unroll
         for (int q = 0; q < NB; ++q) {
             const bool neg = rc[q].w & 1u, pad = (rc[q].w & 2u) || j + q >= rows;
@@ -2136,22 +2136,27 @@ __device__ __forceinline__ void owner_grp_rows(const uint4* __restrict__ rec, in
     }
 }
 
-// Owner-computes for ONE owner bucket of short constraints (k <= 3), grouped records (host.hpp grp_*): block = 32
-// variable slots x one x^T slice of SB = 8 PPT points; warp w = group w of the block (4 variable slots x 8 lanes),
-// lane = PPT consecutive points (vector gathers).  The host sorts each 256-variable window by occurrence counts and
-// deals it to 8 blocks of 8 groups, padding a group's lists to its longest: trip counts are warp-uniform, a block's
-// warps finish together, a record row is two 32 B sectors.  The next batch of records is loaded while the current
-// one's gathers and products run (two dependent misses per batch -> one).  Gradient entries are stored straight
-// from registers (the window's blocks complete the rows' sectors in L2).  Per (variable, point) the order of the fp64 sum: rows A (the occurrences at literal index 0,
-// which also carry the constraint's f and fused check) ascending position, rows B ascending position, then the
-// variable's remaining T slots ascending -- fixed, and independent of the batch and of the point's slice position.
-template <typename T, int K, int NCH, int PPT, int NB>
-__global__ void __launch_bounds__(256, (PPT == 4 && NB == 4) || sizeof(T) == 8 ? 2 : PPT >= 2 ? 3 : 4) owner_grp_kernel(OwnerArgs<T> a, int32_t bucket) {
-    constexpr int SB = 8 * PPT;
-    __shared__ double sf[32][SB];
-    __shared__ int su[32][SB];
-    const int t = threadIdx.x, lane = t & 7, slot = t >> 3;
-    const int64_t v0 = (int64_t)blockIdx.x * 32, b0 = (int64_t)blockIdx.y * SB;
+// Owner-computes for ONE owner bucket of short constraints (k <= 3), grouped records (host.hpp grp_*): block =
+// 256 / LANES variable slots x one x^T slice of SB = LANES PPT points; warp w = group w of the block (32 / LANES
+// variable slots x LANES lanes), lane = PPT consecutive points (vector gathers).  The host sorts each window of 8
+// blocks' variables by occurrence counts and deals it to the 8 blocks of 8 groups, padding a group's lists to its
+// longest: trip counts are warp-uniform, a block's warps finish together, a record row is G = 32 / LANES records
+// side by side.  The next batch of records is loaded while the current one's gathers and products run (two
+// dependent misses per batch -> one).  Gradient entries are stored straight from registers (the window's blocks
+// complete the rows' sectors in L2).  Per (variable, point) the order of the fp64 sum: rows A (the occurrences at
+// literal index 0, which also carry the constraint's f and fused check) ascending position, rows B ascending
+// position, then the variable's remaining T slots ascending -- fixed, and independent of the batch, of the slice
+// width and of the point's slice position.
+template <typename T, int K, int NCH, int LANES, int PPT>
+__global__ void __launch_bounds__(256, sizeof(T) == 8 ? 2 : 3) owner_grp_kernel(OwnerArgs<T> a, int32_t bucket) {
+    constexpr int SB = LANES * PPT;          // points per x^T slice
+    constexpr int G = 32 / LANES;            // variable slots per warp (= group)
+    constexpr int NS = 8 * G;                // variable slots per block
+    constexpr int NB = PPT == 4 ? 2 : 4;     // record rows per batch (registers: 80 at 4 points per thread)
+    __shared__ double sf[NS][SB];
+    __shared__ int su[NS][SB];
+    const int t = threadIdx.x, lane = t % LANES, slot = t / LANES;
+    const int64_t v0 = (int64_t)blockIdx.x * NS, b0 = (int64_t)blockIdx.y * SB;
     const bool want_term = a.grad != nullptr, want_unsat = a.upart != nullptr;
     const BucketReg<T> bk = load_bucket<T>(a.buckets + bucket);
     const int32_t v = a.grp_var[v0 + slot];
@@ -2174,12 +2179,12 @@ __global__ void __launch_bounds__(256, (PPT == 4 && NB == 4) || sizeof(T) == 8 ?
             aoN[c][p] = fmaT(-bk.c1[c], xv[p], bk.c0[c]);
         }
     }
-    const uint4 d = a.grp_desc[blockIdx.x * 8 + (slot >> 2)];
-    const uint4* rec = a.grp_rec + (((int64_t)d.y << 32) | d.x) + (slot & 3);   // record row 0 of the group, this slot
-    owner_grp_rows<T, K, NCH, PPT, NB, true>(rec, (int)d.z, xTs, pitch, a.w_pos, bk, xv, aoP, aoN, gP, gN, want_term, want_unsat,
-                                         acc, facc, uacc);
-    owner_grp_rows<T, K, NCH, PPT, NB, false>(rec + 4 * (int64_t)d.z, (int)d.w, xTs, pitch, a.w_pos, bk, xv, aoP, aoN, gP, gN,
-                                          want_term, want_unsat, acc, facc, uacc);
+    const uint4 d = a.grp_desc[blockIdx.x * 8 + t / 32];
+    const uint4* rec = a.grp_rec + (((int64_t)d.y << 32) | d.x) + slot % G;   // record row 0 of the group, this slot
+    owner_grp_rows<T, K, NCH, PPT, NB, G, true>(rec, (int)d.z, xTs, pitch, a.w_pos, bk, xv, aoP, aoN, gP, gN, want_term,
+                                                want_unsat, acc, facc, uacc);
+    owner_grp_rows<T, K, NCH, PPT, NB, G, false>(rec + G * (int64_t)d.z, (int)d.w, xTs, pitch, a.w_pos, bk, xv, aoP, aoN,
+                                                 gP, gN, want_term, want_unsat, acc, facc, uacc);
     if (want_term && v >= 0) {   // the variable's remaining T slots (long fast / root-path constraints), ascending
         const int64_t e = a.occ_off[v + 1];
         for (int64_t q = a.occ_off[v]; q < e; ++q) {
@@ -2195,17 +2200,17 @@ __global__ void __launch_bounds__(256, (PPT == 4 && NB == 4) || sizeof(T) == 8 ?
     for (int p = 0; p < PPT; ++p) {
         sf[slot][lane * PPT + p] = facc[p];
         su[slot][lane * PPT + p] = uacc[p];
-        // the gradient entry straight from the register (the block's variables are scattered over a 256-variable
-        // window: the window's 8 blocks, launched together, complete its rows' sectors in L2)
+        // the gradient entry straight from the register (the block's variables are scattered over its window: the
+        // window's 8 blocks, launched together, complete the rows' sectors in L2)
         const int64_t pb = b0 + lane * PPT + p;
         if (want_term && v >= 0 && pb < a.B) __stcs(a.grad + pb * a.n + v, (T)acc[p]);
     }
     __syncthreads();
-    if (t < SB && b0 + t < a.B) {   // partial f / unsat of this variable block, slot order
+    if (t < SB && b0 + t < a.B) {   // partial f / unsat of this block, slot order
         double f = 0.0;
         int u = 0;
 #pragma unroll 8
-        for (int j = 0; j < 32; ++j) {
+        for (int j = 0; j < NS; ++j) {
             f += sf[j][t];
             u += su[j][t];
         }

@@ -221,15 +221,18 @@ def test_owner_computes_option(precision, monkeypatch):
     assert torch.equal(f2, f[33:50]) and torch.equal(g2, g[33:50]) and torch.equal(u2, u[33:50])
 
 
-@pytest.mark.parametrize("precision,ppt,k", [(32, 1, 3), (32, 2, 3), (32, 4, 3), (64, 1, 3), (64, 2, 3), (32, 4, 2),
-                                             (64, 2, 2)])
-def test_owner_computes_sliced_uniform(precision, ppt, k, monkeypatch):
+@pytest.mark.parametrize("precision,ppt,lanes,k", [(32, 4, 8, 3), (32, 2, 8, 3), (32, 4, 4, 3), (32, 4, 2, 3),
+                                                   (32, 2, 2, 3), (64, 2, 8, 3), (64, 2, 2, 3), (32, 4, 8, 2),
+                                                   (64, 2, 4, 2)])
+def test_owner_computes_sliced_uniform(precision, ppt, lanes, k, monkeypatch):
     """FFSAT_OWN=1 on a formula whose fast constraints are ALL short (uniform random k-SAT on the global path, n not a
-    multiple of 32): x^T in 8 ppt-point slices and the single-bucket grouped owner kernel (owner_grp_kernel, ppt points
-    per thread); f, grad, unsat against the oracle on a ragged batch (a partial last slice), and bit-identical when a
-    point is evaluated in another batch / slice position."""
+    multiple of the block): x^T in lanes * ppt-point slices and the single-bucket grouped owner kernel
+    (owner_grp_kernel, lanes threads per variable, ppt points per thread); f, grad, unsat against the oracle on a
+    ragged batch (a partial last slice), and bit-identical when a point is evaluated in another batch / slice
+    position."""
     monkeypatch.setenv("FFSAT_OWN", "1")
     monkeypatch.setenv("FFSAT_OWN_PPT", str(ppt))
+    monkeypatch.setenv("FFSAT_OWN_LANES", str(lanes))
     inst = synth.random_ksat(3001, 12600, k, 5)
     ctx = P.Context.from_instance(inst, precision=precision, path=2, device=0)
     assert ctx.info["n_own_lits"] == ctx.info["n_lits"]
