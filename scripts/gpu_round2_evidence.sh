@@ -1,5 +1,5 @@
 #!/bin/bash
-# Round-2 evidence (second session): GPU tests, smoke, every bench line, the reference arm, a 2-rank dry run, ncu
+# Round-2 evidence (end of round): GPU tests, smoke, every bench line, the reference arm, a 2-rank dry run, ncu
 # launch lists (per-kernel time + DRAM bytes -> profiles/ncu_summary.json) and --set full captures of the dominant
 # kernels, summarised into profiles/ with tag r02.
 mkdir -p gpurun_out
@@ -17,8 +17,7 @@ B="python bench.py --no-cpu-baseline --tts-seeds 0"
 timeout 900 $N -k "regex:fast_tmem_kernel.*bool.0" -s 12 -c 1 -o gpurun_out/prof_tmem -f $B --steps 5 --warmup 3 > /dev/null 2>&1; echo ncu_tmem=$?
 timeout 900 $N -k "regex:fast_tmem_kernel.*bool.1" -s 2 -c 1 -o gpurun_out/prof_tmem_chk -f $B --steps 5 --warmup 3 > /dev/null 2>&1; echo ncu_tmem_chk=$?
 timeout 900 $N -k "regex:sym_tree_kernel" -s 1 -c 1 -o gpurun_out/prof_tree -f $B --config c3 --steps 3 --warmup 1 > /dev/null 2>&1; echo ncu_tree=$?
-timeout 900 $N -k "regex:fast_global_kernel" -s 2 -c 1 -o gpurun_out/prof_global -f $B --config c5 --steps 3 --warmup 1 > /dev/null 2>&1; echo ncu_global=$?
-timeout 900 $N -k "regex:reduce_grad_kernel" -s 2 -c 1 -o gpurun_out/prof_reduce5 -f $B --config c5 --steps 3 --warmup 1 > /dev/null 2>&1; echo ncu_reduce5=$?
+timeout 900 $N -k "regex:owner_grp_kernel" -s 2 -c 1 -o gpurun_out/prof_own -f $B --config c5 --steps 3 --warmup 1 > /dev/null 2>&1; echo ncu_own=$?
 timeout 900 $N -k "regex:fast_global_long" -s 2 -c 1 -o gpurun_out/prof_long -f $B --config c4 --steps 3 --warmup 3 > /dev/null 2>&1; echo ncu_long=$?
 timeout 900 $N -k "regex:fast_global_kernel" -s 2 -c 1 -o gpurun_out/prof_short -f $B --config c4 --steps 3 --warmup 3 > /dev/null 2>&1; echo ncu_short=$?
 python scripts/profiles_summarize.py r02 > gpurun_out/profiles_summarize.log 2>&1; echo summarize=$?

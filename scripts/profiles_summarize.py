@@ -21,7 +21,7 @@ def num(v):
 
 for rep, cfg, kname in (("prof_tmem", "c2", "fast_tmem_kernel"), ("prof_tmem_chk", "c2", "fast_tmem_kernel_check"),
                         ("prof_tiled", "c2", "fast_wide_kernel"), ("prof_sym", "c3", "sym_item_kernel"),
-                        ("prof_tree", "c3", "sym_tree_kernel"), ("prof_own", "c5", "owner_uni_kernel"),
+                        ("prof_tree", "c3", "sym_tree_kernel"), ("prof_own", "c5", "owner_grp_kernel"),
                         ("prof_global", "c5", "fast_global_kernel"), ("prof_short", "c4", "fast_global_kernel"),
                         ("prof_long", "c4", "fast_global_long_kernel"), ("prof_reduce5", "c5", "reduce_grad_kernel")):
     p = os.path.join(G, rep + ".ncu-rep")
