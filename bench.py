@@ -485,14 +485,8 @@ def main():
     gh = torch.empty((B, inst.n), dtype=dt).pin_memory()
     e2e_steps = max(5, min(args.steps, 50))
     if cfg["mode"] == "constraint":
-        xdev = torch.empty((B, inst.n), dtype=dt, device=dev)
-
         def host_eval():
-            xdev.copy_(xh, non_blocking=True)
-            f_, g_, _ = se.eval(xdev, chunks=c3_chunks)
-            fh.copy_(f_, non_blocking=True)
-            gh.copy_(g_, non_blocking=True)
-            torch.cuda.synchronize()
+            se.eval_host(xh, fh, gh, chunks=c3_chunks)   # one rank: ffsat_eval's pipelined host staging
     else:
         def host_eval():
             P.ffsat_eval(ctx.ptr, xh, B, fh, gh)   # synchronous: H2D, kernels, D2H

@@ -86,6 +86,13 @@ dev::PmReduce<T> pm_reduce_args(const ffsat_ctx* c, const Scratch& S, int64_t B,
     return r;
 }
 
+// Points per thread of owner_grp_kernel for a batch of B points: the layout's choice, except that fp32 batches of at
+// most 16 points take 2 per thread (one 16-point slice instead of a half-empty 32-point one).  A point's arithmetic
+// and summation order do not depend on it (same records, same order): the bits are the same either way.
+inline int own_ppt_for(const Layout& L, int64_t B, size_t es) {
+    return (es == 4 && L.own_ppt == 4 && L.own_lanes * 2 >= B) ? 2 : L.own_ppt;
+}
+
 // owner_grp_kernel for the bucket's (k, product channels), threads per variable and points per thread (fp32: 4 or 2,
 // fp64: 2; 16- or 8-byte gathers)
 template <typename T, int K, int NCH>
@@ -128,7 +135,7 @@ void eval_device_t(ffsat_ctx* c, Scratch& S, const T* x, int64_t B, double* f, T
     const bool need_xT = L.path == 2 || L.sym_lane;
     if (need_xT && L.n > 0) {
         dim3 tg(blocks_for(L.n, 32), blocks_for(B, 32)), tb(32, 8);
-        const int sw = L.own_uni >= 0 ? L.own_lanes * L.own_ppt : kOwnSlice;   // slice width of the owner kernel
+        const int sw = L.own_uni >= 0 ? L.own_lanes * own_ppt_for(L, B, sizeof(T)) : kOwnSlice;   // owner slice width
         if (L.own_sliced && sw == 32) dev::transpose_kernel<T, 32><<<tg, tb, 0, st>>>(x, S.xT.as<T>(), B, L.n);
         else if (L.own_sliced && sw == 16) dev::transpose_kernel<T, 16><<<tg, tb, 0, st>>>(x, S.xT.as<T>(), B, L.n);
         else if (L.own_sliced && sw == 4) dev::transpose_kernel<T, 4><<<tg, tb, 0, st>>>(x, S.xT.as<T>(), B, L.n);
@@ -305,11 +312,12 @@ void eval_device_t(ffsat_ctx* c, Scratch& S, const T* x, int64_t B, double* f, T
         o.row0 = c->n_chunks + c->n_fold;
         if (L.own_sliced && L.own_uni >= 0) {   // one owner bucket: grouped records, coefficients once
             o.grp_desc = c->grp_desc.as<uint4>(); o.grp_var = c->grp_var.as<int32_t>(); o.grp_rec = c->grp_rec.as<uint4>();
-            const int sw = L.own_lanes * L.own_ppt;
+            const int ppt = own_ppt_for(L, B, sizeof(T));
+            const int sw = L.own_lanes * ppt;
             o.grp_pitch = (uint32_t)(sw * sizeof(T));
             dim3 grid(blocks_for(L.n, 256 / L.own_lanes), blocks_for(B, sw));
             const int key = L.fbuckets[(size_t)L.own_uni].k * 10 + fast_nch(L.fbuckets[(size_t)L.own_uni]);
-            launch_owner_grp<T>(key, L.own_lanes, L.own_ppt, grid, st, o, L.own_uni);
+            launch_owner_grp<T>(key, L.own_lanes, ppt, grid, st, o, L.own_uni);
         } else if (L.own_sliced) {   // kOwnSlice points x 256 / kOwnSlice variables per block
             dim3 grid(blocks_for(L.n, 256 / kOwnSlice), blocks_for(B, kOwnSlice));
             dev::owner_grad_kernel<T, kOwnSlice><<<grid, 256, 0, st>>>(o);

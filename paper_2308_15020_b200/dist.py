@@ -115,6 +115,25 @@ class ShardedEval:
             w.wait()
         return tuple(torch.cat([p[j] for p in parts]) for j in range(3))
 
+    def eval_host(self, xh, fh, gh, uh=None, chunks: int = 1):
+        """The same from pinned HOST buffers (x [B][n] in; f [B], grad [B][n], unsat [B] out, filled in place).  One
+        rank: the library's host-buffer evaluation (ffsat_eval with host pointers: staged in chunks so the H2D copy of
+        one overlaps the evaluation of another and the D2H copy of the previous one).  Several ranks: H2D, the
+        sharded evaluation and its all-reduce, D2H."""
+        import torch
+        if self.world <= 1 and self.ctx is not None:
+            from .ffsat import ffsat_eval
+            ffsat_eval(self.ctx.ptr, xh, xh.shape[0], fh, gh, uh)
+            return fh, gh, uh
+        dev = torch.device("cuda", torch.cuda.current_device())
+        f, g, u = self.eval(xh.to(dev, non_blocking=True), chunks=chunks)
+        fh.copy_(f, non_blocking=True)
+        gh.copy_(g, non_blocking=True)
+        if uh is not None:
+            uh.copy_(u, non_blocking=True)
+        torch.cuda.synchronize()
+        return fh, gh, uh
+
 
 INT64_MAX = (1 << 63) - 1
 

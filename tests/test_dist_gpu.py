@@ -247,3 +247,25 @@ def test_nccl_collectives_on_library_buffers():
         assert torch.equal(f, f0) and torch.equal(g, g0) and torch.equal(u, u0)
     finally:
         dist.destroy_process_group()
+
+
+def test_sharded_eval_host_buffers_one_rank():
+    """ShardedEval.eval_host (pinned host buffers in and out; one rank: the library's pipelined host staging, here a
+    c5-shaped 3-SAT formula on the grouped owner path in two 16-point chunks) gives the same bits as the device
+    evaluation, and f / grad / unsat match the oracle."""
+    torch.cuda.set_device(0)
+    inst = synth.random_ksat(3001, 12600, 3, 41)
+    se = D.ShardedEval(inst.arrays(), 0, 1, device=0, precision=32, path=2)
+    X = synth.points("U", 32, inst.n, 42, np.float32)
+    xh = torch.from_numpy(X).pin_memory()
+    fh = torch.empty(32, dtype=torch.float64).pin_memory()
+    gh = torch.empty((32, inst.n), dtype=torch.float32).pin_memory()
+    uh = torch.empty(32, dtype=torch.int32).pin_memory()
+    se.eval_host(xh, fh, gh, uh)
+    f, g, u = se.eval(torch.from_numpy(X).cuda())
+    assert torch.equal(fh, f.cpu()) and torch.equal(gh, g.cpu()) and torch.equal(uh, u.cpu())
+    Fo = OracleFormula.from_arrays(*inst.arrays())
+    fo, go = cdp.evaluate(Fo, X.astype(np.float64))
+    assert np.max(np.abs(fh.numpy() - fo) / np.maximum(1, np.abs(fo))) <= 1e-4
+    assert np.max(np.abs(gh.numpy() - go) / np.maximum(1, np.abs(go))) <= 1e-4
+    assert np.array_equal(uh.numpy(), cdp.check(Fo, X.astype(np.float64))[0])

@@ -263,6 +263,29 @@ def test_owner_grouped_default_on_single_short_bucket(precision, monkeypatch):
     assert torch.equal(f2, f[31:69]) and torch.equal(g2, g[31:69]) and torch.equal(u2, u[31:69])
 
 
+def test_owner_grouped_small_batches_and_host_chunks(monkeypatch):
+    """Batches of <= 16 points take 2 points per thread (16-point x^T slices) and host batches of 17..32 points go as
+    two 16-point chunks: the same bits as the 4-per-thread evaluation of a larger batch (a point's arithmetic and
+    summation order do not depend on the slice width), and the oracle on a 16-point batch."""
+    monkeypatch.delenv("FFSAT_OWN", raising=False)
+    monkeypatch.delenv("FFSAT_OWN_PPT", raising=False)
+    inst = synth.random_ksat(4001, 16800, 3, 21)
+    ctx = P.Context.from_instance(inst, precision=32, path=2, device=0)
+    assert ctx.info["n_own_lits"] == ctx.info["n_lits"]
+    compare(inst, synth.points("U", 16, inst.n, 22), ctx=ctx)
+    X = synth.points("U", 70, inst.n, 23, ctx.dtype)
+    xd = torch.from_numpy(X).cuda()
+    f, g, u = ctx.eval(xd, grad=True, unsat=True)
+    f, g, u = f.cpu().numpy(), g.cpu().numpy(), u.cpu().numpy()
+    for lo, hi in ((0, 16), (16, 27), (40, 41)):
+        fs, gs, us = ctx.eval(xd[lo:hi].contiguous(), grad=True, unsat=True)
+        assert np.array_equal(fs.cpu().numpy(), f[lo:hi]) and np.array_equal(gs.cpu().numpy(), g[lo:hi])
+        assert np.array_equal(us.cpu().numpy(), u[lo:hi])
+    for lo, hi in ((0, 32), (10, 35), (3, 20)):   # host buffers: two 16-point chunks / one chunk
+        fh, gh, uh = ctx.eval(np.ascontiguousarray(X[lo:hi]), grad=True, unsat=True)
+        assert np.array_equal(fh, f[lo:hi]) and np.array_equal(gh, g[lo:hi]) and np.array_equal(uh, u[lo:hi])
+
+
 def test_owner_grouped_with_root_path_slots(monkeypatch):
     """The grouped owner kernel also adds a variable's T slots (here the root-path terms of long at-most-b
     constraints sharing the variables with the 3-literal clauses), fp64, against the oracle."""
