@@ -108,7 +108,11 @@ typedef struct {
     int32_t max_k;
     int64_t device_bytes;   /* persistent device memory held by the context */
     int64_t n_own_lits;     /* global path: literals of the short constraints whose gradient terms the owner-computes
-                               kernel forms per variable (no T-buffer round trip); 0 otherwise */
+                               kernel forms per variable (no T-buffer round trip; SURVEY 8(e) "owner-computes").  On
+                               by default when the fast constraints are one bucket of k <= 3 clauses (uniform random
+                               3-SAT, c5); environment FFSAT_OWN=0 disables it, FFSAT_OWN=1 extends it to every
+                               k <= 3 bucket.  Results agree within the stated tolerance either way (the summation
+                               order differs); 0 when not used */
     int64_t n_tree_cons;    /* fp64 symmetric constraints on the product-tree path (long k) */
     int64_t tree_work;      /* their FP64 instructions per point (the tree path's algorithmic count) */
 } ffsat_info_t;
