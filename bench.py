@@ -52,6 +52,7 @@ CONFIGS = {
     "c4p": dict(make=lambda: synth.config4_parity(0), B=1024, mode="restart", desc="c4(i): parity learning with error N=60, m=120 XOR (P:1066-1071)"),
     "c4": dict(make=lambda: synth.config4_hybrid(0), B=1024, mode="restart", desc="c4: n=1024, 2048 planted 3-CNF + 512 XOR k=3..64"),
     "c5": dict(make=lambda: synth.config5(0), B=32, mode="constraint", desc="c5: uniform random 3-SAT n=1e6 m=4.2e6, constraint-sharded"),
+    "c5b1": dict(make=lambda: synth.config5(0), B=1, mode="constraint", desc="c5 at B=1: uniform random 3-SAT n=1e6 m=4.2e6, one point"),
 }
 SM_COUNT = 148
 FP32_LANES, FP64_LANES = 128, 64  # FP32 / FP64 lanes per SM per clock (B200 guide unit counts)
@@ -280,7 +281,7 @@ def roofline_of(info, inst, B, ph, args):
     alu_src = (f"{SM_COUNT} SMs x {lanes} {'FP64' if f64 else 'FP32'} lanes x {mhz:.0f} MHz ({peak_src} sm_max_mhz); "
                "one FMA / MUL = one lane-op")
     res = {}
-    eval_kernels = ("transpose_kernel+fast_global_kernel+fast_global_long_kernel+owner_grad_kernel+owner_grp_kernel+"
+    eval_kernels = ("transpose_kernel+canon_copy_kernel+fast_global_kernel+fast_global_long_kernel+owner_grad_kernel+owner_grp_kernel+"
                     "fold_rows_kernel+reduce_grad_kernel+reduce_f_kernel"
                     if info["path"] == 2 else "fast_wide_kernel+fast_tiled_kernel+reduce_grad_kernel+reduce_f_kernel")
     traffic_eval = ncu_traffic(eval_kernels, args.config, any_of=True)

@@ -90,7 +90,7 @@ dev::PmReduce<T> pm_reduce_args(const ffsat_ctx* c, const Scratch& S, int64_t B,
 // most 16 points take 2 per thread (one 16-point slice instead of a half-empty 32-point one).  A point's arithmetic
 // and summation order do not depend on it (same records, same order): the bits are the same either way.
 inline int own_ppt_for(const Layout& L, int64_t B, size_t es) {
-    return (es == 4 && L.own_ppt == 4 && L.own_lanes * 2 >= B) ? 2 : L.own_ppt;
+    return (es == 4 && L.own_ppt == 4 && L.own_lanes * 2 >= B) ? 2 : L.own_ppt;   // (1 lane: 1 point per thread)
 }
 
 // owner_grp_kernel for the bucket's (k, product channels), threads per variable and points per thread (fp32: 4 or 2,
@@ -98,7 +98,9 @@ inline int own_ppt_for(const Layout& L, int64_t B, size_t es) {
 template <typename T, int K, int NCH>
 void launch_owner_grp_k(int lanes, int ppt, dim3 grid, cudaStream_t st, const dev::OwnerArgs<T>& o, int32_t bucket) {
     constexpr int P4 = sizeof(T) == 4 ? 4 : 2;
-    if (ppt == 2 || sizeof(T) == 8) {
+    if (lanes == 1) {
+        dev::owner_grp_kernel<T, K, NCH, 1, 1><<<grid, 256, 0, st>>>(o, bucket);
+    } else if (ppt == 2 || sizeof(T) == 8) {
         if (lanes == 2) dev::owner_grp_kernel<T, K, NCH, 2, 2><<<grid, 256, 0, st>>>(o, bucket);
         else if (lanes == 4) dev::owner_grp_kernel<T, K, NCH, 4, 2><<<grid, 256, 0, st>>>(o, bucket);
         else dev::owner_grp_kernel<T, K, NCH, 8, 2><<<grid, 256, 0, st>>>(o, bucket);
@@ -139,6 +141,9 @@ void eval_device_t(ffsat_ctx* c, Scratch& S, const T* x, int64_t B, double* f, T
         if (L.own_sliced && sw == 32) dev::transpose_kernel<T, 32><<<tg, tb, 0, st>>>(x, S.xT.as<T>(), B, L.n);
         else if (L.own_sliced && sw == 16) dev::transpose_kernel<T, 16><<<tg, tb, 0, st>>>(x, S.xT.as<T>(), B, L.n);
         else if (L.own_sliced && sw == 4) dev::transpose_kernel<T, 4><<<tg, tb, 0, st>>>(x, S.xT.as<T>(), B, L.n);
+        else if (L.own_sliced && sw == 1)   // 1-point slices: x^T is x (a canonicalising copy)
+            dev::canon_copy_kernel<T><<<(unsigned)std::min<int64_t>(4 * c->num_sm, blocks_for(B * L.n / (16 / (int64_t)sizeof(T)) + 1, 256)), 256, 0, st>>>(
+                x, S.xT.as<T>(), B * (int64_t)L.n);
         else if (L.own_sliced) dev::transpose_kernel<T, kOwnSlice><<<tg, tb, 0, st>>>(x, S.xT.as<T>(), B, L.n);
         else dev::transpose_kernel<T, 0><<<tg, tb, 0, st>>>(x, S.xT.as<T>(), B, L.n);
         c->launches += 1;

@@ -164,7 +164,7 @@ ffsat_ctx* make_ctx(Formula&& F, const ffsat_options* opt) {
     validate(F);
     std::unique_ptr<ffsat_ctx> c(new ffsat_ctx());
     c->F = std::move(F);
-    c->Lo = build_layout(c->F, o.path, o.precision);
+    c->Lo = build_layout(c->F, o.path, o.precision, o.batch_ref > 0 ? o.batch_ref : 1024);
     c->device = o.device;
     c->batch_ref = o.batch_ref > 0 ? o.batch_ref : 1024;
     if (o.device >= 0) {

@@ -313,7 +313,7 @@ bool tree_path(int k, int precision) {
 int sym_roots(int) { return 1; }
 int sym_group(int k) { int nw, c; sym_geom(k, &nw, &c); return 32 * nw; }
 
-Layout build_layout(const Formula& F, int path, int precision) {
+Layout build_layout(const Formula& F, int path, int precision, int64_t batch_ref) {
     Layout Lo;
     Lo.n = F.n;
     Lo.m = F.m();
@@ -525,13 +525,18 @@ Layout build_layout(const Formula& F, int path, int precision) {
     if (Lo.own && Lo.own_uni >= 0) {
         // one owner bucket: grouped, padded, interleaved records (owner_grp_kernel)
         // 16-byte gathers: 4 fp32 / 2 fp64 points per thread; threads per variable (FFSAT_OWN_LANES 2, 4 or 8)
-        Lo.own_ppt = precision == 64 ? 2 : 4;
-        Lo.own_lanes = kOwnLanes;
+        // single-point plans (batch_ref <= 4): one thread per (variable, point), a warp over 32 variables, x read in
+        // place (1-point slices) -- no lane idles for want of points
+        const bool single = batch_ref <= 4;
+        Lo.own_ppt = single ? 1 : precision == 64 ? 2 : 4;
+        Lo.own_lanes = single ? 1 : kOwnLanes;
         if (const char* e = std::getenv("FFSAT_OWN_PPT")) Lo.own_ppt = std::atoi(e) == 2 ? 2 : Lo.own_ppt;
         if (const char* e = std::getenv("FFSAT_OWN_LANES")) {
             const int v = std::atoi(e);
-            Lo.own_lanes = v == 2 || v == 4 ? v : 8;
+            Lo.own_lanes = v == 1 || v == 2 || v == 4 ? v : 8;
         }
+        if (Lo.own_lanes == 1) Lo.own_ppt = 1;
+        else if (Lo.own_ppt == 1) Lo.own_ppt = 2;
         const int G = 32 / Lo.own_lanes, NS = 8 * G;   // variable slots per group (warp) and per block
         const FastBucket& b = Lo.fbuckets[(size_t)Lo.own_uni];
         const int64_t n = F.n, nblk = (n + NS - 1) / NS;

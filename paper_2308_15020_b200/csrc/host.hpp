@@ -127,7 +127,8 @@ struct Layout {
     // {0, 0, 0, 2}.  Record {position, the other literals' words (literal order), bit 0 own negated | bit 1 pad}
     int32_t own_ppt = 4;                // owner_grp_kernel: points per thread,
     int32_t own_lanes = 8;              // ... threads per variable (x^T slices of own_lanes * own_ppt points; groups of
-                                        // 32 / own_lanes variables, blocks of 8 groups, windows of 8 blocks)
+                                        // 32 / own_lanes variables, blocks of 8 groups, windows of 8 blocks); 1 (one
+                                        // point, a warp over 32 variables) for single-point plans (batch_ref <= 4)
     std::vector<uint32_t> grp_desc;     // 4 per group
     std::vector<int32_t> grp_var;       // [32 * ceil(n / 32)]
     std::vector<uint32_t> grp_rec;      // 4 per record (incl. pads)
@@ -148,7 +149,7 @@ constexpr int kClassCap = 16;
 constexpr int kWidePitch = 132;     // wide tiled kernel row: x (64 points + 2 pad) | gradient (64 + 2)       // constraints per var-disjoint class (2 per warp of an 8-warp CTA)
 
 // Build everything; path: 0 auto, 1 tiled, 2 global; precision 0 auto / 32 / 64.
-Layout build_layout(const Formula& F, int path, int precision);
+Layout build_layout(const Formula& F, int path, int precision, int64_t batch_ref = 1024);
 // Tiled-path admission: the max n whose x and gradient tiles fit shared memory for the dtype.
 int tiled_max_n(int precision);
 size_t tiled_smem_bytes(int n, int precision);

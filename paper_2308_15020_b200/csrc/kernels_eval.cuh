@@ -2153,6 +2153,7 @@ __global__ void __launch_bounds__(256, sizeof(T) == 8 ? 2 : 3) owner_grp_kernel(
     constexpr int G = 32 / LANES;            // variable slots per warp (= group)
     constexpr int NS = 8 * G;                // variable slots per block
     constexpr int NB = PPT == 4 ? 2 : 4;     // record rows per batch (registers: 80 at 4 points per thread)
+    static_assert(LANES * PPT >= 1 && 32 % LANES == 0, "lanes divide a warp");
     __shared__ double sf[NS][SB];
     __shared__ int su[NS][SB];
     const int t = threadIdx.x, lane = t % LANES, slot = t / LANES;
@@ -2385,7 +2386,27 @@ __global__ void __launch_bounds__(32 * NWF) reduce_f_kernel(ReduceFArgs a) {
     }
 }
 
-// x [B][n] -> xT [n][B]
+// x^T in 1-point slices is x itself: a canonicalising copy (-0.0 -> +0.0, as transpose_kernel does), 16 bytes per
+// thread per step, grid-stride.
+template <typename T>
+__global__ void __launch_bounds__(256) canon_copy_kernel(const T* __restrict__ x, T* __restrict__ y, int64_t count) {
+    constexpr int V = 16 / sizeof(T);
+    const bool aligned = ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(y)) & 15) == 0;   // (a view)
+    const int64_t nv = aligned ? count / V : 0, stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nv; i += stride) {
+        if constexpr (sizeof(T) == 4) {
+            float4 q = reinterpret_cast<const float4*>(x)[i];
+            q.x += 0.0f; q.y += 0.0f; q.z += 0.0f; q.w += 0.0f;
+            reinterpret_cast<float4*>(y)[i] = q;
+        } else {
+            double2 q = reinterpret_cast<const double2*>(x)[i];
+            q.x += 0.0; q.y += 0.0;
+            reinterpret_cast<double2*>(y)[i] = q;
+        }
+    }
+    for (int64_t i = nv * V + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count; i += stride) y[i] = x[i] + (T)0;
+}
+
 // x [B][n] -> x^T: W = 0 [n][B]; W > 0: W-point slices [B/W][n][W] (each slice contiguous).
 template <typename T, int W = 0>
 __global__ void __launch_bounds__(256) transpose_kernel(const T* __restrict__ x, T* __restrict__ xT, int64_t B, int32_t n) {

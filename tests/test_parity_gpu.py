@@ -223,7 +223,7 @@ def test_owner_computes_option(precision, monkeypatch):
 
 @pytest.mark.parametrize("precision,ppt,lanes,k", [(32, 4, 8, 3), (32, 2, 8, 3), (32, 4, 4, 3), (32, 4, 2, 3),
                                                    (32, 2, 2, 3), (64, 2, 8, 3), (64, 2, 2, 3), (32, 4, 8, 2),
-                                                   (64, 2, 4, 2)])
+                                                   (64, 2, 4, 2), (32, 1, 1, 3), (64, 1, 1, 3), (32, 1, 1, 2)])
 def test_owner_computes_sliced_uniform(precision, ppt, lanes, k, monkeypatch):
     """FFSAT_OWN=1 on a formula whose fast constraints are ALL short (uniform random k-SAT on the global path, n not a
     multiple of the block): x^T in lanes * ppt-point slices and the single-bucket grouped owner kernel
@@ -284,6 +284,32 @@ def test_owner_grouped_small_batches_and_host_chunks(monkeypatch):
     for lo, hi in ((0, 32), (10, 35), (3, 20)):   # host buffers: two 16-point chunks / one chunk
         fh, gh, uh = ctx.eval(np.ascontiguousarray(X[lo:hi]), grad=True, unsat=True)
         assert np.array_equal(fh, f[lo:hi]) and np.array_equal(gh, g[lo:hi]) and np.array_equal(uh, u[lo:hi])
+
+
+@pytest.mark.parametrize("precision", [32, 64])
+def test_owner_grouped_single_point_plan(precision, monkeypatch):
+    """A single-point plan (batch_ref = 1: c5 at B = 1) takes the one-lane layout -- a warp over 32 variables, one
+    point per thread, groups of 32 window-sorted variables; f, grad, unsat against the oracle at B = 1 and on a
+    small batch (one pass per point), and the same bits for a point alone and inside the batch."""
+    monkeypatch.delenv("FFSAT_OWN", raising=False)
+    monkeypatch.delenv("FFSAT_OWN_LANES", raising=False)
+    monkeypatch.delenv("FFSAT_OWN_PPT", raising=False)
+    inst = synth.random_ksat(6007, 25200, 3, 31)
+    ctx = P.Context.from_instance(inst, precision=precision, path=2, device=0, batch_ref=1)
+    assert ctx.info["n_own_lits"] == ctx.info["n_lits"]
+    compare(inst, synth.points("U", 1, inst.n, 32), precision=precision, ctx=ctx)
+    compare(inst, synth.points("N", 1, inst.n, 33), precision=precision, ctx=ctx)
+    compare(inst, synth.points("Z", 1, inst.n, 34), precision=precision, ctx=ctx)
+    X = synth.points("U", 5, inst.n, 35, ctx.dtype)
+    compare(inst, X, precision=precision, ctx=ctx)
+    xd = torch.from_numpy(X).cuda()
+    f, g, u = ctx.eval(xd, grad=True, unsat=True)
+    f3, g3, u3 = ctx.eval(xd[3:4].contiguous(), grad=True, unsat=True)   # (a view 4-byte aligned only)
+    assert torch.equal(f3, f[3:4]) and torch.equal(g3, g[3:4]) and torch.equal(u3, u[3:4])
+    Z = torch.zeros((2, inst.n), dtype=xd.dtype, device="cuda")
+    Z[1] = -0.0                                                            # signed zeros are canonicalised
+    fz, gz, uz = ctx.eval(Z, grad=True, unsat=True)
+    assert torch.equal(fz[0], fz[1]) and torch.equal(gz[0], gz[1]) and torch.equal(uz[0], uz[1])
 
 
 def test_owner_grouped_with_root_path_slots(monkeypatch):
