@@ -87,10 +87,11 @@ dev::PmReduce<T> pm_reduce_args(const ffsat_ctx* c, const Scratch& S, int64_t B,
 }
 
 // Points per thread of owner_grp_kernel for a batch of B points: the layout's choice, except that fp32 batches of at
-// most 16 points take 2 per thread (one 16-point slice instead of a half-empty 32-point one).  A point's arithmetic
+// most 16 (8) points take 2 (1) per thread (one 16- or 8-point slice instead of a mostly empty 32-point one).  A point's arithmetic
 // and summation order do not depend on it (same records, same order): the bits are the same either way.
 inline int own_ppt_for(const Layout& L, int64_t B, size_t es) {
-    return (es == 4 && L.own_ppt == 4 && L.own_lanes * 2 >= B) ? 2 : L.own_ppt;   // (1 lane: 1 point per thread)
+    if (es != 4 || L.own_ppt != 4 || L.own_lanes != 8) return L.own_ppt;   // (1 lane: 1 point per thread)
+    return B <= 8 ? 1 : B <= 16 ? 2 : 4;
 }
 
 // owner_grp_kernel for the bucket's (k, product channels), threads per variable and points per thread (fp32: 4 or 2,
@@ -100,6 +101,8 @@ void launch_owner_grp_k(int lanes, int ppt, dim3 grid, cudaStream_t st, const de
     constexpr int P4 = sizeof(T) == 4 ? 4 : 2;
     if (lanes == 1) {
         dev::owner_grp_kernel<T, K, NCH, 1, 1><<<grid, 256, 0, st>>>(o, bucket);
+    } else if (ppt == 1 && lanes == 8) {
+        dev::owner_grp_kernel<T, K, NCH, 8, 1><<<grid, 256, 0, st>>>(o, bucket);
     } else if (ppt == 2 || sizeof(T) == 8) {
         if (lanes == 2) dev::owner_grp_kernel<T, K, NCH, 2, 2><<<grid, 256, 0, st>>>(o, bucket);
         else if (lanes == 4) dev::owner_grp_kernel<T, K, NCH, 4, 2><<<grid, 256, 0, st>>>(o, bucket);
@@ -140,6 +143,7 @@ void eval_device_t(ffsat_ctx* c, Scratch& S, const T* x, int64_t B, double* f, T
         const int sw = L.own_uni >= 0 ? L.own_lanes * own_ppt_for(L, B, sizeof(T)) : kOwnSlice;   // owner slice width
         if (L.own_sliced && sw == 32) dev::transpose_kernel<T, 32><<<tg, tb, 0, st>>>(x, S.xT.as<T>(), B, L.n);
         else if (L.own_sliced && sw == 16) dev::transpose_kernel<T, 16><<<tg, tb, 0, st>>>(x, S.xT.as<T>(), B, L.n);
+        else if (L.own_sliced && sw == 8) dev::transpose_kernel<T, 8><<<tg, tb, 0, st>>>(x, S.xT.as<T>(), B, L.n);
         else if (L.own_sliced && sw == 4) dev::transpose_kernel<T, 4><<<tg, tb, 0, st>>>(x, S.xT.as<T>(), B, L.n);
         else if (L.own_sliced && sw == 1)   // 1-point slices: x^T is x (a canonicalising copy)
             dev::canon_copy_kernel<T><<<(unsigned)std::min<int64_t>(4 * c->num_sm, blocks_for(B * L.n / (16 / (int64_t)sizeof(T)) + 1, 256)), 256, 0, st>>>(

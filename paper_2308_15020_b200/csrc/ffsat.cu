@@ -682,13 +682,13 @@ ffsat_status ffsat_eval(ffsat_ctx* c, const void* x, int64_t B, int32_t on_devic
     // streams with their own scratch (each fills half the GPU; the copies of one overlap the other's evaluation)
     const bool dual = nchunk == 1 && B >= 512 && c->Lo.path == 1 && c->Lo.n_sym == 0;
     if (dual) nchunk = 2;
-    // grouped owner path (c5-like: large n, small batches): 17..32 points go as two 16-point chunks -- each one
-    // 16-point x^T slice at 2 points per thread -- so the H2D copy of the second half and the D2H copy of the first
-    // overlap an evaluation (the copies of 2 x 4 n B bytes dominate such a step)
-    const int64_t own_half = c->Lo.own_uni >= 0 && c->esize == 4 && c->Lo.own_ppt == 4 ? c->Lo.own_lanes * 2 : 0;
-    const bool own2 = nchunk == 1 && own_half > 0 && B > own_half && B <= 2 * own_half;
-    if (own2) nchunk = 2;
-    const int64_t Bc = own2 ? own_half : nchunk == 1 ? B : ((B + nchunk - 1) / nchunk + 63) / 64 * 64;
+    // grouped owner path (c5-like: large n, small batches): 9..32 points go as 8-point chunks -- each one 8-point
+    // x^T slice at 1 point per thread -- so the H2D copies of the later chunks and the D2H copies of the earlier ones
+    // overlap the evaluations (the copies of 2 x 4 n B bytes dominate such a step)
+    const int64_t own_q = c->Lo.own_uni >= 0 && c->esize == 4 && c->Lo.own_ppt == 4 && c->Lo.own_lanes == 8 ? 8 : 0;
+    const bool ownq = nchunk == 1 && own_q > 0 && B > own_q && B <= 4 * own_q;
+    if (ownq) nchunk = (B + own_q - 1) / own_q;
+    const int64_t Bc = ownq ? own_q : nchunk == 1 ? B : ((B + nchunk - 1) / nchunk + 63) / 64 * 64;
     const int64_t nck = Bc > 0 ? (B + Bc - 1) / Bc : 0;
     const size_t n = (size_t)c->Lo.n;
     c->x_stage.ensure(std::max<size_t>(16, (size_t)(nck * Bc) * n * es));

@@ -264,9 +264,9 @@ def test_owner_grouped_default_on_single_short_bucket(precision, monkeypatch):
 
 
 def test_owner_grouped_small_batches_and_host_chunks(monkeypatch):
-    """Batches of <= 16 points take 2 points per thread (16-point x^T slices) and host batches of 17..32 points go as
-    two 16-point chunks: the same bits as the 4-per-thread evaluation of a larger batch (a point's arithmetic and
-    summation order do not depend on the slice width), and the oracle on a 16-point batch."""
+    """Batches of <= 16 (<= 8) points take 2 (1) points per thread (16- / 8-point x^T slices) and host batches of
+    9..32 points go as 8-point chunks: the same bits as the 4-per-thread evaluation of a larger batch (a point's
+    arithmetic and summation order do not depend on the slice width), and the oracle on a 16-point batch."""
     monkeypatch.delenv("FFSAT_OWN", raising=False)
     monkeypatch.delenv("FFSAT_OWN_PPT", raising=False)
     inst = synth.random_ksat(4001, 16800, 3, 21)
@@ -277,7 +277,7 @@ def test_owner_grouped_small_batches_and_host_chunks(monkeypatch):
     xd = torch.from_numpy(X).cuda()
     f, g, u = ctx.eval(xd, grad=True, unsat=True)
     f, g, u = f.cpu().numpy(), g.cpu().numpy(), u.cpu().numpy()
-    for lo, hi in ((0, 16), (16, 27), (40, 41)):
+    for lo, hi in ((0, 16), (16, 27), (40, 41), (50, 58)):
         fs, gs, us = ctx.eval(xd[lo:hi].contiguous(), grad=True, unsat=True)
         assert np.array_equal(fs.cpu().numpy(), f[lo:hi]) and np.array_equal(gs.cpu().numpy(), g[lo:hi])
         assert np.array_equal(us.cpu().numpy(), u[lo:hi])
