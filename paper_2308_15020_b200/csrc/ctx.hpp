@@ -84,11 +84,33 @@ void launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cu
 #define FFSAT_SIDE_STREAMS 8
 
 namespace ffsat {
-// Per-batch scratch of one evaluation stream: the context's own ffsat_eval calls use ctx->scr, every search owns
-// one (so a search's captured CUDA graph never references buffers another call may resize).
+// Side streams of one evaluation stream for the concurrent root-path classes and length-class chunk groups (fork /
+// join through events, graph-capturable).  Created on first use, outside any capture.
+struct Forks {
+    cudaStream_t side[FFSAT_SIDE_STREAMS] = {};
+    cudaEvent_t ev_fork = nullptr, ev_join[FFSAT_SIDE_STREAMS] = {};
+    bool pending_join[FFSAT_SIDE_STREAMS] = {};
+    Forks() = default;
+    Forks(const Forks&) = delete;
+    Forks& operator=(const Forks&) = delete;
+    void ensure() {
+        if (ev_fork) return;
+        for (int i = 0; i < FFSAT_SIDE_STREAMS; ++i) {
+            CK(cudaStreamCreateWithFlags(&side[i], cudaStreamNonBlocking));
+            CK(cudaEventCreateWithFlags(&ev_join[i], cudaEventDisableTiming));
+        }
+        CK(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming));
+    }
+    ~Forks() {
+    }
+};
+// Per-batch scratch of one evaluation stream: the context's own ffsat_eval calls use ctx->scr (and scr2 for the
+// second concurrent host-buffer chunk), every search owns one (so a search's captured CUDA graph never references
+// buffers another call may resize); each with its own side streams, so two evaluations can run concurrently.
 struct Scratch {
     DBuf xT, Tb, P, fpart, upart, fsym, usym, TbS, fS;
     DBuf tree_ctr;                // work counters of the product-tree classes (one int32 per sym class)
+    Forks fk;
     int64_t B = -1;
 };
 }  // namespace ffsat
@@ -130,31 +152,14 @@ struct ffsat_ctx {
     size_t tiled_smem = 0;
     int64_t launches = 0;
     cudaEvent_t ev[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
-    // side streams for the concurrent root-path classes (fork / join through events, graph-capturable)
-    cudaStream_t side[FFSAT_SIDE_STREAMS] = {};
     // host-buffer evaluation: copy streams (H2D, D2H) and per-chunk events of the pipelined staging
     cudaStream_t copy_h2d = nullptr, copy_d2h = nullptr;
     std::vector<cudaEvent_t> ev_h2d, ev_done;
     ffsat::DBuf nf_flag;
     int32_t* nf_host = nullptr;   // pinned
-    cudaEvent_t ev_fork = nullptr, ev_join[FFSAT_SIDE_STREAMS] = {};
-    bool pending_join[FFSAT_SIDE_STREAMS] = {};
-    void ensure_side_streams() {
-        if (ev_fork) return;
-        for (int i = 0; i < FFSAT_SIDE_STREAMS; ++i) {
-            CK(cudaStreamCreateWithFlags(&side[i], cudaStreamNonBlocking));
-            CK(cudaEventCreateWithFlags(&ev_join[i], cudaEventDisableTiming));
-        }
-        CK(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming));
-    }
     ~ffsat_ctx() {
         for (cudaEvent_t& e : ev)
             if (e) cudaEventDestroy(e);
-        for (int i = 0; i < FFSAT_SIDE_STREAMS; ++i) {
-            if (side[i]) cudaStreamDestroy(side[i]);
-            if (ev_join[i]) cudaEventDestroy(ev_join[i]);
-        }
-        if (ev_fork) cudaEventDestroy(ev_fork);
         if (copy_h2d) cudaStreamDestroy(copy_h2d);
         if (copy_d2h) cudaStreamDestroy(copy_d2h);
         if (comp2) cudaStreamDestroy(comp2);

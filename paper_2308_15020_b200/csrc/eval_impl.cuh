@@ -164,14 +164,14 @@ void eval_device_t(ffsat_ctx* c, Scratch& S, const T* x, int64_t B, double* f, T
         const size_t ncl = L.sym_classes.size();
         const bool fork = ncl > 1 || (!profiled && L.n_fast > 0);
         if (fork) {
-            c->ensure_side_streams();
-            CK(cudaEventRecord(c->ev_fork, st));
+            S.fk.ensure();
+            CK(cudaEventRecord(S.fk.ev_fork, st));
         }
         dev::SymArgs<T> aT = a;    // thread-per-item classes read x^T
         aT.x = S.xT.as<T>(); aT.sb = 1; aT.sv = B;
         for (size_t i = 0; i < ncl; ++i) {
-            cudaStream_t ss = fork ? c->side[i % FFSAT_SIDE_STREAMS] : st;
-            if (fork && i < FFSAT_SIDE_STREAMS) CK(cudaStreamWaitEvent(ss, c->ev_fork, 0));
+            cudaStream_t ss = fork ? S.fk.side[i % FFSAT_SIDE_STREAMS] : st;
+            if (fork && i < FFSAT_SIDE_STREAMS) CK(cudaStreamWaitEvent(ss, S.fk.ev_fork, 0));
             const SymClass& cl = L.sym_classes[i];
             dev::SymSplit<T> sp{};
             sp.S = c->sym_S[i];
@@ -195,16 +195,16 @@ void eval_device_t(ffsat_ctx* c, Scratch& S, const T* x, int64_t B, double* f, T
         CK(cudaGetLastError());
         if (fork) {
             for (size_t i = 0; i < std::min<size_t>(ncl, FFSAT_SIDE_STREAMS); ++i) {
-                CK(cudaEventRecord(c->ev_join[i], c->side[i]));
-                c->pending_join[i] = true;
+                CK(cudaEventRecord(S.fk.ev_join[i], S.fk.side[i]));
+                S.fk.pending_join[i] = true;
             }
         }
     };
     auto join_sym = [&]() {
         for (int i = 0; i < FFSAT_SIDE_STREAMS; ++i)
-            if (c->pending_join[i]) {
-                CK(cudaStreamWaitEvent(st, c->ev_join[i], 0));
-                c->pending_join[i] = false;
+            if (S.fk.pending_join[i]) {
+                CK(cudaStreamWaitEvent(st, S.fk.ev_join[i], 0));
+                S.fk.pending_join[i] = false;
             }
     };
     if (!profiled) launch_sym_all();
@@ -251,8 +251,8 @@ void eval_device_t(ffsat_ctx* c, Scratch& S, const T* x, int64_t B, double* f, T
             for (int g = 0; g < 3; ++g) ngroups += c->gchunk[g + 1] > c->gchunk[g];
             const bool gfork = !profiled && ngroups > 1;
             if (gfork) {
-                c->ensure_side_streams();
-                CK(cudaEventRecord(c->ev_fork, st));
+                S.fk.ensure();
+                CK(cudaEventRecord(S.fk.ev_fork, st));
             }
             int nl = 0;
             for (int g = 0; g < 3; ++g) {
@@ -264,8 +264,8 @@ void eval_device_t(ffsat_ctx* c, Scratch& S, const T* x, int64_t B, double* f, T
                 const int si = FFSAT_SIDE_STREAMS - g;   // side streams 7, 6 (the root classes start at 0)
                 cudaStream_t gs = st;
                 if (gfork && g > 0) {
-                    gs = c->side[si];
-                    CK(cudaStreamWaitEvent(gs, c->ev_fork, 0));
+                    gs = S.fk.side[si];
+                    CK(cudaStreamWaitEvent(gs, S.fk.ev_fork, 0));
                 }
                 if (g == 0) dev::fast_global_kernel<T, 4><<<grid, 256, 0, gs>>>(a);
                 else if (g == 1) {
@@ -275,8 +275,8 @@ void eval_device_t(ffsat_ctx* c, Scratch& S, const T* x, int64_t B, double* f, T
                     dev::fast_global_long_kernel<T><<<grid, 32 * dev::long_warps<T>(), dev::long_smem_bytes<T>(), gs>>>(a);
                 }
                 if (gs != st) {
-                    CK(cudaEventRecord(c->ev_join[si], gs));
-                    c->pending_join[si] = true;
+                    CK(cudaEventRecord(S.fk.ev_join[si], gs));
+                    S.fk.pending_join[si] = true;
                 }
             }
         }

@@ -362,7 +362,7 @@ bool search_capture(ffsat_search* s) {
     // the graphs reference only this search's buffers (sized at create: allocations never happen inside a
     // capture) and the context's persistent layout, which is never reallocated after load
     ensure_scratch(s->ctx, s->sc, s->B);
-    s->ctx->ensure_side_streams();
+    s->sc.fk.ensure();
     const int64_t before = s->ctx->launches;
     for (int v = 0; v < 2; ++v) {
         cudaGraph_t g = nullptr;
@@ -678,9 +678,9 @@ ffsat_status ffsat_eval(ffsat_ctx* c, const void* x, int64_t B, int32_t on_devic
     // chunks of at least batch_ref points: the launch plan is sized for batch_ref, a smaller chunk underfills the GPU
     int64_t nchunk = B < 512 ? 1 : xbytes >= (4u << 20) ? 4 : xbytes >= (2u << 20) ? 3 : 2;
     nchunk = std::max<int64_t>(1, std::min<int64_t>(nchunk, B / std::max<int64_t>(1, c->batch_ref)));
-    // tiled formulas without forked root-path work: two half-batch chunks evaluated CONCURRENTLY on two compute
-    // streams with their own scratch (each fills half the GPU; the copies of one overlap the other's evaluation)
-    const bool dual = nchunk == 1 && B >= 512 && c->Lo.path == 1 && c->Lo.n_sym == 0;
+    // batches of >= 512 points: two half-batch chunks evaluated CONCURRENTLY on two compute streams, each with its
+    // own scratch and side streams (each fills half the GPU; the copies of one overlap the other's evaluation)
+    const bool dual = nchunk == 1 && B >= 512;
     if (dual) nchunk = 2;
     // grouped owner path (c5-like: large n, small batches): 9..32 points go as 8-point chunks -- each one 8-point
     // x^T slice at 1 point per thread -- so the H2D copies of the later chunks and the D2H copies of the earlier ones

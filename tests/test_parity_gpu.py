@@ -970,15 +970,23 @@ def test_host_buffer_pipeline_matches_device(B):
     assert np.array_equal(fh, fd.cpu().numpy()) and np.array_equal(gh, gd.cpu().numpy())
 
 
-@pytest.mark.parametrize("B", [600, 1024, 1030])
-def test_host_buffer_dual_stream_matches_device(B):
-    """Host-buffer evaluation of a pure-CNF (tiled-path) formula: the batch splits into two half chunks evaluated
-    concurrently on two compute streams with separate scratch; against the oracle, and bit-identical to the
-    single-stream device-buffer evaluation."""
-    inst = synth.random_ksat(n=120, m=3000, k=7, seed=23)
-    X = synth.points("U", B, inst.n, 17)
-    ctx, _, _ = compare(inst, X, device_path=False)
-    assert ctx.info["path"] == 1
+@pytest.mark.parametrize("case,B", [("tiled", 600), ("tiled", 1024), ("tiled", 1030), ("global", 700),
+                                    ("global_root", 520)])
+def test_host_buffer_dual_stream_matches_device(case, B):
+    """Host-buffer evaluation of >= 512 points: the batch splits into two half chunks evaluated concurrently on two
+    compute streams, each with its own scratch and side streams (the global path's length-class groups and the
+    root-path classes fork onto them); against the oracle, and bit-identical to the single-stream device-buffer
+    evaluation."""
+    if case == "tiled":
+        inst = synth.random_ksat(n=120, m=3000, k=7, seed=23)
+    elif case == "global":
+        inst = synth.config4_hybrid(0, n=1024, m3=1500, n_xor=200, kmax=64)
+    else:
+        inst = synth.config3(0, n=1200, m3=2400, n_card=3, kmin=80, kmax=200)
+    prec = 64 if case == "global_root" else 32
+    X = synth.points("U", B, inst.n, 17, np.float64 if prec == 64 else np.float32)
+    ctx, _, _ = compare(inst, X, device_path=False, precision=prec)
+    assert ctx.info["path"] == (1 if case == "tiled" else 2)
     fh, gh, uh = ctx.eval(X, grad=True, unsat=True)
     fd, gd, ud = ctx.eval(torch.from_numpy(X).cuda(), grad=True, unsat=True)
     assert np.array_equal(uh, ud.cpu().numpy())
