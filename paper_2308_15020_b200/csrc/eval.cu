@@ -131,7 +131,7 @@ void plan_chunks(ffsat_ctx* c) {
     // owner_grad_kernel's f / unsat partial rows, one per 8-variable tile, folded 256 to a row (fold_rows_kernel);
     // partial row layout: [chunk rows | folded rows | variable-tile rows]
     // the owner kernels' variable tiles (partial f rows): 256 / kOwnSlice variables (sliced) or 8 (unsliced)
-    c->n_vtiles = !L.own ? 0 : L.own_uni >= 0 ? (L.n + 256 / L.own_lanes - 1) / (256 / L.own_lanes)
+    c->n_vtiles = !L.own ? 0 : L.own_uni >= 0 ? (L.n + 32 * L.own_wpb / L.own_lanes - 1) / (32 * L.own_wpb / L.own_lanes)
                  : L.own_sliced ? (L.n + 256 / kOwnSlice - 1) / (256 / kOwnSlice) : (L.n + 7) / 8;
     c->n_fold = (c->n_vtiles + 255) / 256;
     const int64_t rows = (L.n_fast > 0 ? c->n_chunks + c->n_fold : 0) + L.n_sym;

@@ -96,32 +96,39 @@ inline int own_ppt_for(const Layout& L, int64_t B, size_t es) {
 
 // owner_grp_kernel for the bucket's (k, product channels), threads per variable and points per thread (fp32: 4 or 2,
 // fp64: 2; 16- or 8-byte gathers)
-template <typename T, int K, int NCH>
-void launch_owner_grp_k(int lanes, int ppt, dim3 grid, cudaStream_t st, const dev::OwnerArgs<T>& o, int32_t bucket) {
+template <typename T, int K, int NCH, int WPB>
+void launch_owner_grp_w(int lanes, int ppt, dim3 grid, cudaStream_t st, const dev::OwnerArgs<T>& o, int32_t bucket) {
     constexpr int P4 = sizeof(T) == 4 ? 4 : 2;
+    const dim3 blk(32 * WPB);
     if (lanes == 1) {
-        dev::owner_grp_kernel<T, K, NCH, 1, 1><<<grid, 256, 0, st>>>(o, bucket);
+        dev::owner_grp_kernel<T, K, NCH, 1, 1, WPB><<<grid, blk, 0, st>>>(o, bucket);
     } else if (ppt == 1 && lanes == 8) {
-        dev::owner_grp_kernel<T, K, NCH, 8, 1><<<grid, 256, 0, st>>>(o, bucket);
+        dev::owner_grp_kernel<T, K, NCH, 8, 1, WPB><<<grid, blk, 0, st>>>(o, bucket);
     } else if (ppt == 2 || sizeof(T) == 8) {
-        if (lanes == 2) dev::owner_grp_kernel<T, K, NCH, 2, 2><<<grid, 256, 0, st>>>(o, bucket);
-        else if (lanes == 4) dev::owner_grp_kernel<T, K, NCH, 4, 2><<<grid, 256, 0, st>>>(o, bucket);
-        else dev::owner_grp_kernel<T, K, NCH, 8, 2><<<grid, 256, 0, st>>>(o, bucket);
+        if (lanes == 2) dev::owner_grp_kernel<T, K, NCH, 2, 2, WPB><<<grid, blk, 0, st>>>(o, bucket);
+        else if (lanes == 4) dev::owner_grp_kernel<T, K, NCH, 4, 2, WPB><<<grid, blk, 0, st>>>(o, bucket);
+        else dev::owner_grp_kernel<T, K, NCH, 8, 2, WPB><<<grid, blk, 0, st>>>(o, bucket);
     } else {
-        if (lanes == 2) dev::owner_grp_kernel<T, K, NCH, 2, P4><<<grid, 256, 0, st>>>(o, bucket);
-        else if (lanes == 4) dev::owner_grp_kernel<T, K, NCH, 4, P4><<<grid, 256, 0, st>>>(o, bucket);
-        else dev::owner_grp_kernel<T, K, NCH, 8, P4><<<grid, 256, 0, st>>>(o, bucket);
+        if (lanes == 2) dev::owner_grp_kernel<T, K, NCH, 2, P4, WPB><<<grid, blk, 0, st>>>(o, bucket);
+        else if (lanes == 4) dev::owner_grp_kernel<T, K, NCH, 4, P4, WPB><<<grid, blk, 0, st>>>(o, bucket);
+        else dev::owner_grp_kernel<T, K, NCH, 8, P4, WPB><<<grid, blk, 0, st>>>(o, bucket);
     }
 }
+template <typename T, int K, int NCH>
+void launch_owner_grp_k(int lanes, int ppt, int wpb, dim3 grid, cudaStream_t st, const dev::OwnerArgs<T>& o, int32_t bucket) {
+    if (wpb == 4) launch_owner_grp_w<T, K, NCH, 4>(lanes, ppt, grid, st, o, bucket);
+    else if (wpb == 2) launch_owner_grp_w<T, K, NCH, 2>(lanes, ppt, grid, st, o, bucket);
+    else launch_owner_grp_w<T, K, NCH, 8>(lanes, ppt, grid, st, o, bucket);
+}
 template <typename T>
-void launch_owner_grp(int key, int lanes, int ppt, dim3 grid, cudaStream_t st, const dev::OwnerArgs<T>& o, int32_t bucket) {
+void launch_owner_grp(int key, int lanes, int ppt, int wpb, dim3 grid, cudaStream_t st, const dev::OwnerArgs<T>& o, int32_t bucket) {
     switch (key) {
-    case 11: launch_owner_grp_k<T, 1, 1>(lanes, ppt, grid, st, o, bucket); break;
-    case 12: launch_owner_grp_k<T, 1, 2>(lanes, ppt, grid, st, o, bucket); break;
-    case 21: launch_owner_grp_k<T, 2, 1>(lanes, ppt, grid, st, o, bucket); break;
-    case 22: launch_owner_grp_k<T, 2, 2>(lanes, ppt, grid, st, o, bucket); break;
-    case 31: launch_owner_grp_k<T, 3, 1>(lanes, ppt, grid, st, o, bucket); break;
-    default: launch_owner_grp_k<T, 3, 2>(lanes, ppt, grid, st, o, bucket); break;
+    case 11: launch_owner_grp_k<T, 1, 1>(lanes, ppt, wpb, grid, st, o, bucket); break;
+    case 12: launch_owner_grp_k<T, 1, 2>(lanes, ppt, wpb, grid, st, o, bucket); break;
+    case 21: launch_owner_grp_k<T, 2, 1>(lanes, ppt, wpb, grid, st, o, bucket); break;
+    case 22: launch_owner_grp_k<T, 2, 2>(lanes, ppt, wpb, grid, st, o, bucket); break;
+    case 31: launch_owner_grp_k<T, 3, 1>(lanes, ppt, wpb, grid, st, o, bucket); break;
+    default: launch_owner_grp_k<T, 3, 2>(lanes, ppt, wpb, grid, st, o, bucket); break;
     }
 }
 
@@ -324,9 +331,9 @@ void eval_device_t(ffsat_ctx* c, Scratch& S, const T* x, int64_t B, double* f, T
             const int ppt = own_ppt_for(L, B, sizeof(T));
             const int sw = L.own_lanes * ppt;
             o.grp_pitch = (uint32_t)(sw * sizeof(T));
-            dim3 grid(blocks_for(L.n, 256 / L.own_lanes), blocks_for(B, sw));
+            dim3 grid(blocks_for(L.n, 32 * L.own_wpb / L.own_lanes), blocks_for(B, sw));
             const int key = L.fbuckets[(size_t)L.own_uni].k * 10 + fast_nch(L.fbuckets[(size_t)L.own_uni]);
-            launch_owner_grp<T>(key, L.own_lanes, ppt, grid, st, o, L.own_uni);
+            launch_owner_grp<T>(key, L.own_lanes, ppt, L.own_wpb, grid, st, o, L.own_uni);
         } else if (L.own_sliced) {   // kOwnSlice points x 256 / kOwnSlice variables per block
             dim3 grid(blocks_for(L.n, 256 / kOwnSlice), blocks_for(B, kOwnSlice));
             dev::owner_grad_kernel<T, kOwnSlice><<<grid, 256, 0, st>>>(o);

@@ -2147,11 +2147,11 @@ __device__ __forceinline__ void owner_grp_rows(const uint4* __restrict__ rec, in
 // literal index 0, which also carry the constraint's f and fused check) ascending position, rows B ascending
 // position, then the variable's remaining T slots ascending -- fixed, and independent of the batch, of the slice
 // width and of the point's slice position.
-template <typename T, int K, int NCH, int LANES, int PPT>
-__global__ void __launch_bounds__(256, sizeof(T) == 8 ? 2 : 3) owner_grp_kernel(OwnerArgs<T> a, int32_t bucket) {
+template <typename T, int K, int NCH, int LANES, int PPT, int WPB = 8>
+__global__ void __launch_bounds__(32 * WPB, (sizeof(T) == 8 ? 2 : 3) * 8 / WPB) owner_grp_kernel(OwnerArgs<T> a, int32_t bucket) {
     constexpr int SB = LANES * PPT;          // points per x^T slice
     constexpr int G = 32 / LANES;            // variable slots per warp (= group)
-    constexpr int NS = 8 * G;                // variable slots per block
+    constexpr int NS = WPB * G;              // variable slots per block (WPB warps = groups)
     constexpr int NB = PPT == 4 ? 2 : 4;     // record rows per batch (registers: 80 at 4 points per thread)
     static_assert(LANES * PPT >= 1 && 32 % LANES == 0, "lanes divide a warp");
     __shared__ double sf[NS][SB];
@@ -2180,7 +2180,7 @@ __global__ void __launch_bounds__(256, sizeof(T) == 8 ? 2 : 3) owner_grp_kernel(
             aoN[c][p] = fmaT(-bk.c1[c], xv[p], bk.c0[c]);
         }
     }
-    const uint4 d = a.grp_desc[blockIdx.x * 8 + t / 32];
+    const uint4 d = a.grp_desc[blockIdx.x * WPB + t / 32];
     const uint4* rec = a.grp_rec + (((int64_t)d.y << 32) | d.x) + slot % G;   // record row 0 of the group, this slot
     owner_grp_rows<T, K, NCH, PPT, NB, G, true>(rec, (int)d.z, xTs, pitch, a.w_pos, bk, xv, aoP, aoN, gP, gN, want_term,
                                                 want_unsat, acc, facc, uacc);
