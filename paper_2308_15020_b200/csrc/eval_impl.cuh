@@ -118,6 +118,7 @@ template <typename T, int K, int NCH>
 void launch_owner_grp_k(int lanes, int ppt, int wpb, dim3 grid, cudaStream_t st, const dev::OwnerArgs<T>& o, int32_t bucket) {
     if (wpb == 4) launch_owner_grp_w<T, K, NCH, 4>(lanes, ppt, grid, st, o, bucket);
     else if (wpb == 2) launch_owner_grp_w<T, K, NCH, 2>(lanes, ppt, grid, st, o, bucket);
+    else if (wpb == 1) launch_owner_grp_w<T, K, NCH, 1>(lanes, ppt, grid, st, o, bucket);
     else launch_owner_grp_w<T, K, NCH, 8>(lanes, ppt, grid, st, o, bucket);
 }
 template <typename T>

@@ -535,10 +535,13 @@ Layout build_layout(const Formula& F, int path, int precision, int64_t batch_ref
             const int v = std::atoi(e);
             Lo.own_lanes = v == 1 || v == 2 || v == 4 ? v : 8;
         }
-        // 2-warp CTAs: a CTA holds its SM slot only until the slower of 2 groups ends (c5 owner kernel 0.94 ms at 8
-        // warps, 0.88 at 4, 0.85 at 2)
-        Lo.own_wpb = 2;
-        if (const char* e = std::getenv("FFSAT_OWN_WPB")) Lo.own_wpb = std::atoi(e) == 8 ? 8 : std::atoi(e) == 4 ? 4 : 2;
+        // one-warp CTAs: a CTA's SM slot is released as soon as its group ends, not when the slowest of several
+        // groups does (c5 owner kernel 0.94 ms at 8 warps per CTA, 0.88 at 4, 0.85 at 2, 0.81 at 1)
+        Lo.own_wpb = 1;
+        if (const char* e = std::getenv("FFSAT_OWN_WPB")) {
+            const int w = std::atoi(e);
+            Lo.own_wpb = w == 8 || w == 4 || w == 2 ? w : 1;
+        }
         if (Lo.own_lanes == 1) Lo.own_ppt = 1;
         else if (Lo.own_ppt == 1) Lo.own_ppt = 2;
         const int G = 32 / Lo.own_lanes, NS = 8 * G;   // variable slots per group (warp) and per block

@@ -125,7 +125,7 @@ struct Layout {
     // rows A, rows B}; its records interleaved [row][G slots], rows A = the occurrences at literal index 0 (ascending
     // position), rows B = the others (ascending position), each padded to the group's longest list with pad records
     // {0, 0, 0, 2}.  Record {position, the other literals' words (literal order), bit 0 own negated | bit 1 pad}
-    int32_t own_wpb = 2;                // owner_grp_kernel: warps (groups) per CTA (the records' blocks of 8 groups
+    int32_t own_wpb = 1;                // owner_grp_kernel: warps (groups) per CTA (the records' blocks of 8 groups
                                         // are split over 8 / own_wpb CTAs; FFSAT_OWN_WPB),
     int32_t own_ppt = 4;                // ... points per thread,
     int32_t own_lanes = 8;              // ... threads per variable (x^T slices of own_lanes * own_ppt points; groups of
